@@ -1,0 +1,112 @@
+"""Pins for oracle.priority: the correctly rounded fp32 power and quantisation.
+
+Special cases reduce to exactly computable values: alpha=1 (fp32 rounding of a
+double, done by numpy), alpha=0.5 (integer square root), alpha=2 and 3 (exact
+rational powers).  The test's own round-to-fp32 of an exact rational is plain
+integer arithmetic written independently of the oracle's mpf path."""
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import priority as P
+
+
+def rn32_fraction(x: Fraction) -> Fraction:
+    """Independent round-half-even of a positive rational to 24 significant bits."""
+    assert x > 0
+    e = x.numerator.bit_length() - x.denominator.bit_length()
+    while Fraction(2) ** e > x:
+        e -= 1
+    while Fraction(2) ** (e + 1) <= x:
+        e += 1
+    e = max(e, -126)
+    quantum = Fraction(2) ** (e - 23)
+    k = x / quantum
+    fl = k.numerator // k.denominator
+    rem = k - fl
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and fl % 2 == 1):
+        fl += 1
+    return fl * quantum
+
+
+def val(td, alpha, eps=1e-3):
+    M, E = P.priority_value(td, alpha, eps)
+    return Fraction(M) * Fraction(2) ** E
+
+
+def p_of(td, eps=1e-3):
+    return abs(float(td)) + eps
+
+
+TDS = np.concatenate([np.abs(np.random.default_rng(0).normal(0, 1, 300)),
+                      np.random.default_rng(1).lognormal(0, 2, 200),
+                      [0.0, 1e-8, 0.999, 1.0, 2.0, 1e6]]).astype(np.float32)
+
+
+def test_alpha_one_is_fp32_rounding():
+    for td in TDS:
+        p = p_of(td)
+        assert val(td, 1.0) == Fraction(float(np.float32(p)))
+
+
+def test_alpha_zero_is_one():
+    for td in TDS[:50]:
+        assert val(td, 0.0) == 1
+
+
+def test_alpha_half_is_rounded_isqrt():
+    for td in TDS:
+        p = Fraction(p_of(td))
+        # sqrt(p) to 80 fractional bits via isqrt, then exact rounding; ties are
+        # impossible (sqrt of a double is never an fp32 midpoint) so the 80-bit
+        # truncation decides the rounding unless the remainder is exactly 0.
+        num = p.numerator << 400
+        s = math.isqrt(num * p.denominator)          # floor(sqrt(p) * 2^200 * den)
+        approx = Fraction(s, p.denominator << 200)
+        exact_sq = (s * s == num * p.denominator)
+        v = rn32_fraction(approx if exact_sq else approx + Fraction(1, p.denominator << 201))
+        assert val(td, 0.5) == v
+
+
+@pytest.mark.parametrize("alpha", [2.0, 3.0])
+def test_integer_alpha_exact(alpha):
+    for td in TDS[:200]:
+        p = Fraction(p_of(td))
+        assert val(td, alpha) == rn32_fraction(p ** int(alpha))
+
+
+@pytest.mark.parametrize("alpha", [0.6, 0.9, 0.4, 0.123456789])
+def test_general_alpha_within_half_ulp(alpha):
+    for td in TDS:
+        p = p_of(td)
+        ref = math.pow(p, alpha)                      # libm double, <= 1 ulp64
+        v = float(val(td, alpha))
+        e = math.frexp(v)[1] - 1
+        ulp32 = 2.0 ** (max(e, -126) - 23)
+        assert abs(v - ref) <= 0.5 * ulp32 * (1 + 1e-9) + 4 * abs(ref) * 2 ** -53
+
+
+def test_quantise_ties_to_even():
+    cap = P.q_cap(16)
+    F = 32
+    assert P.quantise(1, -33, F, cap) == (0, False)       # 0.5 -> 0
+    assert P.quantise(3, -33, F, cap) == (2, False)       # 1.5 -> 2
+    assert P.quantise(5, -33, F, cap) == (2, False)       # 2.5 -> 2
+    assert P.quantise(3, -34, F, cap) == (1, False)       # 0.75 -> 1
+    assert P.quantise(1 << 23, -23, F, cap) == (1 << 32, False)   # 1.0 -> 2^32
+    assert P.quantise(1, 100, F, cap) == (cap, True)      # saturation
+    assert P.quantise(0, None, F, cap) == (cap, True)     # +inf
+
+
+def test_q_cap_root_fits():
+    for n in [1, 16, 25600, 1 << 17, 1 << 20]:
+        assert P.q_cap(n) * n <= (1 << 63) - 1
+        assert (P.q_cap(n) + 1) * n > (1 << 63) - 1
+
+
+def test_rn32_helper_matches_numpy():
+    g = np.random.default_rng(5)
+    for x in np.concatenate([g.normal(0, 1e3, 500) ** 2, 10.0 ** g.uniform(-40, 38, 500)]):
+        assert P.rn32(float(x)) == float(np.float32(x))
