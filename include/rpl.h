@@ -1,0 +1,254 @@
+/*
+ * rpl.h — C ABI of librpl: the B200 (sm_100a) replay + return-estimation hot path
+ * of rlpyt (arXiv 1909.01500).  SURVEY.md §8(b) lists these entry points.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n, S:n = /root/reference/SPEC.md
+ * line n, "§8c #k" = reading k of SURVEY.md §8(c) (restated in DESIGN.md).
+ *
+ * Conventions for every call
+ *  - Pointers are CUDA DEVICE pointers unless the comment says (host).
+ *  - `stream` is a cudaStream_t passed as an opaque pointer (NULL = legacy
+ *    default stream).  Every call only ENQUEUES kernels on `stream` and returns;
+ *    no call synchronises the device or allocates memory.  Torch (or any caller)
+ *    owns all device buffers.
+ *  - Layouts are row-major and contiguous.  [T,B] is time-major ("[Time, Batch]",
+ *    P:232): element (t,b) is at t*B + b.
+ *  - Return value: RPL_OK (0) or a negative rpl_status.  Argument/shape errors are
+ *    detected on the host before anything is enqueued.  Data-dependent errors are
+ *    OR-ed into *dev_err (a device int32, may be NULL) as RPL_DERR_* bits while the
+ *    kernel still produces the defined output described per call.
+ *  - Calls on the same sum tree must be stream-ordered by the caller (the device
+ *    analogue of rlpyt's replay read-write lock).  No kernel uses
+ *    floating-point atomics: every output is bit-deterministic for fixed inputs.
+ */
+#ifndef RPL_H_
+#define RPL_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RPL_ABI_VERSION 1
+#define RPL_MAX_LEVELS 12
+
+typedef enum {
+  RPL_OK = 0,
+  RPL_EINVAL = -1,       /* null pointer, bad shape or parameter */
+  RPL_ERANGE = -2,       /* host-visible range error (e.g. n_step > T) */
+  RPL_EEMPTY = -3,       /* sampling requested with n == 0 where not allowed */
+  RPL_ECUDA = -4,        /* kernel launch / CUDA runtime failure */
+  RPL_EUNSUPPORTED = -5  /* configuration not supported by this build */
+} rpl_status;
+
+/* device error word bits */
+enum {
+  RPL_DERR_IDX = 1,           /* a leaf index outside [0, n_leaves): entry skipped */
+  RPL_DERR_SATURATED = 2,     /* a priority exceeded q_cap: clamped to q_cap */
+  RPL_DERR_EMPTY = 4,         /* sampling from a tree whose total is 0: idx = -1 */
+  RPL_DERR_INVALID_LEAF = 8,  /* gather window not fully inside the valid ring rows */
+  RPL_DERR_TREE = 16          /* descent found a prefix >= node sum (inconsistent tree) */
+};
+
+const char* rpl_strerror(int status);
+int rpl_abi_version(void);
+/* Number of kernel launches this process has issued through librpl (host counter). */
+int64_t rpl_launch_count(void);
+
+/* =========================================================================
+ * (1) Return estimation over time-major [T,B] buffers.  fp32 I/O, fp64
+ *     accumulation, one rounding to fp32 per output (§8c #21).
+ *     r: rewards f32 [T,B]; d: done u8 [T,B] (1 = episode ended after row t, §8c #1).
+ * ========================================================================= */
+
+/* R_t = r_t + gamma (1 - d_t) R_{t+1},  R_T = bootstrap[b] (or 0 if bootstrap == NULL).
+ * S:346 (discounted return), S:751 (returns).  ret: f32 [T,B].  T, B >= 1. */
+int rpl_returns_discounted(const float* r, const uint8_t* d, const float* bootstrap,
+                           int64_t T, int64_t B, double gamma, float* ret, void* stream);
+
+/* n-step return, S:591-599, P:38:
+ *   R^n_t = sum_{i<n} gamma^i r_{t+i} prod_{j<i} (1 - d_{t+j}),  done^n_t = OR_{i<n} d_{t+i},
+ * for output rows t = 0 .. T-n (ret_n, done_n are [T-n+1, B]).
+ * If q != NULL (value of s_tau, f32 [T,B]) then q_boot (f32 [B], the value at row T) is
+ * required and ret_n holds the target  y_t = R^n_t + gamma^n (1 - done^n_t) q_{t+n}
+ * (S:713-714).  If rescale != 0 the target is y_t = h(R^n_t + gamma^n (1-done^n_t) h^-1(q_{t+n}))
+ * (§8c #5), or h(R^n_t) when q == NULL; eps = rescale_eps (> 0).
+ * done_n may be NULL.  1 <= n <= T, else RPL_ERANGE. */
+int rpl_returns_nstep(const float* r, const uint8_t* d, int64_t T, int64_t B, int32_t n,
+                      double gamma, const float* q, const float* q_boot, int32_t rescale,
+                      double rescale_eps, float* ret_n, uint8_t* done_n, void* stream);
+
+/* GAE:  delta_t = r_t + gamma (1-d_t) V_{t+1} - V_t  (V_T = bootstrap_v[b]),
+ * A_t = delta_t + gamma lambda (1-d_t) A_{t+1}, A_T = 0;  ret_t = A_t + V_t.
+ * v: f32 [T,B]; bootstrap_v: f32 [B] (required); adv, ret: f32 [T,B] (ret may be NULL). */
+int rpl_gae(const float* r, const float* v, const uint8_t* d, const float* bootstrap_v,
+            int64_t T, int64_t B, double gamma, double lambda, float* adv, float* ret, void* stream);
+
+/* Value rescaling h (inverse == 0) or h^-1 (inverse != 0), elementwise over n floats, S:810:
+ *   h(x) = sign(x)(sqrt(|x|+1) - 1) + eps x, evaluated in fp64 in the cancellation-free
+ *   forms of §8c #4; eps > 0.  x, y: f32 [n] (may alias). */
+int rpl_value_rescale(const float* x, float* y, int64_t n, double eps, int32_t inverse, void* stream);
+
+/* =========================================================================
+ * (2) Prioritized replay on an int64 fixed-point sum tree ("prioritized replay
+ *     (sum tree)").  Storage is ONE caller-owned int64 device array of
+ *     layout.n_words words:
+ *       [level 0 (root) | level 1 | ... | level depth (leaves)]  then  [header words]
+ *     Level l holds level_len[l] nodes at word level_off[l]; node j of level l covers
+ *     leaves [j*W^(depth-l), (j+1)*W^(depth-l)); its W children are nodes j*W..j*W+W-1
+ *     of level l+1.  Every level is zero-padded to a multiple of W.  Leaf i is word
+ *     level_off[depth] + i and holds q_i = round_half_even(RN32(p_i^alpha) * 2^F)
+ *     (§8c #7).  Header: [hdr_off+0] max-priority-seen, [hdr_off+1] sampler
+ *     ticket (library scratch, always 0 between calls).
+ * ========================================================================= */
+typedef struct {
+  int64_t n_leaves;
+  int32_t fanout;       /* W: power of two in [2, 32] */
+  int32_t depth;        /* D >= 1: smallest with W^D >= n_leaves */
+  int32_t frac_bits;    /* F in [0, 62] */
+  int32_t _pad;
+  int64_t q_cap;        /* floor((2^63-1) / n_leaves): the root never overflows */
+  int64_t level_off[RPL_MAX_LEVELS];
+  int64_t level_len[RPL_MAX_LEVELS];  /* padded to a multiple of W (except the root) */
+  int64_t hdr_off;
+  int64_t n_words;      /* int64 words the caller must allocate */
+} rpl_tree_layout;
+
+/* Fill *out (host) for n_leaves >= 1, fanout in {2,4,8,16,32}, frac_bits in [0,62]. */
+int rpl_sumtree_layout(int64_t n_leaves, int32_t fanout, int32_t frac_bits, rpl_tree_layout* out);
+
+/* Zero every node and set max-seen to 2^F (priority 1.0, §8c #12). */
+int rpl_sumtree_init(const rpl_tree_layout* L, int64_t* tree, void* stream);
+
+/* Batched priority update (a5-a7): for k in 0..n-1, p = RN64(|td_abs[k]| + eps_p),
+ * q = RNE(RN32(p^alpha) * 2^F) clamped to q_cap; leaf idx[k] := q.  Duplicate indices: the
+ * LAST position in the batch wins.  Internal nodes are updated exactly (int64).
+ * max-seen := max(max-seen, every valid q in the batch).  Bad idx -> skipped + RPL_DERR_IDX.
+ * alpha >= 0, eps_p >= 0.  n >= 0 (n == 0 is a no-op). */
+int rpl_sumtree_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx,
+                       const float* td_abs, int64_t n, double alpha, double eps_p,
+                       int32_t* dev_err, void* stream);
+
+/* Direct leaf write (append / validity maintenance, §8a a12): leaf idx[k] := q[k]
+ * (last write wins; max-seen updated), or := current max-seen when q == NULL.
+ * q values > q_cap are clamped (+ RPL_DERR_SATURATED); q < 0 is invalid (skipped + IDX). */
+int rpl_sumtree_set_q(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx,
+                      const int64_t* q, int64_t n, int32_t* dev_err, void* stream);
+
+/* Stratified proportional sampling by tree descent (a8) + IS weights (a9).
+ * Q = root.  Stratum k of n: lo_k = floor(k Q / n), hi_k = lo_{k+1};
+ * prefix_k = lo_k + floor(u_k (hi_k - lo_k) / 2^64) with u_k = draws[k], or, when
+ * draws == NULL, u_k = Philox4x32-10(ctr = offset + k, key = seed) words 0|1<<32.
+ * out_idx[k] = the unique leaf i with C_i <= prefix_k < C_{i+1} (C = exclusive prefix
+ * sums), out_q[k] = q_i, *out_qmin = min_k out_q[k].  If out_w != NULL:
+ * out_w[k] = (N P_k)^-beta / max_j (N P_j)^-beta = (qmin / q_k)^beta  (§8c #10),
+ * computed in fp64.  Q == 0 -> out_idx = -1, out_q = 0, RPL_DERR_EMPTY.  `tree` is
+ * written only in its sampler-ticket header word.  n >= 1. */
+int rpl_sumtree_sample(const rpl_tree_layout* L, int64_t* tree, int64_t n, const uint64_t* draws,
+                       uint64_t seed, uint64_t offset, double beta, int64_t* out_idx,
+                       int64_t* out_q, int64_t* out_qmin, float* out_w, int32_t* dev_err,
+                       void* stream);
+
+/* Sharded sampling: rank `rank` of n_shards holds one tree; shard_totals
+ * (device int64 [n_shards], e.g. all-gathered rpl_sumtree_total outputs) define the global
+ * total Q and the shard-major global leaf order (global idx = rank * shard_leaves + local).
+ * Every rank evaluates the same n global strata; it descends only the strata whose prefix
+ * falls in its own range and writes out_idx[k] = global leaf index (or -1 when not owned),
+ * out_q[k] (0 when not owned), *out_qmin = min over owned (INT64_MAX if none).  Equal to
+ * rpl_sumtree_sample on the concatenation of the shards (§8c #17). */
+int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t rank,
+                               int32_t n_shards, int64_t shard_leaves, const int64_t* shard_totals,
+                               int64_t n, const uint64_t* draws, uint64_t seed, uint64_t offset,
+                               int64_t* out_idx, int64_t* out_q, int64_t* out_qmin,
+                               int32_t* dev_err, void* stream);
+
+/* Descent for explicit prefixes: out_idx[k] = leaf with C_i <= prefix[k] < C_{i+1}.
+ * prefix >= total -> clamped to the last non-empty leaf + RPL_DERR_TREE. */
+int rpl_sumtree_find(const rpl_tree_layout* L, const int64_t* tree, const int64_t* prefix,
+                     int64_t n, int64_t* out_idx, int32_t* dev_err, void* stream);
+
+/* *out_total = root (int64, device). */
+int rpl_sumtree_total(const rpl_tree_layout* L, const int64_t* tree, int64_t* out_total, void* stream);
+
+/* Recompute every internal node from the leaves (resume after restoring leaves). */
+int rpl_sumtree_rebuild(const rpl_tree_layout* L, int64_t* tree, void* stream);
+
+/* w[k] = (qmin / q[k])^beta in fp64, rounded to f32 (§8c #10); q[k] <= 0 -> w = 0. */
+int rpl_is_weights(const int64_t* q, const int64_t* qmin, int64_t n, double beta, float* w,
+                   void* stream);
+
+/* =========================================================================
+ * (3) Gather of sampled transitions / sequences from a frame-deduplicated ring
+ *     ("n-step returns; sequence replay; periodic storage of recurrent state;
+ *     frame-based buffer ... storing only unique Atari frames").
+ *
+ * Ring: cap_T rows x B columns, time-major; obs [cap_T, B, obs_bytes] (one unique frame
+ * or vector per row), act [cap_T, B, act_bytes], rew f32 [cap_T, B], done u8 [cap_T, B],
+ * rnn [cap_T/period, B, rnn_parts, rnn_bytes].  `cursor` = ring row of the next append,
+ * `size` = number of valid rows.  Row arithmetic wraps modulo cap_T.
+ *
+ * Frame stacks (k items, oldest -> newest) are rebuilt as a frame-stacking wrapper
+ * would have produced them: a row tau whose previous row ended an episode
+ * (done[tau-1] = 1) starts a new episode, and stack slots before the episode start
+ * repeat its first frame (pad_mode RPL_PAD_REPEAT) or are zero
+ * (RPL_PAD_ZERO) (§8c #13).
+ *
+ * TRANSITION (leaf = row*B + b): o_obs [n, k, obs_bytes] = stack at row, o_next_obs = stack
+ * at row+n_step, o_act [n, act_bytes] = act[row], o_ret f32 [n] = R^n over rows
+ * row..row+n_step-1, o_done_n u8 [n] (§8c #14).
+ * SEQUENCE (leaf = block*B + b, row0 = block*period, §8c #15-16): L = seq_len rows from
+ * row0, all outputs time-major [L, n, ...]: o_obs [L, n, k, obs_bytes] (RPL_OUT_STACKED)
+ * or the raw rows row0-k+1 .. row0+L-1 as [L+k-1, n, obs_bytes] (RPL_OUT_UNIQUE);
+ * o_act, o_rew, o_done at rows row0..row0+L-1; o_prev_act, o_prev_rew at rows
+ * row0-1..row0+L-2, zero on an episode's first row (§8c #18); o_rnn [rnn_parts, n,
+ * rnn_bytes] = rnn[block, b] (P:232 [Num_Layers, Batch, Hidden] per part, §8c #19).
+ * Any output pointer may be NULL (not produced).  If o_w, q and qmin are all non-NULL,
+ * o_w[k] = (qmin/q[k])^beta (a9).  idx[k] < 0 -> sample skipped (outputs untouched).
+ * A window not fully inside the valid rows sets RPL_DERR_INVALID_LEAF (output still the
+ * defined function of the ring contents).  obs_bytes % 16 == 0 with 16-byte aligned
+ * pointers uses TMA bulk copies; other sizes use vectorised LSU copies.
+ * ========================================================================= */
+enum { RPL_GATHER_TRANSITION = 0, RPL_GATHER_SEQUENCE = 1 };
+enum { RPL_PAD_REPEAT = 0, RPL_PAD_ZERO = 1 };
+enum { RPL_OUT_STACKED = 0, RPL_OUT_UNIQUE = 1 };
+
+typedef struct {
+  int32_t kind, pad_mode, out_mode, k;
+  int64_t cap_T, B, cursor, size;
+  int64_t obs_bytes, act_bytes, rnn_bytes;
+  int32_t n_step, seq_len, period, rnn_parts;
+  double gamma;
+  const void* obs;
+  const void* act;
+  const float* rew;
+  const uint8_t* done;
+  const void* rnn;
+  void* o_obs;
+  void* o_next_obs;
+  void* o_act;
+  void* o_prev_act;
+  float* o_rew;
+  float* o_prev_rew;
+  uint8_t* o_done;
+  float* o_ret;
+  uint8_t* o_done_n;
+  float* o_w;
+  void* o_rnn;
+} rpl_gather_desc;
+
+int rpl_gather(const rpl_gather_desc* desc /* host */, const int64_t* idx, const int64_t* q,
+               const int64_t* qmin, double beta, int64_t n, int32_t* dev_err, void* stream);
+
+/* -------------------------------------------------------------------------
+ * Diagnostics (tests only): v[k] = RN32(RN64(|td_abs[k]| + eps_p)^alpha) exactly as
+ * rpl_sumtree_update computes it (§8c #7); force_slow != 0 runs the double-double
+ * fallback for every element; out_slow[k] (may be NULL) = 1 when the fallback ran.
+ * ------------------------------------------------------------------------- */
+int rpl_debug_priority_values(const float* td_abs, int64_t n, double alpha, double eps_p,
+                              int32_t force_slow, float* out_v, uint8_t* out_slow, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RPL_H_ */

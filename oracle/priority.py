@@ -73,6 +73,8 @@ def rn32(x: float) -> float:
 def priority_value(td_abs: float, alpha: float, eps_p: float = 1e-3) -> tuple[int, int]:
     """v = RN32((RN64(|delta| + eps_p)) ** alpha) as (M, E). S:624, §8c #7."""
     p = abs(float(td_abs)) + float(eps_p)        # IEEE double add: RN64
+    if math.isnan(p) or math.isinf(p):
+        return 0, None                           # non-finite priority: saturates (header rpl.h)
     if alpha == 0.0:
         return 1 << 23, -23                      # p**0 == 1 exactly
     y = _C.power(_C.mpf(p), _C.mpf(float(alpha)))

@@ -54,13 +54,13 @@ class SumTreeOracle:
     def update(self, idx, td_abs, alpha: float, eps_p: float = 1e-3):
         for i, d in zip(idx, td_abs):
             i = int(i)
+            if i < 0 or i >= self.n_leaves:
+                self.err_idx = True
+                continue
             M, E = _pr.priority_value(float(d), alpha, eps_p)
             qv, sat = _pr.quantise(M, E, self.frac_bits, self.cap)
             if sat:
                 self.err_saturated = True
-            if i < 0 or i >= self.n_leaves:
-                self.err_idx = True
-                continue
             self.q[i] = qv
             self.max_seen = max(self.max_seen, qv)
 
@@ -70,7 +70,7 @@ class SumTreeOracle:
         for k, i in enumerate(idx):
             i = int(i)
             v = self.max_seen if q is None else int(q[k])
-            if i < 0 or i >= self.n_leaves:
+            if i < 0 or i >= self.n_leaves or v < 0:
                 self.err_idx = True
                 continue
             if v > self.cap:

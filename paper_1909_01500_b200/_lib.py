@@ -1,0 +1,112 @@
+"""ctypes loader for librpl.so (include/rpl.h).  Argument marshalling only.
+
+The product path has no fallback: if the shared library is missing or fails to
+load, importing this module raises.  Nothing here (or anywhere in the package)
+imports the CPU oracle.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librpl.so")
+
+RPL_MAX_LEVELS = 12
+
+RPL_OK = 0
+STATUS = {0: "RPL_OK", -1: "RPL_EINVAL", -2: "RPL_ERANGE", -3: "RPL_EEMPTY", -4: "RPL_ECUDA",
+          -5: "RPL_EUNSUPPORTED"}
+DERR = {1: "RPL_DERR_IDX", 2: "RPL_DERR_SATURATED", 4: "RPL_DERR_EMPTY", 8: "RPL_DERR_INVALID_LEAF",
+        16: "RPL_DERR_TREE"}
+GATHER_TRANSITION, GATHER_SEQUENCE = 0, 1
+PAD_REPEAT, PAD_ZERO = 0, 1
+OUT_STACKED, OUT_UNIQUE = 0, 1
+
+
+class TreeLayout(C.Structure):
+    _fields_ = [
+        ("n_leaves", C.c_int64),
+        ("fanout", C.c_int32),
+        ("depth", C.c_int32),
+        ("frac_bits", C.c_int32),
+        ("_pad", C.c_int32),
+        ("q_cap", C.c_int64),
+        ("level_off", C.c_int64 * RPL_MAX_LEVELS),
+        ("level_len", C.c_int64 * RPL_MAX_LEVELS),
+        ("hdr_off", C.c_int64),
+        ("n_words", C.c_int64),
+    ]
+
+
+class GatherDesc(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int32), ("pad_mode", C.c_int32), ("out_mode", C.c_int32), ("k", C.c_int32),
+        ("cap_T", C.c_int64), ("B", C.c_int64), ("cursor", C.c_int64), ("size", C.c_int64),
+        ("obs_bytes", C.c_int64), ("act_bytes", C.c_int64), ("rnn_bytes", C.c_int64),
+        ("n_step", C.c_int32), ("seq_len", C.c_int32), ("period", C.c_int32), ("rnn_parts", C.c_int32),
+        ("gamma", C.c_double),
+        ("obs", C.c_void_p), ("act", C.c_void_p), ("rew", C.c_void_p), ("done", C.c_void_p),
+        ("rnn", C.c_void_p),
+        ("o_obs", C.c_void_p), ("o_next_obs", C.c_void_p), ("o_act", C.c_void_p), ("o_prev_act", C.c_void_p),
+        ("o_rew", C.c_void_p), ("o_prev_rew", C.c_void_p), ("o_done", C.c_void_p), ("o_ret", C.c_void_p),
+        ("o_done_n", C.c_void_p), ("o_w", C.c_void_p), ("o_rnn", C.c_void_p),
+    ]
+
+
+P = C.c_void_p
+I64 = C.c_int64
+I32 = C.c_int32
+U64 = C.c_uint64
+D = C.c_double
+
+_SIGS = {
+    "rpl_strerror": ([C.c_int], C.c_char_p),
+    "rpl_abi_version": ([], C.c_int),
+    "rpl_launch_count": ([], I64),
+    "rpl_returns_discounted": ([P, P, P, I64, I64, D, P, P], C.c_int),
+    "rpl_returns_nstep": ([P, P, I64, I64, I32, D, P, P, I32, D, P, P, P], C.c_int),
+    "rpl_gae": ([P, P, P, P, I64, I64, D, D, P, P, P], C.c_int),
+    "rpl_value_rescale": ([P, P, I64, D, I32, P], C.c_int),
+    "rpl_sumtree_layout": ([I64, I32, I32, C.POINTER(TreeLayout)], C.c_int),
+    "rpl_sumtree_init": ([C.POINTER(TreeLayout), P, P], C.c_int),
+    "rpl_sumtree_update": ([C.POINTER(TreeLayout), P, P, P, I64, D, D, P, P], C.c_int),
+    "rpl_sumtree_set_q": ([C.POINTER(TreeLayout), P, P, P, I64, P, P], C.c_int),
+    "rpl_sumtree_sample": ([C.POINTER(TreeLayout), P, I64, P, U64, U64, D, P, P, P, P, P, P], C.c_int),
+    "rpl_sumtree_sample_sharded": ([C.POINTER(TreeLayout), P, I32, I32, I64, P, I64, P, U64, U64, P, P, P, P, P],
+                                   C.c_int),
+    "rpl_sumtree_find": ([C.POINTER(TreeLayout), P, P, I64, P, P, P], C.c_int),
+    "rpl_sumtree_total": ([C.POINTER(TreeLayout), P, P, P], C.c_int),
+    "rpl_sumtree_rebuild": ([C.POINTER(TreeLayout), P, P], C.c_int),
+    "rpl_is_weights": ([P, P, I64, D, P, P], C.c_int),
+    "rpl_gather": ([C.POINTER(GatherDesc), P, P, P, D, I64, P, P], C.c_int),
+    "rpl_debug_priority_values": ([P, I64, D, D, I32, P, P, P], C.c_int),
+}
+
+EXPORTS = tuple(_SIGS)
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"librpl.so not built at {LIB_PATH}: run `python -m paper_1909_01500_b200.build` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    lib = C.CDLL(LIB_PATH)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+lib = _load()
+assert lib.rpl_abi_version() == 1, "librpl ABI version mismatch"
+
+
+class RplError(RuntimeError):
+    pass
+
+
+def check(status: int, what: str = ""):
+    if status != RPL_OK:
+        msg = lib.rpl_strerror(status).decode()
+        raise RplError(f"{what}: {STATUS.get(status, status)} ({msg})")

@@ -1,0 +1,116 @@
+// Shared device/host helpers for librpl (sm_100a).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rpl.h"
+
+namespace rpl {
+
+extern int64_t g_launches;  // host-side launch counter (rpl_launch_count)
+
+inline int sm_count() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cached = v > 0 ? v : 148;
+  }
+  return cached;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Check the last launch; map failures to RPL_ECUDA.
+inline int launch_status() {
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? RPL_OK : RPL_ECUDA;
+}
+
+__device__ __forceinline__ void set_err(int32_t* err, int32_t bits) {
+  if (err) atomicOr(err, bits);
+}
+
+// 64-bit warp shuffles (int64 payloads)
+__device__ __forceinline__ int64_t shfl_up64(int64_t v, int d) {
+  return (int64_t)__shfl_up_sync(0xffffffffu, (unsigned long long)v, d);
+}
+__device__ __forceinline__ int64_t shfl64(int64_t v, int src) {
+  return (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)v, src);
+}
+__device__ __forceinline__ int64_t shfl_xor64(int64_t v, int m) {
+  return (int64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)v, m);
+}
+
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) v += shfl_xor64(v, m);
+  return v;
+}
+__device__ __forceinline__ int64_t warp_max64(int64_t v) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    int64_t o = shfl_xor64(v, m);
+    v = o > v ? o : v;
+  }
+  return v;
+}
+__device__ __forceinline__ int64_t warp_min64(int64_t v) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    int64_t o = shfl_xor64(v, m);
+    v = o < v ? o : v;
+  }
+  return v;
+}
+
+// Device-side view of the tree layout (passed by value to kernels).
+struct TreeDev {
+  int64_t n_leaves;
+  int64_t q_cap;
+  int64_t level_off[RPL_MAX_LEVELS];
+  int64_t hdr_off;
+  int32_t fanout, log2w, depth, frac_bits;
+};
+
+inline TreeDev tree_dev(const rpl_tree_layout* L) {
+  TreeDev t;
+  t.n_leaves = L->n_leaves;
+  t.q_cap = L->q_cap;
+  for (int i = 0; i < RPL_MAX_LEVELS; ++i) t.level_off[i] = L->level_off[i];
+  t.hdr_off = L->hdr_off;
+  t.fanout = L->fanout;
+  int lg = 0;
+  while ((1 << lg) < L->fanout) ++lg;
+  t.log2w = lg;
+  t.depth = L->depth;
+  t.frac_bits = L->frac_bits;
+  return t;
+}
+
+// Philox4x32-10 [EXT: Salmon et al. 2011]; u64 draw = x0 | x1 << 32 for
+// ctr = (lo32(c), hi32(c), 0, 0), key = (lo32(seed), hi32(seed)).
+__device__ __forceinline__ uint64_t philox_u64(uint64_t seed, uint64_t c) {
+  uint32_t c0 = (uint32_t)c, c1 = (uint32_t)(c >> 32), c2 = 0, c3 = 0;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  return (uint64_t)c0 | ((uint64_t)c1 << 32);
+}
+
+}  // namespace rpl

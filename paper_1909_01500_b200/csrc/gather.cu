@@ -1,0 +1,517 @@
+// Gather of sampled transitions and sequences from the frame-deduplicated ring
+// (P:38, P:123 fn).
+//
+// Design (B200): the gather is a pure HBM copy with a little index arithmetic, so
+// it is built around the Tensor Memory Accelerator's bulk-copy path:
+//   * one CTA per task (transition sample, or sequence sample x chunk of C rows);
+//   * one elected thread issues cp.async.bulk global->shared copies of every
+//     unique frame row the task needs (7056-B Atari frames, 16-B aligned) on one
+//     mbarrier (expect_tx = total bytes);
+//   * meanwhile the other warps resolve episode starts from the done flags
+//     (frame-stack padding, §8c #13), copy the small per-row fields and compute
+//     the fused n-step return (fp64 Horner);
+//   * after the barrier, one lane per output stack issues a cp.async.bulk
+//     shared->global store of the whole k-stack (k*7056 B contiguous in shared
+//     memory when the stack has no padding, else one store per frame).
+// Each unique frame is read from HBM once per task and written once per stack
+// slot that uses it: the algorithmic bytes of SURVEY.md §8(d).
+// Items whose size is not a multiple of 16 bytes (Mujoco vectors) use the same
+// index logic with vectorised LSU copies.
+#include <math.h>
+
+#include "common.cuh"
+
+namespace rpl {
+namespace {
+
+constexpr int G_THREADS = 128;
+constexpr int SEQ_CHUNK = 8;  // output rows per sequence task
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+// Cooperative copy of `bytes` bytes with the widest aligned word.
+__device__ __forceinline__ void coop_copy(void* dst, const void* src, int64_t bytes, int t, int nt) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src);
+  if ((a & 15) == 0 && (bytes & 15) == 0) {
+    const int4* s = reinterpret_cast<const int4*>(src);
+    int4* d = reinterpret_cast<int4*>(dst);
+    for (int64_t i = t; i < bytes / 16; i += nt) d[i] = __ldg(s + i);
+  } else if ((a & 3) == 0 && (bytes & 3) == 0) {
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+    for (int64_t i = t; i < bytes / 4; i += nt) d[i] = __ldg(s + i);
+  } else {
+    const uint8_t* s = reinterpret_cast<const uint8_t*>(src);
+    uint8_t* d = reinterpret_cast<uint8_t*>(dst);
+    for (int64_t i = t; i < bytes; i += nt) d[i] = __ldg(s + i);
+  }
+}
+__device__ __forceinline__ void coop_zero(void* dst, int64_t bytes, int t, int nt) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(dst);
+  if ((a & 15) == 0 && (bytes & 15) == 0) {
+    int4* d = reinterpret_cast<int4*>(dst);
+    for (int64_t i = t; i < bytes / 16; i += nt) d[i] = make_int4(0, 0, 0, 0);
+  } else {
+    uint8_t* d = reinterpret_cast<uint8_t*>(dst);
+    for (int64_t i = t; i < bytes; i += nt) d[i] = 0;
+  }
+}
+
+struct GDesc {
+  int32_t kind, pad_mode, out_mode, k;
+  int64_t cap_T, B, cursor, size;
+  int64_t obs_bytes, act_bytes, rnn_bytes;
+  int32_t n_step, seq_len, period, rnn_parts;
+  double gamma;
+  const uint8_t* obs;
+  const uint8_t* act;
+  const float* rew;
+  const uint8_t* done;
+  const uint8_t* rnn;
+  uint8_t* o_obs;
+  uint8_t* o_next_obs;
+  uint8_t* o_act;
+  uint8_t* o_prev_act;
+  float* o_rew;
+  float* o_prev_rew;
+  uint8_t* o_done;
+  float* o_ret;
+  uint8_t* o_done_n;
+  float* o_w;
+  uint8_t* o_rnn;
+  int use_tma;
+};
+
+__device__ __forceinline__ int64_t wrap(int64_t r, int64_t cap) {
+  r %= cap;
+  return r < 0 ? r + cap : r;
+}
+
+// Source slot (window index) of stack slot j for target row index `ti` (window
+// coordinates: window index w <-> ring row first + w).  Episode start s(t) is the
+// latest row s in (t-k+1, t] whose previous row ended an episode, else t-k+1
+// (frame-stacking wrapper semantics, §8c #13).  Returns -1 for a zero slot.
+// dwin[w] = done flag of window row w-1 (dwin has one extra leading entry).
+__device__ __forceinline__ int stack_src(const uint8_t* dwin, int ti, int j, int k, int pad_mode) {
+  int s = ti;
+  while (s > ti - k + 1 && !dwin[s]) --s;  // dwin[s] = done[row s - 1]
+  const int want = ti - k + 1 + j;
+  if (want >= s) return want;
+  return pad_mode == RPL_PAD_ZERO ? -1 : s;
+}
+
+// ---------------------------------------------------------------------------
+// Transitions: one CTA per sample.  Window rows r-k+1 .. r+n (NR = k+n rows).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(G_THREADS)
+k_gather_transition(GDesc D, const int64_t* __restrict__ idx, int64_t n, const int64_t* __restrict__ q,
+                    const int64_t* __restrict__ qmin, double beta, int32_t* err) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint8_t dwin[64];
+  __shared__ int sslot[2][32];
+  const int tid = threadIdx.x;
+  const int64_t s = blockIdx.x;
+  const int64_t leaf = idx[s];
+  if (leaf < 0) return;
+  const int k = D.k, ns = D.n_step;
+  const int NR = k + ns;
+  if (leaf >= D.cap_T * D.B) {
+    if (tid == 0) set_err(err, RPL_DERR_IDX);
+    return;
+  }
+  const int64_t r = leaf / D.B, b = leaf - (leaf / D.B) * D.B;
+  const int64_t first = r - (k - 1);
+  const int64_t ob = D.obs_bytes;
+
+  const bool tma = D.use_tma && (D.o_obs || D.o_next_obs);
+  if (tma) {
+    if (tid == 0) {
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+      mbar_expect_tx(&bar, (uint32_t)(NR * ob));
+      for (int w = 0; w < NR; ++w) {
+        const int64_t row = wrap(first + w, D.cap_T);
+        bulk_g2s(smem + (int64_t)w * ob, D.obs + (row * D.B + b) * ob, (uint32_t)ob, &bar);
+      }
+    }
+  }
+  // done flags of rows first-1 .. r+n  (dwin[w] = done[first + w - 1])
+  if (tid < NR + 1) dwin[tid] = __ldg(D.done + wrap(first + tid - 1, D.cap_T) * D.B + b);
+  if (tid == 0) {
+    const int64_t age = wrap(D.cursor - 1 - r, D.cap_T);
+    if (!(age >= ns && age <= D.size - k)) set_err(err, RPL_DERR_INVALID_LEAF);
+  }
+  __syncthreads();
+  // stack slot sources: [0] obs at window index k-1, [1] next obs at window index k-1+n
+  if (tid < 2 * k) {
+    const int which = tid / k, j = tid - which * k;
+    sslot[which][j] = stack_src(dwin, (k - 1) + which * ns, j, k, D.pad_mode);
+  }
+  // scalars (warp 1): action, fused n-step return, IS weight (a9)
+  if (tid >= 32 && tid < 64) {
+    const int l = tid - 32;
+    if (D.o_act) {
+      const uint8_t* src = D.act + (r * D.B + b) * D.act_bytes;
+      uint8_t* dst = D.o_act + s * D.act_bytes;
+      for (int64_t i = l; i < D.act_bytes; i += 32) dst[i] = src[i];
+    }
+    if (l == 0) {
+      if (D.o_ret || D.o_done_n) {
+        double acc = 0.0;
+        uint8_t dn = 0;
+        for (int i = ns - 1; i >= 0; --i) {
+          const int64_t row = wrap(r + i, D.cap_T);
+          const uint8_t di = __ldg(D.done + row * D.B + b);
+          const double ri = (double)__ldg(D.rew + row * D.B + b);
+          acc = di ? ri : fma(D.gamma, acc, ri);
+          dn |= di;
+        }
+        if (D.o_ret) D.o_ret[s] = (float)acc;
+        if (D.o_done_n) D.o_done_n[s] = dn ? 1 : 0;
+      }
+      if (D.o_w && q && qmin) {
+        const int64_t qs = q[s];
+        D.o_w[s] = qs > 0 ? (float)pow((double)(*qmin) / (double)qs, beta) : 0.0f;
+      }
+    }
+  }
+  __syncthreads();
+
+  uint8_t* outs[2] = {D.o_obs ? D.o_obs + s * k * ob : nullptr, D.o_next_obs ? D.o_next_obs + s * k * ob : nullptr};
+  if (tma) {
+    uint8_t* zrow = smem + (int64_t)NR * ob;  // zero row for RPL_PAD_ZERO
+    bool needs_zero = false;
+    for (int w = 0; w < 2; ++w)
+      for (int j = 0; j < k; ++j) needs_zero |= (sslot[w][j] < 0);
+    if (needs_zero) {
+      coop_zero(zrow, ob, tid, G_THREADS);
+      fence_proxy_async();
+      __syncthreads();
+    }
+    if (tid < 32) {
+      if (tid == 0) mbar_wait(&bar, 0);
+      __syncwarp();
+      fence_proxy_async();
+      // lane 0: obs stack, lane 1: next-obs stack
+      if (tid < 2 && outs[tid]) {
+        const int* sl = sslot[tid];
+        bool contiguous = true;
+        for (int j = 1; j < k; ++j) contiguous &= (sl[j] == sl[0] + j) && sl[0] >= 0;
+        if (contiguous && sl[0] >= 0) {
+          bulk_s2g(outs[tid], smem + (int64_t)sl[0] * ob, (uint32_t)(k * ob));
+        } else {
+          for (int j = 0; j < k; ++j)
+            bulk_s2g(outs[tid] + j * ob, sl[j] < 0 ? zrow : smem + (int64_t)sl[j] * ob, (uint32_t)ob);
+        }
+        bulk_commit();
+        bulk_wait_read0();
+      }
+    }
+  } else if (!D.use_tma) {
+    for (int w = 0; w < 2; ++w) {
+      if (!outs[w]) continue;
+      for (int j = 0; j < k; ++j) {
+        const int src = sslot[w][j];
+        if (src < 0) {
+          coop_zero(outs[w] + j * ob, ob, tid, G_THREADS);
+        } else {
+          const int64_t row = wrap(first + src, D.cap_T);
+          coop_copy(outs[w] + j * ob, D.obs + (row * D.B + b) * ob, ob, tid, G_THREADS);
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Sequences: grid (chunks, samples).  Stacked: output rows tau in [c*C, c*C+C) of
+// L, window rows row0 + c*C - (k-1) .. row0 + c*C + C - 1.  Unique: output rows
+// u in [c*C, c*C+C) of L+k-1 <-> ring rows row0 - (k-1) + u.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(G_THREADS)
+k_gather_sequence(GDesc D, const int64_t* __restrict__ idx, int64_t n, const int64_t* __restrict__ q,
+                  const int64_t* __restrict__ qmin, double beta, int32_t* err) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint8_t dwin[64];
+  __shared__ int sslot[SEQ_CHUNK][8];
+  const int tid = threadIdx.x;
+  const int64_t s = blockIdx.y;
+  const int c = blockIdx.x;
+  const int64_t leaf = idx[s];
+  if (leaf < 0) return;
+  const int k = D.k, L = D.seq_len;
+  const int64_t nblk = D.cap_T / D.period;
+  if (leaf >= nblk * D.B) {
+    if (tid == 0 && c == 0) set_err(err, RPL_DERR_IDX);
+    return;
+  }
+  const int64_t blk = leaf / D.B, b = leaf - (leaf / D.B) * D.B;
+  const int64_t row0 = blk * D.period;
+  const int64_t ob = D.obs_bytes;
+  const bool stacked = D.out_mode == RPL_OUT_STACKED;
+  const int rows_out = stacked ? L : L + k - 1;
+  const int o0 = c * SEQ_CHUNK;
+  if (o0 >= rows_out && o0 >= L) return;
+  const int Cn = max(0, min(SEQ_CHUNK, rows_out - o0));
+  // window (frames to stage): stacked -> [row0+o0-(k-1), row0+o0+Cn); unique -> [row0-(k-1)+o0, +Cn)
+  const int64_t first = stacked ? row0 + o0 - (k - 1) : row0 - (k - 1) + o0;
+  const int NR = stacked ? (Cn > 0 ? Cn + k - 1 : 0) : Cn;
+
+  if (D.use_tma && NR > 0 && D.o_obs) {
+    if (tid == 0) {
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+      mbar_expect_tx(&bar, (uint32_t)(NR * ob));
+      for (int w = 0; w < NR; ++w) {
+        const int64_t row = wrap(first + w, D.cap_T);
+        bulk_g2s(smem + (int64_t)w * ob, D.obs + (row * D.B + b) * ob, (uint32_t)ob, &bar);
+      }
+    }
+  }
+  if (tid < NR + 1) dwin[tid] = __ldg(D.done + wrap(first + tid - 1, D.cap_T) * D.B + b);
+  if (tid == 0 && c == 0) {
+    const int64_t age = wrap(D.cursor - 1 - row0, D.cap_T);
+    const int hist = k - 1 > 1 ? k - 1 : 1;
+    if (!(age >= L - 1 && age + hist <= D.size - 1)) set_err(err, RPL_DERR_INVALID_LEAF);
+  }
+  __syncthreads();
+  if (stacked && tid < Cn * k) {
+    const int tau = tid / k, j = tid - (tid / k) * k;
+    sslot[tau][j] = stack_src(dwin, tau + k - 1, j, k, D.pad_mode);
+  }
+  // per-row scalars for output rows tau in [o0, o0+C) of L (both modes)
+  {
+    const int t_hi = min(o0 + SEQ_CHUNK, L);
+    for (int tau = o0 + (tid >> 5); tau < t_hi; tau += G_THREADS / 32) {
+      const int l = tid & 31;
+      const int64_t row = wrap(row0 + tau, D.cap_T);
+      const int64_t prow = wrap(row0 + tau - 1, D.cap_T);
+      const uint8_t pd = __ldg(D.done + prow * D.B + b);  // previous row ended an episode?
+      if (D.o_act)
+        for (int64_t i = l; i < D.act_bytes; i += 32)
+          D.o_act[(tau * n + s) * D.act_bytes + i] = D.act[(row * D.B + b) * D.act_bytes + i];
+      if (D.o_prev_act)
+        for (int64_t i = l; i < D.act_bytes; i += 32)
+          D.o_prev_act[(tau * n + s) * D.act_bytes + i] = pd ? 0 : D.act[(prow * D.B + b) * D.act_bytes + i];
+      if (l == 0) {
+        if (D.o_rew) D.o_rew[tau * n + s] = __ldg(D.rew + row * D.B + b);
+        if (D.o_prev_rew) D.o_prev_rew[tau * n + s] = pd ? 0.0f : __ldg(D.rew + prow * D.B + b);
+        if (D.o_done) D.o_done[tau * n + s] = __ldg(D.done + row * D.B + b);
+      }
+    }
+  }
+  // stored recurrent state at the sequence start (chunk 0), [parts, n, rnn_bytes]
+  if (c == 0 && D.o_rnn) {
+    for (int p = 0; p < D.rnn_parts; ++p)
+      coop_copy(D.o_rnn + (p * n + s) * D.rnn_bytes,
+                D.rnn + ((blk * D.B + b) * D.rnn_parts + p) * D.rnn_bytes, D.rnn_bytes, tid, G_THREADS);
+  }
+  if (c == 0 && D.o_w && q && qmin && tid == 0) {
+    const int64_t qs = q[s];
+    D.o_w[s] = qs > 0 ? (float)pow((double)(*qmin) / (double)qs, beta) : 0.0f;
+  }
+  __syncthreads();
+  if (!D.o_obs || NR == 0) return;
+
+  if (D.use_tma) {
+    uint8_t* zrow = smem + (int64_t)NR * ob;
+    bool needs_zero = false;
+    if (stacked)
+      for (int t = 0; t < Cn; ++t)
+        for (int j = 0; j < k; ++j) needs_zero |= (sslot[t][j] < 0);
+    if (needs_zero) {
+      coop_zero(zrow, ob, tid, G_THREADS);
+      fence_proxy_async();
+      __syncthreads();
+    }
+    if (tid < 32) {
+      if (tid == 0) mbar_wait(&bar, 0);
+      __syncwarp();
+      fence_proxy_async();
+      if (stacked) {
+        if (tid < Cn) {
+          const int tau = tid;
+          uint8_t* dst = D.o_obs + (((int64_t)(o0 + tau) * n + s) * k) * ob;
+          const int* sl = sslot[tau];
+          bool contiguous = sl[0] >= 0;
+          for (int j = 1; j < k; ++j) contiguous &= (sl[j] == sl[0] + j);
+          if (contiguous) {
+            bulk_s2g(dst, smem + (int64_t)sl[0] * ob, (uint32_t)(k * ob));
+          } else {
+            for (int j = 0; j < k; ++j)
+              bulk_s2g(dst + j * ob, sl[j] < 0 ? zrow : smem + (int64_t)sl[j] * ob, (uint32_t)ob);
+          }
+          bulk_commit();
+          bulk_wait_read0();
+        }
+      } else {
+        if (tid < Cn) {
+          uint8_t* dst = D.o_obs + ((int64_t)(o0 + tid) * n + s) * ob;
+          bulk_s2g(dst, smem + (int64_t)tid * ob, (uint32_t)ob);
+          bulk_commit();
+          bulk_wait_read0();
+        }
+      }
+    }
+  } else {
+    if (stacked) {
+      for (int tau = 0; tau < Cn; ++tau) {
+        uint8_t* dst = D.o_obs + (((int64_t)(o0 + tau) * n + s) * k) * ob;
+        for (int j = 0; j < k; ++j) {
+          const int src = sslot[tau][j];
+          if (src < 0) coop_zero(dst + j * ob, ob, tid, G_THREADS);
+          else coop_copy(dst + j * ob, D.obs + (wrap(first + src, D.cap_T) * D.B + b) * ob, ob, tid, G_THREADS);
+        }
+      }
+    } else {
+      for (int u = 0; u < Cn; ++u)
+        coop_copy(D.o_obs + ((int64_t)(o0 + u) * n + s) * ob,
+                  D.obs + (wrap(first + u, D.cap_T) * D.B + b) * ob, ob, tid, G_THREADS);
+    }
+  }
+}
+
+GDesc to_dev(const rpl_gather_desc* d) {
+  GDesc g;
+  g.kind = d->kind;
+  g.pad_mode = d->pad_mode;
+  g.out_mode = d->out_mode;
+  g.k = d->k;
+  g.cap_T = d->cap_T;
+  g.B = d->B;
+  g.cursor = d->cursor;
+  g.size = d->size;
+  g.obs_bytes = d->obs_bytes;
+  g.act_bytes = d->act_bytes;
+  g.rnn_bytes = d->rnn_bytes;
+  g.n_step = d->n_step;
+  g.seq_len = d->seq_len;
+  g.period = d->period;
+  g.rnn_parts = d->rnn_parts;
+  g.gamma = d->gamma;
+  g.obs = static_cast<const uint8_t*>(d->obs);
+  g.act = static_cast<const uint8_t*>(d->act);
+  g.rew = d->rew;
+  g.done = d->done;
+  g.rnn = static_cast<const uint8_t*>(d->rnn);
+  g.o_obs = static_cast<uint8_t*>(d->o_obs);
+  g.o_next_obs = static_cast<uint8_t*>(d->o_next_obs);
+  g.o_act = static_cast<uint8_t*>(d->o_act);
+  g.o_prev_act = static_cast<uint8_t*>(d->o_prev_act);
+  g.o_rew = d->o_rew;
+  g.o_prev_rew = d->o_prev_rew;
+  g.o_done = d->o_done;
+  g.o_ret = d->o_ret;
+  g.o_done_n = d->o_done_n;
+  g.o_w = d->o_w;
+  g.o_rnn = static_cast<uint8_t*>(d->o_rnn);
+  g.use_tma = 0;
+  return g;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+}  // namespace rpl
+
+using namespace rpl;
+
+extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q, const int64_t* qmin,
+                          double beta, int64_t n, int32_t* dev_err, void* stream) {
+  if (!desc || n < 0) return RPL_EINVAL;
+  if (n == 0) return RPL_OK;
+  if (!idx || !desc->done || !desc->obs || desc->cap_T < 1 || desc->B < 1 || desc->k < 1 || desc->k > 8 ||
+      desc->obs_bytes < 1 || desc->size < 0 || desc->size > desc->cap_T || desc->cursor < 0 ||
+      desc->cursor >= desc->cap_T)
+    return RPL_EINVAL;
+  if (desc->pad_mode != RPL_PAD_REPEAT && desc->pad_mode != RPL_PAD_ZERO) return RPL_EINVAL;
+  if ((desc->o_act || desc->o_prev_act) && (!desc->act || desc->act_bytes < 1)) return RPL_EINVAL;
+  if (desc->o_w && !(beta >= 0.0)) return RPL_EINVAL;
+  GDesc g = to_dev(desc);
+  const bool tma_ok = (desc->obs_bytes % 16 == 0) && aligned16(desc->obs) && aligned16(desc->o_obs) &&
+                      aligned16(desc->o_next_obs) && desc->obs_bytes <= 32768;
+  cudaStream_t st = as_stream(stream);
+  if (desc->kind == RPL_GATHER_TRANSITION) {
+    if (desc->n_step < 1 || desc->k + desc->n_step > 31) return RPL_EINVAL;
+    if ((desc->o_ret || desc->o_done_n) && !desc->rew) return RPL_EINVAL;
+    const int NR = desc->k + desc->n_step;
+    const int64_t smem = (int64_t)(NR + 1) * desc->obs_bytes;
+    g.use_tma = (tma_ok && smem <= 200 * 1024) ? 1 : 0;
+    const size_t dyn = g.use_tma ? (size_t)smem : 0;
+    static size_t set_t = 0;
+    if (dyn > 48 * 1024 && dyn > set_t) {
+      cudaFuncSetAttribute(k_gather_transition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      set_t = dyn;
+    }
+    if (n > 0x7fffffff) return RPL_EINVAL;
+    k_gather_transition<<<(unsigned)n, G_THREADS, dyn, st>>>(g, idx, n, q, qmin, beta, dev_err);
+    return launch_status();
+  }
+  if (desc->kind == RPL_GATHER_SEQUENCE) {
+    if (desc->seq_len < 1 || desc->period < 1 || desc->cap_T % desc->period != 0) return RPL_EINVAL;
+    if (desc->o_rnn && (!desc->rnn || desc->rnn_parts < 1 || desc->rnn_bytes < 1)) return RPL_EINVAL;
+    if ((desc->o_rew || desc->o_prev_rew) && !desc->rew) return RPL_EINVAL;
+    if (desc->out_mode != RPL_OUT_STACKED && desc->out_mode != RPL_OUT_UNIQUE) return RPL_EINVAL;
+    if (SEQ_CHUNK + desc->k > 32) return RPL_EINVAL;
+    const int64_t smem = (int64_t)(SEQ_CHUNK + desc->k) * desc->obs_bytes;
+    g.use_tma = (tma_ok && smem <= 200 * 1024) ? 1 : 0;
+    const size_t dyn = g.use_tma ? (size_t)smem : 0;
+    static size_t set_s = 0;
+    if (dyn > 48 * 1024 && dyn > set_s) {
+      cudaFuncSetAttribute(k_gather_sequence, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      set_s = dyn;
+    }
+    const int rows_out = desc->out_mode == RPL_OUT_STACKED ? desc->seq_len : desc->seq_len + desc->k - 1;
+    const int chunks = (rows_out + SEQ_CHUNK - 1) / SEQ_CHUNK;
+    if (n > 65535) return RPL_EINVAL;
+    dim3 grid((unsigned)chunks, (unsigned)n);
+    k_gather_sequence<<<grid, G_THREADS, dyn, st>>>(g, idx, n, q, qmin, beta, dev_err);
+    return launch_status();
+  }
+  return RPL_EINVAL;
+}

@@ -1,0 +1,480 @@
+// Prioritized replay on a wide int64 fixed-point sum tree.
+//
+// P:38 "prioritized replay (sum tree)"; S:553-629 (tree, sampling, IS weights,
+// priority updates); S:660 (max-priority-seen); readings §8c #7-#12, #17.
+//
+// Layout (rpl.h): levels root..leaves, fan-out W (<= 32, one warp lane per child),
+// every level padded to a multiple of W; leaf q_i = RNE(RN32(p_i^alpha) 2^F).
+// Integer sums make propagation order-independent and bit-exact.
+//
+//  update  one CTA: priority transform (crpow.cuh) -> last-writer-wins dedupe in a
+//          shared-memory hash table (atomicMax of batch position per leaf) -> the
+//          winner writes its leaf and adds its int64 delta to each ancestor
+//          (root delta warp-aggregated).  Chunks of 1024 entries are applied in
+//          batch order, so any batch size keeps last-write-wins.
+//  sample  one warp per draw: integer stratum -> prefix -> per level the warp loads
+//          the W child sums (one coalesced 256-B load), inclusive int64 warp scan,
+//          ballot(prefix < incl) picks the child.  The last CTA (ticket in the tree
+//          header) reduces the batch-min q and writes the IS weights (a9).
+#include <math.h>
+
+#include "common.cuh"
+#include "crpow.cuh"
+
+namespace rpl {
+namespace {
+
+constexpr int UPD_THREADS = 1024;
+constexpr int HASH_SLOTS = 2048;
+constexpr unsigned long long HASH_EMPTY = ~0ull;
+constexpr int SAMPLE_WARPS = 8;
+
+enum { MODE_TD = 0, MODE_Q = 1, MODE_MAXSEEN = 2 };
+
+__device__ __forceinline__ uint32_t hash_slot(int64_t leaf) {
+  return (uint32_t)(((unsigned long long)leaf * 0x9E3779B97F4A7C15ull) >> 53) & (HASH_SLOTS - 1);
+}
+
+__global__ void __launch_bounds__(UPD_THREADS)
+k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__ idx,
+              const float* __restrict__ td, const int64_t* __restrict__ qin, int mode, int64_t n,
+              double alpha, double eps_p, int32_t* err, int force_slow) {
+  __shared__ unsigned long long hkey[HASH_SLOTS];
+  __shared__ int hval[HASH_SLOTS];
+  __shared__ int64_t sred[UPD_THREADS / 32];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  int64_t* leaves = tree + L.level_off[L.depth];
+  int64_t* hdr = tree + L.hdr_off;
+  const int64_t maxseen_now = hdr[0];
+  int64_t local_max = INT64_MIN;
+  int32_t errbits = 0;
+
+  for (int64_t base = 0; base < n; base += UPD_THREADS) {
+    for (int s = tid; s < HASH_SLOTS; s += UPD_THREADS) {
+      hkey[s] = HASH_EMPTY;
+      hval[s] = -1;
+    }
+    __syncthreads();
+    const int64_t i = base + tid;
+    int64_t leaf = -1, q = 0;
+    if (i < n) {
+      leaf = idx[i];
+      bool ok = leaf >= 0 && leaf < L.n_leaves;
+      if (ok) {
+        if (mode == MODE_TD) {
+          const double p = (double)fabsf(td[i]) + eps_p;  // RN64(|delta| + eps_p)
+          float v;
+          if (!isfinite(p)) {
+            v = __int_as_float(0x7f800000);
+          } else {
+            bool slow = false;
+            v = cr_powf(p, alpha, force_slow != 0, &slow);
+          }
+          bool sat = false;
+          q = quantise_q(v, L.frac_bits, L.q_cap, &sat);
+          if (sat) errbits |= RPL_DERR_SATURATED;
+          local_max = q > local_max ? q : local_max;
+        } else if (mode == MODE_Q) {
+          q = qin[i];
+          if (q < 0) {
+            ok = false;
+          } else {
+            if (q > L.q_cap) {
+              q = L.q_cap;
+              errbits |= RPL_DERR_SATURATED;
+            }
+            local_max = q > local_max ? q : local_max;
+          }
+        } else {
+          q = maxseen_now;
+        }
+      }
+      if (!ok) {
+        errbits |= RPL_DERR_IDX;
+        leaf = -1;
+      }
+    }
+    uint32_t slot = 0;
+    if (leaf >= 0) {
+      slot = hash_slot(leaf);
+      while (true) {
+        unsigned long long prev = atomicCAS(&hkey[slot], HASH_EMPTY, (unsigned long long)leaf);
+        if (prev == HASH_EMPTY || prev == (unsigned long long)leaf) break;
+        slot = (slot + 1) & (HASH_SLOTS - 1);
+      }
+      atomicMax(&hval[slot], tid);  // last position in the batch wins
+    }
+    __syncthreads();
+    int64_t delta = 0;
+    if (leaf >= 0 && hval[slot] == tid) {
+      const int64_t old = __ldcg(leaves + leaf);
+      leaves[leaf] = q;
+      delta = q - old;
+      if (delta != 0) {
+        int64_t node = leaf;
+        for (int l = L.depth - 1; l >= 1; --l) {
+          node >>= L.log2w;
+          atomicAdd(reinterpret_cast<unsigned long long*>(tree + L.level_off[l] + node),
+                    (unsigned long long)delta);
+        }
+      }
+    }
+    const int64_t rd = warp_sum64(delta);
+    if (lane == 0 && rd != 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(tree + L.level_off[0]), (unsigned long long)rd);
+    __syncthreads();
+  }
+  // max-priority-seen
+  int64_t m = warp_max64(local_max);
+  if (lane == 0) sred[tid >> 5] = m;
+  __syncthreads();
+  if (tid < 32) {
+    m = tid < UPD_THREADS / 32 ? sred[tid] : INT64_MIN;
+    m = warp_max64(m);
+    if (tid == 0 && m > maxseen_now) atomicMax(reinterpret_cast<long long*>(hdr), (long long)m);
+  }
+  if (errbits) set_err(err, errbits);
+}
+
+__device__ __forceinline__ uint64_t stratum_lo(uint64_t k, uint64_t Q, uint64_t n) {
+  // floor(k Q / n) without 128-bit products: k*(Q/n) + floor(k*(Q%n)/n); k <= n < 2^31
+  return k * (Q / n) + (k * (Q % n)) / n;
+}
+
+// Descend from the root for `prefix` (< node sum); returns leaf index, writes q.
+__device__ __forceinline__ int64_t descend(const TreeDev& L, const int64_t* __restrict__ tree,
+                                           int64_t prefix, int64_t* q_out, int32_t* errbits) {
+  const int lane = threadIdx.x & 31;
+  int64_t node = 0;
+  int64_t c = 0;
+  for (int l = 0; l < L.depth; ++l) {
+    const int64_t base = L.level_off[l + 1] + (node << L.log2w);
+    c = lane < L.fanout ? tree[base + lane] : 0;
+    int64_t incl = c;
+#pragma unroll
+    for (int dlt = 1; dlt < 32; dlt <<= 1) {
+      const int64_t o = shfl_up64(incl, dlt);
+      if (lane >= dlt) incl += o;
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, prefix < incl);
+    int f;
+    if (bal == 0) {  // prefix >= node sum: inconsistent tree / out of range -> clamp
+      *errbits |= RPL_DERR_TREE;
+      const unsigned nz = __ballot_sync(0xffffffffu, c > 0);
+      f = nz ? 31 - __clz(nz) : 0;
+      const int64_t inc_last = shfl64(incl, f);
+      prefix = nz ? inc_last - 1 : 0;  // the last unit of the last non-empty child
+    } else {
+      f = __ffs(bal) - 1;
+    }
+    const int64_t inc_f = shfl64(incl, f);
+    const int64_t c_f = shfl64(c, f);
+    prefix -= inc_f - c_f;
+    if (prefix < 0) prefix = 0;
+    node = (node << L.log2w) + f;
+    c = c_f;
+  }
+  *q_out = c;
+  return node;
+}
+
+template <bool SHARDED>
+__global__ void __launch_bounds__(SAMPLE_WARPS * 32)
+k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* __restrict__ draws,
+              uint64_t seed, uint64_t offset, double beta, int64_t* __restrict__ out_idx,
+              int64_t* __restrict__ out_q, int64_t* __restrict__ out_qmin, float* __restrict__ out_w,
+              int32_t* err, int rank, int n_shards, int64_t shard_leaves,
+              const int64_t* __restrict__ totals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * SAMPLE_WARPS + (threadIdx.x >> 5);
+  int32_t errbits = 0;
+  uint64_t Q, own_lo = 0, own_T = 0;
+  if (SHARDED) {
+    Q = 0;
+    for (int g = 0; g < n_shards; ++g) {
+      const uint64_t tg = (uint64_t)totals[g];
+      if (g < rank) own_lo += tg;
+      if (g == rank) own_T = tg;
+      Q += tg;
+    }
+  } else {
+    Q = (uint64_t)tree[L.level_off[0]];
+  }
+  if (k < n) {
+    int64_t leaf = -1, q = 0;
+    if (Q == 0) {
+      errbits |= RPL_DERR_EMPTY;
+    } else {
+      const uint64_t lo = stratum_lo((uint64_t)k, Q, (uint64_t)n);
+      const uint64_t hi = stratum_lo((uint64_t)k + 1, Q, (uint64_t)n);
+      const uint64_t u = draws ? draws[k] : philox_u64(seed, offset + (uint64_t)k);
+      uint64_t prefix = lo + __umul64hi(u, hi - lo);
+      bool mine = true;
+      if (SHARDED) {
+        mine = prefix >= own_lo && prefix < own_lo + own_T;
+        prefix -= own_lo;
+      }
+      if (mine) {
+        leaf = descend(L, tree, (int64_t)prefix, &q, &errbits);
+        if (SHARDED) leaf += (int64_t)rank * shard_leaves;
+      }
+    }
+    if (lane == 0) {
+      out_idx[k] = leaf;
+      out_q[k] = q;
+    }
+  }
+  if (lane == 0 && errbits) set_err(err, errbits);
+
+  // last CTA: batch-min q and IS weights (§8c #10)
+  __shared__ int s_last;
+  __shared__ int64_t s_min[SAMPLE_WARPS];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned long long* ticket = reinterpret_cast<unsigned long long*>(tree + L.hdr_off + 1);
+    const unsigned long long t = atomicAdd(ticket, 1ull);
+    s_last = (t == (unsigned long long)gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  int64_t m = INT64_MAX;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    const int64_t qj = __ldcg(out_q + j);
+    const int64_t ij = __ldcg(out_idx + j);
+    if (ij >= 0 && qj < m) m = qj;
+  }
+  m = warp_min64(m);
+  if (lane == 0) s_min[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = lane < SAMPLE_WARPS ? s_min[lane] : INT64_MAX;
+    m = warp_min64(m);
+    if (lane == 0) s_min[0] = m;
+  }
+  __syncthreads();
+  const int64_t qmin = s_min[0];
+  if (threadIdx.x == 0) {
+    if (out_qmin) *out_qmin = (!SHARDED && Q == 0) ? 0 : qmin;
+    *reinterpret_cast<unsigned long long*>(tree + L.hdr_off + 1) = 0ull;  // reset ticket
+  }
+  if (out_w) {
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+      const int64_t qj = __ldcg(out_q + j);
+      out_w[j] = qj > 0 ? (float)pow((double)qmin / (double)qj, beta) : 0.0f;
+    }
+  }
+}
+
+__global__ void k_tree_find(TreeDev L, const int64_t* __restrict__ tree, const int64_t* __restrict__ prefix,
+                            int64_t n, int64_t* __restrict__ out_idx, int32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * SAMPLE_WARPS + (threadIdx.x >> 5);
+  if (k >= n) return;
+  int32_t errbits = 0;
+  const int64_t Q = tree[L.level_off[0]];
+  int64_t p = prefix[k];
+  if (p < 0) {
+    p = 0;
+    errbits |= RPL_DERR_TREE;
+  }
+  int64_t q;
+  const int64_t leaf = Q > 0 ? descend(L, tree, p, &q, &errbits) : -1;
+  if (Q == 0) errbits |= RPL_DERR_EMPTY;
+  if (lane == 0) {
+    out_idx[k] = leaf;
+    if (errbits) set_err(err, errbits);
+  }
+}
+
+__global__ void k_tree_total(const int64_t* __restrict__ tree, int64_t* __restrict__ out) {
+  *out = tree[0];
+}
+
+__global__ void k_tree_level(TreeDev L, int64_t* __restrict__ tree, int l, int64_t len) {
+  // node j of level l := sum of its W children on level l+1
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= len) return;
+  const int64_t* ch = tree + L.level_off[l + 1] + (j << L.log2w);
+  int64_t s = 0;
+  for (int c = 0; c < L.fanout; ++c) s += ch[c];
+  tree[L.level_off[l] + j] = s;
+}
+
+__global__ void k_tree_header(int64_t* __restrict__ hdr, int64_t maxseen) {
+  hdr[0] = maxseen;
+  for (int i = 1; i < 8; ++i) hdr[i] = 0;
+}
+
+__global__ void k_is_weights(const int64_t* __restrict__ q, const int64_t* __restrict__ qmin, int64_t n,
+                             double beta, float* __restrict__ w) {
+  const double m = (double)*qmin;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t qj = q[j];
+    w[j] = qj > 0 ? (float)pow(m / (double)qj, beta) : 0.0f;
+  }
+}
+
+__global__ void k_priority_values(const float* __restrict__ td, int64_t n, double alpha, double eps_p,
+                                  int force_slow, float* __restrict__ v, uint8_t* __restrict__ slow_flag) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double p = (double)fabsf(td[j]) + eps_p;
+    bool slow = false;
+    float r;
+    if (!isfinite(p)) r = __int_as_float(0x7f800000);
+    else r = cr_powf(p, alpha, force_slow != 0, &slow);
+    v[j] = r;
+    if (slow_flag) slow_flag[j] = slow ? 1 : 0;
+  }
+}
+
+bool layout_ok(const rpl_tree_layout* L) {
+  return L && L->n_leaves >= 1 && L->fanout >= 2 && L->fanout <= 32 && (L->fanout & (L->fanout - 1)) == 0 &&
+         L->depth >= 1 && L->depth < RPL_MAX_LEVELS && L->frac_bits >= 0 && L->frac_bits <= 62;
+}
+
+int launch_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, const float* td,
+                  const int64_t* q, int mode, int64_t n, double alpha, double eps_p, int32_t* err,
+                  void* stream, int force_slow) {
+  if (!layout_ok(L) || !tree || n < 0) return RPL_EINVAL;
+  if (n == 0) return RPL_OK;
+  if (!idx) return RPL_EINVAL;
+  k_tree_update<<<1, UPD_THREADS, 0, as_stream(stream)>>>(tree_dev(L), tree, idx, td, q, mode, n, alpha,
+                                                           eps_p, err, force_slow);
+  return launch_status();
+}
+
+}  // namespace
+}  // namespace rpl
+
+using namespace rpl;
+
+extern "C" int rpl_sumtree_layout(int64_t n_leaves, int32_t fanout, int32_t frac_bits, rpl_tree_layout* out) {
+  if (!out || n_leaves < 1 || fanout < 2 || fanout > 32 || (fanout & (fanout - 1)) != 0 || frac_bits < 0 ||
+      frac_bits > 62)
+    return RPL_EINVAL;
+  int depth = 1;
+  int64_t capn = fanout;
+  while (capn < n_leaves) {
+    capn *= fanout;
+    ++depth;
+    if (depth + 1 > RPL_MAX_LEVELS) return RPL_EUNSUPPORTED;
+  }
+  rpl_tree_layout L{};
+  L.n_leaves = n_leaves;
+  L.fanout = fanout;
+  L.depth = depth;
+  L.frac_bits = frac_bits;
+  L.q_cap = INT64_MAX / n_leaves;
+  int64_t off = 0;
+  for (int l = 0; l <= depth; ++l) {
+    int64_t span = 1;
+    for (int i = 0; i < depth - l; ++i) span *= fanout;
+    const int64_t nodes = (n_leaves + span - 1) / span;
+    const int64_t len = l == 0 ? 1 : ((nodes + fanout - 1) / fanout) * fanout;
+    L.level_off[l] = off;
+    L.level_len[l] = len;
+    off += len;
+  }
+  L.hdr_off = off;
+  L.n_words = off + 8;
+  *out = L;
+  return RPL_OK;
+}
+
+extern "C" int rpl_sumtree_init(const rpl_tree_layout* L, int64_t* tree, void* stream) {
+  if (!layout_ok(L) || !tree) return RPL_EINVAL;
+  if (cudaMemsetAsync(tree, 0, (size_t)L->n_words * sizeof(int64_t), as_stream(stream)) != cudaSuccess)
+    return RPL_ECUDA;
+  k_tree_header<<<1, 1, 0, as_stream(stream)>>>(tree + L->hdr_off, (int64_t)1 << L->frac_bits);
+  return launch_status();
+}
+
+extern "C" int rpl_sumtree_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx,
+                                  const float* td_abs, int64_t n, double alpha, double eps_p,
+                                  int32_t* dev_err, void* stream) {
+  if (n > 0 && !td_abs) return RPL_EINVAL;
+  if (!(alpha >= 0.0) || !(eps_p >= 0.0)) return RPL_EINVAL;
+  return launch_update(L, tree, idx, td_abs, nullptr, MODE_TD, n, alpha, eps_p, dev_err, stream, 0);
+}
+
+extern "C" int rpl_sumtree_set_q(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, const int64_t* q,
+                                 int64_t n, int32_t* dev_err, void* stream) {
+  return launch_update(L, tree, idx, nullptr, q, q ? MODE_Q : MODE_MAXSEEN, n, 0.0, 0.0, dev_err, stream, 0);
+}
+
+extern "C" int rpl_sumtree_sample(const rpl_tree_layout* L, int64_t* tree, int64_t n, const uint64_t* draws,
+                                  uint64_t seed, uint64_t offset, double beta, int64_t* out_idx, int64_t* out_q,
+                                  int64_t* out_qmin, float* out_w, int32_t* dev_err, void* stream) {
+  if (!layout_ok(L) || !tree || !out_idx || !out_q || n < 1 || n > (1ll << 30)) return RPL_EINVAL;
+  if (out_w && !(beta >= 0.0)) return RPL_EINVAL;
+  const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
+  k_tree_sample<false><<<(unsigned)blocks, SAMPLE_WARPS * 32, 0, as_stream(stream)>>>(
+      tree_dev(L), tree, n, draws, seed, offset, beta, out_idx, out_q, out_qmin, out_w, dev_err, 0, 1, 0,
+      nullptr);
+  return launch_status();
+}
+
+extern "C" int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t rank, int32_t n_shards,
+                                          int64_t shard_leaves, const int64_t* shard_totals, int64_t n,
+                                          const uint64_t* draws, uint64_t seed, uint64_t offset, int64_t* out_idx,
+                                          int64_t* out_q, int64_t* out_qmin, int32_t* dev_err, void* stream) {
+  if (!layout_ok(L) || !tree || !out_idx || !out_q || !shard_totals || n < 1 || n > (1ll << 30)) return RPL_EINVAL;
+  if (n_shards < 1 || rank < 0 || rank >= n_shards || shard_leaves < L->n_leaves) return RPL_EINVAL;
+  const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
+  k_tree_sample<true><<<(unsigned)blocks, SAMPLE_WARPS * 32, 0, as_stream(stream)>>>(
+      tree_dev(L), tree, n, draws, seed, offset, 0.0, out_idx, out_q, out_qmin, nullptr, dev_err, rank, n_shards,
+      shard_leaves, shard_totals);
+  return launch_status();
+}
+
+extern "C" int rpl_sumtree_find(const rpl_tree_layout* L, const int64_t* tree, const int64_t* prefix, int64_t n,
+                                int64_t* out_idx, int32_t* dev_err, void* stream) {
+  if (!layout_ok(L) || !tree || !prefix || !out_idx || n < 0) return RPL_EINVAL;
+  if (n == 0) return RPL_OK;
+  const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
+  k_tree_find<<<(unsigned)blocks, SAMPLE_WARPS * 32, 0, as_stream(stream)>>>(tree_dev(L), tree, prefix, n,
+                                                                              out_idx, dev_err);
+  return launch_status();
+}
+
+extern "C" int rpl_sumtree_total(const rpl_tree_layout* L, const int64_t* tree, int64_t* out_total, void* stream) {
+  if (!layout_ok(L) || !tree || !out_total) return RPL_EINVAL;
+  k_tree_total<<<1, 1, 0, as_stream(stream)>>>(tree, out_total);
+  return launch_status();
+}
+
+extern "C" int rpl_sumtree_rebuild(const rpl_tree_layout* L, int64_t* tree, void* stream) {
+  if (!layout_ok(L) || !tree) return RPL_EINVAL;
+  TreeDev T = tree_dev(L);
+  for (int l = L->depth - 1; l >= 0; --l) {
+    const int64_t len = L->level_len[l];
+    k_tree_level<<<(unsigned)((len + 255) / 256), 256, 0, as_stream(stream)>>>(T, tree, l, len);
+    int s = launch_status();
+    if (s != RPL_OK) return s;
+  }
+  return RPL_OK;
+}
+
+extern "C" int rpl_is_weights(const int64_t* q, const int64_t* qmin, int64_t n, double beta, float* w,
+                              void* stream) {
+  if (!q || !qmin || !w || n < 0 || !(beta >= 0.0)) return RPL_EINVAL;
+  if (n == 0) return RPL_OK;
+  const int threads = 256;
+  const int64_t blocks = (n + threads - 1) / threads;
+  k_is_weights<<<(unsigned)(blocks > 1024 ? 1024 : blocks), threads, 0, as_stream(stream)>>>(q, qmin, n, beta, w);
+  return launch_status();
+}
+
+extern "C" int rpl_debug_priority_values(const float* td_abs, int64_t n, double alpha, double eps_p,
+                                         int32_t force_slow, float* out_v, uint8_t* out_slow, void* stream) {
+  if (!td_abs || !out_v || n < 0 || !(alpha >= 0.0) || !(eps_p >= 0.0)) return RPL_EINVAL;
+  if (n == 0) return RPL_OK;
+  const int threads = 256;
+  const int64_t blocks = (n + threads - 1) / threads;
+  k_priority_values<<<(unsigned)(blocks > 4096 ? 4096 : blocks), threads, 0, as_stream(stream)>>>(
+      td_abs, n, alpha, eps_p, force_slow, out_v, out_slow);
+  return launch_status();
+}

@@ -1,0 +1,342 @@
+"""Torch-tensor binding over the librpl C ABI (include/rpl.h).
+
+Argument marshalling only: shape/dtype/device checks, output allocation and the
+current CUDA stream.  Every step of the hot path runs inside librpl's kernels.
+Function names follow the ABI (rpl_<name> -> <name>).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import GatherDesc, TreeLayout, check, lib
+
+__all__ = [
+    "returns_discounted", "returns_nstep", "gae", "value_rescale", "SumTree", "is_weights", "gather",
+    "GatherRing", "check_err", "launch_count", "debug_priority_values",
+]
+
+
+def _stream(device=None):
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _req(t, dtype, name, shape=None):
+    if t is None:
+        raise ValueError(f"{name} is required")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path)")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    return t
+
+
+def launch_count() -> int:
+    return int(lib.rpl_launch_count())
+
+
+def check_err(dev_err: torch.Tensor, allowed: int = 0):
+    """Raise if any RPL_DERR_* bit outside `allowed` is set (the only host sync)."""
+    v = int(dev_err.item())
+    bad = v & ~allowed
+    if bad:
+        names = [n for b, n in _lib.DERR.items() if bad & b]
+        raise _lib.RplError("device error bits: " + ", ".join(names))
+    return v
+
+
+# ---------------------------------------------------------------- returns
+def returns_discounted(r, d, bootstrap, gamma, out=None):
+    T, B = r.shape
+    _req(r, torch.float32, "r")
+    _req(d, torch.uint8, "d", (T, B))
+    if bootstrap is not None:
+        _req(bootstrap, torch.float32, "bootstrap", (B,))
+    out = torch.empty_like(r) if out is None else _req(out, torch.float32, "out", (T, B))
+    check(lib.rpl_returns_discounted(_ptr(r), _ptr(d), _ptr(bootstrap), T, B, float(gamma), _ptr(out),
+                                     _stream(r.device)), "rpl_returns_discounted")
+    return out
+
+
+def returns_nstep(r, d, n, gamma, q=None, q_boot=None, rescale=False, eps=1e-3, out=None, done_out=None):
+    T, B = r.shape
+    _req(r, torch.float32, "r")
+    _req(d, torch.uint8, "d", (T, B))
+    if q is not None:
+        _req(q, torch.float32, "q", (T, B))
+        _req(q_boot, torch.float32, "q_boot", (B,))
+    rows = T - int(n) + 1
+    if out is None:
+        out = torch.empty((max(rows, 0), B), dtype=torch.float32, device=r.device)
+    if done_out is None:
+        done_out = torch.empty((max(rows, 0), B), dtype=torch.uint8, device=r.device)
+    check(lib.rpl_returns_nstep(_ptr(r), _ptr(d), T, B, int(n), float(gamma), _ptr(q), _ptr(q_boot),
+                                1 if rescale else 0, float(eps), _ptr(out), _ptr(done_out), _stream(r.device)),
+          "rpl_returns_nstep")
+    return out, done_out
+
+
+def gae(r, v, d, bootstrap_v, gamma, lam, adv=None, ret=None):
+    T, B = r.shape
+    _req(r, torch.float32, "r")
+    _req(v, torch.float32, "v", (T, B))
+    _req(d, torch.uint8, "d", (T, B))
+    _req(bootstrap_v, torch.float32, "bootstrap_v", (B,))
+    adv = torch.empty_like(r) if adv is None else adv
+    ret = torch.empty_like(r) if ret is None else ret
+    check(lib.rpl_gae(_ptr(r), _ptr(v), _ptr(d), _ptr(bootstrap_v), T, B, float(gamma), float(lam), _ptr(adv),
+                      _ptr(ret), _stream(r.device)), "rpl_gae")
+    return adv, ret
+
+
+def value_rescale(x, eps=1e-3, inverse=False, out=None):
+    _req(x, torch.float32, "x")
+    out = torch.empty_like(x) if out is None else out
+    check(lib.rpl_value_rescale(_ptr(x), _ptr(out), x.numel(), float(eps), 1 if inverse else 0,
+                                _stream(x.device)), "rpl_value_rescale")
+    return out
+
+
+def debug_priority_values(td_abs, alpha, eps_p=1e-3, force_slow=False):
+    _req(td_abs, torch.float32, "td_abs")
+    v = torch.empty_like(td_abs)
+    slow = torch.empty(td_abs.shape, dtype=torch.uint8, device=td_abs.device)
+    check(lib.rpl_debug_priority_values(_ptr(td_abs), td_abs.numel(), float(alpha), float(eps_p),
+                                        1 if force_slow else 0, _ptr(v), _ptr(slow), _stream(td_abs.device)),
+          "rpl_debug_priority_values")
+    return v, slow
+
+
+def is_weights(q, qmin, beta, out=None):
+    _req(q, torch.int64, "q")
+    _req(qmin, torch.int64, "qmin")
+    out = torch.empty(q.shape, dtype=torch.float32, device=q.device) if out is None else out
+    check(lib.rpl_is_weights(_ptr(q), _ptr(qmin), q.numel(), float(beta), _ptr(out), _stream(q.device)),
+          "rpl_is_weights")
+    return out
+
+
+# ---------------------------------------------------------------- sum tree
+class SumTree:
+    """One int64 device array holding the whole tree (rpl.h layout)."""
+
+    def __init__(self, n_leaves: int, fanout: int = 32, frac_bits: int = 32, device="cuda"):
+        self.layout = TreeLayout()
+        check(lib.rpl_sumtree_layout(int(n_leaves), int(fanout), int(frac_bits), C.byref(self.layout)),
+              "rpl_sumtree_layout")
+        L = self.layout
+        self.n_leaves = int(n_leaves)
+        self.fanout = int(fanout)
+        self.frac_bits = int(frac_bits)
+        self.depth = int(L.depth)
+        self.q_cap = int(L.q_cap)
+        self.device = torch.device(device)
+        self.storage = torch.empty(int(L.n_words), dtype=torch.int64, device=self.device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._lp = C.byref(self.layout)
+        self.init()
+
+    # views
+    def level(self, l: int) -> torch.Tensor:
+        off, ln = int(self.layout.level_off[l]), int(self.layout.level_len[l])
+        return self.storage[off:off + ln]
+
+    @property
+    def leaves(self) -> torch.Tensor:
+        off = int(self.layout.level_off[self.depth])
+        return self.storage[off:off + self.n_leaves]
+
+    @property
+    def header(self) -> torch.Tensor:
+        off = int(self.layout.hdr_off)
+        return self.storage[off:off + 8]
+
+    def _s(self):
+        return _stream(self.device)
+
+    def init(self):
+        check(lib.rpl_sumtree_init(self._lp, _ptr(self.storage), self._s()), "rpl_sumtree_init")
+
+    def update(self, idx, td_abs, alpha, eps_p=1e-3, err=None):
+        _req(idx, torch.int64, "idx")
+        _req(td_abs, torch.float32, "td_abs", idx.shape)
+        e = self.err if err is None else err
+        check(lib.rpl_sumtree_update(self._lp, _ptr(self.storage), _ptr(idx), _ptr(td_abs), idx.numel(),
+                                     float(alpha), float(eps_p), _ptr(e), self._s()), "rpl_sumtree_update")
+
+    def set_q(self, idx, q=None, err=None):
+        _req(idx, torch.int64, "idx")
+        if q is not None:
+            _req(q, torch.int64, "q", idx.shape)
+        e = self.err if err is None else err
+        check(lib.rpl_sumtree_set_q(self._lp, _ptr(self.storage), _ptr(idx), _ptr(q), idx.numel(), _ptr(e),
+                                    self._s()), "rpl_sumtree_set_q")
+
+    def sample(self, n, draws=None, seed=0, offset=0, beta=None, out=None, err=None):
+        """Returns (idx, q, qmin[1], w or None)."""
+        n = int(n)
+        if out is None:
+            idx = torch.empty(n, dtype=torch.int64, device=self.device)
+            q = torch.empty(n, dtype=torch.int64, device=self.device)
+            qmin = torch.empty(1, dtype=torch.int64, device=self.device)
+            w = torch.empty(n, dtype=torch.float32, device=self.device) if beta is not None else None
+        else:
+            idx, q, qmin, w = out
+        if draws is not None:  # uint64 draws carried as their int64 bit patterns
+            _req(draws, torch.int64, "draws", (n,))
+        e = self.err if err is None else err
+        check(lib.rpl_sumtree_sample(self._lp, _ptr(self.storage), n, _ptr(draws), int(seed) & (2 ** 64 - 1),
+                                     int(offset) & (2 ** 64 - 1), float(beta or 0.0), _ptr(idx), _ptr(q),
+                                     _ptr(qmin), _ptr(w), _ptr(e), self._s()), "rpl_sumtree_sample")
+        return idx, q, qmin, w
+
+    def sample_sharded(self, rank, n_shards, shard_totals, n, draws=None, seed=0, offset=0, out=None, err=None):
+        n = int(n)
+        _req(shard_totals, torch.int64, "shard_totals", (n_shards,))
+        if out is None:
+            idx = torch.empty(n, dtype=torch.int64, device=self.device)
+            q = torch.empty(n, dtype=torch.int64, device=self.device)
+            qmin = torch.empty(1, dtype=torch.int64, device=self.device)
+        else:
+            idx, q, qmin = out
+        e = self.err if err is None else err
+        check(lib.rpl_sumtree_sample_sharded(self._lp, _ptr(self.storage), int(rank), int(n_shards),
+                                             self.n_leaves, _ptr(shard_totals), n, _ptr(draws),
+                                             int(seed) & (2 ** 64 - 1), int(offset) & (2 ** 64 - 1), _ptr(idx),
+                                             _ptr(q), _ptr(qmin), _ptr(e), self._s()),
+              "rpl_sumtree_sample_sharded")
+        return idx, q, qmin
+
+    def find(self, prefix, err=None):
+        _req(prefix, torch.int64, "prefix")
+        out = torch.empty_like(prefix)
+        e = self.err if err is None else err
+        check(lib.rpl_sumtree_find(self._lp, _ptr(self.storage), _ptr(prefix), prefix.numel(), _ptr(out), _ptr(e),
+                                   self._s()), "rpl_sumtree_find")
+        return out
+
+    def total(self, out=None):
+        out = torch.empty(1, dtype=torch.int64, device=self.device) if out is None else out
+        check(lib.rpl_sumtree_total(self._lp, _ptr(self.storage), _ptr(out), self._s()), "rpl_sumtree_total")
+        return out
+
+    def rebuild(self):
+        check(lib.rpl_sumtree_rebuild(self._lp, _ptr(self.storage), self._s()), "rpl_sumtree_rebuild")
+
+
+# ---------------------------------------------------------------- gather
+@dataclass
+class GatherRing:
+    """Device replay ring (time-major [cap_T, B, ...]) for rpl_gather."""
+    obs: torch.Tensor            # [cap_T, B, *item] (u8 frames or f32 vectors)
+    act: torch.Tensor            # [cap_T, B] int64 or [cap_T, B, A] f32
+    rew: torch.Tensor            # [cap_T, B] f32
+    done: torch.Tensor           # [cap_T, B] u8
+    cursor: int
+    size: int
+    rnn: torch.Tensor | None = None  # [cap_T/period, B, parts, H] f32
+
+    @property
+    def cap_T(self):
+        return int(self.obs.shape[0])
+
+    @property
+    def B(self):
+        return int(self.obs.shape[1])
+
+    @property
+    def item_shape(self):
+        return tuple(self.obs.shape[2:])
+
+    @property
+    def obs_bytes(self):
+        return int(self.obs[0, 0].numel() * self.obs.element_size())
+
+    @property
+    def act_shape(self):
+        return tuple(self.act.shape[2:])
+
+    @property
+    def act_bytes(self):
+        return int(self.act[0, 0].numel() * self.act.element_size())
+
+
+def _desc(ring: GatherRing, kind, k, pad_mode, out_mode, n_step, seq_len, period, gamma):
+    for name in ("obs", "act", "rew", "done"):
+        t = getattr(ring, name)
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"ring.{name} must be a contiguous CUDA tensor")
+    g = GatherDesc()
+    g.kind, g.pad_mode, g.out_mode, g.k = kind, pad_mode, out_mode, k
+    g.cap_T, g.B, g.cursor, g.size = ring.cap_T, ring.B, int(ring.cursor), int(ring.size)
+    g.obs_bytes, g.act_bytes = ring.obs_bytes, ring.act_bytes
+    g.n_step, g.seq_len, g.period = n_step, seq_len, period
+    g.gamma = float(gamma)
+    g.obs, g.act, g.rew, g.done = ring.obs.data_ptr(), ring.act.data_ptr(), ring.rew.data_ptr(), ring.done.data_ptr()
+    if ring.rnn is not None:
+        g.rnn = ring.rnn.data_ptr()
+        g.rnn_parts = int(ring.rnn.shape[2])
+        g.rnn_bytes = int(ring.rnn[0, 0, 0].numel() * ring.rnn.element_size())
+    return g
+
+
+def gather(ring: GatherRing, idx, kind="transition", k=4, n_step=1, gamma=0.99, seq_len=1, period=1,
+           pad_mode=_lib.PAD_REPEAT, out_mode=_lib.OUT_STACKED, q=None, qmin=None, beta=0.0, outputs=None,
+           err=None, want=None):
+    """rpl_gather.  Returns a dict of output tensors (allocated unless given in `outputs`)."""
+    _req(idx, torch.int64, "idx")
+    n = idx.numel()
+    dev = ring.obs.device
+    kind_i = _lib.GATHER_TRANSITION if kind == "transition" else _lib.GATHER_SEQUENCE
+    g = _desc(ring, kind_i, k, pad_mode, out_mode, n_step if kind_i == 0 else 1, seq_len, period, gamma)
+    o = {} if outputs is None else dict(outputs)
+    item = ring.item_shape
+    od = ring.obs.dtype
+    wants = set(want) if want is not None else None
+
+    def alloc(name, shape, dtype):
+        if name not in o and (wants is None or name in wants):
+            o[name] = torch.empty(shape, dtype=dtype, device=dev)
+
+    if kind_i == _lib.GATHER_TRANSITION:
+        alloc("obs", (n, k) + item, od)
+        alloc("next_obs", (n, k) + item, od)
+        alloc("act", (n,) + ring.act_shape, ring.act.dtype)
+        alloc("ret", (n,), torch.float32)
+        alloc("done_n", (n,), torch.uint8)
+    else:
+        L = seq_len
+        if out_mode == _lib.OUT_STACKED:
+            alloc("obs", (L, n, k) + item, od)
+        else:
+            alloc("obs", (L + k - 1, n) + item, od)
+        alloc("act", (L, n) + ring.act_shape, ring.act.dtype)
+        alloc("prev_act", (L, n) + ring.act_shape, ring.act.dtype)
+        alloc("rew", (L, n), torch.float32)
+        alloc("prev_rew", (L, n), torch.float32)
+        alloc("done", (L, n), torch.uint8)
+        if ring.rnn is not None:
+            alloc("rnn", (int(ring.rnn.shape[2]), n, int(ring.rnn.shape[3])), ring.rnn.dtype)
+    if q is not None and qmin is not None:
+        alloc("w", (n,), torch.float32)
+    fields = {"obs": "o_obs", "next_obs": "o_next_obs", "act": "o_act", "prev_act": "o_prev_act", "rew": "o_rew",
+              "prev_rew": "o_prev_rew", "done": "o_done", "ret": "o_ret", "done_n": "o_done_n", "w": "o_w",
+              "rnn": "o_rnn"}
+    for name, f in fields.items():
+        if name in o and o[name] is not None:
+            setattr(g, f, o[name].data_ptr())
+    e = err
+    check(lib.rpl_gather(C.byref(g), _ptr(idx), _ptr(q), _ptr(qmin), float(beta), n, _ptr(e), _stream(dev)),
+          "rpl_gather")
+    return o

@@ -1,0 +1,76 @@
+"""CPU checks of the boundary: librpl.so loads (no GPU needed), exports every
+symbol include/rpl.h declares, and the ctypes structs match the C layout."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "rpl.h")
+PKG = os.path.join(ROOT, "paper_1909_01500_b200")
+
+
+def declared():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rpl_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1909_01500_b200 import build
+    build.build()
+    return ctypes.CDLL(build.LIB)
+
+
+def test_exports_every_declared_symbol(lib):
+    names = declared()
+    assert len(names) >= 19
+    for n in names:
+        assert hasattr(lib, n), n
+    from paper_1909_01500_b200 import _lib
+    assert sorted(_lib.EXPORTS) == names
+
+
+def test_version_and_strerror(lib):
+    lib.rpl_abi_version.restype = ctypes.c_int
+    assert lib.rpl_abi_version() == 1
+    lib.rpl_strerror.restype = ctypes.c_char_p
+    assert b"invalid" in lib.rpl_strerror(-1)
+
+
+def test_struct_layouts_match_c(tmp_path):
+    from paper_1909_01500_b200._lib import GatherDesc, TreeLayout
+    prog = tmp_path / "sz.c"
+    prog.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "rpl.h"\n'
+        "int main(){printf(\"%zu %zu %zu %zu %zu %zu\\n\", sizeof(rpl_tree_layout), offsetof(rpl_tree_layout, q_cap),"
+        " offsetof(rpl_tree_layout, n_words), sizeof(rpl_gather_desc), offsetof(rpl_gather_desc, gamma),"
+        " offsetof(rpl_gather_desc, o_rnn));return 0;}\n")
+    exe = tmp_path / "sz"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(prog), "-o", str(exe)])
+    vals = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    assert vals == [ctypes.sizeof(TreeLayout), TreeLayout.q_cap.offset, TreeLayout.n_words.offset,
+                    ctypes.sizeof(GatherDesc), GatherDesc.gamma.offset, GatherDesc.o_rnn.offset]
+
+
+def test_host_validation_without_gpu(lib):
+    # argument errors are detected on the host before anything is enqueued
+    from paper_1909_01500_b200._lib import TreeLayout, lib as L
+    lay = TreeLayout()
+    assert L.rpl_sumtree_layout(0, 32, 32, ctypes.byref(lay)) == -1
+    assert L.rpl_sumtree_layout(100, 3, 32, ctypes.byref(lay)) == -1
+    assert L.rpl_sumtree_layout(1 << 20, 32, 32, ctypes.byref(lay)) == 0
+    assert lay.depth == 4 and lay.q_cap == ((1 << 63) - 1) // (1 << 20)
+    assert [lay.level_len[i] for i in range(5)] == [1, 32, 1024, 32768, 1 << 20]
+    assert L.rpl_returns_nstep(None, None, 4, 4, 1, 0.9, None, None, 0, 0.0, None, None, None) == -1
+
+
+def test_product_never_imports_oracle():
+    for dirpath, _, files in os.walk(PKG):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+oracle", txt, re.M), f

@@ -1,0 +1,156 @@
+"""GPU parity: rpl_gather (transition and sequence gathers) vs the naive
+full-stack oracle — bytes bit-exact, n-step returns within 1e-5 relative."""
+import numpy as np
+import pytest
+
+from oracle import gather as OG
+from oracle import returns as OR
+from oracle import sumtree as OS
+from synth import make_ring, rng
+from tests._tol import check_rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rpl(cuda):
+    import paper_1909_01500_b200 as rpl
+    return rpl
+
+
+def T_(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def H(t):
+    return t.cpu().numpy()
+
+
+def dev_ring(rpl, ring):
+    return rpl.GatherRing(obs=T_(ring.obs), act=T_(ring.act), rew=T_(ring.rew), done=T_(ring.done),
+                          cursor=ring.cursor, size=ring.size, rnn=None if ring.rnn is None else T_(ring.rnn))
+
+
+def valid_transition_leaves(ring, k, n, count, g):
+    cap, B = ring.obs.shape[:2]
+    out = []
+    while len(out) < count:
+        row, b = int(g.integers(0, cap)), int(g.integers(0, B))
+        if OG.window_valid_transition(row, cap, ring.cursor, ring.size, k, n):
+            out.append(row * B + b)
+    return np.array(out, np.int64)
+
+
+@pytest.mark.parametrize("pad_mode", [0, 1])
+@pytest.mark.parametrize("n_step", [1, 3, 5])
+def test_transition_frames(rpl, pad_mode, n_step):
+    import torch
+    ring = make_ring(5 + n_step, cap=64, B=8, ep_len=6.0, reward_kind="heavy")
+    dr = dev_ring(rpl, ring)
+    g = rng(7)
+    idx = valid_transition_leaves(ring, 4, n_step, 300, g)
+    # also include ring-wrapping windows and a skipped entry
+    idx[0] = (ring.cursor + 3) % 64 * 8 + 1
+    idx[1] = -1
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = rpl.gather(dr, T_(idx), kind="transition", k=4, n_step=n_step, gamma=0.99, pad_mode=pad_mode, err=err)
+    ref = OG.gather_transitions(idx, 8, ring.obs, ring.act, ring.rew, ring.done, 4, n_step, 0.99, pad_mode)
+    ok = idx >= 0
+    assert np.array_equal(H(out["obs"])[ok], ref["obs"][ok])
+    assert np.array_equal(H(out["next_obs"])[ok], ref["next_obs"][ok])
+    assert np.array_equal(H(out["act"])[ok], ref["act"][ok])
+    assert np.array_equal(H(out["done_n"])[ok], ref["done_n"][ok])
+    absR = OG.gather_transitions(idx, 8, ring.obs, ring.act, np.abs(ring.rew), ring.done, 4, n_step, 0.99)["ret"]
+    check_rel(H(out["ret"])[ok], ref["ret"][ok], absR[ok], what="fused n-step")
+
+
+def test_transition_invalid_window_flag(rpl):
+    import torch
+    ring = make_ring(3, cap=32, B=2, ep_len=100.0)
+    dr = dev_ring(rpl, ring)
+    bad_row = (ring.cursor - 1) % 32  # newest row: its n-step lookahead is not stored
+    idx = np.array([bad_row * 2], np.int64)
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    rpl.gather(dr, T_(idx), kind="transition", k=4, n_step=3, err=err)
+    assert int(H(err)[0]) & 8
+
+
+def test_transition_vector_obs(rpl):
+    # Mujoco: obs f32 D=17 (68 B, LSU path) and D=376, actions f32 [A]
+    for D, A in [(17, 6), (376, 17)]:
+        ring = make_ring(11 + D, cap=128, B=16, obs_shape=(D,), obs_dtype=np.float32, act_dim=A, ep_len=50.0,
+                         reward_kind="mujoco")
+        dr = dev_ring(rpl, ring)
+        idx = valid_transition_leaves(ring, 1, 3, 256, rng(D))
+        out = rpl.gather(dr, T_(idx), kind="transition", k=1, n_step=3, gamma=0.99)
+        ref = OG.gather_transitions(idx, 16, ring.obs, ring.act, ring.rew, ring.done, 1, 3, 0.99)
+        assert np.array_equal(H(out["obs"]), ref["obs"])
+        assert np.array_equal(H(out["next_obs"]), ref["next_obs"])
+        assert np.array_equal(H(out["act"]), ref["act"])
+        check_rel(H(out["ret"]), ref["ret"], np.abs(ref["ret"]) + 10.0, what="mujoco ret")
+
+
+def test_transition_fused_is_weights(rpl):
+    import torch
+    ring = make_ring(21, cap=64, B=4, ep_len=20.0)
+    dr = dev_ring(rpl, ring)
+    idx = valid_transition_leaves(ring, 4, 3, 64, rng(1))
+    g = rng(2)
+    q = g.integers(1, 1 << 40, 64).astype(np.int64)
+    qmin = np.array([q.min()], np.int64)
+    out = rpl.gather(dr, T_(idx), kind="transition", k=4, n_step=3, q=T_(q), qmin=T_(qmin), beta=0.4)
+    ref = OS.is_weights([int(x) for x in q], int(q.sum()), 256, 0.4)
+    check_rel(H(out["w"]), ref, what="fused w")
+
+
+@pytest.mark.parametrize("out_mode", [0, 1])
+@pytest.mark.parametrize("pad_mode", [0, 1])
+def test_sequences(rpl, out_mode, pad_mode):
+    import torch
+    period, L, k = 40, 125, 4
+    ring = make_ring(31 + out_mode, cap=400, B=4, ep_len=30.0, period=period, rnn_h=64, reward_kind="r2d2")
+    dr = dev_ring(rpl, ring)
+    g = rng(3)
+    nblk = 400 // period
+    idx = []
+    while len(idx) < 24:
+        blk, b = int(g.integers(0, nblk)), int(g.integers(0, 4))
+        if OG.window_valid_sequence(blk * period, 400, ring.cursor, ring.size, k, L):
+            idx.append(blk * 4 + b)
+    idx = np.array(idx, np.int64)
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = rpl.gather(dr, T_(idx), kind="sequence", k=k, seq_len=L, period=period, pad_mode=pad_mode,
+                     out_mode=out_mode, err=err)
+    ref = OG.gather_sequences(idx, 4, ring.obs, ring.act, ring.rew, ring.done, ring.rnn, k, L, period, pad_mode,
+                              stacked=(out_mode == 0))
+    for name in ("obs", "act", "prev_act", "rew", "prev_rew", "done", "rnn"):
+        assert np.array_equal(H(out[name]), ref[name]), name
+    assert int(H(err)[0]) == 0
+
+
+def test_sequence_then_nstep_target(rpl):
+    # R2D2 step tail: gathered rows 40..123 of L=125 -> rescaled 5-step targets for the 80 train rows
+    import torch
+    period, L, k = 40, 125, 4
+    ring = make_ring(41, cap=400, B=8, ep_len=200.0, period=period, rnn_h=32, reward_kind="r2d2")
+    dr = dev_ring(rpl, ring)
+    idx = []
+    g = rng(4)
+    while len(idx) < 16:
+        blk, b = int(g.integers(0, 10)), int(g.integers(0, 8))
+        if OG.window_valid_sequence(blk * period, 400, ring.cursor, ring.size, k, L):
+            idx.append(blk * 8 + b)
+    idx = np.array(idx, np.int64)
+    out = rpl.gather(dr, T_(idx), kind="sequence", k=k, seq_len=L, period=period, want=["rew", "done"])
+    qv = g.normal(0, 10, (L, 16)).astype(np.float32)
+    r_tr = out["rew"][40:124].contiguous()
+    d_tr = out["done"][40:124].contiguous()
+    q_tr = T_(qv[40:124])
+    y, dn = rpl.returns_nstep(r_tr, d_tr, 5, 0.997, q=q_tr, q_boot=T_(qv[124]), rescale=True)
+    ref_seq = OG.gather_sequences(idx, 8, ring.obs, ring.act, ring.rew, ring.done, ring.rnn, k, L, period)
+    yr, dnr = OR.nstep_return(ref_seq["rew"][40:124], ref_seq["done"][40:124], 5, 0.997, q=qv[40:124],
+                              q_boot=qv[124], rescale=True)
+    assert y.shape == (80, 16)
+    check_rel(H(y), yr, np.abs(yr) + 1e-3, what="r2d2 targets")
+    assert np.array_equal(H(dn), dnr)
