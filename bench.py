@@ -1,0 +1,550 @@
+#!/usr/bin/env python
+"""bench.py — B200 replay + return-estimation hot path of rlpyt (arXiv 1909.01500).
+
+Metric (BASELINE.json): "prioritized samples/sec (update+sample+gather) and return
+elems/sec, 1/2/4/8 B200".  One STEP = one learner update's replay work on the
+R2D2 config (BASELINE.json configs[4]):
+
+    rpl_sumtree_update   64 sequence priorities of the previous batch  (a5-a7)
+    rpl_sumtree_sample   64 stratified draws + IS weights               (a8-a9)
+    rpl_gather           64 sequences x 125 rows, frame stacks, prev fields,
+                         stored LSTM state                              (a11)
+    rpl_returns_nstep    rescaled 5-step targets for the 80 train rows  (a2, a4)
+
+`value` = sequences/s over all ranks (weak scaling: 64 sequences per rank per
+step, Mode L of SURVEY.md §8e).  A secondary line-item times GAE + discounted
+returns on the PPO config [128, 4096] (configs[1]; a1, a3) in elements/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl rpl|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (N > 1, NCCL)
+
+--impl reference times the CPU oracle (oracle/) on the same workload: the
+reference arm of this tier (no upstream code exists).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+FRAME = 84 * 84
+
+# R2D2: 1M-step ring [4000, 256] (configs[4]), sharded by env columns in Mode L.
+R2D2 = dict(cap_T=4000, B=256, period=40, burn_in=40, train=80, tail=5, k=4, n_step=5, gamma=0.997,
+            alpha=0.9, beta=0.6, batch=64, rnn_h=512, rnn_parts=2, eps=1e-3, eps_p=1e-3, fanout=32)
+R2D2["L"] = R2D2["burn_in"] + R2D2["train"] + R2D2["tail"]
+PPO = dict(T=128, B=4096, gamma=0.99, lam=0.95)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--impl", default="rpl", choices=["rpl", "reference"])
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget (cpu_baseline)")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/baseline/e2e)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def seq_bytes_per_sample(c, act_bytes=8):
+    """Algorithmic HBM bytes one sequence of rpl_gather moves:
+    reads the L+k-1 unique frames, the per-row scalars and the stored state;
+    writes L k-stacks and the per-row fields."""
+    L, k = c["L"], c["k"]
+    rd = (L + k - 1) * FRAME                      # unique frames
+    rd += (L + 1) * (act_bytes + 4 + 1)           # act, rew, done of rows row0-1 .. row0+L-1
+    rd += c["rnn_parts"] * c["rnn_h"] * 4         # stored (h, c)
+    wr = L * k * FRAME                            # stacked observations
+    wr += L * (2 * act_bytes + 4 + 4 + 1)         # act, prev_act, rew, prev_rew, done
+    wr += c["rnn_parts"] * c["rnn_h"] * 4
+    return rd + wr
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_rpl(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if args.gpus > 1 and world == 1:
+        raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_1909_01500_b200 as rpl
+    from paper_1909_01500_b200 import replay as R
+    from synth import make_ring, rng
+
+    c = dict(R2D2)
+    b0, b1 = R.shard_columns(c["B"], world, rank)
+    Bl = b1 - b0
+    n = c["batch"]
+    L, k, period = c["L"], c["k"], c["period"]
+
+    # ---- inputs (seeded synthetic, resident in HBM before timing) ----
+    t_setup = time.time()
+    if world == 1:
+        host = make_ring(2019, c["cap_T"], Bl, ep_len=2000.0, reward_kind="r2d2", period=period,
+                         rnn_parts=c["rnn_parts"], rnn_h=c["rnn_h"], cursor=1234 % c["cap_T"])
+        ring = rpl.GatherRing(obs=torch.from_numpy(host.obs).to(dev), act=torch.from_numpy(host.act).to(dev),
+                              rew=torch.from_numpy(host.rew).to(dev), done=torch.from_numpy(host.done).to(dev),
+                              cursor=host.cursor, size=host.size, rnn=torch.from_numpy(host.rnn).to(dev))
+    else:
+        from synth.device import make_ring_device
+        host = None
+        ring = make_ring_device(2019 + 7919 * rank, c["cap_T"], Bl, dev, ep_len=2000.0, period=period,
+                                rnn_parts=c["rnn_parts"], rnn_h=c["rnn_h"], cursor=1234 % c["cap_T"])
+    n_leaves = (c["cap_T"] // period) * Bl
+    tree = rpl.SumTree(n_leaves, c["fanout"], 32, device=dev)
+    blocks = R.valid_sequence_blocks(c["cap_T"], period, ring.cursor, ring.size, k, L)
+    valid = torch.from_numpy(R.leaves_of(blocks, Bl)).to(dev)
+    g = rng(77 + rank)
+    td0 = np.abs(g.normal(size=valid.numel())).astype(np.float32)
+    tree.update(valid, torch.from_numpy(td0).to(dev), c["alpha"], c["eps_p"])
+    P = 8  # distinct per-step |delta| and target-Q inputs (cycled)
+    td_pool = torch.from_numpy(np.abs(g.normal(size=(P, n * max(1, world)))).astype(np.float32)).to(dev)
+    n_glob = n * world
+    q_pool = torch.from_numpy(g.normal(0, 10, (P, L, n_glob)).astype(np.float32)).to(dev)
+    seed = 0x5EED
+
+    plan = rpl.GatherPlan(ring, n_glob, kind="sequence", k=k, seq_len=L, period=period, with_weights=False)
+    out = plan.outputs
+    idx_buf = [torch.full((n_glob,), -1, dtype=torch.int64, device=dev) for _ in range(2)]
+    q_buf = torch.zeros(n_glob, dtype=torch.int64, device=dev)
+    qmin = torch.zeros(1, dtype=torch.int64, device=dev)
+    w = torch.zeros(n_glob, dtype=torch.float32, device=dev)
+    y = torch.empty((c["train"], n_glob), dtype=torch.float32, device=dev)
+    dn = torch.empty((c["train"], n_glob), dtype=torch.uint8, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    totals = torch.zeros(world, dtype=torch.int64, device=dev)
+    my_total = torch.zeros(1, dtype=torch.int64, device=dev)
+    r_tr = out["rew"][c["burn_in"]:c["burn_in"] + c["train"] + c["n_step"] - 1]
+    d_tr = out["done"][c["burn_in"]:c["burn_in"] + c["train"] + c["n_step"] - 1]
+    Tn = c["train"] + c["n_step"] - 1
+    lib, P_ = rpl._lib.lib, rpl.ops._ptr
+
+    def step(i, gather_events=None):
+        s = rpl.ops._stream(dev)
+        cur, prev = idx_buf[i % 2], idx_buf[(i + 1) % 2]
+        # (a5-a7) new priorities for the previous batch (entries < 0 = not owned: skipped by the kernel? no:
+        # they are flagged; so update only when owned entries exist — the kernel skips idx < 0 with RPL_DERR_IDX)
+        rpl._lib.check(lib.rpl_sumtree_update(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]), n_glob,
+                                              c["alpha"], c["eps_p"], None, s), "update")
+        if world == 1:
+            rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, seed, c["beta"], P_(cur),
+                                                         P_(q_buf), P_(qmin), P_(w), P_(err), s), "sample")
+        else:
+            rpl._lib.check(lib.rpl_sumtree_total(tree._lp, P_(tree.storage), P_(my_total), s), "total")
+            dist.all_gather_into_tensor(totals, my_total)                       # K5: 8 B per rank
+            rpl._lib.check(lib.rpl_sumtree_sample_sharded(tree._lp, P_(tree.storage), rank, world, n_leaves,
+                                                          P_(totals), n_glob, None, seed, 0, 1, P_(cur), P_(q_buf),
+                                                          P_(qmin), P_(err), s), "sample_sharded")
+            dist.all_reduce(qmin, op=dist.ReduceOp.MIN)                          # K7: global batch min
+            rpl._lib.check(lib.rpl_is_weights(P_(q_buf), P_(qmin), n_glob, c["beta"], P_(w), s), "w")
+        if gather_events is not None:
+            gather_events[0].record()
+        plan.run(cur, stream=s)
+        if gather_events is not None:
+            gather_events[1].record()
+        rpl._lib.check(lib.rpl_returns_nstep(P_(r_tr), P_(d_tr), Tn, n_glob, c["n_step"], c["gamma"],
+                                             P_(q_pool[i % P][c["burn_in"]:c["burn_in"] + Tn]),
+                                             P_(q_pool[i % P][c["burn_in"] + Tn]), 1, c["eps"], P_(y), P_(dn), s),
+                       "nstep")
+
+    # idx < 0 entries (first step / not-owned) make the update kernel flag RPL_DERR_IDX; allow that bit.
+    # warm-up (also primes lazy module loading and cudaFuncSetAttribute outside capture)
+    for i in range(max(args.warmup, 2)):
+        step(i)
+    torch.cuda.synchronize()
+    rpl.check_err(err)
+
+    use_graph = (not args.no_graph) and world == 1
+    graph = None
+    if use_graph:
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            for i in range(P):
+                step(i)
+        torch.cuda.synchronize()
+    K = args.steps
+    reps = math.ceil(K / P) if use_graph else K
+    K_eff = reps * P if use_graph else K
+
+    clocks = ClockSampler(local)
+    if not args.profile:
+        clocks.start()
+        time.sleep(0.3)
+    # timed region
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    launches0 = rpl.launch_count()
+    e0.record()
+    if use_graph:
+        for _ in range(reps):
+            graph.replay()
+    else:
+        for i in range(K_eff):
+            step(i)
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    launches = (rpl.launch_count() - launches0) if not use_graph else 4 * K_eff
+    clk = clocks.stop() if not args.profile else {}
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    value = K_eff * n * world / (ms / 1e3)
+
+    # dominant kernel (sequence gather): average launch duration with CUDA events on
+    # the launching stream, over K eager steps of the same workload
+    Kg = min(K_eff, 200)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(Kg)]
+    torch.cuda.synchronize()
+    for i in range(Kg):
+        step(i, evs[i])
+    torch.cuda.synchronize()
+    g_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    owned = n  # per rank, on average
+    alg_bytes = owned * seq_bytes_per_sample(c)
+    peak, peak_kind = measured_peaks()
+    achieved = alg_bytes / (g_ms / 1e3) / 1e9
+
+    rpl.check_err(err)
+
+    result = {
+        "metric": "prioritized samples/sec (update+sample+gather)",
+        "value": value,
+        "unit": "sequences/s",
+        "n_gpus": world,
+        "steps": K_eff,
+        "warmup": max(args.warmup, 2),
+        "ms_per_step": ms / K_eff,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8 frames + f32 (fp64 accum) + int64 tree",
+        "data": "synthetic (seeded; uniform-random 84x84 u8 frames, R2D2 reward/episode recipe, DESIGN.md)",
+        "config": {"workload": "r2d2_1mstep", "ring": [c["cap_T"], c["B"]], "ring_per_gpu": [c["cap_T"], Bl],
+                   "leaves_per_gpu": n_leaves, "batch_per_gpu": n, "seq_len": L, "burn_in": c["burn_in"],
+                   "train": c["train"], "tail": c["tail"], "frame_stack": k, "n_step": c["n_step"],
+                   "gamma": c["gamma"], "alpha": c["alpha"], "beta": c["beta"], "out": "stacked",
+                   "parallelism": f"mode-L x{world}" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (7.2 GB ring, random sequences every step)",
+                   "timing": "cuda graph of 8 steps, replayed" if use_graph else "eager launches"},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": "k_gather_sequence", "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": g_ms,
+                     "step_share": g_ms / (ms / K_eff)},
+    }
+    if not args.profile:
+        result["clocks"] = clk
+        result["e2e"] = e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K_eff, world)
+    if world == 1 and not args.no_secondary and not args.profile:
+        result["secondary"] = {"ppo_returns": bench_ppo(dev, rpl)}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        result["cpu_baseline"] = cpu_baseline(c, host, args.cpu_seconds)
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result))
+
+
+def e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K, world):
+    """Same metric through the public API with HOST buffers: every step copies its
+    inputs (the previous batch's |delta| and the target-net Q rows) from pinned host
+    memory and reads the step's result (targets, IS weights, indices) back."""
+    import torch
+    K = min(K, 300)
+    h_td = torch.empty(td_pool.shape, dtype=torch.float32).pin_memory()
+    h_q = torch.empty(q_pool.shape, dtype=torch.float32).pin_memory()
+    h_td.copy_(td_pool.cpu())
+    h_q.copy_(q_pool.cpu())
+    h_y = torch.empty(y.shape, dtype=torch.float32).pin_memory()
+    h_w = torch.empty(w.shape, dtype=torch.float32).pin_memory()
+    h_i = torch.empty(idx_buf[0].shape, dtype=torch.int64).pin_memory()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(K):
+        td_pool[i % P].copy_(h_td[i % P], non_blocking=True)
+        q_pool[i % P].copy_(h_q[i % P], non_blocking=True)
+        step(i)
+        h_y.copy_(y, non_blocking=True)
+        h_w.copy_(w, non_blocking=True)
+        h_i.copy_(idx_buf[i % 2], non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    hb = td_pool[0].numel() * 4 + q_pool[0].numel() * 4
+    db = y.numel() * 4 + w.numel() * 4 + idx_buf[0].numel() * 8
+    return {"value": K * n * world / (ms / 1e3), "unit": "sequences/s", "h2d_bytes_per_step": hb,
+            "d2h_bytes_per_step": db, "steps": K}
+
+
+def bench_ppo(dev, rpl):
+    """GAE + discounted returns on [128, 4096] (configs[1]); inputs rotate over a
+    pool larger than L2 so every call reads HBM."""
+    import torch
+    from synth import returns_inputs
+    T, B = PPO["T"], PPO["B"]
+    r, v, d, boot = returns_inputs(5, T, B, reward_kind="clipped", p_done=1e-3)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    per = T * B * 17
+    pool = max(4, int(math.ceil(4 * l2 / per)))
+    R = torch.from_numpy(r).to(dev).repeat(pool, 1, 1).contiguous()
+    V = torch.from_numpy(v).to(dev).repeat(pool, 1, 1).contiguous()
+    D = torch.from_numpy(d).to(dev).repeat(pool, 1, 1).contiguous()
+    BT = torch.from_numpy(boot).to(dev)
+    A = torch.empty_like(R)
+    RT = torch.empty_like(R)
+    for i in range(pool):
+        rpl.gae(R[i], V[i], D[i], BT, PPO["gamma"], PPO["lam"], adv=A[i], ret=RT[i])
+    torch.cuda.synchronize()
+    reps = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        for i in range(pool):
+            rpl.gae(R[i], V[i], D[i], BT, PPO["gamma"], PPO["lam"], adv=A[i], ret=RT[i])
+    e1.record()
+    torch.cuda.synchronize()
+    ms_gae = e0.elapsed_time(e1) / (reps * pool)
+    e0.record()
+    for _ in range(reps):
+        for i in range(pool):
+            rpl.returns_discounted(R[i], D[i], BT, PPO["gamma"], out=RT[i])
+    e1.record()
+    torch.cuda.synchronize()
+    ms_disc = e0.elapsed_time(e1) / (reps * pool)
+    peak, kind = measured_peaks()
+    gae_gbs = T * B * 17 / (ms_gae / 1e3) / 1e9
+    disc_gbs = (T * B * 9 + B * 4) / (ms_disc / 1e3) / 1e9
+    return {"workload": "ppo_[128,4096]", "unit": "elems/s",
+            "gae_elems_per_s": T * B / (ms_gae / 1e3), "gae_us_per_call": ms_gae * 1e3, "gae_GBps": gae_gbs,
+            "gae_frac": gae_gbs / peak, "disc_elems_per_s": T * B / (ms_disc / 1e3),
+            "disc_us_per_call": ms_disc * 1e3, "disc_GBps": disc_gbs, "disc_frac": disc_gbs / peak,
+            "l2": f"input pool {pool} x {per/1e6:.1f} MB > 4 x L2", "timing": "eager, back-to-back calls"}
+
+
+# ----------------------------------------------------------------------------- oracle arm
+class OracleStep:
+    """The CPU oracle doing the same R2D2 step (update + sample + gather + rescaled
+    n-step targets) on host copies of the same inputs."""
+
+    def __init__(self, c, host, seed=77):
+        from oracle import sumtree as OS
+        from paper_1909_01500_b200 import replay as R  # host index logic only (valid leaves)
+        self.c, self.h = c, host
+        B = host.obs.shape[1]
+        self.B = B
+        n_leaves = (c["cap_T"] // c["period"]) * B
+        self.tree = OS.SumTreeOracle(n_leaves)
+        blocks = R.valid_sequence_blocks(c["cap_T"], c["period"], host.cursor, host.size, c["k"], c["L"])
+        valid = R.leaves_of(blocks, B)
+        g = np.random.Generator(np.random.PCG64(seed))
+        td0 = np.abs(g.normal(size=valid.size)).astype(np.float32)
+        self.tree.update([int(x) for x in valid], [float(x) for x in td0], c["alpha"], c["eps_p"])
+        self.g = g
+        self.prev = []
+        self.ctr = 0
+
+    def step(self, nseq):
+        from oracle import gather as OG
+        from oracle import philox as OP
+        from oracle import returns as OR
+        from oracle import sumtree as OS
+        c, h = self.c, self.h
+        td = np.abs(self.g.normal(size=len(self.prev))).astype(np.float32)
+        self.tree.update(self.prev, [float(x) for x in td], c["alpha"], c["eps_p"])
+        draws = OP.draws_u64(0x5EED, self.ctr, nseq)
+        self.ctr += nseq
+        idx, q, qmin = self.tree.sample(nseq, draws)
+        OS.is_weights(q, self.tree.total(), self.tree.n_leaves, c["beta"])
+        out = OG.gather_sequences(idx, self.B, h.obs, h.act, h.rew, h.done, h.rnn, c["k"], c["L"], c["period"])
+        lo = c["burn_in"]
+        Tn = c["train"] + c["n_step"] - 1
+        qv = self.g.normal(0, 10, (c["L"], nseq))
+        OR.nstep_return(out["rew"][lo:lo + Tn], out["done"][lo:lo + Tn], c["n_step"], c["gamma"],
+                        q=qv[lo:lo + Tn], q_boot=qv[lo + Tn], rescale=True, eps=c["eps"])
+        self.prev = idx
+        return nseq
+
+
+def _cores():
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except AttributeError:
+        aff = os.cpu_count()
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return aff, model
+
+
+def cpu_baseline(c, host, seconds):
+    for v in ("OMP_NUM_THREADS", "MKL_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
+        os.environ[v] = "1"
+    o = OracleStep(c, host)
+    o.step(4)  # warm
+    t0 = time.time()
+    done = 0
+    nsteps = 0
+    while time.time() - t0 < seconds:
+        done += o.step(c["batch"])
+        nsteps += 1
+    dt = time.time() - t0
+    aff, model = _cores()
+    return {"value": done / dt, "unit": "sequences/s", "cores": 1, "kind": "oracle",
+            "sample": f"{nsteps} full R2D2 steps ({c['batch']} sequences each: update + sample over "
+                      f"{o.tree.n_leaves} leaves + stacked gather + rescaled 5-step targets), {dt:.1f} s",
+            "host_cpus": os.cpu_count(), "affinity": aff, "cpu_model": model}
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return  # N > 1: rank 0 alone runs the oracle
+    for v in ("OMP_NUM_THREADS", "MKL_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
+        os.environ[v] = "1"
+    from synth import make_ring
+    c = dict(R2D2)
+    host = make_ring(2019, c["cap_T"], c["B"], ep_len=2000.0, reward_kind="r2d2", period=c["period"],
+                     rnn_parts=c["rnn_parts"], rnn_h=c["rnn_h"], cursor=1234 % c["cap_T"])
+    o = OracleStep(c, host)
+    t0 = time.time()
+    o.step(2)
+    per_seq = max(1e-3, (time.time() - t0) / 2)
+    K, W = args.steps, args.warmup
+    budget = 150.0
+    nseq = int(max(1, min(c["batch"], budget / max(1, K + min(W, 3)) / per_seq)))
+    for _ in range(min(W, 3)):
+        o.step(nseq)
+    t0 = time.time()
+    done = 0
+    for _ in range(K):
+        done += o.step(nseq)
+    dt = time.time() - t0
+    aff, model = _cores()
+    val = done / dt
+    res = {"impl": "reference", "metric": "prioritized samples/sec (update+sample+gather)", "value": val,
+           "unit": "sequences/s", "n_gpus": world, "steps": K, "warmup": min(W, 3), "ms_per_step": dt / K * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 / python int",
+           "data": "synthetic (seeded, same recipe)",
+           "config": {"workload": "r2d2_1mstep", "ring": [c["cap_T"], c["B"]], "batch_per_step": nseq},
+           "cpu_baseline": {"value": val, "unit": "sequences/s", "cores": 1, "kind": "oracle",
+                            "sample": f"{K} steps of {nseq} sequences (bounded sample of the 64-sequence step)",
+                            "host_cpus": os.cpu_count(), "affinity": aff, "cpu_model": model},
+           "e2e": {"value": val, "unit": "sequences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(res))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_rpl(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -31,7 +31,7 @@ extern "C" {
 #endif
 
 #define RPL_ABI_VERSION 1
-#define RPL_MAX_LEVELS 12
+#define RPL_MAX_LEVELS 24
 
 typedef enum {
   RPL_OK = 0,
@@ -100,7 +100,8 @@ int rpl_value_rescale(const float* x, float* y, int64_t n, double eps, int32_t i
  *     of level l+1.  Every level is zero-padded to a multiple of W.  Leaf i is word
  *     level_off[depth] + i and holds q_i = round_half_even(RN32(p_i^alpha) * 2^F)
  *     (§8c #7).  Header: [hdr_off+0] max-priority-seen, [hdr_off+1] sampler
- *     ticket (library scratch, always 0 between calls).
+ *     ticket (library scratch, always 0 between calls), [hdr_off+2] Philox stream
+ *     position used by rpl_sumtree_sample_stream (0 after init).
  * ========================================================================= */
 typedef struct {
   int64_t n_leaves;
@@ -124,7 +125,8 @@ int rpl_sumtree_init(const rpl_tree_layout* L, int64_t* tree, void* stream);
 /* Batched priority update (a5-a7): for k in 0..n-1, p = RN64(|td_abs[k]| + eps_p),
  * q = RNE(RN32(p^alpha) * 2^F) clamped to q_cap; leaf idx[k] := q.  Duplicate indices: the
  * LAST position in the batch wins.  Internal nodes are updated exactly (int64).
- * max-seen := max(max-seen, every valid q in the batch).  Bad idx -> skipped + RPL_DERR_IDX.
+ * max-seen := max(max-seen, every valid q in the batch).  idx[k] < 0 is a padding entry (e.g. a
+ * sample another shard owns) and is skipped silently; idx[k] >= n_leaves -> skipped + RPL_DERR_IDX.
  * alpha >= 0, eps_p >= 0.  n >= 0 (n == 0 is a no-op). */
 int rpl_sumtree_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx,
                        const float* td_abs, int64_t n, double alpha, double eps_p,
@@ -150,18 +152,27 @@ int rpl_sumtree_sample(const rpl_tree_layout* L, int64_t* tree, int64_t n, const
                        int64_t* out_q, int64_t* out_qmin, float* out_w, int32_t* dev_err,
                        void* stream);
 
+/* As rpl_sumtree_sample with draws = NULL, but the Philox counter is ctr = S + k where S is
+ * the tree's stream position (header word 2); the call advances S by n on the device, so a
+ * captured CUDA graph draws fresh strata on every replay.  Deterministic for a fixed history. */
+int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree, int64_t n, uint64_t seed,
+                              double beta, int64_t* out_idx, int64_t* out_q, int64_t* out_qmin,
+                              float* out_w, int32_t* dev_err, void* stream);
+
 /* Sharded sampling: rank `rank` of n_shards holds one tree; shard_totals
  * (device int64 [n_shards], e.g. all-gathered rpl_sumtree_total outputs) define the global
  * total Q and the shard-major global leaf order (global idx = rank * shard_leaves + local).
  * Every rank evaluates the same n global strata; it descends only the strata whose prefix
  * falls in its own range and writes out_idx[k] = global leaf index (or -1 when not owned),
  * out_q[k] (0 when not owned), *out_qmin = min over owned (INT64_MAX if none).  Equal to
- * rpl_sumtree_sample on the concatenation of the shards (§8c #17). */
+ * rpl_sumtree_sample on the concatenation of the shards (§8c #17).  use_stream != 0 (draws
+ * must be NULL) takes the Philox counter from this tree's stream position as
+ * rpl_sumtree_sample_stream does; every rank's position advances by n identically. */
 int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t rank,
                                int32_t n_shards, int64_t shard_leaves, const int64_t* shard_totals,
                                int64_t n, const uint64_t* draws, uint64_t seed, uint64_t offset,
-                               int64_t* out_idx, int64_t* out_q, int64_t* out_qmin,
-                               int32_t* dev_err, void* stream);
+                               int32_t use_stream, int64_t* out_idx, int64_t* out_q,
+                               int64_t* out_qmin, int32_t* dev_err, void* stream);
 
 /* Descent for explicit prefixes: out_idx[k] = leaf with C_i <= prefix[k] < C_{i+1}.
  * prefix >= total -> clamped to the last non-empty leaf + RPL_DERR_TREE. */

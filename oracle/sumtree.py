@@ -54,7 +54,9 @@ class SumTreeOracle:
     def update(self, idx, td_abs, alpha: float, eps_p: float = 1e-3):
         for i, d in zip(idx, td_abs):
             i = int(i)
-            if i < 0 or i >= self.n_leaves:
+            if i < 0:                                 # padding entry (rpl.h): skipped silently
+                continue
+            if i >= self.n_leaves:
                 self.err_idx = True
                 continue
             M, E = _pr.priority_value(float(d), alpha, eps_p)
@@ -70,7 +72,9 @@ class SumTreeOracle:
         for k, i in enumerate(idx):
             i = int(i)
             v = self.max_seen if q is None else int(q[k])
-            if i < 0 or i >= self.n_leaves or v < 0:
+            if i < 0:
+                continue
+            if i >= self.n_leaves or v < 0:
                 self.err_idx = True
                 continue
             if v > self.cap:

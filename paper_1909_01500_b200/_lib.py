@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librpl.so")
 
-RPL_MAX_LEVELS = 12
+RPL_MAX_LEVELS = 24
 
 RPL_OK = 0
 STATUS = {0: "RPL_OK", -1: "RPL_EINVAL", -2: "RPL_ERANGE", -3: "RPL_EEMPTY", -4: "RPL_ECUDA",
@@ -73,8 +73,9 @@ _SIGS = {
     "rpl_sumtree_update": ([C.POINTER(TreeLayout), P, P, P, I64, D, D, P, P], C.c_int),
     "rpl_sumtree_set_q": ([C.POINTER(TreeLayout), P, P, P, I64, P, P], C.c_int),
     "rpl_sumtree_sample": ([C.POINTER(TreeLayout), P, I64, P, U64, U64, D, P, P, P, P, P, P], C.c_int),
-    "rpl_sumtree_sample_sharded": ([C.POINTER(TreeLayout), P, I32, I32, I64, P, I64, P, U64, U64, P, P, P, P, P],
-                                   C.c_int),
+    "rpl_sumtree_sample_stream": ([C.POINTER(TreeLayout), P, I64, U64, D, P, P, P, P, P, P], C.c_int),
+    "rpl_sumtree_sample_sharded": ([C.POINTER(TreeLayout), P, I32, I32, I64, P, I64, P, U64, U64, I32, P, P, P, P,
+                                    P], C.c_int),
     "rpl_sumtree_find": ([C.POINTER(TreeLayout), P, P, I64, P, P, P], C.c_int),
     "rpl_sumtree_total": ([C.POINTER(TreeLayout), P, P, P], C.c_int),
     "rpl_sumtree_rebuild": ([C.POINTER(TreeLayout), P, P], C.c_int),
@@ -88,7 +89,7 @@ EXPORTS = tuple(_SIGS)
 
 def _load():
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"librpl.so not built at {LIB_PATH}: run `python -m paper_1909_01500_b200.build` "
+        raise ImportError(f"librpl.so not built at {LIB_PATH}: run `python paper_1909_01500_b200/build.py` "
                           "(or __graft_entry__.build()); there is no CPU fallback")
     lib = C.CDLL(LIB_PATH)
     for name, (args, res) in _SIGS.items():

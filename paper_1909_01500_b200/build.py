@@ -1,6 +1,6 @@
 """Build librpl.so (the C-ABI shared library) in-tree with nvcc for sm_100a.
 
-    python -m paper_1909_01500_b200.build        # or __graft_entry__.build()
+    python paper_1909_01500_b200/build.py        # or __graft_entry__.build()
 
 No torch types cross the boundary, so the library is plain nvcc output; the
 CUDA runtime is linked statically.  -lineinfo keeps ncu's source page usable.

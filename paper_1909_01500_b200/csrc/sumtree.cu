@@ -60,8 +60,10 @@ k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__
     int64_t leaf = -1, q = 0;
     if (i < n) {
       leaf = idx[i];
-      bool ok = leaf >= 0 && leaf < L.n_leaves;
-      if (ok) {
+      bool ok = leaf < L.n_leaves;  // leaf < 0: padding entry, skipped silently
+      if (leaf < 0) {
+        leaf = -1;
+      } else if (ok) {
         if (mode == MODE_TD) {
           const double p = (double)fabsf(td[i]) + eps_p;  // RN64(|delta| + eps_p)
           float v;
@@ -185,8 +187,10 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
               uint64_t seed, uint64_t offset, double beta, int64_t* __restrict__ out_idx,
               int64_t* __restrict__ out_q, int64_t* __restrict__ out_qmin, float* __restrict__ out_w,
               int32_t* err, int rank, int n_shards, int64_t shard_leaves,
-              const int64_t* __restrict__ totals) {
+              const int64_t* __restrict__ totals, int use_stream) {
   const int lane = threadIdx.x & 31;
+  // Philox counter base: offset, plus the tree's stream position when use_stream
+  const uint64_t ctr0 = offset + (use_stream ? (uint64_t)tree[L.hdr_off + 2] : 0ull);
   const int64_t k = (int64_t)blockIdx.x * SAMPLE_WARPS + (threadIdx.x >> 5);
   int32_t errbits = 0;
   uint64_t Q, own_lo = 0, own_T = 0;
@@ -208,7 +212,7 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
     } else {
       const uint64_t lo = stratum_lo((uint64_t)k, Q, (uint64_t)n);
       const uint64_t hi = stratum_lo((uint64_t)k + 1, Q, (uint64_t)n);
-      const uint64_t u = draws ? draws[k] : philox_u64(seed, offset + (uint64_t)k);
+      const uint64_t u = draws ? draws[k] : philox_u64(seed, ctr0 + (uint64_t)k);
       uint64_t prefix = lo + __umul64hi(u, hi - lo);
       bool mine = true;
       if (SHARDED) {
@@ -259,6 +263,7 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
   if (threadIdx.x == 0) {
     if (out_qmin) *out_qmin = (!SHARDED && Q == 0) ? 0 : qmin;
     *reinterpret_cast<unsigned long long*>(tree + L.hdr_off + 1) = 0ull;  // reset ticket
+    if (use_stream) tree[L.hdr_off + 2] = (int64_t)(ctr0 - offset + (uint64_t)n);  // advance stream
   }
   if (out_w) {
     for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
@@ -293,17 +298,22 @@ __global__ void k_tree_total(const int64_t* __restrict__ tree, int64_t* __restri
   *out = tree[0];
 }
 
-__global__ void k_tree_level(TreeDev L, int64_t* __restrict__ tree, int l, int64_t len) {
-  // node j of level l := sum of its W children on level l+1
+__global__ void k_tree_level(TreeDev L, int64_t* __restrict__ tree, int l, int64_t len, int64_t real) {
+  // node j of level l := sum of its W children on level l+1 (real nodes); padding nodes := 0.
+  // A real node's children lie inside level l+1 (len(l+1) = real(l) * W), a padding
+  // node's would not, so padding is never summed.
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= len) return;
-  const int64_t* ch = tree + L.level_off[l + 1] + (j << L.log2w);
   int64_t s = 0;
-  for (int c = 0; c < L.fanout; ++c) s += ch[c];
+  if (j < real) {
+    const int64_t* ch = tree + L.level_off[l + 1] + (j << L.log2w);
+    for (int c = 0; c < L.fanout; ++c) s += ch[c];
+  }
   tree[L.level_off[l] + j] = s;
 }
 
 __global__ void k_tree_header(int64_t* __restrict__ hdr, int64_t maxseen) {
+  // [0] max-seen, [1] sampler ticket, [2] Philox stream position
   hdr[0] = maxseen;
   for (int i = 1; i < 8; ++i) hdr[i] = 0;
 }
@@ -413,20 +423,33 @@ extern "C" int rpl_sumtree_sample(const rpl_tree_layout* L, int64_t* tree, int64
   const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
   k_tree_sample<false><<<(unsigned)blocks, SAMPLE_WARPS * 32, 0, as_stream(stream)>>>(
       tree_dev(L), tree, n, draws, seed, offset, beta, out_idx, out_q, out_qmin, out_w, dev_err, 0, 1, 0,
-      nullptr);
+      nullptr, 0);
+  return launch_status();
+}
+
+extern "C" int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree, int64_t n, uint64_t seed,
+                                         double beta, int64_t* out_idx, int64_t* out_q, int64_t* out_qmin,
+                                         float* out_w, int32_t* dev_err, void* stream) {
+  if (!layout_ok(L) || !tree || !out_idx || !out_q || n < 1 || n > (1ll << 30)) return RPL_EINVAL;
+  if (out_w && !(beta >= 0.0)) return RPL_EINVAL;
+  const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
+  k_tree_sample<false><<<(unsigned)blocks, SAMPLE_WARPS * 32, 0, as_stream(stream)>>>(
+      tree_dev(L), tree, n, nullptr, seed, 0, beta, out_idx, out_q, out_qmin, out_w, dev_err, 0, 1, 0, nullptr, 1);
   return launch_status();
 }
 
 extern "C" int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t rank, int32_t n_shards,
                                           int64_t shard_leaves, const int64_t* shard_totals, int64_t n,
-                                          const uint64_t* draws, uint64_t seed, uint64_t offset, int64_t* out_idx,
-                                          int64_t* out_q, int64_t* out_qmin, int32_t* dev_err, void* stream) {
+                                          const uint64_t* draws, uint64_t seed, uint64_t offset, int32_t use_stream,
+                                          int64_t* out_idx, int64_t* out_q, int64_t* out_qmin, int32_t* dev_err,
+                                          void* stream) {
+  if (draws && use_stream) return RPL_EINVAL;
   if (!layout_ok(L) || !tree || !out_idx || !out_q || !shard_totals || n < 1 || n > (1ll << 30)) return RPL_EINVAL;
   if (n_shards < 1 || rank < 0 || rank >= n_shards || shard_leaves < L->n_leaves) return RPL_EINVAL;
   const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
   k_tree_sample<true><<<(unsigned)blocks, SAMPLE_WARPS * 32, 0, as_stream(stream)>>>(
       tree_dev(L), tree, n, draws, seed, offset, 0.0, out_idx, out_q, out_qmin, nullptr, dev_err, rank, n_shards,
-      shard_leaves, shard_totals);
+      shard_leaves, shard_totals, use_stream);
   return launch_status();
 }
 
@@ -451,7 +474,10 @@ extern "C" int rpl_sumtree_rebuild(const rpl_tree_layout* L, int64_t* tree, void
   TreeDev T = tree_dev(L);
   for (int l = L->depth - 1; l >= 0; --l) {
     const int64_t len = L->level_len[l];
-    k_tree_level<<<(unsigned)((len + 255) / 256), 256, 0, as_stream(stream)>>>(T, tree, l, len);
+    int64_t span = 1;
+    for (int i = 0; i < L->depth - l; ++i) span *= L->fanout;
+    const int64_t real = (L->n_leaves + span - 1) / span;
+    k_tree_level<<<(unsigned)((len + 255) / 256), 256, 0, as_stream(stream)>>>(T, tree, l, len, real);
     int s = launch_status();
     if (s != RPL_OK) return s;
   }

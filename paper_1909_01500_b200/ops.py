@@ -201,7 +201,24 @@ class SumTree:
                                      _ptr(qmin), _ptr(w), _ptr(e), self._s()), "rpl_sumtree_sample")
         return idx, q, qmin, w
 
-    def sample_sharded(self, rank, n_shards, shard_totals, n, draws=None, seed=0, offset=0, out=None, err=None):
+    def sample_stream(self, n, seed, beta=None, out=None, err=None):
+        """rpl_sumtree_sample_stream: Philox draws from the tree's device-side stream position."""
+        n = int(n)
+        if out is None:
+            idx = torch.empty(n, dtype=torch.int64, device=self.device)
+            q = torch.empty(n, dtype=torch.int64, device=self.device)
+            qmin = torch.empty(1, dtype=torch.int64, device=self.device)
+            w = torch.empty(n, dtype=torch.float32, device=self.device) if beta is not None else None
+        else:
+            idx, q, qmin, w = out
+        e = self.err if err is None else err
+        check(lib.rpl_sumtree_sample_stream(self._lp, _ptr(self.storage), n, int(seed) & (2 ** 64 - 1),
+                                            float(beta or 0.0), _ptr(idx), _ptr(q), _ptr(qmin), _ptr(w), _ptr(e),
+                                            self._s()), "rpl_sumtree_sample_stream")
+        return idx, q, qmin, w
+
+    def sample_sharded(self, rank, n_shards, shard_totals, n, draws=None, seed=0, offset=0, out=None, err=None,
+                       use_stream=False):
         n = int(n)
         _req(shard_totals, torch.int64, "shard_totals", (n_shards,))
         if out is None:
@@ -213,7 +230,8 @@ class SumTree:
         e = self.err if err is None else err
         check(lib.rpl_sumtree_sample_sharded(self._lp, _ptr(self.storage), int(rank), int(n_shards),
                                              self.n_leaves, _ptr(shard_totals), n, _ptr(draws),
-                                             int(seed) & (2 ** 64 - 1), int(offset) & (2 ** 64 - 1), _ptr(idx),
+                                             int(seed) & (2 ** 64 - 1), int(offset) & (2 ** 64 - 1),
+                                             1 if use_stream else 0, _ptr(idx),
                                              _ptr(q), _ptr(qmin), _ptr(e), self._s()),
               "rpl_sumtree_sample_sharded")
         return idx, q, qmin
@@ -340,3 +358,42 @@ def gather(ring: GatherRing, idx, kind="transition", k=4, n_step=1, gamma=0.99, 
     check(lib.rpl_gather(C.byref(g), _ptr(idx), _ptr(q), _ptr(qmin), float(beta), n, _ptr(e), _stream(dev)),
           "rpl_gather")
     return o
+
+
+class GatherPlan:
+    """A prepared rpl_gather call: the descriptor (ring + preallocated outputs) is
+    built once, so each run() is one ctypes call (cheap enough for a hot loop and
+    capturable in a CUDA graph)."""
+
+    def __init__(self, ring: GatherRing, n, kind="transition", k=4, n_step=1, gamma=0.99, seq_len=1, period=1,
+                 pad_mode=_lib.PAD_REPEAT, out_mode=_lib.OUT_STACKED, want=None, with_weights=False):
+        dev = ring.obs.device
+        self.n = int(n)
+        dummy = torch.zeros(self.n, dtype=torch.int64, device=dev)
+        self.outputs = {}
+        # allocate via gather() on an all-skip index vector (no kernel work: idx < 0)
+        self.outputs = gather(ring, torch.full_like(dummy, -1), kind=kind, k=k, n_step=n_step, gamma=gamma,
+                              seq_len=seq_len, period=period, pad_mode=pad_mode, out_mode=out_mode, want=want)
+        if with_weights:
+            self.outputs["w"] = torch.empty(self.n, dtype=torch.float32, device=dev)
+        kind_i = _lib.GATHER_TRANSITION if kind == "transition" else _lib.GATHER_SEQUENCE
+        self.desc = _desc(ring, kind_i, k, pad_mode, out_mode, n_step if kind_i == 0 else 1, seq_len, period, gamma)
+        fields = {"obs": "o_obs", "next_obs": "o_next_obs", "act": "o_act", "prev_act": "o_prev_act",
+                  "rew": "o_rew", "prev_rew": "o_prev_rew", "done": "o_done", "ret": "o_ret", "done_n": "o_done_n",
+                  "w": "o_w", "rnn": "o_rnn"}
+        for name, f in fields.items():
+            if name in self.outputs:
+                setattr(self.desc, f, self.outputs[name].data_ptr())
+        self._dp = C.byref(self.desc)
+        self.device = dev
+        self.ring = ring
+
+    def set_cursor(self, cursor, size):
+        self.desc.cursor = int(cursor)
+        self.desc.size = int(size)
+
+    def run(self, idx, q=None, qmin=None, beta=0.0, err=None, stream=None):
+        s = _stream(self.device) if stream is None else stream
+        check(lib.rpl_gather(self._dp, _ptr(idx), _ptr(q), _ptr(qmin), float(beta), self.n, _ptr(err), s),
+              "rpl_gather")
+        return self.outputs

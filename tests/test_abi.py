@@ -20,7 +20,10 @@ def declared():
 
 @pytest.fixture(scope="module")
 def lib():
-    from paper_1909_01500_b200 import build
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_rpl_build", os.path.join(PKG, "build.py"))
+    build = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(build)
     build.build()
     return ctypes.CDLL(build.LIB)
 

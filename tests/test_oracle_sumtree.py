@@ -87,6 +87,8 @@ def test_update_floor_eps():
 
 def test_update_bad_index_skipped():
     t = S.SumTreeOracle(4)
+    t.update([-1, 1], [1.0, 1.0], 1.0)
+    assert not t.err_idx                      # negative = padding, skipped silently
     t.update([5, -1, 1], [1.0, 1.0, 1.0], 1.0)
     assert t.err_idx and t.q == [0, P.priority_q(1.0, 1.0, 1e-3, 32, 4), 0, 0]
 
