@@ -16,7 +16,7 @@ from ._lib import GatherDesc, TreeLayout, check, lib
 
 __all__ = [
     "returns_discounted", "returns_nstep", "gae", "value_rescale", "SumTree", "is_weights", "gather",
-    "GatherRing", "check_err", "launch_count", "debug_priority_values",
+    "GatherRing", "GatherPlan", "check_err", "launch_count", "debug_priority_values",
 ]
 
 
