@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget (cpu_baseline)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/baseline/e2e)")
+    ap.add_argument("--seq-variant", type=int, default=None, help="diagnostics: sequence-gather kernel variant")
     return ap.parse_args()
 
 
@@ -159,6 +160,8 @@ def run_rpl(args):
     import paper_1909_01500_b200 as rpl
     from paper_1909_01500_b200 import replay as R
     from synth import make_ring, rng
+    if args.seq_variant is not None:
+        rpl._lib.check(rpl._lib.lib.rpl_debug_set_gather_variant(int(args.seq_variant)), "variant")
 
     c = dict(R2D2)
     b0, b1 = R.shard_columns(c["B"], world, rank)
@@ -391,25 +394,34 @@ def bench_ppo(dev, rpl):
     BT = torch.from_numpy(boot).to(dev)
     A = torch.empty_like(R)
     RT = torch.empty_like(R)
-    for i in range(pool):
-        rpl.gae(R[i], V[i], D[i], BT, PPO["gamma"], PPO["lam"], adv=A[i], ret=RT[i])
-    torch.cuda.synchronize()
-    reps = 20
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        for i in range(pool):
-            rpl.gae(R[i], V[i], D[i], BT, PPO["gamma"], PPO["lam"], adv=A[i], ret=RT[i])
-    e1.record()
-    torch.cuda.synchronize()
-    ms_gae = e0.elapsed_time(e1) / (reps * pool)
-    e0.record()
-    for _ in range(reps):
-        for i in range(pool):
-            rpl.returns_discounted(R[i], D[i], BT, PPO["gamma"], out=RT[i])
-    e1.record()
-    torch.cuda.synchronize()
-    ms_disc = e0.elapsed_time(e1) / (reps * pool)
+    def capture(fn):
+        for i in range(pool):  # warm (outside capture)
+            fn(i)
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream(dev)
+        st.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.graph(gr, stream=st):
+            for i in range(pool):
+                fn(i)
+        torch.cuda.synchronize()
+        return gr
+
+    def timeit(gr, reps=10):
+        gr.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            gr.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / (reps * pool)
+
+    g_gae = capture(lambda i: rpl.gae(R[i], V[i], D[i], BT, PPO["gamma"], PPO["lam"], adv=A[i], ret=RT[i]))
+    g_disc = capture(lambda i: rpl.returns_discounted(R[i], D[i], BT, PPO["gamma"], out=RT[i]))
+    ms_gae = timeit(g_gae)
+    ms_disc = timeit(g_disc)
     peak, kind = measured_peaks()
     gae_gbs = T * B * 17 / (ms_gae / 1e3) / 1e9
     disc_gbs = (T * B * 9 + B * 4) / (ms_disc / 1e3) / 1e9
@@ -417,7 +429,8 @@ def bench_ppo(dev, rpl):
             "gae_elems_per_s": T * B / (ms_gae / 1e3), "gae_us_per_call": ms_gae * 1e3, "gae_GBps": gae_gbs,
             "gae_frac": gae_gbs / peak, "disc_elems_per_s": T * B / (ms_disc / 1e3),
             "disc_us_per_call": ms_disc * 1e3, "disc_GBps": disc_gbs, "disc_frac": disc_gbs / peak,
-            "l2": f"input pool {pool} x {per/1e6:.1f} MB > 4 x L2", "timing": "eager, back-to-back calls"}
+            "l2": f"input pool {pool} x {per/1e6:.1f} MB > 4 x L2",
+            "timing": "CUDA graph of one call per pool entry, replayed; per-call average"}
 
 
 # ----------------------------------------------------------------------------- oracle arm

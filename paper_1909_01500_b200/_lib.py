@@ -82,6 +82,7 @@ _SIGS = {
     "rpl_is_weights": ([P, P, I64, D, P, P], C.c_int),
     "rpl_gather": ([C.POINTER(GatherDesc), P, P, P, D, I64, P, P], C.c_int),
     "rpl_debug_priority_values": ([P, I64, D, D, I32, P, P, P], C.c_int),
+    "rpl_debug_set_gather_variant": ([I32], C.c_int),
 }
 
 EXPORTS = tuple(_SIGS)

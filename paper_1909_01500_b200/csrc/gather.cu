@@ -416,6 +416,338 @@ k_gather_sequence(GDesc D, const int64_t* __restrict__ idx, int64_t n, const int
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Sequences, persistent TMA pipeline (stacked output).  The n*L output rows are
+// split into equal contiguous ranges, one per CTA, in (sample, row) order; a
+// range breaks into "pieces" (runs of rows of one sample).  A piece of R rows
+// needs the R+k-1 frames rows tau0-k+1 .. tau0+R-1, each loaded ONCE into a
+// ring of NS shared-memory slots:
+//   warp 0 / lane 0  producer: cp.async.bulk global->shared, one mbarrier per
+//                    slot; a slot is refilled once the consumer has released it;
+//   warp 1 / lane 0  consumer: per output row, waits for its k frames and issues
+//                    one cp.async.bulk shared->global store of the k-stack
+//                    (per-frame stores when padded or wrapping the ring); keeps
+//                    PIPE_G store groups in flight and releases frames whose
+//                    last reader has finished (cp.async.bulk.wait_group.read);
+//   warps 2-3        per-row fields, stored recurrent state, IS weights.
+// Loads and stores of different rows overlap continuously, and each frame is
+// read from HBM once per piece (pieces add k-1 frames at their start).
+// ---------------------------------------------------------------------------
+constexpr int PIPE_THREADS = 128;
+constexpr int PIPE_MAX_NS = 32;
+constexpr int PIPE_MAX_ROWS = 512;  // output rows per CTA
+template <int G>
+__device__ __forceinline__ void bulk_wait_read_G() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(G) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <int PIPE_G>  // store groups (output rows) in flight per consumer
+__global__ void __launch_bounds__(PIPE_THREADS)
+k_gather_seq_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, int64_t rows_per_cta,
+                  const int64_t* __restrict__ q, const int64_t* __restrict__ qmin, double beta, int32_t* err) {
+  extern __shared__ __align__(128) uint8_t smem[];  // NS frame slots + 1 zero slot
+  __shared__ __align__(8) uint64_t full[PIPE_MAX_NS];
+  __shared__ int8_t start_off[PIPE_MAX_ROWS];
+  __shared__ int rel_hist[64];
+  __shared__ volatile int free_count;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int k = D.k, L = D.seq_len;
+  const int64_t ob = D.obs_bytes;
+  const int64_t total = n * (int64_t)L;
+  const int64_t g0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t g1 = min(total, g0 + rows_per_cta);
+  if (g0 >= g1) return;
+  const int nrows = (int)(g1 - g0);
+  const int64_t nblk = D.cap_T / D.period;
+  uint8_t* zrow = smem + (int64_t)NS * ob;
+
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+    free_count = 0;
+  }
+  // per-row episode-start offsets (frame-stack padding, §8c #13) and validity flags
+  for (int c = tid; c < nrows; c += PIPE_THREADS) {
+    const int64_t g = g0 + c;
+    const int64_t s = g / L;
+    const int tau = (int)(g - s * L);
+    const int64_t leaf = idx[s];
+    int8_t so = 0;
+    if (leaf >= 0 && leaf < nblk * D.B) {
+      const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
+      const int64_t row = blk * D.period + tau;
+      int st = 0;  // start offset in (tau-k+1 .. tau]: latest row whose previous row ended an episode
+      for (int j = k - 1; j >= 1; --j) {
+        if (__ldg(D.done + wrap(row - (k - 1) + j - 1, D.cap_T) * D.B + b)) {
+          st = j;
+          break;
+        }
+      }
+      so = (int8_t)st;
+      if (tau == 0) {
+        const int64_t age = wrap(D.cursor - 1 - blk * D.period, D.cap_T);
+        const int hist = k - 1 > 1 ? k - 1 : 1;
+        if (!(age >= L - 1 && age + hist <= D.size - 1)) set_err(err, RPL_DERR_INVALID_LEAF);
+      }
+    } else if (leaf >= nblk * D.B && tau == 0) {
+      set_err(err, RPL_DERR_IDX);
+    }
+    start_off[c] = so;
+  }
+  if (D.pad_mode == RPL_PAD_ZERO) coop_zero(zrow, ob, tid, PIPE_THREADS);
+  fence_proxy_async();
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- producer ----------------
+      int64_t i = 0;  // frame position
+      int64_t g = g0;
+      while (g < g1) {
+        const int64_t s = g / L;
+        const int tau0 = (int)(g - s * L);
+        const int R = (int)min((int64_t)(L - tau0), g1 - g);
+        const int64_t leaf = idx[s];
+        if (leaf >= 0 && leaf < nblk * D.B) {
+          const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
+          const int64_t first = blk * D.period + tau0 - (k - 1);
+          for (int w = 0; w < R + k - 1; ++w, ++i) {
+            const int slot = (int)(i % NS);
+            if (i >= NS) {
+              while (free_count <= i - NS) __nanosleep(20);
+              fence_proxy_async();
+            }
+            mbar_expect_tx(&full[slot], (uint32_t)ob);
+            bulk_g2s(smem + (int64_t)slot * ob, D.obs + (wrap(first + w, D.cap_T) * D.B + b) * ob, (uint32_t)ob,
+                     &full[slot]);
+          }
+        }
+        g += R;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- consumer ----------------
+      int64_t F = 0;   // first frame position of the current piece
+      int c = 0;       // CTA-local row counter
+      int64_t g = g0;
+      while (g < g1) {
+        const int64_t s = g / L;
+        const int tau0 = (int)(g - s * L);
+        const int R = (int)min((int64_t)(L - tau0), g1 - g);
+        const int64_t leaf = idx[s];
+        const bool ok = leaf >= 0 && leaf < nblk * D.B;
+        for (int m = 0; m < R; ++m, ++c) {
+          if (ok) {
+            const int so = start_off[c];
+            // wait for the frames of this row: window coords m .. m+k-1 (positions F+m ..)
+            for (int j = (so > 0 ? so : 0); j < k; ++j) {
+              const int64_t pos = F + m + j;
+              mbar_wait(&full[pos % NS], (uint32_t)((pos / NS) & 1));
+            }
+            uint8_t* dst = D.o_obs + (((int64_t)(tau0 + m) * n + s) * k) * ob;
+            const int64_t p0 = F + m;
+            const int sl0 = (int)(p0 % NS);
+            if (so == 0 && sl0 + k <= NS) {
+              bulk_s2g(dst, smem + (int64_t)sl0 * ob, (uint32_t)(k * ob));
+            } else {
+              for (int j = 0; j < k; ++j) {
+                const uint8_t* src;
+                if (j >= so) src = smem + (int64_t)((p0 + j) % NS) * ob;
+                else src = D.pad_mode == RPL_PAD_ZERO ? zrow : smem + (int64_t)((p0 + so) % NS) * ob;
+                bulk_s2g(dst + j * ob, src, (uint32_t)ob);
+              }
+            }
+          }
+          bulk_commit();
+          // frames released once this row's store has read them: all positions < F+m+1,
+          // and at the end of the piece its whole window
+          rel_hist[c & 63] = (int)(ok ? (m == R - 1 ? F + R + k - 1 : F + m + 1) : F);
+          bulk_wait_read_G<PIPE_G>();
+          if (c >= PIPE_G) free_count = rel_hist[(c - PIPE_G) & 63];
+        }
+        if (ok) F += R + k - 1;
+        g += R;
+      }
+      bulk_wait_all();
+      free_count = 0x7fffffff;
+    }
+  } else {
+    // ---------------- per-row fields, stored state, IS weights (warps 2-3) ----------------
+    const int t2 = tid - 64;
+    for (int c = t2; c < nrows; c += PIPE_THREADS - 64) {
+      const int64_t gg = g0 + c;
+      const int64_t s = gg / L;
+      const int tau = (int)(gg - s * L);
+      const int64_t leaf = idx[s];
+      if (leaf < 0 || leaf >= nblk * D.B) continue;
+      const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
+      const int64_t row = wrap(blk * D.period + tau, D.cap_T);
+      const int64_t prow = wrap(blk * D.period + tau - 1, D.cap_T);
+      const uint8_t pd = __ldg(D.done + prow * D.B + b);
+      const int64_t o = (int64_t)tau * n + s;
+      if (D.o_act) coop_copy(D.o_act + o * D.act_bytes, D.act + (row * D.B + b) * D.act_bytes, D.act_bytes, 0, 1);
+      if (D.o_prev_act) {
+        if (pd) coop_zero(D.o_prev_act + o * D.act_bytes, D.act_bytes, 0, 1);
+        else coop_copy(D.o_prev_act + o * D.act_bytes, D.act + (prow * D.B + b) * D.act_bytes, D.act_bytes, 0, 1);
+      }
+      if (D.o_rew) D.o_rew[o] = __ldg(D.rew + row * D.B + b);
+      if (D.o_prev_rew) D.o_prev_rew[o] = pd ? 0.0f : __ldg(D.rew + prow * D.B + b);
+      if (D.o_done) D.o_done[o] = __ldg(D.done + row * D.B + b);
+      if (tau == 0 && D.o_w && q && qmin) {
+        const int64_t qs = q[s];
+        D.o_w[s] = qs > 0 ? (float)pow((double)(*qmin) / (double)qs, beta) : 0.0f;
+      }
+    }
+    // stored recurrent state for samples whose row 0 lies in this CTA
+    if (D.o_rnn) {
+      for (int64_t s = (g0 + L - 1) / L; s * L < g1; ++s) {
+        const int64_t leaf = idx[s];
+        if (leaf < 0 || leaf >= nblk * D.B) continue;
+        const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
+        for (int p = 0; p < D.rnn_parts; ++p)
+          coop_copy(D.o_rnn + (p * n + s) * D.rnn_bytes, D.rnn + ((blk * D.B + b) * D.rnn_parts + p) * D.rnn_bytes,
+                    D.rnn_bytes, t2, PIPE_THREADS - 64);
+      }
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Sequences, frame-centric LSU variant (stacked output): one warp per unique
+// frame (sample s, window row w in [-(k-1), L-1]).  The warp loads the frame
+// once into registers (16-B vector loads, several in flight per lane) and stores
+// it to every stack slot whose source it is: stack tau in [w, w+k-1] takes it at
+// slot w-(tau-k+1) when w >= s(tau), and at the padded slots below when w is the
+// episode start s(tau) (repeat mode; zero mode writes zeros there instead).
+// Each frame is read from L2/HBM once; every output byte is written once.
+// ---------------------------------------------------------------------------
+constexpr int FC_WARPS = 4;
+constexpr int FC_MAX_V4 = 16;  // 16 x 32 lanes x 16 B = 8 KB per warp pass
+
+__device__ __forceinline__ int seq_start(const GDesc& D, int64_t row0, int64_t b, int tau, int k) {
+  // s(tau) - (tau-k+1) in [0, k-1]: latest row in (tau-k+1, tau] whose previous row ended an episode
+  for (int j = k - 1; j >= 1; --j)
+    if (__ldg(D.done + wrap(row0 + tau - (k - 1) + j - 1, D.cap_T) * D.B + b)) return j;
+  return 0;
+}
+
+__global__ void __launch_bounds__(FC_WARPS * 32)
+k_gather_seq_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, const int64_t* __restrict__ q,
+                 const int64_t* __restrict__ qmin, double beta, int32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const int k = D.k, L = D.seq_len;
+  const int W = L + k - 1;  // unique frames per sample
+  const int64_t task = (int64_t)blockIdx.x * FC_WARPS + (threadIdx.x >> 5);
+  if (task >= n * W) return;
+  const int64_t s = task / W;
+  const int w = (int)(task - s * W) - (k - 1);  // window row, -(k-1) .. L-1
+  const int64_t leaf = idx[s];
+  const int64_t nblk = D.cap_T / D.period;
+  if (leaf < 0) return;
+  if (leaf >= nblk * D.B) {
+    if (lane == 0 && w == 0) set_err(err, RPL_DERR_IDX);
+    return;
+  }
+  const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
+  const int64_t row0 = blk * D.period;
+  const int64_t ob = D.obs_bytes;
+  const int4* src = reinterpret_cast<const int4*>(D.obs + (wrap(row0 + w, D.cap_T) * D.B + b) * ob);
+  const int nv = (int)(ob / 16);
+  // destinations: lane j < k*k enumerates (stack tau = w + t, slot) pairs
+  // stack tau = w + t (t = 0..k-1) uses this frame at natural slot k-1-t if w >= s(tau);
+  // padded slots 0..(s(tau)-(tau-k+1))-1 take the start frame when w == s(tau).
+  uint32_t natural = 0, padrep = 0, padzero = 0;  // bit t: stack w+t
+  int padcnt[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) padcnt[t] = 0;
+  if (lane == 0 && w == 0 && D.o_w && q && qmin) {
+    const int64_t qs = q[s];
+    D.o_w[s] = qs > 0 ? (float)pow((double)(*qmin) / (double)qs, beta) : 0.0f;
+  }
+  for (int t = 0; t < k; ++t) {
+    const int tau = w + t;
+    if (tau < 0 || tau >= L) continue;
+    const int so = seq_start(D, row0, b, tau, k);  // s(tau) = tau-k+1+so
+    const int stw = tau - k + 1 + so;
+    if (w >= stw) natural |= 1u << t;
+    if (so > 0 && w == stw) {
+      padcnt[t] = so;
+      if (D.pad_mode == RPL_PAD_ZERO) padzero |= 1u << t;
+      else padrep |= 1u << t;
+    }
+  }
+  if (!(natural | padrep | padzero)) return;
+  for (int base = 0; base < nv; base += 32 * FC_MAX_V4) {
+    int4 v[FC_MAX_V4];
+#pragma unroll
+    for (int u = 0; u < FC_MAX_V4; ++u) {
+      const int i = base + u * 32 + lane;
+      if (i < nv) v[u] = __ldg(src + i);
+    }
+    for (int t = 0; t < k; ++t) {
+      const int tau = w + t;
+      if (tau < 0 || tau >= L) continue;
+      int4* stack = reinterpret_cast<int4*>(D.o_obs + (((int64_t)tau * n + s) * k) * ob);
+      if (natural & (1u << t)) {
+        int4* dst = stack + (int64_t)(k - 1 - t) * (ob / 16);
+#pragma unroll
+        for (int u = 0; u < FC_MAX_V4; ++u) {
+          const int i = base + u * 32 + lane;
+          if (i < nv) dst[i] = v[u];
+        }
+      }
+      if ((padrep | padzero) & (1u << t)) {
+        for (int j = 0; j < padcnt[t]; ++j) {
+          int4* dst = stack + (int64_t)j * (ob / 16);
+#pragma unroll
+          for (int u = 0; u < FC_MAX_V4; ++u) {
+            const int i = base + u * 32 + lane;
+            if (i < nv) dst[i] = (padzero & (1u << t)) ? make_int4(0, 0, 0, 0) : v[u];
+          }
+        }
+      }
+    }
+  }
+}
+
+// per-row fields + stored state for the LSU variant (one thread per output row)
+__global__ void k_gather_seq_fields(GDesc D, const int64_t* __restrict__ idx, int64_t n, int32_t* err) {
+  const int L = D.seq_len;
+  const int64_t nblk = D.cap_T / D.period;
+  for (int64_t gg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gg < n * L; gg += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = gg / L;
+    const int tau = (int)(gg - s * L);
+    const int64_t leaf = idx[s];
+    if (leaf < 0 || leaf >= nblk * D.B) continue;
+    const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
+    const int64_t row = wrap(blk * D.period + tau, D.cap_T);
+    const int64_t prow = wrap(blk * D.period + tau - 1, D.cap_T);
+    const uint8_t pd = __ldg(D.done + prow * D.B + b);
+    const int64_t o = (int64_t)tau * n + s;
+    if (D.o_act) coop_copy(D.o_act + o * D.act_bytes, D.act + (row * D.B + b) * D.act_bytes, D.act_bytes, 0, 1);
+    if (D.o_prev_act) {
+      if (pd) coop_zero(D.o_prev_act + o * D.act_bytes, D.act_bytes, 0, 1);
+      else coop_copy(D.o_prev_act + o * D.act_bytes, D.act + (prow * D.B + b) * D.act_bytes, D.act_bytes, 0, 1);
+    }
+    if (D.o_rew) D.o_rew[o] = __ldg(D.rew + row * D.B + b);
+    if (D.o_prev_rew) D.o_prev_rew[o] = pd ? 0.0f : __ldg(D.rew + prow * D.B + b);
+    if (D.o_done) D.o_done[o] = __ldg(D.done + row * D.B + b);
+    if (tau == 0) {
+      const int64_t age = wrap(D.cursor - 1 - blk * D.period, D.cap_T);
+      const int hist = D.k - 1 > 1 ? D.k - 1 : 1;
+      if (!(age >= L - 1 && age + hist <= D.size - 1)) set_err(err, RPL_DERR_INVALID_LEAF);
+      if (D.o_rnn)
+        for (int p = 0; p < D.rnn_parts; ++p)
+          coop_copy(D.o_rnn + (p * n + s) * D.rnn_bytes, D.rnn + ((blk * D.B + b) * D.rnn_parts + p) * D.rnn_bytes,
+                    D.rnn_bytes, 0, 1);
+    }
+  }
+}
+
 GDesc to_dev(const rpl_gather_desc* d) {
   GDesc g;
   g.kind = d->kind;
@@ -456,10 +788,18 @@ GDesc to_dev(const rpl_gather_desc* d) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+int g_seq_variant = 0;  // 0: persistent TMA pipeline (default), 1: chunked TMA kernel, 2: frame-centric LSU
+
 }  // namespace
 }  // namespace rpl
 
 using namespace rpl;
+
+extern "C" int rpl_debug_set_gather_variant(int32_t variant) {
+  if (variant < 0 || variant > 2) return RPL_EINVAL;
+  g_seq_variant = variant;
+  return RPL_OK;
+}
 
 extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q, const int64_t* qmin,
                           double beta, int64_t n, int32_t* dev_err, void* stream) {
@@ -498,6 +838,52 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
     if ((desc->o_rew || desc->o_prev_rew) && !desc->rew) return RPL_EINVAL;
     if (desc->out_mode != RPL_OUT_STACKED && desc->out_mode != RPL_OUT_UNIQUE) return RPL_EINVAL;
     if (SEQ_CHUNK + desc->k > 32) return RPL_EINVAL;
+    if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs && g_seq_variant == 2 &&
+        desc->obs_bytes <= 16 * 32 * FC_MAX_V4 * 4) {
+      const int64_t tasks = n * (int64_t)(desc->seq_len + desc->k - 1);
+      k_gather_seq_lsu<<<(unsigned)((tasks + FC_WARPS - 1) / FC_WARPS), FC_WARPS * 32, 0, st>>>(g, idx, n, q, qmin,
+                                                                                               beta, dev_err);
+      int r = launch_status();
+      if (r != RPL_OK) return r;
+      const int64_t rows = n * (int64_t)desc->seq_len;
+      k_gather_seq_fields<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(g, idx, n, dev_err);
+      return launch_status();
+    }
+    if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs && g_seq_variant == 0) {
+      // persistent TMA pipeline: NS frame slots (+1 zero slot); CTAs_per_SM CTAs per SM
+      // Slots the consumer may need beyond the released ones: G+1 rows of advance, the
+      // k-1 window, and k-1 per piece boundary crossed.  With L > G at most two boundaries
+      // fall in G+1 consecutive rows (a CTA's short first and last pieces): NS >= G + 3k - 2.
+      // Otherwise every row may open a piece: NS >= (G+1) k + k.
+      int NS = (int)(216 * 1024 / desc->obs_bytes) - 1;
+      if (NS > PIPE_MAX_NS) NS = PIPE_MAX_NS;
+      const int k = desc->k, L = desc->seq_len;
+      int G = 0;
+      if (L > 16 && NS >= 16 + 3 * k - 2) G = 16;
+      else if (NS >= 5 * k + k) G = 4;
+      if (G > 0) {
+        const size_t dyn = (size_t)(NS + 1) * desc->obs_bytes;
+        static size_t set_p = 0;
+        if (dyn > 48 * 1024 && dyn > set_p) {
+          cudaFuncSetAttribute(k_gather_seq_pipe<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+          cudaFuncSetAttribute(k_gather_seq_pipe<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+          set_p = dyn;
+        }
+        const int64_t total = n * (int64_t)desc->seq_len;
+        int64_t grid = (int64_t)sm_count();
+        int64_t rows_per_cta = (total + grid - 1) / grid;
+        if (rows_per_cta > PIPE_MAX_ROWS) rows_per_cta = PIPE_MAX_ROWS;
+        grid = (total + rows_per_cta - 1) / rows_per_cta;
+        g.use_tma = 1;
+        if (G == 16)
+          k_gather_seq_pipe<16><<<(unsigned)grid, PIPE_THREADS, dyn, st>>>(g, idx, n, NS, rows_per_cta, q, qmin,
+                                                                             beta, dev_err);
+        else
+          k_gather_seq_pipe<4><<<(unsigned)grid, PIPE_THREADS, dyn, st>>>(g, idx, n, NS, rows_per_cta, q, qmin,
+                                                                            beta, dev_err);
+        return launch_status();
+      }
+    }
     const int64_t smem = (int64_t)(SEQ_CHUNK + desc->k) * desc->obs_bytes;
     g.use_tma = (tma_ok && smem <= 200 * 1024) ? 1 : 0;
     const size_t dyn = g.use_tma ? (size_t)smem : 0;

@@ -104,9 +104,16 @@ def test_transition_fused_is_weights(rpl):
     check_rel(H(out["w"]), ref, what="fused w")
 
 
+@pytest.fixture(params=[0, 1, 2], ids=["pipe", "chunk", "lsu"])
+def variant(rpl, request):
+    assert rpl._lib.lib.rpl_debug_set_gather_variant(request.param) == 0
+    yield request.param
+    rpl._lib.lib.rpl_debug_set_gather_variant(0)
+
+
 @pytest.mark.parametrize("out_mode", [0, 1])
 @pytest.mark.parametrize("pad_mode", [0, 1])
-def test_sequences(rpl, out_mode, pad_mode):
+def test_sequences(rpl, out_mode, pad_mode, variant):
     import torch
     period, L, k = 40, 125, 4
     ring = make_ring(31 + out_mode, cap=400, B=4, ep_len=30.0, period=period, rnn_h=64, reward_kind="r2d2")
@@ -154,3 +161,31 @@ def test_sequence_then_nstep_target(rpl):
     assert y.shape == (80, 16)
     check_rel(H(y), yr, np.abs(yr) + 1e-3, what="r2d2 targets")
     assert np.array_equal(H(dn), dnr)
+
+
+@pytest.mark.parametrize("L,k,n_s", [(1, 4, 7), (2, 4, 300), (5, 4, 33), (40, 1, 50), (47, 2, 190), (125, 4, 64),
+                                     (120, 8, 20)])
+def test_sequence_shapes(rpl, L, k, n_s, variant):
+    # degenerate and ragged lengths exercise the pipeline's piece logic (rows split
+    # across CTAs, short pieces, ring-slot wrap) and every stack depth
+    import torch
+    period = 40
+    ring = make_ring(50 + L + k, cap=400, B=3, ep_len=7.0, period=period, rnn_h=8, reward_kind="r2d2",
+                     obs_shape=(16, 24))
+    dr = dev_ring(rpl, ring)
+    g = rng(L * 31 + k)
+    nblk = 400 // period
+    idx = []
+    while len(idx) < n_s:
+        blk, b = int(g.integers(0, nblk)), int(g.integers(0, 3))
+        if OG.window_valid_sequence(blk * period, 400, ring.cursor, ring.size, k, L):
+            idx.append(blk * 3 + b)
+    idx = np.array(idx, np.int64)
+    idx[len(idx) // 2] = -1  # a skipped sample in the middle
+    out = rpl.gather(dr, T_(idx), kind="sequence", k=k, seq_len=L, period=period)
+    ref = OG.gather_sequences(idx, 3, ring.obs, ring.act, ring.rew, ring.done, ring.rnn, k, L, period)
+    ok = idx >= 0
+    assert np.array_equal(H(out["obs"])[:, ok], ref["obs"][:, ok])
+    for name in ("act", "prev_act", "rew", "prev_rew", "done"):
+        assert np.array_equal(H(out[name])[:, ok], ref[name][:, ok]), name
+    assert np.array_equal(H(out["rnn"])[:, ok], ref["rnn"][:, ok])
