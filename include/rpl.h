@@ -259,9 +259,9 @@ int rpl_gather(const rpl_gather_desc* desc /* host */, const int64_t* idx, const
 int rpl_debug_priority_values(const float* td_abs, int64_t n, double alpha, double eps_p,
                               int32_t force_slow, float* out_v, uint8_t* out_slow, void* stream);
 
-/* Diagnostics (tests only): select the sequence-gather kernel, 0 = persistent TMA pipeline
- * (default), 1 = one CTA per 8-row chunk (TMA), 2 = frame-centric LSU copy.  All produce
- * identical outputs. */
+/* Diagnostics (tests only): select the sequence-gather kernel, 0 = persistent pipeline with
+ * TMA loads and LSU stores (default), 1 = one CTA per 8-row chunk (TMA both ways),
+ * 2 = frame-centric LSU copy, 3 = persistent all-TMA pipeline.  All produce identical outputs. */
 int rpl_debug_set_gather_variant(int32_t variant);
 
 #ifdef __cplusplus

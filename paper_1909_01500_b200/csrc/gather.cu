@@ -748,6 +748,189 @@ __global__ void k_gather_seq_fields(GDesc D, const int64_t* __restrict__ idx, in
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Sequences, persistent pipeline with TMA loads and LSU stores (default).
+// Same row partition and piece structure as k_gather_seq_pipe, but the stores
+// are issued by CONSUMER WARPS as 16-B st.global from shared memory instead of
+// bulk stores: bulk stores and bulk loads share the SM's TMA queue, so in the
+// all-TMA pipeline every frame load waits behind up to G queued 28-KB stores
+// (measured: ~22 GB/s/SM).  Here the TMA engine only streams loads (warp 0,
+// lane 0, one mbarrier per slot) while 7 consumer warps each copy one k-stack
+// (k*7056 B) per row, then flag the row done; the producer refills a slot once
+// the contiguous done-frontier has passed every row that reads it.
+// ---------------------------------------------------------------------------
+constexpr int PL_THREADS = 256;  // warp 0 producer, warps 1..7 consumers
+constexpr int PL_CONSUMERS = PL_THREADS / 32 - 1;
+
+__global__ void __launch_bounds__(PL_THREADS, 1)
+k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, int64_t rows_per_cta,
+                      const int64_t* __restrict__ q, const int64_t* __restrict__ qmin, double beta, int32_t* err) {
+  extern __shared__ __align__(128) uint8_t smem[];  // NS frame slots
+  __shared__ __align__(8) uint64_t full[PIPE_MAX_NS];
+  __shared__ int8_t start_off[PIPE_MAX_ROWS];
+  __shared__ int rel[PIPE_MAX_ROWS];        // frames released when row c (and all before) are done
+  __shared__ int row_first[PIPE_MAX_ROWS];  // frame position of row c's window start (-1: skipped row)
+  __shared__ volatile int row_done[PIPE_MAX_ROWS];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int k = D.k, L = D.seq_len;
+  const int64_t ob = D.obs_bytes;
+  const int nv = (int)(ob / 16);
+  const int64_t total = n * (int64_t)L;
+  const int64_t g0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t g1 = min(total, g0 + rows_per_cta);
+  if (g0 >= g1) return;
+  const int nrows = (int)(g1 - g0);
+  const int64_t nblk = D.cap_T / D.period;
+
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+    // frame positions per row (pieces: runs of rows of one sample)
+    int64_t F = 0;
+    int c = 0;
+    for (int64_t g = g0; g < g1;) {
+      const int64_t s = g / L;
+      const int tau0 = (int)(g - s * L);
+      const int R = (int)min((int64_t)(L - tau0), g1 - g);
+      const int64_t leaf = idx[s];
+      const bool ok = leaf >= 0 && leaf < nblk * D.B;
+      for (int m = 0; m < R; ++m, ++c) {
+        row_first[c] = ok ? (int)(F + m) : -1;
+        rel[c] = (int)(ok ? (m == R - 1 ? F + R + k - 1 : F + m + 1) : F);
+        row_done[c] = 0;
+      }
+      if (ok) F += R + k - 1;
+      g += R;
+    }
+  }
+  for (int c = tid; c < nrows; c += PL_THREADS) {
+    const int64_t g = g0 + c;
+    const int64_t s = g / L;
+    const int tau = (int)(g - s * L);
+    const int64_t leaf = idx[s];
+    int8_t so = 0;
+    if (leaf >= 0 && leaf < nblk * D.B) {
+      const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
+      const int64_t row = blk * D.period + tau;
+      for (int j = k - 1; j >= 1; --j) {
+        if (__ldg(D.done + wrap(row - (k - 1) + j - 1, D.cap_T) * D.B + b)) {
+          so = (int8_t)j;
+          break;
+        }
+      }
+      if (tau == 0) {
+        const int64_t age = wrap(D.cursor - 1 - blk * D.period, D.cap_T);
+        const int hist = k - 1 > 1 ? k - 1 : 1;
+        if (!(age >= L - 1 && age + hist <= D.size - 1)) set_err(err, RPL_DERR_INVALID_LEAF);
+      }
+    } else if (leaf >= nblk * D.B && tau == 0) {
+      set_err(err, RPL_DERR_IDX);
+    }
+    start_off[c] = so;
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- producer: TMA loads only ----------------
+      int frontier = 0;      // rows [0, frontier) are done
+      int released = 0;      // frames < released may be overwritten
+      int64_t i = 0;
+      int c = 0;
+      for (int64_t g = g0; g < g1;) {
+        const int64_t s = g / L;
+        const int tau0 = (int)(g - s * L);
+        const int R = (int)min((int64_t)(L - tau0), g1 - g);
+        const int64_t leaf = idx[s];
+        if (leaf >= 0 && leaf < nblk * D.B) {
+          const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
+          const int64_t first = blk * D.period + tau0 - (k - 1);
+          for (int w = 0; w < R + k - 1; ++w, ++i) {
+            if (i >= NS) {
+              while (released <= i - NS) {
+                if (frontier < nrows && row_done[frontier]) {
+                  released = rel[frontier];
+                  ++frontier;
+                } else {
+                  __nanosleep(32);
+                }
+              }
+              fence_proxy_async();
+            }
+            const int slot = (int)(i % NS);
+            mbar_expect_tx(&full[slot], (uint32_t)ob);
+            bulk_g2s(smem + (int64_t)slot * ob, D.obs + (wrap(first + w, D.cap_T) * D.B + b) * ob, (uint32_t)ob,
+                     &full[slot]);
+          }
+        }
+        c += R;
+        g += R;
+      }
+    }
+  } else {
+    // ---------------- consumers: one k-stack per row, LSU stores ----------------
+    for (int c = warp - 1; c < nrows; c += PL_CONSUMERS) {
+      const int64_t g = g0 + c;
+      const int64_t s = g / L;
+      const int tau = (int)(g - s * L);
+      const int p0 = row_first[c];
+      if (p0 >= 0) {
+        const int so = start_off[c];
+        for (int j = so; j < k; ++j) {
+          const int64_t pos = p0 + j;
+          mbar_wait(&full[pos % NS], (uint32_t)((pos / NS) & 1));
+        }
+        int4* dst = reinterpret_cast<int4*>(D.o_obs + (((int64_t)tau * n + s) * k) * ob);
+        for (int j = 0; j < k; ++j) {
+          int4* d = dst + (int64_t)j * nv;
+          if (j < so && D.pad_mode == RPL_PAD_ZERO) {
+            for (int v = lane; v < nv; v += 32) d[v] = make_int4(0, 0, 0, 0);
+          } else {
+            const int src = j < so ? so : j;
+            const int4* sp = reinterpret_cast<const int4*>(smem + (int64_t)((p0 + src) % NS) * ob);
+#pragma unroll 4
+            for (int v = lane; v < nv; v += 32) d[v] = sp[v];
+          }
+        }
+        // per-row fields
+        if (lane == 0) {
+          const int64_t leaf = idx[s];
+          const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
+          const int64_t row = wrap(blk * D.period + tau, D.cap_T);
+          const int64_t prow = wrap(blk * D.period + tau - 1, D.cap_T);
+          const uint8_t pd = __ldg(D.done + prow * D.B + b);
+          const int64_t o = (int64_t)tau * n + s;
+          if (D.o_act) coop_copy(D.o_act + o * D.act_bytes, D.act + (row * D.B + b) * D.act_bytes, D.act_bytes, 0, 1);
+          if (D.o_prev_act) {
+            if (pd) coop_zero(D.o_prev_act + o * D.act_bytes, D.act_bytes, 0, 1);
+            else coop_copy(D.o_prev_act + o * D.act_bytes, D.act + (prow * D.B + b) * D.act_bytes, D.act_bytes, 0, 1);
+          }
+          if (D.o_rew) D.o_rew[o] = __ldg(D.rew + row * D.B + b);
+          if (D.o_prev_rew) D.o_prev_rew[o] = pd ? 0.0f : __ldg(D.rew + prow * D.B + b);
+          if (D.o_done) D.o_done[o] = __ldg(D.done + row * D.B + b);
+          if (tau == 0 && D.o_w && q && qmin) {
+            const int64_t qs = q[s];
+            D.o_w[s] = qs > 0 ? (float)pow((double)(*qmin) / (double)qs, beta) : 0.0f;
+          }
+        }
+        if (tau == 0 && D.o_rnn) {
+          const int64_t leaf = idx[s];
+          const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
+          for (int p = 0; p < D.rnn_parts; ++p)
+            coop_copy(D.o_rnn + (p * n + s) * D.rnn_bytes, D.rnn + ((blk * D.B + b) * D.rnn_parts + p) * D.rnn_bytes,
+                      D.rnn_bytes, lane, 32);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        fence_proxy_async();
+        row_done[c] = 1;
+      }
+    }
+  }
+}
+
 GDesc to_dev(const rpl_gather_desc* d) {
   GDesc g;
   g.kind = d->kind;
@@ -788,7 +971,9 @@ GDesc to_dev(const rpl_gather_desc* d) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-int g_seq_variant = 0;  // 0: persistent TMA pipeline (default), 1: chunked TMA kernel, 2: frame-centric LSU
+// 0: TMA-load / LSU-store pipeline (default), 1: chunked all-TMA kernel, 2: frame-centric
+// LSU, 3: all-TMA pipeline
+int g_seq_variant = 0;
 
 }  // namespace
 }  // namespace rpl
@@ -796,7 +981,7 @@ int g_seq_variant = 0;  // 0: persistent TMA pipeline (default), 1: chunked TMA 
 using namespace rpl;
 
 extern "C" int rpl_debug_set_gather_variant(int32_t variant) {
-  if (variant < 0 || variant > 2) return RPL_EINVAL;
+  if (variant < 0 || variant > 3) return RPL_EINVAL;
   g_seq_variant = variant;
   return RPL_OK;
 }
@@ -850,6 +1035,31 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       return launch_status();
     }
     if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs && g_seq_variant == 0) {
+      // default: TMA-load / LSU-store pipeline.  The producer runs up to NS frames past the
+      // release point of the done-frontier row f, whose own window starts exactly there, so
+      // NS >= k guarantees progress; more slots let the other consumers run ahead.
+      int NS = (int)(200 * 1024 / desc->obs_bytes);
+      if (NS > PIPE_MAX_NS) NS = PIPE_MAX_NS;
+      const int k = desc->k;
+      if (NS >= 2 * k) {
+        const size_t dyn = (size_t)NS * desc->obs_bytes;
+        static size_t set_l = 0;
+        if (dyn > 48 * 1024 && dyn > set_l) {
+          cudaFuncSetAttribute(k_gather_seq_pipe_lsu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+          set_l = dyn;
+        }
+        const int64_t total = n * (int64_t)desc->seq_len;
+        int64_t grid = (int64_t)sm_count();
+        int64_t rows_per_cta = (total + grid - 1) / grid;
+        if (rows_per_cta > PIPE_MAX_ROWS) rows_per_cta = PIPE_MAX_ROWS;
+        grid = (total + rows_per_cta - 1) / rows_per_cta;
+        g.use_tma = 1;
+        k_gather_seq_pipe_lsu<<<(unsigned)grid, PL_THREADS, dyn, st>>>(g, idx, n, NS, rows_per_cta, q, qmin, beta,
+                                                                        dev_err);
+        return launch_status();
+      }
+    }
+    if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs && (g_seq_variant == 3 || g_seq_variant == 0)) {
       // persistent TMA pipeline: NS frame slots (+1 zero slot); CTAs_per_SM CTAs per SM
       // Slots the consumer may need beyond the released ones: G+1 rows of advance, the
       // k-1 window, and k-1 per piece boundary crossed.  With L > G at most two boundaries

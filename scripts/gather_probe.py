@@ -15,15 +15,15 @@ from synth.device import make_ring_device  # noqa: E402
 dev = torch.device("cuda:0")
 res = {}
 FR = 7056
-for cap, B in [(200, 64), (800, 256), (4000, 256)]:
+for cap, B in [(4000, 256), (1024000, 1)]:
     ring = make_ring_device(1, cap, B, dev, period=40, rnn_h=512, cursor=17)
     blocks = R.valid_sequence_blocks(cap, 40, ring.cursor, ring.size, 4, 125)
     leaves = R.leaves_of(blocks, B)
     g = np.random.default_rng(0)
-    for variant in (0, 1, 2):
+    for variant in (0, 1):
         rpl._lib.lib.rpl_debug_set_gather_variant(variant)
         for mode in ("stacked", "unique"):
-            if mode == "unique" and variant != 0:
+            if mode == "unique" and variant != 1:
                 continue
             plan = rpl.GatherPlan(ring, 64, kind="sequence", k=4, seq_len=125, period=40,
                                   out_mode=0 if mode == "stacked" else 1)
