@@ -755,15 +755,20 @@ __global__ void k_gather_seq_fields(GDesc D, const int64_t* __restrict__ idx, in
 // are issued by CONSUMER WARPS as 16-B st.global from shared memory instead of
 // bulk stores: bulk stores and bulk loads share the SM's TMA queue, so in the
 // all-TMA pipeline every frame load waits behind up to G queued 28-KB stores
-// (measured: ~22 GB/s/SM).  Here the TMA engine only streams loads (warp 0,
-// lane 0, one mbarrier per slot) while 7 consumer warps each copy one k-stack
-// (k*7056 B) per row, then flag the row done; the producer refills a slot once
-// the contiguous done-frontier has passed every row that reads it.
+// (measured: ~22 GB/s/SM).  Roles:
+//   warp 0, lane 0   producer: TMA bulk loads of each piece's unique frames
+//                    into NS slots (one mbarrier per slot); refills a slot once
+//                    the contiguous done-frontier has passed every row reading it;
+//   warp 1           meta: episode-start offsets of every row (lane per row, all
+//                    done-flag loads in flight at once), then the per-row fields,
+//                    IS weights and stored recurrent state — the latency-bound
+//                    scattered loads never sit on a consumer's critical path
+//                    (ncu r1: they were ~20% of the consumers' stall samples);
+//   warps 2..NC+1    consumers: one k-stack (k*7056 B) per row, LDS.128 ->
+//                    STG.128, then flag the row done.
 // ---------------------------------------------------------------------------
-constexpr int PL_THREADS = 256;  // warp 0 producer, warps 1..7 consumers
-constexpr int PL_CONSUMERS = PL_THREADS / 32 - 1;
-
-__global__ void __launch_bounds__(PL_THREADS, 1)
+template <int NC>
+__global__ void __launch_bounds__((NC + 2) * 32, 1)
 k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, int64_t rows_per_cta,
                       const int64_t* __restrict__ q, const int64_t* __restrict__ qmin, double beta, int32_t* err) {
   extern __shared__ __align__(128) uint8_t smem[];  // NS frame slots
@@ -772,6 +777,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   __shared__ int rel[PIPE_MAX_ROWS];        // frames released when row c (and all before) are done
   __shared__ int row_first[PIPE_MAX_ROWS];  // frame position of row c's window start (-1: skipped row)
   __shared__ volatile int row_done[PIPE_MAX_ROWS];
+  constexpr int NT = (NC + 2) * 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k = D.k, L = D.seq_len;
   const int64_t ob = D.obs_bytes;
@@ -798,37 +804,12 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       for (int m = 0; m < R; ++m, ++c) {
         row_first[c] = ok ? (int)(F + m) : -1;
         rel[c] = (int)(ok ? (m == R - 1 ? F + R + k - 1 : F + m + 1) : F);
-        row_done[c] = 0;
       }
       if (ok) F += R + k - 1;
       g += R;
     }
   }
-  for (int c = tid; c < nrows; c += PL_THREADS) {
-    const int64_t g = g0 + c;
-    const int64_t s = g / L;
-    const int tau = (int)(g - s * L);
-    const int64_t leaf = idx[s];
-    int8_t so = 0;
-    if (leaf >= 0 && leaf < nblk * D.B) {
-      const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
-      const int64_t row = blk * D.period + tau;
-      for (int j = k - 1; j >= 1; --j) {
-        if (__ldg(D.done + wrap(row - (k - 1) + j - 1, D.cap_T) * D.B + b)) {
-          so = (int8_t)j;
-          break;
-        }
-      }
-      if (tau == 0) {
-        const int64_t age = wrap(D.cursor - 1 - blk * D.period, D.cap_T);
-        const int hist = k - 1 > 1 ? k - 1 : 1;
-        if (!(age >= L - 1 && age + hist <= D.size - 1)) set_err(err, RPL_DERR_INVALID_LEAF);
-      }
-    } else if (leaf >= nblk * D.B && tau == 0) {
-      set_err(err, RPL_DERR_IDX);
-    }
-    start_off[c] = so;
-  }
+  for (int c = tid; c < nrows; c += NT) row_done[c] = 0;
   __syncthreads();
 
   if (warp == 0) {
@@ -837,7 +818,6 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       int frontier = 0;      // rows [0, frontier) are done
       int released = 0;      // frames < released may be overwritten
       int64_t i = 0;
-      int c = 0;
       for (int64_t g = g0; g < g1;) {
         const int64_t s = g / L;
         const int tau0 = (int)(g - s * L);
@@ -864,13 +844,97 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
                      &full[slot]);
           }
         }
-        c += R;
         g += R;
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- meta warp ----------------
+    // (1) episode-start offsets: every lane owns rows lane, lane+32, ...; the k-1
+    //     done flags of a row are loaded together before any is inspected.
+    for (int c = lane; c < nrows; c += 32) {
+      const int64_t g = g0 + c;
+      const int64_t s = g / L;
+      const int tau = (int)(g - s * L);
+      const int64_t leaf = idx[s];
+      int8_t so = 0;
+      if (leaf >= 0 && leaf < nblk * D.B) {
+        const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
+        const int64_t row = blk * D.period + tau;
+        uint8_t dw[8];
+#pragma unroll
+        for (int j = 1; j < 8; ++j)
+          dw[j] = j < k ? __ldg(D.done + wrap(row - (k - 1) + j - 1, D.cap_T) * D.B + b) : (uint8_t)0;
+#pragma unroll
+        for (int j = 1; j < 8; ++j)
+          if (dw[j]) so = (int8_t)j;  // latest episode start in the window wins
+        if (tau == 0) {
+          const int64_t age = wrap(D.cursor - 1 - blk * D.period, D.cap_T);
+          const int hist = k - 1 > 1 ? k - 1 : 1;
+          if (!(age >= L - 1 && age + hist <= D.size - 1)) set_err(err, RPL_DERR_INVALID_LEAF);
+        }
+      } else if (leaf >= nblk * D.B && tau == 0) {
+        set_err(err, RPL_DERR_IDX);
+      }
+      start_off[c] = so;
+    }
+    __threadfence_block();
+    asm volatile("bar.arrive 1, %0;" ::"n"((NC + 1) * 32) : "memory");
+    // (2) per-row fields: act, prev_act, rew, prev_rew, done, IS weight
+    const int64_t ab = D.act_bytes;
+    for (int c = lane; c < nrows; c += 32) {
+      if (row_first[c] < 0) continue;
+      const int64_t g = g0 + c;
+      const int64_t s = g / L;
+      const int tau = (int)(g - s * L);
+      const int64_t leaf = idx[s];
+      const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
+      const int64_t row = wrap(blk * D.period + tau, D.cap_T);
+      const int64_t prow = wrap(blk * D.period + tau - 1, D.cap_T);
+      const int64_t e = row * D.B + b, pe = prow * D.B + b;
+      const uint8_t pd = __ldg(D.done + pe);
+      const uint8_t dd = __ldg(D.done + e);
+      const float rw = D.o_rew ? __ldg(D.rew + e) : 0.0f;
+      const float prw = D.o_prev_rew ? __ldg(D.rew + pe) : 0.0f;
+      const int64_t o = (int64_t)tau * n + s;
+      if (ab == 8 && ((reinterpret_cast<uintptr_t>(D.act) | reinterpret_cast<uintptr_t>(D.o_act) |
+                       reinterpret_cast<uintptr_t>(D.o_prev_act)) & 7) == 0) {
+        const uint64_t* a = reinterpret_cast<const uint64_t*>(D.act);
+        const uint64_t av = D.o_act ? __ldg(a + e) : 0ull;
+        const uint64_t pav = D.o_prev_act ? __ldg(a + pe) : 0ull;
+        if (D.o_act) reinterpret_cast<uint64_t*>(D.o_act)[o] = av;
+        if (D.o_prev_act) reinterpret_cast<uint64_t*>(D.o_prev_act)[o] = pd ? 0ull : pav;
+      } else {
+        if (D.o_act) coop_copy(D.o_act + o * ab, D.act + e * ab, ab, 0, 1);
+        if (D.o_prev_act) {
+          if (pd) coop_zero(D.o_prev_act + o * ab, ab, 0, 1);
+          else coop_copy(D.o_prev_act + o * ab, D.act + pe * ab, ab, 0, 1);
+        }
+      }
+      if (D.o_rew) D.o_rew[o] = rw;
+      if (D.o_prev_rew) D.o_prev_rew[o] = pd ? 0.0f : prw;
+      if (D.o_done) D.o_done[o] = dd;
+      if (tau == 0 && D.o_w && q && qmin) {
+        const int64_t qs = q[s];
+        D.o_w[s] = qs > 0 ? (float)pow((double)(*qmin) / (double)qs, beta) : 0.0f;
+      }
+    }
+    // (3) stored recurrent state of every sample whose first row lives here
+    if (D.o_rnn) {
+      for (int c = 0; c < nrows; ++c) {
+        const int64_t g = g0 + c;
+        const int64_t s = g / L;
+        if (g != s * L || row_first[c] < 0) continue;
+        const int64_t leaf = idx[s];
+        const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
+        for (int p = 0; p < D.rnn_parts; ++p)
+          coop_copy(D.o_rnn + (p * n + s) * D.rnn_bytes, D.rnn + ((blk * D.B + b) * D.rnn_parts + p) * D.rnn_bytes,
+                    D.rnn_bytes, lane, 32);
       }
     }
   } else {
     // ---------------- consumers: one k-stack per row, LSU stores ----------------
-    for (int c = warp - 1; c < nrows; c += PL_CONSUMERS) {
+    asm volatile("bar.sync 1, %0;" ::"n"((NC + 1) * 32) : "memory");
+    for (int c = warp - 2; c < nrows; c += NC) {
       const int64_t g = g0 + c;
       const int64_t s = g / L;
       const int tau = (int)(g - s * L);
@@ -892,34 +956,6 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
 #pragma unroll 4
             for (int v = lane; v < nv; v += 32) d[v] = sp[v];
           }
-        }
-        // per-row fields
-        if (lane == 0) {
-          const int64_t leaf = idx[s];
-          const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
-          const int64_t row = wrap(blk * D.period + tau, D.cap_T);
-          const int64_t prow = wrap(blk * D.period + tau - 1, D.cap_T);
-          const uint8_t pd = __ldg(D.done + prow * D.B + b);
-          const int64_t o = (int64_t)tau * n + s;
-          if (D.o_act) coop_copy(D.o_act + o * D.act_bytes, D.act + (row * D.B + b) * D.act_bytes, D.act_bytes, 0, 1);
-          if (D.o_prev_act) {
-            if (pd) coop_zero(D.o_prev_act + o * D.act_bytes, D.act_bytes, 0, 1);
-            else coop_copy(D.o_prev_act + o * D.act_bytes, D.act + (prow * D.B + b) * D.act_bytes, D.act_bytes, 0, 1);
-          }
-          if (D.o_rew) D.o_rew[o] = __ldg(D.rew + row * D.B + b);
-          if (D.o_prev_rew) D.o_prev_rew[o] = pd ? 0.0f : __ldg(D.rew + prow * D.B + b);
-          if (D.o_done) D.o_done[o] = __ldg(D.done + row * D.B + b);
-          if (tau == 0 && D.o_w && q && qmin) {
-            const int64_t qs = q[s];
-            D.o_w[s] = qs > 0 ? (float)pow((double)(*qmin) / (double)qs, beta) : 0.0f;
-          }
-        }
-        if (tau == 0 && D.o_rnn) {
-          const int64_t leaf = idx[s];
-          const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
-          for (int p = 0; p < D.rnn_parts; ++p)
-            coop_copy(D.o_rnn + (p * n + s) * D.rnn_bytes, D.rnn + ((blk * D.B + b) * D.rnn_parts + p) * D.rnn_bytes,
-                      D.rnn_bytes, lane, 32);
         }
       }
       __syncwarp();
@@ -971,7 +1007,20 @@ GDesc to_dev(const rpl_gather_desc* d) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// 0: TMA-load / LSU-store pipeline (default), 1: chunked all-TMA kernel, 2: frame-centric
+template <int NC>
+int launch_seq_lsu(const GDesc& g, const int64_t* idx, int64_t n, int NS, int64_t rows_per_cta, const int64_t* q,
+                   const int64_t* qmin, double beta, int32_t* dev_err, size_t dyn, int64_t grid, cudaStream_t st) {
+  static size_t set_l = 0;
+  if (dyn > 48 * 1024 && dyn > set_l) {
+    cudaFuncSetAttribute(k_gather_seq_pipe_lsu<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    set_l = dyn;
+  }
+  k_gather_seq_pipe_lsu<NC><<<(unsigned)grid, (NC + 2) * 32, dyn, st>>>(g, idx, n, NS, rows_per_cta, q, qmin, beta,
+                                                                         dev_err);
+  return launch_status();
+}
+
+// 0: TMA-load / LSU-store pipeline (default, 8 consumer warps; 4: 14, 5: 4), 1: chunked all-TMA kernel, 2: frame-centric
 // LSU, 3: all-TMA pipeline
 int g_seq_variant = 0;
 
@@ -981,7 +1030,7 @@ int g_seq_variant = 0;
 using namespace rpl;
 
 extern "C" int rpl_debug_set_gather_variant(int32_t variant) {
-  if (variant < 0 || variant > 3) return RPL_EINVAL;
+  if (variant < 0 || variant > 5) return RPL_EINVAL;
   g_seq_variant = variant;
   return RPL_OK;
 }
@@ -1034,7 +1083,8 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       k_gather_seq_fields<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(g, idx, n, dev_err);
       return launch_status();
     }
-    if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs && g_seq_variant == 0) {
+    if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs &&
+        (g_seq_variant == 0 || g_seq_variant == 4 || g_seq_variant == 5)) {
       // default: TMA-load / LSU-store pipeline.  The producer runs up to NS frames past the
       // release point of the done-frontier row f, whose own window starts exactly there, so
       // NS >= k guarantees progress; more slots let the other consumers run ahead.
@@ -1043,20 +1093,18 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       const int k = desc->k;
       if (NS >= 2 * k) {
         const size_t dyn = (size_t)NS * desc->obs_bytes;
-        static size_t set_l = 0;
-        if (dyn > 48 * 1024 && dyn > set_l) {
-          cudaFuncSetAttribute(k_gather_seq_pipe_lsu, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-          set_l = dyn;
-        }
         const int64_t total = n * (int64_t)desc->seq_len;
         int64_t grid = (int64_t)sm_count();
         int64_t rows_per_cta = (total + grid - 1) / grid;
         if (rows_per_cta > PIPE_MAX_ROWS) rows_per_cta = PIPE_MAX_ROWS;
         grid = (total + rows_per_cta - 1) / rows_per_cta;
         g.use_tma = 1;
-        k_gather_seq_pipe_lsu<<<(unsigned)grid, PL_THREADS, dyn, st>>>(g, idx, n, NS, rows_per_cta, q, qmin, beta,
-                                                                        dev_err);
-        return launch_status();
+        // consumer warps: 8 (default), 14 (variant 4), 4 (variant 5)
+        if (g_seq_variant == 4) return launch_seq_lsu<14>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn,
+                                                          grid, st);
+        if (g_seq_variant == 5) return launch_seq_lsu<4>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn,
+                                                         grid, st);
+        return launch_seq_lsu<8>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn, grid, st);
       }
     }
     if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs && (g_seq_variant == 3 || g_seq_variant == 0)) {

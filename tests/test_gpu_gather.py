@@ -104,7 +104,7 @@ def test_transition_fused_is_weights(rpl):
     check_rel(H(out["w"]), ref, what="fused w")
 
 
-@pytest.fixture(params=[0, 1, 2, 3], ids=["pipe", "chunk", "lsu", "tmapipe"])
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5], ids=["pipe", "chunk", "lsu", "tmapipe", "pipe14", "pipe4"])
 def variant(rpl, request):
     assert rpl._lib.lib.rpl_debug_set_gather_variant(request.param) == 0
     yield request.param
@@ -189,3 +189,78 @@ def test_sequence_shapes(rpl, L, k, n_s, variant):
     for name in ("act", "prev_act", "rew", "prev_rew", "done"):
         assert np.array_equal(H(out[name])[:, ok], ref[name][:, ok]), name
     assert np.array_equal(H(out["rnn"])[:, ok], ref["rnn"][:, ok])
+
+
+def _column_ring(dr, b, with_rnn):
+    """Host copy of ring column b (all rows) as a [cap_T, 1] ring for the oracle."""
+    obs = H(dr.obs[:, b:b + 1])
+    rnn = H(dr.rnn[:, b:b + 1]) if with_rnn else None
+    return obs, H(dr.act[:, b:b + 1]), H(dr.rew[:, b:b + 1]), H(dr.done[:, b:b + 1]), rnn
+
+
+def test_r2d2_full_size_sampled(rpl):
+    # BASELINE configs[4] in bench.py's launch configuration: [4000, 256] ring (7.2 GB),
+    # 64 sequences x 125 rows, k=4, stored (h, c) 512 — sampled sequences vs the oracle
+    import torch
+    from paper_1909_01500_b200 import replay as R
+    from synth.device import make_ring_device
+    dev = torch.device("cuda")
+    cap, B, period, L, k = 4000, 256, 40, 125, 4
+    dr = make_ring_device(2019, cap, B, dev, ep_len=2000.0, period=period, rnn_h=512, cursor=1234)
+    blocks = R.valid_sequence_blocks(cap, period, dr.cursor, dr.size, k, L)
+    g = rng(11)
+    leaves = g.choice(R.leaves_of(blocks, B), 64).astype(np.int64)
+    # the oldest and the newest valid blocks (ring wrap around the cursor)
+    age = (dr.cursor - 1 - blocks * period) % cap
+    leaves[5] = int(blocks[np.argmax(age)]) * B + 7
+    leaves[6] = int(blocks[np.argmin(age)]) * B + 255
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    plan = rpl.GatherPlan(dr, 64, kind="sequence", k=k, seq_len=L, period=period)
+    out = plan.run(T_(leaves), err=err)
+    torch.cuda.synchronize()
+    assert int(H(err)[0]) == 0
+    for s in list(range(0, 64, 9)) + [5, 6, 63]:
+        blk, b = divmod(int(leaves[s]), B)
+        obs, act, rew, done, rnn = _column_ring(dr, b, True)
+        ref = OG.gather_sequences(np.array([blk], np.int64), 1, obs, act, rew, done, rnn, k, L, period)
+        assert np.array_equal(H(out["obs"][:, s]), ref["obs"][:, 0]), s
+        for name in ("act", "prev_act", "rew", "prev_rew", "done"):
+            assert np.array_equal(H(out[name][:, s]), ref[name][:, 0]), (name, s)
+        assert np.array_equal(H(out["rnn"][:, s]), ref["rnn"][:, 0]), s
+    del dr
+    torch.cuda.empty_cache()
+
+
+def test_dqn_full_size_sampled(rpl):
+    # BASELINE configs[2]: [4096, 256] frame ring (2^20 transitions, 7.4 GB), batch 512,
+    # k=4, n=3, gamma=0.99 with fused n-step and IS weights — sampled transitions vs the oracle
+    import torch
+    from paper_1909_01500_b200 import replay as R
+    from synth.device import make_ring_device
+    dev = torch.device("cuda")
+    cap, B, k, n = 4096, 256, 4, 3
+    dr = make_ring_device(7, cap, B, dev, ep_len=2000.0, period=64, rnn_h=1, cursor=777)
+    dr.rnn = None
+    rows = R.valid_transition_rows(cap, dr.cursor, dr.size, k, n)
+    g = rng(12)
+    leaves = g.choice(R.leaves_of(rows, B), 512).astype(np.int64)
+    q = g.integers(1 << 20, 1 << 34, 512).astype(np.int64)
+    qmin = np.array([q.min()], np.int64)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    out = rpl.gather(dr, T_(leaves), kind="transition", k=k, n_step=n, gamma=0.99, q=T_(q), qmin=T_(qmin),
+                     beta=0.4, err=err)
+    torch.cuda.synchronize()
+    assert int(H(err)[0]) == 0
+    w_ref = OS.is_weights([int(x) for x in q], int(q.sum()), cap * B, 0.4)
+    check_rel(H(out["w"]), w_ref, what="w")
+    for s in list(range(0, 512, 37)) + [511]:
+        row, b = divmod(int(leaves[s]), B)
+        obs, act, rew, done, _ = _column_ring(dr, b, False)
+        ref = OG.gather_transitions(np.array([row], np.int64), 1, obs, act, rew, done, k, n, 0.99)
+        assert np.array_equal(H(out["obs"][s]), ref["obs"][0]), s
+        assert np.array_equal(H(out["next_obs"][s]), ref["next_obs"][0]), s
+        assert int(H(out["act"][s])) == int(ref["act"][0])
+        assert int(H(out["done_n"][s])) == int(ref["done_n"][0])
+        check_rel(H(out["ret"][s:s + 1]), ref["ret"][:1], np.abs(ref["ret"][:1]) + 1.0, what="ret")
+    del dr
+    torch.cuda.empty_cache()
