@@ -45,6 +45,10 @@ R2D2 = dict(cap_T=4000, B=256, period=40, burn_in=40, train=80, tail=5, k=4, n_s
             alpha=0.9, beta=0.6, batch=64, rnn_h=512, rnn_parts=2, eps=1e-3, eps_p=1e-3, fanout=32)
 R2D2["L"] = R2D2["burn_in"] + R2D2["train"] + R2D2["tail"]
 PPO = dict(T=128, B=4096, gamma=0.99, lam=0.95)
+# DQN/Rainbow Atari (configs[2]) and SAC/TD3 Mujoco (configs[3]) secondary line items
+DQN = dict(cap_T=4096, B=256, k=4, n_step=3, gamma=0.99, alpha=0.6, beta=0.4, eps_p=1e-3, fanout=32,
+           batches=(32, 128, 512))
+MUJOCO = dict(cap_T=65536, B=16, n_step=3, gamma=0.99, batch=256, dims=((17, 6), (376, 17)))
 
 
 def parse():
@@ -337,7 +341,8 @@ def run_rpl(args):
         result["clocks"] = clk
         result["e2e"] = e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K_eff, world)
     if world == 1 and not args.no_secondary and not args.profile:
-        result["secondary"] = {"ppo_returns": bench_ppo(dev, rpl)}
+        result["secondary"] = {"ppo_returns": bench_ppo(dev, rpl), "dqn_replay": bench_dqn(dev, rpl),
+                               "mujoco_replay": bench_mujoco(dev, rpl)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         result["cpu_baseline"] = cpu_baseline(c, host, args.cpu_seconds)
     if world > 1:
@@ -431,6 +436,129 @@ def bench_ppo(dev, rpl):
             "disc_us_per_call": ms_disc * 1e3, "disc_GBps": disc_gbs, "disc_frac": disc_gbs / peak,
             "l2": f"input pool {pool} x {per/1e6:.1f} MB > 4 x L2",
             "timing": "CUDA graph of one call per pool entry, replayed; per-call average"}
+
+
+def _graph_time(dev, step, P=8, reps=25):
+    """Capture P consecutive steps in one CUDA graph (after warm-up) and return the
+    mean device time per step over `reps` replays (CUDA events on the replay stream)."""
+    import torch
+    for i in range(2 * P):
+        step(i)
+    torch.cuda.synchronize()
+    st = torch.cuda.Stream(dev)
+    st.wait_stream(torch.cuda.current_stream(dev))
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=st):
+        for i in range(P):
+            step(i)
+    torch.cuda.synchronize()
+    gr.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        gr.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / (reps * P)
+
+
+def transition_bytes(k, n, obs_bytes, act_bytes, stacked_frames=True):
+    """Algorithmic bytes of one gathered transition: unique obs rows
+    t-k+1..t+n read once, two k-stacks written, n rewards + n dones + action in,
+    action + return + done_n + IS weight out."""
+    rd = (k + n) * obs_bytes + n * 5 + act_bytes
+    wr = 2 * k * obs_bytes + act_bytes + 4 + 1 + 4
+    return rd + wr
+
+
+def bench_dqn(dev, rpl):
+    """configs[2]: 2^20-transition frame ring [4096, 256], tree of 2^20 leaves; one step
+    = update(previous batch) -> sample_stream(bs) + IS weights -> transition gather
+    (k=4 stacks at t and t+3, fused 3-step return)."""
+    import torch
+    from paper_1909_01500_b200 import replay as R
+    from synth.device import make_ring_device
+    c = DQN
+    ring = make_ring_device(404, c["cap_T"], c["B"], dev, ep_len=2000.0, cursor=1111, with_rnn=False)
+    N = c["cap_T"] * c["B"]
+    tree = rpl.SumTree(N, c["fanout"], 32, device=dev)
+    rows = R.valid_transition_rows(c["cap_T"], ring.cursor, ring.size, c["k"], c["n_step"])
+    valid = torch.from_numpy(R.leaves_of(rows, c["B"])).to(dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    tree.update(valid, torch.randn(valid.numel(), generator=g, device=dev).abs(), c["alpha"], c["eps_p"])
+    out = {}
+    lib, P_ = rpl._lib.lib, rpl.ops._ptr
+    for bs in c["batches"]:
+        plan = rpl.GatherPlan(ring, bs, kind="transition", k=c["k"], n_step=c["n_step"], gamma=c["gamma"])
+        idx = [torch.full((bs,), -1, dtype=torch.int64, device=dev) for _ in range(2)]
+        q = torch.zeros(bs, dtype=torch.int64, device=dev)
+        qmin = torch.zeros(1, dtype=torch.int64, device=dev)
+        w = torch.zeros(bs, dtype=torch.float32, device=dev)
+        td = torch.randn((8, bs), generator=g, device=dev).abs()
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+
+        def step(i):
+            s = rpl.ops._stream(dev)
+            cur, prev = idx[i % 2], idx[(i + 1) % 2]
+            rpl._lib.check(lib.rpl_sumtree_update(tree._lp, P_(tree.storage), P_(prev), P_(td[i % 8]), bs,
+                                                  c["alpha"], c["eps_p"], None, s), "update")
+            rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), bs, 0xD00, c["beta"], P_(cur),
+                                                         P_(q), P_(qmin), P_(w), P_(err), s), "sample")
+            plan.run(cur, err=err, stream=s)
+
+        ms = _graph_time(dev, step)
+        rpl.check_err(err)
+        nb = bs * transition_bytes(c["k"], c["n_step"], 7056, 8)
+        out[f"bs{bs}"] = {"us_per_step": ms * 1e3, "samples_per_s": bs / (ms / 1e3),
+                          "step_GBps": nb / (ms / 1e3) / 1e9}
+    del ring, tree
+    torch.cuda.empty_cache()
+    return {"workload": "dqn_atari_1M_transitions", "unit": "transitions/s", "ring": [c["cap_T"], c["B"]],
+            "leaves": N, "k": c["k"], "n_step": c["n_step"], "alpha": c["alpha"], "beta": c["beta"],
+            "timing": "CUDA graph of 8 steps (update+sample+gather), replayed", **out}
+
+
+def bench_mujoco(dev, rpl):
+    """configs[3]: uniform + n-step replay over a [65536, 16] f32 vector ring (2^20
+    transitions); one step = rpl_sample_uniform(256) -> transition gather (obs at t
+    and t+3, action, fused 3-step return)."""
+    import torch
+    from paper_1909_01500_b200 import replay as R
+    from synth.device import make_ring_device
+    c = MUJOCO
+    res = {}
+    for D, A in c["dims"]:
+        ring = make_ring_device(505 + D, c["cap_T"], c["B"], dev, ep_len=1000.0, cursor=2222, vec_dim=D, act_dim=A,
+                                with_rnn=False)
+        rows = R.valid_transition_rows(c["cap_T"], ring.cursor, ring.size, 1, c["n_step"])
+        # valid rows form one ring interval: oldest valid row and count
+        age = (ring.cursor - 1 - rows) % c["cap_T"]
+        lo_row = int(rows[np.argmax(age)])
+        n_rows = int(rows.size)
+        bs = c["batch"]
+        plan = rpl.GatherPlan(ring, bs, kind="transition", k=1, n_step=c["n_step"], gamma=c["gamma"])
+        idx = torch.zeros(bs, dtype=torch.int64, device=dev)
+        ctr = torch.zeros(1, dtype=torch.int64, device=dev)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+
+        def step(i):
+            s = rpl.ops._stream(dev)
+            rpl._lib.check(rpl._lib.lib.rpl_sample_uniform(bs, 0xA11, 0, rpl.ops._ptr(ctr), lo_row, n_rows,
+                                                           c["cap_T"], c["B"], rpl.ops._ptr(idx), s), "uniform")
+            plan.run(idx, err=err, stream=s)
+
+        ms = _graph_time(dev, step)
+        rpl.check_err(err)
+        nb = bs * transition_bytes(1, c["n_step"], 4 * D, 4 * A)
+        res[f"D{D}_A{A}"] = {"us_per_step": ms * 1e3, "samples_per_s": bs / (ms / 1e3),
+                             "step_GBps": nb / (ms / 1e3) / 1e9}
+        del ring
+        torch.cuda.empty_cache()
+    return {"workload": "mujoco_uniform_1M_transitions", "unit": "transitions/s", "ring": [c["cap_T"], c["B"]],
+            "batch": c["batch"], "n_step": c["n_step"],
+            "timing": "CUDA graph of 8 steps (uniform sample+gather), replayed", **res}
 
 
 # ----------------------------------------------------------------------------- oracle arm

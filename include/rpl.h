@@ -185,6 +185,17 @@ int rpl_sumtree_total(const rpl_tree_layout* L, const int64_t* tree, int64_t* ou
 /* Recompute every internal node from the leaves (resume after restoring leaves). */
 int rpl_sumtree_rebuild(const rpl_tree_layout* L, int64_t* tree, void* stream);
 
+/* Uniform replay (SAC/TD3 Mujoco config, BASELINE configs[3]; "uniform
+ * sampling ... with replacement"): n transition leaves drawn uniformly, with replacement,
+ * from the valid window of ring rows lo_row .. lo_row+n_rows-1 (mod cap_T) x all B columns.
+ *   M = n_rows * B,  m_k = floor(u_k * M / 2^64)  (u_k the k-th Philox draw, R23),
+ *   out_idx[k] = ((lo_row + m_k / B) mod cap_T) * B + (m_k mod B).
+ * Draw k uses counter offset + k, plus *ctr when ctr (device uint64, may be NULL) is given;
+ * the call then advances *ctr by n on the device, so a captured graph draws fresh indices.
+ * RPL_EINVAL: n < 1, n_rows < 1 or > cap_T, lo_row outside [0, cap_T), B < 1, M >= 2^62. */
+int rpl_sample_uniform(int64_t n, uint64_t seed, uint64_t offset, uint64_t* ctr, int64_t lo_row,
+                       int64_t n_rows, int64_t cap_T, int64_t B, int64_t* out_idx, void* stream);
+
 /* w[k] = (qmin / q[k])^beta in fp64, rounded to f32 (§8c #10); q[k] <= 0 -> w = 0. */
 int rpl_is_weights(const int64_t* q, const int64_t* qmin, int64_t n, double beta, float* w,
                    void* stream);
@@ -260,9 +271,17 @@ int rpl_debug_priority_values(const float* td_abs, int64_t n, double alpha, doub
                               int32_t force_slow, float* out_v, uint8_t* out_slow, void* stream);
 
 /* Diagnostics (tests only): select the sequence-gather kernel, 0 = persistent pipeline with
- * TMA loads and LSU stores (default), 1 = one CTA per 8-row chunk (TMA both ways),
- * 2 = frame-centric LSU copy, 3 = persistent all-TMA pipeline.  All produce identical outputs. */
+ * TMA loads and LSU stores (default, 8 consumer warps), 1 = one CTA per 8-row chunk (TMA both
+ * ways), 2 = frame-centric LSU copy, 3 = persistent all-TMA pipeline, 4 / 5 = variant 0 with
+ * 14 / 4 consumer warps.  All produce identical outputs. */
 int rpl_debug_set_gather_variant(int32_t variant);
+
+/* Diagnostics (measurement only): bit mask applied to the default sequence gather.
+ * 1 = skip the frame stores, 2 = skip the frame loads (outputs are then garbage),
+ * 4 = streaming (evict-first) frame stores, 8 = evict-first L2 policy on the frame loads,
+ * 16 = skip the per-row fields and stored state.
+ * 0 (default) restores normal operation.  Returns RPL_EINVAL for other values. */
+int rpl_debug_set_gather_diag(int32_t mask);
 
 #ifdef __cplusplus
 }

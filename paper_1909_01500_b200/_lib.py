@@ -80,9 +80,11 @@ _SIGS = {
     "rpl_sumtree_total": ([C.POINTER(TreeLayout), P, P, P], C.c_int),
     "rpl_sumtree_rebuild": ([C.POINTER(TreeLayout), P, P], C.c_int),
     "rpl_is_weights": ([P, P, I64, D, P, P], C.c_int),
+    "rpl_sample_uniform": ([I64, U64, U64, P, I64, I64, I64, I64, P, P], C.c_int),
     "rpl_gather": ([C.POINTER(GatherDesc), P, P, P, D, I64, P, P], C.c_int),
     "rpl_debug_priority_values": ([P, I64, D, D, I32, P, P, P], C.c_int),
     "rpl_debug_set_gather_variant": ([I32], C.c_int),
+    "rpl_debug_set_gather_diag": ([I32], C.c_int),
 }
 
 EXPORTS = tuple(_SIGS)

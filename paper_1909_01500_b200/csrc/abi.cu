@@ -1,8 +1,20 @@
 // ABI helpers: version, error strings, launch counter (include/rpl.h).
 #include "common.cuh"
 
+#include <stdlib.h>
+#include <string.h>
+
 namespace rpl {
 int64_t g_launches = 0;
+
+bool pdl_enabled() {
+  static int cached = -1;
+  if (cached < 0) {
+    const char* v = getenv("RPL_PDL");
+    cached = (v && strcmp(v, "0") == 0) ? 0 : 1;
+  }
+  return cached == 1;
+}
 }
 
 extern "C" const char* rpl_strerror(int status) {

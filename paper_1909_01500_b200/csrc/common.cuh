@@ -30,6 +30,40 @@ inline int launch_status() {
   return e == cudaSuccess ? RPL_OK : RPL_ECUDA;
 }
 
+// Programmatic dependent launch (PDL).  Hot-path kernels are launched with the
+// programmatic-stream-serialization attribute, so a kernel's launch and prologue
+// (shared-memory / mbarrier setup) overlap the tail of the previous kernel on the
+// stream; pdl_wait() — executed before the kernel's first global-memory access —
+// blocks until the previous grid has completed and its writes are visible, so
+// stream order (the device analogue of the paper's RW lock) is unchanged.
+// pdl_trigger() lets the next grid start launching once every CTA has called it.
+// RPL_PDL=0 in the environment disables the attribute (A/B measurement).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  ++g_launches;
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return RPL_ECUDA;
+  }
+  return RPL_OK;
+}
+
 __device__ __forceinline__ void set_err(int32_t* err, int32_t bits) {
   if (err) atomicOr(err, bits);
 }

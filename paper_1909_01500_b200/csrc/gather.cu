@@ -50,6 +50,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   uint32_t done = 0;
   while (!done) {
@@ -123,6 +132,7 @@ struct GDesc {
   float* o_w;
   uint8_t* o_rnn;
   int use_tma;
+  int diag;  // rpl_debug_set_gather_diag mask (0 in normal operation)
 };
 
 __device__ __forceinline__ int64_t wrap(int64_t r, int64_t cap) {
@@ -155,6 +165,7 @@ k_gather_transition(GDesc D, const int64_t* __restrict__ idx, int64_t n, const i
   __shared__ int sslot[2][32];
   const int tid = threadIdx.x;
   const int64_t s = blockIdx.x;
+  pdl_wait();
   const int64_t leaf = idx[s];
   if (leaf < 0) return;
   const int k = D.k, ns = D.n_step;
@@ -751,221 +762,299 @@ __global__ void k_gather_seq_fields(GDesc D, const int64_t* __restrict__ idx, in
 
 // ---------------------------------------------------------------------------
 // Sequences, persistent pipeline with TMA loads and LSU stores (default).
-// Same row partition and piece structure as k_gather_seq_pipe, but the stores
-// are issued by CONSUMER WARPS as 16-B st.global from shared memory instead of
-// bulk stores: bulk stores and bulk loads share the SM's TMA queue, so in the
-// all-TMA pipeline every frame load waits behind up to G queued 28-KB stores
-// (measured: ~22 GB/s/SM).  Roles:
-//   warp 0, lane 0   producer: TMA bulk loads of each piece's unique frames
-//                    into NS slots (one mbarrier per slot); refills a slot once
-//                    the contiguous done-frontier has passed every row reading it;
-//   warp 1           meta: episode-start offsets of every row (lane per row, all
-//                    done-flag loads in flight at once), then the per-row fields,
+// A CTA owns a contiguous run of output rows g = s*L + tau (time-major within
+// each sample s), i.e. one or a few "pieces" (runs of rows of one sample); a
+// piece of R rows reads its R + k - 1 unique frames once.  Stores are issued by
+// CONSUMER WARPS as 16-B st.global from shared memory rather than bulk stores:
+// bulk stores and bulk loads share the SM's TMA queue, so in the all-TMA
+// pipeline every frame load waits behind queued 28-KB stores.  Roles:
+//   warp 0, lane 0   producer: TMA bulk loads of each piece's frames into NS
+//                    slots (one mbarrier per slot); refills a slot once the
+//                    contiguous done-frontier has passed every row reading it;
+//   warp 1           meta: per-row fields (act, prev_act, rew, prev_rew, done),
 //                    IS weights and stored recurrent state — the latency-bound
-//                    scattered loads never sit on a consumer's critical path
-//                    (ncu r1: they were ~20% of the consumers' stall samples);
+//                    scattered loads never sit on a consumer's critical path;
 //   warps 2..NC+1    consumers: one k-stack (k*7056 B) per row, LDS.128 ->
 //                    STG.128, then flag the row done.
+// Index math is 32-bit and incremental (ring rows, slots and mbarrier parities
+// are tabulated once per row in parallel): 64-bit div/mod on the producer's
+// serial path cost ~19 us per launch before (ncu r1, diag 19).
 // ---------------------------------------------------------------------------
+constexpr int PL_MAX_ROWS = 256;  // output rows per CTA (host caps rows_per_cta)
+
 template <int NC>
 __global__ void __launch_bounds__((NC + 2) * 32, 1)
 k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, int64_t rows_per_cta,
                       const int64_t* __restrict__ q, const int64_t* __restrict__ qmin, double beta, int32_t* err) {
   extern __shared__ __align__(128) uint8_t smem[];  // NS frame slots
   __shared__ __align__(8) uint64_t full[PIPE_MAX_NS];
-  __shared__ int8_t start_off[PIPE_MAX_ROWS];
-  __shared__ int rel[PIPE_MAX_ROWS];        // frames released when row c (and all before) are done
-  __shared__ int row_first[PIPE_MAX_ROWS];  // frame position of row c's window start (-1: skipped row)
-  __shared__ volatile int row_done[PIPE_MAX_ROWS];
+  // per piece p (sample s = s_first + p)
+  __shared__ int p_b[PL_MAX_ROWS];     // ring column, -1: skipped sample
+  __shared__ int p_row0[PL_MAX_ROWS];  // ring row of the piece's first output row
+  __shared__ int p_blk[PL_MAX_ROWS];   // storage block (stored RNN state)
+  __shared__ int p_F[PL_MAX_ROWS];     // frame position of the piece's first frame
+  // per output row c
+  __shared__ int row_first[PL_MAX_ROWS];  // frame position of the row's window start (-1: skipped)
+  __shared__ int rel[PL_MAX_ROWS];        // frames released once rows <= c are done
+  __shared__ int row_ring[PL_MAX_ROWS];   // ring row
+  __shared__ short row_piece[PL_MAX_ROWS];
+  __shared__ short row_tau[PL_MAX_ROWS];
+  __shared__ int8_t start_off[PL_MAX_ROWS];
+  __shared__ volatile int row_done[PL_MAX_ROWS];
+  __shared__ int s_npieces;
   constexpr int NT = (NC + 2) * 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k = D.k, L = D.seq_len;
-  const int64_t ob = D.obs_bytes;
-  const int nv = (int)(ob / 16);
-  const int64_t total = n * (int64_t)L;
-  const int64_t g0 = (int64_t)blockIdx.x * rows_per_cta;
-  const int64_t g1 = min(total, g0 + rows_per_cta);
+  const int ob = (int)D.obs_bytes;
+  const int nv = ob / 16;
+  const int cap = (int)D.cap_T, Bc = (int)D.B, period = (int)D.period;
+  const int total = (int)(n * (int64_t)L);
+  const int g0 = (int)((int64_t)blockIdx.x * rows_per_cta);
+  const int g1 = min(total, g0 + (int)rows_per_cta);
   if (g0 >= g1) return;
-  const int nrows = (int)(g1 - g0);
-  const int64_t nblk = D.cap_T / D.period;
+  const int nrows = g1 - g0;
+  const int s_first = g0 / L;
+  const int npieces = (g1 - 1) / L - s_first + 1;
+  const int64_t nleaves = (int64_t)(cap / period) * Bc;
 
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
-    // frame positions per row (pieces: runs of rows of one sample)
-    int64_t F = 0;
-    int c = 0;
-    for (int64_t g = g0; g < g1;) {
-      const int64_t s = g / L;
-      const int tau0 = (int)(g - s * L);
-      const int R = (int)min((int64_t)(L - tau0), g1 - g);
-      const int64_t leaf = idx[s];
-      const bool ok = leaf >= 0 && leaf < nblk * D.B;
-      for (int m = 0; m < R; ++m, ++c) {
-        row_first[c] = ok ? (int)(F + m) : -1;
-        rel[c] = (int)(ok ? (m == R - 1 ? F + R + k - 1 : F + m + 1) : F);
-      }
-      if (ok) F += R + k - 1;
-      g += R;
-    }
+    s_npieces = npieces;
   }
   for (int c = tid; c < nrows; c += NT) row_done[c] = 0;
+  pdl_wait();  // idx comes from the sampler launched just before
+  // (A) pieces, in parallel: one sampled leaf each
+  for (int pc = tid; pc < npieces; pc += NT) {
+    const int sm = s_first + pc;
+    const int tau0 = max(g0 - sm * L, 0);
+    const int64_t leaf = idx[sm];
+    int bcol = -1, row0 = 0, blk = 0;
+    if (leaf >= 0 && leaf < nleaves) {
+      blk = (int)(leaf / Bc);
+      bcol = (int)(leaf - (int64_t)blk * Bc);
+      row0 = (int)(((int64_t)blk * period + tau0) % cap);
+      if (tau0 == 0) {
+        const int64_t age = wrap(D.cursor - 1 - (int64_t)blk * period, D.cap_T);
+        const int hist = k - 1 > 1 ? k - 1 : 1;
+        if (!(age >= L - 1 && age + hist <= D.size - 1)) set_err(err, RPL_DERR_INVALID_LEAF);
+      }
+    } else if (leaf >= nleaves && tau0 == 0) {
+      set_err(err, RPL_DERR_IDX);
+    }
+    p_b[pc] = bcol;
+    p_row0[pc] = row0;
+    p_blk[pc] = blk;
+  }
+  __syncthreads();
+  // (B) frame positions: exclusive scan over pieces (serial: a CTA holds one to a few pieces)
+  if (tid == 0) {
+    int F = 0;
+    for (int pc = 0; pc < npieces; ++pc) {
+      p_F[pc] = F;
+      if (p_b[pc] >= 0) {
+        const int sm = s_first + pc;
+        const int R = min(g1, (sm + 1) * L) - max(g0, sm * L);
+        F += R + k - 1;
+      }
+    }
+  }
   __syncthreads();
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- producer: TMA loads only ----------------
-      int frontier = 0;      // rows [0, frontier) are done
-      int released = 0;      // frames < released may be overwritten
-      int64_t i = 0;
-      for (int64_t g = g0; g < g1;) {
-        const int64_t s = g / L;
-        const int tau0 = (int)(g - s * L);
-        const int R = (int)min((int64_t)(L - tau0), g1 - g);
-        const int64_t leaf = idx[s];
-        if (leaf >= 0 && leaf < nblk * D.B) {
-          const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
-          const int64_t first = blk * D.period + tau0 - (k - 1);
-          for (int w = 0; w < R + k - 1; ++w, ++i) {
-            if (i >= NS) {
-              while (released <= i - NS) {
-                if (frontier < nrows && row_done[frontier]) {
-                  released = rel[frontier];
-                  ++frontier;
-                } else {
-                  __nanosleep(32);
-                }
+      int frontier = 0;  // rows [0, frontier) are done
+      int released = 0;  // frames < released may be overwritten
+      int i = 0, slot = 0;
+      for (int pc = 0; pc < npieces; ++pc) {
+        const int bcol = p_b[pc];
+        if (bcol < 0) continue;
+        const int sm = s_first + pc;
+        const int R = min(g1, (sm + 1) * L) - max(g0, sm * L);
+        int row = p_row0[pc] - (k - 1);
+        while (row < 0) row += cap;
+        const uint8_t* col = D.obs + (int64_t)bcol * ob;
+        const int64_t rstride = (int64_t)Bc * ob;
+        for (int w = 0; w < R + k - 1; ++w, ++i) {
+          if (i >= NS) {
+            while (released <= i - NS) {
+              if (frontier < nrows && row_done[frontier]) {
+                released = rel[frontier];
+                ++frontier;
+              } else {
+                __nanosleep(20);
               }
-              fence_proxy_async();
             }
-            const int slot = (int)(i % NS);
-            mbar_expect_tx(&full[slot], (uint32_t)ob);
-            bulk_g2s(smem + (int64_t)slot * ob, D.obs + (wrap(first + w, D.cap_T) * D.B + b) * ob, (uint32_t)ob,
-                     &full[slot]);
+            fence_proxy_async();
           }
+          if (!(D.diag & 2)) {
+            mbar_expect_tx(&full[slot], (uint32_t)ob);
+            const uint8_t* src = col + (int64_t)row * rstride;
+            if (D.diag & 8) bulk_g2s_evict_first(smem + slot * ob, src, (uint32_t)ob, &full[slot]);
+            else bulk_g2s(smem + slot * ob, src, (uint32_t)ob, &full[slot]);
+          }
+          if (++row == cap) row = 0;
+          if (++slot == NS) slot = 0;
         }
-        g += R;
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------- meta warp ----------------
-    // (1) episode-start offsets: every lane owns rows lane, lane+32, ...; the k-1
-    //     done flags of a row are loaded together before any is inspected.
-    for (int c = lane; c < nrows; c += 32) {
-      const int64_t g = g0 + c;
-      const int64_t s = g / L;
-      const int tau = (int)(g - s * L);
-      const int64_t leaf = idx[s];
-      int8_t so = 0;
-      if (leaf >= 0 && leaf < nblk * D.B) {
-        const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
-        const int64_t row = blk * D.period + tau;
-        uint8_t dw[8];
-#pragma unroll
-        for (int j = 1; j < 8; ++j)
-          dw[j] = j < k ? __ldg(D.done + wrap(row - (k - 1) + j - 1, D.cap_T) * D.B + b) : (uint8_t)0;
-#pragma unroll
-        for (int j = 1; j < 8; ++j)
-          if (dw[j]) so = (int8_t)j;  // latest episode start in the window wins
-        if (tau == 0) {
-          const int64_t age = wrap(D.cursor - 1 - blk * D.period, D.cap_T);
-          const int hist = k - 1 > 1 ? k - 1 : 1;
-          if (!(age >= L - 1 && age + hist <= D.size - 1)) set_err(err, RPL_DERR_INVALID_LEAF);
-        }
-      } else if (leaf >= nblk * D.B && tau == 0) {
-        set_err(err, RPL_DERR_IDX);
-      }
-      start_off[c] = so;
-    }
-    __threadfence_block();
-    asm volatile("bar.arrive 1, %0;" ::"n"((NC + 1) * 32) : "memory");
-    // (2) per-row fields: act, prev_act, rew, prev_rew, done, IS weight
-    const int64_t ab = D.act_bytes;
-    for (int c = lane; c < nrows; c += 32) {
-      if (row_first[c] < 0) continue;
-      const int64_t g = g0 + c;
-      const int64_t s = g / L;
-      const int tau = (int)(g - s * L);
-      const int64_t leaf = idx[s];
-      const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
-      const int64_t row = wrap(blk * D.period + tau, D.cap_T);
-      const int64_t prow = wrap(blk * D.period + tau - 1, D.cap_T);
-      const int64_t e = row * D.B + b, pe = prow * D.B + b;
-      const uint8_t pd = __ldg(D.done + pe);
-      const uint8_t dd = __ldg(D.done + e);
-      const float rw = D.o_rew ? __ldg(D.rew + e) : 0.0f;
-      const float prw = D.o_prev_rew ? __ldg(D.rew + pe) : 0.0f;
-      const int64_t o = (int64_t)tau * n + s;
-      if (ab == 8 && ((reinterpret_cast<uintptr_t>(D.act) | reinterpret_cast<uintptr_t>(D.o_act) |
-                       reinterpret_cast<uintptr_t>(D.o_prev_act)) & 7) == 0) {
-        const uint64_t* a = reinterpret_cast<const uint64_t*>(D.act);
-        const uint64_t av = D.o_act ? __ldg(a + e) : 0ull;
-        const uint64_t pav = D.o_prev_act ? __ldg(a + pe) : 0ull;
-        if (D.o_act) reinterpret_cast<uint64_t*>(D.o_act)[o] = av;
-        if (D.o_prev_act) reinterpret_cast<uint64_t*>(D.o_prev_act)[o] = pd ? 0ull : pav;
-      } else {
-        if (D.o_act) coop_copy(D.o_act + o * ab, D.act + e * ab, ab, 0, 1);
-        if (D.o_prev_act) {
-          if (pd) coop_zero(D.o_prev_act + o * ab, ab, 0, 1);
-          else coop_copy(D.o_prev_act + o * ab, D.act + pe * ab, ab, 0, 1);
-        }
-      }
-      if (D.o_rew) D.o_rew[o] = rw;
-      if (D.o_prev_rew) D.o_prev_rew[o] = pd ? 0.0f : prw;
-      if (D.o_done) D.o_done[o] = dd;
-      if (tau == 0 && D.o_w && q && qmin) {
-        const int64_t qs = q[s];
-        D.o_w[s] = qs > 0 ? (float)pow((double)(*qmin) / (double)qs, beta) : 0.0f;
-      }
-    }
-    // (3) stored recurrent state of every sample whose first row lives here
-    if (D.o_rnn) {
-      for (int c = 0; c < nrows; ++c) {
-        const int64_t g = g0 + c;
-        const int64_t s = g / L;
-        if (g != s * L || row_first[c] < 0) continue;
-        const int64_t leaf = idx[s];
-        const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
-        for (int p = 0; p < D.rnn_parts; ++p)
-          coop_copy(D.o_rnn + (p * n + s) * D.rnn_bytes, D.rnn + ((blk * D.B + b) * D.rnn_parts + p) * D.rnn_bytes,
-                    D.rnn_bytes, lane, 32);
       }
     }
   } else {
-    // ---------------- consumers: one k-stack per row, LSU stores ----------------
-    asm volatile("bar.sync 1, %0;" ::"n"((NC + 1) * 32) : "memory");
-    for (int c = warp - 2; c < nrows; c += NC) {
-      const int64_t g = g0 + c;
-      const int64_t s = g / L;
-      const int tau = (int)(g - s * L);
-      const int p0 = row_first[c];
-      if (p0 >= 0) {
-        const int so = start_off[c];
-        for (int j = so; j < k; ++j) {
-          const int64_t pos = p0 + j;
-          mbar_wait(&full[pos % NS], (uint32_t)((pos / NS) & 1));
+    // (C) row tables + episode-start offsets, rows spread over warps 1..NC+1; the
+    //     k-1 done flags of a row are loaded together before any is inspected.
+    for (int c = tid - 32; c < nrows; c += NT - 32) {
+      const int g = g0 + c;
+      const int sm = g / L;
+      const int tau = g - sm * L;
+      const int pc = sm - s_first;
+      const int bcol = p_b[pc];
+      const int m = g - max(g0, sm * L);
+      int8_t so = 0;
+      int ring = 0;
+      if (bcol >= 0) {
+        const int R = min(g1, (sm + 1) * L) - max(g0, sm * L);
+        const int F = p_F[pc];
+        row_first[c] = F + m;
+        rel[c] = m == R - 1 ? F + R + k - 1 : F + m + 1;
+        ring = p_row0[pc] + m;
+        if (ring >= cap) ring -= cap;
+        uint8_t dw[8];
+#pragma unroll
+        for (int j = 1; j < 8; ++j) {
+          int rr = ring - k + j;  // done flag of window row j-1 = ring row (ring - (k-1) + j - 1)
+          while (rr < 0) rr += cap;
+          dw[j] = j < k ? __ldg(D.done + (int64_t)rr * Bc + bcol) : (uint8_t)0;
         }
-        int4* dst = reinterpret_cast<int4*>(D.o_obs + (((int64_t)tau * n + s) * k) * ob);
-        for (int j = 0; j < k; ++j) {
-          int4* d = dst + (int64_t)j * nv;
-          if (j < so && D.pad_mode == RPL_PAD_ZERO) {
-            for (int v = lane; v < nv; v += 32) d[v] = make_int4(0, 0, 0, 0);
-          } else {
-            const int src = j < so ? so : j;
-            const int4* sp = reinterpret_cast<const int4*>(smem + (int64_t)((p0 + src) % NS) * ob);
-#pragma unroll 4
-            for (int v = lane; v < nv; v += 32) d[v] = sp[v];
+#pragma unroll
+        for (int j = 1; j < 8; ++j)
+          if (dw[j]) so = (int8_t)j;  // latest episode start in the window wins
+      } else {
+        row_first[c] = -1;
+        rel[c] = p_F[pc];
+      }
+      row_ring[c] = ring;
+      row_piece[c] = (short)pc;
+      row_tau[c] = (short)tau;
+      start_off[c] = so;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"((NC + 1) * 32) : "memory");
+
+    if (warp == 1) {
+      // ---------------- meta warp: per-row fields, IS weights ----------------
+      const int64_t ab = D.act_bytes;
+      const bool a8 = ab == 8 && ((reinterpret_cast<uintptr_t>(D.act) | reinterpret_cast<uintptr_t>(D.o_act) |
+                                   reinterpret_cast<uintptr_t>(D.o_prev_act)) & 7) == 0;
+      for (int c = lane; c < nrows && !(D.diag & 16); c += 32) {
+        if (row_first[c] < 0) continue;
+        const int pc = row_piece[c];
+        const int sm = s_first + pc;
+        const int tau = row_tau[c];
+        const int bcol = p_b[pc];
+        const int ring = row_ring[c];
+        const int prow = ring == 0 ? cap - 1 : ring - 1;
+        const int64_t e = (int64_t)ring * Bc + bcol, pe = (int64_t)prow * Bc + bcol;
+        const uint8_t pd = __ldg(D.done + pe);
+        const uint8_t dd = __ldg(D.done + e);
+        const float rw = D.o_rew ? __ldg(D.rew + e) : 0.0f;
+        const float prw = D.o_prev_rew ? __ldg(D.rew + pe) : 0.0f;
+        const int64_t o = (int64_t)tau * n + sm;
+        if (a8) {
+          const uint64_t* a = reinterpret_cast<const uint64_t*>(D.act);
+          const uint64_t av = D.o_act ? __ldg(a + e) : 0ull;
+          const uint64_t pav = D.o_prev_act ? __ldg(a + pe) : 0ull;
+          if (D.o_act) reinterpret_cast<uint64_t*>(D.o_act)[o] = av;
+          if (D.o_prev_act) reinterpret_cast<uint64_t*>(D.o_prev_act)[o] = pd ? 0ull : pav;
+        } else {
+          if (D.o_act) coop_copy(D.o_act + o * ab, D.act + e * ab, ab, 0, 1);
+          if (D.o_prev_act) {
+            if (pd) coop_zero(D.o_prev_act + o * ab, ab, 0, 1);
+            else coop_copy(D.o_prev_act + o * ab, D.act + pe * ab, ab, 0, 1);
           }
         }
+        if (D.o_rew) D.o_rew[o] = rw;
+        if (D.o_prev_rew) D.o_prev_rew[o] = pd ? 0.0f : prw;
+        if (D.o_done) D.o_done[o] = dd;
+        if (tau == 0 && D.o_w && q && qmin) {
+          const int64_t qs = q[sm];
+          D.o_w[sm] = qs > 0 ? (float)pow((double)(*qmin) / (double)qs, beta) : 0.0f;
+        }
       }
-      __syncwarp();
-      if (lane == 0) {
-        fence_proxy_async();
-        row_done[c] = 1;
+      // stored recurrent state of every sample whose first row lives here
+      if (D.o_rnn && !(D.diag & 16)) {
+        const int nparts = D.rnn_parts;
+        const int64_t rb = D.rnn_bytes;
+        for (int pc = 0; pc < npieces; ++pc) {
+          const int sm = s_first + pc;
+          if (sm * L < g0 || p_b[pc] < 0) continue;  // first row not in this CTA, or skipped
+          const int64_t blk = p_blk[pc], bcol = p_b[pc];
+          for (int pp = 0; pp < nparts; ++pp)
+            coop_copy(D.o_rnn + (pp * n + sm) * rb, D.rnn + ((blk * Bc + bcol) * nparts + pp) * rb, rb, lane, 32);
+        }
+      }
+    } else {
+      // ---------------- consumers: one k-stack per row, LSU stores ----------------
+      for (int c = warp - 2; c < nrows; c += NC) {
+        const int p0 = row_first[c];
+        if (p0 >= 0) {
+          const int so = start_off[c];
+          const int sm = s_first + row_piece[c];
+          const int tau = row_tau[c];
+          const int s0 = p0 % NS;
+          const uint32_t par0 = (uint32_t)((p0 / NS) & 1);
+          if (!(D.diag & 2))
+            for (int j = so; j < k; ++j) {
+              int sl = s0 + j;
+              uint32_t par = par0;
+              if (sl >= NS) {
+                sl -= NS;
+                par ^= 1u;
+              }
+              mbar_wait(&full[sl], par);
+            }
+          int4* dst = reinterpret_cast<int4*>(D.o_obs + ((int64_t)tau * n + sm) * k * ob);
+          if (!(D.diag & 1))
+            for (int j = 0; j < k; ++j) {
+              int4* d = dst + j * nv;
+              if (j < so && D.pad_mode == RPL_PAD_ZERO) {
+                for (int v = lane; v < nv; v += 32) d[v] = make_int4(0, 0, 0, 0);
+              } else {
+                int sl = s0 + (j < so ? so : j);
+                if (sl >= NS) sl -= NS;
+                const int4* sp = reinterpret_cast<const int4*>(smem + sl * ob);
+                if (D.diag & 4) {
+#pragma unroll 4
+                  for (int v = lane; v < nv; v += 32) __stcs(d + v, sp[v]);
+                } else {
+#pragma unroll 4
+                  for (int v = lane; v < nv; v += 32) d[v] = sp[v];
+                }
+              }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          fence_proxy_async();
+          row_done[c] = 1;
+        }
       }
     }
   }
+  pdl_trigger();
 }
+
+template <int NC>
+int launch_seq_lsu(const GDesc& g, const int64_t* idx, int64_t n, int NS, int64_t rows_per_cta, const int64_t* q,
+                   const int64_t* qmin, double beta, int32_t* dev_err, size_t dyn, int64_t grid, cudaStream_t st) {
+  static size_t set_l = 0;
+  if (dyn > 48 * 1024 && dyn > set_l) {
+    cudaFuncSetAttribute(k_gather_seq_pipe_lsu<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    set_l = dyn;
+  }
+  return launch_pdl(k_gather_seq_pipe_lsu<NC>, dim3((unsigned)grid), dim3((NC + 2) * 32), dyn, st, g, idx, n, NS,
+                    rows_per_cta, q, qmin, beta, dev_err);
+}
+
+int g_seq_diag = 0;
 
 GDesc to_dev(const rpl_gather_desc* d) {
   GDesc g;
@@ -1002,23 +1091,12 @@ GDesc to_dev(const rpl_gather_desc* d) {
   g.o_w = d->o_w;
   g.o_rnn = static_cast<uint8_t*>(d->o_rnn);
   g.use_tma = 0;
+  g.diag = g_seq_diag;
   return g;
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-template <int NC>
-int launch_seq_lsu(const GDesc& g, const int64_t* idx, int64_t n, int NS, int64_t rows_per_cta, const int64_t* q,
-                   const int64_t* qmin, double beta, int32_t* dev_err, size_t dyn, int64_t grid, cudaStream_t st) {
-  static size_t set_l = 0;
-  if (dyn > 48 * 1024 && dyn > set_l) {
-    cudaFuncSetAttribute(k_gather_seq_pipe_lsu<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    set_l = dyn;
-  }
-  k_gather_seq_pipe_lsu<NC><<<(unsigned)grid, (NC + 2) * 32, dyn, st>>>(g, idx, n, NS, rows_per_cta, q, qmin, beta,
-                                                                         dev_err);
-  return launch_status();
-}
 
 // 0: TMA-load / LSU-store pipeline (default, 8 consumer warps; 4: 14, 5: 4), 1: chunked all-TMA kernel, 2: frame-centric
 // LSU, 3: all-TMA pipeline
@@ -1032,6 +1110,12 @@ using namespace rpl;
 extern "C" int rpl_debug_set_gather_variant(int32_t variant) {
   if (variant < 0 || variant > 5) return RPL_EINVAL;
   g_seq_variant = variant;
+  return RPL_OK;
+}
+
+extern "C" int rpl_debug_set_gather_diag(int32_t mask) {
+  if (mask < 0 || mask > 31) return RPL_EINVAL;
+  g_seq_diag = mask;
   return RPL_OK;
 }
 
@@ -1063,8 +1147,8 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       set_t = dyn;
     }
     if (n > 0x7fffffff) return RPL_EINVAL;
-    k_gather_transition<<<(unsigned)n, G_THREADS, dyn, st>>>(g, idx, n, q, qmin, beta, dev_err);
-    return launch_status();
+    return launch_pdl(k_gather_transition, dim3((unsigned)n), dim3(G_THREADS), dyn, st, g, idx, n, q, qmin, beta,
+                      dev_err);
   }
   if (desc->kind == RPL_GATHER_SEQUENCE) {
     if (desc->seq_len < 1 || desc->period < 1 || desc->cap_T % desc->period != 0) return RPL_EINVAL;
@@ -1091,12 +1175,13 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       int NS = (int)(200 * 1024 / desc->obs_bytes);
       if (NS > PIPE_MAX_NS) NS = PIPE_MAX_NS;
       const int k = desc->k;
-      if (NS >= 2 * k) {
+      const int64_t total = n * (int64_t)desc->seq_len;
+      if (NS >= 2 * k && total < (1ll << 30) && desc->cap_T < (1ll << 30) && desc->B < (1ll << 30) &&
+          desc->cap_T * desc->B < (1ll << 40)) {
         const size_t dyn = (size_t)NS * desc->obs_bytes;
-        const int64_t total = n * (int64_t)desc->seq_len;
         int64_t grid = (int64_t)sm_count();
         int64_t rows_per_cta = (total + grid - 1) / grid;
-        if (rows_per_cta > PIPE_MAX_ROWS) rows_per_cta = PIPE_MAX_ROWS;
+        if (rows_per_cta > PL_MAX_ROWS) rows_per_cta = PL_MAX_ROWS;
         grid = (total + rows_per_cta - 1) / rows_per_cta;
         g.use_tma = 1;
         // consumer warps: 8 (default), 14 (variant 4), 4 (variant 5)

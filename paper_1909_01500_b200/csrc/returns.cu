@@ -37,6 +37,7 @@ k_scan(const float* __restrict__ r, const float* __restrict__ v, const uint8_t* 
   __shared__ double sA[WARPS][32];
   __shared__ double sB[WARPS][32];
   __shared__ double sCarry[32];
+  pdl_wait();
 
   // carry = x just after the current chunk: R_T = bootstrap (discounted), A_T = 0 (GAE)
   if (w == 0) sCarry[lane] = (!GAE && boot != nullptr && cv) ? (double)boot[col] : 0.0;
@@ -133,6 +134,7 @@ __global__ void k_nstep(const float* __restrict__ r, const uint8_t* __restrict__
                         float* __restrict__ out, uint8_t* __restrict__ done_out) {
   const int64_t rows = T - n + 1;
   const int64_t total = rows * B;
+  pdl_wait();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = e / B;
@@ -158,6 +160,7 @@ __global__ void k_nstep(const float* __restrict__ r, const uint8_t* __restrict__
 
 __global__ void k_rescale(const float* __restrict__ x, float* __restrict__ y, int64_t n,
                           double eps, int inverse) {
+  pdl_wait();
   const int64_t n4 = n / 4;
   const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -196,9 +199,8 @@ extern "C" int rpl_returns_discounted(const float* r, const uint8_t* d, const fl
                                       int64_t T, int64_t B, double gamma, float* ret, void* stream) {
   if (!r || !d || !ret || T < 1 || B < 1) return RPL_EINVAL;
   dim3 grid((unsigned)((B + 31) / 32));
-  k_scan<SCAN_WARPS, SCAN_S, false><<<grid, SCAN_WARPS * 32, 0, as_stream(stream)>>>(
-      r, nullptr, d, bootstrap, T, B, gamma, 0.0, ret, nullptr);
-  return launch_status();
+  return launch_pdl(k_scan<SCAN_WARPS, SCAN_S, false>, grid, dim3(SCAN_WARPS * 32), 0, as_stream(stream), r,
+                    (const float*)nullptr, d, bootstrap, T, B, gamma, 0.0, ret, (float*)nullptr);
 }
 
 extern "C" int rpl_gae(const float* r, const float* v, const uint8_t* d, const float* bootstrap_v,
@@ -206,9 +208,8 @@ extern "C" int rpl_gae(const float* r, const float* v, const uint8_t* d, const f
                        void* stream) {
   if (!r || !v || !d || !bootstrap_v || !adv || T < 1 || B < 1) return RPL_EINVAL;
   dim3 grid((unsigned)((B + 31) / 32));
-  k_scan<SCAN_WARPS, SCAN_S, true><<<grid, SCAN_WARPS * 32, 0, as_stream(stream)>>>(
-      r, v, d, bootstrap_v, T, B, gamma, lambda, adv, ret);
-  return launch_status();
+  return launch_pdl(k_scan<SCAN_WARPS, SCAN_S, true>, grid, dim3(SCAN_WARPS * 32), 0, as_stream(stream), r, v, d,
+                    bootstrap_v, T, B, gamma, lambda, adv, ret);
 }
 
 extern "C" int rpl_returns_nstep(const float* r, const uint8_t* d, int64_t T, int64_t B, int32_t n,
@@ -220,9 +221,8 @@ extern "C" int rpl_returns_nstep(const float* r, const uint8_t* d, int64_t T, in
   if (rescale && !(rescale_eps > 0.0)) return RPL_EINVAL;
   const int64_t work = (T - n + 1) * B;
   const int threads = 256;
-  k_nstep<<<elementwise_grid(work, threads), threads, 0, as_stream(stream)>>>(
-      r, d, T, B, n, gamma, q, q_boot, rescale ? 1 : 0, rescale_eps, ret_n, done_n);
-  return launch_status();
+  return launch_pdl(k_nstep, dim3(elementwise_grid(work, threads)), dim3(threads), 0, as_stream(stream), r, d, T, B,
+                    (int)n, gamma, q, q_boot, rescale ? 1 : 0, rescale_eps, ret_n, done_n);
 }
 
 extern "C" int rpl_value_rescale(const float* x, float* y, int64_t n, double eps, int32_t inverse,
@@ -230,7 +230,6 @@ extern "C" int rpl_value_rescale(const float* x, float* y, int64_t n, double eps
   if (!x || !y || n < 0 || !(eps > 0.0)) return RPL_EINVAL;
   if (n == 0) return RPL_OK;
   const int threads = 256;
-  k_rescale<<<elementwise_grid((n + 3) / 4, threads), threads, 0, as_stream(stream)>>>(
-      x, y, n, eps, inverse ? 1 : 0);
-  return launch_status();
+  return launch_pdl(k_rescale, dim3(elementwise_grid((n + 3) / 4, threads)), dim3(threads), 0, as_stream(stream), x,
+                    y, n, eps, inverse ? 1 : 0);
 }

@@ -46,6 +46,7 @@ k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__
   const int lane = tid & 31;
   int64_t* leaves = tree + L.level_off[L.depth];
   int64_t* hdr = tree + L.hdr_off;
+  pdl_wait();
   const int64_t maxseen_now = hdr[0];
   int64_t local_max = INT64_MIN;
   int32_t errbits = 0;
@@ -189,6 +190,7 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
               int32_t* err, int rank, int n_shards, int64_t shard_leaves,
               const int64_t* __restrict__ totals, int use_stream) {
   const int lane = threadIdx.x & 31;
+  pdl_wait();
   // Philox counter base: offset, plus the tree's stream position when use_stream
   const uint64_t ctr0 = offset + (use_stream ? (uint64_t)tree[L.hdr_off + 2] : 0ull);
   const int64_t k = (int64_t)blockIdx.x * SAMPLE_WARPS + (threadIdx.x >> 5);
@@ -295,6 +297,7 @@ __global__ void k_tree_find(TreeDev L, const int64_t* __restrict__ tree, const i
 }
 
 __global__ void k_tree_total(const int64_t* __restrict__ tree, int64_t* __restrict__ out) {
+  pdl_wait();
   *out = tree[0];
 }
 
@@ -320,11 +323,28 @@ __global__ void k_tree_header(int64_t* __restrict__ hdr, int64_t maxseen) {
 
 __global__ void k_is_weights(const int64_t* __restrict__ q, const int64_t* __restrict__ qmin, int64_t n,
                              double beta, float* __restrict__ w) {
+  pdl_wait();
   const double m = (double)*qmin;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t qj = q[j];
     w[j] = qj > 0 ? (float)pow(m / (double)qj, beta) : 0.0f;
   }
+}
+
+constexpr int UNI_THREADS = 256;
+__global__ void __launch_bounds__(UNI_THREADS)
+k_sample_uniform(int64_t n, uint64_t seed, uint64_t offset, uint64_t* ctr, int64_t lo_row, int64_t n_rows,
+                 int64_t cap_T, int64_t B, int64_t* __restrict__ out_idx) {
+  pdl_wait();
+  const uint64_t base = offset + (ctr ? *ctr : 0ull);
+  const uint64_t M = (uint64_t)n_rows * (uint64_t)B;
+  for (int64_t k = threadIdx.x; k < n; k += UNI_THREADS) {
+    const uint64_t m = __umul64hi(philox_u64(seed, base + (uint64_t)k), M);
+    const int64_t row = (lo_row + (int64_t)(m / (uint64_t)B)) % cap_T;
+    out_idx[k] = row * B + (int64_t)(m % (uint64_t)B);
+  }
+  __syncthreads();
+  if (ctr && threadIdx.x == 0) *ctr = base - offset + (uint64_t)n;
 }
 
 __global__ void k_priority_values(const float* __restrict__ td, int64_t n, double alpha, double eps_p,
@@ -351,9 +371,8 @@ int launch_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, c
   if (!layout_ok(L) || !tree || n < 0) return RPL_EINVAL;
   if (n == 0) return RPL_OK;
   if (!idx) return RPL_EINVAL;
-  k_tree_update<<<1, UPD_THREADS, 0, as_stream(stream)>>>(tree_dev(L), tree, idx, td, q, mode, n, alpha,
-                                                           eps_p, err, force_slow);
-  return launch_status();
+  return launch_pdl(k_tree_update, dim3(1), dim3(UPD_THREADS), 0, as_stream(stream), tree_dev(L), tree, idx, td, q,
+                    mode, n, alpha, eps_p, err, force_slow);
 }
 
 }  // namespace
@@ -421,10 +440,9 @@ extern "C" int rpl_sumtree_sample(const rpl_tree_layout* L, int64_t* tree, int64
   if (!layout_ok(L) || !tree || !out_idx || !out_q || n < 1 || n > (1ll << 30)) return RPL_EINVAL;
   if (out_w && !(beta >= 0.0)) return RPL_EINVAL;
   const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
-  k_tree_sample<false><<<(unsigned)blocks, SAMPLE_WARPS * 32, 0, as_stream(stream)>>>(
-      tree_dev(L), tree, n, draws, seed, offset, beta, out_idx, out_q, out_qmin, out_w, dev_err, 0, 1, 0,
-      nullptr, 0);
-  return launch_status();
+  return launch_pdl(k_tree_sample<false>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
+                    tree_dev(L), tree, n, draws, seed, offset, beta, out_idx, out_q, out_qmin, out_w, dev_err, 0, 1,
+                    (int64_t)0, (const int64_t*)nullptr, 0);
 }
 
 extern "C" int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree, int64_t n, uint64_t seed,
@@ -433,9 +451,9 @@ extern "C" int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree
   if (!layout_ok(L) || !tree || !out_idx || !out_q || n < 1 || n > (1ll << 30)) return RPL_EINVAL;
   if (out_w && !(beta >= 0.0)) return RPL_EINVAL;
   const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
-  k_tree_sample<false><<<(unsigned)blocks, SAMPLE_WARPS * 32, 0, as_stream(stream)>>>(
-      tree_dev(L), tree, n, nullptr, seed, 0, beta, out_idx, out_q, out_qmin, out_w, dev_err, 0, 1, 0, nullptr, 1);
-  return launch_status();
+  return launch_pdl(k_tree_sample<false>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
+                    tree_dev(L), tree, n, (const uint64_t*)nullptr, seed, (uint64_t)0, beta, out_idx, out_q, out_qmin,
+                    out_w, dev_err, 0, 1, (int64_t)0, (const int64_t*)nullptr, 1);
 }
 
 extern "C" int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t rank, int32_t n_shards,
@@ -447,10 +465,9 @@ extern "C" int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tre
   if (!layout_ok(L) || !tree || !out_idx || !out_q || !shard_totals || n < 1 || n > (1ll << 30)) return RPL_EINVAL;
   if (n_shards < 1 || rank < 0 || rank >= n_shards || shard_leaves < L->n_leaves) return RPL_EINVAL;
   const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
-  k_tree_sample<true><<<(unsigned)blocks, SAMPLE_WARPS * 32, 0, as_stream(stream)>>>(
-      tree_dev(L), tree, n, draws, seed, offset, 0.0, out_idx, out_q, out_qmin, nullptr, dev_err, rank, n_shards,
-      shard_leaves, shard_totals, use_stream);
-  return launch_status();
+  return launch_pdl(k_tree_sample<true>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
+                    tree_dev(L), tree, n, draws, seed, offset, 0.0, out_idx, out_q, out_qmin, (float*)nullptr, dev_err,
+                    (int)rank, (int)n_shards, shard_leaves, shard_totals, (int)use_stream);
 }
 
 extern "C" int rpl_sumtree_find(const rpl_tree_layout* L, const int64_t* tree, const int64_t* prefix, int64_t n,
@@ -465,8 +482,7 @@ extern "C" int rpl_sumtree_find(const rpl_tree_layout* L, const int64_t* tree, c
 
 extern "C" int rpl_sumtree_total(const rpl_tree_layout* L, const int64_t* tree, int64_t* out_total, void* stream) {
   if (!layout_ok(L) || !tree || !out_total) return RPL_EINVAL;
-  k_tree_total<<<1, 1, 0, as_stream(stream)>>>(tree, out_total);
-  return launch_status();
+  return launch_pdl(k_tree_total, dim3(1), dim3(1), 0, as_stream(stream), tree, out_total);
 }
 
 extern "C" int rpl_sumtree_rebuild(const rpl_tree_layout* L, int64_t* tree, void* stream) {
@@ -490,8 +506,8 @@ extern "C" int rpl_is_weights(const int64_t* q, const int64_t* qmin, int64_t n, 
   if (n == 0) return RPL_OK;
   const int threads = 256;
   const int64_t blocks = (n + threads - 1) / threads;
-  k_is_weights<<<(unsigned)(blocks > 1024 ? 1024 : blocks), threads, 0, as_stream(stream)>>>(q, qmin, n, beta, w);
-  return launch_status();
+  return launch_pdl(k_is_weights, dim3((unsigned)(blocks > 1024 ? 1024 : blocks)), dim3(threads), 0,
+                    as_stream(stream), q, qmin, n, beta, w);
 }
 
 extern "C" int rpl_debug_priority_values(const float* td_abs, int64_t n, double alpha, double eps_p,
@@ -503,4 +519,13 @@ extern "C" int rpl_debug_priority_values(const float* td_abs, int64_t n, double 
   k_priority_values<<<(unsigned)(blocks > 4096 ? 4096 : blocks), threads, 0, as_stream(stream)>>>(
       td_abs, n, alpha, eps_p, force_slow, out_v, out_slow);
   return launch_status();
+}
+
+extern "C" int rpl_sample_uniform(int64_t n, uint64_t seed, uint64_t offset, uint64_t* ctr, int64_t lo_row,
+                                  int64_t n_rows, int64_t cap_T, int64_t B, int64_t* out_idx, void* stream) {
+  if (!out_idx || n < 1 || B < 1 || cap_T < 1 || n_rows < 1 || n_rows > cap_T || lo_row < 0 || lo_row >= cap_T)
+    return RPL_EINVAL;
+  if ((double)n_rows * (double)B >= 4.6e18) return RPL_EINVAL;
+  return launch_pdl(k_sample_uniform, dim3(1), dim3(UNI_THREADS), 0, as_stream(stream), n, seed, offset, ctr, lo_row,
+                    n_rows, cap_T, B, out_idx);
 }

@@ -16,7 +16,7 @@ from ._lib import GatherDesc, TreeLayout, check, lib
 
 __all__ = [
     "returns_discounted", "returns_nstep", "gae", "value_rescale", "SumTree", "is_weights", "gather",
-    "GatherRing", "GatherPlan", "check_err", "launch_count", "debug_priority_values",
+    "GatherRing", "GatherPlan", "check_err", "launch_count", "debug_priority_values", "sample_uniform",
 ]
 
 
@@ -124,6 +124,20 @@ def is_weights(q, qmin, beta, out=None):
     out = torch.empty(q.shape, dtype=torch.float32, device=q.device) if out is None else out
     check(lib.rpl_is_weights(_ptr(q), _ptr(qmin), q.numel(), float(beta), _ptr(out), _stream(q.device)),
           "rpl_is_weights")
+    return out
+
+
+def sample_uniform(n, seed, lo_row, n_rows, cap_T, B, offset=0, ctr=None, device="cuda", out=None):
+    """rpl_sample_uniform: n leaves uniform over rows lo_row..lo_row+n_rows-1 (mod cap_T) x B columns.
+    `ctr` (a 1-element int64 CUDA tensor) makes the draw stream advance on the device."""
+    if ctr is not None:
+        _req(ctr, torch.int64, "ctr", (1,))
+        device = ctr.device
+    out = torch.empty(int(n), dtype=torch.int64, device=device) if out is None else out
+    _req(out, torch.int64, "out", (int(n),))
+    check(lib.rpl_sample_uniform(int(n), int(seed) & (2**64 - 1), int(offset) & (2**64 - 1), _ptr(ctr), int(lo_row),
+                                 int(n_rows), int(cap_T), int(B), _ptr(out), _stream(out.device)),
+          "rpl_sample_uniform")
     return out
 
 

@@ -263,3 +263,26 @@ def test_dqn_full_size_tree(rpl):
     assert [int(x) for x in H(t.leaves)] == orc.q
     assert int(H(t.total())[0]) == orc.total()
     assert int(H(t.err)[0]) == 0
+
+
+@pytest.mark.parametrize("lo,nr,cap,B,n", [(0, 1, 1, 1, 5), (41, 17, 50, 4, 1000), (3, 65530, 65536, 16, 256),
+                                           (10, 4089, 4096, 256, 777)])
+def test_sample_uniform_vs_oracle(rpl, lo, nr, cap, B, n):
+    import torch
+    from oracle import uniform as OU
+    out = rpl.sample_uniform(n, seed=77, lo_row=lo, n_rows=nr, cap_T=cap, B=B, offset=5)
+    assert H(out).tolist() == OU.uniform_indices(n, 77, 5, lo, nr, cap, B)
+    # device stream counter: two calls draw consecutive counters and advance it by n each
+    ctr = torch.zeros(1, dtype=torch.int64, device="cuda")
+    a = rpl.sample_uniform(n, seed=3, lo_row=lo, n_rows=nr, cap_T=cap, B=B, ctr=ctr)
+    b = rpl.sample_uniform(n, seed=3, lo_row=lo, n_rows=nr, cap_T=cap, B=B, ctr=ctr)
+    assert int(H(ctr)[0]) == 2 * n
+    assert H(a).tolist() == OU.uniform_indices(n, 3, 0, lo, nr, cap, B)
+    assert H(b).tolist() == OU.uniform_indices(n, 3, n, lo, nr, cap, B)
+
+
+def test_sample_uniform_errors(rpl):
+    lib = rpl._lib.lib
+    assert lib.rpl_sample_uniform(0, 1, 0, None, 0, 1, 1, 1, 1, None) == -1
+    assert lib.rpl_sample_uniform(1, 1, 0, None, 5, 1, 4, 1, 1, None) == -1   # lo_row >= cap
+    assert lib.rpl_sample_uniform(1, 1, 0, None, 0, 5, 4, 1, 1, None) == -1   # n_rows > cap
