@@ -134,6 +134,19 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def gather_traffic():
+    """DRAM bytes (read + write) per launch of the sequence gather from the committed
+    ncu --set full capture (profiles/gather_traffic.json, written by
+    scripts/ncu_summary.py from the same launch configuration)."""
+    p = os.path.join(ROOT, "profiles", "gather_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"bytes": d["dram_bytes_read"] + d["dram_bytes_write"], "source": d["source"]}
+    except (OSError, KeyError, ValueError):
+        return {}
+
+
 def seq_bytes_per_sample(c, act_bytes=8):
     """Algorithmic HBM bytes one sequence of rpl_gather moves:
     reads the L+k-1 unique frames, the per-row scalars and the stored state;
@@ -310,6 +323,7 @@ def run_rpl(args):
     achieved = alg_bytes / (g_ms / 1e3) / 1e9
 
     rpl.check_err(err)
+    traffic = gather_traffic()
 
     result = {
         "metric": "prioritized samples/sec (update+sample+gather)",
@@ -332,9 +346,10 @@ def run_rpl(args):
                    "l2": "inputs larger than L2 (7.2 GB ring, random sequences every step)",
                    "timing": "cuda graph of 8 steps, replayed" if use_graph else "eager launches"},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "k_gather_sequence", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": "k_gather_seq_pipe_lsu", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": g_ms,
+                     "traffic": traffic.get("bytes"), "traffic_source": traffic.get("source"),
+                     "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": g_ms,
                      "step_share": g_ms / (ms / K_eff)},
     }
     if not args.profile:

@@ -278,7 +278,8 @@ int rpl_debug_set_gather_variant(int32_t variant);
 
 /* Diagnostics (measurement only): bit mask applied to the default sequence gather.
  * 1 = skip the frame stores, 2 = skip the frame loads (outputs are then garbage),
- * 4 = streaming (evict-first) frame stores, 8 = evict-first L2 policy on the frame loads,
+ * 4 = normal-priority frame stores, 8 = normal L2 policy on the frame loads (the default is
+ * evict-first for both: frames are streamed once),
  * 16 = skip the per-row fields and stored state.
  * 0 (default) restores normal operation.  Returns RPL_EINVAL for other values. */
 int rpl_debug_set_gather_diag(int32_t mask);
