@@ -212,12 +212,12 @@ def run_rpl(args):
     q_pool = torch.from_numpy(g.normal(0, 10, (P, L, n_glob)).astype(np.float32)).to(dev)
     seed = 0x5EED
 
-    plan = rpl.GatherPlan(ring, n_glob, kind="sequence", k=k, seq_len=L, period=period, with_weights=False)
+    plan = rpl.GatherPlan(ring, n_glob, kind="sequence", k=k, seq_len=L, period=period, with_weights=True)
     out = plan.outputs
     idx_buf = [torch.full((n_glob,), -1, dtype=torch.int64, device=dev) for _ in range(2)]
     q_buf = torch.zeros(n_glob, dtype=torch.int64, device=dev)
     qmin = torch.zeros(1, dtype=torch.int64, device=dev)
-    w = torch.zeros(n_glob, dtype=torch.float32, device=dev)
+    w = plan.outputs["w"]  # IS weights: written by the gather (1 GPU) or rpl_is_weights (Mode L)
     y = torch.empty((c["train"], n_glob), dtype=torch.float32, device=dev)
     dn = torch.empty((c["train"], n_glob), dtype=torch.uint8, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -231,13 +231,13 @@ def run_rpl(args):
     def step(i, gather_events=None):
         s = rpl.ops._stream(dev)
         cur, prev = idx_buf[i % 2], idx_buf[(i + 1) % 2]
-        # (a5-a7) new priorities for the previous batch (entries < 0 = not owned: skipped by the kernel? no:
-        # they are flagged; so update only when owned entries exist — the kernel skips idx < 0 with RPL_DERR_IDX)
+        # (a5-a7) new priorities for the previous batch (entries < 0 — not owned — are skipped, R22)
         rpl._lib.check(lib.rpl_sumtree_update(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]), n_glob,
                                               c["alpha"], c["eps_p"], None, s), "update")
         if world == 1:
+            # (a8) draws only; the batch-min normaliser and IS weights (a9) are fused into the gather
             rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, seed, c["beta"], P_(cur),
-                                                         P_(q_buf), P_(qmin), P_(w), P_(err), s), "sample")
+                                                         P_(q_buf), None, None, P_(err), s), "sample")
         else:
             rpl._lib.check(lib.rpl_sumtree_total(tree._lp, P_(tree.storage), P_(my_total), s), "total")
             dist.all_gather_into_tensor(totals, my_total)                       # K5: 8 B per rank
@@ -248,7 +248,10 @@ def run_rpl(args):
             rpl._lib.check(lib.rpl_is_weights(P_(q_buf), P_(qmin), n_glob, c["beta"], P_(w), s), "w")
         if gather_events is not None:
             gather_events[0].record()
-        plan.run(cur, stream=s)
+        if world == 1:
+            plan.run(cur, q=q_buf, qmin=None, beta=c["beta"], stream=s)
+        else:
+            plan.run(cur, stream=s)
         if gather_events is not None:
             gather_events[1].record()
         rpl._lib.check(lib.rpl_returns_nstep(P_(r_tr), P_(d_tr), Tn, n_glob, c["n_step"], c["gamma"],
@@ -506,11 +509,10 @@ def bench_dqn(dev, rpl):
     out = {}
     lib, P_ = rpl._lib.lib, rpl.ops._ptr
     for bs in c["batches"]:
-        plan = rpl.GatherPlan(ring, bs, kind="transition", k=c["k"], n_step=c["n_step"], gamma=c["gamma"])
+        plan = rpl.GatherPlan(ring, bs, kind="transition", k=c["k"], n_step=c["n_step"], gamma=c["gamma"],
+                              with_weights=True)
         idx = [torch.full((bs,), -1, dtype=torch.int64, device=dev) for _ in range(2)]
         q = torch.zeros(bs, dtype=torch.int64, device=dev)
-        qmin = torch.zeros(1, dtype=torch.int64, device=dev)
-        w = torch.zeros(bs, dtype=torch.float32, device=dev)
         td = torch.randn((8, bs), generator=g, device=dev).abs()
         err = torch.zeros(1, dtype=torch.int32, device=dev)
 
@@ -520,8 +522,8 @@ def bench_dqn(dev, rpl):
             rpl._lib.check(lib.rpl_sumtree_update(tree._lp, P_(tree.storage), P_(prev), P_(td[i % 8]), bs,
                                                   c["alpha"], c["eps_p"], None, s), "update")
             rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), bs, 0xD00, c["beta"], P_(cur),
-                                                         P_(q), P_(qmin), P_(w), P_(err), s), "sample")
-            plan.run(cur, err=err, stream=s)
+                                                         P_(q), None, None, P_(err), s), "sample")
+            plan.run(cur, q=q, qmin=None, beta=c["beta"], err=err, stream=s)  # IS weights fused
 
         ms = _graph_time(dev, step)
         rpl.check_err(err)

@@ -146,7 +146,9 @@ int rpl_sumtree_set_q(const rpl_tree_layout* L, int64_t* tree, const int64_t* id
  * sums), out_q[k] = q_i, *out_qmin = min_k out_q[k].  If out_w != NULL:
  * out_w[k] = (N P_k)^-beta / max_j (N P_j)^-beta = (qmin / q_k)^beta  (§8c #10),
  * computed in fp64.  Q == 0 -> out_idx = -1, out_q = 0, RPL_DERR_EMPTY.  `tree` is
- * written only in its sampler-ticket header word.  n >= 1. */
+ * written only in its sampler-ticket header word.  n >= 1.  out_qmin and out_w may be NULL;
+ * with both NULL the call needs no grid-wide reduction (one dependent round trip less) and
+ * the IS weights can be produced by rpl_gather from out_q (qmin = NULL there). */
 int rpl_sumtree_sample(const rpl_tree_layout* L, int64_t* tree, int64_t n, const uint64_t* draws,
                        uint64_t seed, uint64_t offset, double beta, int64_t* out_idx,
                        int64_t* out_q, int64_t* out_qmin, float* out_w, int32_t* dev_err,
@@ -225,8 +227,10 @@ int rpl_is_weights(const int64_t* q, const int64_t* qmin, int64_t n, double beta
  * o_act, o_rew, o_done at rows row0..row0+L-1; o_prev_act, o_prev_rew at rows
  * row0-1..row0+L-2, zero on an episode's first row (§8c #18); o_rnn [rnn_parts, n,
  * rnn_bytes] = rnn[block, b] (P:232 [Num_Layers, Batch, Hidden] per part, §8c #19).
- * Any output pointer may be NULL (not produced).  If o_w, q and qmin are all non-NULL,
- * o_w[k] = (qmin/q[k])^beta (a9).  idx[k] < 0 -> sample skipped (outputs untouched).
+ * Any output pointer may be NULL (not produced).  If o_w and q are non-NULL,
+ * o_w[k] = (qmin/q[k])^beta (a9, §8c #10) with qmin = *qmin when qmin != NULL (e.g. the
+ * all-reduced global batch min of sharded sampling), else the min of q[j] over this call's
+ * entries with idx[j] >= 0 (the sampled batch).  idx[k] < 0 -> sample skipped (outputs untouched).
  * A window not fully inside the valid rows sets RPL_DERR_INVALID_LEAF (output still the
  * defined function of the ring contents).  obs_bytes % 16 == 0 with 16-byte aligned
  * pointers uses TMA bulk copies; other sizes use vectorised LSU copies.

@@ -82,6 +82,26 @@ __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
+// IS-weight normaliser (a9, §8c #10): *qmin when the caller passes it (e.g. the global
+// batch min of Mode L), else the min of q over this batch's sampled entries (idx >= 0),
+// computed by the calling warp (all 32 lanes must call) — this lets the sampler skip its
+// grid-wide reduction.
+__device__ __forceinline__ int64_t warp_batch_qmin(const int64_t* __restrict__ qmin, const int64_t* __restrict__ idx,
+                                                   const int64_t* __restrict__ q, int64_t n) {
+  if (qmin) return *qmin;
+  int64_t m = INT64_MAX;
+  for (int64_t j = threadIdx.x & 31; j < n; j += 32) {
+    const int64_t i = idx[j], v = q[j];
+    if (i >= 0 && v < m) m = v;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const int64_t x = (int64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)m, o);
+    m = x < m ? x : m;
+  }
+  return m;
+}
+
 // Cooperative copy of `bytes` bytes with the widest aligned word.
 __device__ __forceinline__ void coop_copy(void* dst, const void* src, int64_t bytes, int t, int nt) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src);
@@ -206,6 +226,7 @@ k_gather_transition(GDesc D, const int64_t* __restrict__ idx, int64_t n, const i
   // scalars (warp 1): action, fused n-step return, IS weight (a9)
   if (tid >= 32 && tid < 64) {
     const int l = tid - 32;
+    const int64_t qm = (D.o_w && q) ? warp_batch_qmin(qmin, idx, q, n) : 0;
     if (D.o_act) {
       const uint8_t* src = D.act + (r * D.B + b) * D.act_bytes;
       uint8_t* dst = D.o_act + s * D.act_bytes;
@@ -225,9 +246,9 @@ k_gather_transition(GDesc D, const int64_t* __restrict__ idx, int64_t n, const i
         if (D.o_ret) D.o_ret[s] = (float)acc;
         if (D.o_done_n) D.o_done_n[s] = dn ? 1 : 0;
       }
-      if (D.o_w && q && qmin) {
+      if (D.o_w && q) {
         const int64_t qs = q[s];
-        D.o_w[s] = qs > 0 ? (float)pow((double)(*qmin) / (double)qs, beta) : 0.0f;
+        D.o_w[s] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
       }
     }
   }
@@ -363,9 +384,10 @@ k_gather_sequence(GDesc D, const int64_t* __restrict__ idx, int64_t n, const int
       coop_copy(D.o_rnn + (p * n + s) * D.rnn_bytes,
                 D.rnn + ((blk * D.B + b) * D.rnn_parts + p) * D.rnn_bytes, D.rnn_bytes, tid, G_THREADS);
   }
-  if (c == 0 && D.o_w && q && qmin && tid == 0) {
+  if (c == 0 && D.o_w && q && tid < 32) {
+    const int64_t qm = warp_batch_qmin(qmin, idx, q, n);
     const int64_t qs = q[s];
-    D.o_w[s] = qs > 0 ? (float)pow((double)(*qmin) / (double)qs, beta) : 0.0f;
+    if (tid == 0) D.o_w[s] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
   }
   __syncthreads();
   if (!D.o_obs || NR == 0) return;
@@ -589,6 +611,7 @@ k_gather_seq_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, i
   } else {
     // ---------------- per-row fields, stored state, IS weights (warps 2-3) ----------------
     const int t2 = tid - 64;
+    const int64_t qm = (D.o_w && q) ? warp_batch_qmin(qmin, idx, q, n) : 0;
     for (int c = t2; c < nrows; c += PIPE_THREADS - 64) {
       const int64_t gg = g0 + c;
       const int64_t s = gg / L;
@@ -608,9 +631,9 @@ k_gather_seq_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, i
       if (D.o_rew) D.o_rew[o] = __ldg(D.rew + row * D.B + b);
       if (D.o_prev_rew) D.o_prev_rew[o] = pd ? 0.0f : __ldg(D.rew + prow * D.B + b);
       if (D.o_done) D.o_done[o] = __ldg(D.done + row * D.B + b);
-      if (tau == 0 && D.o_w && q && qmin) {
+      if (tau == 0 && D.o_w && q) {
         const int64_t qs = q[s];
-        D.o_w[s] = qs > 0 ? (float)pow((double)(*qmin) / (double)qs, beta) : 0.0f;
+        D.o_w[s] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
       }
     }
     // stored recurrent state for samples whose row 0 lies in this CTA
@@ -676,9 +699,10 @@ k_gather_seq_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, const int6
   int padcnt[8];
 #pragma unroll
   for (int t = 0; t < 8; ++t) padcnt[t] = 0;
-  if (lane == 0 && w == 0 && D.o_w && q && qmin) {
+  if (w == 0 && D.o_w && q) {  // warp-uniform (w is this warp's frame)
+    const int64_t qm = warp_batch_qmin(qmin, idx, q, n);
     const int64_t qs = q[s];
-    D.o_w[s] = qs > 0 ? (float)pow((double)(*qmin) / (double)qs, beta) : 0.0f;
+    if (lane == 0) D.o_w[s] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
   }
   for (int t = 0; t < k; ++t) {
     const int tau = w + t;
@@ -944,6 +968,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
 
     if (warp == 1) {
       // ---------------- meta warp: per-row fields, IS weights ----------------
+      const int64_t qm = (D.o_w && q) ? warp_batch_qmin(qmin, idx, q, n) : 0;
       const int64_t ab = D.act_bytes;
       const bool a8 = ab == 8 && ((reinterpret_cast<uintptr_t>(D.act) | reinterpret_cast<uintptr_t>(D.o_act) |
                                    reinterpret_cast<uintptr_t>(D.o_prev_act)) & 7) == 0;
@@ -977,9 +1002,9 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         if (D.o_rew) D.o_rew[o] = rw;
         if (D.o_prev_rew) D.o_prev_rew[o] = pd ? 0.0f : prw;
         if (D.o_done) D.o_done[o] = dd;
-        if (tau == 0 && D.o_w && q && qmin) {
+        if (tau == 0 && D.o_w && q) {
           const int64_t qs = q[sm];
-          D.o_w[sm] = qs > 0 ? (float)pow((double)(*qmin) / (double)qs, beta) : 0.0f;
+          D.o_w[sm] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
         }
       }
       // stored recurrent state of every sample whose first row lives here

@@ -191,8 +191,20 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
               const int64_t* __restrict__ totals, int use_stream) {
   const int lane = threadIdx.x & 31;
   pdl_wait();
+  // Without a batch reduction (no IS weights, no qmin requested) there is no grid-wide
+  // end ticket; a stream-mode call then takes its ticket at the start instead: every CTA
+  // reads the stream position (acquire: ordered before its ticket increment) and the CTA
+  // that arrives last advances the position once all CTAs have read it.
+  const bool reduce = out_w != nullptr || out_qmin != nullptr;
+  unsigned long long* ticket = reinterpret_cast<unsigned long long*>(tree + L.hdr_off + 1);
+  uint64_t spos = 0;
+  if (use_stream) {
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(spos) : "l"(tree + L.hdr_off + 2) : "memory");
+  }
+  __shared__ unsigned long long s_t0;
+  if (use_stream && !reduce && threadIdx.x == 0) s_t0 = atomicAdd(ticket, 1ull);
   // Philox counter base: offset, plus the tree's stream position when use_stream
-  const uint64_t ctr0 = offset + (use_stream ? (uint64_t)tree[L.hdr_off + 2] : 0ull);
+  const uint64_t ctr0 = offset + spos;
   const int64_t k = (int64_t)blockIdx.x * SAMPLE_WARPS + (threadIdx.x >> 5);
   int32_t errbits = 0;
   uint64_t Q, own_lo = 0, own_T = 0;
@@ -233,13 +245,22 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
   }
   if (lane == 0 && errbits) set_err(err, errbits);
 
+  if (!reduce) {
+    if (use_stream) {
+      __syncthreads();
+      if (threadIdx.x == 0 && s_t0 == (unsigned long long)gridDim.x - 1) {
+        tree[L.hdr_off + 2] = (int64_t)(spos + (uint64_t)n);  // advance the stream
+        *ticket = 0ull;
+      }
+    }
+    return;
+  }
   // last CTA: batch-min q and IS weights (§8c #10)
   __shared__ int s_last;
   __shared__ int64_t s_min[SAMPLE_WARPS];
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    unsigned long long* ticket = reinterpret_cast<unsigned long long*>(tree + L.hdr_off + 1);
     const unsigned long long t = atomicAdd(ticket, 1ull);
     s_last = (t == (unsigned long long)gridDim.x - 1);
   }

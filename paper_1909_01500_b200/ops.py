@@ -215,13 +215,14 @@ class SumTree:
                                      _ptr(qmin), _ptr(w), _ptr(e), self._s()), "rpl_sumtree_sample")
         return idx, q, qmin, w
 
-    def sample_stream(self, n, seed, beta=None, out=None, err=None):
-        """rpl_sumtree_sample_stream: Philox draws from the tree's device-side stream position."""
+    def sample_stream(self, n, seed, beta=None, out=None, err=None, want_qmin=True):
+        """rpl_sumtree_sample_stream: Philox draws from the tree's device-side stream position.
+        want_qmin=False with beta=None skips the batch reduction (qmin returned as None)."""
         n = int(n)
         if out is None:
             idx = torch.empty(n, dtype=torch.int64, device=self.device)
             q = torch.empty(n, dtype=torch.int64, device=self.device)
-            qmin = torch.empty(1, dtype=torch.int64, device=self.device)
+            qmin = torch.empty(1, dtype=torch.int64, device=self.device) if (want_qmin or beta is not None) else None
             w = torch.empty(n, dtype=torch.float32, device=self.device) if beta is not None else None
         else:
             idx, q, qmin, w = out
@@ -360,7 +361,7 @@ def gather(ring: GatherRing, idx, kind="transition", k=4, n_step=1, gamma=0.99, 
         alloc("done", (L, n), torch.uint8)
         if ring.rnn is not None:
             alloc("rnn", (int(ring.rnn.shape[2]), n, int(ring.rnn.shape[3])), ring.rnn.dtype)
-    if q is not None and qmin is not None:
+    if q is not None:
         alloc("w", (n,), torch.float32)
     fields = {"obs": "o_obs", "next_obs": "o_next_obs", "act": "o_act", "prev_act": "o_prev_act", "rew": "o_rew",
               "prev_rew": "o_prev_rew", "done": "o_done", "ret": "o_ret", "done_n": "o_done_n", "w": "o_w",

@@ -264,3 +264,30 @@ def test_dqn_full_size_sampled(rpl):
         check_rel(H(out["ret"][s:s + 1]), ref["ret"][:1], np.abs(ref["ret"][:1]) + 1.0, what="ret")
     del dr
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("kind", ["transition", "sequence"])
+def test_gather_batch_min_weights(rpl, kind, variant):
+    # qmin = NULL: the gather normalises the IS weights by the batch min over idx >= 0
+    g = rng(8)
+    if kind == "transition":
+        ring = make_ring(71, cap=64, B=8, ep_len=9.0)
+        idx = valid_transition_leaves(ring, 4, 3, 40, g)
+        kw = dict(kind="transition", k=4, n_step=3)
+    else:
+        ring = make_ring(72, cap=400, B=4, ep_len=30.0, period=40, rnn_h=8, reward_kind="r2d2")
+        idx = []
+        while len(idx) < 40:
+            blk, b = int(g.integers(0, 10)), int(g.integers(0, 4))
+            if OG.window_valid_sequence(blk * 40, 400, ring.cursor, ring.size, 4, 45):
+                idx.append(blk * 4 + b)
+        idx = np.array(idx, np.int64)
+        kw = dict(kind="sequence", k=4, seq_len=45, period=40)
+    idx[3] = -1  # skipped entry: its (tiny) q must not enter the min
+    q = g.integers(1 << 20, 1 << 40, idx.size).astype(np.int64)
+    q[3] = 1
+    dr = dev_ring(rpl, ring)
+    out = rpl.gather(dr, T_(idx), q=T_(q), qmin=None, beta=0.6, want=["w", "obs"], **kw)
+    qm = int(q[idx >= 0].min())
+    ok = idx >= 0
+    check_rel(H(out["w"])[ok], (qm / q[ok].astype(np.float64)) ** 0.6, what="batch-min w")

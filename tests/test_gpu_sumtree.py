@@ -286,3 +286,21 @@ def test_sample_uniform_errors(rpl):
     assert lib.rpl_sample_uniform(0, 1, 0, None, 0, 1, 1, 1, 1, None) == -1
     assert lib.rpl_sample_uniform(1, 1, 0, None, 5, 1, 4, 1, 1, None) == -1   # lo_row >= cap
     assert lib.rpl_sample_uniform(1, 1, 0, None, 0, 5, 4, 1, 1, None) == -1   # n_rows > cap
+
+
+def test_stream_without_reduction_matches(rpl):
+    # sample_stream with no qmin / IS weights (no grid-wide reduction) draws the same
+    # strata and advances the stream exactly like the reducing call
+    a = rpl.SumTree(25600, 32)
+    b = rpl.SumTree(25600, 32)
+    g = rng(21)
+    td = T_(td_abs(g, 25600))
+    ii = T_(np.arange(25600, dtype=np.int64))
+    a.update(ii, td, 0.9)
+    b.update(ii, td, 0.9)
+    for _ in range(3):
+        ia, qa, ma, wa = a.sample_stream(200, 9, beta=0.6)
+        ib, qb, mb, wb = b.sample_stream(200, 9, want_qmin=False)
+        assert mb is None and wb is None
+        assert np.array_equal(H(ia), H(ib)) and np.array_equal(H(qa), H(qb))
+    assert np.array_equal(H(a.header), H(b.header))
