@@ -1082,6 +1082,276 @@ int launch_seq_lsu(const GDesc& g, const int64_t* idx, int64_t n, int NS, int64_
                     rows_per_cta, q, qmin, beta, dev_err);
 }
 
+// ---------------------------------------------------------------------------
+// Sequences, variant 6: LSU frame loads, TMA bulk stores.  The mirror image of the
+// default kernel: loader warps stream the unique frames global -> registers ->
+// shared memory (ld.global.cs, evict-first) and flag each slot; ONE thread issues
+// every k-stack store as cp.async.bulk shared -> global (L2 evict-first), so the
+// SM's TMA queue carries only stores (measured ceiling for 28-KB bulk stores:
+// 6.3 TB/s) and the LSU only the 1-in-5 bytes that are loads.  The issuer keeps
+// LB_G row groups in flight and releases frames once their group has been read.
+// Same tables, meta warp and outputs as the default kernel.
+// ---------------------------------------------------------------------------
+constexpr int LB_G = 8;
+
+__device__ __forceinline__ void bulk_s2g_ef(void* dst, const void* src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes), "l"(pol)
+               : "memory");
+}
+
+template <int NL>
+__global__ void __launch_bounds__((NL + 2) * 32, 1)
+k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, int64_t rows_per_cta,
+                      const int64_t* __restrict__ q, const int64_t* __restrict__ qmin, double beta, int32_t* err) {
+  extern __shared__ __align__(128) uint8_t smem[];  // NS frame slots + 1 zero slot
+  __shared__ int p_b[PL_MAX_ROWS];
+  __shared__ int p_row0[PL_MAX_ROWS];
+  __shared__ int p_blk[PL_MAX_ROWS];
+  __shared__ int p_F[PL_MAX_ROWS];
+  __shared__ int p_R[PL_MAX_ROWS];
+  __shared__ int row_first[PL_MAX_ROWS];
+  __shared__ int rel[PL_MAX_ROWS];
+  __shared__ int row_ring[PL_MAX_ROWS];
+  __shared__ short row_piece[PL_MAX_ROWS];
+  __shared__ short row_tau[PL_MAX_ROWS];
+  __shared__ int8_t start_off[PL_MAX_ROWS];
+  __shared__ volatile int frame_ready[PIPE_MAX_NS];
+  __shared__ volatile int s_released;
+  __shared__ int s_ftotal;
+  constexpr int NT = (NL + 2) * 32;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int k = D.k, L = D.seq_len;
+  const int ob = (int)D.obs_bytes;
+  const int nv = ob / 16;
+  const int cap = (int)D.cap_T, Bc = (int)D.B, period = (int)D.period;
+  const int total = (int)(n * (int64_t)L);
+  const int g0 = (int)((int64_t)blockIdx.x * rows_per_cta);
+  const int g1 = min(total, g0 + (int)rows_per_cta);
+  if (g0 >= g1) return;
+  const int nrows = g1 - g0;
+  const int s_first = g0 / L;
+  const int npieces = (g1 - 1) / L - s_first + 1;
+  const int64_t nleaves = (int64_t)(cap / period) * Bc;
+  uint8_t* zslot = smem + NS * ob;
+
+  for (int i = tid; i < NS; i += NT) frame_ready[i] = -1;
+  if (tid == 0) s_released = 0;
+  if (D.pad_mode == RPL_PAD_ZERO) {
+    for (int v = tid; v < nv; v += NT) reinterpret_cast<int4*>(zslot)[v] = make_int4(0, 0, 0, 0);
+    fence_proxy_async();
+  }
+  pdl_wait();
+  for (int pc = tid; pc < npieces; pc += NT) {
+    const int sm = s_first + pc;
+    const int tau0 = max(g0 - sm * L, 0);
+    const int64_t leaf = idx[sm];
+    int bcol = -1, row0 = 0, blk = 0;
+    if (leaf >= 0 && leaf < nleaves) {
+      blk = (int)(leaf / Bc);
+      bcol = (int)(leaf - (int64_t)blk * Bc);
+      row0 = (int)(((int64_t)blk * period + tau0) % cap);
+      if (tau0 == 0) {
+        const int64_t age = wrap(D.cursor - 1 - (int64_t)blk * period, D.cap_T);
+        const int hist = k - 1 > 1 ? k - 1 : 1;
+        if (!(age >= L - 1 && age + hist <= D.size - 1)) set_err(err, RPL_DERR_INVALID_LEAF);
+      }
+    } else if (leaf >= nleaves && tau0 == 0) {
+      set_err(err, RPL_DERR_IDX);
+    }
+    p_b[pc] = bcol;
+    p_row0[pc] = row0;
+    p_blk[pc] = blk;
+    p_R[pc] = min(g1, (sm + 1) * L) - max(g0, sm * L);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int F = 0;
+    for (int pc = 0; pc < npieces; ++pc) {
+      p_F[pc] = F;
+      if (p_b[pc] >= 0) F += p_R[pc] + k - 1;
+    }
+    s_ftotal = F;
+  }
+  __syncthreads();
+  // row tables + episode-start offsets (all warps)
+  for (int c = tid; c < nrows; c += NT) {
+    const int g = g0 + c;
+    const int sm = g / L;
+    const int tau = g - sm * L;
+    const int pc = sm - s_first;
+    const int bcol = p_b[pc];
+    const int m = g - max(g0, sm * L);
+    int8_t so = 0;
+    int ring = 0;
+    if (bcol >= 0) {
+      const int R = p_R[pc];
+      const int F = p_F[pc];
+      row_first[c] = F + m;
+      rel[c] = m == R - 1 ? F + R + k - 1 : F + m + 1;
+      ring = p_row0[pc] + m;
+      if (ring >= cap) ring -= cap;
+      uint8_t dw[8];
+#pragma unroll
+      for (int j = 1; j < 8; ++j) {
+        int rr = ring - k + j;
+        while (rr < 0) rr += cap;
+        dw[j] = j < k ? __ldg(D.done + (int64_t)rr * Bc + bcol) : (uint8_t)0;
+      }
+#pragma unroll
+      for (int j = 1; j < 8; ++j)
+        if (dw[j]) so = (int8_t)j;
+    } else {
+      row_first[c] = -1;
+      rel[c] = p_F[pc];
+    }
+    row_ring[c] = ring;
+    row_piece[c] = (short)pc;
+    row_tau[c] = (short)tau;
+    start_off[c] = so;
+  }
+  __syncthreads();
+  const int ftotal = s_ftotal;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- store issuer: TMA bulk stores only ----------------
+      uint64_t pol;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      for (int c = 0; c < nrows; ++c) {
+        const int p0 = row_first[c];
+        if (p0 >= 0 && !(D.diag & 1)) {
+          const int so = start_off[c];
+          const int sm = s_first + row_piece[c];
+          const int tau = row_tau[c];
+          const int s0 = p0 % NS;
+          for (int j = so; j < k; ++j) {
+            int sl = s0 + j;
+            if (sl >= NS) sl -= NS;
+            while (frame_ready[sl] != p0 + j + 1) __nanosleep(20);
+          }
+          fence_proxy_async();
+          uint8_t* dst = D.o_obs + ((int64_t)tau * n + sm) * k * ob;
+          if (so == 0 && s0 + k <= NS) {
+            bulk_s2g_ef(dst, smem + s0 * ob, (uint32_t)(k * ob), pol);
+          } else {
+            for (int j = 0; j < k; ++j) {
+              const uint8_t* src;
+              if (j < so && D.pad_mode == RPL_PAD_ZERO) {
+                src = zslot;
+              } else {
+                int sl = s0 + (j < so ? so : j);
+                if (sl >= NS) sl -= NS;
+                src = smem + sl * ob;
+              }
+              bulk_s2g_ef(dst + j * ob, src, (uint32_t)ob, pol);
+            }
+          }
+        }
+        bulk_commit();
+        bulk_wait_read_G<LB_G>();
+        if (c >= LB_G) s_released = rel[c - LB_G];
+      }
+      bulk_wait_all();
+    }
+  } else if (warp == 1) {
+    // ---------------- meta warp (as in the default kernel) ----------------
+    const int64_t qm = (D.o_w && q) ? warp_batch_qmin(qmin, idx, q, n) : 0;
+    const int64_t ab = D.act_bytes;
+    const bool a8 = ab == 8 && ((reinterpret_cast<uintptr_t>(D.act) | reinterpret_cast<uintptr_t>(D.o_act) |
+                                 reinterpret_cast<uintptr_t>(D.o_prev_act)) & 7) == 0;
+    for (int c = lane; c < nrows && !(D.diag & 16); c += 32) {
+      if (row_first[c] < 0) continue;
+      const int pc = row_piece[c];
+      const int sm = s_first + pc;
+      const int tau = row_tau[c];
+      const int bcol = p_b[pc];
+      const int ring = row_ring[c];
+      const int prow = ring == 0 ? cap - 1 : ring - 1;
+      const int64_t e = (int64_t)ring * Bc + bcol, pe = (int64_t)prow * Bc + bcol;
+      const uint8_t pd = __ldg(D.done + pe);
+      const uint8_t dd = __ldg(D.done + e);
+      const float rw = D.o_rew ? __ldg(D.rew + e) : 0.0f;
+      const float prw = D.o_prev_rew ? __ldg(D.rew + pe) : 0.0f;
+      const int64_t o = (int64_t)tau * n + sm;
+      if (a8) {
+        const uint64_t* a = reinterpret_cast<const uint64_t*>(D.act);
+        const uint64_t av = D.o_act ? __ldg(a + e) : 0ull;
+        const uint64_t pav = D.o_prev_act ? __ldg(a + pe) : 0ull;
+        if (D.o_act) reinterpret_cast<uint64_t*>(D.o_act)[o] = av;
+        if (D.o_prev_act) reinterpret_cast<uint64_t*>(D.o_prev_act)[o] = pd ? 0ull : pav;
+      } else {
+        if (D.o_act) coop_copy(D.o_act + o * ab, D.act + e * ab, ab, 0, 1);
+        if (D.o_prev_act) {
+          if (pd) coop_zero(D.o_prev_act + o * ab, ab, 0, 1);
+          else coop_copy(D.o_prev_act + o * ab, D.act + pe * ab, ab, 0, 1);
+        }
+      }
+      if (D.o_rew) D.o_rew[o] = rw;
+      if (D.o_prev_rew) D.o_prev_rew[o] = pd ? 0.0f : prw;
+      if (D.o_done) D.o_done[o] = dd;
+      if (tau == 0 && D.o_w && q) {
+        const int64_t qs = q[sm];
+        D.o_w[sm] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
+      }
+    }
+    if (D.o_rnn && !(D.diag & 16)) {
+      const int nparts = D.rnn_parts;
+      const int64_t rb = D.rnn_bytes;
+      for (int pc = 0; pc < npieces; ++pc) {
+        const int sm = s_first + pc;
+        if (sm * L < g0 || p_b[pc] < 0) continue;
+        const int64_t blk = p_blk[pc], bcol = p_b[pc];
+        for (int pp = 0; pp < nparts; ++pp)
+          coop_copy(D.o_rnn + (pp * n + sm) * rb, D.rnn + ((blk * Bc + bcol) * nparts + pp) * rb, rb, lane, 32);
+      }
+    }
+  } else {
+    // ---------------- loaders: frames global -> registers -> shared memory ----------------
+    const int64_t rstride = (int64_t)Bc * ob;
+    int pc = 0;  // piece cursor (frame positions increase monotonically per warp)
+    for (int f = warp - 2; f < ftotal; f += NL) {
+      while (p_b[pc] < 0 || f >= p_F[pc] + p_R[pc] + k - 1) ++pc;
+      int row = p_row0[pc] - (k - 1) + (f - p_F[pc]);
+      while (row < 0) row += cap;
+      while (row >= cap) row -= cap;
+      const int4* src = reinterpret_cast<const int4*>(D.obs + (int64_t)p_b[pc] * ob + (int64_t)row * rstride);
+      while (f >= s_released + NS) __nanosleep(20);
+      const int sl = f % NS;
+      int4* dst = reinterpret_cast<int4*>(smem + sl * ob);
+      if (!(D.diag & 2)) {
+        constexpr int U = 8;
+        for (int v0 = lane; v0 < nv; v0 += 32 * U) {
+          int4 r[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (v0 + 32 * u < nv) r[u] = __ldcs(src + v0 + 32 * u);
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (v0 + 32 * u < nv) dst[v0 + 32 * u] = r[u];
+        }
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) frame_ready[sl] = f + 1;
+    }
+  }
+  pdl_trigger();
+}
+
+template <int NL>
+int launch_seq_ldg_bulk(const GDesc& g, const int64_t* idx, int64_t n, int NS, int64_t rows_per_cta,
+                        const int64_t* q, const int64_t* qmin, double beta, int32_t* dev_err, size_t dyn,
+                        int64_t grid, cudaStream_t st) {
+  static size_t set_l = 0;
+  if (dyn > 48 * 1024 && dyn > set_l) {
+    cudaFuncSetAttribute(k_gather_seq_ldg_bulk<NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    set_l = dyn;
+  }
+  return launch_pdl(k_gather_seq_ldg_bulk<NL>, dim3((unsigned)grid), dim3((NL + 2) * 32), dyn, st, g, idx, n, NS,
+                    rows_per_cta, q, qmin, beta, dev_err);
+}
+
 int env_diag() {
   const char* v = getenv("RPL_GATHER_DIAG");  // measurement only (rpl_debug_set_gather_diag)
   return v ? atoi(v) : 0;
@@ -1140,7 +1410,7 @@ int g_seq_variant = 0;
 using namespace rpl;
 
 extern "C" int rpl_debug_set_gather_variant(int32_t variant) {
-  if (variant < 0 || variant > 5) return RPL_EINVAL;
+  if (variant < 0 || variant > 6) return RPL_EINVAL;
   g_seq_variant = variant;
   return RPL_OK;
 }
@@ -1198,6 +1468,21 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       const int64_t rows = n * (int64_t)desc->seq_len;
       k_gather_seq_fields<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(g, idx, n, dev_err);
       return launch_status();
+    }
+    if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs && g_seq_variant == 6) {
+      int NS = (int)(200 * 1024 / desc->obs_bytes) - 1;  // + one zero slot
+      if (NS > PIPE_MAX_NS) NS = PIPE_MAX_NS;
+      const int k = desc->k;
+      const int64_t total = n * (int64_t)desc->seq_len;
+      if (NS >= LB_G + 3 * k && total < (1ll << 30) && desc->cap_T < (1ll << 30) && desc->B < (1ll << 30)) {
+        const size_t dyn = (size_t)(NS + 1) * desc->obs_bytes;
+        int64_t grid = (int64_t)sm_count();
+        int64_t rows_per_cta = (total + grid - 1) / grid;
+        if (rows_per_cta > PL_MAX_ROWS) rows_per_cta = PL_MAX_ROWS;
+        grid = (total + rows_per_cta - 1) / rows_per_cta;
+        g.use_tma = 1;
+        return launch_seq_ldg_bulk<8>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn, grid, st);
+      }
     }
     if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs &&
         (g_seq_variant == 0 || g_seq_variant == 4 || g_seq_variant == 5)) {
