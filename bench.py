@@ -63,6 +63,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget (cpu_baseline)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/baseline/e2e)")
     ap.add_argument("--seq-variant", type=int, default=None, help="diagnostics: sequence-gather kernel variant")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: functional checks only)")
+    ap.add_argument("--same-device", action="store_true",
+                    help="functional check: every rank on cuda:0 (with --backend gloo on a 1-GPU box)")
     return ap.parse_args()
 
 
@@ -169,10 +173,14 @@ def run_rpl(args):
     world, rank, local = dist_env()
     if args.gpus > 1 and world == 1:
         raise SystemExit("--gpus N > 1 must be launched with torchrun (one process per GPU)")
+    local = 0 if args.same_device else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     import paper_1909_01500_b200 as rpl
     from paper_1909_01500_b200 import replay as R
@@ -223,6 +231,16 @@ def run_rpl(args):
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     totals = torch.zeros(world, dtype=torch.int64, device=dev)
     my_total = torch.zeros(1, dtype=torch.int64, device=dev)
+    n_owned = torch.zeros(1, dtype=torch.int64, device=dev)
+    if world > 1:
+        # compacted sharded sample: this rank's owned draws first, the gather schedules only those
+        plan.desc.n_active = n_owned.data_ptr()
+
+    def all_gather_totals():
+        if args.backend == "nccl":
+            dist.all_gather_into_tensor(totals, my_total)
+        else:
+            dist.all_gather(list(totals.chunk(world)), my_total)
     r_tr = out["rew"][c["burn_in"]:c["burn_in"] + c["train"] + c["n_step"] - 1]
     d_tr = out["done"][c["burn_in"]:c["burn_in"] + c["train"] + c["n_step"] - 1]
     Tn = c["train"] + c["n_step"] - 1
@@ -240,18 +258,15 @@ def run_rpl(args):
                                                          P_(q_buf), None, None, P_(err), s), "sample")
         else:
             rpl._lib.check(lib.rpl_sumtree_total(tree._lp, P_(tree.storage), P_(my_total), s), "total")
-            dist.all_gather_into_tensor(totals, my_total)                       # K5: 8 B per rank
+            all_gather_totals()                                                  # K5: 8 B per rank
             rpl._lib.check(lib.rpl_sumtree_sample_sharded(tree._lp, P_(tree.storage), rank, world, n_leaves,
                                                           P_(totals), n_glob, None, seed, 0, 1, P_(cur), P_(q_buf),
-                                                          P_(qmin), P_(err), s), "sample_sharded")
+                                                          P_(qmin), P_(n_owned), P_(err), s), "sample_sharded")
             dist.all_reduce(qmin, op=dist.ReduceOp.MIN)                          # K7: global batch min
-            rpl._lib.check(lib.rpl_is_weights(P_(q_buf), P_(qmin), n_glob, c["beta"], P_(w), s), "w")
         if gather_events is not None:
             gather_events[0].record()
-        if world == 1:
-            plan.run(cur, q=q_buf, qmin=None, beta=c["beta"], stream=s)
-        else:
-            plan.run(cur, stream=s)
+        # IS weights fused into the gather: batch min (1 GPU) or the all-reduced global min (Mode L)
+        plan.run(cur, q=q_buf, qmin=None if world == 1 else qmin, beta=c["beta"], stream=s)
         if gather_events is not None:
             gather_events[1].record()
         rpl._lib.check(lib.rpl_returns_nstep(P_(r_tr), P_(d_tr), Tn, n_glob, c["n_step"], c["gamma"],
@@ -266,16 +281,23 @@ def run_rpl(args):
     torch.cuda.synchronize()
     rpl.check_err(err)
 
-    use_graph = (not args.no_graph) and world == 1
+    # CUDA graph of P steps; with N > 1 the NCCL collectives are captured too (gloo: eager)
+    use_graph = (not args.no_graph) and (world == 1 or args.backend == "nccl")
     graph = None
     if use_graph:
-        s = torch.cuda.Stream(dev)
-        s.wait_stream(torch.cuda.current_stream(dev))
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=s):
-            for i in range(P):
-                step(i)
-        torch.cuda.synchronize()
+        try:
+            s = torch.cuda.Stream(dev)
+            s.wait_stream(torch.cuda.current_stream(dev))
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=s):
+                for i in range(P):
+                    step(i)
+            torch.cuda.synchronize()
+        except Exception as e:  # capture unsupported here: fall back to eager launches
+            print(f"[bench] graph capture failed ({type(e).__name__}: {e}); timing eager steps", file=sys.stderr)
+            graph = None
+            use_graph = False
+            torch.cuda.synchronize()
     K = args.steps
     reps = math.ceil(K / P) if use_graph else K
     K_eff = reps * P if use_graph else K
@@ -303,7 +325,7 @@ def run_rpl(args):
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    launches = (rpl.launch_count() - launches0) if not use_graph else 4 * K_eff
+    launches = (rpl.launch_count() - launches0) if not use_graph else (4 if world == 1 else 5) * K_eff
     clk = clocks.stop() if not args.profile else {}
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:

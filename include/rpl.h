@@ -169,12 +169,18 @@ int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree, int64_t n
  * out_q[k] (0 when not owned), *out_qmin = min over owned (INT64_MAX if none).  Equal to
  * rpl_sumtree_sample on the concatenation of the shards (§8c #17).  use_stream != 0 (draws
  * must be NULL) takes the Philox counter from this tree's stream position as
- * rpl_sumtree_sample_stream does; every rank's position advances by n identically. */
+ * rpl_sumtree_sample_stream does; every rank's position advances by n identically.
+ * out_count (device int64, may be NULL): when given, the output is COMPACTED — the owned
+ * draws (a contiguous run of strata, because prefixes are non-decreasing in k) are written
+ * to positions 0..m-1 in stratum order, positions m..n-1 get idx -1 / q 0, and
+ * *out_count = m; pass it to rpl_gather_desc.n_active so the gather only schedules m
+ * samples.  out_qmin may be NULL (no batch reduction). */
 int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t rank,
                                int32_t n_shards, int64_t shard_leaves, const int64_t* shard_totals,
                                int64_t n, const uint64_t* draws, uint64_t seed, uint64_t offset,
                                int32_t use_stream, int64_t* out_idx, int64_t* out_q,
-                               int64_t* out_qmin, int32_t* dev_err, void* stream);
+                               int64_t* out_qmin, int64_t* out_count, int32_t* dev_err,
+                               void* stream);
 
 /* Descent for explicit prefixes: out_idx[k] = leaf with C_i <= prefix[k] < C_{i+1}.
  * prefix >= total -> clamped to the last non-empty leaf + RPL_DERR_TREE. */
@@ -261,6 +267,10 @@ typedef struct {
   uint8_t* o_done_n;
   float* o_w;
   void* o_rnn;
+  /* Optional device int64 (may be NULL): only entries k < *n_active are gathered, the rest
+   * are skipped as if idx[k] < 0.  With the compacted sharded sampler this lets the
+   * persistent gather spread exactly the owned samples over all SMs. */
+  const int64_t* n_active;
 } rpl_gather_desc;
 
 int rpl_gather(const rpl_gather_desc* desc /* host */, const int64_t* idx, const int64_t* q,

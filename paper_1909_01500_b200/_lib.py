@@ -51,6 +51,7 @@ class GatherDesc(C.Structure):
         ("o_obs", C.c_void_p), ("o_next_obs", C.c_void_p), ("o_act", C.c_void_p), ("o_prev_act", C.c_void_p),
         ("o_rew", C.c_void_p), ("o_prev_rew", C.c_void_p), ("o_done", C.c_void_p), ("o_ret", C.c_void_p),
         ("o_done_n", C.c_void_p), ("o_w", C.c_void_p), ("o_rnn", C.c_void_p),
+        ("n_active", C.c_void_p),
     ]
 
 
@@ -75,7 +76,7 @@ _SIGS = {
     "rpl_sumtree_sample": ([C.POINTER(TreeLayout), P, I64, P, U64, U64, D, P, P, P, P, P, P], C.c_int),
     "rpl_sumtree_sample_stream": ([C.POINTER(TreeLayout), P, I64, U64, D, P, P, P, P, P, P], C.c_int),
     "rpl_sumtree_sample_sharded": ([C.POINTER(TreeLayout), P, I32, I32, I64, P, I64, P, U64, U64, I32, P, P, P, P,
-                                    P], C.c_int),
+                                    P, P], C.c_int),
     "rpl_sumtree_find": ([C.POINTER(TreeLayout), P, P, I64, P, P, P], C.c_int),
     "rpl_sumtree_total": ([C.POINTER(TreeLayout), P, P, P], C.c_int),
     "rpl_sumtree_rebuild": ([C.POINTER(TreeLayout), P, P], C.c_int),

@@ -154,7 +154,15 @@ struct GDesc {
   uint8_t* o_rnn;
   int use_tma;
   int diag;  // rpl_debug_set_gather_diag mask (0 in normal operation)
+  const int64_t* n_active;  // device count of leading entries to gather (NULL: all n)
 };
+
+// Number of leading entries of idx to gather (rpl_gather_desc.n_active); read after pdl_wait.
+__device__ __forceinline__ int64_t active_n(const GDesc& D, int64_t n) {
+  if (!D.n_active) return n;
+  const int64_t a = *D.n_active;
+  return a < 0 ? 0 : (a < n ? a : n);
+}
 
 __device__ __forceinline__ int64_t wrap(int64_t r, int64_t cap) {
   r %= cap;
@@ -187,6 +195,7 @@ k_gather_transition(GDesc D, const int64_t* __restrict__ idx, int64_t n, const i
   const int tid = threadIdx.x;
   const int64_t s = blockIdx.x;
   pdl_wait();
+  if (s >= active_n(D, n)) return;
   const int64_t leaf = idx[s];
   if (leaf < 0) return;
   const int k = D.k, ns = D.n_step;
@@ -314,6 +323,7 @@ k_gather_sequence(GDesc D, const int64_t* __restrict__ idx, int64_t n, const int
   __shared__ int sslot[SEQ_CHUNK][8];
   const int tid = threadIdx.x;
   const int64_t s = blockIdx.y;
+  if (s >= active_n(D, n)) return;
   const int c = blockIdx.x;
   const int64_t leaf = idx[s];
   if (leaf < 0) return;
@@ -487,6 +497,7 @@ k_gather_seq_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, i
   __shared__ int rel_hist[64];
   __shared__ volatile int free_count;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t n_eff = active_n(D, n);
   const int k = D.k, L = D.seq_len;
   const int64_t ob = D.obs_bytes;
   const int64_t total = n * (int64_t)L;
@@ -507,7 +518,7 @@ k_gather_seq_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, i
     const int64_t g = g0 + c;
     const int64_t s = g / L;
     const int tau = (int)(g - s * L);
-    const int64_t leaf = idx[s];
+    const int64_t leaf = s < n_eff ? idx[s] : -1;
     int8_t so = 0;
     if (leaf >= 0 && leaf < nblk * D.B) {
       const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
@@ -543,7 +554,7 @@ k_gather_seq_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, i
         const int64_t s = g / L;
         const int tau0 = (int)(g - s * L);
         const int R = (int)min((int64_t)(L - tau0), g1 - g);
-        const int64_t leaf = idx[s];
+        const int64_t leaf = s < n_eff ? idx[s] : -1;
         if (leaf >= 0 && leaf < nblk * D.B) {
           const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
           const int64_t first = blk * D.period + tau0 - (k - 1);
@@ -571,7 +582,7 @@ k_gather_seq_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, i
         const int64_t s = g / L;
         const int tau0 = (int)(g - s * L);
         const int R = (int)min((int64_t)(L - tau0), g1 - g);
-        const int64_t leaf = idx[s];
+        const int64_t leaf = s < n_eff ? idx[s] : -1;
         const bool ok = leaf >= 0 && leaf < nblk * D.B;
         for (int m = 0; m < R; ++m, ++c) {
           if (ok) {
@@ -616,7 +627,7 @@ k_gather_seq_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, i
       const int64_t gg = g0 + c;
       const int64_t s = gg / L;
       const int tau = (int)(gg - s * L);
-      const int64_t leaf = idx[s];
+      const int64_t leaf = s < n_eff ? idx[s] : -1;
       if (leaf < 0 || leaf >= nblk * D.B) continue;
       const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
       const int64_t row = wrap(blk * D.period + tau, D.cap_T);
@@ -639,7 +650,7 @@ k_gather_seq_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, i
     // stored recurrent state for samples whose row 0 lies in this CTA
     if (D.o_rnn) {
       for (int64_t s = (g0 + L - 1) / L; s * L < g1; ++s) {
-        const int64_t leaf = idx[s];
+        const int64_t leaf = s < n_eff ? idx[s] : -1;
         if (leaf < 0 || leaf >= nblk * D.B) continue;
         const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
         for (int p = 0; p < D.rnn_parts; ++p)
@@ -680,7 +691,7 @@ k_gather_seq_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, const int6
   if (task >= n * W) return;
   const int64_t s = task / W;
   const int w = (int)(task - s * W) - (k - 1);  // window row, -(k-1) .. L-1
-  const int64_t leaf = idx[s];
+  const int64_t leaf = s < active_n(D, n) ? idx[s] : -1;
   const int64_t nblk = D.cap_T / D.period;
   if (leaf < 0) return;
   if (leaf >= nblk * D.B) {
@@ -757,7 +768,7 @@ __global__ void k_gather_seq_fields(GDesc D, const int64_t* __restrict__ idx, in
   for (int64_t gg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gg < n * L; gg += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = gg / L;
     const int tau = (int)(gg - s * L);
-    const int64_t leaf = idx[s];
+    const int64_t leaf = s < active_n(D, n) ? idx[s] : -1;
     if (leaf < 0 || leaf >= nblk * D.B) continue;
     const int64_t blk = leaf / D.B, b = leaf - blk * D.B;
     const int64_t row = wrap(blk * D.period + tau, D.cap_T);
@@ -833,14 +844,17 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   const int ob = (int)D.obs_bytes;
   const int nv = ob / 16;
   const int cap = (int)D.cap_T, Bc = (int)D.B, period = (int)D.period;
-  const int total = (int)(n * (int64_t)L);
-  const int g0 = (int)((int64_t)blockIdx.x * rows_per_cta);
-  const int g1 = min(total, g0 + (int)rows_per_cta);
+  const int64_t nleaves = (int64_t)(cap / period) * Bc;
+  pdl_wait();  // idx (and n_active) come from the sampler launched just before
+  // rows g = s*L + tau of the active samples, split evenly over the grid
+  const int total = (int)(active_n(D, n) * L);
+  const int rpc = D.n_active ? (total + (int)gridDim.x - 1) / (int)gridDim.x : (int)rows_per_cta;
+  const int g0 = (int)blockIdx.x * rpc;
+  const int g1 = min(total, g0 + rpc);
   if (g0 >= g1) return;
   const int nrows = g1 - g0;
   const int s_first = g0 / L;
   const int npieces = (g1 - 1) / L - s_first + 1;
-  const int64_t nleaves = (int64_t)(cap / period) * Bc;
 
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
@@ -848,7 +862,6 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
     s_npieces = npieces;
   }
   for (int c = tid; c < nrows; c += NT) row_done[c] = 0;
-  pdl_wait();  // idx comes from the sampler launched just before
   // (A) pieces, in parallel: one sampled leaf each
   for (int pc = tid; pc < npieces; pc += NT) {
     const int sm = s_first + pc;
@@ -1125,14 +1138,17 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   const int ob = (int)D.obs_bytes;
   const int nv = ob / 16;
   const int cap = (int)D.cap_T, Bc = (int)D.B, period = (int)D.period;
-  const int total = (int)(n * (int64_t)L);
-  const int g0 = (int)((int64_t)blockIdx.x * rows_per_cta);
-  const int g1 = min(total, g0 + (int)rows_per_cta);
+  const int64_t nleaves = (int64_t)(cap / period) * Bc;
+  pdl_wait();  // idx (and n_active) come from the sampler launched just before
+  // rows g = s*L + tau of the active samples, split evenly over the grid
+  const int total = (int)(active_n(D, n) * L);
+  const int rpc = D.n_active ? (total + (int)gridDim.x - 1) / (int)gridDim.x : (int)rows_per_cta;
+  const int g0 = (int)blockIdx.x * rpc;
+  const int g1 = min(total, g0 + rpc);
   if (g0 >= g1) return;
   const int nrows = g1 - g0;
   const int s_first = g0 / L;
   const int npieces = (g1 - 1) / L - s_first + 1;
-  const int64_t nleaves = (int64_t)(cap / period) * Bc;
   uint8_t* zslot = smem + NS * ob;
 
   for (int i = tid; i < NS; i += NT) frame_ready[i] = -1;
@@ -1141,7 +1157,6 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
     for (int v = tid; v < nv; v += NT) reinterpret_cast<int4*>(zslot)[v] = make_int4(0, 0, 0, 0);
     fence_proxy_async();
   }
-  pdl_wait();
   for (int pc = tid; pc < npieces; pc += NT) {
     const int sm = s_first + pc;
     const int tau0 = max(g0 - sm * L, 0);
@@ -1394,6 +1409,7 @@ GDesc to_dev(const rpl_gather_desc* d) {
   g.o_rnn = static_cast<uint8_t*>(d->o_rnn);
   g.use_tma = 0;
   g.diag = g_seq_diag;
+  g.n_active = d->n_active;
   return g;
 }
 

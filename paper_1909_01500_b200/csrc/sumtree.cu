@@ -145,6 +145,29 @@ __device__ __forceinline__ uint64_t stratum_lo(uint64_t k, uint64_t Q, uint64_t 
   return k * (Q / n) + (k * (Q % n)) / n;
 }
 
+// Global prefix of stratum k (a8, §8c #8): lo_k + floor(u_k (hi_k - lo_k) / 2^64).
+// Non-decreasing in k (prefix_k < hi_k = lo_{k+1} <= prefix_{k+1}, or = lo_k for an
+// empty stratum), so the strata a shard owns form one contiguous run.
+__device__ __forceinline__ uint64_t stratum_prefix(int64_t k, uint64_t Q, int64_t n, const uint64_t* draws,
+                                                   uint64_t seed, uint64_t ctr0) {
+  const uint64_t lo = stratum_lo((uint64_t)k, Q, (uint64_t)n);
+  const uint64_t hi = stratum_lo((uint64_t)k + 1, Q, (uint64_t)n);
+  const uint64_t u = draws ? draws[k] : philox_u64(seed, ctr0 + (uint64_t)k);
+  return lo + __umul64hi(u, hi - lo);
+}
+
+// First stratum k in [0, n] whose prefix is >= x (n if none).
+__device__ __forceinline__ int64_t first_stratum_at_least(uint64_t x, uint64_t Q, int64_t n, const uint64_t* draws,
+                                                          uint64_t seed, uint64_t ctr0) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (stratum_prefix(mid, Q, n, draws, seed, ctr0) < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
 // Descend from the root for `prefix` (< node sum); returns leaf index, writes q.
 __device__ __forceinline__ int64_t descend(const TreeDev& L, const int64_t* __restrict__ tree,
                                            int64_t prefix, int64_t* q_out, int32_t* errbits) {
@@ -188,7 +211,7 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
               uint64_t seed, uint64_t offset, double beta, int64_t* __restrict__ out_idx,
               int64_t* __restrict__ out_q, int64_t* __restrict__ out_qmin, float* __restrict__ out_w,
               int32_t* err, int rank, int n_shards, int64_t shard_leaves,
-              const int64_t* __restrict__ totals, int use_stream) {
+              const int64_t* __restrict__ totals, int use_stream, int64_t* __restrict__ out_count) {
   const int lane = threadIdx.x & 31;
   pdl_wait();
   // Without a batch reduction (no IS weights, no qmin requested) there is no grid-wide
@@ -219,16 +242,22 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
   } else {
     Q = (uint64_t)tree[L.level_off[0]];
   }
+  // compacted sharded output: the owned run of strata [k0, k1) goes to positions
+  // 0 .. m-1 (stratum order), positions m .. n-1 get -1; *out_count = m
+  const bool compact = SHARDED && out_count != nullptr;
+  int64_t k0 = 0, m_own = 0;
+  if (compact && Q > 0) {
+    k0 = first_stratum_at_least(own_lo, Q, n, draws, seed, ctr0);
+    m_own = first_stratum_at_least(own_lo + own_T, Q, n, draws, seed, ctr0) - k0;
+  }
   if (k < n) {
     int64_t leaf = -1, q = 0;
+    bool mine = false;
     if (Q == 0) {
       errbits |= RPL_DERR_EMPTY;
     } else {
-      const uint64_t lo = stratum_lo((uint64_t)k, Q, (uint64_t)n);
-      const uint64_t hi = stratum_lo((uint64_t)k + 1, Q, (uint64_t)n);
-      const uint64_t u = draws ? draws[k] : philox_u64(seed, ctr0 + (uint64_t)k);
-      uint64_t prefix = lo + __umul64hi(u, hi - lo);
-      bool mine = true;
+      uint64_t prefix = stratum_prefix(k, Q, n, draws, seed, ctr0);
+      mine = true;
       if (SHARDED) {
         mine = prefix >= own_lo && prefix < own_lo + own_T;
         prefix -= own_lo;
@@ -239,8 +268,20 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
       }
     }
     if (lane == 0) {
-      out_idx[k] = leaf;
-      out_q[k] = q;
+      if (!compact) {
+        out_idx[k] = leaf;
+        out_q[k] = q;
+      } else {
+        if (mine) {
+          out_idx[k - k0] = leaf;
+          out_q[k - k0] = q;
+        }
+        if (k >= m_own) {
+          out_idx[k] = -1;
+          out_q[k] = 0;
+        }
+        if (k == 0) *out_count = m_own;
+      }
     }
   }
   if (lane == 0 && errbits) set_err(err, errbits);
@@ -463,7 +504,7 @@ extern "C" int rpl_sumtree_sample(const rpl_tree_layout* L, int64_t* tree, int64
   const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
   return launch_pdl(k_tree_sample<false>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
                     tree_dev(L), tree, n, draws, seed, offset, beta, out_idx, out_q, out_qmin, out_w, dev_err, 0, 1,
-                    (int64_t)0, (const int64_t*)nullptr, 0);
+                    (int64_t)0, (const int64_t*)nullptr, 0, (int64_t*)nullptr);
 }
 
 extern "C" int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree, int64_t n, uint64_t seed,
@@ -474,21 +515,21 @@ extern "C" int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree
   const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
   return launch_pdl(k_tree_sample<false>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
                     tree_dev(L), tree, n, (const uint64_t*)nullptr, seed, (uint64_t)0, beta, out_idx, out_q, out_qmin,
-                    out_w, dev_err, 0, 1, (int64_t)0, (const int64_t*)nullptr, 1);
+                    out_w, dev_err, 0, 1, (int64_t)0, (const int64_t*)nullptr, 1, (int64_t*)nullptr);
 }
 
 extern "C" int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t rank, int32_t n_shards,
                                           int64_t shard_leaves, const int64_t* shard_totals, int64_t n,
                                           const uint64_t* draws, uint64_t seed, uint64_t offset, int32_t use_stream,
-                                          int64_t* out_idx, int64_t* out_q, int64_t* out_qmin, int32_t* dev_err,
-                                          void* stream) {
+                                          int64_t* out_idx, int64_t* out_q, int64_t* out_qmin, int64_t* out_count,
+                                          int32_t* dev_err, void* stream) {
   if (draws && use_stream) return RPL_EINVAL;
   if (!layout_ok(L) || !tree || !out_idx || !out_q || !shard_totals || n < 1 || n > (1ll << 30)) return RPL_EINVAL;
   if (n_shards < 1 || rank < 0 || rank >= n_shards || shard_leaves < L->n_leaves) return RPL_EINVAL;
   const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
   return launch_pdl(k_tree_sample<true>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
                     tree_dev(L), tree, n, draws, seed, offset, 0.0, out_idx, out_q, out_qmin, (float*)nullptr, dev_err,
-                    (int)rank, (int)n_shards, shard_leaves, shard_totals, (int)use_stream);
+                    (int)rank, (int)n_shards, shard_leaves, shard_totals, (int)use_stream, out_count);
 }
 
 extern "C" int rpl_sumtree_find(const rpl_tree_layout* L, const int64_t* tree, const int64_t* prefix, int64_t n,

@@ -233,9 +233,13 @@ class SumTree:
         return idx, q, qmin, w
 
     def sample_sharded(self, rank, n_shards, shard_totals, n, draws=None, seed=0, offset=0, out=None, err=None,
-                       use_stream=False):
+                       use_stream=False, count=None):
+        """rpl_sumtree_sample_sharded.  count (1-element int64 CUDA tensor) selects the compacted
+        output: owned draws first, *count = their number."""
         n = int(n)
         _req(shard_totals, torch.int64, "shard_totals", (n_shards,))
+        if count is not None:
+            _req(count, torch.int64, "count", (1,))
         if out is None:
             idx = torch.empty(n, dtype=torch.int64, device=self.device)
             q = torch.empty(n, dtype=torch.int64, device=self.device)
@@ -247,7 +251,7 @@ class SumTree:
                                              self.n_leaves, _ptr(shard_totals), n, _ptr(draws),
                                              int(seed) & (2 ** 64 - 1), int(offset) & (2 ** 64 - 1),
                                              1 if use_stream else 0, _ptr(idx),
-                                             _ptr(q), _ptr(qmin), _ptr(e), self._s()),
+                                             _ptr(q), _ptr(qmin), _ptr(count), _ptr(e), self._s()),
               "rpl_sumtree_sample_sharded")
         return idx, q, qmin
 

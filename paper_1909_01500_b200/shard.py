@@ -12,7 +12,8 @@ proportional sample over the union of the shards needs one exchange per step:
       by the global batch max weight (§8c #10).
 
 Frames never cross NVLink: each rank gathers its owned samples locally and feeds
-its own learner.  The result equals rpl_sumtree_sample on the shard-major
+its own learner.  With compact=True the owned draws come first (count on the device),
+so the rank's gather schedules only them (rpl_gather_desc.n_active).  The result equals rpl_sumtree_sample on the shard-major
 concatenation of the trees (§8c #17; tests/test_gpu_sumtree.py).
 
 The tree object is duck-typed (total(), sample_sharded(), .device) so the
@@ -25,7 +26,7 @@ import torch.distributed as dist
 
 
 class ShardedSampler:
-    def __init__(self, tree, n_per_rank: int, seed: int, group=None, is_weights=None):
+    def __init__(self, tree, n_per_rank: int, seed: int, group=None, is_weights=None, compact=False):
         self.tree = tree
         self.group = group
         self.world = dist.get_world_size(group)
@@ -40,6 +41,8 @@ class ShardedSampler:
         self.qmin = torch.zeros(1, dtype=torch.int64, device=dev)
         self.w = torch.zeros(self.n_glob, dtype=torch.float32, device=dev)
         self._is_weights = is_weights
+        self.compact = bool(compact)
+        self.count = torch.zeros(1, dtype=torch.int64, device=dev)
 
     def sample(self, beta: float):
         """One global stratified sample of n_glob draws.  Returns (idx, q, w): idx[k] is
@@ -47,8 +50,9 @@ class ShardedSampler:
         -1 elsewhere; w is normalised by the global batch min q."""
         self.tree.total(out=self.my_total)
         dist.all_gather_into_tensor(self.totals, self.my_total, group=self.group)          # K5
+        kw = {"count": self.count} if self.compact else {}
         self.tree.sample_sharded(self.rank, self.world, self.totals, self.n_glob, seed=self.seed,
-                                 out=(self.idx, self.q, self.qmin), use_stream=True)
+                                 out=(self.idx, self.q, self.qmin), use_stream=True, **kw)
         dist.all_reduce(self.qmin, op=dist.ReduceOp.MIN, group=self.group)                 # K7
         if self._is_weights is None:
             from .ops import is_weights

@@ -291,3 +291,49 @@ def test_gather_batch_min_weights(rpl, kind, variant):
     qm = int(q[idx >= 0].min())
     ok = idx >= 0
     check_rel(H(out["w"])[ok], (qm / q[ok].astype(np.float64)) ** 0.6, what="batch-min w")
+
+
+def test_sequence_n_active(rpl, variant):
+    # rpl_gather_desc.n_active: only entries k < *n_active are gathered; the rest are
+    # skipped exactly as idx < 0 (outputs left untouched) — every kernel variant
+    import torch
+    period, L, k = 40, 45, 4
+    ring = make_ring(91, cap=400, B=4, ep_len=25.0, period=period, rnn_h=16, reward_kind="r2d2")
+    dr = dev_ring(rpl, ring)
+    g = rng(9)
+    idx = []
+    while len(idx) < 30:
+        blk, b = int(g.integers(0, 10)), int(g.integers(0, 4))
+        if OG.window_valid_sequence(blk * period, 400, ring.cursor, ring.size, k, L):
+            idx.append(blk * 4 + b)
+    idx = np.array(idx, np.int64)
+    m = 17
+    plan = rpl.GatherPlan(dr, idx.size, kind="sequence", k=k, seq_len=L, period=period)
+    for t in plan.outputs.values():
+        t.fill_(7) if t.dtype != torch.float32 else t.fill_(7.5)
+    cnt = torch.tensor([m], dtype=torch.int64, device="cuda")
+    plan.desc.n_active = cnt.data_ptr()
+    out = plan.run(T_(idx))
+    ref = OG.gather_sequences(idx[:m], 4, ring.obs, ring.act, ring.rew, ring.done, ring.rnn, k, L, period)
+    for name in ("obs", "act", "prev_act", "rew", "prev_rew", "done"):
+        o = H(out[name])
+        assert np.array_equal(o[:, :m], ref[name]), name
+        assert np.all(o[:, m:] == (7.5 if o.dtype == np.float32 else 7)), name
+    assert np.array_equal(H(out["rnn"])[:, :m], ref["rnn"])
+
+
+def test_transition_n_active(rpl):
+    import torch
+    ring = make_ring(92, cap=64, B=8, ep_len=9.0)
+    dr = dev_ring(rpl, ring)
+    idx = valid_transition_leaves(ring, 4, 3, 50, rng(10))
+    m = 23
+    plan = rpl.GatherPlan(dr, idx.size, kind="transition", k=4, n_step=3, gamma=0.99)
+    for t in plan.outputs.values():
+        t.zero_()
+    cnt = torch.tensor([m], dtype=torch.int64, device="cuda")
+    plan.desc.n_active = cnt.data_ptr()
+    out = plan.run(T_(idx))
+    ref = OG.gather_transitions(idx[:m], 8, ring.obs, ring.act, ring.rew, ring.done, 4, 3, 0.99)
+    assert np.array_equal(H(out["obs"])[:m], ref["obs"]) and np.all(H(out["obs"])[m:] == 0)
+    assert np.array_equal(H(out["next_obs"])[:m], ref["next_obs"])

@@ -304,3 +304,47 @@ def test_stream_without_reduction_matches(rpl):
         assert mb is None and wb is None
         assert np.array_equal(H(ia), H(ib)) and np.array_equal(H(qa), H(qb))
     assert np.array_equal(H(a.header), H(b.header))
+
+
+@pytest.mark.parametrize("mode", ["draws", "stream"])
+def test_sharded_compacted(rpl, mode):
+    # out_count: the owned draws move to the front in stratum order, the rest are -1 / 0;
+    # the union over ranks (in rank order) equals the concatenated oracle's sample
+    import torch
+    g = rng(33)
+    G, n_local, n = 3, 2000, 200
+    shards, orcs = [], []
+    for s in range(G):
+        t = rpl.SumTree(n_local, 32)
+        td = td_abs(g, n_local)
+        t.update(T_(np.arange(n_local, dtype=np.int64)), T_(td), 0.9)
+        o = OS.SumTreeOracle(n_local)
+        o.update(list(range(n_local)), [float(x) for x in td], 0.9)
+        shards.append(t)
+        orcs.append(o)
+    shards[1].update(T_(np.arange(0, n_local, 2, dtype=np.int64)),
+                     T_(np.zeros(n_local // 2, np.float32)), 0.9)   # an uneven shard
+    orcs[1].update(list(range(0, n_local, 2)), [0.0] * (n_local // 2), 0.9)
+    totals = torch.cat([t.total() for t in shards])
+    for step in range(2):
+        draws = OP.draws_u64(4, step * n, n)
+        ref_idx, ref_q, _ = OS.sharded_sample(orcs, n, draws)
+        collected, collected_q = [], []
+        for rank, t in enumerate(shards):
+            cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+            if mode == "draws":
+                idx, q, _ = t.sample_sharded(rank, G, totals, n, draws=T_(as_i64(draws)), count=cnt)
+                full, fq, _ = t.sample_sharded(rank, G, totals, n, draws=T_(as_i64(draws)))
+            else:
+                full, fq, _ = t.sample_sharded(rank, G, totals, n, seed=4, use_stream=True)
+                t.header[2] -= n  # rewind the stream: the compacted call must draw the same strata
+                idx, q, _ = t.sample_sharded(rank, G, totals, n, seed=4, use_stream=True, count=cnt)
+            m = int(H(cnt)[0])
+            idx, q, full, fq = H(idx), H(q), H(full), H(fq)
+            own = full >= 0
+            assert m == int(own.sum())
+            assert np.array_equal(idx[:m], full[own]) and np.array_equal(q[:m], fq[own])
+            assert np.all(idx[m:] == -1) and np.all(q[m:] == 0)
+            collected += idx[:m].tolist()
+            collected_q += q[:m].tolist()
+        assert collected == ref_idx and collected_q == ref_q

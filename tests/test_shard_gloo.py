@@ -33,7 +33,7 @@ class OracleShardTree:
         out[0] = self.o.total()
         return out
 
-    def sample_sharded(self, rank, n_shards, shard_totals, n, seed=0, out=None, use_stream=False):
+    def sample_sharded(self, rank, n_shards, shard_totals, n, seed=0, out=None, use_stream=False, count=None):
         idx, q, qmin = out
         totals = [int(x) for x in shard_totals]
         Q = sum(totals)
@@ -53,6 +53,12 @@ class OracleShardTree:
                 idx[k] = -1
                 q[k] = 0
         qmin[0] = m if m is not None else (1 << 63) - 1
+        if count is not None:  # compacted output (rpl_sumtree_sample_sharded with out_count)
+            own = idx >= 0
+            c = int(own.sum())
+            idx[:c], q[:c] = idx[own].clone(), q[own].clone()
+            idx[c:], q[c:] = -1, 0
+            count[0] = c
 
 
 def cpu_is_weights(q, qmin, beta, out):
@@ -66,17 +72,18 @@ def leaves_of(rank):
     return [int(x) for x in g.integers(1, 1 << 20, N_LOCAL)]
 
 
-def worker(rank, world, port, queue):
+def worker(rank, world, port, queue, compact=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1909_01500_b200.shard import ShardedSampler
     tree = OracleShardTree(leaves_of(rank))
-    smp = ShardedSampler(tree, N_PER_RANK, SEED, is_weights=cpu_is_weights)
+    smp = ShardedSampler(tree, N_PER_RANK, SEED, is_weights=cpu_is_weights, compact=compact)
     res = []
     for _ in range(STEPS):
         idx, q, w = smp.sample(BETA)
-        res.append((idx.clone().numpy(), q.clone().numpy(), w.clone().numpy(), smp.totals.clone().numpy()))
+        res.append((idx.clone().numpy(), q.clone().numpy(), w.clone().numpy(), smp.totals.clone().numpy(),
+                    int(smp.count[0])))
     queue.put((rank, res))
     dist.barrier()
     dist.destroy_process_group()
@@ -115,7 +122,7 @@ def test_mode_l_two_ranks_gloo():
         merged = np.full(n_glob, -1, np.int64)
         w_merged = np.zeros(n_glob)
         for r in range(world):
-            idx, qq, w, totals = out[r][step]
+            idx, qq, w, totals, _ = out[r][step]
             assert list(totals) == [sum(s.q) for s in shards]          # K5 all-gather
             own = idx >= 0
             assert not (merged[own] >= 0).any()                          # disjoint ownership
@@ -127,3 +134,38 @@ def test_mode_l_two_ranks_gloo():
         assert list(merged) == ref_idx                                   # == concatenated oracle
         ref_w = OS.is_weights(ref_q, sum(sum(s.q) for s in shards), world * N_LOCAL, BETA)
         np.testing.assert_allclose(w_merged, ref_w, rtol=1e-6)           # K7 global batch min (f32)
+
+
+@pytest.mark.timeout(120)
+def test_mode_l_two_ranks_gloo_compacted():
+    # compacted protocol: each rank's owned draws first; concatenating the ranks' first
+    # `count` entries in rank order reproduces the global sample in stratum order
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, world, port, q, True)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=100) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    shards = []
+    for r in range(world):
+        t = OS.SumTreeOracle(N_LOCAL, 0)
+        t.q = leaves_of(r)
+        shards.append(t)
+    n_glob = N_PER_RANK * world
+    for step in range(STEPS):
+        draws = OP.draws_u64(SEED, step * n_glob, n_glob)
+        ref_idx, ref_q, _ = OS.sharded_sample(shards, n_glob, draws)
+        merged, merged_w = [], []
+        for r in range(world):
+            idx, qq, w, totals, cnt = out[r][step]
+            assert (idx[:cnt] >= 0).all() and (idx[cnt:] == -1).all()
+            merged += idx[:cnt].tolist()
+            merged_w += w[:cnt].tolist()
+        assert merged == ref_idx
+        ref_w = OS.is_weights(ref_q, sum(sum(s.q) for s in shards), world * N_LOCAL, BETA)
+        np.testing.assert_allclose(merged_w, ref_w, rtol=1e-6)
