@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget (cpu_baseline)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/baseline/e2e)")
     ap.add_argument("--seq-variant", type=int, default=None, help="diagnostics: sequence-gather kernel variant")
+    ap.add_argument("--mode", default="L", choices=["L", "C"],
+                    help="N > 1 replay mode (SURVEY §8e): L = owner computes, each rank feeds its own learner; "
+                         "C = every owner's gather writes into the rank-0 learner's batch over NVLink (CUDA IPC)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: functional checks only)")
     ap.add_argument("--same-device", action="store_true",
@@ -220,7 +223,19 @@ def run_rpl(args):
     q_pool = torch.from_numpy(g.normal(0, 10, (P, L, n_glob)).astype(np.float32)).to(dev)
     seed = 0x5EED
 
-    plan = rpl.GatherPlan(ring, n_glob, kind="sequence", k=k, seq_len=L, period=period, with_weights=True)
+    mode_c = world > 1 and args.mode == "C"
+    learner = (not mode_c) or rank == 0  # ranks that consume a batch (and compute its targets)
+    central = None
+    if mode_c:
+        # Mode C: rank 0's batch buffers, mapped into every rank (CUDA IPC over NVLink)
+        from paper_1909_01500_b200.shard import CentralBatch
+        root_plan = (rpl.GatherPlan(ring, n_glob, kind="sequence", k=k, seq_len=L, period=period, with_weights=True)
+                     if rank == 0 else None)
+        central = CentralBatch(root_plan.outputs if rank == 0 else None)
+        plan = root_plan if rank == 0 else rpl.GatherPlan(ring, n_glob, kind="sequence", k=k, seq_len=L,
+                                                          period=period, with_weights=True, outputs=central.outputs)
+    else:
+        plan = rpl.GatherPlan(ring, n_glob, kind="sequence", k=k, seq_len=L, period=period, with_weights=True)
     out = plan.outputs
     idx_buf = [torch.full((n_glob,), -1, dtype=torch.int64, device=dev) for _ in range(2)]
     q_buf = torch.zeros(n_glob, dtype=torch.int64, device=dev)
@@ -231,10 +246,12 @@ def run_rpl(args):
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     totals = torch.zeros(world, dtype=torch.int64, device=dev)
     my_total = torch.zeros(1, dtype=torch.int64, device=dev)
-    n_owned = torch.zeros(1, dtype=torch.int64, device=dev)
+    n_owned = torch.zeros(2, dtype=torch.int64, device=dev)  # [owned m, first owned stratum k0]
     if world > 1:
         # compacted sharded sample: this rank's owned draws first, the gather schedules only those
         plan.desc.n_active = n_owned.data_ptr()
+        if mode_c:  # ... and writes them at their global batch positions in the learner's buffers
+            plan.desc.col_offset = n_owned.data_ptr() + 8
 
     def all_gather_totals():
         if args.backend == "nccl":
@@ -266,13 +283,16 @@ def run_rpl(args):
         if gather_events is not None:
             gather_events[0].record()
         # IS weights fused into the gather: batch min (1 GPU) or the all-reduced global min (Mode L)
-        plan.run(cur, q=q_buf, qmin=None if world == 1 else qmin, beta=c["beta"], stream=s)
+        plan.run(cur, q=q_buf, qmin=None if world == 1 else qmin, beta=c["beta"], err=err, stream=s)
         if gather_events is not None:
             gather_events[1].record()
-        rpl._lib.check(lib.rpl_returns_nstep(P_(r_tr), P_(d_tr), Tn, n_glob, c["n_step"], c["gamma"],
-                                             P_(q_pool[i % P][c["burn_in"]:c["burn_in"] + Tn]),
-                                             P_(q_pool[i % P][c["burn_in"] + Tn]), 1, c["eps"], P_(y), P_(dn), s),
-                       "nstep")
+        if mode_c:
+            central.arrived()                                                    # K8: batch complete on rank 0
+        if learner:
+            rpl._lib.check(lib.rpl_returns_nstep(P_(r_tr), P_(d_tr), Tn, n_glob, c["n_step"], c["gamma"],
+                                                 P_(q_pool[i % P][c["burn_in"]:c["burn_in"] + Tn]),
+                                                 P_(q_pool[i % P][c["burn_in"] + Tn]), 1, c["eps"], P_(y), P_(dn),
+                                                 s), "nstep")
 
     # idx < 0 entries (first step / not-owned) make the update kernel flag RPL_DERR_IDX; allow that bit.
     # warm-up (also primes lazy module loading and cudaFuncSetAttribute outside capture)
@@ -325,7 +345,7 @@ def run_rpl(args):
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    launches = (rpl.launch_count() - launches0) if not use_graph else (4 if world == 1 else 5) * K_eff
+    launches = (rpl.launch_count() - launches0) if not use_graph else (4 if world == 1 else 4 + int(learner)) * K_eff
     clk = clocks.stop() if not args.profile else {}
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -367,7 +387,7 @@ def run_rpl(args):
                    "leaves_per_gpu": n_leaves, "batch_per_gpu": n, "seq_len": L, "burn_in": c["burn_in"],
                    "train": c["train"], "tail": c["tail"], "frame_stack": k, "n_step": c["n_step"],
                    "gamma": c["gamma"], "alpha": c["alpha"], "beta": c["beta"], "out": "stacked",
-                   "parallelism": f"mode-L x{world}" if world > 1 else "single",
+                   "parallelism": (f"mode-{args.mode} x{world}" if world > 1 else "single"),
                    "l2": "inputs larger than L2 (7.2 GB ring, random sequences every step)",
                    "timing": "cuda graph of 8 steps, replayed" if use_graph else "eager launches"},
         "gpu_launches": launches,

@@ -170,11 +170,14 @@ int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree, int64_t n
  * rpl_sumtree_sample on the concatenation of the shards (§8c #17).  use_stream != 0 (draws
  * must be NULL) takes the Philox counter from this tree's stream position as
  * rpl_sumtree_sample_stream does; every rank's position advances by n identically.
- * out_count (device int64, may be NULL): when given, the output is COMPACTED — the owned
- * draws (a contiguous run of strata, because prefixes are non-decreasing in k) are written
- * to positions 0..m-1 in stratum order, positions m..n-1 get idx -1 / q 0, and
- * *out_count = m; pass it to rpl_gather_desc.n_active so the gather only schedules m
- * samples.  out_qmin may be NULL (no batch reduction). */
+ * out_count (device int64[2], may be NULL): when given, the output is COMPACTED — the
+ * owned draws (a contiguous run of strata k0..k0+m-1, because prefixes are non-decreasing
+ * in k) are written to positions 0..m-1 in stratum order as LOCAL leaf indices (this
+ * shard's own tree / ring: what its update and gather take; global = rank * shard_leaves +
+ * local), positions m..n-1 get idx -1 / q 0, out_count[0] = m and out_count[1] = k0.  Pass &out_count[0] as
+ * rpl_gather_desc.n_active (the gather schedules only the m owned samples) and, for a
+ * central learner, &out_count[1] as rpl_gather_desc.col_offset (each owner writes its
+ * samples at their global batch positions).  out_qmin may be NULL (no batch reduction). */
 int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t rank,
                                int32_t n_shards, int64_t shard_leaves, const int64_t* shard_totals,
                                int64_t n, const uint64_t* draws, uint64_t seed, uint64_t offset,
@@ -271,6 +274,13 @@ typedef struct {
    * are skipped as if idx[k] < 0.  With the compacted sharded sampler this lets the
    * persistent gather spread exactly the owned samples over all SMs. */
   const int64_t* n_active;
+  /* Optional device int64 (may be NULL = 0): every output of entry k is written at batch
+   * column *col_offset + k of the output arrays, whose column count (stride) is n.  With
+   * output pointers into a central learner's buffers (CUDA IPC / peer memory over NVLink)
+   * each owner's gather writes its samples straight into the learner's batch (Mode C).
+   * Honoured by the default sequence pipeline, the chunked sequence kernel and the
+   * transition kernel (other diagnostic variants fall back to the default when set). */
+  const int64_t* col_offset;
 } rpl_gather_desc;
 
 int rpl_gather(const rpl_gather_desc* desc /* host */, const int64_t* idx, const int64_t* q,

@@ -52,6 +52,7 @@ class GatherDesc(C.Structure):
         ("o_rew", C.c_void_p), ("o_prev_rew", C.c_void_p), ("o_done", C.c_void_p), ("o_ret", C.c_void_p),
         ("o_done_n", C.c_void_p), ("o_w", C.c_void_p), ("o_rnn", C.c_void_p),
         ("n_active", C.c_void_p),
+        ("col_offset", C.c_void_p),
     ]
 
 

@@ -155,7 +155,11 @@ struct GDesc {
   int use_tma;
   int diag;  // rpl_debug_set_gather_diag mask (0 in normal operation)
   const int64_t* n_active;  // device count of leading entries to gather (NULL: all n)
+  const int64_t* col_offset;  // device output column offset (NULL: 0)
 };
+
+// Output column offset (rpl_gather_desc.col_offset); read after pdl_wait.
+__device__ __forceinline__ int64_t col_off(const GDesc& D) { return D.col_offset ? *D.col_offset : 0; }
 
 // Number of leading entries of idx to gather (rpl_gather_desc.n_active); read after pdl_wait.
 __device__ __forceinline__ int64_t active_n(const GDesc& D, int64_t n) {
@@ -196,6 +200,7 @@ k_gather_transition(GDesc D, const int64_t* __restrict__ idx, int64_t n, const i
   const int64_t s = blockIdx.x;
   pdl_wait();
   if (s >= active_n(D, n)) return;
+  const int64_t sc = s + col_off(D);  // output column (Mode C offset)
   const int64_t leaf = idx[s];
   if (leaf < 0) return;
   const int k = D.k, ns = D.n_step;
@@ -238,7 +243,7 @@ k_gather_transition(GDesc D, const int64_t* __restrict__ idx, int64_t n, const i
     const int64_t qm = (D.o_w && q) ? warp_batch_qmin(qmin, idx, q, n) : 0;
     if (D.o_act) {
       const uint8_t* src = D.act + (r * D.B + b) * D.act_bytes;
-      uint8_t* dst = D.o_act + s * D.act_bytes;
+      uint8_t* dst = D.o_act + sc * D.act_bytes;
       for (int64_t i = l; i < D.act_bytes; i += 32) dst[i] = src[i];
     }
     if (l == 0) {
@@ -252,18 +257,18 @@ k_gather_transition(GDesc D, const int64_t* __restrict__ idx, int64_t n, const i
           acc = di ? ri : fma(D.gamma, acc, ri);
           dn |= di;
         }
-        if (D.o_ret) D.o_ret[s] = (float)acc;
-        if (D.o_done_n) D.o_done_n[s] = dn ? 1 : 0;
+        if (D.o_ret) D.o_ret[sc] = (float)acc;
+        if (D.o_done_n) D.o_done_n[sc] = dn ? 1 : 0;
       }
       if (D.o_w && q) {
         const int64_t qs = q[s];
-        D.o_w[s] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
+        D.o_w[sc] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
       }
     }
   }
   __syncthreads();
 
-  uint8_t* outs[2] = {D.o_obs ? D.o_obs + s * k * ob : nullptr, D.o_next_obs ? D.o_next_obs + s * k * ob : nullptr};
+  uint8_t* outs[2] = {D.o_obs ? D.o_obs + sc * k * ob : nullptr, D.o_next_obs ? D.o_next_obs + sc * k * ob : nullptr};
   if (tma) {
     uint8_t* zrow = smem + (int64_t)NR * ob;  // zero row for RPL_PAD_ZERO
     bool needs_zero = false;
@@ -324,6 +329,7 @@ k_gather_sequence(GDesc D, const int64_t* __restrict__ idx, int64_t n, const int
   const int tid = threadIdx.x;
   const int64_t s = blockIdx.y;
   if (s >= active_n(D, n)) return;
+  const int64_t sc = s + col_off(D);  // output column (Mode C offset)
   const int c = blockIdx.x;
   const int64_t leaf = idx[s];
   if (leaf < 0) return;
@@ -377,27 +383,27 @@ k_gather_sequence(GDesc D, const int64_t* __restrict__ idx, int64_t n, const int
       const uint8_t pd = __ldg(D.done + prow * D.B + b);  // previous row ended an episode?
       if (D.o_act)
         for (int64_t i = l; i < D.act_bytes; i += 32)
-          D.o_act[(tau * n + s) * D.act_bytes + i] = D.act[(row * D.B + b) * D.act_bytes + i];
+          D.o_act[(tau * n + sc) * D.act_bytes + i] = D.act[(row * D.B + b) * D.act_bytes + i];
       if (D.o_prev_act)
         for (int64_t i = l; i < D.act_bytes; i += 32)
-          D.o_prev_act[(tau * n + s) * D.act_bytes + i] = pd ? 0 : D.act[(prow * D.B + b) * D.act_bytes + i];
+          D.o_prev_act[(tau * n + sc) * D.act_bytes + i] = pd ? 0 : D.act[(prow * D.B + b) * D.act_bytes + i];
       if (l == 0) {
-        if (D.o_rew) D.o_rew[tau * n + s] = __ldg(D.rew + row * D.B + b);
-        if (D.o_prev_rew) D.o_prev_rew[tau * n + s] = pd ? 0.0f : __ldg(D.rew + prow * D.B + b);
-        if (D.o_done) D.o_done[tau * n + s] = __ldg(D.done + row * D.B + b);
+        if (D.o_rew) D.o_rew[tau * n + sc] = __ldg(D.rew + row * D.B + b);
+        if (D.o_prev_rew) D.o_prev_rew[tau * n + sc] = pd ? 0.0f : __ldg(D.rew + prow * D.B + b);
+        if (D.o_done) D.o_done[tau * n + sc] = __ldg(D.done + row * D.B + b);
       }
     }
   }
   // stored recurrent state at the sequence start (chunk 0), [parts, n, rnn_bytes]
   if (c == 0 && D.o_rnn) {
     for (int p = 0; p < D.rnn_parts; ++p)
-      coop_copy(D.o_rnn + (p * n + s) * D.rnn_bytes,
+      coop_copy(D.o_rnn + (p * n + sc) * D.rnn_bytes,
                 D.rnn + ((blk * D.B + b) * D.rnn_parts + p) * D.rnn_bytes, D.rnn_bytes, tid, G_THREADS);
   }
   if (c == 0 && D.o_w && q && tid < 32) {
     const int64_t qm = warp_batch_qmin(qmin, idx, q, n);
     const int64_t qs = q[s];
-    if (tid == 0) D.o_w[s] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
+    if (tid == 0) D.o_w[sc] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
   }
   __syncthreads();
   if (!D.o_obs || NR == 0) return;
@@ -420,7 +426,7 @@ k_gather_sequence(GDesc D, const int64_t* __restrict__ idx, int64_t n, const int
       if (stacked) {
         if (tid < Cn) {
           const int tau = tid;
-          uint8_t* dst = D.o_obs + (((int64_t)(o0 + tau) * n + s) * k) * ob;
+          uint8_t* dst = D.o_obs + (((int64_t)(o0 + tau) * n + sc) * k) * ob;
           const int* sl = sslot[tau];
           bool contiguous = sl[0] >= 0;
           for (int j = 1; j < k; ++j) contiguous &= (sl[j] == sl[0] + j);
@@ -435,7 +441,7 @@ k_gather_sequence(GDesc D, const int64_t* __restrict__ idx, int64_t n, const int
         }
       } else {
         if (tid < Cn) {
-          uint8_t* dst = D.o_obs + ((int64_t)(o0 + tid) * n + s) * ob;
+          uint8_t* dst = D.o_obs + ((int64_t)(o0 + tid) * n + sc) * ob;
           bulk_s2g(dst, smem + (int64_t)tid * ob, (uint32_t)ob);
           bulk_commit();
           bulk_wait_read0();
@@ -445,7 +451,7 @@ k_gather_sequence(GDesc D, const int64_t* __restrict__ idx, int64_t n, const int
   } else {
     if (stacked) {
       for (int tau = 0; tau < Cn; ++tau) {
-        uint8_t* dst = D.o_obs + (((int64_t)(o0 + tau) * n + s) * k) * ob;
+        uint8_t* dst = D.o_obs + (((int64_t)(o0 + tau) * n + sc) * k) * ob;
         for (int j = 0; j < k; ++j) {
           const int src = sslot[tau][j];
           if (src < 0) coop_zero(dst + j * ob, ob, tid, G_THREADS);
@@ -454,7 +460,7 @@ k_gather_sequence(GDesc D, const int64_t* __restrict__ idx, int64_t n, const int
       }
     } else {
       for (int u = 0; u < Cn; ++u)
-        coop_copy(D.o_obs + ((int64_t)(o0 + u) * n + s) * ob,
+        coop_copy(D.o_obs + ((int64_t)(o0 + u) * n + sc) * ob,
                   D.obs + (wrap(first + u, D.cap_T) * D.B + b) * ob, ob, tid, G_THREADS);
     }
   }
@@ -848,6 +854,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   pdl_wait();  // idx (and n_active) come from the sampler launched just before
   // rows g = s*L + tau of the active samples, split evenly over the grid
   const int total = (int)(active_n(D, n) * L);
+  const int64_t coff = col_off(D);  // output column of entry 0 (Mode C)
   const int rpc = D.n_active ? (total + (int)gridDim.x - 1) / (int)gridDim.x : (int)rows_per_cta;
   const int g0 = (int)blockIdx.x * rpc;
   const int g1 = min(total, g0 + rpc);
@@ -998,7 +1005,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         const uint8_t dd = __ldg(D.done + e);
         const float rw = D.o_rew ? __ldg(D.rew + e) : 0.0f;
         const float prw = D.o_prev_rew ? __ldg(D.rew + pe) : 0.0f;
-        const int64_t o = (int64_t)tau * n + sm;
+        const int64_t o = (int64_t)tau * n + coff + sm;
         if (a8) {
           const uint64_t* a = reinterpret_cast<const uint64_t*>(D.act);
           const uint64_t av = D.o_act ? __ldg(a + e) : 0ull;
@@ -1017,7 +1024,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         if (D.o_done) D.o_done[o] = dd;
         if (tau == 0 && D.o_w && q) {
           const int64_t qs = q[sm];
-          D.o_w[sm] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
+          D.o_w[coff + sm] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
         }
       }
       // stored recurrent state of every sample whose first row lives here
@@ -1029,7 +1036,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
           if (sm * L < g0 || p_b[pc] < 0) continue;  // first row not in this CTA, or skipped
           const int64_t blk = p_blk[pc], bcol = p_b[pc];
           for (int pp = 0; pp < nparts; ++pp)
-            coop_copy(D.o_rnn + (pp * n + sm) * rb, D.rnn + ((blk * Bc + bcol) * nparts + pp) * rb, rb, lane, 32);
+            coop_copy(D.o_rnn + (pp * n + coff + sm) * rb, D.rnn + ((blk * Bc + bcol) * nparts + pp) * rb, rb, lane, 32);
         }
       }
     } else {
@@ -1052,7 +1059,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
               }
               mbar_wait(&full[sl], par);
             }
-          int4* dst = reinterpret_cast<int4*>(D.o_obs + ((int64_t)tau * n + sm) * k * ob);
+          int4* dst = reinterpret_cast<int4*>(D.o_obs + ((int64_t)tau * n + coff + sm) * k * ob);
           if (!(D.diag & 1))
             for (int j = 0; j < k; ++j) {
               int4* d = dst + j * nv;
@@ -1142,6 +1149,7 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   pdl_wait();  // idx (and n_active) come from the sampler launched just before
   // rows g = s*L + tau of the active samples, split evenly over the grid
   const int total = (int)(active_n(D, n) * L);
+  const int64_t coff = col_off(D);  // output column of entry 0 (Mode C)
   const int rpc = D.n_active ? (total + (int)gridDim.x - 1) / (int)gridDim.x : (int)rows_per_cta;
   const int g0 = (int)blockIdx.x * rpc;
   const int g1 = min(total, g0 + rpc);
@@ -1246,7 +1254,7 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
             while (frame_ready[sl] != p0 + j + 1) __nanosleep(20);
           }
           fence_proxy_async();
-          uint8_t* dst = D.o_obs + ((int64_t)tau * n + sm) * k * ob;
+          uint8_t* dst = D.o_obs + ((int64_t)tau * n + coff + sm) * k * ob;
           if (so == 0 && s0 + k <= NS) {
             bulk_s2g_ef(dst, smem + s0 * ob, (uint32_t)(k * ob), pol);
           } else {
@@ -1288,7 +1296,7 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       const uint8_t dd = __ldg(D.done + e);
       const float rw = D.o_rew ? __ldg(D.rew + e) : 0.0f;
       const float prw = D.o_prev_rew ? __ldg(D.rew + pe) : 0.0f;
-      const int64_t o = (int64_t)tau * n + sm;
+      const int64_t o = (int64_t)tau * n + coff + sm;
       if (a8) {
         const uint64_t* a = reinterpret_cast<const uint64_t*>(D.act);
         const uint64_t av = D.o_act ? __ldg(a + e) : 0ull;
@@ -1307,7 +1315,7 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       if (D.o_done) D.o_done[o] = dd;
       if (tau == 0 && D.o_w && q) {
         const int64_t qs = q[sm];
-        D.o_w[sm] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
+        D.o_w[coff + sm] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
       }
     }
     if (D.o_rnn && !(D.diag & 16)) {
@@ -1318,7 +1326,7 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         if (sm * L < g0 || p_b[pc] < 0) continue;
         const int64_t blk = p_blk[pc], bcol = p_b[pc];
         for (int pp = 0; pp < nparts; ++pp)
-          coop_copy(D.o_rnn + (pp * n + sm) * rb, D.rnn + ((blk * Bc + bcol) * nparts + pp) * rb, rb, lane, 32);
+          coop_copy(D.o_rnn + (pp * n + coff + sm) * rb, D.rnn + ((blk * Bc + bcol) * nparts + pp) * rb, rb, lane, 32);
       }
     }
   } else {
@@ -1410,6 +1418,7 @@ GDesc to_dev(const rpl_gather_desc* d) {
   g.use_tma = 0;
   g.diag = g_seq_diag;
   g.n_active = d->n_active;
+  g.col_offset = d->col_offset;
   return g;
 }
 
@@ -1449,6 +1458,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
   if ((desc->o_act || desc->o_prev_act) && (!desc->act || desc->act_bytes < 1)) return RPL_EINVAL;
   if (desc->o_w && !(beta >= 0.0)) return RPL_EINVAL;
   GDesc g = to_dev(desc);
+  const int seq_variant = desc->col_offset ? 0 : g_seq_variant;  // col_offset: default kernels only
   const bool tma_ok = (desc->obs_bytes % 16 == 0) && aligned16(desc->obs) && aligned16(desc->o_obs) &&
                       aligned16(desc->o_next_obs) && desc->obs_bytes <= 32768;
   cudaStream_t st = as_stream(stream);
@@ -1474,7 +1484,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
     if ((desc->o_rew || desc->o_prev_rew) && !desc->rew) return RPL_EINVAL;
     if (desc->out_mode != RPL_OUT_STACKED && desc->out_mode != RPL_OUT_UNIQUE) return RPL_EINVAL;
     if (SEQ_CHUNK + desc->k > 32) return RPL_EINVAL;
-    if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs && g_seq_variant == 2 &&
+    if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs && seq_variant == 2 &&
         desc->obs_bytes <= 16 * 32 * FC_MAX_V4 * 4) {
       const int64_t tasks = n * (int64_t)(desc->seq_len + desc->k - 1);
       k_gather_seq_lsu<<<(unsigned)((tasks + FC_WARPS - 1) / FC_WARPS), FC_WARPS * 32, 0, st>>>(g, idx, n, q, qmin,
@@ -1485,7 +1495,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       k_gather_seq_fields<<<(unsigned)((rows + 255) / 256), 256, 0, st>>>(g, idx, n, dev_err);
       return launch_status();
     }
-    if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs && g_seq_variant == 6) {
+    if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs && seq_variant == 6) {
       int NS = (int)(200 * 1024 / desc->obs_bytes) - 1;  // + one zero slot
       if (NS > PIPE_MAX_NS) NS = PIPE_MAX_NS;
       const int k = desc->k;
@@ -1501,7 +1511,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       }
     }
     if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs &&
-        (g_seq_variant == 0 || g_seq_variant == 4 || g_seq_variant == 5)) {
+        (seq_variant == 0 || seq_variant == 4 || seq_variant == 5)) {
       // default: TMA-load / LSU-store pipeline.  The producer runs up to NS frames past the
       // release point of the done-frontier row f, whose own window starts exactly there, so
       // NS >= k guarantees progress; more slots let the other consumers run ahead.
@@ -1518,14 +1528,15 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
         grid = (total + rows_per_cta - 1) / rows_per_cta;
         g.use_tma = 1;
         // consumer warps: 8 (default), 14 (variant 4), 4 (variant 5)
-        if (g_seq_variant == 4) return launch_seq_lsu<14>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn,
+        if (seq_variant == 4) return launch_seq_lsu<14>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn,
                                                           grid, st);
-        if (g_seq_variant == 5) return launch_seq_lsu<4>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn,
+        if (seq_variant == 5) return launch_seq_lsu<4>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn,
                                                          grid, st);
         return launch_seq_lsu<8>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn, grid, st);
       }
     }
-    if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs && (g_seq_variant == 3 || g_seq_variant == 0)) {
+    if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs &&
+        (seq_variant == 3 || (seq_variant == 0 && !desc->col_offset))) {
       // persistent TMA pipeline: NS frame slots (+1 zero slot); CTAs_per_SM CTAs per SM
       // Slots the consumer may need beyond the released ones: G+1 rows of advance, the
       // k-1 window, and k-1 per piece boundary crossed.  With L > G at most two boundaries

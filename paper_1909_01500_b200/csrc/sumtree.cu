@@ -264,7 +264,9 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
       }
       if (mine) {
         leaf = descend(L, tree, (int64_t)prefix, &q, &errbits);
-        if (SHARDED) leaf += (int64_t)rank * shard_leaves;
+        // global index (shard-major, §8c #17); the compacted form keeps the LOCAL leaf
+        // for the owner's own update / gather
+        if (SHARDED && !compact) leaf += (int64_t)rank * shard_leaves;
       }
     }
     if (lane == 0) {
@@ -280,7 +282,10 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
           out_idx[k] = -1;
           out_q[k] = 0;
         }
-        if (k == 0) *out_count = m_own;
+        if (k == 0) {
+          out_count[0] = m_own;
+          out_count[1] = k0;  // global batch position of compacted entry 0 (Mode C column offset)
+        }
       }
     }
   }

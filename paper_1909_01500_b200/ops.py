@@ -234,12 +234,12 @@ class SumTree:
 
     def sample_sharded(self, rank, n_shards, shard_totals, n, draws=None, seed=0, offset=0, out=None, err=None,
                        use_stream=False, count=None):
-        """rpl_sumtree_sample_sharded.  count (1-element int64 CUDA tensor) selects the compacted
-        output: owned draws first, *count = their number."""
+        """rpl_sumtree_sample_sharded.  count (2-element int64 CUDA tensor) selects the compacted
+        output: owned draws first; count = [their number m, their first global stratum k0]."""
         n = int(n)
         _req(shard_totals, torch.int64, "shard_totals", (n_shards,))
         if count is not None:
-            _req(count, torch.int64, "count", (1,))
+            _req(count, torch.int64, "count", (2,))
         if out is None:
             idx = torch.empty(n, dtype=torch.int64, device=self.device)
             q = torch.empty(n, dtype=torch.int64, device=self.device)
@@ -385,15 +385,17 @@ class GatherPlan:
     capturable in a CUDA graph)."""
 
     def __init__(self, ring: GatherRing, n, kind="transition", k=4, n_step=1, gamma=0.99, seq_len=1, period=1,
-                 pad_mode=_lib.PAD_REPEAT, out_mode=_lib.OUT_STACKED, want=None, with_weights=False):
+                 pad_mode=_lib.PAD_REPEAT, out_mode=_lib.OUT_STACKED, want=None, with_weights=False, outputs=None):
+        """outputs: optional dict of preallocated output tensors (e.g. a central learner's
+        buffers mapped over CUDA IPC, Mode C); missing ones are allocated here."""
         dev = ring.obs.device
         self.n = int(n)
         dummy = torch.zeros(self.n, dtype=torch.int64, device=dev)
-        self.outputs = {}
         # allocate via gather() on an all-skip index vector (no kernel work: idx < 0)
         self.outputs = gather(ring, torch.full_like(dummy, -1), kind=kind, k=k, n_step=n_step, gamma=gamma,
-                              seq_len=seq_len, period=period, pad_mode=pad_mode, out_mode=out_mode, want=want)
-        if with_weights:
+                              seq_len=seq_len, period=period, pad_mode=pad_mode, out_mode=out_mode, want=want,
+                              outputs=outputs)
+        if with_weights and "w" not in self.outputs:
             self.outputs["w"] = torch.empty(self.n, dtype=torch.float32, device=dev)
         kind_i = _lib.GATHER_TRANSITION if kind == "transition" else _lib.GATHER_SEQUENCE
         self.desc = _desc(ring, kind_i, k, pad_mode, out_mode, n_step if kind_i == 0 else 1, seq_len, period, gamma)

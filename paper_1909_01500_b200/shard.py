@@ -12,8 +12,9 @@ proportional sample over the union of the shards needs one exchange per step:
       by the global batch max weight (§8c #10).
 
 Frames never cross NVLink: each rank gathers its owned samples locally and feeds
-its own learner.  With compact=True the owned draws come first (count on the device),
-so the rank's gather schedules only them (rpl_gather_desc.n_active).  The result equals rpl_sumtree_sample on the shard-major
+its own learner.  With compact=True the owned draws come first as LOCAL leaf indices
+(count = [m, k0] on the device), so the rank's update and gather take them directly and
+the gather schedules only them (rpl_gather_desc.n_active).  The result equals rpl_sumtree_sample on the shard-major
 concatenation of the trees (§8c #17; tests/test_gpu_sumtree.py).
 
 The tree object is duck-typed (total(), sample_sharded(), .device) so the
@@ -42,14 +43,17 @@ class ShardedSampler:
         self.w = torch.zeros(self.n_glob, dtype=torch.float32, device=dev)
         self._is_weights = is_weights
         self.compact = bool(compact)
-        self.count = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.count = torch.zeros(2, dtype=torch.int64, device=dev)  # [owned m, first stratum k0]
 
     def sample(self, beta: float):
         """One global stratified sample of n_glob draws.  Returns (idx, q, w): idx[k] is
         the GLOBAL leaf (rank * shard_leaves + local) for the draws this rank owns and
         -1 elsewhere; w is normalised by the global batch min q."""
         self.tree.total(out=self.my_total)
-        dist.all_gather_into_tensor(self.totals, self.my_total, group=self.group)          # K5
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_gather_into_tensor(self.totals, self.my_total, group=self.group)      # K5
+        else:  # gloo (CPU tests, functional checks): list form
+            dist.all_gather(list(self.totals.chunk(self.world)), self.my_total, group=self.group)
         kw = {"count": self.count} if self.compact else {}
         self.tree.sample_sharded(self.rank, self.world, self.totals, self.n_glob, seed=self.seed,
                                  out=(self.idx, self.q, self.qmin), use_stream=True, **kw)
@@ -64,3 +68,39 @@ class ShardedSampler:
     def owned(self):
         """Boolean mask of the draws this rank owns (host sync; diagnostics)."""
         return self.idx >= 0
+
+
+class CentralBatch:
+    """Mode C (BASELINE north_star "gathers the batch back to the learner
+    GPU"): the learner rank owns the batch buffers; every other rank maps them through
+    CUDA IPC (peer memory over NVLink) so that its gather kernel writes its owned samples
+    straight into the learner's batch at their global positions — the transfer is fused
+    into the gather, no staging copy and no NCCL send of frames.  Used with a compacted
+    ShardedSampler: count = [m, k0] feeds rpl_gather_desc.n_active / col_offset.
+
+    A small all-reduce after the gather (K8, `arrived`) tells the learner the batch is
+    complete: a rank's NCCL kernel runs after its gather on the same stream, so its
+    completion on the learner implies every owner's peer writes have landed."""
+
+    def __init__(self, outputs_on_root, group=None, root: int = 0):
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.group = group
+        self.root = root
+        self.rank = dist.get_rank(group)
+        names = sorted(outputs_on_root) if outputs_on_root is not None else None
+        if self.rank == root:
+            payload = [[(n, reduce_tensor(outputs_on_root[n])) for n in names]]
+        else:
+            payload = [None]
+        dist.broadcast_object_list(payload, src=root, group=group)
+        if self.rank == root:
+            self.outputs = dict(outputs_on_root)
+        else:
+            self.outputs = {n: fn(*args) for n, (fn, args) in payload[0]}
+        dev = next(iter(self.outputs.values())).device if self.rank == root else torch.device("cuda",
+                                                                                             torch.cuda.current_device())
+        self.flag = torch.zeros(1, dtype=torch.int64, device=dev)
+
+    def arrived(self):
+        """K8: completion signal after this rank's gather (stream-ordered, 8 bytes)."""
+        dist.all_reduce(self.flag, group=self.group)

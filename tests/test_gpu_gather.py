@@ -337,3 +337,44 @@ def test_transition_n_active(rpl):
     ref = OG.gather_transitions(idx[:m], 8, ring.obs, ring.act, ring.rew, ring.done, 4, 3, 0.99)
     assert np.array_equal(H(out["obs"])[:m], ref["obs"]) and np.all(H(out["obs"])[m:] == 0)
     assert np.array_equal(H(out["next_obs"])[:m], ref["next_obs"])
+
+
+@pytest.mark.parametrize("kind", ["sequence", "transition", "sequence_unique"])
+def test_col_offset(rpl, kind):
+    # rpl_gather_desc.col_offset: entry k lands in output column *col_offset + k of arrays
+    # with n columns; other columns untouched (Mode C writes into a central batch)
+    import torch
+    g = rng(13)
+    if kind == "transition":
+        ring = make_ring(93, cap=64, B=8, ep_len=9.0)
+        idx = valid_transition_leaves(ring, 4, 3, 40, g)
+        kw = dict(kind="transition", k=4, n_step=3, gamma=0.99)
+    else:
+        ring = make_ring(94, cap=400, B=4, ep_len=25.0, period=40, rnn_h=16, reward_kind="r2d2")
+        idx = []
+        while len(idx) < 40:
+            blk, b = int(g.integers(0, 10)), int(g.integers(0, 4))
+            if OG.window_valid_sequence(blk * 40, 400, ring.cursor, ring.size, 4, 45):
+                idx.append(blk * 4 + b)
+        idx = np.array(idx, np.int64)
+        kw = dict(kind="sequence", k=4, seq_len=45, period=40, out_mode=1 if kind.endswith("unique") else 0)
+    dr = dev_ring(rpl, ring)
+    m, off = 11, 23
+    sub = idx.copy()
+    sub[m:] = -1
+    plan = rpl.GatherPlan(dr, idx.size, **kw)
+    for t in plan.outputs.values():
+        t.zero_()
+    cnt = torch.tensor([m, off], dtype=torch.int64, device="cuda")
+    plan.desc.n_active = cnt.data_ptr()
+    plan.desc.col_offset = cnt.data_ptr() + 8
+    out = {kk: H(v) for kk, v in plan.run(T_(idx)).items()}
+    ref = rpl.gather(dr, T_(idx[:m]), **kw)
+    axis = 0 if kind == "transition" else 1
+    for name, r in ref.items():
+        r = H(r)
+        o = out[name]
+        got = np.take(o, np.arange(off, off + m), axis=axis)
+        assert np.array_equal(got, r), name
+        rest = np.delete(o, np.arange(off, off + m), axis=axis)
+        assert not rest.any(), name

@@ -331,7 +331,7 @@ def test_sharded_compacted(rpl, mode):
         ref_idx, ref_q, _ = OS.sharded_sample(orcs, n, draws)
         collected, collected_q = [], []
         for rank, t in enumerate(shards):
-            cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+            cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
             if mode == "draws":
                 idx, q, _ = t.sample_sharded(rank, G, totals, n, draws=T_(as_i64(draws)), count=cnt)
                 full, fq, _ = t.sample_sharded(rank, G, totals, n, draws=T_(as_i64(draws)))
@@ -343,8 +343,11 @@ def test_sharded_compacted(rpl, mode):
             idx, q, full, fq = H(idx), H(q), H(full), H(fq)
             own = full >= 0
             assert m == int(own.sum())
-            assert np.array_equal(idx[:m], full[own]) and np.array_equal(q[:m], fq[own])
+            if m:
+                assert int(H(cnt)[1]) == int(np.nonzero(own)[0][0])  # k0: global position of entry 0
+            # compacted entries are LOCAL leaves (global = rank * shard_leaves + local)
+            assert np.array_equal(idx[:m] + rank * n_local, full[own]) and np.array_equal(q[:m], fq[own])
             assert np.all(idx[m:] == -1) and np.all(q[m:] == 0)
-            collected += idx[:m].tolist()
+            collected += (idx[:m] + rank * n_local).tolist()
             collected_q += q[:m].tolist()
         assert collected == ref_idx and collected_q == ref_q

@@ -56,9 +56,10 @@ class OracleShardTree:
         if count is not None:  # compacted output (rpl_sumtree_sample_sharded with out_count)
             own = idx >= 0
             c = int(own.sum())
-            idx[:c], q[:c] = idx[own].clone(), q[own].clone()
+            idx[:c], q[:c] = idx[own].clone() - rank * self.n_leaves, q[own].clone()  # local leaves
             idx[c:], q[c:] = -1, 0
             count[0] = c
+            count[1] = int(np.nonzero(own.numpy())[0][0]) if c else 0
 
 
 def cpu_is_weights(q, qmin, beta, out):
@@ -164,7 +165,7 @@ def test_mode_l_two_ranks_gloo_compacted():
         for r in range(world):
             idx, qq, w, totals, cnt = out[r][step]
             assert (idx[:cnt] >= 0).all() and (idx[cnt:] == -1).all()
-            merged += idx[:cnt].tolist()
+            merged += (idx[:cnt] + r * N_LOCAL).tolist()   # compacted entries are local leaves
             merged_w += w[:cnt].tolist()
         assert merged == ref_idx
         ref_w = OS.is_weights(ref_q, sum(sum(s.q) for s in shards), world * N_LOCAL, BETA)
