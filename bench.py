@@ -353,6 +353,11 @@ def run_rpl(args):
     ms = float(ms_t.item())
     value = K_eff * n * world / (ms / 1e3)
 
+    pipelined = None
+    if world == 1 and not args.no_secondary and not args.profile:
+        pipelined = pipelined_step(dev, rpl, tree, plan, idx_buf, td_pool, q_pool, r_tr, d_tr, y, dn, err, c, n,
+                                   P, seed, Tn)
+
     # dominant kernel (sequence gather): average launch duration with CUDA events on
     # the launching stream, over K eager steps of the same workload
     Kg = min(K_eff, 200)
@@ -401,7 +406,8 @@ def run_rpl(args):
         result["clocks"] = clk
         result["e2e"] = e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K_eff, world)
     if world == 1 and not args.no_secondary and not args.profile:
-        result["secondary"] = {"ppo_returns": bench_ppo(dev, rpl), "dqn_replay": bench_dqn(dev, rpl),
+        result["secondary"] = {"r2d2_pipelined": pipelined, "tree_latency": tree_latency(dev, rpl),
+                               "ppo_returns": bench_ppo(dev, rpl), "dqn_replay": bench_dqn(dev, rpl),
                                "mujoco_replay": bench_mujoco(dev, rpl)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         result["cpu_baseline"] = cpu_baseline(c, host, args.cpu_seconds)
@@ -496,6 +502,91 @@ def bench_ppo(dev, rpl):
             "disc_us_per_call": ms_disc * 1e3, "disc_GBps": disc_gbs, "disc_frac": disc_gbs / peak,
             "l2": f"input pool {pool} x {per/1e6:.1f} MB > 4 x L2",
             "timing": "CUDA graph of one call per pool entry, replayed; per-call average"}
+
+
+def pipelined_step(dev, rpl, tree, plan, idx_buf, td_pool, q_pool, r_tr, d_tr, y, dn, err, c, n, P, seed, Tn):
+    """SURVEY §8d's secondary step variant: the same four calls, but update(i+1) +
+    sample(i+1) run on a second stream while gather(i) + n-step(i) run (the paper's
+    asynchronous sampler/optimiser overlap, Fig. 3).  Dependencies: gather(i) waits for
+    sample(i); sample(i) waits for gather(i-2) (it overwrites that batch's idx / q)."""
+    import torch
+    lib, P_ = rpl._lib.lib, rpl.ops._ptr
+    qb = [torch.zeros(n, dtype=torch.int64, device=dev) for _ in range(2)]
+    sA, sB = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    ev_s = [torch.cuda.Event() for _ in range(P)]
+    ev_g = [torch.cuda.Event() for _ in range(P)]
+
+    def run(P_steps):
+        for i in range(P_steps):
+            cur, prev = idx_buf[i % 2], idx_buf[(i + 1) % 2]
+            with torch.cuda.stream(sA):
+                if i >= 2:
+                    sA.wait_event(ev_g[(i - 2) % P])
+                a = rpl.ops._stream(dev)
+                rpl._lib.check(lib.rpl_sumtree_update(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]), n,
+                                                      c["alpha"], c["eps_p"], None, a), "update")
+                rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, seed, c["beta"],
+                                                             P_(cur), P_(qb[i % 2]), None, None, P_(err), a),
+                               "sample")
+                ev_s[i % P].record(sA)
+            with torch.cuda.stream(sB):
+                sB.wait_event(ev_s[i % P])
+                b = rpl.ops._stream(dev)
+                plan.run(cur, q=qb[i % 2], qmin=None, beta=c["beta"], err=err, stream=b)
+                rpl._lib.check(lib.rpl_returns_nstep(P_(r_tr), P_(d_tr), Tn, n, c["n_step"], c["gamma"],
+                                                     P_(q_pool[i % P][c["burn_in"]:c["burn_in"] + Tn]),
+                                                     P_(q_pool[i % P][c["burn_in"] + Tn]), 1, c["eps"], P_(y),
+                                                     P_(dn), b), "nstep")
+                ev_g[i % P].record(sB)
+
+    cap = torch.cuda.Stream(dev)
+    cap.wait_stream(torch.cuda.current_stream(dev))
+    for s_ in (sA, sB):
+        s_.wait_stream(cap)
+    run(P)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cap):
+        sA.wait_stream(cap)
+        sB.wait_stream(cap)
+        run(P)
+        cap.wait_stream(sA)
+        cap.wait_stream(sB)
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    reps = 50
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    rpl.check_err(err)
+    ms = e0.elapsed_time(e1) / (reps * P)
+    return {"us_per_step": ms * 1e3, "sequences_per_s": n / (ms / 1e3),
+            "timing": "CUDA graph of 8 steps on two streams (update+sample || gather+n-step), replayed"}
+
+
+def tree_latency(dev, rpl):
+    """Sampled-lookup latency: events over a graph of 16 sample-only
+    (and update-only) launches on the R2D2 (25,600 leaves, n=64) and DQN (2^20, n=512) trees."""
+    import torch
+    res = {}
+    for N, n in ((25600, 64), (1 << 20, 512)):
+        t = rpl.SumTree(N, 32, device=dev)
+        g = torch.Generator(device=dev)
+        g.manual_seed(N)
+        t.update(torch.arange(N, device=dev), torch.rand(N, generator=g, device=dev) + 1e-3, 0.9)
+        idx = torch.randint(0, N, (n,), generator=g, device=dev)
+        td = torch.rand(n, generator=g, device=dev)
+        outs = (torch.empty(n, dtype=torch.int64, device=dev), torch.empty(n, dtype=torch.int64, device=dev), None,
+                None)
+        us_s = _graph_time(dev, lambda i: t.sample_stream(n, 3, out=outs, want_qmin=False), P=16, reps=20) * 1e3
+        us_u = _graph_time(dev, lambda i: t.update(idx, td, 0.9), P=16, reps=20) * 1e3
+        res[f"N{N}_n{n}"] = {"sample_us": us_s, "update_us": us_u, "depth": t.depth}
+        del t
+    return {"unit": "us per launch (graph-replayed, back to back)", **res}
 
 
 def _graph_time(dev, step, P=8, reps=25):
