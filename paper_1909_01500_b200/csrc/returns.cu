@@ -14,7 +14,9 @@
 // is read from HBM once and each output written once: 9 B/elem (discounted),
 // 17 B/elem (GAE).  fp64 accumulation with one rounding to fp32 keeps the 1e-5
 // relative bound where fp32 scans lose everything to cancellation (§8c #21).
+#include <cuda.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -113,6 +115,134 @@ k_scan(const float* __restrict__ r, const float* __restrict__ v, const uint8_t* 
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA variant (default when the layout allows it): the CTA's [CH rows x 32 columns]
+// tiles of r, V and d arrive by three 2-D tensor copies (cp.async.bulk.tensor) into
+// shared memory on one mbarrier instead of 24 LDGs per thread: the per-SM L1 miss
+// queue no longer caps the bytes in flight (ncu/globaltimer r1: the LDG load phase was
+// ~3.8 us of a 5.9 us call).  OOB rows / columns are zero-filled by the TMA unit.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int WARPS, int S, bool GAE>
+__global__ void __launch_bounds__(WARPS * 32)
+k_scan_tma(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUtensorMap tm_v,
+           const __grid_constant__ CUtensorMap tm_d, const float* __restrict__ v, const float* __restrict__ boot,
+           int64_t T, int64_t B, double gamma, double lam, float* __restrict__ out0, float* __restrict__ out1) {
+  constexpr int CH = WARPS * S;
+  __shared__ __align__(128) float s_r[CH][32];
+  __shared__ __align__(128) float s_v[GAE ? CH : 1][32];
+  __shared__ __align__(128) uint8_t s_d[CH][32];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ double sA[WARPS][32];
+  __shared__ double sB[WARPS][32];
+  __shared__ double sCarry[32];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int64_t col = (int64_t)blockIdx.x * 32 + lane;
+  const bool cv = col < B;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_r) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_d) : "memory");
+    if (GAE) asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_v) : "memory");
+  }
+  __syncthreads();
+  pdl_wait();
+  if (w == 0) sCarry[lane] = (!GAE && boot != nullptr && cv) ? (double)boot[col] : 0.0;
+  const double bootv = (GAE && cv) ? (double)boot[col] : 0.0;
+  const double ga = GAE ? gamma * lam : gamma;
+  const int64_t nchunks = (T + CH - 1) / CH;
+  uint32_t phase = 0;
+  for (int64_t c = nchunks - 1; c >= 0; --c) {
+    if (threadIdx.x == 0) {
+      const uint32_t bytes = (uint32_t)(CH * 32 * 4 * (GAE ? 2 : 1) + CH * 32);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&bar)), "r"(bytes)
+                   : "memory");
+      const int x = blockIdx.x * 32, y = (int)(c * CH);
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+          ::"r"(s_u32(&s_r[0][0])), "l"(&tm_r), "r"(x), "r"(y), "r"(s_u32(&bar)) : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+          ::"r"(s_u32(&s_d[0][0])), "l"(&tm_d), "r"(x), "r"(y), "r"(s_u32(&bar)) : "memory");
+      if (GAE)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+            ::"r"(s_u32(&s_v[0][0])), "l"(&tm_v), "r"(x), "r"(y), "r"(s_u32(&bar)) : "memory");
+    }
+    {
+      uint32_t done = 0;
+      while (!done)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(s_u32(&bar)), "r"(phase) : "memory");
+      phase ^= 1u;
+    }
+    const int64_t t0 = c * CH + (int64_t)w * S;
+    double b[S];
+    float vv[S];
+    float rr[S];
+    uint32_t dmask = 0;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      rr[i] = s_r[w * S + i][lane];
+      dmask |= (s_d[w * S + i][lane] ? 1u : 0u) << i;
+      if (GAE) vv[i] = s_v[w * S + i][lane];
+    }
+    double vseg_next = 0.0;
+    if (GAE && cv && t0 < T) {
+      const int64_t tn = t0 + S;
+      if (tn >= T) vseg_next = bootv;
+      else if (w + 1 < WARPS) vseg_next = (double)s_v[(w + 1) * S][lane];
+      else vseg_next = (double)__ldg(v + tn * B + col);  // first row of the next chunk
+    }
+    __syncthreads();  // every thread holds its rows: the next chunk's TMA may overwrite the tiles
+    const int nvalid = cv ? (int)max((int64_t)0, min((int64_t)S, T - t0)) : 0;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      const double nd = ((dmask >> i) & 1u) ? 0.0 : 1.0;
+      if (GAE) {
+        double vnext;
+        if (i + 1 < S) vnext = (i + 1 < nvalid) ? (double)vv[i + 1] : bootv;
+        else vnext = vseg_next;
+        b[i] = i < nvalid ? ((double)rr[i] + gamma * nd * vnext) - (double)vv[i] : 0.0;
+      } else {
+        b[i] = i < nvalid ? (double)rr[i] : 0.0;
+      }
+    }
+#define RPL_A(i) ((i) < nvalid ? (((dmask >> (i)) & 1u) ? 0.0 : ga) : 1.0)
+    double A = 1.0, Bc = 0.0;
+#pragma unroll
+    for (int i = S - 1; i >= 0; --i) {
+      const double ai = RPL_A(i);
+      Bc = fma(ai, Bc, b[i]);
+      A = ai * A;
+    }
+    sA[w][lane] = A;
+    sB[w][lane] = Bc;
+    __syncthreads();
+    double x = sCarry[lane];
+#pragma unroll
+    for (int ww = WARPS - 1; ww > 0; --ww) {
+      if (ww > w) x = fma(sA[ww][lane], x, sB[ww][lane]);
+    }
+#pragma unroll
+    for (int i = S - 1; i >= 0; --i) {
+      x = fma(RPL_A(i), x, b[i]);
+      const int64_t t = t0 + i;
+      if (i < nvalid) {
+        out0[t * B + col] = (float)x;
+        if (GAE && out1 != nullptr) out1[t * B + col] = (float)(x + (double)vv[i]);
+      }
+    }
+#undef RPL_A
+    __syncthreads();
+    if (w == 0) sCarry[lane] = x;
+  }
+}
+
 __device__ __forceinline__ double h_fwd(double x, double eps) {
   // h(x) = x (1/(sqrt(|x|+1)+1) + eps)  ==  sign(x)(sqrt(|x|+1)-1) + eps x   (§8c #4)
   return x * (1.0 / (sqrt(fabs(x) + 1.0) + 1.0) + eps);
@@ -145,12 +275,28 @@ __global__ void k_nstep(const float* __restrict__ r, const uint8_t* __restrict__
       acc = rescale ? h_inv(qv, eps) : qv;
     }
     uint8_t dn = 0;
-    for (int i = n - 1; i >= 0; --i) {
-      const int64_t o = (t + i) * B + b;
-      const uint8_t di = __ldg(d + o);
-      const double ri = (double)__ldg(r + o);
-      acc = di ? ri : fma(gamma, acc, ri);
-      dn |= di;
+    // Horner from the last of the n rows; rows are fetched in blocks of 8 whose loads
+    // are all issued before the recurrence consumes them (one latency per block, not per row)
+    constexpr int NB = 8;
+    for (int hi = n; hi > 0; hi -= NB) {
+      const int lo = hi > NB ? hi - NB : 0;
+      float rb[NB];
+      uint8_t db[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const int i = lo + j;
+        const int64_t o = (t + i) * B + b;
+        rb[j] = i < hi ? __ldg(r + o) : 0.0f;
+        db[j] = i < hi ? __ldg(d + o) : (uint8_t)0;
+      }
+#pragma unroll
+      for (int j = NB - 1; j >= 0; --j) {
+        if (lo + j < hi) {
+          const double ri = (double)rb[j];
+          acc = db[j] ? ri : fma(gamma, acc, ri);
+          dn |= db[j];
+        }
+      }
     }
     if (rescale) acc = h_fwd(acc, eps);
     out[e] = (float)acc;
@@ -195,12 +341,83 @@ int elementwise_grid(int64_t work, int threads) {
 
 using namespace rpl;
 
+// Measurement-only knob (RPL_SCAN_VARIANT): 0 = TMA tiles when the layout allows (default,
+// else LDG 16 warps x 8 rows), 3 = LDG 16 warps x 8 rows, 1 = LDG 32 warps x 4 rows,
+// 2 = LDG 8 warps x 16 rows.  Same fp64 affine-map arithmetic; segment boundaries differ.
+int scan_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RPL_SCAN_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+typedef CUresult (*encode_fn_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+encode_fn_t encode_fn() {
+  static encode_fn_t fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<encode_fn_t>(p);
+  }
+  return fn;
+}
+
+// [T, B] row-major tensor map with a [box_rows x 32 columns] box; false if the layout is
+// not TMA-addressable (base not 16-B aligned, row pitch not a multiple of 16 B).
+bool tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esize, int64_t T, int64_t B,
+             int box_rows) {
+  encode_fn_t fn = encode_fn();
+  if (!fn || !base || (reinterpret_cast<uintptr_t>(base) & 15) || ((B * esize) & 15)) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)B, (cuuint64_t)T};
+  const cuuint64_t strides[1] = {(cuuint64_t)(B * esize)};
+  const cuuint32_t box[2] = {32u, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1u, 1u};
+  return fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+template <bool GAE>
+int launch_scan(const float* r, const float* v, const uint8_t* d, const float* boot, int64_t T, int64_t B,
+                double gamma, double lam, float* o0, float* o1, cudaStream_t st) {
+  dim3 grid((unsigned)((B + 31) / 32));
+  if (scan_variant() == 0 && T < (1ll << 31) && B < (1ll << 31)) {
+    CUtensorMap mr, mv, md;
+    constexpr int CH = SCAN_WARPS * SCAN_S;
+    if (tmap_2d(&mr, r, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH) &&
+        tmap_2d(&md, d, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, T, B, CH) &&
+        (!GAE || tmap_2d(&mv, v, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH))) {
+      if (!GAE) mv = mr;
+      return launch_pdl(k_scan_tma<SCAN_WARPS, SCAN_S, GAE>, grid, dim3(SCAN_WARPS * 32), 0, st, mr, mv, md, v,
+                        boot, T, B, gamma, lam, o0, o1);
+    }
+  }
+  switch (scan_variant()) {
+    case 1:
+      return launch_pdl(k_scan<32, 4, GAE>, grid, dim3(32 * 32), 0, st, r, v, d, boot, T, B, gamma, lam, o0, o1);
+    case 2:
+      return launch_pdl(k_scan<8, 16, GAE>, grid, dim3(8 * 32), 0, st, r, v, d, boot, T, B, gamma, lam, o0, o1);
+    default:
+      return launch_pdl(k_scan<SCAN_WARPS, SCAN_S, GAE>, grid, dim3(SCAN_WARPS * 32), 0, st, r, v, d, boot, T, B,
+                        gamma, lam, o0, o1);
+  }
+}
+
 extern "C" int rpl_returns_discounted(const float* r, const uint8_t* d, const float* bootstrap,
                                       int64_t T, int64_t B, double gamma, float* ret, void* stream) {
   if (!r || !d || !ret || T < 1 || B < 1) return RPL_EINVAL;
   dim3 grid((unsigned)((B + 31) / 32));
-  return launch_pdl(k_scan<SCAN_WARPS, SCAN_S, false>, grid, dim3(SCAN_WARPS * 32), 0, as_stream(stream), r,
-                    (const float*)nullptr, d, bootstrap, T, B, gamma, 0.0, ret, (float*)nullptr);
+  (void)grid;
+  return launch_scan<false>(r, nullptr, d, bootstrap, T, B, gamma, 0.0, ret, nullptr, as_stream(stream));
 }
 
 extern "C" int rpl_gae(const float* r, const float* v, const uint8_t* d, const float* bootstrap_v,
@@ -208,8 +425,8 @@ extern "C" int rpl_gae(const float* r, const float* v, const uint8_t* d, const f
                        void* stream) {
   if (!r || !v || !d || !bootstrap_v || !adv || T < 1 || B < 1) return RPL_EINVAL;
   dim3 grid((unsigned)((B + 31) / 32));
-  return launch_pdl(k_scan<SCAN_WARPS, SCAN_S, true>, grid, dim3(SCAN_WARPS * 32), 0, as_stream(stream), r, v, d,
-                    bootstrap_v, T, B, gamma, lambda, adv, ret);
+  (void)grid;
+  return launch_scan<true>(r, v, d, bootstrap_v, T, B, gamma, lambda, adv, ret, as_stream(stream));
 }
 
 extern "C" int rpl_returns_nstep(const float* r, const uint8_t* d, int64_t T, int64_t B, int32_t n,

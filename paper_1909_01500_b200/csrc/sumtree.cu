@@ -47,7 +47,18 @@ k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__
   int64_t* leaves = tree + L.level_off[L.depth];
   int64_t* hdr = tree + L.hdr_off;
   pdl_wait();
-  const int64_t maxseen_now = hdr[0];
+  // Issue the first chunk's loads — the entry, and for a single-chunk batch the leaf's
+  // current value — before the hash-table reset and the priority transform, so their
+  // latency overlaps that work instead of sitting on the critical path.
+  const bool single = n <= UPD_THREADS;
+  int64_t pre_leaf = -1, pre_old = 0;
+  float pre_td = 0.0f;
+  if (tid < n) {
+    pre_leaf = idx[tid];
+    if (mode == MODE_TD) pre_td = td[tid];
+  }
+  if (single && pre_leaf >= 0 && pre_leaf < L.n_leaves) pre_old = __ldcg(leaves + pre_leaf);
+  const int64_t maxseen_now = __ldcg(hdr);
   int64_t local_max = INT64_MIN;
   int32_t errbits = 0;
 
@@ -60,13 +71,13 @@ k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__
     const int64_t i = base + tid;
     int64_t leaf = -1, q = 0;
     if (i < n) {
-      leaf = idx[i];
+      leaf = base == 0 ? pre_leaf : idx[i];
       bool ok = leaf < L.n_leaves;  // leaf < 0: padding entry, skipped silently
       if (leaf < 0) {
         leaf = -1;
       } else if (ok) {
         if (mode == MODE_TD) {
-          const double p = (double)fabsf(td[i]) + eps_p;  // RN64(|delta| + eps_p)
+          const double p = (double)fabsf(base == 0 ? pre_td : td[i]) + eps_p;  // RN64(|delta| + eps_p)
           float v;
           if (!isfinite(p)) {
             v = __int_as_float(0x7f800000);
@@ -111,7 +122,8 @@ k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__
     __syncthreads();
     int64_t delta = 0;
     if (leaf >= 0 && hval[slot] == tid) {
-      const int64_t old = __ldcg(leaves + leaf);
+      // earlier chunks may have rewritten this leaf: reload unless the batch is one chunk
+      const int64_t old = single ? pre_old : __ldcg(leaves + leaf);
       leaves[leaf] = q;
       delta = q - old;
       if (delta != 0) {

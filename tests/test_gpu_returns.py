@@ -57,7 +57,10 @@ def test_toy_golden(rpl):
     check_rel(H(ret), g["gae_ret"], what="ret")
 
 
-SHAPES = [(1, 1), (1, 7), (5, 3), (16, 32), (127, 33), (128, 64), (129, 31), (300, 100), (1000, 5)]
+# B % 16 == 0 takes the TMA-tile kernel (ragged T, partial 32-column blocks, multi-chunk T),
+# other B the LDG kernel
+SHAPES = [(1, 1), (1, 7), (5, 3), (16, 32), (127, 33), (128, 64), (129, 31), (300, 100), (1000, 5), (300, 48),
+          (129, 16), (1000, 80), (257, 4096)]
 
 
 @pytest.mark.parametrize("T,B", SHAPES)
