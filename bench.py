@@ -42,7 +42,7 @@ FRAME = 84 * 84
 
 # R2D2: 1M-step ring [4000, 256] (configs[4]), sharded by env columns in Mode L.
 R2D2 = dict(cap_T=4000, B=256, period=40, burn_in=40, train=80, tail=5, k=4, n_step=5, gamma=0.997,
-            alpha=0.9, beta=0.6, batch=64, rnn_h=512, rnn_parts=2, eps=1e-3, eps_p=1e-3, fanout=32)
+            alpha=0.9, beta=0.6, batch=64, rnn_h=512, rnn_parts=2, eps=1e-3, eps_p=1e-3, fanout=32, eta=0.9)
 R2D2["L"] = R2D2["burn_in"] + R2D2["train"] + R2D2["tail"]
 PPO = dict(T=128, B=4096, gamma=0.99, lam=0.95)
 # DQN/Rainbow Atari (configs[2]) and SAC/TD3 Mujoco (configs[3]) secondary line items
@@ -218,7 +218,8 @@ def run_rpl(args):
     td0 = np.abs(g.normal(size=valid.numel())).astype(np.float32)
     tree.update(valid, torch.from_numpy(td0).to(dev), c["alpha"], c["eps_p"])
     P = 8  # distinct per-step |delta| and target-Q inputs (cycled)
-    td_pool = torch.from_numpy(np.abs(g.normal(size=(P, n * max(1, world)))).astype(np.float32)).to(dev)
+    # per-step |delta| of the previous batch's train rows, [P][train, n_glob] (R2D2 learner output)
+    td_pool = torch.from_numpy(np.abs(g.normal(size=(P, c["train"], n * max(1, world)))).astype(np.float32)).to(dev)
     n_glob = n * world
     q_pool = torch.from_numpy(g.normal(0, 10, (P, L, n_glob)).astype(np.float32)).to(dev)
     seed = 0x5EED
@@ -267,8 +268,10 @@ def run_rpl(args):
         s = rpl.ops._stream(dev)
         cur, prev = idx_buf[i % 2], idx_buf[(i + 1) % 2]
         # (a5-a7) new priorities for the previous batch (entries < 0 — not owned — are skipped, R22)
-        rpl._lib.check(lib.rpl_sumtree_update(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]), n_glob,
-                                              c["alpha"], c["eps_p"], None, s), "update")
+        # (NEXT-1 fused) sequence priority = eta max + (1 - eta) mean of the 80 per-step |delta| (R26)
+        rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]),
+                                                  c["train"], n_glob, c["eta"], c["alpha"], c["eps_p"], None, s),
+                       "update_seq")
         if world == 1:
             # (a8) draws only; the batch-min normaliser and IS weights (a9) are fused into the gather
             rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, seed, c["beta"], P_(cur),
@@ -523,8 +526,9 @@ def pipelined_step(dev, rpl, tree, plan, idx_buf, td_pool, q_pool, r_tr, d_tr, y
                 if i >= 2:
                     sA.wait_event(ev_g[(i - 2) % P])
                 a = rpl.ops._stream(dev)
-                rpl._lib.check(lib.rpl_sumtree_update(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]), n,
-                                                      c["alpha"], c["eps_p"], None, a), "update")
+                rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]),
+                                                          c["train"], n, c["eta"], c["alpha"], c["eps_p"], None, a),
+                               "update_seq")
                 rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, seed, c["beta"],
                                                              P_(cur), P_(qb[i % 2]), None, None, P_(err), a),
                                "sample")
@@ -739,8 +743,10 @@ class OracleStep:
         from oracle import returns as OR
         from oracle import sumtree as OS
         c, h = self.c, self.h
-        td = np.abs(self.g.normal(size=len(self.prev))).astype(np.float32)
-        self.tree.update(self.prev, [float(x) for x in td], c["alpha"], c["eps_p"])
+        from oracle import priority as OPR
+        steps = np.abs(self.g.normal(size=(c["train"], len(self.prev)))).astype(np.float32)
+        td = [OPR.sequence_td(steps[:, j], c["eta"]) for j in range(len(self.prev))]
+        self.tree.update(self.prev, td, c["alpha"], c["eps_p"])
         draws = OP.draws_u64(0x5EED, self.ctr, nseq)
         self.ctr += nseq
         idx, q, qmin = self.tree.sample(nseq, draws)
@@ -786,7 +792,7 @@ def cpu_baseline(c, host, seconds):
     dt = time.time() - t0
     aff, model = _cores()
     return {"value": done / dt, "unit": "sequences/s", "cores": 1, "kind": "oracle",
-            "sample": f"{nsteps} full R2D2 steps ({c['batch']} sequences each: update + sample over "
+            "sample": f"{nsteps} full R2D2 steps ({c['batch']} sequences each: eta-mixed update + sample over "
                       f"{o.tree.n_leaves} leaves + stacked gather + rescaled 5-step targets), {dt:.1f} s",
             "host_cpus": os.cpu_count(), "affinity": aff, "cpu_model": model}
 

@@ -132,6 +132,17 @@ int rpl_sumtree_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* i
                        const float* td_abs, int64_t n, double alpha, double eps_p,
                        int32_t* dev_err, void* stream);
 
+/* R2D2 sequence priorities (§8f NEXT-1; "eta = 0.9 mix of max and mean", reading
+ * R26): td_steps [T_p, n] f32, time-major per-step |delta| of the n sampled sequences
+ * (e.g. the 80 train rows).  Sequence k gets
+ *   td_k = RN32(eta * max_t |d_tk| + (1 - eta) * (sum_t |d_tk|) / T_p)
+ * (fp64, sum in increasing t, no fused multiply-add), then exactly rpl_sumtree_update's
+ * transform and write: identical to rpl_sumtree_update(idx, td, n, alpha, eps_p).
+ * eta in [0, 1]; T_p >= 1. */
+int rpl_sumtree_update_seq(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx,
+                           const float* td_steps, int64_t T_p, int64_t n, double eta, double alpha,
+                           double eps_p, int32_t* dev_err, void* stream);
+
 /* Direct leaf write (append / validity maintenance, §8a a12): leaf idx[k] := q[k]
  * (last write wins; max-seen updated), or := current max-seen when q == NULL.
  * q values > q_cap are clamped (+ RPL_DERR_SATURATED); q < 0 is invalid (skipped + IDX). */

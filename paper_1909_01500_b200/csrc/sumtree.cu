@@ -29,7 +29,36 @@ constexpr int HASH_SLOTS = 2048;
 constexpr unsigned long long HASH_EMPTY = ~0ull;
 constexpr int SAMPLE_WARPS = 8;
 
-enum { MODE_TD = 0, MODE_Q = 1, MODE_MAXSEEN = 2 };
+enum { MODE_TD = 0, MODE_Q = 1, MODE_MAXSEEN = 2, MODE_SEQ = 3 };
+
+// R2D2 sequence priority (§8f NEXT-1, reading R26): column i of the time-major per-step
+// |delta| [T_p, n] -> RN32(eta * max + (1 - eta) * mean).  Eight lanes per sequence:
+// lane j sums rows t = j (mod 8) in increasing t (its loads all in flight at once), then
+// the fixed pairwise tree ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)) via xor-shuffles 1, 2, 4 —
+// the oracle's exact fp64 operation order; no FMA contraction.  All 32 lanes of the warp
+// must call (groups of 8 consecutive lanes share i).
+__device__ __forceinline__ float sequence_td8(const float* __restrict__ steps, int64_t T_p, int64_t n, int64_t i,
+                                              bool active, double eta) {
+  const int j = threadIdx.x & 7;
+  double mx = 0.0, sm = 0.0;
+  if (active) {
+    for (int64_t t = j; t < T_p; t += 8) {
+      const double v = fabs((double)__ldg(steps + t * n + i));
+      if (v > mx) mx = v;
+      sm = __dadd_rn(sm, v);
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    const double so = __shfl_xor_sync(0xffffffffu, sm, o);
+    const double mo = __shfl_xor_sync(0xffffffffu, mx, o);
+    sm = __dadd_rn(sm, so);  // IEEE addition is commutative: both partners get the same sum
+    if (mo > mx) mx = mo;
+  }
+  const double mean = __ddiv_rn(sm, (double)T_p);
+  const double mix = __dadd_rn(__dmul_rn(eta, mx), __dmul_rn(__dadd_rn(1.0, -eta), mean));
+  return __double2float_rn(mix);
+}
 
 __device__ __forceinline__ uint32_t hash_slot(int64_t leaf) {
   return (uint32_t)(((unsigned long long)leaf * 0x9E3779B97F4A7C15ull) >> 53) & (HASH_SLOTS - 1);
@@ -38,10 +67,11 @@ __device__ __forceinline__ uint32_t hash_slot(int64_t leaf) {
 __global__ void __launch_bounds__(UPD_THREADS)
 k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__ idx,
               const float* __restrict__ td, const int64_t* __restrict__ qin, int mode, int64_t n,
-              double alpha, double eps_p, int32_t* err, int force_slow) {
+              double alpha, double eps_p, int32_t* err, int force_slow, int64_t T_p, double eta) {
   __shared__ unsigned long long hkey[HASH_SLOTS];
   __shared__ int hval[HASH_SLOTS];
   __shared__ int64_t sred[UPD_THREADS / 32];
+  __shared__ float s_td[UPD_THREADS];  // MODE_SEQ: this chunk's sequence priorities
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   int64_t* leaves = tree + L.level_off[L.depth];
@@ -67,6 +97,14 @@ k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__
       hkey[s] = HASH_EMPTY;
       hval[s] = -1;
     }
+    if (mode == MODE_SEQ) {  // this chunk's sequence priorities, 8 lanes per sequence
+      const int64_t cnt = min((int64_t)UPD_THREADS, n - base);
+      for (int64_t r0 = 0; r0 < cnt; r0 += UPD_THREADS / 8) {
+        const int64_t jj = r0 + (tid >> 3);
+        const float v = sequence_td8(td, T_p, n, base + jj, jj < cnt, eta);
+        if ((tid & 7) == 0 && jj < cnt) s_td[jj] = v;
+      }
+    }
     __syncthreads();
     const int64_t i = base + tid;
     int64_t leaf = -1, q = 0;
@@ -76,8 +114,9 @@ k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__
       if (leaf < 0) {
         leaf = -1;
       } else if (ok) {
-        if (mode == MODE_TD) {
-          const double p = (double)fabsf(base == 0 ? pre_td : td[i]) + eps_p;  // RN64(|delta| + eps_p)
+        if (mode == MODE_TD || mode == MODE_SEQ) {
+          const float tdi = mode == MODE_SEQ ? s_td[tid] : (base == 0 ? pre_td : td[i]);
+          const double p = (double)fabsf(tdi) + eps_p;  // RN64(|delta| + eps_p)
           float v;
           if (!isfinite(p)) {
             v = __int_as_float(0x7f800000);
@@ -446,12 +485,12 @@ bool layout_ok(const rpl_tree_layout* L) {
 
 int launch_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, const float* td,
                   const int64_t* q, int mode, int64_t n, double alpha, double eps_p, int32_t* err,
-                  void* stream, int force_slow) {
+                  void* stream, int force_slow, int64_t T_p = 0, double eta = 0.0) {
   if (!layout_ok(L) || !tree || n < 0) return RPL_EINVAL;
   if (n == 0) return RPL_OK;
   if (!idx) return RPL_EINVAL;
   return launch_pdl(k_tree_update, dim3(1), dim3(UPD_THREADS), 0, as_stream(stream), tree_dev(L), tree, idx, td, q,
-                    mode, n, alpha, eps_p, err, force_slow);
+                    mode, n, alpha, eps_p, err, force_slow, T_p, eta);
 }
 
 }  // namespace
@@ -607,4 +646,12 @@ extern "C" int rpl_sample_uniform(int64_t n, uint64_t seed, uint64_t offset, uin
   if ((double)n_rows * (double)B >= 4.6e18) return RPL_EINVAL;
   return launch_pdl(k_sample_uniform, dim3(1), dim3(UNI_THREADS), 0, as_stream(stream), n, seed, offset, ctr, lo_row,
                     n_rows, cap_T, B, out_idx);
+}
+
+extern "C" int rpl_sumtree_update_seq(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx,
+                                      const float* td_steps, int64_t T_p, int64_t n, double eta, double alpha,
+                                      double eps_p, int32_t* dev_err, void* stream) {
+  if (n > 0 && (!td_steps || T_p < 1)) return RPL_EINVAL;
+  if (!(alpha >= 0.0) || !(eps_p >= 0.0) || !(eta >= 0.0 && eta <= 1.0)) return RPL_EINVAL;
+  return launch_update(L, tree, idx, td_steps, nullptr, MODE_SEQ, n, alpha, eps_p, dev_err, stream, 0, T_p, eta);
 }

@@ -189,6 +189,17 @@ class SumTree:
         check(lib.rpl_sumtree_update(self._lp, _ptr(self.storage), _ptr(idx), _ptr(td_abs), idx.numel(),
                                      float(alpha), float(eps_p), _ptr(e), self._s()), "rpl_sumtree_update")
 
+    def update_seq(self, idx, td_steps, alpha, eta=0.9, eps_p=1e-3, err=None):
+        """rpl_sumtree_update_seq: R2D2 eta-mix of per-step |delta| [T_p, n] per sequence, then update."""
+        _req(idx, torch.int64, "idx")
+        _req(td_steps, torch.float32, "td_steps")
+        if td_steps.dim() != 2 or td_steps.shape[1] != idx.numel():
+            raise ValueError("td_steps must be [T_p, n] with n = idx.numel()")
+        e = self.err if err is None else err
+        check(lib.rpl_sumtree_update_seq(self._lp, _ptr(self.storage), _ptr(idx), _ptr(td_steps),
+                                         td_steps.shape[0], idx.numel(), float(eta), float(alpha), float(eps_p),
+                                         _ptr(e), self._s()), "rpl_sumtree_update_seq")
+
     def set_q(self, idx, q=None, err=None):
         _req(idx, torch.int64, "idx")
         if q is not None:

@@ -351,3 +351,25 @@ def test_sharded_compacted(rpl, mode):
             collected += (idx[:m] + rank * n_local).tolist()
             collected_q += q[:m].tolist()
         assert collected == ref_idx and collected_q == ref_q
+
+
+@pytest.mark.parametrize("T_p,n,eta", [(80, 64, 0.9), (1, 5, 0.9), (7, 300, 0.0), (80, 1200, 1.0), (33, 64, 0.37)])
+def test_update_seq_vs_oracle(rpl, T_p, n, eta):
+    # NEXT-1: R2D2 eta-mix of per-step |delta| per sequence, then the update — tree bit-exact
+    import torch
+    g = rng(T_p * 1000 + n)
+    N = 25600
+    steps = np.abs(g.lognormal(0, 2, (T_p, n))).astype(np.float32)
+    steps[:, :3] = 0.0                                   # an all-zero sequence -> eps_p floor
+    idx = g.integers(0, N, n).astype(np.int64)
+    idx[5 % n] = idx[0]                                  # duplicate: the later column wins
+    t = rpl.SumTree(N, 32)
+    t.update_seq(T_(idx), T_(steps), 0.9, eta=eta)
+    orc = OS.SumTreeOracle(N)
+    td = [OPR.sequence_td(steps[:, k], eta) for k in range(n)]
+    orc.update([int(x) for x in idx], td, 0.9)
+    check_tree_consistent(t, orc)
+    # == rpl_sumtree_update on the oracle's fp32 mixes
+    t2 = rpl.SumTree(N, 32)
+    t2.update(T_(idx), T_(np.array(td, np.float32)), 0.9)
+    assert np.array_equal(H(t.storage), H(t2.storage))

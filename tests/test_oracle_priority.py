@@ -110,3 +110,23 @@ def test_rn32_helper_matches_numpy():
     g = np.random.default_rng(5)
     for x in np.concatenate([g.normal(0, 1e3, 500) ** 2, 10.0 ** g.uniform(-40, 38, 500)]):
         assert P.rn32(float(x)) == float(np.float32(x))
+
+
+# ---- R2D2 sequence priority (reading R26) ----
+def test_sequence_td_eta_one_is_max_and_zero_is_mean():
+    col = [0.5, 3.25, 1.0, 0.0]
+    assert P.sequence_td(col, 1.0) == 3.25                      # eta = 1: the max (already fp32)
+    assert P.sequence_td(col, 0.0) == (0.5 + 3.25 + 1.0) / 4    # eta = 0: the mean, exact here
+
+
+def test_sequence_td_worked_example_and_constant():
+    # [1, 2, 3], eta = 0.9: 0.9*3 + 0.1*2 = 2.9 -> the fp32 nearest 2.9
+    assert P.sequence_td([1.0, 2.0, 3.0], 0.9) == float(np.float32(2.9))
+    c = float(np.float32(0.37))
+    assert P.sequence_td([c] * 80, 0.9) == c                    # constant column -> itself
+
+
+def test_sequence_td_order_of_max_and_abs():
+    a = P.sequence_td([-4.0, 1.0, 2.0], 0.5)
+    b = P.sequence_td([2.0, 1.0, 4.0], 0.5)
+    assert a == b == float(np.float32(0.5 * 4 + 0.5 * (7 / 3)))
