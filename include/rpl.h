@@ -297,6 +297,32 @@ typedef struct {
 int rpl_gather(const rpl_gather_desc* desc /* host */, const int64_t* idx, const int64_t* q,
                const int64_t* qmin, double beta, int64_t n, int32_t* dev_err, void* stream);
 
+/* =========================================================================
+ * (4) Ring append and validity maintenance (§8a a12, §8f NEXT-2; P:75-84 the sampler
+ *     writes batches while the optimiser samples).
+ * ========================================================================= */
+
+/* Copy a sampler batch of T_b rows into the ring described by `ring` (its obs / act / rew /
+ * done / rnn pointers, geometry and `cursor`): batch arrays obs [T_b, B, obs_bytes],
+ * act [T_b, B, act_bytes], rew f32 [T_b, B], done u8 [T_b, B] go to ring rows cursor ..
+ * cursor+T_b-1 (mod cap_T) — at most two cudaMemcpyAsync each, so the source may be host
+ * (pinned) or device memory.  rnn [n_blk, B, rnn_parts, rnn_bytes] holds the stored state
+ * of the batch rows t with (cursor + t) % period == 0, in order (periodic storage).
+ * Any source may be NULL (not written).  The caller advances cursor / size afterwards and
+ * calls rpl_replay_validity.  RPL_EINVAL: T_b > cap_T, bad geometry. */
+int rpl_ring_append(const rpl_gather_desc* ring, const void* obs, const void* act, const float* rew,
+                    const uint8_t* done, const void* rnn, int64_t T_b, void* stream);
+
+/* Tree validity maintenance after the ring moved from (cursor_old, size_old) to
+ * (cursor_new, size_new): every leaf (kind TRANSITION: row*B+b with k, n_step; SEQUENCE:
+ * block*B+b with k, seq_len, period) whose validity (§8c #2, #16) changed gets q = the
+ * tree's max-priority-seen (became valid) or q = 0 (became invalid: never sampled),
+ * with exact int64 propagation.  Leaves whose validity did not change keep their q.
+ * L->n_leaves must equal (cap_T or cap_T/period) * B. */
+int rpl_replay_validity(const rpl_tree_layout* L, int64_t* tree, int32_t kind, int64_t cap_T, int64_t B,
+                        int32_t k, int32_t n_step, int32_t seq_len, int32_t period, int64_t cursor_old,
+                        int64_t size_old, int64_t cursor_new, int64_t size_new, void* stream);
+
 /* -------------------------------------------------------------------------
  * Diagnostics (tests only): v[k] = RN32(RN64(|td_abs[k]| + eps_p)^alpha) exactly as
  * rpl_sumtree_update computes it (§8c #7); force_slow != 0 runs the double-double

@@ -85,6 +85,9 @@ _SIGS = {
     "rpl_is_weights": ([P, P, I64, D, P, P], C.c_int),
     "rpl_sample_uniform": ([I64, U64, U64, P, I64, I64, I64, I64, P, P], C.c_int),
     "rpl_gather": ([C.POINTER(GatherDesc), P, P, P, D, I64, P, P], C.c_int),
+    "rpl_ring_append": ([C.POINTER(GatherDesc), P, P, P, P, P, I64, P], C.c_int),
+    "rpl_replay_validity": ([C.POINTER(TreeLayout), P, I32, I64, I64, I32, I32, I32, I32, I64, I64, I64, I64, P],
+                            C.c_int),
     "rpl_debug_priority_values": ([P, I64, D, D, I32, P, P, P], C.c_int),
     "rpl_debug_set_gather_variant": ([I32], C.c_int),
     "rpl_debug_set_gather_diag": ([I32], C.c_int),

@@ -17,6 +17,7 @@ from ._lib import GatherDesc, TreeLayout, check, lib
 __all__ = [
     "returns_discounted", "returns_nstep", "gae", "value_rescale", "SumTree", "is_weights", "gather",
     "GatherRing", "GatherPlan", "check_err", "launch_count", "debug_priority_values", "sample_uniform",
+    "ring_append",
 ]
 
 
@@ -199,6 +200,14 @@ class SumTree:
         check(lib.rpl_sumtree_update_seq(self._lp, _ptr(self.storage), _ptr(idx), _ptr(td_steps),
                                          td_steps.shape[0], idx.numel(), float(eta), float(alpha), float(eps_p),
                                          _ptr(e), self._s()), "rpl_sumtree_update_seq")
+
+    def validity(self, kind, cap_T, B, k, cursor_old, size_old, cursor_new, size_new, n_step=1, seq_len=1,
+                 period=1):
+        """rpl_replay_validity: leaves that became valid get max-seen, those that became invalid 0."""
+        kind_i = _lib.GATHER_TRANSITION if kind == "transition" else _lib.GATHER_SEQUENCE
+        check(lib.rpl_replay_validity(self._lp, _ptr(self.storage), kind_i, int(cap_T), int(B), int(k), int(n_step),
+                                      int(seq_len), int(period), int(cursor_old), int(size_old), int(cursor_new),
+                                      int(size_new), self._s()), "rpl_replay_validity")
 
     def set_q(self, idx, q=None, err=None):
         _req(idx, torch.int64, "idx")
@@ -429,3 +438,21 @@ class GatherPlan:
         check(lib.rpl_gather(self._dp, _ptr(idx), _ptr(q), _ptr(qmin), float(beta), self.n, _ptr(err), s),
               "rpl_gather")
         return self.outputs
+
+
+def ring_append(ring: GatherRing, obs=None, act=None, rew=None, done=None, rnn=None, period=1):
+    """rpl_ring_append: write a [T_b, B, ...] sampler batch (host-pinned or device tensors) at
+    ring.cursor, then advance ring.cursor / ring.size.  Returns (cursor_old, size_old) for
+    SumTree.validity."""
+    src = next(t for t in (obs, act, rew, done) if t is not None)
+    T_b = int(src.shape[0])
+    for name, t in (("obs", obs), ("act", act), ("rew", rew), ("done", done), ("rnn", rnn)):
+        if t is not None and not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+    g = _desc(ring, _lib.GATHER_SEQUENCE, 1, _lib.PAD_REPEAT, _lib.OUT_STACKED, 1, 1, period, 0.0)
+    check(lib.rpl_ring_append(C.byref(g), _ptr(obs), _ptr(act), _ptr(rew), _ptr(done), _ptr(rnn), T_b,
+                              _stream(ring.obs.device)), "rpl_ring_append")
+    old = (ring.cursor, ring.size)
+    ring.cursor = (ring.cursor + T_b) % ring.cap_T
+    ring.size = min(ring.cap_T, ring.size + T_b)
+    return old
