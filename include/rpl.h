@@ -323,6 +323,31 @@ int rpl_replay_validity(const rpl_tree_layout* L, int64_t* tree, int32_t kind, i
                         int32_t k, int32_t n_step, int32_t seq_len, int32_t period, int64_t cursor_old,
                         int64_t size_old, int64_t cursor_new, int64_t size_new, void* stream);
 
+/* =========================================================================
+ * (5) Learning targets right after the gather (§8f NEXT-3; P:34 Double-DQN / Categorical,
+ *     P:38 n-step).
+ * ========================================================================= */
+
+/* n-step targets with the double-Q bootstrap: q_online, q_target [T+1, B, A] f32 (the two
+ * networks' action values for rows 0..T); for output row t (0..T-n) the bootstrap is
+ * q_target[t+n, b, a*] with a* = argmax_a q_online[t+n, b, a] (first maximum, NaN never
+ * wins, R27) — then exactly rpl_returns_nstep's target (R24), rescaled (R4, R5) when
+ * rescale != 0.  ret_n [T-n+1, B] f32, done_n (may be NULL) u8, a_star (may be NULL) int32. */
+int rpl_returns_nstep_dq(const float* r, const uint8_t* d, int64_t T, int64_t B, int32_t n, double gamma,
+                         const float* q_online, const float* q_target, int32_t A, int32_t rescale,
+                         double rescale_eps, float* ret_n, uint8_t* done_n, int32_t* a_star, void* stream);
+
+/* Categorical (C51) projection [EXT: Bellemare et al. 2017, Alg. 1]: for each sample s,
+ * a* = argmax q_online[s, :] (R27; q_online may be NULL when A == 1), p = p_target[s, a*, :]
+ * over n_atoms atoms z_j = v_min + j (v_max - v_min)/(n_atoms - 1), g = gamma_n unless
+ * done_n[s] (then 0; done_n may be NULL), Tz_j = clip(R[s] + g z_j, v_min, v_max),
+ * b_j = (Tz_j - v_min)/dz, and m_out[s, i] = sum_j p_j max(0, 1 - |b_j - i|) (fp64, R28:
+ * the algorithm's floor/ceil split written as a gather).  p_target [n, A, n_atoms] f32,
+ * m_out [n, n_atoms] f32, a_star [n] int32 (may be NULL). */
+int rpl_c51_project(const float* p_target, const float* q_online, const float* R, const uint8_t* done_n,
+                    int64_t n, int32_t A, int32_t n_atoms, double v_min, double v_max, double gamma_n,
+                    float* m_out, int32_t* a_star, void* stream);
+
 /* -------------------------------------------------------------------------
  * Diagnostics (tests only): v[k] = RN32(RN64(|td_abs[k]| + eps_p)^alpha) exactly as
  * rpl_sumtree_update computes it (§8c #7); force_slow != 0 runs the double-double

@@ -17,7 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "librpl.so")
-SOURCES = ["abi.cu", "returns.cu", "sumtree.cu", "gather.cu", "append.cu"]
+SOURCES = ["abi.cu", "returns.cu", "sumtree.cu", "gather.cu", "append.cu", "targets.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 

@@ -17,7 +17,7 @@ from ._lib import GatherDesc, TreeLayout, check, lib
 __all__ = [
     "returns_discounted", "returns_nstep", "gae", "value_rescale", "SumTree", "is_weights", "gather",
     "GatherRing", "GatherPlan", "check_err", "launch_count", "debug_priority_values", "sample_uniform",
-    "ring_append",
+    "ring_append", "returns_nstep_dq", "c51_project",
 ]
 
 
@@ -86,6 +86,43 @@ def returns_nstep(r, d, n, gamma, q=None, q_boot=None, rescale=False, eps=1e-3, 
                                 1 if rescale else 0, float(eps), _ptr(out), _ptr(done_out), _stream(r.device)),
           "rpl_returns_nstep")
     return out, done_out
+
+
+def returns_nstep_dq(r, d, n, gamma, q_online, q_target, rescale=False, eps=1e-3, out=None, done_out=None):
+    """rpl_returns_nstep_dq: q_online / q_target [T+1, B, A]. Returns (y, done_n, a_star)."""
+    T, B = r.shape
+    _req(r, torch.float32, "r")
+    _req(d, torch.uint8, "d", (T, B))
+    _req(q_online, torch.float32, "q_online")
+    A = int(q_online.shape[-1])
+    _req(q_target, torch.float32, "q_target", (T + 1, B, A))
+    if tuple(q_online.shape) != (T + 1, B, A):
+        raise ValueError("q_online must be [T+1, B, A]")
+    rows = T - int(n) + 1
+    out = torch.empty((rows, B), dtype=torch.float32, device=r.device) if out is None else out
+    done_out = torch.empty((rows, B), dtype=torch.uint8, device=r.device) if done_out is None else done_out
+    a_star = torch.empty((rows, B), dtype=torch.int32, device=r.device)
+    check(lib.rpl_returns_nstep_dq(_ptr(r), _ptr(d), T, B, int(n), float(gamma), _ptr(q_online), _ptr(q_target), A,
+                                   1 if rescale else 0, float(eps), _ptr(out), _ptr(done_out), _ptr(a_star),
+                                   _stream(r.device)), "rpl_returns_nstep_dq")
+    return out, done_out, a_star
+
+
+def c51_project(p_target, q_online, R, done_n, v_min, v_max, gamma_n, out=None):
+    """rpl_c51_project: p_target [n, A, N], q_online [n, A] or None (A == 1). Returns (m [n, N], a_star)."""
+    _req(p_target, torch.float32, "p_target")
+    n, A, N = (int(x) for x in p_target.shape)
+    if q_online is not None:
+        _req(q_online, torch.float32, "q_online", (n, A))
+    _req(R, torch.float32, "R", (n,))
+    if done_n is not None:
+        _req(done_n, torch.uint8, "done_n", (n,))
+    out = torch.empty((n, N), dtype=torch.float32, device=p_target.device) if out is None else out
+    a_star = torch.empty(n, dtype=torch.int32, device=p_target.device)
+    check(lib.rpl_c51_project(_ptr(p_target), _ptr(q_online), _ptr(R), _ptr(done_n), n, A, N, float(v_min),
+                              float(v_max), float(gamma_n), _ptr(out), _ptr(a_star), _stream(p_target.device)),
+          "rpl_c51_project")
+    return out, a_star
 
 
 def gae(r, v, d, bootstrap_v, gamma, lam, adv=None, ret=None):
