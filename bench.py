@@ -45,6 +45,9 @@ R2D2 = dict(cap_T=4000, B=256, period=40, burn_in=40, train=80, tail=5, k=4, n_s
             alpha=0.9, beta=0.6, batch=64, rnn_h=512, rnn_parts=2, eps=1e-3, eps_p=1e-3, fanout=32, eta=0.9)
 R2D2["L"] = R2D2["burn_in"] + R2D2["train"] + R2D2["tail"]
 PPO = dict(T=128, B=4096, gamma=0.99, lam=0.95)
+SPEC_HBM_GBS = 8000.0
+# north_star's "1M-sequence R2D2 buffer": 2^20 sequence leaves over 8 GPUs; one shard per GPU
+R2D2_1MSEQ_SHARD = dict(cap_T=40960, B=128)
 # DQN/Rainbow Atari (configs[2]) and SAC/TD3 Mujoco (configs[3]) secondary line items
 DQN = dict(cap_T=4096, B=256, k=4, n_step=3, gamma=0.99, alpha=0.6, beta=0.4, eps_p=1e-3, fanout=32,
            batches=(32, 128, 512))
@@ -403,13 +406,16 @@ def run_rpl(args):
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic.get("bytes"), "traffic_source": traffic.get("source"),
                      "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": g_ms,
-                     "step_share": g_ms / (ms / K_eff)},
+                     "step_share": g_ms / (ms / K_eff),
+                     "frac_of_spec": achieved / SPEC_HBM_GBS, "spec_peak": SPEC_HBM_GBS,
+                     "spec_note": "north_star's ~8 TB/s nominal (DGX B200 figure) as the second denominator"},
     }
     if not args.profile:
         result["clocks"] = clk
         result["e2e"] = e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K_eff, world)
     if world == 1 and not args.no_secondary and not args.profile:
-        result["secondary"] = {"r2d2_pipelined": pipelined, "tree_latency": tree_latency(dev, rpl),
+        result["secondary"] = {"r2d2_pipelined": pipelined, "r2d2_1mseq": bench_r2d2_1mseq(dev, rpl, c),
+                               "tree_latency": tree_latency(dev, rpl),
                                "ppo_returns": bench_ppo(dev, rpl), "dqn_replay": bench_dqn(dev, rpl),
                                "mujoco_replay": bench_mujoco(dev, rpl)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -570,6 +576,58 @@ def pipelined_step(dev, rpl, tree, plan, idx_buf, td_pool, q_pool, r_tr, d_tr, y
     ms = e0.elapsed_time(e1) / (reps * P)
     return {"us_per_step": ms * 1e3, "sequences_per_s": n / (ms / 1e3),
             "timing": "CUDA graph of 8 steps on two streams (update+sample || gather+n-step), replayed"}
+
+
+def bench_r2d2_1mseq(dev, rpl, c):
+    """The north_star's 1M-sequence buffer at N=1: ONE of its 8 shards, a [40960, 128] ring
+    (37 GB of frames, 131,072 sequence leaves, D=4 tree), same 4-call step as the headline
+    (graph of 8 steps).  The frames span ~145x the TLB reach."""
+    import torch
+    from paper_1909_01500_b200 import replay as R
+    from synth.device import make_ring_device
+    cap, B = R2D2_1MSEQ_SHARD["cap_T"], R2D2_1MSEQ_SHARD["B"]
+    L, k, period, n = c["L"], c["k"], c["period"], c["batch"]
+    ring = make_ring_device(31337, cap, B, dev, ep_len=2000.0, period=period, rnn_parts=c["rnn_parts"],
+                            rnn_h=c["rnn_h"], cursor=777)
+    n_leaves = (cap // period) * B
+    tree = rpl.SumTree(n_leaves, c["fanout"], 32, device=dev)
+    valid = torch.from_numpy(R.leaves_of(R.valid_sequence_blocks(cap, period, ring.cursor, ring.size, k, L), B)).to(dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(3)
+    tree.update(valid, torch.randn(valid.numel(), generator=g, device=dev).abs(), c["alpha"], c["eps_p"])
+    plan = rpl.GatherPlan(ring, n, kind="sequence", k=k, seq_len=L, period=period, with_weights=True)
+    out = plan.outputs
+    idx = [torch.full((n,), -1, dtype=torch.int64, device=dev) for _ in range(2)]
+    q = torch.zeros(n, dtype=torch.int64, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    td = torch.randn((8, c["train"], n), generator=g, device=dev).abs()
+    qv = torch.randn((8, L, n), generator=g, device=dev) * 10
+    Tn = c["train"] + c["n_step"] - 1
+    r_tr = out["rew"][c["burn_in"]:c["burn_in"] + Tn]
+    d_tr = out["done"][c["burn_in"]:c["burn_in"] + Tn]
+    y = torch.empty((c["train"], n), dtype=torch.float32, device=dev)
+    dn = torch.empty((c["train"], n), dtype=torch.uint8, device=dev)
+    lib, P_ = rpl._lib.lib, rpl.ops._ptr
+
+    def step(i):
+        s = rpl.ops._stream(dev)
+        rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(idx[(i + 1) % 2]), P_(td[i % 8]),
+                                                  c["train"], n, c["eta"], c["alpha"], c["eps_p"], None, s), "upd")
+        rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, 0xBEEF, c["beta"], P_(idx[i % 2]),
+                                                     P_(q), None, None, P_(err), s), "sample")
+        plan.run(idx[i % 2], q=q, qmin=None, beta=c["beta"], err=err, stream=s)
+        rpl._lib.check(lib.rpl_returns_nstep(P_(r_tr), P_(d_tr), Tn, n, c["n_step"], c["gamma"],
+                                             P_(qv[i % 8][c["burn_in"]:c["burn_in"] + Tn]),
+                                             P_(qv[i % 8][c["burn_in"] + Tn]), 1, c["eps"], P_(y), P_(dn), s), "nstep")
+
+    ms = _graph_time(dev, step, P=8, reps=50)
+    rpl.check_err(err)
+    res = {"workload": "r2d2_1mseq_one_shard", "ring_per_gpu": [cap, B], "ring_gb": ring.obs.numel() / 1e9,
+           "leaves_per_gpu": n_leaves, "tree_depth": tree.depth, "us_per_step": ms * 1e3,
+           "sequences_per_s": n / (ms / 1e3), "timing": "CUDA graph of 8 steps, replayed"}
+    del ring, tree, plan, out
+    torch.cuda.empty_cache()
+    return res
 
 
 def tree_latency(dev, rpl):
