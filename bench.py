@@ -144,6 +144,17 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def r2d2_config(c, world, mode="L"):
+    """The workload description both arms print (BASELINE configs[4])."""
+    Bl = c["B"] // max(1, world)
+    return {"workload": "r2d2_1mstep", "ring": [c["cap_T"], c["B"]], "ring_per_gpu": [c["cap_T"], Bl],
+            "leaves_per_gpu": (c["cap_T"] // c["period"]) * Bl, "batch_per_gpu": c["batch"], "seq_len": c["L"],
+            "burn_in": c["burn_in"], "train": c["train"], "tail": c["tail"], "frame_stack": c["k"],
+            "n_step": c["n_step"], "gamma": c["gamma"], "alpha": c["alpha"], "beta": c["beta"], "eta": c["eta"],
+            "out": "stacked", "parallelism": (f"mode-{mode} x{world}" if world > 1 else "single"),
+            "l2": "inputs larger than L2 (7.2 GB ring, random sequences every step)"}
+
+
 def gather_traffic():
     """DRAM bytes (read + write) per launch of the sequence gather from the committed
     ncu --set full capture (profiles/gather_traffic.json, written by
@@ -394,13 +405,8 @@ def run_rpl(args):
         "vs_baseline": None,
         "dtype": "u8 frames + f32 (fp64 accum) + int64 tree",
         "data": "synthetic (seeded; uniform-random 84x84 u8 frames, R2D2 reward/episode recipe, DESIGN.md)",
-        "config": {"workload": "r2d2_1mstep", "ring": [c["cap_T"], c["B"]], "ring_per_gpu": [c["cap_T"], Bl],
-                   "leaves_per_gpu": n_leaves, "batch_per_gpu": n, "seq_len": L, "burn_in": c["burn_in"],
-                   "train": c["train"], "tail": c["tail"], "frame_stack": k, "n_step": c["n_step"],
-                   "gamma": c["gamma"], "alpha": c["alpha"], "beta": c["beta"], "out": "stacked",
-                   "parallelism": (f"mode-{args.mode} x{world}" if world > 1 else "single"),
-                   "l2": "inputs larger than L2 (7.2 GB ring, random sequences every step)",
-                   "timing": "cuda graph of 8 steps, replayed" if use_graph else "eager launches"},
+        "config": dict(r2d2_config(c, world, args.mode),
+                       timing="cuda graph of 8 steps, replayed" if use_graph else "eager launches"),
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "k_gather_seq_pipe_lsu", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
@@ -885,7 +891,8 @@ def run_reference(args):
            "unit": "sequences/s", "n_gpus": world, "steps": K, "warmup": min(W, 3), "ms_per_step": dt / K * 1e3,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 / python int",
            "data": "synthetic (seeded, same recipe)",
-           "config": {"workload": "r2d2_1mstep", "ring": [c["cap_T"], c["B"]], "batch_per_step": nseq},
+           "config": dict(r2d2_config(c, 1), timing="host wall clock, single thread",
+                          oracle_batch_per_step=nseq),
            "cpu_baseline": {"value": val, "unit": "sequences/s", "cores": 1, "kind": "oracle",
                             "sample": f"{K} steps of {nseq} sequences (bounded sample of the 64-sequence step)",
                             "host_cpus": os.cpu_count(), "affinity": aff, "cpu_model": model},
