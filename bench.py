@@ -421,6 +421,8 @@ def run_rpl(args):
         result["e2e"] = e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K_eff, world)
     if world == 1 and not args.no_secondary and not args.profile:
         result["secondary"] = {"r2d2_pipelined": pipelined, "r2d2_1mseq": bench_r2d2_1mseq(dev, rpl, c),
+                               "r2d2_unique_output": unique_output_step(dev, rpl, tree, ring, idx_buf, td_pool, q_pool,
+                                                                        err, c, n, P, seed),
                                "tree_latency": tree_latency(dev, rpl),
                                "ppo_returns": bench_ppo(dev, rpl), "dqn_replay": bench_dqn(dev, rpl),
                                "mujoco_replay": bench_mujoco(dev, rpl)}
@@ -634,6 +636,44 @@ def bench_r2d2_1mseq(dev, rpl, c):
     del ring, tree, plan, out
     torch.cuda.empty_cache()
     return res
+
+
+def unique_output_step(dev, rpl, tree, ring, idx_buf, td_pool, q_pool, err, c, n, P, seed):
+    """The headline step with RPL_OUT_UNIQUE output: the gather writes each sequence's 128
+    unique frames once ([L+k-1, n, 84, 84]) instead of 125 k-stacks (the learner's first
+    layer stacks on the fly) — SURVEY §8d's 'unique' byte count: 116 MB per 64 sequences."""
+    import torch
+    from paper_1909_01500_b200 import _lib
+    lib, P_ = rpl._lib.lib, rpl.ops._ptr
+    L, k, period = c["L"], c["k"], c["period"]
+    plan = rpl.GatherPlan(ring, n, kind="sequence", k=k, seq_len=L, period=period, with_weights=True,
+                          out_mode=_lib.OUT_UNIQUE)
+    out = plan.outputs
+    q = torch.zeros(n, dtype=torch.int64, device=dev)
+    Tn = c["train"] + c["n_step"] - 1
+    r_tr = out["rew"][c["burn_in"]:c["burn_in"] + Tn]
+    d_tr = out["done"][c["burn_in"]:c["burn_in"] + Tn]
+    y = torch.empty((c["train"], n), dtype=torch.float32, device=dev)
+    dn = torch.empty((c["train"], n), dtype=torch.uint8, device=dev)
+
+    def step(i):
+        s = rpl.ops._stream(dev)
+        cur, prev = idx_buf[i % 2], idx_buf[(i + 1) % 2]
+        rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]),
+                                                  c["train"], n, c["eta"], c["alpha"], c["eps_p"], None, s), "upd")
+        rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, seed, c["beta"], P_(cur), P_(q),
+                                                     None, None, P_(err), s), "sample")
+        plan.run(cur, q=q, qmin=None, beta=c["beta"], err=err, stream=s)
+        rpl._lib.check(lib.rpl_returns_nstep(P_(r_tr), P_(d_tr), Tn, n, c["n_step"], c["gamma"],
+                                             P_(q_pool[i % P][c["burn_in"]:c["burn_in"] + Tn]),
+                                             P_(q_pool[i % P][c["burn_in"] + Tn]), 1, c["eps"], P_(y), P_(dn), s),
+                       "nstep")
+
+    ms = _graph_time(dev, step, P=8, reps=50)
+    rpl.check_err(err)
+    ub = seq_bytes_per_sample(c) - c["L"] * k * FRAME + (c["L"] + k - 1) * FRAME
+    return {"out": "unique", "us_per_step": ms * 1e3, "sequences_per_s": n / (ms / 1e3),
+            "alg_bytes_per_sequence": ub, "timing": "CUDA graph of 8 steps, replayed"}
 
 
 def tree_latency(dev, rpl):

@@ -855,6 +855,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   // rows g = s*L + tau of the active samples, split evenly over the grid
   const int total = (int)(active_n(D, n) * L);
   const int64_t coff = col_off(D);  // output column of entry 0 (Mode C)
+  const bool unique = D.out_mode == RPL_OUT_UNIQUE;
   const int rpc = D.n_active ? (total + (int)gridDim.x - 1) / (int)gridDim.x : (int)rows_per_cta;
   const int g0 = (int)blockIdx.x * rpc;
   const int g1 = min(total, g0 + rpc);
@@ -1043,7 +1044,28 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       // ---------------- consumers: one k-stack per row, LSU stores ----------------
       for (int c = warp - 2; c < nrows; c += NC) {
         const int p0 = row_first[c];
-        if (p0 >= 0) {
+        if (p0 >= 0 && unique) {
+          // RPL_OUT_UNIQUE: raw rows, each written once — row tau stores its newest frame
+          // (unique row tau+k-1); the sample's first row also stores unique rows 0..k-2
+          const int sm = s_first + row_piece[c];
+          const int tau = row_tau[c];
+          const int s0 = p0 % NS;
+          const uint32_t par0 = (uint32_t)((p0 / NS) & 1);
+          for (int j = tau == 0 ? 0 : k - 1; j < k; ++j) {
+            int sl = s0 + j;
+            uint32_t par = par0;
+            if (sl >= NS) {
+              sl -= NS;
+              par ^= 1u;
+            }
+            if (!(D.diag & 2)) mbar_wait(&full[sl], par);
+            if (D.diag & 1) continue;
+            int4* d = reinterpret_cast<int4*>(D.o_obs + ((int64_t)(tau + j) * n + coff + sm) * ob);
+            const int4* sp = reinterpret_cast<const int4*>(smem + sl * ob);
+#pragma unroll 4
+            for (int v = lane; v < nv; v += 32) __stcs(d + v, sp[v]);
+          }
+        } else if (p0 >= 0) {
           const int so = start_off[c];
           const int sm = s_first + row_piece[c];
           const int tau = row_tau[c];
@@ -1510,8 +1532,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
         return launch_seq_ldg_bulk<8>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn, grid, st);
       }
     }
-    if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs &&
-        (seq_variant == 0 || seq_variant == 4 || seq_variant == 5)) {
+    if (tma_ok && desc->o_obs && (seq_variant == 0 || seq_variant == 4 || seq_variant == 5)) {
       // default: TMA-load / LSU-store pipeline.  The producer runs up to NS frames past the
       // release point of the done-frontier row f, whose own window starts exactly there, so
       // NS >= k guarantees progress; more slots let the other consumers run ahead.

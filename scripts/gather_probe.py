@@ -23,7 +23,7 @@ for cap, B in [(4000, 256), (1024000, 1)]:
     for variant in (0, 1, 4, 5):
         rpl._lib.lib.rpl_debug_set_gather_variant(variant)
         for mode in ("stacked", "unique"):
-            if mode == "unique" and variant != 1:
+            if mode == "unique" and variant not in (0, 1):
                 continue
             plan = rpl.GatherPlan(ring, 64, kind="sequence", k=4, seq_len=125, period=40,
                                   out_mode=0 if mode == "stacked" else 1)
