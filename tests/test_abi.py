@@ -49,14 +49,16 @@ def test_struct_layouts_match_c(tmp_path):
     prog = tmp_path / "sz.c"
     prog.write_text(
         '#include <stdio.h>\n#include <stddef.h>\n#include "rpl.h"\n'
-        "int main(){printf(\"%zu %zu %zu %zu %zu %zu\\n\", sizeof(rpl_tree_layout), offsetof(rpl_tree_layout, q_cap),"
-        " offsetof(rpl_tree_layout, n_words), sizeof(rpl_gather_desc), offsetof(rpl_gather_desc, gamma),"
-        " offsetof(rpl_gather_desc, o_rnn));return 0;}\n")
+        "int main(){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(rpl_tree_layout),"
+        " offsetof(rpl_tree_layout, q_cap), offsetof(rpl_tree_layout, n_words), sizeof(rpl_gather_desc),"
+        " offsetof(rpl_gather_desc, gamma), offsetof(rpl_gather_desc, o_rnn), offsetof(rpl_gather_desc, n_active),"
+        " offsetof(rpl_gather_desc, col_offset));return 0;}\n")
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(prog), "-o", str(exe)])
     vals = [int(x) for x in subprocess.check_output([str(exe)]).split()]
     assert vals == [ctypes.sizeof(TreeLayout), TreeLayout.q_cap.offset, TreeLayout.n_words.offset,
-                    ctypes.sizeof(GatherDesc), GatherDesc.gamma.offset, GatherDesc.o_rnn.offset]
+                    ctypes.sizeof(GatherDesc), GatherDesc.gamma.offset, GatherDesc.o_rnn.offset,
+                    GatherDesc.n_active.offset, GatherDesc.col_offset.offset]
 
 
 def test_host_validation_without_gpu(lib):
@@ -69,6 +71,16 @@ def test_host_validation_without_gpu(lib):
     assert lay.depth == 4 and lay.q_cap == ((1 << 63) - 1) // (1 << 20)
     assert [lay.level_len[i] for i in range(5)] == [1, 32, 1024, 32768, 1 << 20]
     assert L.rpl_returns_nstep(None, None, 4, 4, 1, 0.9, None, None, 0, 0.0, None, None, None) == -1
+    # later entries: null / out-of-range arguments rejected before any launch
+    assert L.rpl_returns_nstep_dq(None, None, 4, 4, 1, 0.9, None, None, 3, 0, 0.0, None, None, None, None) == -1
+    assert L.rpl_c51_project(None, None, None, None, 4, 1, 51, -10.0, 10.0, 0.9, None, None, None) == -1
+    assert L.rpl_sample_uniform(0, 1, 0, None, 0, 1, 1, 1, None, None) == -1
+    assert L.rpl_sumtree_update_seq(ctypes.byref(lay), None, None, None, 0, 4, 0.9, 0.9, 1e-3, None, None) == -1
+    assert L.rpl_sumtree_update_seq(ctypes.byref(lay), None, None, None, 80, 4, 1.5, 0.9, 1e-3, None, None) == -1
+    assert L.rpl_replay_validity(ctypes.byref(lay), None, 0, 4096, 256, 4, 3, 1, 1, 0, 0, 1, 1, None) == -1
+    assert L.rpl_replay_validity(ctypes.byref(lay), 1, 0, 4096, 255, 4, 3, 1, 1, 0, 0, 1, 1, None) == -1  # N mismatch
+    assert L.rpl_ring_append(None, None, None, None, None, None, 1, None) == -1
+    assert L.rpl_debug_set_gather_variant(99) == -1 and L.rpl_debug_set_gather_diag(99) == -1
 
 
 def test_product_never_imports_oracle():
