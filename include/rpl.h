@@ -201,6 +201,13 @@ int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t 
 int rpl_sumtree_find(const rpl_tree_layout* L, const int64_t* tree, const int64_t* prefix,
                      int64_t n, int64_t* out_idx, int32_t* dev_err, void* stream);
 
+/* Buffer-wide IS normaliser (§8f NEXT-4, R29): *out_min (device int64) = min over the
+ * leaves with q > 0 (INT64_MAX when none).  Passing it as rpl_gather's qmin gives
+ * w_i = (N P_i)^-beta / max_j over the WHOLE buffer (N P_j)^-beta = (q_min / q_i)^beta,
+ * the PER-paper normalisation, instead of the batch max (R10).  Two launches, one
+ * grid-wide read of the leaf level. */
+int rpl_sumtree_min(const rpl_tree_layout* L, const int64_t* tree, int64_t* out_min, void* stream);
+
 /* *out_total = root (int64, device). */
 int rpl_sumtree_total(const rpl_tree_layout* L, const int64_t* tree, int64_t* out_total, void* stream);
 

@@ -121,3 +121,11 @@ def sharded_sample(shards, n: int, draws):
     cat = SumTreeOracle(sum(s.n_leaves for s in shards), shards[0].frac_bits)
     cat.q = list(itertools.chain.from_iterable(s.q for s in shards))
     return cat.sample(n, draws)
+
+
+def buffer_min(q_leaves) -> int:
+    """Buffer-wide IS normaliser (§8f NEXT-4, R29): min over the leaves with q > 0
+    (2**63 - 1 when there are none); w_i = (q_min / q_i)^beta then normalises by the
+    largest weight any stored transition could receive (PER), not the batch's."""
+    pos = [int(x) for x in q_leaves if int(x) > 0]
+    return min(pos) if pos else (1 << 63) - 1

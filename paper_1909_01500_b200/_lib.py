@@ -81,6 +81,7 @@ _SIGS = {
                                     P, P], C.c_int),
     "rpl_sumtree_find": ([C.POINTER(TreeLayout), P, P, I64, P, P, P], C.c_int),
     "rpl_sumtree_total": ([C.POINTER(TreeLayout), P, P, P], C.c_int),
+    "rpl_sumtree_min": ([C.POINTER(TreeLayout), P, P, P], C.c_int),
     "rpl_sumtree_rebuild": ([C.POINTER(TreeLayout), P, P], C.c_int),
     "rpl_is_weights": ([P, P, I64, D, P, P], C.c_int),
     "rpl_sample_uniform": ([I64, U64, U64, P, I64, I64, I64, I64, P, P], C.c_int),

@@ -414,6 +414,22 @@ __global__ void k_tree_find(TreeDev L, const int64_t* __restrict__ tree, const i
   }
 }
 
+// Buffer-wide IS normaliser (§8f NEXT-4, reading R29): min over the leaves with q > 0.
+__global__ void k_min_init(int64_t* __restrict__ out) {
+  pdl_wait();
+  *out = INT64_MAX;
+}
+__global__ void k_leaf_min(const int64_t* __restrict__ leaves, int64_t n, int64_t* __restrict__ out) {
+  pdl_wait();
+  int64_t m = INT64_MAX;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = __ldcg(leaves + i);
+    if (v > 0 && v < m) m = v;
+  }
+  m = warp_min64(m);
+  if ((threadIdx.x & 31) == 0 && m != INT64_MAX) atomicMin(reinterpret_cast<long long*>(out), (long long)m);
+}
+
 __global__ void k_tree_total(const int64_t* __restrict__ tree, int64_t* __restrict__ out) {
   pdl_wait();
   *out = tree[0];
@@ -654,4 +670,16 @@ extern "C" int rpl_sumtree_update_seq(const rpl_tree_layout* L, int64_t* tree, c
   if (n > 0 && (!td_steps || T_p < 1)) return RPL_EINVAL;
   if (!(alpha >= 0.0) || !(eps_p >= 0.0) || !(eta >= 0.0 && eta <= 1.0)) return RPL_EINVAL;
   return launch_update(L, tree, idx, td_steps, nullptr, MODE_SEQ, n, alpha, eps_p, dev_err, stream, 0, T_p, eta);
+}
+
+extern "C" int rpl_sumtree_min(const rpl_tree_layout* L, const int64_t* tree, int64_t* out_min, void* stream) {
+  if (!layout_ok(L) || !tree || !out_min) return RPL_EINVAL;
+  int r = launch_pdl(k_min_init, dim3(1), dim3(1), 0, as_stream(stream), out_min);
+  if (r != RPL_OK) return r;
+  const int threads = 256;
+  int64_t blocks = (L->n_leaves + threads - 1) / threads;
+  const int64_t cap = (int64_t)sm_count() * 4;
+  if (blocks > cap) blocks = cap;
+  return launch_pdl(k_leaf_min, dim3((unsigned)blocks), dim3(threads), 0, as_stream(stream),
+                    (const int64_t*)(tree + L->level_off[L->depth]), L->n_leaves, out_min);
 }

@@ -325,6 +325,12 @@ class SumTree:
         check(lib.rpl_sumtree_total(self._lp, _ptr(self.storage), _ptr(out), self._s()), "rpl_sumtree_total")
         return out
 
+    def min_q(self, out=None):
+        """rpl_sumtree_min: buffer-wide min q over non-zero leaves (NEXT-4 IS normaliser)."""
+        out = torch.empty(1, dtype=torch.int64, device=self.device) if out is None else out
+        check(lib.rpl_sumtree_min(self._lp, _ptr(self.storage), _ptr(out), self._s()), "rpl_sumtree_min")
+        return out
+
     def rebuild(self):
         check(lib.rpl_sumtree_rebuild(self._lp, _ptr(self.storage), self._s()), "rpl_sumtree_rebuild")
 

@@ -373,3 +373,23 @@ def test_update_seq_vs_oracle(rpl, T_p, n, eta):
     t2 = rpl.SumTree(N, 32)
     t2.update(T_(idx), T_(np.array(td, np.float32)), 0.9)
     assert np.array_equal(H(t.storage), H(t2.storage))
+
+
+def test_buffer_min_and_buffer_normalised_weights(rpl):
+    # NEXT-4: rpl_sumtree_min over non-zero leaves; the gather normalises IS weights by it
+    import torch
+    g = rng(44)
+    N = 1 << 20
+    t = rpl.SumTree(N, 32)
+    idx = np.unique(g.integers(0, N, 50000)).astype(np.int64)
+    td = td_abs(g, idx.size)
+    t.update(T_(idx), T_(td), 0.6)
+    orc = OS.SumTreeOracle(N)
+    orc.update([int(x) for x in idx], [float(x) for x in td], 0.6)
+    m = t.min_q()
+    assert int(H(m)[0]) == OS.buffer_min(orc.q)
+    w = rpl.is_weights(t.leaves[torch.from_numpy(idx[:100]).cuda()].contiguous(), m, 0.4)
+    ref = [(OS.buffer_min(orc.q) / orc.q[int(i)]) ** 0.4 for i in idx[:100]]
+    check_rel(H(w), np.array(ref), what="buffer-normalised w")
+    e = rpl.SumTree(64, 32)
+    assert int(H(e.min_q())[0]) == (1 << 63) - 1

@@ -186,3 +186,21 @@ def test_sharded_equals_concatenated():
         lo, hi = (k * Q) // 32, ((k + 1) * Q) // 32
         prefix = lo + ((draws[k] * (hi - lo)) >> 64)
         assert linear_find(allq, prefix) == i
+
+
+def test_buffer_min_is_the_per_normaliser():
+    # NEXT-4 (R29): normalising by the buffer's largest weight, w_i = (N P_i)^-b / max_j (N P_j)^-b
+    # over every stored leaf with P_j > 0, equals (q_min / q_i)^b with q_min = buffer_min
+    import random
+    rnd = random.Random(5)
+    q = [rnd.randint(1, 1 << 40) if rnd.random() < 0.8 else 0 for _ in range(200)]
+    Q = sum(q)
+    N = len(q)
+    beta = 0.4
+    wmax = max((N * qi / Q) ** -beta for qi in q if qi > 0)
+    qm = S.buffer_min(q)
+    assert qm == min(x for x in q if x > 0)
+    for qi in q:
+        if qi > 0:
+            assert abs((N * qi / Q) ** -beta / wmax - (qm / qi) ** beta) <= 1e-12
+    assert S.buffer_min([0, 0]) == (1 << 63) - 1
