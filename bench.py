@@ -284,7 +284,7 @@ def run_rpl(args):
         # (a5-a7) new priorities for the previous batch (entries < 0 — not owned — are skipped, R22)
         # (NEXT-1 fused) sequence priority = eta max + (1 - eta) mean of the 80 per-step |delta| (R26)
         rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]),
-                                                  c["train"], n_glob, c["eta"], c["alpha"], c["eps_p"], None, s),
+                                                  c["train"], n_glob, c["eta"], c["alpha"], c["eps_p"], 0, None, s),
                        "update_seq")
         if world == 1:
             # (a8) draws only; the batch-min normaliser and IS weights (a9) are fused into the gather
@@ -541,7 +541,7 @@ def pipelined_step(dev, rpl, tree, plan, idx_buf, td_pool, q_pool, r_tr, d_tr, y
                     sA.wait_event(ev_g[(i - 2) % P])
                 a = rpl.ops._stream(dev)
                 rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]),
-                                                          c["train"], n, c["eta"], c["alpha"], c["eps_p"], None, a),
+                                                          c["train"], n, c["eta"], c["alpha"], c["eps_p"], 0, None, a),
                                "update_seq")
                 rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, seed, c["beta"],
                                                              P_(cur), P_(qb[i % 2]), None, None, P_(err), a),
@@ -620,7 +620,7 @@ def bench_r2d2_1mseq(dev, rpl, c):
     def step(i):
         s = rpl.ops._stream(dev)
         rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(idx[(i + 1) % 2]), P_(td[i % 8]),
-                                                  c["train"], n, c["eta"], c["alpha"], c["eps_p"], None, s), "upd")
+                                                  c["train"], n, c["eta"], c["alpha"], c["eps_p"], 0, None, s), "upd")
         rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, 0xBEEF, c["beta"], P_(idx[i % 2]),
                                                      P_(q), None, None, P_(err), s), "sample")
         plan.run(idx[i % 2], q=q, qmin=None, beta=c["beta"], err=err, stream=s)
@@ -660,7 +660,7 @@ def unique_output_step(dev, rpl, tree, ring, idx_buf, td_pool, q_pool, err, c, n
         s = rpl.ops._stream(dev)
         cur, prev = idx_buf[i % 2], idx_buf[(i + 1) % 2]
         rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]),
-                                                  c["train"], n, c["eta"], c["alpha"], c["eps_p"], None, s), "upd")
+                                                  c["train"], n, c["eta"], c["alpha"], c["eps_p"], 0, None, s), "upd")
         rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, seed, c["beta"], P_(cur), P_(q),
                                                      None, None, P_(err), s), "sample")
         plan.run(cur, q=q, qmin=None, beta=c["beta"], err=err, stream=s)

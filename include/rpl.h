@@ -138,10 +138,18 @@ int rpl_sumtree_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* i
  *   td_k = RN32(eta * max_t |d_tk| + (1 - eta) * (sum_t |d_tk|) / T_p)
  * (fp64, sum in increasing t, no fused multiply-add), then exactly rpl_sumtree_update's
  * transform and write: identical to rpl_sumtree_update(idx, td, n, alpha, eps_p).
- * eta in [0, 1]; T_p >= 1. */
+ * eta in [0, 1]; T_p >= 1.  flags: 0 or RPL_UPD_LIVE_ONLY. */
 int rpl_sumtree_update_seq(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx,
                            const float* td_steps, int64_t T_p, int64_t n, double eta, double alpha,
-                           double eps_p, int32_t* dev_err, void* stream);
+                           double eps_p, int32_t flags, int32_t* dev_err, void* stream);
+
+/* rpl_sumtree_update with flags.  RPL_UPD_LIVE_ONLY: entries whose leaf is currently 0 (made
+ * invalid by an append since it was sampled, or never written) are skipped silently and do
+ * not count toward max-seen — a learner's late priorities cannot revive a stale leaf
+ * (asynchronous replay; reading R30). */
+enum { RPL_UPD_LIVE_ONLY = 1 };
+int rpl_sumtree_update_ex(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, const float* td_abs,
+                          int64_t n, double alpha, double eps_p, int32_t flags, int32_t* dev_err, void* stream);
 
 /* Direct leaf write (append / validity maintenance, §8a a12): leaf idx[k] := q[k]
  * (last write wins; max-seen updated), or := current max-seen when q == NULL.

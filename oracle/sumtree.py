@@ -51,13 +51,17 @@ class SumTreeOracle:
         return i
 
     # ---- S:621-629, S:660 -----------------------------------------------
-    def update(self, idx, td_abs, alpha: float, eps_p: float = 1e-3):
+    def update(self, idx, td_abs, alpha: float, eps_p: float = 1e-3, live_only: bool = False):
+        """live_only (reading R30): a leaf whose q is 0 when its entry is applied (invalid
+        since it was sampled, or never written) is skipped."""
         for i, d in zip(idx, td_abs):
             i = int(i)
             if i < 0:                                 # padding entry (rpl.h): skipped silently
                 continue
             if i >= self.n_leaves:
                 self.err_idx = True
+                continue
+            if live_only and self.q[i] == 0:
                 continue
             M, E = _pr.priority_value(float(d), alpha, eps_p)
             qv, sat = _pr.quantise(M, E, self.frac_bits, self.cap)

@@ -67,7 +67,7 @@ __device__ __forceinline__ uint32_t hash_slot(int64_t leaf) {
 __global__ void __launch_bounds__(UPD_THREADS)
 k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__ idx,
               const float* __restrict__ td, const int64_t* __restrict__ qin, int mode, int64_t n,
-              double alpha, double eps_p, int32_t* err, int force_slow, int64_t T_p, double eta) {
+              double alpha, double eps_p, int32_t* err, int force_slow, int64_t T_p, double eta, int live_only) {
   __shared__ unsigned long long hkey[HASH_SLOTS];
   __shared__ int hval[HASH_SLOTS];
   __shared__ int64_t sred[UPD_THREADS / 32];
@@ -127,17 +127,13 @@ k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__
           bool sat = false;
           q = quantise_q(v, L.frac_bits, L.q_cap, &sat);
           if (sat) errbits |= RPL_DERR_SATURATED;
-          local_max = q > local_max ? q : local_max;
         } else if (mode == MODE_Q) {
           q = qin[i];
           if (q < 0) {
             ok = false;
-          } else {
-            if (q > L.q_cap) {
-              q = L.q_cap;
-              errbits |= RPL_DERR_SATURATED;
-            }
-            local_max = q > local_max ? q : local_max;
+          } else if (q > L.q_cap) {
+            q = L.q_cap;
+            errbits |= RPL_DERR_SATURATED;
           }
         } else {
           q = maxseen_now;
@@ -147,6 +143,10 @@ k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__
         errbits |= RPL_DERR_IDX;
         leaf = -1;
       }
+      // RPL_UPD_LIVE_ONLY: a leaf that is currently 0 (invalid since it was sampled, or
+      // never written) is left untouched, so a late priority cannot revive it
+      if (leaf >= 0 && live_only && (single ? pre_old : __ldcg(leaves + leaf)) == 0) leaf = -1;
+      if (leaf >= 0 && mode != MODE_MAXSEEN) local_max = q > local_max ? q : local_max;
     }
     uint32_t slot = 0;
     if (leaf >= 0) {
@@ -501,12 +501,12 @@ bool layout_ok(const rpl_tree_layout* L) {
 
 int launch_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, const float* td,
                   const int64_t* q, int mode, int64_t n, double alpha, double eps_p, int32_t* err,
-                  void* stream, int force_slow, int64_t T_p = 0, double eta = 0.0) {
+                  void* stream, int force_slow, int64_t T_p = 0, double eta = 0.0, int live_only = 0) {
   if (!layout_ok(L) || !tree || n < 0) return RPL_EINVAL;
   if (n == 0) return RPL_OK;
   if (!idx) return RPL_EINVAL;
   return launch_pdl(k_tree_update, dim3(1), dim3(UPD_THREADS), 0, as_stream(stream), tree_dev(L), tree, idx, td, q,
-                    mode, n, alpha, eps_p, err, force_slow, T_p, eta);
+                    mode, n, alpha, eps_p, err, force_slow, T_p, eta, live_only);
 }
 
 }  // namespace
@@ -666,10 +666,21 @@ extern "C" int rpl_sample_uniform(int64_t n, uint64_t seed, uint64_t offset, uin
 
 extern "C" int rpl_sumtree_update_seq(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx,
                                       const float* td_steps, int64_t T_p, int64_t n, double eta, double alpha,
-                                      double eps_p, int32_t* dev_err, void* stream) {
+                                      double eps_p, int32_t flags, int32_t* dev_err, void* stream) {
   if (n > 0 && (!td_steps || T_p < 1)) return RPL_EINVAL;
-  if (!(alpha >= 0.0) || !(eps_p >= 0.0) || !(eta >= 0.0 && eta <= 1.0)) return RPL_EINVAL;
-  return launch_update(L, tree, idx, td_steps, nullptr, MODE_SEQ, n, alpha, eps_p, dev_err, stream, 0, T_p, eta);
+  if (!(alpha >= 0.0) || !(eps_p >= 0.0) || !(eta >= 0.0 && eta <= 1.0) || (flags & ~RPL_UPD_LIVE_ONLY))
+    return RPL_EINVAL;
+  return launch_update(L, tree, idx, td_steps, nullptr, MODE_SEQ, n, alpha, eps_p, dev_err, stream, 0, T_p, eta,
+                       (flags & RPL_UPD_LIVE_ONLY) ? 1 : 0);
+}
+
+extern "C" int rpl_sumtree_update_ex(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, const float* td_abs,
+                                     int64_t n, double alpha, double eps_p, int32_t flags, int32_t* dev_err,
+                                     void* stream) {
+  if (n > 0 && !td_abs) return RPL_EINVAL;
+  if (!(alpha >= 0.0) || !(eps_p >= 0.0) || (flags & ~RPL_UPD_LIVE_ONLY)) return RPL_EINVAL;
+  return launch_update(L, tree, idx, td_abs, nullptr, MODE_TD, n, alpha, eps_p, dev_err, stream, 0, 0, 0.0,
+                       (flags & RPL_UPD_LIVE_ONLY) ? 1 : 0);
 }
 
 extern "C" int rpl_sumtree_min(const rpl_tree_layout* L, const int64_t* tree, int64_t* out_min, void* stream) {

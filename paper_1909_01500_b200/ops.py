@@ -220,14 +220,18 @@ class SumTree:
     def init(self):
         check(lib.rpl_sumtree_init(self._lp, _ptr(self.storage), self._s()), "rpl_sumtree_init")
 
-    def update(self, idx, td_abs, alpha, eps_p=1e-3, err=None):
+    def update(self, idx, td_abs, alpha, eps_p=1e-3, err=None, live_only=False):
         _req(idx, torch.int64, "idx")
         _req(td_abs, torch.float32, "td_abs", idx.shape)
         e = self.err if err is None else err
+        if live_only:
+            check(lib.rpl_sumtree_update_ex(self._lp, _ptr(self.storage), _ptr(idx), _ptr(td_abs), idx.numel(),
+                                            float(alpha), float(eps_p), 1, _ptr(e), self._s()), "rpl_sumtree_update_ex")
+            return
         check(lib.rpl_sumtree_update(self._lp, _ptr(self.storage), _ptr(idx), _ptr(td_abs), idx.numel(),
                                      float(alpha), float(eps_p), _ptr(e), self._s()), "rpl_sumtree_update")
 
-    def update_seq(self, idx, td_steps, alpha, eta=0.9, eps_p=1e-3, err=None):
+    def update_seq(self, idx, td_steps, alpha, eta=0.9, eps_p=1e-3, err=None, live_only=False):
         """rpl_sumtree_update_seq: R2D2 eta-mix of per-step |delta| [T_p, n] per sequence, then update."""
         _req(idx, torch.int64, "idx")
         _req(td_steps, torch.float32, "td_steps")
@@ -236,7 +240,7 @@ class SumTree:
         e = self.err if err is None else err
         check(lib.rpl_sumtree_update_seq(self._lp, _ptr(self.storage), _ptr(idx), _ptr(td_steps),
                                          td_steps.shape[0], idx.numel(), float(eta), float(alpha), float(eps_p),
-                                         _ptr(e), self._s()), "rpl_sumtree_update_seq")
+                                         1 if live_only else 0, _ptr(e), self._s()), "rpl_sumtree_update_seq")
 
     def validity(self, kind, cap_T, B, k, cursor_old, size_old, cursor_new, size_new, n_step=1, seq_len=1,
                  period=1):

@@ -75,11 +75,12 @@ def test_host_validation_without_gpu(lib):
     assert L.rpl_returns_nstep_dq(None, None, 4, 4, 1, 0.9, None, None, 3, 0, 0.0, None, None, None, None) == -1
     assert L.rpl_c51_project(None, None, None, None, 4, 1, 51, -10.0, 10.0, 0.9, None, None, None) == -1
     assert L.rpl_sample_uniform(0, 1, 0, None, 0, 1, 1, 1, None, None) == -1
-    assert L.rpl_sumtree_update_seq(ctypes.byref(lay), None, None, None, 0, 4, 0.9, 0.9, 1e-3, None, None) == -1
-    assert L.rpl_sumtree_update_seq(ctypes.byref(lay), None, None, None, 80, 4, 1.5, 0.9, 1e-3, None, None) == -1
+    assert L.rpl_sumtree_update_seq(ctypes.byref(lay), None, None, None, 0, 4, 0.9, 0.9, 1e-3, 0, None, None) == -1
+    assert L.rpl_sumtree_update_seq(ctypes.byref(lay), None, None, None, 80, 4, 1.5, 0.9, 1e-3, 0, None, None) == -1
     assert L.rpl_replay_validity(ctypes.byref(lay), None, 0, 4096, 256, 4, 3, 1, 1, 0, 0, 1, 1, None) == -1
     assert L.rpl_replay_validity(ctypes.byref(lay), 1, 0, 4096, 255, 4, 3, 1, 1, 0, 0, 1, 1, None) == -1  # N mismatch
     assert L.rpl_ring_append(None, None, None, None, None, None, 1, None) == -1
+    assert L.rpl_sumtree_update_ex(ctypes.byref(lay), None, None, None, 4, 0.9, 1e-3, 2, None, None) == -1
     assert L.rpl_debug_set_gather_variant(99) == -1 and L.rpl_debug_set_gather_diag(99) == -1
 
 

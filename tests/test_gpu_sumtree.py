@@ -393,3 +393,27 @@ def test_buffer_min_and_buffer_normalised_weights(rpl):
     check_rel(H(w), np.array(ref), what="buffer-normalised w")
     e = rpl.SumTree(64, 32)
     assert int(H(e.min_q())[0]) == (1 << 63) - 1
+
+
+@pytest.mark.parametrize("seq", [False, True])
+def test_update_live_only(rpl, seq):
+    # RPL_UPD_LIVE_ONLY (R30): entries on zero leaves are skipped (no revival, no max-seen)
+    g = rng(71)
+    N = 5000
+    t = rpl.SumTree(N, 32)
+    orc = OS.SumTreeOracle(N)
+    live = np.arange(0, N, 3, dtype=np.int64)
+    td0 = td_abs(g, live.size)
+    t.update(T_(live), T_(td0), 0.9)
+    orc.update([int(x) for x in live], [float(x) for x in td0], 0.9)
+    idx = g.integers(0, N, 700).astype(np.int64)
+    if seq:
+        steps = np.abs(g.lognormal(0, 3, (12, idx.size))).astype(np.float32)
+        t.update_seq(T_(idx), T_(steps), 0.9, eta=0.9, live_only=True)
+        td = [OPR.sequence_td(steps[:, k], 0.9) for k in range(idx.size)]
+    else:
+        tdv = (td_abs(g, idx.size) * 50).astype(np.float32)
+        t.update(T_(idx), T_(tdv), 0.9, live_only=True)
+        td = [float(x) for x in tdv]
+    orc.update([int(x) for x in idx], td, 0.9, live_only=True)
+    check_tree_consistent(t, orc)
