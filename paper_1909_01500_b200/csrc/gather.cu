@@ -60,6 +60,18 @@ __device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src,
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
+// Intra-CTA flags with release / acquire semantics (the producer / consumer hand-offs of
+// the persistent gathers): everything a thread did before flag_release is visible to a
+// thread whose flag_acquire observes the value.
+__device__ __forceinline__ void flag_release(volatile int* f, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32((const void*)f)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int flag_acquire(volatile int* f) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32((const void*)f)) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   uint32_t done = 0;
   while (!done) {
@@ -925,7 +937,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         for (int w = 0; w < R + k - 1; ++w, ++i) {
           if (i >= NS) {
             while (released <= i - NS) {
-              if (frontier < nrows && row_done[frontier]) {
+              if (frontier < nrows && flag_acquire(&row_done[frontier])) {
                 released = rel[frontier];
                 ++frontier;
               } else {
@@ -933,6 +945,9 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
               }
             }
             fence_proxy_async();
+            // the slot's previous phase completed before its readers finished: observe it, so
+            // every arrive on a barrier follows the completion of its previous phase
+            if (!(D.diag & 2)) mbar_wait(&full[slot], (uint32_t)(((i / NS) - 1) & 1));
           }
           if (!(D.diag & 2)) {
             mbar_expect_tx(&full[slot], (uint32_t)ob);
@@ -1104,7 +1119,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         __syncwarp();
         if (lane == 0) {
           fence_proxy_async();
-          row_done[c] = 1;
+          flag_release(&row_done[c], 1);
         }
       }
     }
@@ -1273,7 +1288,7 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
           for (int j = so; j < k; ++j) {
             int sl = s0 + j;
             if (sl >= NS) sl -= NS;
-            while (frame_ready[sl] != p0 + j + 1) __nanosleep(20);
+            while (flag_acquire(&frame_ready[sl]) != p0 + j + 1) __nanosleep(20);
           }
           fence_proxy_async();
           uint8_t* dst = D.o_obs + ((int64_t)tau * n + coff + sm) * k * ob;
@@ -1295,7 +1310,7 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         }
         bulk_commit();
         bulk_wait_read_G<LB_G>();
-        if (c >= LB_G) s_released = rel[c - LB_G];
+        if (c >= LB_G) flag_release(&s_released, rel[c - LB_G]);
       }
       bulk_wait_all();
     }
@@ -1361,7 +1376,7 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       while (row < 0) row += cap;
       while (row >= cap) row -= cap;
       const int4* src = reinterpret_cast<const int4*>(D.obs + (int64_t)p_b[pc] * ob + (int64_t)row * rstride);
-      while (f >= s_released + NS) __nanosleep(20);
+      while (f >= flag_acquire(&s_released) + NS) __nanosleep(20);
       const int sl = f % NS;
       int4* dst = reinterpret_cast<int4*>(smem + sl * ob);
       if (!(D.diag & 2)) {
@@ -1378,7 +1393,7 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       }
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) frame_ready[sl] = f + 1;
+      if (lane == 0) flag_release(&frame_ready[sl], f + 1);
     }
   }
   pdl_trigger();
