@@ -102,9 +102,18 @@ __device__ __forceinline__ int64_t warp_batch_qmin(const int64_t* __restrict__ q
                                                    const int64_t* __restrict__ q, int64_t n) {
   if (qmin) return *qmin;
   int64_t m = INT64_MAX;
-  for (int64_t j = threadIdx.x & 31; j < n; j += 32) {
-    const int64_t i = idx[j], v = q[j];
-    if (i >= 0 && v < m) m = v;
+  // blocks of 8 loads per lane in flight before any is consumed (one latency per 256 entries)
+  for (int64_t j0 = threadIdx.x & 31; j0 < n; j0 += 32 * 8) {
+    int64_t iv[8], qv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t j = j0 + 32 * u;
+      iv[u] = j < n ? __ldg(idx + j) : -1;
+      qv[u] = j < n ? __ldg(q + j) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (iv[u] >= 0 && qv[u] < m) m = qv[u];
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) {
@@ -258,17 +267,25 @@ k_gather_transition(GDesc D, const int64_t* __restrict__ idx, int64_t n, const i
       uint8_t* dst = D.o_act + sc * D.act_bytes;
       for (int64_t i = l; i < D.act_bytes; i += 32) dst[i] = src[i];
     }
+    // n-step rows: lane i < n loads row r+i (all loads in flight at once), lane 0 runs the
+    // Horner recurrence over the shuffled values (R24)
+    float ri_l = 0.0f;
+    uint8_t di_l = 0;
+    if ((D.o_ret || D.o_done_n) && l < ns) {
+      const int64_t row = wrap(r + l, D.cap_T);
+      di_l = __ldg(D.done + row * D.B + b);
+      ri_l = __ldg(D.rew + row * D.B + b);
+    }
+    double acc = 0.0;
+    uint8_t dn = 0;
+    for (int i = ns - 1; i >= 0; --i) {  // ns <= 31 (host check)
+      const float ri = __shfl_sync(0xffffffffu, ri_l, i);
+      const uint8_t di = (uint8_t)__shfl_sync(0xffffffffu, (int)di_l, i);
+      acc = di ? (double)ri : fma(D.gamma, acc, (double)ri);
+      dn |= di;
+    }
     if (l == 0) {
       if (D.o_ret || D.o_done_n) {
-        double acc = 0.0;
-        uint8_t dn = 0;
-        for (int i = ns - 1; i >= 0; --i) {
-          const int64_t row = wrap(r + i, D.cap_T);
-          const uint8_t di = __ldg(D.done + row * D.B + b);
-          const double ri = (double)__ldg(D.rew + row * D.B + b);
-          acc = di ? ri : fma(D.gamma, acc, ri);
-          dn |= di;
-        }
         if (D.o_ret) D.o_ret[sc] = (float)acc;
         if (D.o_done_n) D.o_done_n[sc] = dn ? 1 : 0;
       }
