@@ -241,14 +241,22 @@ def run_rpl(args):
     mode_c = world > 1 and args.mode == "C"
     learner = (not mode_c) or rank == 0  # ranks that consume a batch (and compute its targets)
     central = None
+    stacked = None
     if mode_c:
-        # Mode C: rank 0's batch buffers, mapped into every rank (CUDA IPC over NVLink)
+        # Mode C: rank 0's batch buffers, mapped into every rank (CUDA IPC over NVLink).  The owners
+        # ship UNIQUE frame rows + episode-start offsets (116 MB per 64 sequences instead of 284 MB
+        # of stacks); the learner rebuilds the k-stacks locally (rpl_stack_frames).
+        from paper_1909_01500_b200 import _lib as _L
         from paper_1909_01500_b200.shard import CentralBatch
-        root_plan = (rpl.GatherPlan(ring, n_glob, kind="sequence", k=k, seq_len=L, period=period, with_weights=True)
-                     if rank == 0 else None)
+        want = ["obs", "act", "prev_act", "rew", "prev_rew", "done", "rnn", "start"]
+        root_plan = (rpl.GatherPlan(ring, n_glob, kind="sequence", k=k, seq_len=L, period=period, with_weights=True,
+                                    out_mode=_L.OUT_UNIQUE, want=want) if rank == 0 else None)
         central = CentralBatch(root_plan.outputs if rank == 0 else None)
         plan = root_plan if rank == 0 else rpl.GatherPlan(ring, n_glob, kind="sequence", k=k, seq_len=L,
-                                                          period=period, with_weights=True, outputs=central.outputs)
+                                                          period=period, with_weights=True, out_mode=_L.OUT_UNIQUE,
+                                                          want=want, outputs=central.outputs)
+        if rank == 0:
+            stacked = torch.empty((L, n_glob, k) + tuple(ring.item_shape), dtype=torch.uint8, device=dev)
     else:
         plan = rpl.GatherPlan(ring, n_glob, kind="sequence", k=k, seq_len=L, period=period, with_weights=True)
     out = plan.outputs
@@ -305,6 +313,9 @@ def run_rpl(args):
             gather_events[1].record()
         if mode_c:
             central.arrived()                                                    # K8: batch complete on rank 0
+            if rank == 0:  # learner: k-stacks from the shipped unique rows (local HBM)
+                rpl._lib.check(lib.rpl_stack_frames(P_(out["obs"]), P_(out["start"]), L, n_glob, k, ring.obs_bytes,
+                                                    0, P_(stacked), None, s), "stack")
         if learner:
             rpl._lib.check(lib.rpl_returns_nstep(P_(r_tr), P_(d_tr), Tn, n_glob, c["n_step"], c["gamma"],
                                                  P_(q_pool[i % P][c["burn_in"]:c["burn_in"] + Tn]),
@@ -362,7 +373,8 @@ def run_rpl(args):
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    launches = (rpl.launch_count() - launches0) if not use_graph else (4 if world == 1 else 4 + int(learner)) * K_eff
+    launches = ((rpl.launch_count() - launches0) if not use_graph
+                else (4 if world == 1 else 4 + int(learner) + int(mode_c and rank == 0)) * K_eff)
     clk = clocks.stop() if not args.profile else {}
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -386,6 +398,8 @@ def run_rpl(args):
     g_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
     owned = n  # per rank, on average
     alg_bytes = owned * seq_bytes_per_sample(c)
+    if mode_c:  # Mode C gathers unique rows (the learner re-stacks them)
+        alg_bytes = owned * (seq_bytes_per_sample(c) - L * k * FRAME + (L + k - 1) * FRAME)
     peak, peak_kind = measured_peaks()
     achieved = alg_bytes / (g_ms / 1e3) / 1e9
 

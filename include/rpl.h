@@ -307,10 +307,24 @@ typedef struct {
    * Honoured by the default sequence pipeline, the chunked sequence kernel and the
    * transition kernel (other diagnostic variants fall back to the default when set). */
   const int64_t* col_offset;
+  /* Optional int8 [L, n] output (SEQUENCE, default kernel only — RPL_EUNSUPPORTED when it
+   * cannot run): the episode-start offset of each output row, i.e. how many leading stack
+   * slots are padding (§8c #13).  With RPL_OUT_UNIQUE it is all a consumer needs to
+   * rebuild the k-stacks (rpl_stack_frames) — Mode C ships unique rows + offsets. */
+  int8_t* o_start;
 } rpl_gather_desc;
 
 int rpl_gather(const rpl_gather_desc* desc /* host */, const int64_t* idx, const int64_t* q,
                const int64_t* qmin, double beta, int64_t n, int32_t* dev_err, void* stream);
+
+/* k-stacks from unique rows (Mode C learner side, §8e): uniq [L+k-1, n, obs_bytes] as written
+ * by rpl_gather with RPL_OUT_UNIQUE, start int8 [L, n] its o_start; out [L, n, k, obs_bytes]
+ * gets out[tau, s, j] = uniq[tau + max(j, start[tau, s]), s] (zero when j < start and
+ * pad_mode == RPL_PAD_ZERO) — bit-identical to rpl_gather's RPL_OUT_STACKED output.
+ * n_active (device, may be NULL) limits the samples.  obs_bytes % 16 == 0, 16-B aligned
+ * pointers, k <= 8, n <= 65535. */
+int rpl_stack_frames(const void* uniq, const int8_t* start, int64_t L, int64_t n, int32_t k, int64_t obs_bytes,
+                     int32_t pad_mode, void* out, const int64_t* n_active, void* stream);
 
 /* =========================================================================
  * (4) Ring append and validity maintenance (§8a a12, §8f NEXT-2; P:75-84 the sampler

@@ -53,6 +53,7 @@ class GatherDesc(C.Structure):
         ("o_done_n", C.c_void_p), ("o_w", C.c_void_p), ("o_rnn", C.c_void_p),
         ("n_active", C.c_void_p),
         ("col_offset", C.c_void_p),
+        ("o_start", C.c_void_p),
     ]
 
 
@@ -88,6 +89,7 @@ _SIGS = {
     "rpl_sample_uniform": ([I64, U64, U64, P, I64, I64, I64, I64, P, P], C.c_int),
     "rpl_gather": ([C.POINTER(GatherDesc), P, P, P, D, I64, P, P], C.c_int),
     "rpl_ring_append": ([C.POINTER(GatherDesc), P, P, P, P, P, I64, P], C.c_int),
+    "rpl_stack_frames": ([P, P, I64, I64, I32, I64, I32, P, P, P], C.c_int),
     "rpl_returns_nstep_dq": ([P, P, I64, I64, I32, D, P, P, I32, I32, D, P, P, P, P], C.c_int),
     "rpl_c51_project": ([P, P, P, P, I64, I32, I32, D, D, D, P, P, P], C.c_int),
     "rpl_replay_validity": ([C.POINTER(TreeLayout), P, I32, I64, I64, I32, I32, I32, I32, I64, I64, I64, I64, P],

@@ -177,6 +177,7 @@ struct GDesc {
   int diag;  // rpl_debug_set_gather_diag mask (0 in normal operation)
   const int64_t* n_active;  // device count of leading entries to gather (NULL: all n)
   const int64_t* col_offset;  // device output column offset (NULL: 0)
+  int8_t* o_start;            // per-row episode-start offsets [L, n] (NULL: not produced)
 };
 
 // Output column offset (rpl_gather_desc.col_offset); read after pdl_wait.
@@ -1055,6 +1056,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         if (D.o_rew) D.o_rew[o] = rw;
         if (D.o_prev_rew) D.o_prev_rew[o] = pd ? 0.0f : prw;
         if (D.o_done) D.o_done[o] = dd;
+        if (D.o_start) D.o_start[o] = start_off[c];
         if (tau == 0 && D.o_w && q) {
           const int64_t qs = q[sm];
           D.o_w[coff + sm] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
@@ -1473,6 +1475,7 @@ GDesc to_dev(const rpl_gather_desc* d) {
   g.diag = g_seq_diag;
   g.n_active = d->n_active;
   g.col_offset = d->col_offset;
+  g.o_start = d->o_start;
   return g;
 }
 
@@ -1512,7 +1515,8 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
   if ((desc->o_act || desc->o_prev_act) && (!desc->act || desc->act_bytes < 1)) return RPL_EINVAL;
   if (desc->o_w && !(beta >= 0.0)) return RPL_EINVAL;
   GDesc g = to_dev(desc);
-  const int seq_variant = desc->col_offset ? 0 : g_seq_variant;  // col_offset: default kernels only
+  // col_offset / o_start: default kernels only
+  const int seq_variant = (desc->col_offset || desc->o_start) ? 0 : g_seq_variant;
   const bool tma_ok = (desc->obs_bytes % 16 == 0) && aligned16(desc->obs) && aligned16(desc->o_obs) &&
                       aligned16(desc->o_next_obs) && desc->obs_bytes <= 32768;
   cudaStream_t st = as_stream(stream);
@@ -1589,7 +1593,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       }
     }
     if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs &&
-        (seq_variant == 3 || (seq_variant == 0 && !desc->col_offset))) {
+        (seq_variant == 3 || (seq_variant == 0 && !desc->col_offset && !desc->o_start))) {
       // persistent TMA pipeline: NS frame slots (+1 zero slot); CTAs_per_SM CTAs per SM
       // Slots the consumer may need beyond the released ones: G+1 rows of advance, the
       // k-1 window, and k-1 per piece boundary crossed.  With L > G at most two boundaries
@@ -1624,6 +1628,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
         return launch_status();
       }
     }
+    if (desc->o_start) return RPL_EUNSUPPORTED;  // produced by the persistent default kernel only
     const int64_t smem = (int64_t)(SEQ_CHUNK + desc->k) * desc->obs_bytes;
     g.use_tma = (tma_ok && smem <= 200 * 1024) ? 1 : 0;
     const size_t dyn = g.use_tma ? (size_t)smem : 0;
@@ -1640,4 +1645,56 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
     return launch_status();
   }
   return RPL_EINVAL;
+}
+
+// ---------------------------------------------------------------------------
+// k-stacks from unique rows (Mode C learner side, §8e): out[tau, s] slot j = unique row
+// tau + max(j, start[tau, s]) of sample s (zero when j < start and pad_mode is ZERO) —
+// the same frame-stacking-wrapper rule (§8c #13) the gather applies, with the episode
+// starts computed by the owners (rpl_gather_desc.o_start).  One warp per output stack;
+// its k source rows are the neighbours' too, so they come mostly from L1/L2.
+// ---------------------------------------------------------------------------
+namespace rpl {
+namespace {
+constexpr int ST_WARPS = 8;
+
+__global__ void __launch_bounds__(ST_WARPS * 32)
+k_stack_frames(const uint8_t* __restrict__ uniq, const int8_t* __restrict__ start, int L, int64_t n, int k,
+               int64_t ob, int pad_mode, uint8_t* __restrict__ out, const int64_t* __restrict__ n_active) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int tau = blockIdx.x * ST_WARPS + (threadIdx.x >> 5);
+  const int64_t s = blockIdx.y;
+  const int64_t na = n_active ? *n_active : n;
+  if (tau >= L || s >= na) return;
+  const int so = start[(int64_t)tau * n + s];
+  const int nv = (int)(ob / 16);
+  int4* dst = reinterpret_cast<int4*>(out + (((int64_t)tau * n + s) * k) * ob);
+  for (int j = 0; j < k; ++j) {
+    int4* d = dst + (int64_t)j * nv;
+    if (j < so && pad_mode == RPL_PAD_ZERO) {
+      for (int v = lane; v < nv; v += 32) __stcs(d + v, make_int4(0, 0, 0, 0));
+    } else {
+      const int u = tau + (j < so ? so : j);
+      const int4* src = reinterpret_cast<const int4*>(uniq + ((int64_t)u * n + s) * ob);
+#pragma unroll 4
+      for (int v = lane; v < nv; v += 32) __stcs(d + v, __ldg(src + v));
+    }
+  }
+}
+}  // namespace
+}  // namespace rpl
+
+extern "C" int rpl_stack_frames(const void* uniq, const int8_t* start, int64_t L, int64_t n, int32_t k,
+                                int64_t obs_bytes, int32_t pad_mode, void* out, const int64_t* n_active,
+                                void* stream) {
+  if (!uniq || !start || !out || L < 1 || n < 0 || k < 1 || k > 8 || obs_bytes < 16 || (obs_bytes & 15) ||
+      (reinterpret_cast<uintptr_t>(uniq) & 15) || (reinterpret_cast<uintptr_t>(out) & 15) || L > (1 << 30) ||
+      n > 65535 || (pad_mode != RPL_PAD_REPEAT && pad_mode != RPL_PAD_ZERO))
+    return RPL_EINVAL;
+  if (n == 0) return RPL_OK;
+  const dim3 grid((unsigned)((L + ST_WARPS - 1) / ST_WARPS), (unsigned)n);
+  return launch_pdl(k_stack_frames, grid, dim3(ST_WARPS * 32), 0, as_stream(stream),
+                    static_cast<const uint8_t*>(uniq), start, (int)L, n, (int)k, obs_bytes, (int)pad_mode,
+                    static_cast<uint8_t*>(out), n_active);
 }

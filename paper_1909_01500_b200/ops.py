@@ -17,7 +17,7 @@ from ._lib import GatherDesc, TreeLayout, check, lib
 __all__ = [
     "returns_discounted", "returns_nstep", "gae", "value_rescale", "SumTree", "is_weights", "gather",
     "GatherRing", "GatherPlan", "check_err", "launch_count", "debug_priority_values", "sample_uniform",
-    "ring_append", "returns_nstep_dq", "c51_project",
+    "ring_append", "returns_nstep_dq", "c51_project", "stack_frames",
 ]
 
 
@@ -432,11 +432,13 @@ def gather(ring: GatherRing, idx, kind="transition", k=4, n_step=1, gamma=0.99, 
         alloc("done", (L, n), torch.uint8)
         if ring.rnn is not None:
             alloc("rnn", (int(ring.rnn.shape[2]), n, int(ring.rnn.shape[3])), ring.rnn.dtype)
+        if wants is not None and "start" in wants:  # episode-start offsets (Mode C shipping)
+            alloc("start", (L, n), torch.int8)
     if q is not None:
         alloc("w", (n,), torch.float32)
     fields = {"obs": "o_obs", "next_obs": "o_next_obs", "act": "o_act", "prev_act": "o_prev_act", "rew": "o_rew",
               "prev_rew": "o_prev_rew", "done": "o_done", "ret": "o_ret", "done_n": "o_done_n", "w": "o_w",
-              "rnn": "o_rnn"}
+              "rnn": "o_rnn", "start": "o_start"}
     for name, f in fields.items():
         if name in o and o[name] is not None:
             setattr(g, f, o[name].data_ptr())
@@ -468,7 +470,8 @@ class GatherPlan:
         self.desc = _desc(ring, kind_i, k, pad_mode, out_mode, n_step if kind_i == 0 else 1, seq_len, period, gamma)
         fields = {"obs": "o_obs", "next_obs": "o_next_obs", "act": "o_act", "prev_act": "o_prev_act",
                   "rew": "o_rew", "prev_rew": "o_prev_rew", "done": "o_done", "ret": "o_ret", "done_n": "o_done_n",
-                  "w": "o_w", "rnn": "o_rnn"}
+                  "w": "o_w", "rnn": "o_rnn",
+                  "start": "o_start"}
         for name, f in fields.items():
             if name in self.outputs:
                 setattr(self.desc, f, self.outputs[name].data_ptr())
@@ -503,3 +506,17 @@ def ring_append(ring: GatherRing, obs=None, act=None, rew=None, done=None, rnn=N
     ring.cursor = (ring.cursor + T_b) % ring.cap_T
     ring.size = min(ring.cap_T, ring.size + T_b)
     return old
+
+
+def stack_frames(uniq, start, k, pad_mode=_lib.PAD_REPEAT, out=None, n_active=None):
+    """rpl_stack_frames: uniq [L+k-1, n, *item] + start int8 [L, n] -> stacked [L, n, k, *item]."""
+    _req(start, torch.int8, "start")
+    L, n = (int(x) for x in start.shape)
+    if uniq.shape[0] != L + k - 1 or uniq.shape[1] != n or not uniq.is_contiguous():
+        raise ValueError("uniq must be a contiguous [L+k-1, n, ...] tensor")
+    item = tuple(uniq.shape[2:])
+    ob = int(uniq[0, 0].numel() * uniq.element_size())
+    out = torch.empty((L, n, k) + item, dtype=uniq.dtype, device=uniq.device) if out is None else out
+    check(lib.rpl_stack_frames(_ptr(uniq), _ptr(start), L, n, int(k), ob, int(pad_mode), _ptr(out), _ptr(n_active),
+                               _stream(uniq.device)), "rpl_stack_frames")
+    return out

@@ -378,3 +378,27 @@ def test_col_offset(rpl, kind):
         assert np.array_equal(got, r), name
         rest = np.delete(o, np.arange(off, off + m), axis=axis)
         assert not rest.any(), name
+
+
+@pytest.mark.parametrize("pad_mode", [0, 1])
+def test_unique_plus_start_stacks_equal_stacked(rpl, pad_mode):
+    # Mode C shipping: RPL_OUT_UNIQUE rows + o_start offsets, re-stacked by rpl_stack_frames,
+    # are bit-identical to the stacked gather (and to the oracle)
+    import torch
+    period, L, k = 40, 125, 4
+    ring = make_ring(97, cap=400, B=4, ep_len=12.0, period=period, rnn_h=8, reward_kind="r2d2")
+    dr = dev_ring(rpl, ring)
+    g = rng(19)
+    idx = []
+    while len(idx) < 20:
+        blk, b = int(g.integers(0, 10)), int(g.integers(0, 4))
+        if OG.window_valid_sequence(blk * period, 400, ring.cursor, ring.size, k, L):
+            idx.append(blk * 4 + b)
+    idx = np.array(idx, np.int64)
+    uq = rpl.gather(dr, T_(idx), kind="sequence", k=k, seq_len=L, period=period, pad_mode=pad_mode, out_mode=1,
+                    want=["obs", "start"])
+    st = rpl.stack_frames(uq["obs"], uq["start"], k, pad_mode=pad_mode)
+    ref = OG.gather_sequences(idx, 4, ring.obs, ring.act, ring.rew, ring.done, ring.rnn, k, L, period, pad_mode)
+    assert np.array_equal(H(st), ref["obs"])
+    sg = rpl.gather(dr, T_(idx), kind="sequence", k=k, seq_len=L, period=period, pad_mode=pad_mode, want=["obs"])
+    assert np.array_equal(H(st), H(sg["obs"]))

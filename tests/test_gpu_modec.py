@@ -1,8 +1,9 @@
 """Mode C end to end on one GPU: two ranks (gloo, both on cuda:0) each own half of the
-ring columns and one sum tree; the compacted sharded sampler + rpl_gather with
-n_active / col_offset write every owned sequence straight into rank 0's batch buffers
-(mapped through CUDA IPC, CentralBatch).  Rank 0 then checks the whole central batch
-against the oracle gather of the global sample (sharded == concatenated, §8c #17)."""
+ring columns and one sum tree; the compacted sharded sampler + rpl_gather (unique rows +
+episode-start offsets) with n_active / col_offset write every owned sequence straight into
+rank 0's batch buffers (mapped through CUDA IPC, CentralBatch); rank 0 re-stacks the frames
+(rpl_stack_frames) and checks the whole central batch against the oracle gather of the
+global sample (sharded == concatenated, §8c #17)."""
 import os
 import socket
 
@@ -51,11 +52,12 @@ def _worker(rank, world, port, queue):
     tree.update(torch.from_numpy(valid).to(dev), torch.from_numpy(np.abs(g.normal(size=valid.size)).astype(np.float32)).to(dev), 0.9)
     smp = ShardedSampler(tree, N_PER, seed=17, compact=True)
     n_glob = N_PER * world
-    root_plan = rpl.GatherPlan(ring, n_glob, kind="sequence", k=K, seq_len=L, period=PERIOD,
-                               with_weights=True) if rank == 0 else None
+    want = ["obs", "act", "prev_act", "rew", "prev_rew", "done", "rnn", "start"]
+    root_plan = rpl.GatherPlan(ring, n_glob, kind="sequence", k=K, seq_len=L, period=PERIOD, with_weights=True,
+                               out_mode=1, want=want) if rank == 0 else None
     cb = CentralBatch(root_plan.outputs if rank == 0 else None)
     plan = root_plan if rank == 0 else rpl.GatherPlan(ring, n_glob, kind="sequence", k=K, seq_len=L, period=PERIOD,
-                                                      with_weights=True, outputs=cb.outputs)
+                                                      with_weights=True, out_mode=1, want=want, outputs=cb.outputs)
     plan.desc.n_active = smp.count.data_ptr()
     plan.desc.col_offset = smp.count.data_ptr() + 8
     if rank == 0:
@@ -74,6 +76,8 @@ def _worker(rank, world, port, queue):
     dist.all_gather_object(parts, mine)
     if rank == 0:
         res = {name: t.cpu().numpy() for name, t in cb.outputs.items()}
+        # learner side: k-stacks rebuilt from the shipped unique rows + episode-start offsets
+        res["obs"] = rpl.stack_frames(cb.outputs["obs"], cb.outputs["start"], K).cpu().numpy()
         queue.put((parts, res, n_leaves))
     dist.barrier()
     dist.destroy_process_group()
