@@ -204,3 +204,16 @@ def test_buffer_min_is_the_per_normaliser():
         if qi > 0:
             assert abs((N * qi / Q) ** -beta / wmax - (qm / qi) ** beta) <= 1e-12
     assert S.buffer_min([0, 0]) == (1 << 63) - 1
+
+
+def test_live_only_update_never_revives_and_keeps_max_seen():
+    # R30: entries on zero leaves are skipped entirely (value and max-seen); live leaves update
+    t = S.SumTreeOracle(8, 0)
+    t.q = [5, 0, 7, 0, 0, 3, 0, 1]
+    before_max = t.max_seen
+    t.update([1, 3, 4], [100.0, 200.0, 300.0], 1.0, 0.0, live_only=True)
+    assert t.q == [5, 0, 7, 0, 0, 3, 0, 1] and t.max_seen == before_max
+    t.update([0, 1], [2.0, 9.0], 1.0, 0.0, live_only=True)
+    assert t.q[0] == 2 and t.q[1] == 0                  # F = 0: q = RNE(p^1) = 2
+    t.update([1], [9.0], 1.0, 0.0)                      # the plain update writes it
+    assert t.q[1] == 9 and t.max_seen == 9
