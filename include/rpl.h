@@ -180,6 +180,17 @@ int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree, int64_t n
                               double beta, int64_t* out_idx, int64_t* out_q, int64_t* out_qmin,
                               float* out_w, int32_t* dev_err, void* stream);
 
+/* Sampling WITHOUT replacement (§8f NEXT-4, reading R32): n successive proportional draws,
+ * each over the leaves not drawn yet — draw k: prefix_k = floor(u_k * Q_k / 2^64) with Q_k the
+ * total after removing the k earlier leaves, u_k = Philox4x32-10(seed, offset + k [+ the tree's
+ * stream position when use_stream, advanced by n]) (R23); the leaf whose half-open interval
+ * holds prefix_k.  The tree is restored exactly before the call returns (integer sums).
+ * Fewer than n non-zero leaves: the remaining entries are -1 (+RPL_DERR_EMPTY).  One warp,
+ * n x depth dependent L2 round trips: for small batches. */
+int rpl_sumtree_sample_unique(const rpl_tree_layout* L, int64_t* tree, int64_t n, uint64_t seed,
+                              uint64_t offset, int32_t use_stream, int64_t* out_idx, int64_t* out_q,
+                              int32_t* dev_err, void* stream);
+
 /* Sharded sampling: rank `rank` of n_shards holds one tree; shard_totals
  * (device int64 [n_shards], e.g. all-gathered rpl_sumtree_total outputs) define the global
  * total Q and the shard-major global leaf order (global idx = rank * shard_leaves + local).

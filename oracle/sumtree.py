@@ -133,3 +133,28 @@ def buffer_min(q_leaves) -> int:
     largest weight any stored transition could receive (PER), not the batch's."""
     pos = [int(x) for x in q_leaves if int(x) > 0]
     return min(pos) if pos else (1 << 63) - 1
+
+
+def sample_unique(q_leaves, n, draws):
+    """Sampling WITHOUT replacement (§8f NEXT-4, R32): successive proportional draws; draw k
+    takes prefix = floor(u_k Q_k / 2**64) over the leaves not drawn yet (Q_k their total) and
+    the unique leaf whose half-open interval holds it.  Returns (idx, q) lists; -1 / 0 once
+    no mass is left."""
+    q = [int(x) for x in q_leaves]
+    out_i, out_q = [], []
+    for k in range(n):
+        Q = sum(q)
+        if Q == 0:
+            out_i.append(-1)
+            out_q.append(0)
+            continue
+        prefix = (int(draws[k]) * Q) >> 64
+        acc = 0
+        for i, v in enumerate(q):
+            if acc <= prefix < acc + v:
+                break
+            acc += v
+        out_i.append(i)
+        out_q.append(q[i])
+        q[i] = 0
+    return out_i, out_q

@@ -84,6 +84,7 @@ _SIGS = {
     "rpl_sumtree_find": ([C.POINTER(TreeLayout), P, P, I64, P, P, P], C.c_int),
     "rpl_sumtree_total": ([C.POINTER(TreeLayout), P, P, P], C.c_int),
     "rpl_sumtree_min": ([C.POINTER(TreeLayout), P, P, P], C.c_int),
+    "rpl_sumtree_sample_unique": ([C.POINTER(TreeLayout), P, I64, U64, U64, I32, P, P, P, P], C.c_int),
     "rpl_sumtree_rebuild": ([C.POINTER(TreeLayout), P, P], C.c_int),
     "rpl_is_weights": ([P, P, I64, D, P, P], C.c_int),
     "rpl_sample_uniform": ([I64, U64, U64, P, I64, I64, I64, I64, P, P], C.c_int),

@@ -393,6 +393,87 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
   }
 }
 
+// Sampling WITHOUT replacement (§8f NEXT-4, reading R32): successive proportional draws —
+// draw k takes prefix_k = floor(u_k Q_k / 2^64) on the tree with the k leaves drawn so far
+// removed (their q subtracted along their root paths), then every removed leaf is put back.
+// One warp, n sequential descents: exact (integer tree) but latency-bound (n x D dependent
+// L2 round trips), meant for small batches.
+__global__ void __launch_bounds__(32)
+k_tree_sample_unique(TreeDev L, int64_t* __restrict__ tree, int64_t n, uint64_t seed, uint64_t offset,
+                     int use_stream, int64_t* __restrict__ out_idx, int64_t* __restrict__ out_q, int32_t* err) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  int64_t* leaves = tree + L.level_off[L.depth];
+  const uint64_t ctr0 = offset + (use_stream ? (uint64_t)__ldcg(tree + L.hdr_off + 2) : 0ull);
+  int32_t errbits = 0;
+  int64_t drawn = 0;
+  for (int64_t k = 0; k < n; ++k) {
+    const uint64_t Q = (uint64_t)__ldcg(tree + L.level_off[0]);
+    if (Q == 0) {  // fewer non-zero leaves than n: the rest stay -1
+      if (lane == 0) {
+        out_idx[k] = -1;
+        out_q[k] = 0;
+      }
+      errbits |= RPL_DERR_EMPTY;
+      continue;
+    }
+    const uint64_t u = philox_u64(seed, ctr0 + (uint64_t)k);
+    int64_t q = 0;
+    int64_t prefix = (int64_t)__umul64hi(u, Q);
+    // descent with L2-coherent loads (the removals below are plain stores of this warp)
+    int64_t node = 0, c = 0;
+    for (int l = 0; l < L.depth; ++l) {
+      const int64_t base = L.level_off[l + 1] + (node << L.log2w);
+      c = lane < L.fanout ? __ldcg(tree + base + lane) : 0;
+      int64_t incl = c;
+#pragma unroll
+      for (int dlt = 1; dlt < 32; dlt <<= 1) {
+        const int64_t o = shfl_up64(incl, dlt);
+        if (lane >= dlt) incl += o;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, prefix < incl);
+      const int f = bal ? __ffs(bal) - 1 : 0;
+      if (!bal) errbits |= RPL_DERR_TREE;
+      const int64_t inc_f = shfl64(incl, f);
+      const int64_t c_f = shfl64(c, f);
+      prefix -= inc_f - c_f;
+      node = (node << L.log2w) + f;
+      c = c_f;
+    }
+    q = c;
+    if (lane == 0) {
+      out_idx[k] = node;
+      out_q[k] = q;
+      // remove the leaf: subtract q along its root path
+      leaves[node] = 0;
+      int64_t a = node;
+      for (int l = L.depth - 1; l >= 0; --l) {
+        a >>= L.log2w;
+        tree[L.level_off[l] + a] -= q;
+      }
+      __threadfence_block();
+    }
+    __syncwarp();
+    ++drawn;
+  }
+  // put every drawn leaf back (integer sums: exact restore)
+  if (lane == 0) {
+    for (int64_t k = 0; k < drawn; ++k) {
+      const int64_t leaf = out_idx[k];
+      if (leaf < 0) continue;
+      const int64_t q = out_q[k];
+      leaves[leaf] = q;
+      int64_t a = leaf;
+      for (int l = L.depth - 1; l >= 0; --l) {
+        a >>= L.log2w;
+        tree[L.level_off[l] + a] += q;
+      }
+    }
+    if (use_stream) tree[L.hdr_off + 2] = (int64_t)(ctr0 - offset + (uint64_t)n);
+    if (errbits) set_err(err, errbits);
+  }
+}
+
 __global__ void k_tree_find(TreeDev L, const int64_t* __restrict__ tree, const int64_t* __restrict__ prefix,
                             int64_t n, int64_t* __restrict__ out_idx, int32_t* err) {
   const int lane = threadIdx.x & 31;
@@ -693,4 +774,12 @@ extern "C" int rpl_sumtree_min(const rpl_tree_layout* L, const int64_t* tree, in
   if (blocks > cap) blocks = cap;
   return launch_pdl(k_leaf_min, dim3((unsigned)blocks), dim3(threads), 0, as_stream(stream),
                     (const int64_t*)(tree + L->level_off[L->depth]), L->n_leaves, out_min);
+}
+
+extern "C" int rpl_sumtree_sample_unique(const rpl_tree_layout* L, int64_t* tree, int64_t n, uint64_t seed,
+                                         uint64_t offset, int32_t use_stream, int64_t* out_idx, int64_t* out_q,
+                                         int32_t* dev_err, void* stream) {
+  if (!layout_ok(L) || !tree || !out_idx || !out_q || n < 1 || n > (1ll << 30)) return RPL_EINVAL;
+  return launch_pdl(k_tree_sample_unique, dim3(1), dim3(32), 0, as_stream(stream), tree_dev(L), tree, n, seed, offset,
+                    (int)(use_stream != 0), out_idx, out_q, dev_err);
 }

@@ -329,6 +329,17 @@ class SumTree:
         check(lib.rpl_sumtree_total(self._lp, _ptr(self.storage), _ptr(out), self._s()), "rpl_sumtree_total")
         return out
 
+    def sample_unique(self, n, seed, offset=0, use_stream=False, err=None):
+        """rpl_sumtree_sample_unique: n distinct leaves by successive proportional draws."""
+        n = int(n)
+        idx = torch.empty(n, dtype=torch.int64, device=self.device)
+        q = torch.empty(n, dtype=torch.int64, device=self.device)
+        e = self.err if err is None else err
+        check(lib.rpl_sumtree_sample_unique(self._lp, _ptr(self.storage), n, int(seed) & (2 ** 64 - 1),
+                                            int(offset) & (2 ** 64 - 1), 1 if use_stream else 0, _ptr(idx), _ptr(q),
+                                            _ptr(e), self._s()), "rpl_sumtree_sample_unique")
+        return idx, q
+
     def min_q(self, out=None):
         """rpl_sumtree_min: buffer-wide min q over non-zero leaves (NEXT-4 IS normaliser)."""
         out = torch.empty(1, dtype=torch.int64, device=self.device) if out is None else out

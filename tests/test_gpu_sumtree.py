@@ -417,3 +417,22 @@ def test_update_live_only(rpl, seq):
         td = [float(x) for x in tdv]
     orc.update([int(x) for x in idx], td, 0.9, live_only=True)
     check_tree_consistent(t, orc)
+
+
+@pytest.mark.parametrize("N,n,zeros", [(25600, 64, 0.2), (100, 60, 0.5), (40, 40, 0.3)])
+def test_sample_unique_vs_oracle(rpl, N, n, zeros):
+    # NEXT-4 (R32): distinct successive proportional draws, tree restored bit-exactly
+    g = rng(N + n)
+    t = rpl.SumTree(N, 32)
+    orc = OS.SumTreeOracle(N)
+    live = np.array([i for i in range(N) if g.random() >= zeros], np.int64)
+    td = td_abs(g, live.size)
+    t.update(T_(live), T_(td), 0.6)
+    orc.update([int(x) for x in live], [float(x) for x in td], 0.6)
+    before = H(t.storage).copy()
+    idx, q = t.sample_unique(n, seed=123, offset=7)
+    ref_i, ref_q = OS.sample_unique(orc.q, n, OP.draws_u64(123, 7, n))
+    assert H(idx).tolist() == ref_i and H(q).tolist() == ref_q
+    assert np.array_equal(H(t.storage), before)               # tree restored exactly
+    got = [i for i in H(idx).tolist() if i >= 0]
+    assert len(got) == len(set(got))

@@ -217,3 +217,25 @@ def test_live_only_update_never_revives_and_keeps_max_seen():
     assert t.q[0] == 2 and t.q[1] == 0                  # F = 0: q = RNE(p^1) = 2
     t.update([1], [9.0], 1.0, 0.0)                      # the plain update writes it
     assert t.q[1] == 9 and t.max_seen == 9
+
+
+def test_sample_unique_pins():
+    # R32: successive proportional draws without replacement
+    import random
+    rnd = random.Random(3)
+    q = [0, 4, 0, 1, 7, 2, 0, 9]
+    draws = [rnd.getrandbits(64) for _ in range(8)]
+    idx, qq = S.sample_unique(q, 8, draws)
+    nz = [i for i, v in enumerate(q) if v > 0]
+    assert sorted(i for i in idx if i >= 0) == nz            # every non-zero leaf exactly once
+    assert idx[len(nz):] == [-1] * (8 - len(nz)) and all(q[i] == v for i, v in zip(idx, qq) if i >= 0)
+    t = S.SumTreeOracle(len(q), 0)
+    t.q = list(q)
+    assert idx[0] == t.find((draws[0] * sum(q)) >> 64)       # the first draw is the proportional one
+    # two leaves, q = [1, 3]: first draw is leaf 1 with probability 3/4 exactly over u
+    assert S.sample_unique([1, 3], 2, [0, 0])[0] == [0, 1]
+    assert S.sample_unique([1, 3], 2, [2 ** 62, 0])[0] == [1, 0]   # u/2^64 = 1/4 -> prefix 1
+    counts = [0, 0]
+    for _ in range(4000):
+        counts[S.sample_unique([1, 3], 1, [rnd.getrandbits(64)])[0][0]] += 1
+    assert abs(counts[1] / 4000 - 0.75) < 0.03
