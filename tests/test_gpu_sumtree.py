@@ -436,3 +436,19 @@ def test_sample_unique_vs_oracle(rpl, N, n, zeros):
     assert np.array_equal(H(t.storage), before)               # tree restored exactly
     got = [i for i in H(idx).tolist() if i >= 0]
     assert len(got) == len(set(got))
+
+
+def test_more_strata_than_mass(rpl):
+    # Q < n: empty strata take lo_k (§8c #8); zero leaves still never drawn
+    import torch
+    t = rpl.SumTree(5, 32, frac_bits=0)
+    q = np.array([0, 2, 0, 1, 2], np.int64)
+    t.set_q(T_(np.arange(5, dtype=np.int64)), T_(q))
+    orc = OS.SumTreeOracle(5, 0)
+    orc.q = [int(x) for x in q]
+    for n in (5, 16, 33):
+        draws = OP.draws_u64(31, n, n)
+        idx, qq, qmin, _ = t.sample(n, draws=T_(as_i64(draws)))
+        oi, oq, oqm = orc.sample(n, draws)
+        assert H(idx).tolist() == oi and H(qq).tolist() == oq and int(H(qmin)[0]) == oqm
+        assert all(q[i] > 0 for i in oi)
