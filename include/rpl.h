@@ -20,6 +20,12 @@
  *  - Calls on the same sum tree must be stream-ordered by the caller (the device
  *    analogue of rlpyt's replay read-write lock).  No kernel uses
  *    floating-point atomics: every output is bit-deterministic for fixed inputs.
+ *  - Thread safety: calls may come from several host threads / devices.  The library's
+ *    only state is per-device attribute caches (SM count, raised shared-memory limits)
+ *    behind a mutex, a one-time driver-entry-point lookup and an atomic launch counter;
+ *    the rpl_debug_* knobs are process-global and meant for tests.
+ *  - rpl_ring_append uses cudaMemcpyAsync: with pageable (non-pinned) host sources the
+ *    copy is synchronous with respect to the host.
  */
 #ifndef RPL_H_
 #define RPL_H_

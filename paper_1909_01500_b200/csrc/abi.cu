@@ -5,15 +5,14 @@
 #include <string.h>
 
 namespace rpl {
-int64_t g_launches = 0;
+std::atomic<int64_t> g_launches{0};
 
 bool pdl_enabled() {
-  static int cached = -1;
-  if (cached < 0) {
+  static const bool on = [] {
     const char* v = getenv("RPL_PDL");
-    cached = (v && strcmp(v, "0") == 0) ? 0 : 1;
-  }
-  return cached == 1;
+    return !(v && strcmp(v, "0") == 0);
+  }();
+  return on;
 }
 }
 
@@ -31,4 +30,4 @@ extern "C" const char* rpl_strerror(int status) {
 
 extern "C" int rpl_abi_version(void) { return RPL_ABI_VERSION; }
 
-extern "C" int64_t rpl_launch_count(void) { return rpl::g_launches; }
+extern "C" int64_t rpl_launch_count(void) { return rpl::g_launches.load(); }

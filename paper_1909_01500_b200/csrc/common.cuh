@@ -3,22 +3,47 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "rpl.h"
 
 namespace rpl {
 
-extern int64_t g_launches;  // host-side launch counter (rpl_launch_count)
+extern std::atomic<int64_t> g_launches;  // host-side launch counter (rpl_launch_count)
+
+// Per-device attribute caches (the library's only state; thread-safe).
+inline std::mutex& cache_mutex() {
+  static std::mutex m;
+  return m;
+}
 
 inline int sm_count() {
-  static int cached = 0;
-  if (cached == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int v = 0;
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    cached = v > 0 ? v : 148;
+  static std::map<int, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(cache_mutex());
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return cache[dev] = (v > 0 ? v : 148);
+}
+
+// Raise a kernel's dynamic shared-memory limit to `bytes` once per (device, kernel).
+inline void ensure_smem(const void* kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(cache_mutex());
+  size_t& cur = done[std::make_pair(dev, kernel)];
+  if (bytes > cur) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cur = bytes;
   }
-  return cached;
 }
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }

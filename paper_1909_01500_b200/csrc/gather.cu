@@ -1149,11 +1149,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
 template <int NC>
 int launch_seq_lsu(const GDesc& g, const int64_t* idx, int64_t n, int NS, int64_t rows_per_cta, const int64_t* q,
                    const int64_t* qmin, double beta, int32_t* dev_err, size_t dyn, int64_t grid, cudaStream_t st) {
-  static size_t set_l = 0;
-  if (dyn > 48 * 1024 && dyn > set_l) {
-    cudaFuncSetAttribute(k_gather_seq_pipe_lsu<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    set_l = dyn;
-  }
+  ensure_smem(reinterpret_cast<const void*>(k_gather_seq_pipe_lsu<NC>), dyn);
   return launch_pdl(k_gather_seq_pipe_lsu<NC>, dim3((unsigned)grid), dim3((NC + 2) * 32), dyn, st, g, idx, n, NS,
                     rows_per_cta, q, qmin, beta, dev_err);
 }
@@ -1422,11 +1418,7 @@ template <int NL>
 int launch_seq_ldg_bulk(const GDesc& g, const int64_t* idx, int64_t n, int NS, int64_t rows_per_cta,
                         const int64_t* q, const int64_t* qmin, double beta, int32_t* dev_err, size_t dyn,
                         int64_t grid, cudaStream_t st) {
-  static size_t set_l = 0;
-  if (dyn > 48 * 1024 && dyn > set_l) {
-    cudaFuncSetAttribute(k_gather_seq_ldg_bulk<NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    set_l = dyn;
-  }
+  ensure_smem(reinterpret_cast<const void*>(k_gather_seq_ldg_bulk<NL>), dyn);
   return launch_pdl(k_gather_seq_ldg_bulk<NL>, dim3((unsigned)grid), dim3((NL + 2) * 32), dyn, st, g, idx, n, NS,
                     rows_per_cta, q, qmin, beta, dev_err);
 }
@@ -1527,11 +1519,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
     const int64_t smem = (int64_t)(NR + 1) * desc->obs_bytes;
     g.use_tma = (tma_ok && smem <= 200 * 1024) ? 1 : 0;
     const size_t dyn = g.use_tma ? (size_t)smem : 0;
-    static size_t set_t = 0;
-    if (dyn > 48 * 1024 && dyn > set_t) {
-      cudaFuncSetAttribute(k_gather_transition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-      set_t = dyn;
-    }
+    ensure_smem(reinterpret_cast<const void*>(k_gather_transition), dyn);
     if (n > 0x7fffffff) return RPL_EINVAL;
     return launch_pdl(k_gather_transition, dim3((unsigned)n), dim3(G_THREADS), dyn, st, g, idx, n, q, qmin, beta,
                       dev_err);
@@ -1607,12 +1595,8 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       else if (NS >= 5 * k + k) G = 4;
       if (G > 0) {
         const size_t dyn = (size_t)(NS + 1) * desc->obs_bytes;
-        static size_t set_p = 0;
-        if (dyn > 48 * 1024 && dyn > set_p) {
-          cudaFuncSetAttribute(k_gather_seq_pipe<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-          cudaFuncSetAttribute(k_gather_seq_pipe<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-          set_p = dyn;
-        }
+        ensure_smem(reinterpret_cast<const void*>(k_gather_seq_pipe<16>), dyn);
+        ensure_smem(reinterpret_cast<const void*>(k_gather_seq_pipe<4>), dyn);
         const int64_t total = n * (int64_t)desc->seq_len;
         int64_t grid = (int64_t)sm_count();
         int64_t rows_per_cta = (total + grid - 1) / grid;
@@ -1632,11 +1616,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
     const int64_t smem = (int64_t)(SEQ_CHUNK + desc->k) * desc->obs_bytes;
     g.use_tma = (tma_ok && smem <= 200 * 1024) ? 1 : 0;
     const size_t dyn = g.use_tma ? (size_t)smem : 0;
-    static size_t set_s = 0;
-    if (dyn > 48 * 1024 && dyn > set_s) {
-      cudaFuncSetAttribute(k_gather_sequence, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-      set_s = dyn;
-    }
+    ensure_smem(reinterpret_cast<const void*>(k_gather_sequence), dyn);
     const int rows_out = desc->out_mode == RPL_OUT_STACKED ? desc->seq_len : desc->seq_len + desc->k - 1;
     const int chunks = (rows_out + SEQ_CHUNK - 1) / SEQ_CHUNK;
     if (n > 65535) return RPL_EINVAL;

@@ -345,11 +345,10 @@ using namespace rpl;
 // else LDG 16 warps x 8 rows), 3 = LDG 16 warps x 8 rows, 1 = LDG 32 warps x 4 rows,
 // 2 = LDG 8 warps x 16 rows.  Same fp64 affine-map arithmetic; segment boundaries differ.
 int scan_variant() {
-  static int v = -1;
-  if (v < 0) {
+  static const int v = [] {
     const char* e = getenv("RPL_SCAN_VARIANT");
-    v = e ? atoi(e) : 0;
-  }
+    return e ? atoi(e) : 0;
+  }();
   return v;
 }
 
@@ -358,16 +357,14 @@ typedef CUresult (*encode_fn_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, v
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 encode_fn_t encode_fn() {
-  static encode_fn_t fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static const encode_fn_t fn = []() -> encode_fn_t {  // thread-safe one-time lookup
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<encode_fn_t>(p);
-  }
+      return reinterpret_cast<encode_fn_t>(p);
+    return nullptr;
+  }();
   return fn;
 }
 
