@@ -452,3 +452,52 @@ def test_more_strata_than_mass(rpl):
         oi, oq, oqm = orc.sample(n, draws)
         assert H(idx).tolist() == oi and H(qq).tolist() == oq and int(H(qmin)[0]) == oqm
         assert all(q[i] > 0 for i in oi)
+
+
+def test_gpu_frequencies_chi2_upper_tail(rpl):
+    # S:653 / S:991: 1e5 stratified draws on 64 leaves follow p^alpha / sum p^alpha; stratified
+    # sampling is under-dispersed, so only the upper tail is tested (§4 of SURVEY)
+    import torch
+    g = rng(99)
+    N = 64
+    t = rpl.SumTree(N, 32)
+    td = (g.random(N) * 3).astype(np.float32)
+    t.update(T_(np.arange(N, dtype=np.int64)), T_(td), 1.0)
+    q = H(t.leaves).astype(np.float64)
+    counts = np.zeros(N)
+    for rep in range(20):
+        idx, _, _, _ = t.sample(5000, seed=rep, offset=0)
+        counts += np.bincount(H(idx), minlength=N)
+    exp = counts.sum() * q / q.sum()
+    chi2 = float(((counts - exp) ** 2 / exp).sum())
+    assert chi2 < 63 + 4 * np.sqrt(2 * 63)                  # far below: stratified draws
+    assert (counts[q == 0] == 0).all()
+
+
+def test_determinism_two_runs(rpl):
+    # identical inputs -> bit-identical tree, samples and gathered batches (no float atomics)
+    import torch
+    from synth import make_ring
+
+    def run():
+        ring = make_ring(7, cap=400, B=4, ep_len=25.0, period=40, rnn_h=8, reward_kind="r2d2")
+        dr = rpl.GatherRing(obs=T_(ring.obs), act=T_(ring.act), rew=T_(ring.rew), done=T_(ring.done),
+                            cursor=ring.cursor, size=ring.size, rnn=T_(ring.rnn))
+        t = rpl.SumTree(40, 32)
+        t.update(T_(np.arange(40, dtype=np.int64)), T_(td_abs(rng(1), 40)), 0.9)
+        outs = []
+        for i in range(3):
+            idx, q, _, _ = t.sample_stream(16, 5, want_qmin=False)
+            idx = torch.where(idx >= 0, idx, torch.zeros_like(idx))
+            o = rpl.gather(dr, idx, kind="sequence", k=4, seq_len=45, period=40, q=q, beta=0.6)
+            t.update_seq(idx, T_(np.abs(rng(i).normal(size=(45, 16))).astype(np.float32)), 0.9)
+            outs.append((H(idx), H(q), {k: H(v) for k, v in o.items()}))
+        return outs, H(t.storage)
+
+    a, ta = run()
+    b, tb = run()
+    assert np.array_equal(ta, tb)
+    for (ia, qa, oa), (ib, qb, ob) in zip(a, b):
+        assert np.array_equal(ia, ib) and np.array_equal(qa, qb)
+        for k in oa:
+            assert np.array_equal(oa[k], ob[k]), k
