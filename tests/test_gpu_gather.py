@@ -402,3 +402,47 @@ def test_unique_plus_start_stacks_equal_stacked(rpl, pad_mode):
     assert np.array_equal(H(st), ref["obs"])
     sg = rpl.gather(dr, T_(idx), kind="sequence", k=k, seq_len=L, period=period, pad_mode=pad_mode, want=["obs"])
     assert np.array_equal(H(st), H(sg["obs"]))
+
+
+def test_random_gather_stress(rpl):
+    # >= 1e4 random frame and sequence gathers (random geometry, ring wrap,
+    # episode starts inside stacks, both paddings and output modes) bit-exact vs the oracle
+    g = rng(2024)
+    total_seq = total_tr = 0
+    cfg = 0
+    while total_seq < 6000 or total_tr < 6000:
+        cfg += 1
+        period = int(g.choice([4, 8, 20]))
+        cap = period * int(g.integers(8, 20))
+        B = int(g.integers(1, 6))
+        k = int(g.integers(1, 6))
+        pad = int(g.integers(0, 2))
+        ring = make_ring(5000 + cfg, cap=cap, B=B, ep_len=float(g.uniform(3, 30)), period=period, rnn_h=4,
+                         reward_kind="r2d2", obs_shape=(4, 8))
+        dr = dev_ring(rpl, ring)
+        if cfg % 2:
+            L = int(g.integers(1, 3 * period))
+            if not any(OG.window_valid_sequence(b * period, cap, ring.cursor, ring.size, k, L) for b in range(cap // period)):
+                continue
+            idx = []
+            while len(idx) < 400:
+                blk, b = int(g.integers(0, cap // period)), int(g.integers(0, B))
+                if OG.window_valid_sequence(blk * period, cap, ring.cursor, ring.size, k, L):
+                    idx.append(blk * B + b)
+            idx = np.array(idx, np.int64)
+            om = int(g.integers(0, 2))
+            out = rpl.gather(dr, T_(idx), kind="sequence", k=k, seq_len=L, period=period, pad_mode=pad, out_mode=om)
+            ref = OG.gather_sequences(idx, B, ring.obs, ring.act, ring.rew, ring.done, ring.rnn, k, L, period, pad,
+                                      stacked=(om == 0))
+            for name in ("obs", "act", "prev_act", "rew", "prev_rew", "done", "rnn"):
+                assert np.array_equal(H(out[name]), ref[name]), (cfg, name)
+            total_seq += idx.size
+        else:
+            n = int(g.integers(1, 6))
+            idx = valid_transition_leaves(ring, k, n, 400, g)
+            out = rpl.gather(dr, T_(idx), kind="transition", k=k, n_step=n, gamma=0.97, pad_mode=pad)
+            ref = OG.gather_transitions(idx, B, ring.obs, ring.act, ring.rew, ring.done, k, n, 0.97, pad)
+            assert np.array_equal(H(out["obs"]), ref["obs"]) and np.array_equal(H(out["next_obs"]), ref["next_obs"])
+            assert np.array_equal(H(out["act"]), ref["act"]) and np.array_equal(H(out["done_n"]), ref["done_n"])
+            check_rel(H(out["ret"]), ref["ret"], np.abs(ref["ret"]) + 1.0, what="stress ret")
+            total_tr += idx.size
