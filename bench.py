@@ -384,8 +384,12 @@ def run_rpl(args):
 
     pipelined = None
     if world == 1 and not args.no_secondary and not args.profile:
-        pipelined = pipelined_step(dev, rpl, tree, plan, idx_buf, td_pool, q_pool, r_tr, d_tr, y, dn, err, c, n,
-                                   P, seed, Tn)
+        try:
+            pipelined = pipelined_step(dev, rpl, tree, plan, idx_buf, td_pool, q_pool, r_tr, d_tr, y, dn, err, c, n,
+                                       P, seed, Tn)
+        except Exception as e:  # pragma: no cover
+            pipelined = {"error": f"{type(e).__name__}: {e}"[:300]}
+            torch.cuda.synchronize()
 
     # dominant kernel (sequence gather): average launch duration with CUDA events on
     # the launching stream, over K eager steps of the same workload
@@ -434,15 +438,29 @@ def run_rpl(args):
         result["clocks"] = clk
         result["e2e"] = e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K_eff, world)
     if world == 1 and not args.no_secondary and not args.profile:
-        result["secondary"] = {"r2d2_seeds": seed_sweep(dev, rpl, c, ms / K_eff * 1e3),
-                               "r2d2_pipelined": pipelined, "r2d2_1mseq": bench_r2d2_1mseq(dev, rpl, c),
-                               "r2d2_unique_output": unique_output_step(dev, rpl, tree, ring, idx_buf, td_pool, q_pool,
-                                                                        err, c, n, P, seed),
-                               "tree_latency": tree_latency(dev, rpl),
-                               "ppo_returns": bench_ppo(dev, rpl), "dqn_replay": bench_dqn(dev, rpl),
-                               "mujoco_replay": bench_mujoco(dev, rpl)}
+        # each secondary is isolated: a failure is reported in its slot, never loses the line
+        jobs = [("r2d2_seeds", lambda: seed_sweep(dev, rpl, c, ms / K_eff * 1e3)),
+                ("r2d2_pipelined", lambda: pipelined),
+                ("r2d2_1mseq", lambda: bench_r2d2_1mseq(dev, rpl, c)),
+                ("r2d2_unique_output", lambda: unique_output_step(dev, rpl, tree, ring, idx_buf, td_pool, q_pool, err,
+                                                                  c, n, P, seed)),
+                ("tree_latency", lambda: tree_latency(dev, rpl)),
+                ("ppo_returns", lambda: bench_ppo(dev, rpl)),
+                ("dqn_replay", lambda: bench_dqn(dev, rpl)),
+                ("mujoco_replay", lambda: bench_mujoco(dev, rpl))]
+        result["secondary"] = {}
+        for name, fn in jobs:
+            try:
+                result["secondary"][name] = fn()
+            except Exception as e:  # pragma: no cover
+                result["secondary"][name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+                torch.cuda.synchronize()
+                torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
-        result["cpu_baseline"] = cpu_baseline(c, host, args.cpu_seconds)
+        try:
+            result["cpu_baseline"] = cpu_baseline(c, host, args.cpu_seconds)
+        except Exception as e:  # pragma: no cover
+            result["cpu_baseline"] = {"error": f"{type(e).__name__}: {e}"[:300], "kind": "oracle"}
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:
