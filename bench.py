@@ -389,7 +389,6 @@ def run_rpl(args):
                                        P, seed, Tn)
         except Exception as e:  # pragma: no cover
             pipelined = {"error": f"{type(e).__name__}: {e}"[:300]}
-            torch.cuda.synchronize()
 
     # dominant kernel (sequence gather): average launch duration with CUDA events on
     # the launching stream, over K eager steps of the same workload
@@ -454,8 +453,11 @@ def run_rpl(args):
                 result["secondary"][name] = fn()
             except Exception as e:  # pragma: no cover
                 result["secondary"][name] = {"error": f"{type(e).__name__}: {e}"[:300]}
-                torch.cuda.synchronize()
-                torch.cuda.empty_cache()
+                try:
+                    torch.cuda.synchronize()
+                    torch.cuda.empty_cache()
+                except Exception:  # pragma: no cover  (sticky CUDA error: skip the rest)
+                    break
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         try:
             result["cpu_baseline"] = cpu_baseline(c, host, args.cpu_seconds)
