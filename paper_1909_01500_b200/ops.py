@@ -349,6 +349,21 @@ class SumTree:
     def rebuild(self):
         check(lib.rpl_sumtree_rebuild(self._lp, _ptr(self.storage), self._s()), "rpl_sumtree_rebuild")
 
+    # ---- checkpoint / resume: leaves + header are the state; internal nodes are
+    # recomputed exactly from the leaves (int64 sums) by rpl_sumtree_rebuild
+    def state_dict(self):
+        return {"n_leaves": self.n_leaves, "fanout": self.fanout, "frac_bits": self.frac_bits,
+                "leaves": self.leaves.detach().cpu().clone(), "header": self.header.detach().cpu().clone()}
+
+    def load_state_dict(self, sd):
+        if (int(sd["n_leaves"]), int(sd["fanout"]), int(sd["frac_bits"])) != (self.n_leaves, self.fanout,
+                                                                            self.frac_bits):
+            raise ValueError("tree geometry mismatch")
+        self.storage.zero_()
+        self.leaves.copy_(sd["leaves"].to(self.device))
+        self.header.copy_(sd["header"].to(self.device))
+        self.rebuild()
+
 
 # ---------------------------------------------------------------- gather
 @dataclass
