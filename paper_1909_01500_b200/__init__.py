@@ -5,6 +5,10 @@ torch binding with the ABI's names; `replay` holds the host-side shard logic.
 Importing the package loads librpl.so and fails loudly if it is missing.
 """
 from . import _lib  # noqa: F401  (loads librpl.so or raises)
-from .ops import *  # noqa: F401,F403
+from . import nvtx as _nvtx
+from . import ops as _ops
+
+_nvtx.install(_ops)  # RPL_NVTX=1: NVTX range per binding call (no-op otherwise)
+from .ops import *  # noqa: E402,F401,F403
 
 __version__ = "0.1.0"
