@@ -1423,6 +1423,167 @@ int launch_seq_ldg_bulk(const GDesc& g, const int64_t* idx, int64_t n, int NS, i
                     rows_per_cta, q, qmin, beta, dev_err);
 }
 
+// ---------------------------------------------------------------------------
+// Transitions, persistent pipeline (large batches, n >= 2 x SMs): a CTA owns a run of
+// samples; warp 0 lane 0 streams each sample's k+n unique frames (TMA, evict-first) into
+// one of SPF slot groups (one mbarrier per group), warp 1 resolves every sample's stack
+// sources (episode starts, §8c #13) and writes the scalars (action, fused n-step return,
+// done_n, IS weight), and the consumer warps expand the two k-stacks of each sample
+// (obs at window k-1, next obs at k-1+n, §8c #14) with 16-B streaming stores.  A sample's
+// slot group is refilled once both of its stacks are written.  Same outputs as
+// k_gather_transition (which keeps small batches: one latency chain per sample).
+// ---------------------------------------------------------------------------
+constexpr int TP_MAX_S = 64;  // samples per CTA
+constexpr int TP_MAX_G = 8;   // slot groups (samples in flight)
+
+template <int NC>
+__global__ void __launch_bounds__((NC + 2) * 32, 1)
+k_gather_trans_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int SPF, int spc,
+                    const int64_t* __restrict__ q, const int64_t* __restrict__ qmin, double beta, int32_t* err) {
+  extern __shared__ __align__(128) uint8_t smem[];  // SPF groups of NR frame slots
+  __shared__ __align__(8) uint64_t full[TP_MAX_G];
+  __shared__ int s_b[TP_MAX_S];            // ring column, -1: skipped sample
+  __shared__ int s_r[TP_MAX_S];            // ring row of the transition
+  __shared__ int8_t ssl[TP_MAX_S][2][8];   // stack slot -> window index (-1: zero)
+  __shared__ volatile int sdone[TP_MAX_S]; // stacks written (0..2)
+  constexpr int NT = (NC + 2) * 32;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int k = D.k, ns = D.n_step, NR = k + ns;
+  const int ob = (int)D.obs_bytes;
+  const int nv = ob / 16;
+  const int cap = (int)D.cap_T, Bc = (int)D.B;
+  pdl_wait();
+  const int64_t n_eff = active_n(D, n);
+  const int64_t coff = col_off(D);
+  const int64_t s0 = (int64_t)blockIdx.x * spc;
+  const int64_t s1 = min(n_eff, s0 + spc);
+  if (s0 >= s1) return;
+  const int nsm = (int)(s1 - s0);
+  if (tid == 0) {
+    for (int i = 0; i < SPF; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+  }
+  for (int j = tid; j < nsm; j += NT) {
+    const int64_t leaf = idx[s0 + j];
+    int bcol = -1, row = 0;
+    if (leaf >= 0 && leaf < (int64_t)cap * Bc) {
+      row = (int)(leaf / Bc);
+      bcol = (int)(leaf - (int64_t)row * Bc);
+      const int64_t age = wrap(D.cursor - 1 - row, D.cap_T);
+      if (!(age >= ns && age <= D.size - k)) set_err(err, RPL_DERR_INVALID_LEAF);
+    } else if (leaf >= (int64_t)cap * Bc) {
+      set_err(err, RPL_DERR_IDX);
+    }
+    s_b[j] = bcol;
+    s_r[j] = row;
+    sdone[j] = bcol < 0 ? 2 : 0;
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- producer ----------------
+      const int64_t rstride = (int64_t)Bc * ob;
+      for (int j = 0; j < nsm; ++j) {
+        const int bcol = s_b[j];
+        if (bcol < 0) continue;
+        const int grp = j % SPF;
+        if (j >= SPF) {
+          while (flag_acquire(&sdone[j - SPF]) < 2) __nanosleep(20);
+          fence_proxy_async();
+          mbar_wait(&full[grp], (uint32_t)(((j / SPF) - 1) & 1));  // previous phase completed
+        }
+        mbar_expect_tx(&full[grp], (uint32_t)(NR * ob));
+        int row = s_r[j] - (k - 1);
+        while (row < 0) row += cap;
+        const uint8_t* col = D.obs + (int64_t)bcol * ob;
+        for (int w = 0; w < NR; ++w) {
+          bulk_g2s_evict_first(smem + (grp * NR + w) * ob, col + (int64_t)row * rstride, (uint32_t)ob, &full[grp]);
+          if (++row == cap) row = 0;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- meta: stack sources, then scalars ----------------
+    for (int j = lane; j < nsm; j += 32) {
+      const int bcol = s_b[j];
+      if (bcol < 0) continue;
+      uint8_t dw[32];  // dw[w] = done[first + w - 1], w = 0..NR
+      int rr = s_r[j] - k;
+      while (rr < 0) rr += cap;
+      for (int w = 0; w <= NR; ++w) {
+        dw[w] = __ldg(D.done + (int64_t)rr * Bc + bcol);
+        if (++rr == cap) rr = 0;
+      }
+      for (int which = 0; which < 2; ++which)
+        for (int jj = 0; jj < k; ++jj) ssl[j][which][jj] = (int8_t)stack_src(dw, (k - 1) + which * ns, jj, k, D.pad_mode);
+    }
+    __threadfence_block();
+    asm volatile("bar.arrive 1, %0;" ::"n"((NC + 1) * 32) : "memory");
+    const int64_t qm = (D.o_w && q) ? warp_batch_qmin(qmin, idx, q, n) : 0;
+    for (int j = lane; j < nsm; j += 32) {
+      const int bcol = s_b[j];
+      if (bcol < 0) continue;
+      const int64_t sc = coff + s0 + j;
+      const int64_t r = s_r[j];
+      if (D.o_act) coop_copy(D.o_act + sc * D.act_bytes, D.act + (r * Bc + bcol) * D.act_bytes, D.act_bytes, 0, 1);
+      if (D.o_ret || D.o_done_n) {
+        float rb[32];
+        uint8_t db[32];
+        int64_t row = r;
+        for (int i = 0; i < ns; ++i) {  // all n rows in flight before the recurrence
+          rb[i] = __ldg(D.rew + row * Bc + bcol);
+          db[i] = __ldg(D.done + row * Bc + bcol);
+          if (++row == cap) row = 0;
+        }
+        double acc = 0.0;
+        uint8_t dn = 0;
+        for (int i = ns - 1; i >= 0; --i) {  // Horner (R24)
+          acc = db[i] ? (double)rb[i] : fma(D.gamma, acc, (double)rb[i]);
+          dn |= db[i];
+        }
+        if (D.o_ret) D.o_ret[sc] = (float)acc;
+        if (D.o_done_n) D.o_done_n[sc] = dn ? 1 : 0;
+      }
+      if (D.o_w && q) {
+        const int64_t qs = q[s0 + j];
+        D.o_w[sc] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
+      }
+    }
+  } else {
+    // ---------------- consumers: one k-stack per item (sample, which) ----------------
+    asm volatile("bar.sync 1, %0;" ::"n"((NC + 1) * 32) : "memory");
+    for (int it = warp - 2; it < 2 * nsm; it += NC) {
+      const int j = it >> 1, which = it & 1;
+      if (s_b[j] < 0) continue;
+      uint8_t* outb = which ? D.o_next_obs : D.o_obs;
+      if (outb) {
+        const int grp = j % SPF;
+        mbar_wait(&full[grp], (uint32_t)((j / SPF) & 1));
+        int4* dst = reinterpret_cast<int4*>(outb + (coff + s0 + j) * (int64_t)k * ob);
+        for (int jj = 0; jj < k; ++jj) {
+          int4* d = dst + jj * nv;
+          const int src = ssl[j][which][jj];
+          if (src < 0) {
+            for (int v = lane; v < nv; v += 32) __stcs(d + v, make_int4(0, 0, 0, 0));
+          } else {
+            const int4* sp = reinterpret_cast<const int4*>(smem + (grp * NR + src) * ob);
+#pragma unroll 4
+            for (int v = lane; v < nv; v += 32) __stcs(d + v, sp[v]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        fence_proxy_async();
+        asm volatile("red.release.cta.shared::cta.add.s32 [%0], 1;" ::"r"(smem_u32((const void*)&sdone[j]))
+                     : "memory");
+      }
+    }
+  }
+  pdl_trigger();
+}
+
 int env_diag() {
   const char* v = getenv("RPL_GATHER_DIAG");  // measurement only (rpl_debug_set_gather_diag)
   return v ? atoi(v) : 0;
@@ -1516,6 +1677,20 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
     if (desc->n_step < 1 || desc->k + desc->n_step > 31) return RPL_EINVAL;
     if ((desc->o_ret || desc->o_done_n) && !desc->rew) return RPL_EINVAL;
     const int NR = desc->k + desc->n_step;
+    // large batches: persistent pipeline (several samples per CTA, loads overlapping stores)
+    if (tma_ok && seq_variant != 1 && n >= 2 * (int64_t)sm_count() && NR <= 30 && desc->k <= 8) {
+      int SPF = (int)(200 * 1024 / ((int64_t)NR * desc->obs_bytes));
+      if (SPF > TP_MAX_G) SPF = TP_MAX_G;
+      int64_t spc = (n + sm_count() - 1) / sm_count();
+      if (SPF >= 2 && spc <= TP_MAX_S) {
+        const size_t dyn = (size_t)SPF * NR * desc->obs_bytes;
+        ensure_smem(reinterpret_cast<const void*>(k_gather_trans_pipe<8>), dyn);
+        const int64_t grid = (n + spc - 1) / spc;
+        g.use_tma = 1;
+        return launch_pdl(k_gather_trans_pipe<8>, dim3((unsigned)grid), dim3(10 * 32), dyn, st, g, idx, n, SPF,
+                          (int)spc, q, qmin, beta, dev_err);
+      }
+    }
     const int64_t smem = (int64_t)(NR + 1) * desc->obs_bytes;
     g.use_tma = (tma_ok && smem <= 200 * 1024) ? 1 : 0;
     const size_t dyn = g.use_tma ? (size_t)smem : 0;

@@ -322,12 +322,12 @@ def test_sequence_n_active(rpl, variant):
     assert np.array_equal(H(out["rnn"])[:, :m], ref["rnn"])
 
 
-def test_transition_n_active(rpl):
+@pytest.mark.parametrize("nn,m", [(50, 23), (400, 333)])  # 400: the persistent pipeline path
+def test_transition_n_active(rpl, nn, m):
     import torch
     ring = make_ring(92, cap=64, B=8, ep_len=9.0)
     dr = dev_ring(rpl, ring)
-    idx = valid_transition_leaves(ring, 4, 3, 50, rng(10))
-    m = 23
+    idx = valid_transition_leaves(ring, 4, 3, nn, rng(10))
     plan = rpl.GatherPlan(dr, idx.size, kind="transition", k=4, n_step=3, gamma=0.99)
     for t in plan.outputs.values():
         t.zero_()
