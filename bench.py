@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget (cpu_baseline)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/baseline/e2e)")
+    ap.add_argument("--tree-fused", type=int, default=0, choices=[0, 1],
+                    help="1 GPU: priority update + sampling as one launch (rpl_sumtree_update_sample; "
+                         "measured 1.7 us/step slower than the PDL-chained pair)")
     ap.add_argument("--seq-variant", type=int, default=None, help="diagnostics: sequence-gather kernel variant")
     ap.add_argument("--mode", default="L", choices=["L", "C"],
                     help="N > 1 replay mode (SURVEY §8e): L = owner computes, each rank feeds its own learner; "
@@ -291,14 +294,21 @@ def run_rpl(args):
         cur, prev = idx_buf[i % 2], idx_buf[(i + 1) % 2]
         # (a5-a7) new priorities for the previous batch (entries < 0 — not owned — are skipped, R22)
         # (NEXT-1 fused) sequence priority = eta max + (1 - eta) mean of the 80 per-step |delta| (R26)
-        rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]),
-                                                  c["train"], n_glob, c["eta"], c["alpha"], c["eps_p"], 0, None, s),
-                       "update_seq")
-        if world == 1:
+        if world == 1 and args.tree_fused:
+            # (a5-a8) update + stratified draws in one launch (grid barrier between them);
+            # the batch-min normaliser and IS weights (a9) are fused into the gather
+            rpl._lib.check(lib.rpl_sumtree_update_sample(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]),
+                                                         c["train"], n_glob, c["eta"], c["alpha"], c["eps_p"], 0, n,
+                                                         seed, P_(cur), P_(q_buf), P_(err), s), "update_sample")
+        else:
+            rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]),
+                                                      c["train"], n_glob, c["eta"], c["alpha"], c["eps_p"], 0, None,
+                                                      s), "update_seq")
+        if world == 1 and not args.tree_fused:
             # (a8) draws only; the batch-min normaliser and IS weights (a9) are fused into the gather
             rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, seed, c["beta"], P_(cur),
                                                          P_(q_buf), None, None, P_(err), s), "sample")
-        else:
+        elif world > 1:
             rpl._lib.check(lib.rpl_sumtree_total(tree._lp, P_(tree.storage), P_(my_total), s), "total")
             all_gather_totals()                                                  # K5: 8 B per rank
             rpl._lib.check(lib.rpl_sumtree_sample_sharded(tree._lp, P_(tree.storage), rank, world, n_leaves,
@@ -423,7 +433,9 @@ def run_rpl(args):
         "dtype": "u8 frames + f32 (fp64 accum) + int64 tree",
         "data": "synthetic (seeded; uniform-random 84x84 u8 frames, R2D2 reward/episode recipe, DESIGN.md)",
         "config": dict(r2d2_config(c, world, args.mode),
-                       timing="cuda graph of 8 steps, replayed" if use_graph else "eager launches"),
+                       timing="cuda graph of 8 steps, replayed" if use_graph else "eager launches",
+                       tree=("update+sample fused (rpl_sumtree_update_sample)" if world == 1 and args.tree_fused
+                             else "update_seq, then sample")),
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "k_gather_seq_pipe_lsu", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,

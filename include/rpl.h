@@ -107,7 +107,8 @@ int rpl_value_rescale(const float* x, float* y, int64_t n, double eps, int32_t i
  *     level_off[depth] + i and holds q_i = round_half_even(RN32(p_i^alpha) * 2^F)
  *     (§8c #7).  Header: [hdr_off+0] max-priority-seen, [hdr_off+1] sampler
  *     ticket (library scratch, always 0 between calls), [hdr_off+2] Philox stream
- *     position used by rpl_sumtree_sample_stream (0 after init).
+ *     position used by rpl_sumtree_sample_stream (0 after init), [hdr_off+3] grid-barrier
+ *     arrivals (scratch, 0 between calls), [hdr_off+4] grid-barrier generation (scratch).
  * ========================================================================= */
 typedef struct {
   int64_t n_leaves;
@@ -185,6 +186,19 @@ int rpl_sumtree_sample(const rpl_tree_layout* L, int64_t* tree, int64_t n, const
 int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree, int64_t n, uint64_t seed,
                               double beta, int64_t* out_idx, int64_t* out_q, int64_t* out_qmin,
                               float* out_w, int32_t* dev_err, void* stream);
+
+/* One learner step's tree work as ONE launch: the priority update of the previous batch,
+ * then stream sampling of the next — exactly rpl_sumtree_update_seq (T_p >= 1: td is the
+ * time-major [T_p, n_upd] per-step |delta|, eta the max/mean mix) or rpl_sumtree_update_ex
+ * (T_p == 0: td is [n_upd] |delta|; eta ignored), followed by rpl_sumtree_sample_stream
+ * with out_qmin = out_w = NULL (results bit-identical to that pair).  n_upd == 0 samples
+ * only.  flags: RPL_UPD_LIVE_ONLY.  The update runs on one CTA; all CTAs (at most one per
+ * SM, so all co-resident) then meet at a grid barrier kept in header words 3-4.  A tree
+ * must not be used by two of these calls concurrently (as for every tree write). */
+int rpl_sumtree_update_sample(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, const float* td,
+                              int64_t T_p, int64_t n_upd, double eta, double alpha, double eps_p, int32_t flags,
+                              int64_t n, uint64_t seed, int64_t* out_idx, int64_t* out_q, int32_t* dev_err,
+                              void* stream);
 
 /* Sampling WITHOUT replacement (§8f NEXT-4, reading R32): n successive proportional draws,
  * each over the leaves not drawn yet — draw k: prefix_k = floor(u_k * Q_k / 2^64) with Q_k the

@@ -64,23 +64,33 @@ __device__ __forceinline__ uint32_t hash_slot(int64_t leaf) {
   return (uint32_t)(((unsigned long long)leaf * 0x9E3779B97F4A7C15ull) >> 53) & (HASH_SLOTS - 1);
 }
 
-__global__ void __launch_bounds__(UPD_THREADS)
-k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__ idx,
-              const float* __restrict__ td, const int64_t* __restrict__ qin, int mode, int64_t n,
-              double alpha, double eps_p, int32_t* err, int force_slow, int64_t T_p, double eta, int live_only) {
-  __shared__ unsigned long long hkey[HASH_SLOTS];
-  __shared__ int hval[HASH_SLOTS];
-  __shared__ int64_t sred[UPD_THREADS / 32];
-  __shared__ float s_td[UPD_THREADS];  // MODE_SEQ: this chunk's sequence priorities
+struct UpdSmem {
+  unsigned long long hkey[HASH_SLOTS];
+  int hval[HASH_SLOTS];
+  int64_t sred[UPD_THREADS / 32];
+  float s_td[UPD_THREADS];  // MODE_SEQ: this chunk's sequence priorities
+};
+
+// The whole batch update by ONE block of NT threads (NT <= UPD_THREADS, a multiple of 32;
+// every thread must call): entries are processed in chunks of NT in batch order.
+template <int NT>
+__device__ __forceinline__ void tree_update_block(UpdSmem& S, const TreeDev& L, int64_t* __restrict__ tree,
+                                                  const int64_t* __restrict__ idx, const float* __restrict__ td,
+                                                  const int64_t* __restrict__ qin, int mode, int64_t n, double alpha,
+                                                  double eps_p, int32_t* err, int force_slow, int64_t T_p, double eta,
+                                                  int live_only) {
+  unsigned long long* hkey = S.hkey;
+  int* hval = S.hval;
+  int64_t* sred = S.sred;
+  float* s_td = S.s_td;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   int64_t* leaves = tree + L.level_off[L.depth];
   int64_t* hdr = tree + L.hdr_off;
-  pdl_wait();
   // Issue the first chunk's loads — the entry, and for a single-chunk batch the leaf's
   // current value — before the hash-table reset and the priority transform, so their
   // latency overlaps that work instead of sitting on the critical path.
-  const bool single = n <= UPD_THREADS;
+  const bool single = n <= NT;
   int64_t pre_leaf = -1, pre_old = 0;
   float pre_td = 0.0f;
   if (tid < n) {
@@ -92,14 +102,14 @@ k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__
   int64_t local_max = INT64_MIN;
   int32_t errbits = 0;
 
-  for (int64_t base = 0; base < n; base += UPD_THREADS) {
-    for (int s = tid; s < HASH_SLOTS; s += UPD_THREADS) {
+  for (int64_t base = 0; base < n; base += NT) {
+    for (int s = tid; s < HASH_SLOTS; s += NT) {
       hkey[s] = HASH_EMPTY;
       hval[s] = -1;
     }
     if (mode == MODE_SEQ) {  // this chunk's sequence priorities, 8 lanes per sequence
-      const int64_t cnt = min((int64_t)UPD_THREADS, n - base);
-      for (int64_t r0 = 0; r0 < cnt; r0 += UPD_THREADS / 8) {
+      const int64_t cnt = min((int64_t)NT, n - base);
+      for (int64_t r0 = 0; r0 < cnt; r0 += NT / 8) {
         const int64_t jj = r0 + (tid >> 3);
         const float v = sequence_td8(td, T_p, n, base + jj, jj < cnt, eta);
         if ((tid & 7) == 0 && jj < cnt) s_td[jj] = v;
@@ -184,11 +194,21 @@ k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__
   if (lane == 0) sred[tid >> 5] = m;
   __syncthreads();
   if (tid < 32) {
-    m = tid < UPD_THREADS / 32 ? sred[tid] : INT64_MIN;
+    m = tid < NT / 32 ? sred[tid] : INT64_MIN;
     m = warp_max64(m);
     if (tid == 0 && m > maxseen_now) atomicMax(reinterpret_cast<long long*>(hdr), (long long)m);
   }
   if (errbits) set_err(err, errbits);
+}
+
+__global__ void __launch_bounds__(UPD_THREADS)
+k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__ idx,
+              const float* __restrict__ td, const int64_t* __restrict__ qin, int mode, int64_t n,
+              double alpha, double eps_p, int32_t* err, int force_slow, int64_t T_p, double eta, int live_only) {
+  __shared__ UpdSmem S;
+  pdl_wait();
+  tree_update_block<UPD_THREADS>(S, L, tree, idx, td, qin, mode, n, alpha, eps_p, err, force_slow, T_p, eta,
+                                 live_only);
 }
 
 __device__ __forceinline__ uint64_t stratum_lo(uint64_t k, uint64_t Q, uint64_t n) {
@@ -391,6 +411,84 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
       out_w[j] = qj > 0 ? (float)pow((double)qmin / (double)qj, beta) : 0.0f;
     }
   }
+}
+
+// Fused priority update + stream sampling (rpl_sumtree_update_sample): the two calls of a
+// learner step as ONE launch.  CTA 0 runs the whole update (tree_update_block, 256 threads,
+// batch order preserved); every CTA reads the stream position, then all CTAs meet at a
+// grid barrier (header words 3 = arrivals, 4 = generation; sense reversal, so any grid
+// size works), and each warp descends for one stratum of the UPDATED tree.  The grid is
+// capped at the SM count, so all CTAs are co-resident and the spin barrier cannot starve.
+// Result: identical to rpl_sumtree_update(_seq) followed by rpl_sumtree_sample_stream with
+// out_qmin = out_w = NULL.  Measured (R2D2 step, B200): the pair is FASTER — 8.2 us for
+// update_seq + sample_stream against 9.2 us fused, the grid barrier's atomic round trips
+// costing more than the PDL kernel boundary — so bench.py keeps the pair by default
+// (--tree-fused 1 selects this); the entry point is for callers launching without PDL.
+__device__ __forceinline__ void grid_barrier(int64_t* hdr) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(hdr + 3);
+    unsigned long long* gen = reinterpret_cast<unsigned long long*>(hdr + 4);
+    unsigned long long g;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(g) : "l"(gen) : "memory");
+    __threadfence();  // this CTA's tree writes before its arrival
+    const unsigned long long t = atomicAdd(cnt, 1ull);
+    if (t == (unsigned long long)gridDim.x - 1) {
+      *cnt = 0ull;
+      __threadfence();
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(gen), "l"(g + 1ull) : "memory");
+    } else {
+      unsigned long long cur;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(gen) : "memory");
+      } while (cur == g);
+    }
+  }
+  __syncthreads();
+}
+
+// 256 threads: measured 9.2 us for update + sample against 10.2 us with 1024-thread CTAs
+constexpr int FUSED_THREADS = SAMPLE_WARPS * 32;
+constexpr int FUSED_WARPS = FUSED_THREADS / 32;
+
+__global__ void __launch_bounds__(FUSED_THREADS)
+k_tree_update_sample(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__ idx,
+                     const float* __restrict__ td, int64_t n_upd, int64_t T_p, double eta, double alpha, double eps_p,
+                     int live_only, int64_t n, uint64_t seed, int64_t* __restrict__ out_idx,
+                     int64_t* __restrict__ out_q, int32_t* err) {
+  __shared__ UpdSmem S;
+  pdl_wait();
+  int64_t* hdr = tree + L.hdr_off;
+  uint64_t spos = 0;
+  if (threadIdx.x == 0)
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(spos) : "l"(hdr + 2) : "memory");
+  if (blockIdx.x == 0 && n_upd > 0)
+    tree_update_block<FUSED_THREADS>(S, L, tree, idx, td, nullptr, T_p > 0 ? MODE_SEQ : MODE_TD, n_upd, alpha, eps_p,
+                                     err, 0, T_p, eta, live_only);
+  grid_barrier(hdr);  // orders every CTA's read of hdr[2] before CTA 0 advances it below
+  __shared__ uint64_t s_spos;
+  if (threadIdx.x == 0) s_spos = spos;
+  __syncthreads();
+  spos = s_spos;
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * FUSED_WARPS + (threadIdx.x >> 5);
+  int32_t errbits = 0;
+  const uint64_t Q = (uint64_t)__ldcg(tree + L.level_off[0]);
+  for (int64_t kk = k; kk < n; kk += (int64_t)gridDim.x * FUSED_WARPS) {
+    int64_t leaf = -1, q = 0;
+    if (Q == 0) {
+      errbits |= RPL_DERR_EMPTY;
+    } else {
+      const uint64_t prefix = stratum_prefix(kk, Q, n, nullptr, seed, spos);
+      leaf = descend(L, tree, (int64_t)prefix, &q, &errbits);
+    }
+    if (lane == 0) {
+      out_idx[kk] = leaf;
+      out_q[kk] = q;
+    }
+  }
+  if (lane == 0 && errbits) set_err(err, errbits);
+  if (blockIdx.x == 0 && threadIdx.x == 0) hdr[2] = (int64_t)(spos + (uint64_t)n);  // advance the stream
 }
 
 // Sampling WITHOUT replacement (§8f NEXT-4, reading R32): successive proportional draws —
@@ -782,4 +880,20 @@ extern "C" int rpl_sumtree_sample_unique(const rpl_tree_layout* L, int64_t* tree
   if (!layout_ok(L) || !tree || !out_idx || !out_q || n < 1 || n > (1ll << 30)) return RPL_EINVAL;
   return launch_pdl(k_tree_sample_unique, dim3(1), dim3(32), 0, as_stream(stream), tree_dev(L), tree, n, seed, offset,
                     (int)(use_stream != 0), out_idx, out_q, dev_err);
+}
+
+extern "C" int rpl_sumtree_update_sample(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx,
+                                         const float* td, int64_t T_p, int64_t n_upd, double eta, double alpha,
+                                         double eps_p, int32_t flags, int64_t n, uint64_t seed, int64_t* out_idx,
+                                         int64_t* out_q, int32_t* dev_err, void* stream) {
+  if (!layout_ok(L) || !tree || !out_idx || !out_q || n < 1 || n > (1ll << 30) || n_upd < 0 || T_p < 0)
+    return RPL_EINVAL;
+  if (n_upd > 0 && (!idx || !td)) return RPL_EINVAL;
+  if (!(alpha >= 0.0) || !(eps_p >= 0.0) || !(eta >= 0.0 && eta <= 1.0) || (flags & ~RPL_UPD_LIVE_ONLY))
+    return RPL_EINVAL;
+  int64_t blocks = (n + FUSED_WARPS - 1) / FUSED_WARPS;
+  if (blocks > sm_count()) blocks = sm_count();  // co-residency of the grid barrier
+  return launch_pdl(k_tree_update_sample, dim3((unsigned)blocks), dim3(FUSED_THREADS), 0, as_stream(stream),
+                    tree_dev(L), tree, idx, td, n_upd, T_p, eta, alpha, eps_p, (flags & RPL_UPD_LIVE_ONLY) ? 1 : 0, n,
+                    seed, out_idx, out_q, dev_err);
 }

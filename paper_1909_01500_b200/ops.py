@@ -293,6 +293,35 @@ class SumTree:
                                             self._s()), "rpl_sumtree_sample_stream")
         return idx, q, qmin, w
 
+    def update_sample(self, n, seed, idx=None, td=None, alpha=0.6, eta=0.9, eps_p=1e-3, out=None, err=None,
+                      live_only=False):
+        """rpl_sumtree_update_sample: update (td [T_p, n_upd] -> sequence priorities, or [n_upd]
+        -> |delta|) then stream-sample n draws, in one launch.  idx None: sample only.
+        Returns (idx, q)."""
+        n = int(n)
+        if out is None:
+            oi = torch.empty(n, dtype=torch.int64, device=self.device)
+            oq = torch.empty(n, dtype=torch.int64, device=self.device)
+        else:
+            oi, oq = out
+        n_upd, T_p = 0, 0
+        if idx is not None:
+            _req(idx, torch.int64, "idx")
+            _req(td, torch.float32, "td")
+            n_upd = idx.numel()
+            if td.dim() == 2:
+                T_p = td.shape[0]
+                if td.shape[1] != n_upd:
+                    raise ValueError("td must be [T_p, n_upd] or [n_upd]")
+            elif td.numel() != n_upd:
+                raise ValueError("td must be [T_p, n_upd] or [n_upd]")
+        e = self.err if err is None else err
+        check(lib.rpl_sumtree_update_sample(self._lp, _ptr(self.storage), _ptr(idx), _ptr(td), T_p, n_upd,
+                                            float(eta), float(alpha), float(eps_p), 1 if live_only else 0, n,
+                                            int(seed) & (2 ** 64 - 1), _ptr(oi), _ptr(oq), _ptr(e), self._s()),
+              "rpl_sumtree_update_sample")
+        return oi, oq
+
     def sample_sharded(self, rank, n_shards, shard_totals, n, draws=None, seed=0, offset=0, out=None, err=None,
                        use_stream=False, count=None):
         """rpl_sumtree_sample_sharded.  count (2-element int64 CUDA tensor) selects the compacted

@@ -27,24 +27,30 @@ qv = torch.randn((8, L, n), device=dev)
 err = torch.zeros(1, dtype=torch.int32, device=dev)
 Tn = 84
 res = {}
-for mode in (0, 1):
-    plan = rpl.GatherPlan(ring, n, kind="sequence", k=k, seq_len=L, period=period, with_weights=True, out_mode=mode)
-    out = plan.outputs
-    y = torch.empty((80, n), device=dev)
-    dn = torch.empty((80, n), dtype=torch.uint8, device=dev)
-    for upto in range(1, 5):
-        def step(i):
-            s = rpl.ops._stream(dev)
-            rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(idx[(i + 1) % 2]),
-                                                      P_(td[i % 8]), 80, n, 0.9, 0.9, 1e-3, 0, None, s), "u")
-            if upto >= 2:
-                rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, 5, 0.6, P_(idx[i % 2]),
-                                                             P_(q), None, None, P_(err), s), "s")
-            if upto >= 3:
-                plan.run(idx[i % 2], q=q, beta=0.6, err=err, stream=s)
-            if upto >= 4:
-                rpl._lib.check(lib.rpl_returns_nstep(P_(out["rew"][40:124]), P_(out["done"][40:124]), Tn, n, 5, 0.997,
-                                                     P_(qv[i % 8][40:124]), P_(qv[i % 8][124]), 1, 1e-3, P_(y),
-                                                     P_(dn), s), "n")
-        res[f"{'stacked' if mode == 0 else 'unique'}_upto{upto}"] = round(bench._graph_time(dev, step, P=8, reps=50) * 1e3, 2)
+for fused in (0, 1):
+    for mode in ((0, 1) if not fused else (0,)):
+        plan = rpl.GatherPlan(ring, n, kind="sequence", k=k, seq_len=L, period=period, with_weights=True, out_mode=mode)
+        out = plan.outputs
+        y = torch.empty((80, n), device=dev)
+        dn = torch.empty((80, n), dtype=torch.uint8, device=dev)
+        for upto in range(2 if fused else 1, 5):
+            def step(i):
+                s = rpl.ops._stream(dev)
+                if fused:  # rpl_sumtree_update_sample: update + sample in one launch
+                    rpl._lib.check(lib.rpl_sumtree_update_sample(tree._lp, P_(tree.storage), P_(idx[(i + 1) % 2]),
+                                                                 P_(td[i % 8]), 80, n, 0.9, 0.9, 1e-3, 0, n, 5,
+                                                                 P_(idx[i % 2]), P_(q), P_(err), s), "us")
+                else:
+                    rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(idx[(i + 1) % 2]),
+                                                              P_(td[i % 8]), 80, n, 0.9, 0.9, 1e-3, 0, None, s), "u")
+                if upto >= 2 and not fused:
+                    rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, 5, 0.6, P_(idx[i % 2]),
+                                                                 P_(q), None, None, P_(err), s), "s")
+                if upto >= 3:
+                    plan.run(idx[i % 2], q=q, beta=0.6, err=err, stream=s)
+                if upto >= 4:
+                    rpl._lib.check(lib.rpl_returns_nstep(P_(out["rew"][40:124]), P_(out["done"][40:124]), Tn, n, 5, 0.997,
+                                                         P_(qv[i % 8][40:124]), P_(qv[i % 8][124]), 1, 1e-3, P_(y),
+                                                         P_(dn), s), "n")
+            res[f"{'fused_' if fused else ''}{'stacked' if mode == 0 else 'unique'}_upto{upto}"] = round(bench._graph_time(dev, step, P=8, reps=50) * 1e3, 2)
 print(json.dumps(res, indent=1))

@@ -81,6 +81,12 @@ def test_host_validation_without_gpu(lib):
     assert L.rpl_replay_validity(ctypes.byref(lay), 1, 0, 4096, 255, 4, 3, 1, 1, 0, 0, 1, 1, None) == -1  # N mismatch
     assert L.rpl_ring_append(None, None, None, None, None, None, 1, None) == -1
     assert L.rpl_sumtree_update_ex(ctypes.byref(lay), None, None, None, 4, 0.9, 1e-3, 2, None, None) == -1
+    us = L.rpl_sumtree_update_sample
+    assert us(ctypes.byref(lay), None, None, None, 0, 0, 0.9, 0.9, 1e-3, 0, 64, 1, None, None, None, None) == -1
+    assert us(ctypes.byref(lay), 1, None, None, 0, 4, 0.9, 0.9, 1e-3, 0, 64, 1, 1, 1, None, None) == -1  # no idx/td
+    assert us(ctypes.byref(lay), 1, None, None, 0, 0, 1.5, 0.9, 1e-3, 0, 64, 1, 1, 1, None, None) == -1  # eta
+    assert us(ctypes.byref(lay), 1, None, None, 0, 0, 0.9, 0.9, 1e-3, 4, 64, 1, 1, 1, None, None) == -1  # flags
+    assert us(ctypes.byref(lay), 1, None, None, 0, 0, 0.9, 0.9, 1e-3, 0, 0, 1, 1, 1, None, None) == -1   # n
     assert L.rpl_debug_set_gather_variant(99) == -1 and L.rpl_debug_set_gather_diag(99) == -1
 
 

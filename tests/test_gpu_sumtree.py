@@ -521,3 +521,76 @@ def test_checkpoint_resume(rpl):
     a = t.sample_stream(64, 3)
     b = u.sample_stream(64, 3)
     assert np.array_equal(H(a[0]), H(b[0])) and np.array_equal(H(a[1]), H(b[1]))
+
+
+@pytest.mark.parametrize("T_p,n_upd,n,live", [(80, 64, 64, False), (0, 300, 200, False), (12, 1500, 5000, True),
+                                              (80, 0, 64, False), (33, 64, 7, True)])
+def test_update_sample_fused(rpl, T_p, n_upd, n, live):
+    # rpl_sumtree_update_sample == update(_seq) then sample_stream (no reduction), and both
+    # == the oracle: tree bit-exact, draws from the stream position the pair would use
+    g = rng(T_p * 7 + n_upd + n)
+    N = 25600
+    a, b = rpl.SumTree(N, 32), rpl.SumTree(N, 32)
+    orc = OS.SumTreeOracle(N)
+    base = np.arange(0, N, 2, dtype=np.int64)
+    td0 = td_abs(g, base.size)
+    for t in (a, b):
+        t.update(T_(base), T_(td0), 0.9)
+    orc.update([int(x) for x in base], [float(x) for x in td0], 0.9)
+    pos = 0
+    for step in range(3):
+        idx = g.integers(0, N, max(n_upd, 1)).astype(np.int64)[:n_upd]
+        if T_p:
+            td = np.abs(g.lognormal(0, 2, (T_p, n_upd))).astype(np.float32)
+            mix = [OPR.sequence_td(td[:, k], 0.9) for k in range(n_upd)]
+        else:
+            td = (td_abs(g, n_upd) * 3).astype(np.float32)
+            mix = [float(x) for x in td]
+        if n_upd:
+            ia, qa = a.update_sample(n, 11, idx=T_(idx), td=T_(td), alpha=0.9, eta=0.9, live_only=live)
+            if T_p:
+                b.update_seq(T_(idx), T_(td), 0.9, eta=0.9, live_only=live)
+            else:
+                b.update(T_(idx), T_(td), 0.9, live_only=live)
+            orc.update([int(x) for x in idx], mix, 0.9, live_only=live)
+        else:
+            ia, qa = a.update_sample(n, 11)
+        ib, qb, _, _ = b.sample_stream(n, 11, want_qmin=False)
+        ri, rq, _ = orc.sample(n, OP.draws_u64(11, pos, n))
+        pos += n
+        assert np.array_equal(H(ia), H(ib)) and np.array_equal(H(qa), H(qb))
+        assert H(ia).tolist() == list(ri) and H(qa).tolist() == list(rq)
+        check_tree_consistent(a, orc)
+        ha, hb = H(a.header), H(b.header)
+        assert np.array_equal(ha[:4], hb[:4]) and int(ha[2]) == pos and int(ha[3]) == 0  # barrier count reset
+    assert np.array_equal(H(a.storage)[:a.layout.hdr_off], H(b.storage)[:b.layout.hdr_off])
+
+
+def test_update_sample_graph_replay(rpl):
+    # captured in a CUDA graph, every replay advances the stream and re-arms the grid barrier
+    import torch
+    N = 4096
+    t, r = rpl.SumTree(N, 32), rpl.SumTree(N, 32)
+    g = rng(3)
+    td = T_(td_abs(g, N))
+    ii = T_(np.arange(N, dtype=np.int64))
+    t.update(ii, td, 0.6)
+    r.update(ii, td, 0.6)
+    uidx = T_(g.integers(0, N, 64).astype(np.int64))
+    utd = T_(np.abs(g.normal(size=(20, 64))).astype(np.float32))
+    oi = torch.empty(64, dtype=torch.int64, device="cuda")
+    oq = torch.empty_like(oi)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        t.update_sample(64, 5, idx=uidx, td=utd, alpha=0.6, out=(oi, oq))  # warm-up (step 0)
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=s):
+        t.update_sample(64, 5, idx=uidx, td=utd, alpha=0.6, out=(oi, oq))
+    for step in range(4):
+        if step:
+            gr.replay()
+        torch.cuda.synchronize()
+        r.update_seq(uidx, utd, 0.6, eta=0.9)
+        ri, rq, _, _ = r.sample_stream(64, 5, want_qmin=False)
+        assert np.array_equal(H(oi), H(ri)) and np.array_equal(H(oq), H(rq)), step
