@@ -98,3 +98,47 @@ def c51_targets(p_target, q_online, R, done_n, gamma_n, v_min, v_max):
         g = gamma_n * (1.0 - float(done_n[s]))
         out[s] = c51_project(p_target[s, a], float(R[s]), g, v_min, v_max)
     return out
+
+
+# ---- initial priorities of new samples (§8f NEXT-1; P:123 fn; reading R33) ----------
+#
+# P:123 fn: new samples were first prioritised with 1-step TD errors; results "improved when
+# we corrected to use 5-step TD initial priorities".  SPEC S:660 makes n-step-TD initial
+# priorities the recurrent algorithm's option (default n = 5).  R33: the actor stores, per
+# ring row, q_taken = Q(s_t, a_t) and q_boot = its bootstrap value of s_t (max_a Q, or the
+# double-Q value); the per-step TD error of row t is
+#     delta_t = y_t - q_taken_t,  y_t = the n-step target of row t (R24; rescaled per §8c #5)
+# with the bootstrap q_boot at row t+n; rows are taken modulo the ring capacity.  A sequence
+# leaf's initial priority is the R26 mix (sequence_td) of |delta_t| over its TRAIN rows
+# (block start + burn_in .. + train - 1, all stored once the leaf is valid); a transition
+# leaf's is |delta_t| of its own row.
+
+
+def ring_rows(a, row0, count):
+    """Rows row0 .. row0+count-1 of a ring array [cap_T, ...], modulo cap_T."""
+    a = np.asarray(a)
+    cap = a.shape[0]
+    return a[[(row0 + i) % cap for i in range(count)]]
+
+
+def ring_td_abs(rew, done, q_taken, q_boot, row0, T_out, n, gamma, rescale=False, eps=1e-3):
+    """|delta_t| for t = 0 .. T_out-1 (ring row row0 + t) -> float64 [T_out, B].  The n-step
+    target comes from oracle.returns.nstep_return over the unrolled rows row0 .. row0+T_out+n-1
+    with q = q_boot (row t+n is the bootstrap of output row t)."""
+    rows = T_out + n - 1
+    r = ring_rows(rew, row0, rows).astype(np.float64)
+    d = ring_rows(done, row0, rows)
+    qb = ring_rows(q_boot, row0, rows + 1).astype(np.float64)
+    y, _ = _ret.nstep_return(r, d, n, gamma, q=qb[:rows], q_boot=qb[rows], rescale=rescale, eps=eps)
+    qt = ring_rows(q_taken, row0, T_out).astype(np.float64)
+    return np.abs(y - qt)
+
+
+def initial_sequence_priorities(rew, done, q_taken, q_boot, block, period, burn_in, train, n, gamma, eta,
+                                rescale=True, eps=1e-3):
+    """Per env b: the R26 mix of fp32 |delta_t| over block `block`'s train rows -> list [B]
+    of the |delta| values that then enter the priority transform (sequence_td)."""
+    from . import priority as _pr
+    row0 = block * period + burn_in
+    td = ring_td_abs(rew, done, q_taken, q_boot, row0, train, n, gamma, rescale, eps).astype(np.float32)
+    return [_pr.sequence_td(td[:, b], eta) for b in range(td.shape[1])]
