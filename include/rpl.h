@@ -373,6 +373,13 @@ int rpl_stack_frames(const void* uniq, const int8_t* start, int64_t L, int64_t n
 int rpl_ring_append(const rpl_gather_desc* ring, const void* obs, const void* act, const float* rew,
                     const uint8_t* done, const void* rnn, int64_t T_b, void* stream);
 
+/* Any further per-row ring array (e.g. the actor's q_taken / q_boot for initial priorities,
+ * R33): rows [0, T_b) of a [T_b, row_bytes] source -> ring rows cursor .. cursor+T_b-1
+ * (mod cap_T) of ring_array [cap_T, row_bytes]; at most two cudaMemcpyAsync (host or device
+ * source).  RPL_EINVAL on null pointers, cursor outside [0, cap_T), T_b > cap_T. */
+int rpl_ring_append_rows(void* ring_array, int64_t row_bytes, int64_t cap_T, int64_t cursor, const void* src,
+                         int64_t T_b, void* stream);
+
 /* Tree validity maintenance after the ring moved from (cursor_old, size_old) to
  * (cursor_new, size_new): every leaf (kind TRANSITION: row*B+b with k, n_step; SEQUENCE:
  * block*B+b with k, seq_len, period) whose validity (§8c #2, #16) changed gets q = the
@@ -387,6 +394,23 @@ int rpl_replay_validity(const rpl_tree_layout* L, int64_t* tree, int32_t kind, i
  * (5) Learning targets right after the gather (§8f NEXT-3; P:34 Double-DQN / Categorical,
  *     P:38 n-step).
  * ========================================================================= */
+
+/* Initial priorities of new samples (§8f NEXT-1; P:123 fn "5-step TD initial priorities";
+ * S:660; reading R33): per-step |TD error| read straight from ring arrays.  For t in
+ * [0, T_out), b in [0, B), ring row t' = (row0 + t) mod cap_T:
+ *   y = the n-step target of row t' (rpl_returns_nstep's R24 rule: rewards rows t' .. t'+n-1
+ *       cut after the first done, bootstrap q_boot[t'+n] unless done^n; rescaled per R4/R5
+ *       when rescale != 0), all rows modulo cap_T, fp64;
+ *   out[t, b] = RN32(|y - q_taken[t', b]|).
+ * rew [cap_T, B] f32, done [cap_T, B] u8, q_taken / q_boot [cap_T, B] f32 (the actor's
+ * Q(s_t, a_t) and bootstrap value of s_t, appended per row with rpl_ring_append_rows).
+ * out [T_out, B] f32 is time-major with one column per env: for a sequence block it is the
+ * td_steps rpl_sumtree_update_seq takes for that block's B leaves (row0 = block start +
+ * burn-in, T_out = train rows); for transitions, rows row0.. are leaves row0*B .. in order.
+ * RPL_ERANGE: n < 1 or T_out + n > cap_T. */
+int rpl_ring_td_abs(const float* rew, const uint8_t* done, const float* q_taken, const float* q_boot,
+                    int64_t cap_T, int64_t B, int64_t row0, int64_t T_out, int32_t n, double gamma,
+                    int32_t rescale, double rescale_eps, float* out, void* stream);
 
 /* n-step targets with the double-Q bootstrap: q_online, q_target [T+1, B, A] f32 (the two
  * networks' action values for rows 0..T); for output row t (0..T-n) the bootstrap is

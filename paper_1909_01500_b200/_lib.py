@@ -79,6 +79,8 @@ _SIGS = {
     "rpl_sumtree_update_ex": ([C.POINTER(TreeLayout), P, P, P, I64, D, D, I32, P, P], C.c_int),
     "rpl_sumtree_sample": ([C.POINTER(TreeLayout), P, I64, P, U64, U64, D, P, P, P, P, P, P], C.c_int),
     "rpl_sumtree_sample_stream": ([C.POINTER(TreeLayout), P, I64, U64, D, P, P, P, P, P, P], C.c_int),
+    "rpl_ring_td_abs": ([P, P, P, P, I64, I64, I64, I64, I32, D, I32, D, P, P], C.c_int),
+    "rpl_ring_append_rows": ([P, I64, I64, I64, P, I64, P], C.c_int),
     "rpl_sumtree_update_sample": ([C.POINTER(TreeLayout), P, P, P, I64, I64, D, D, D, I32, I64, U64, P, P, P, P],
                                   C.c_int),
     "rpl_sumtree_sample_sharded": ([C.POINTER(TreeLayout), P, I32, I32, I64, P, I64, P, U64, U64, I32, P, P, P, P,

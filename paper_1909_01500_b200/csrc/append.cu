@@ -133,6 +133,13 @@ extern "C" int rpl_ring_append(const rpl_gather_desc* ring, const void* obs, con
   return RPL_OK;
 }
 
+extern "C" int rpl_ring_append_rows(void* ring_array, int64_t row_bytes, int64_t cap_T, int64_t cursor,
+                                    const void* src, int64_t T_b, void* stream) {
+  if (!ring_array || !src || row_bytes < 1 || cap_T < 1 || cursor < 0 || cursor >= cap_T || T_b < 0 || T_b > cap_T)
+    return RPL_EINVAL;
+  return copy_rows(ring_array, src, cursor, cap_T, T_b, row_bytes, as_stream(stream));
+}
+
 extern "C" int rpl_replay_validity(const rpl_tree_layout* L, int64_t* tree, int32_t kind, int64_t cap_T, int64_t B,
                                    int32_t k, int32_t n_step, int32_t seq_len, int32_t period, int64_t cursor_old,
                                    int64_t size_old, int64_t cursor_new, int64_t size_new, void* stream) {

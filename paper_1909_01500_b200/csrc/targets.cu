@@ -75,6 +75,34 @@ __global__ void k_nstep_dq(const float* __restrict__ r, const uint8_t* __restric
   }
 }
 
+// Per-step n-step TD error straight from the ring (NEXT-1 initial priorities, R33): one
+// thread per output (t, b); ring rows modulo cap_T; the same target arithmetic as k_nstep_dq.
+__global__ void k_ring_td_abs(const float* __restrict__ r, const uint8_t* __restrict__ d,
+                              const float* __restrict__ q_taken, const float* __restrict__ q_boot, int64_t cap,
+                              int64_t B, int64_t row0, int64_t T_out, int n, double gamma, int rescale, double eps,
+                              float* __restrict__ out) {
+  pdl_wait();
+  const int64_t total = T_out * B;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / B;
+    const int64_t b = e - t * B;
+    const int64_t row = (row0 + t) % cap;
+    int64_t rb = row + n;  // bootstrap row
+    if (rb >= cap) rb -= cap;
+    const double qv = (double)__ldg(q_boot + rb * B + b);
+    double acc = rescale ? h_inv_t(qv, eps) : qv;
+    for (int i = n - 1; i >= 0; --i) {  // Horner from the last row (R24)
+      int64_t ri = row + i;
+      if (ri >= cap) ri -= cap;
+      const uint8_t di = __ldg(d + ri * B + b);
+      const double rv = (double)__ldg(r + ri * B + b);
+      acc = di ? rv : fma(gamma, acc, rv);
+    }
+    if (rescale) acc = h_fwd_t(acc, eps);
+    out[e] = (float)fabs(acc - (double)__ldg(q_taken + row * B + b));
+  }
+}
+
 constexpr int C51_WARPS = 4;
 
 __global__ void __launch_bounds__(C51_WARPS * 32)
@@ -137,4 +165,20 @@ extern "C" int rpl_c51_project(const float* p_target, const float* q_online, con
   const int64_t blocks = (n + C51_WARPS - 1) / C51_WARPS;
   return launch_pdl(k_c51_project, dim3((unsigned)blocks), dim3(C51_WARPS * 32), 0, as_stream(stream), p_target,
                     q_online, R, done_n, n, (int)A, (int)n_atoms, v_min, v_max, gamma_n, m_out, a_star);
+}
+
+extern "C" int rpl_ring_td_abs(const float* rew, const uint8_t* done, const float* q_taken, const float* q_boot,
+                               int64_t cap_T, int64_t B, int64_t row0, int64_t T_out, int32_t n, double gamma,
+                               int32_t rescale, double rescale_eps, float* out, void* stream) {
+  if (!rew || !done || !q_taken || !q_boot || !out || cap_T < 1 || B < 1 || row0 < 0 || row0 >= cap_T || T_out < 0)
+    return RPL_EINVAL;
+  if (n < 1 || T_out + n > cap_T) return RPL_ERANGE;
+  if (rescale && !(rescale_eps > 0.0)) return RPL_EINVAL;
+  if (T_out == 0) return RPL_OK;
+  const int threads = 256;
+  int64_t blocks = (T_out * B + threads - 1) / threads;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  if (blocks > cap) blocks = cap;
+  return launch_pdl(k_ring_td_abs, dim3((unsigned)blocks), dim3(threads), 0, as_stream(stream), rew, done, q_taken,
+                    q_boot, cap_T, B, row0, T_out, (int)n, gamma, rescale ? 1 : 0, rescale_eps, out);
 }

@@ -17,7 +17,7 @@ from ._lib import GatherDesc, TreeLayout, check, lib
 __all__ = [
     "returns_discounted", "returns_nstep", "gae", "value_rescale", "SumTree", "is_weights", "gather",
     "GatherRing", "GatherPlan", "check_err", "launch_count", "debug_priority_values", "sample_uniform",
-    "ring_append", "returns_nstep_dq", "c51_project", "stack_frames",
+    "ring_append", "returns_nstep_dq", "c51_project", "stack_frames", "ring_append_rows", "ring_td_abs",
 ]
 
 
@@ -561,6 +561,33 @@ def ring_append(ring: GatherRing, obs=None, act=None, rew=None, done=None, rnn=N
     ring.cursor = (ring.cursor + T_b) % ring.cap_T
     ring.size = min(ring.cap_T, ring.size + T_b)
     return old
+
+
+def ring_append_rows(ring_array, src, cursor):
+    """rpl_ring_append_rows: src [T_b, ...] (host-pinned or device) -> ring_array [cap_T, ...]
+    rows cursor .. (mod cap_T).  Does not move any ring cursor."""
+    if not ring_array.is_contiguous() or not src.is_contiguous() or src.dtype != ring_array.dtype \
+            or tuple(src.shape[1:]) != tuple(ring_array.shape[1:]):
+        raise ValueError("src must be a contiguous [T_b, ...] tensor matching ring_array's rows")
+    row_bytes = int(ring_array[0].numel() * ring_array.element_size())
+    check(lib.rpl_ring_append_rows(_ptr(ring_array), row_bytes, int(ring_array.shape[0]), int(cursor), _ptr(src),
+                                   int(src.shape[0]), _stream(ring_array.device)), "rpl_ring_append_rows")
+
+
+def ring_td_abs(rew, done, q_taken, q_boot, row0, T_out, n, gamma, rescale=False, eps=1e-3, out=None):
+    """rpl_ring_td_abs: per-step |n-step TD error| of ring rows row0 .. row0+T_out-1 (mod cap_T)
+    from ring arrays [cap_T, B] -> [T_out, B] f32 (R33)."""
+    cap, B = (int(x) for x in rew.shape)
+    _req(rew, torch.float32, "rew")
+    _req(done, torch.uint8, "done", (cap, B))
+    _req(q_taken, torch.float32, "q_taken", (cap, B))
+    _req(q_boot, torch.float32, "q_boot", (cap, B))
+    out = torch.empty((int(T_out), B), dtype=torch.float32, device=rew.device) if out is None else out
+    _req(out, torch.float32, "out", (int(T_out), B))
+    check(lib.rpl_ring_td_abs(_ptr(rew), _ptr(done), _ptr(q_taken), _ptr(q_boot), cap, B, int(row0), int(T_out),
+                              int(n), float(gamma), 1 if rescale else 0, float(eps), _ptr(out),
+                              _stream(rew.device)), "rpl_ring_td_abs")
+    return out
 
 
 def stack_frames(uniq, start, k, pad_mode=_lib.PAD_REPEAT, out=None, n_active=None):

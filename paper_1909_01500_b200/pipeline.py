@@ -21,6 +21,11 @@ The B200 version keeps the roles and replaces the mechanisms:
   * throttle        an exact budget counter (SPEC's design decision): every appended
                     step credits `cap` units, every consumed sample debits its counted
                     steps; `can_step()` is false while a step would overdraw the budget.
+  * initial         (optional, NEXT-1, P:123 fn "5-step TD initial priorities", S:660,
+    priorities      reading R33) the sampler also hands over the actor's q_taken / q_boot
+                    per row; they are appended to two ring arrays, and a leaf that an append
+                    makes valid gets, instead of max-seen, the priority of its n-step TD
+                    errors (rpl_ring_td_abs -> rpl_sumtree_update_seq / _update_ex).
 
 Host logic only (argument marshalling and event bookkeeping); every data movement and
 tree update runs in librpl.
@@ -32,6 +37,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import ops
+from . import replay as _rp
 
 
 @dataclass
@@ -78,12 +84,29 @@ class ReplayPipeline:
 
     def __init__(self, ring: ops.GatherRing, tree: ops.SumTree, kind: str, T_b: int, k: int = 4, n_step: int = 1,
                  seq_len: int = 1, period: int = 1, train_steps: int = 1, cap: float = 1.0, rnn_parts: int = 2,
-                 rnn_h: int = 512):
+                 rnn_h: int = 512, init_priority: dict | None = None):
         self.ring, self.tree = ring, tree
         self.kind, self.T_b, self.k, self.n_step = kind, int(T_b), int(k), int(n_step)
         self.seq_len, self.period, self.train_steps = int(seq_len), int(period), int(train_steps)
         dev = ring.obs.device
         self.device = dev
+        # init_priority: dict(n, gamma, rescale, eps, alpha, eps_p[, eta, burn_in] for sequences)
+        self.init = dict(init_priority) if init_priority is not None else None
+        if self.init is not None:
+            ip = self.init
+            ip.setdefault("rescale", False)
+            ip.setdefault("eps", 1e-3)
+            ip.setdefault("eps_p", 1e-3)
+            ip.setdefault("eta", 0.9)
+            ip.setdefault("burn_in", 0)
+            if kind == "sequence" and ip["burn_in"] + train_steps + ip["n"] > seq_len:
+                raise ValueError("burn_in + train_steps + n must fit in the sequence window")
+            shape = (ring.cap_T, ring.B)
+            self.q_taken = torch.zeros(shape, dtype=torch.float32, device=dev)
+            self.q_boot = torch.zeros(shape, dtype=torch.float32, device=dev)
+            self._leaf_ids = torch.arange(tree.n_leaves, dtype=torch.int64, device=dev)
+            t_out = train_steps if kind == "sequence" else ring.cap_T
+            self._td = torch.empty((t_out, ring.B), dtype=torch.float32, device=dev)
         self.copy_stream = torch.cuda.Stream(dev)
         self.learn_stream = torch.cuda.Stream(dev)
         self.throttle = ReplayRatio(cap)
@@ -101,6 +124,9 @@ class ReplayPipeline:
             if kind == "sequence" and ring.rnn is not None:
                 nblk = (self.T_b + self.period - 1) // self.period + 1
                 t["rnn"] = pinned((nblk,) + tuple(ring.rnn.shape[1:]), ring.rnn.dtype)
+            if self.init is not None:  # the actor's Q(s_t, a_t) and bootstrap value of s_t
+                t["q_taken"] = pinned(shp, torch.float32)
+                t["q_boot"] = pinned(shp, torch.float32)
             hb = _HostBatch(t)
             hb.ready.record(torch.cuda.current_stream(dev))
             self._bufs.append(hb)
@@ -141,6 +167,9 @@ class ReplayPipeline:
             t = hb.tensors
             rows = self.rnn_rows()
             rnn = t["rnn"][:len(rows)] if ("rnn" in t and rows) else None
+            if self.init is not None:  # at the cursor, before ring_append advances it
+                ops.ring_append_rows(self.q_taken, t["q_taken"], c0)
+                ops.ring_append_rows(self.q_boot, t["q_boot"], c0)
             ops.ring_append(self.ring, obs=t["obs"], act=t["act"], rew=t["rew"], done=t["done"], rnn=rnn,
                             period=self.period)
             copied = torch.cuda.Event()
@@ -159,6 +188,43 @@ class ReplayPipeline:
             with torch.cuda.stream(L):
                 self.tree.validity(self.kind, self.ring.cap_T, self.ring.B, self.k, c0, s0, c1, s1,
                                    n_step=self.n_step, seq_len=self.seq_len, period=self.period)
+                if self.init is not None:
+                    self._initial_priorities(c0, s0, c1, s1)
+
+    def newly_valid(self, c0, s0, c1, s1):
+        """Host bookkeeping: the rows (transitions) or blocks (sequences) an append made valid."""
+        cap = self.ring.cap_T
+        if self.kind == "sequence":
+            before = _rp.valid_sequence_blocks(cap, self.period, c0, s0, self.k, self.seq_len)
+            after = _rp.valid_sequence_blocks(cap, self.period, c1, s1, self.k, self.seq_len)
+        else:
+            before = _rp.valid_transition_rows(cap, c0, s0, self.k, self.n_step)
+            after = _rp.valid_transition_rows(cap, c1, s1, self.k, self.n_step)
+        return sorted(set(after.tolist()) - set(before.tolist()))
+
+    def _initial_priorities(self, c0, s0, c1, s1):
+        """Learner stream, right after validity: n-step TD initial priorities (R33) for every
+        leaf the append made valid (replacing the max-seen validity gave them)."""
+        ip, ring, B = self.init, self.ring, self.ring.B
+        units = self.newly_valid(c0, s0, c1, s1)
+        if self.kind == "sequence":
+            for blk in units:
+                td = ops.ring_td_abs(ring.rew, ring.done, self.q_taken, self.q_boot, blk * self.period + ip["burn_in"],
+                                     self.train_steps, ip["n"], ip["gamma"], ip["rescale"], ip["eps"], out=self._td)
+                self.tree.update_seq(self._leaf_ids[blk * B:(blk + 1) * B], td, ip["alpha"], eta=ip["eta"],
+                                     eps_p=ip["eps_p"])
+            return
+        runs, start = [], None  # runs of consecutive rows (leaf ranges never wrap)
+        for i, r in enumerate(units):
+            if start is None:
+                start = r
+            if i + 1 == len(units) or units[i + 1] != r + 1:
+                runs.append((start, r + 1))
+                start = None
+        for r0, r1 in runs:
+            td = ops.ring_td_abs(ring.rew, ring.done, self.q_taken, self.q_boot, r0, r1 - r0, ip["n"], ip["gamma"],
+                                 ip["rescale"], ip["eps"], out=self._td[:r1 - r0])
+            self.tree.update(self._leaf_ids[r0 * B:r1 * B], td.view(-1), ip["alpha"], eps_p=ip["eps_p"])
 
     def flush(self):
         """Make every submitted batch sampleable before the next step (deterministic order)."""

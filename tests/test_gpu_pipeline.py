@@ -152,3 +152,83 @@ def test_pipeline_overlapped_integrity(rpl):
         assert pipe.throttle.consumed <= pipe.throttle.cap * pipe.throttle.generated
     torch.cuda.synchronize()
     assert checks > 10 and int(H(err)[0]) == 0
+
+
+@pytest.mark.parametrize("kind", ["sequence", "transition"])
+def test_pipeline_initial_priorities(rpl, kind):
+    # NEXT-1 (R33): with init_priority, every valid leaf holds the priority of its n-step TD
+    # errors over the rows the ring holds (leaves cannot change rows while valid); invalid
+    # leaves hold 0.  Checked after every append against the oracle.
+    import torch
+    from oracle import targets as OT
+    from paper_1909_01500_b200.pipeline import ReplayPipeline
+    dev = torch.device("cuda")
+    ring = rpl.GatherRing(obs=torch.zeros((CAP, B, 8, 16), dtype=torch.uint8, device=dev),
+                          act=torch.zeros((CAP, B), dtype=torch.int64, device=dev),
+                          rew=torch.zeros((CAP, B), dtype=torch.float32, device=dev),
+                          done=torch.zeros((CAP, B), dtype=torch.uint8, device=dev), cursor=0, size=0,
+                          rnn=torch.zeros((CAP // PERIOD, B, 2, 4), dtype=torch.float32, device=dev))
+    ip = dict(n=5 if kind == "sequence" else 3, gamma=0.997, rescale=kind == "sequence", alpha=0.9, eta=0.9,
+              burn_in=10)
+    if kind == "sequence":
+        nl = (CAP // PERIOD) * B
+        pipe = ReplayPipeline(ring, rpl.SumTree(nl, 32), "sequence", TB, k=K, seq_len=L, period=PERIOD,
+                              train_steps=30, init_priority=ip)
+    else:
+        nl = CAP * B
+        pipe = ReplayPipeline(ring, rpl.SumTree(nl, 32), "transition", TB, k=K, n_step=3, init_priority=ip)
+    host = _host()
+    hq = {"q_taken": np.zeros((CAP, B), np.float32), "q_boot": np.zeros((CAP, B), np.float32)}
+    g = rng(64)
+    for it in range(9):
+        hb_next = pipe._bufs[pipe._next]
+        hb_next.ready.synchronize()  # its previous copy has finished
+        c0 = ring.cursor
+        for name in ("q_taken", "q_boot"):  # the actor's values for the rows of this batch
+            v = g.normal(0, 3, (TB, B)).astype(np.float32)
+            hb_next.tensors[name].numpy()[...] = v
+            hq[name][[(c0 + i) % CAP for i in range(TB)]] = v
+        if kind == "sequence":
+            _fill(pipe, g, host)
+        else:
+            hb = pipe.host_batch()
+            t = hb.tensors
+            t["obs"].numpy()[...] = g.integers(0, 256, t["obs"].shape, dtype=np.uint8)
+            rew = g.normal(size=(TB, B)).astype(np.float32)
+            done = (g.random((TB, B)) < 0.05).astype(np.uint8)
+            t["rew"].numpy()[...] = rew
+            t["done"].numpy()[...] = done
+            rr = [(c0 + i) % CAP for i in range(TB)]
+            host["rew"][rr], host["done"][rr] = rew, done
+            pipe.submit(hb)
+        pipe.flush()
+        pipe.learn_stream.synchronize()
+        leaves = H(pipe.tree.leaves)
+        cur, size = ring.cursor, ring.size
+        if kind == "sequence":
+            from paper_1909_01500_b200 import replay as RP
+            valid = RP.valid_sequence_blocks(CAP, PERIOD, cur, size, K, L)
+            orc = OS.SumTreeOracle(nl)
+            for blk in valid:
+                p = OT.initial_sequence_priorities(host["rew"], host["done"], hq["q_taken"], hq["q_boot"], int(blk),
+                                                   PERIOD, 10, 30, 5, 0.997, 0.9, rescale=True)
+                orc.update([int(blk) * B + b for b in range(B)], p, 0.9)
+            units = set(int(x) * B + b for x in valid for b in range(B))
+        else:
+            from paper_1909_01500_b200 import replay as RP
+            valid = RP.valid_transition_rows(CAP, cur, size, K, 3)
+            orc = OS.SumTreeOracle(nl)
+            for r in valid:
+                td = OT.ring_td_abs(host["rew"], host["done"], hq["q_taken"], hq["q_boot"], int(r), 1, 3,
+                                    0.997).astype(np.float32)
+                orc.update([int(r) * B + b for b in range(B)], [float(x) for x in td[0]], 0.9)
+            units = set(int(x) * B + b for x in valid for b in range(B))
+        ref = np.array(orc.q, np.int64)
+        for leaf in range(nl):
+            if leaf in units:
+                assert abs(int(leaves[leaf]) - int(ref[leaf])) <= 1e-6 * ref[leaf] + 2, (it, leaf)
+            else:
+                assert leaves[leaf] == 0, (it, leaf)
+        tot = int(H(pipe.tree.total())[0])
+        assert tot == int(leaves.sum())
+    assert len(units) > 0

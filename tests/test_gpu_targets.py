@@ -59,3 +59,41 @@ def test_c51_projection(rpl, n, A, N):
     assert np.allclose(mm.sum(-1), p.sum(-1)[np.arange(n), H(a)], atol=1e-5)
     if qo is not None:
         assert np.array_equal(H(a), [OT.argmax_first(qo[s]) for s in range(n)])
+
+
+@pytest.mark.parametrize("cap,B,row0,T_out,n,rescale", [(200, 64, 40, 80, 5, True), (200, 64, 150, 80, 5, True),
+                                                        (37, 5, 30, 20, 1, False), (12, 3, 0, 7, 5, False),
+                                                        (4096, 256, 4000, 96, 3, False)])
+def test_ring_td_abs_vs_oracle(rpl, cap, B, row0, T_out, n, rescale):
+    # NEXT-1 initial priorities (R33): per-step |n-step TD| from ring arrays, rows mod cap
+    g = rng(cap + row0 + n)
+    rew = (g.normal(size=(cap, B)) * (g.random((cap, B)) < 0.4) * 20).astype(np.float32)
+    done = (g.random((cap, B)) < 0.05).astype(np.uint8)
+    qt = g.normal(0, 5, (cap, B)).astype(np.float32)
+    qb = g.normal(0, 5, (cap, B)).astype(np.float32)
+    qt[row0, 0] = 0.0
+    out = rpl.ring_td_abs(T_(rew), T_(done), T_(qt), T_(qb), row0, T_out, n, 0.997, rescale=rescale)
+    ref = OT.ring_td_abs(rew, done, qt, qb, row0, T_out, n, 0.997, rescale=rescale)
+    rows = [(row0 + t) % cap for t in range(T_out)]
+    scale = np.abs(ref) + np.abs(qt[rows].astype(np.float64)) + 1.0
+    check_rel(H(out), ref, scale=scale, what="ring td")
+
+
+def test_ring_td_abs_errors(rpl):
+    import torch
+    z = torch.zeros((10, 2), device="cuda")
+    d = torch.zeros((10, 2), dtype=torch.uint8, device="cuda")
+    with pytest.raises(RuntimeError):
+        rpl.ring_td_abs(z, d, z, z, 0, 6, 5, 0.9)          # T_out + n > cap
+    with pytest.raises(RuntimeError):
+        rpl.ring_td_abs(z, d, z, z, 10, 1, 1, 0.9)         # row0 outside the ring
+
+
+def test_ring_append_rows(rpl):
+    import torch
+    ring = torch.zeros((10, 3), device="cuda")
+    src = torch.arange(12, dtype=torch.float32).reshape(4, 3).pin_memory()
+    rpl.ring_append_rows(ring, src, 8)                   # wraps: rows 8, 9, 0, 1
+    torch.cuda.synchronize()
+    h = H(ring)
+    assert h[[8, 9, 0, 1]].tolist() == src.numpy().tolist() and not h[2:8].any()
