@@ -447,6 +447,14 @@ int rpl_debug_priority_values(const float* td_abs, int64_t n, double alpha, doub
  * outputs. */
 int rpl_debug_set_gather_variant(int32_t variant);
 
+/* Measurement / test only: kernel choice of rpl_returns_discounted and rpl_gae
+ * (process-global; initial value from RPL_SCAN_VARIANT, else 0).  0 = default (whole-column
+ * TMA tiles when the layout is TMA-addressable, else LDG), 4 / 5 = T <= 128: rows split over
+ * a cluster of 2 / 4 CTAs (DSMEM carry exchange), 6 = TMA tiles, 3 / 1 / 2 = LDG
+ * with 16x8 / 32x4 / 8x16 warps x rows.  Results agree within the fp64-accumulation bound
+ * (segment boundaries differ).  RPL_EINVAL outside 0..6. */
+int rpl_debug_set_scan_variant(int32_t variant);
+
 /* Diagnostics (measurement only): bit mask applied to the default sequence gather.
  * 1 = skip the frame stores, 2 = skip the frame loads (outputs are then garbage),
  * 4 = normal-priority frame stores, 8 = normal L2 policy on the frame loads (the default is

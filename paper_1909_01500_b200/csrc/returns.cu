@@ -18,6 +18,8 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace rpl {
@@ -243,6 +245,156 @@ k_scan_tma(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUt
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster variant for short horizons (T <= CL * WARPS * S, e.g. PPO's T = 128; selectable,
+// not the default — see launch_scan for the measurement): the rows
+// of a 32-column group are split over a thread-block cluster of CL CTAs along T, so each
+// CTA moves 1/CL of the bytes (its TMA tiles arrive CL times sooner) and CL times more
+// SMs work on the call.  Each CTA composes its rows' affine maps into one CTA map per
+// column; after a cluster barrier, CTA `rank` reads the maps of ranks > rank from their
+// shared memory (DSMEM, ld.shared::cluster) to form its carry-in, then emits its rows.
+// A second cluster barrier keeps every CTA's maps alive until all readers are done.
+// ---------------------------------------------------------------------------
+template <int WARPS, int S, int CL, bool GAE>
+__global__ void __launch_bounds__(WARPS * 32)
+k_scan_cluster(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUtensorMap tm_v,
+               const __grid_constant__ CUtensorMap tm_d, const float* __restrict__ v, const float* __restrict__ boot,
+               int64_t T, int64_t B, double gamma, double lam, float* __restrict__ out0, float* __restrict__ out1) {
+  constexpr int CH = WARPS * S;  // rows per CTA
+  __shared__ __align__(128) float s_r[CH][32];
+  __shared__ __align__(128) float s_v[GAE ? CH : 1][32];
+  __shared__ __align__(128) uint8_t s_d[CH][32];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ double sA[WARPS][32];
+  __shared__ double sB[WARPS][32];
+  __shared__ double sMap[2][32];  // this CTA's composed map (A, B) per column, read by lower ranks
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  uint32_t rank;
+  asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int64_t cg = blockIdx.x / CL;
+  const int64_t col = cg * 32 + lane;
+  const bool cv = col < B;
+  const int64_t row0 = (int64_t)rank * CH;
+  const bool has_rows = row0 < T;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_r) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_d) : "memory");
+    if (GAE) asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_v) : "memory");
+  }
+  __syncthreads();
+  pdl_wait();
+  if (threadIdx.x == 0 && has_rows) {
+    const uint32_t bytes = (uint32_t)(CH * 32 * 4 * (GAE ? 2 : 1) + CH * 32);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&bar)), "r"(bytes) : "memory");
+    const int x = (int)(cg * 32), y = (int)row0;
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(s_u32(&s_r[0][0])), "l"(&tm_r), "r"(x), "r"(y), "r"(s_u32(&bar)) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(s_u32(&s_d[0][0])), "l"(&tm_d), "r"(x), "r"(y), "r"(s_u32(&bar)) : "memory");
+    if (GAE)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+          ::"r"(s_u32(&s_v[0][0])), "l"(&tm_v), "r"(x), "r"(y), "r"(s_u32(&bar)) : "memory");
+  }
+  // loads that do not depend on the tiles, issued while they are in flight
+  const double bootv = (GAE && cv) ? (double)__ldg(boot + col) : 0.0;
+  const double carry0 = (!GAE && boot != nullptr && cv) ? (double)__ldg(boot + col) : 0.0;
+  const int64_t t0 = row0 + (int64_t)w * S;
+  const int64_t tn = t0 + S;  // first row after this thread's segment
+  double vnext_global = 0.0;
+  if (GAE && cv && w == WARPS - 1 && tn < T) vnext_global = (double)__ldg(v + tn * B + col);  // next CTA's first row
+  const double ga = GAE ? gamma * lam : gamma;
+  if (has_rows) {
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done) : "r"(s_u32(&bar)), "r"(0u) : "memory");
+  }
+  double b[S];
+  float vv[S];
+  float rr[S];
+  uint32_t dmask = 0;
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    rr[i] = has_rows ? s_r[w * S + i][lane] : 0.f;
+    dmask |= ((has_rows && s_d[w * S + i][lane]) ? 1u : 0u) << i;
+    if (GAE) vv[i] = has_rows ? s_v[w * S + i][lane] : 0.f;
+  }
+  double vseg_next = 0.0;
+  if (GAE && cv && t0 < T) {
+    if (tn >= T) vseg_next = bootv;
+    else if (w + 1 < WARPS) vseg_next = (double)s_v[(w + 1) * S][lane];
+    else vseg_next = vnext_global;
+  }
+  const int nvalid = cv ? (int)max((int64_t)0, min((int64_t)S, T - t0)) : 0;
+#pragma unroll
+  for (int i = 0; i < S; ++i) {
+    const double nd = ((dmask >> i) & 1u) ? 0.0 : 1.0;
+    if (GAE) {
+      double vn;
+      if (i + 1 < S) vn = (i + 1 < nvalid) ? (double)vv[i + 1] : bootv;
+      else vn = vseg_next;
+      b[i] = i < nvalid ? ((double)rr[i] + gamma * nd * vn) - (double)vv[i] : 0.0;
+    } else {
+      b[i] = i < nvalid ? (double)rr[i] : 0.0;
+    }
+  }
+#define RPL_A(i) ((i) < nvalid ? (((dmask >> (i)) & 1u) ? 0.0 : ga) : 1.0)
+  double A = 1.0, Bc = 0.0;
+#pragma unroll
+  for (int i = S - 1; i >= 0; --i) {
+    const double ai = RPL_A(i);
+    Bc = fma(ai, Bc, b[i]);
+    A = ai * A;
+  }
+  sA[w][lane] = A;
+  sB[w][lane] = Bc;
+  __syncthreads();
+  if (w == 0) {  // the CTA map: x_{row0} = Acta x_{row0+CH} + Bcta
+    double Ac = 1.0, Bcc = 0.0;
+#pragma unroll
+    for (int ww = WARPS - 1; ww >= 0; --ww) {
+      Bcc = fma(sA[ww][lane], Bcc, sB[ww][lane]);
+      Ac = sA[ww][lane] * Ac;
+    }
+    sMap[0][lane] = Ac;
+    sMap[1][lane] = Bcc;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  double x = carry0;  // value just after row T-1 (ranks past T hold identity maps)
+  for (int rr_ = CL - 1; rr_ > (int)rank; --rr_) {
+    uint32_t ra, rb;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(s_u32(&sMap[0][lane])), "r"(rr_));
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(s_u32(&sMap[1][lane])), "r"(rr_));
+    double ra_v, rb_v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(ra_v) : "r"(ra) : "memory");
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(rb_v) : "r"(rb) : "memory");
+    x = fma(ra_v, x, rb_v);
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");  // done reading remote maps
+#pragma unroll
+  for (int ww = WARPS - 1; ww > 0; --ww) {
+    if (ww > w) x = fma(sA[ww][lane], x, sB[ww][lane]);
+  }
+#pragma unroll
+  for (int i = S - 1; i >= 0; --i) {
+    x = fma(RPL_A(i), x, b[i]);
+    const int64_t t = t0 + i;
+    if (i < nvalid) {
+      out0[t * B + col] = (float)x;
+      if (GAE && out1 != nullptr) out1[t * B + col] = (float)(x + (double)vv[i]);
+    }
+  }
+#undef RPL_A
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // keep sMap alive for the readers
+}
+
 __device__ __forceinline__ double h_fwd(double x, double eps) {
   // h(x) = x (1/(sqrt(|x|+1)+1) + eps)  ==  sign(x)(sqrt(|x|+1)-1) + eps x   (§8c #4)
   return x * (1.0 / (sqrt(fabs(x) + 1.0) + 1.0) + eps);
@@ -341,14 +493,23 @@ int elementwise_grid(int64_t work, int threads) {
 
 using namespace rpl;
 
-// Measurement-only knob (RPL_SCAN_VARIANT): 0 = TMA tiles when the layout allows (default,
-// else LDG 16 warps x 8 rows), 3 = LDG 16 warps x 8 rows, 1 = LDG 32 warps x 4 rows,
-// 2 = LDG 8 warps x 16 rows.  Same fp64 affine-map arithmetic; segment boundaries differ.
+// Measurement-only knob (RPL_SCAN_VARIANT): 0 = default (TMA tiles when the layout allows,
+// else LDG 16 warps x 8 rows), 4 = cluster of 2 CTAs x 64 rows (T <= 128, else default),
+// 5 = cluster of 4 CTAs x 32 rows (T <= 128, else default), 6 = TMA tiles, 3 = LDG
+// 16 warps x 8 rows, 1 = LDG 32 warps x 4 rows, 2 = LDG 8 warps x 16 rows.  Same fp64
+// affine-map arithmetic; segment boundaries differ.
+std::atomic<int> g_scan_variant{-1};  // -1: not set yet (read RPL_SCAN_VARIANT once)
+
 int scan_variant() {
-  static const int v = [] {
+  int v = g_scan_variant.load(std::memory_order_relaxed);
+  if (v < 0) {
     const char* e = getenv("RPL_SCAN_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
+    int want = e ? atoi(e) : 0;
+    if (want < 0 || want > 6) want = 0;
+    int expect = -1;
+    g_scan_variant.compare_exchange_strong(expect, want);
+    v = g_scan_variant.load(std::memory_order_relaxed);
+  }
   return v;
 }
 
@@ -383,11 +544,40 @@ bool tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esize
          CUDA_SUCCESS;
 }
 
+template <int WARPS, int S, int CL, bool GAE>
+int launch_scan_cluster(const float* r, const float* v, const uint8_t* d, const float* boot, int64_t T, int64_t B,
+                        double gamma, double lam, float* o0, float* o1, cudaStream_t st, bool* used) {
+  *used = false;
+  constexpr int CH = WARPS * S;
+  if (T > (int64_t)CL * CH) return RPL_OK;
+  CUtensorMap mr, mv, md;
+  if (!(tmap_2d(&mr, r, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH) &&
+        tmap_2d(&md, d, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, T, B, CH) &&
+        (!GAE || tmap_2d(&mv, v, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH))))
+    return RPL_OK;
+  if (!GAE) mv = mr;
+  *used = true;
+  const dim3 grid((unsigned)(((B + 31) / 32) * CL));
+  return launch_pdl_cluster(k_scan_cluster<WARPS, S, CL, GAE>, grid, dim3(WARPS * 32), 0, st, (unsigned)CL, mr, mv,
+                            md, v, boot, T, B, gamma, lam, o0, o1);
+}
+
 template <bool GAE>
 int launch_scan(const float* r, const float* v, const uint8_t* d, const float* boot, int64_t T, int64_t B,
                 double gamma, double lam, float* o0, float* o1, cudaStream_t st) {
   dim3 grid((unsigned)((B + 31) / 32));
-  if (scan_variant() == 0 && T < (1ll << 31) && B < (1ll << 31)) {
+  const int var = scan_variant();
+  if ((var == 4 || var == 5) && T < (1ll << 31) && B < (1ll << 31)) {
+    // short horizons: rows split over a cluster (4: 2 CTAs x 64 rows, 5: 4 CTAs x 32 rows).
+    // Measured slower than the whole-column tiles at PPO size (GAE 6.0 / 7.3-7.6 us vs
+    // 4.96 us): the call is latency-bound, and cluster scheduling plus two cluster
+    // barriers cost more than the per-CTA bytes they save.  Kept selectable.
+    bool used = false;
+    const int rc = var == 4 ? launch_scan_cluster<16, 4, 2, GAE>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, &used)
+                            : launch_scan_cluster<8, 4, 4, GAE>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, &used);
+    if (used) return rc;
+  }
+  if ((var == 0 || var == 6) && T < (1ll << 31) && B < (1ll << 31)) {
     CUtensorMap mr, mv, md;
     constexpr int CH = SCAN_WARPS * SCAN_S;
     if (tmap_2d(&mr, r, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH) &&
@@ -446,4 +636,10 @@ extern "C" int rpl_value_rescale(const float* x, float* y, int64_t n, double eps
   const int threads = 256;
   return launch_pdl(k_rescale, dim3(elementwise_grid((n + 3) / 4, threads)), dim3(threads), 0, as_stream(stream), x,
                     y, n, eps, inverse ? 1 : 0);
+}
+
+extern "C" int rpl_debug_set_scan_variant(int32_t variant) {
+  if (variant < 0 || variant > 6) return RPL_EINVAL;
+  g_scan_variant.store(variant);
+  return RPL_OK;
 }

@@ -57,15 +57,23 @@ def test_toy_golden(rpl):
     check_rel(H(ret), g["gae_ret"], what="ret")
 
 
-# B % 16 == 0 takes the TMA-tile kernel (ragged T, partial 32-column blocks, multi-chunk T),
-# other B the LDG kernel
+# B % 16 == 0 takes a TMA kernel — whole-column tiles (multi-chunk T, partial 32-column
+# blocks) or, under scan variants 4 / 5, the cluster split when T <= 128 (ragged last CTA,
+# CTAs past T) — other B the LDG kernel
 SHAPES = [(1, 1), (1, 7), (5, 3), (16, 32), (127, 33), (128, 64), (129, 31), (300, 100), (1000, 5), (300, 48),
-          (129, 16), (1000, 80), (257, 4096)]
+          (129, 16), (1000, 80), (257, 4096), (20, 64), (65, 16), (97, 48), (33, 4096)]
+
+
+@pytest.fixture(params=[0, 4, 5, 3])
+def scan_variant(rpl, request):
+    assert rpl._lib.lib.rpl_debug_set_scan_variant(request.param) == 0
+    yield request.param
+    rpl._lib.lib.rpl_debug_set_scan_variant(0)
 
 
 @pytest.mark.parametrize("T,B", SHAPES)
 @pytest.mark.parametrize("kind", ["clipped", "heavy"])
-def test_discounted_and_gae_random(rpl, T, B, kind):
+def test_discounted_and_gae_random(rpl, T, B, kind, scan_variant):
     seed = 1000 + T * 7 + B
     r, v, d, boot = returns_inputs(seed, T, B, reward_kind=kind, p_done=0.05)
     for gamma, lam in [(0.99, 0.95), (0.997, 1.0), (0.9, 0.0)]:
@@ -81,7 +89,7 @@ def test_discounted_and_gae_random(rpl, T, B, kind):
         check_rel(H(ret), ret_ref, Sg, what="ret")
 
 
-def test_ppo_full_size(rpl):
+def test_ppo_full_size(rpl, scan_variant):
     # BASELINE.json configs[1]: [T=128, B=4096], gamma 0.99, lambda 0.95; every element
     T, B = 128, 4096
     for kind, pd in [("clipped", 0.05), ("heavy", 0.001)]:
