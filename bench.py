@@ -289,19 +289,24 @@ def run_rpl(args):
     Tn = c["train"] + c["n_step"] - 1
     lib, P_ = rpl._lib.lib, rpl.ops._ptr
 
-    def step(i, gather_events=None):
+    def step(i, gather_events=None, y_out=None, w_out=None, io=None):
+        # y_out / w_out: per-step output buffers; io = (td, q, cur_idx, prev_idx) per-step
+        # inputs / index buffers (the e2e schedule gives every step of a graph its own)
         s = rpl.ops._stream(dev)
         cur, prev = idx_buf[i % 2], idx_buf[(i + 1) % 2]
+        td_i, q_i = td_pool[i % P], q_pool[i % P]
+        if io is not None:
+            td_i, q_i, cur, prev = io
         # (a5-a7) new priorities for the previous batch (entries < 0 — not owned — are skipped, R22)
         # (NEXT-1 fused) sequence priority = eta max + (1 - eta) mean of the 80 per-step |delta| (R26)
         if world == 1 and args.tree_fused:
             # (a5-a8) update + stratified draws in one launch (grid barrier between them);
             # the batch-min normaliser and IS weights (a9) are fused into the gather
-            rpl._lib.check(lib.rpl_sumtree_update_sample(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]),
+            rpl._lib.check(lib.rpl_sumtree_update_sample(tree._lp, P_(tree.storage), P_(prev), P_(td_i),
                                                          c["train"], n_glob, c["eta"], c["alpha"], c["eps_p"], 0, n,
                                                          seed, P_(cur), P_(q_buf), P_(err), s), "update_sample")
         else:
-            rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]),
+            rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(prev), P_(td_i),
                                                       c["train"], n_glob, c["eta"], c["alpha"], c["eps_p"], 0, None,
                                                       s), "update_seq")
         if world == 1 and not args.tree_fused:
@@ -318,7 +323,11 @@ def run_rpl(args):
         if gather_events is not None:
             gather_events[0].record()
         # IS weights fused into the gather: batch min (1 GPU) or the all-reduced global min (Mode L)
+        if w_out is not None:
+            plan.desc.o_w = w_out.data_ptr()
         plan.run(cur, q=q_buf, qmin=None if world == 1 else qmin, beta=c["beta"], err=err, stream=s)
+        if w_out is not None:
+            plan.desc.o_w = w.data_ptr()
         if gather_events is not None:
             gather_events[1].record()
         if mode_c:
@@ -328,9 +337,9 @@ def run_rpl(args):
                                                     0, P_(stacked), None, s), "stack")
         if learner:
             rpl._lib.check(lib.rpl_returns_nstep(P_(r_tr), P_(d_tr), Tn, n_glob, c["n_step"], c["gamma"],
-                                                 P_(q_pool[i % P][c["burn_in"]:c["burn_in"] + Tn]),
-                                                 P_(q_pool[i % P][c["burn_in"] + Tn]), 1, c["eps"], P_(y), P_(dn),
-                                                 s), "nstep")
+                                                 P_(q_i[c["burn_in"]:c["burn_in"] + Tn]),
+                                                 P_(q_i[c["burn_in"] + Tn]), 1, c["eps"],
+                                                 P_(y if y_out is None else y_out), P_(dn), s), "nstep")
 
     # idx < 0 entries (first step / not-owned) make the update kernel flag RPL_DERR_IDX; allow that bit.
     # warm-up (also primes lazy module loading and cudaFuncSetAttribute outside capture)
@@ -504,68 +513,67 @@ def e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K, world):
         h_w.copy_(w, non_blocking=True)
         h_i.copy_(idx_buf[i % 2], non_blocking=True)
 
-    # 1 GPU: the same calls in one CUDA graph of P steps, with the host copies on a copy stream
-    # so that step i's results go down and step i+1's inputs come up while step i+1 computes
-    # (every copy is still inside the timed region); multi-rank: eager, serial
+    # 1 GPU: the same calls in CUDA graphs of P steps.  Every step of a graph has its own
+    # input slots, index and output buffers, so no step waits on a copy: the copy stream
+    # brings up the NEXT graph's P input sets (two slot sets, alternating graphs A / B) and
+    # takes each step's results down right after that step (fork only; one join at the graph
+    # end).  Every copy is inside the timed region; multi-rank: eager, serial.
     cs = torch.cuda.Stream(dev)
-    h_y2 = [h_y, torch.empty_like(h_y).pin_memory()]
-    h_w2 = [h_w, torch.empty_like(h_w).pin_memory()]
-    h_i2 = [h_i, torch.empty_like(h_i).pin_memory()]
-    y2 = [y, torch.empty_like(y)]
-    w2 = [w, torch.empty_like(w)]
+    td_set = [td_pool, torch.empty_like(td_pool)]
+    q_set = [q_pool, torch.empty_like(q_pool)]
+    idx_all = [torch.full_like(idx_buf[0], -1) for _ in range(P)]
+    y_all = [torch.empty_like(y) for _ in range(P)]
+    w_all = [torch.empty_like(w) for _ in range(P)]
+    h_y_all = [torch.empty(y.shape, dtype=torch.float32).pin_memory() for _ in range(P)]
+    h_w_all = [torch.empty(w.shape, dtype=torch.float32).pin_memory() for _ in range(P)]
+    h_i_all = [torch.empty(idx_buf[0].shape, dtype=torch.int64).pin_memory() for _ in range(P)]
 
-    def overlapped(Pn):
+    def prefetched(par):
         main = torch.cuda.current_stream(dev)
-        up = [torch.cuda.Event() for _ in range(Pn)]
-        done = [torch.cuda.Event() for _ in range(Pn)]
-        down = [torch.cuda.Event() for _ in range(Pn)]
-        with torch.cuda.stream(cs):
-            cs.wait_stream(main)
-            td_pool[0].copy_(h_td[0], non_blocking=True)
-            q_pool[0].copy_(h_q[0], non_blocking=True)
-            up[0].record(cs)
-        for i in range(Pn):
-            main.wait_event(up[i])
-            if i >= 2:  # step i rewrites idx_buf[i % 2] and y2/w2[i % 2]: their D2H must be done
-                main.wait_event(down[i - 2])
-            step(i)
-            y2[i % 2].copy_(y)  # device-side snapshot: the D2H below overlaps step i+1
-            w2[i % 2].copy_(w)
-            done[i].record(main)
+        cs.wait_stream(main)
+        with torch.cuda.stream(cs):  # the next graph's inputs (set 1 - par)
+            for j in range(P):
+                td_set[1 - par][j].copy_(h_td[j], non_blocking=True)
+                q_set[1 - par][j].copy_(h_q[j], non_blocking=True)
+        for j in range(P):
+            step(j, y_out=y_all[j], w_out=w_all[j], io=(td_set[par][j], q_set[par][j], idx_all[j], idx_all[j - 1]))
+            ev = torch.cuda.Event()
+            ev.record(main)
             with torch.cuda.stream(cs):
-                if i + 1 < Pn:
-                    td_pool[(i + 1) % P].copy_(h_td[(i + 1) % P], non_blocking=True)
-                    q_pool[(i + 1) % P].copy_(h_q[(i + 1) % P], non_blocking=True)
-                    up[i + 1].record(cs)
-                cs.wait_event(done[i])
-                h_y2[i % 2].copy_(y2[i % 2], non_blocking=True)
-                h_w2[i % 2].copy_(w2[i % 2], non_blocking=True)
-                h_i2[i % 2].copy_(idx_buf[i % 2], non_blocking=True)
-                down[i].record(cs)
+                cs.wait_event(ev)
+                h_y_all[j].copy_(y_all[j], non_blocking=True)
+                h_w_all[j].copy_(w_all[j], non_blocking=True)
+                h_i_all[j].copy_(idx_all[j], non_blocking=True)
         main.wait_stream(cs)
 
-    graph = None
+    graphs = None
     if world == 1 and not args.no_graph:
         try:
-            overlapped(P)
+            for par in (0, 1):
+                prefetched(par)
             torch.cuda.synchronize()
             s = torch.cuda.Stream(dev)
             s.wait_stream(torch.cuda.current_stream(dev))
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=s):
-                overlapped(P)
+            graphs = []
+            for par in (0, 1):
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr, stream=s):
+                    prefetched(par)
+                graphs.append(gr)
+            torch.cuda.synchronize()
+            graphs[0].replay()  # fills set 1 for the first timed replay (graph B)
             torch.cuda.synchronize()
         except Exception as e:  # pragma: no cover
             print(f"[bench] e2e graph capture failed ({e}); eager", file=sys.stderr)
-            graph = None
+            graphs = None
             torch.cuda.synchronize()
-    reps = max(1, K // P)
-    K = reps * P if graph is not None else K
+    reps = max(2, K // P)
+    K = reps * P if graphs is not None else K
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    if graph is not None:
-        for _ in range(reps):
-            graph.replay()
+    if graphs is not None:
+        for r_ in range(reps):
+            graphs[(r_ + 1) % 2].replay()
     else:
         for i in range(K):
             e2e_step(i)
@@ -576,8 +584,9 @@ def e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K, world):
     db = y.numel() * 4 + w.numel() * 4 + idx_buf[0].numel() * 8
     return {"value": K * n * world / (ms / 1e3), "unit": "sequences/s", "h2d_bytes_per_step": hb,
             "d2h_bytes_per_step": db, "steps": K,
-            "timing": ("cuda graph of 8 steps; pinned-host H2D of each step's inputs and D2H of its results on "
-                       "a copy stream overlapping the next step") if graph is not None
+            "timing": ("cuda graphs of 8 steps; per step one pinned-host H2D input set (prefetched one graph "
+                       "ahead into alternating slots) and the D2H of its results right after it, on a copy "
+                       "stream overlapping compute") if graphs is not None
             else "eager launches incl. pinned-host H2D/D2H copies"}
 
 
