@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget (cpu_baseline)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/baseline/e2e)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "collective"],
+                    help="N>1: K5/K7 over peer-memory boards fused into the sampler and gather (p2p) or "
+                         "torch.distributed collectives (collective); auto = p2p with nccl, else collective")
     ap.add_argument("--tree-fused", type=int, default=0, choices=[0, 1],
                     help="1 GPU: priority update + sampling as one launch (rpl_sumtree_update_sample; "
                          "measured 1.7 us/step slower than the PDL-chained pair)")
@@ -273,11 +276,17 @@ def run_rpl(args):
     totals = torch.zeros(world, dtype=torch.int64, device=dev)
     my_total = torch.zeros(1, dtype=torch.int64, device=dev)
     n_owned = torch.zeros(2, dtype=torch.int64, device=dev)  # [owned m, first owned stratum k0]
+    p2p = world > 1 and (args.exchange == "p2p" or (args.exchange == "auto" and args.backend == "nccl"))
+    boards = None
     if world > 1:
         # compacted sharded sample: this rank's owned draws first, the gather schedules only those
         plan.desc.n_active = n_owned.data_ptr()
         if mode_c:  # ... and writes them at their global batch positions in the learner's buffers
             plan.desc.col_offset = n_owned.data_ptr() + 8
+        if p2p:  # K5 / K7 through peer-memory boards, fused into the sampler and the gather
+            from paper_1909_01500_b200.shard import PeerBoards
+            boards = PeerBoards(device=dev)
+            plan.set_peers(boards.ptrs, world, rank)
 
     def all_gather_totals():
         if args.backend == "nccl":
@@ -313,6 +322,12 @@ def run_rpl(args):
             # (a8) draws only; the batch-min normaliser and IS weights (a9) are fused into the gather
             rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, seed, c["beta"], P_(cur),
                                                          P_(q_buf), None, None, P_(err), s), "sample")
+        elif p2p:
+            # (a8, K5 fused) every rank publishes its total into the peers' boards and reads all of
+            # them inside the sampler; no collective launch
+            rpl._lib.check(lib.rpl_sumtree_sample_sharded_p2p(tree._lp, P_(tree.storage), rank, world, n_leaves,
+                                                              P_(boards.ptrs), n_glob, seed, P_(cur), P_(q_buf),
+                                                              P_(n_owned), P_(err), s), "sample_sharded_p2p")
         elif world > 1:
             rpl._lib.check(lib.rpl_sumtree_total(tree._lp, P_(tree.storage), P_(my_total), s), "total")
             all_gather_totals()                                                  # K5: 8 B per rank
@@ -325,7 +340,8 @@ def run_rpl(args):
         # IS weights fused into the gather: batch min (1 GPU) or the all-reduced global min (Mode L)
         if w_out is not None:
             plan.desc.o_w = w_out.data_ptr()
-        plan.run(cur, q=q_buf, qmin=None if world == 1 else qmin, beta=c["beta"], err=err, stream=s)
+        # (K7 fused with p2p: the gather publishes / reads the batch mins over the boards)
+        plan.run(cur, q=q_buf, qmin=None if (world == 1 or p2p) else qmin, beta=c["beta"], err=err, stream=s)
         if w_out is not None:
             plan.desc.o_w = w.data_ptr()
         if gather_events is not None:
@@ -393,7 +409,7 @@ def run_rpl(args):
         dist.barrier()
     ms = e0.elapsed_time(e1)
     launches = ((rpl.launch_count() - launches0) if not use_graph
-                else (4 if world == 1 else 4 + int(learner) + int(mode_c and rank == 0)) * K_eff)
+                else (4 if world == 1 else (3 if p2p else 4) + int(learner) + int(mode_c and rank == 0)) * K_eff)
     clk = clocks.stop() if not args.profile else {}
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -444,7 +460,9 @@ def run_rpl(args):
         "config": dict(r2d2_config(c, world, args.mode),
                        timing="cuda graph of 8 steps, replayed" if use_graph else "eager launches",
                        tree=("update+sample fused (rpl_sumtree_update_sample)" if world == 1 and args.tree_fused
-                             else "update_seq, then sample")),
+                             else "update_seq, then sample"),
+                       exchange=(None if world == 1 else "p2p boards (K5 in the sampler, K7 in the gather)" if p2p
+                                 else f"{args.backend} collectives")),
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "k_gather_seq_pipe_lsu", "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,

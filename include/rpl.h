@@ -54,7 +54,8 @@ enum {
   RPL_DERR_SATURATED = 2,     /* a priority exceeded q_cap: clamped to q_cap */
   RPL_DERR_EMPTY = 4,         /* sampling from a tree whose total is 0: idx = -1 */
   RPL_DERR_INVALID_LEAF = 8,  /* gather window not fully inside the valid ring rows */
-  RPL_DERR_TREE = 16          /* descent found a prefix >= node sum (inconsistent tree) */
+  RPL_DERR_TREE = 16,         /* descent found a prefix >= node sum (inconsistent tree) */
+  RPL_DERR_PEER = 32          /* a peer's exchange-board value did not arrive within ~2 s */
 };
 
 const char* rpl_strerror(int status);
@@ -235,6 +236,31 @@ int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t 
                                int64_t* out_qmin, int64_t* out_count, int32_t* dev_err,
                                void* stream);
 
+/* Peer exchange boards (SURVEY.md §8e K5 / K7 without NCCL on the data path): every rank
+ * owns one board of RPL_BOARD_WORDS(n_shards) device int64 words, zeroed before first use
+ * (and again whenever the trees are re-initialised), and maps every peer's board (CUDA IPC
+ * over NVLink; the rank's own board in its own slot).  `boards` is a DEVICE array of
+ * n_shards pointers, boards[g] = rank g's board as seen from this process.  Board layout:
+ * words [2 s, 2 s + 1] = {total, tag} published by rank s (K5), words [2 G + 2 s, +1] =
+ * {batch-min q, tag} published by rank s (K7).  A value is written with a plain store and
+ * its tag with st.release.sys; a reader spins on ld.acquire.sys until the tag equals the
+ * step's tag = the tree's stream position after the step (identical on every rank, never
+ * 0, strictly increasing).  One slot per source suffices: a rank cannot publish step j+1's
+ * total before every peer has consumed step j's values (step j's gather on each rank waits
+ * for every rank's K7 value, which each rank publishes after its K5 read).  A wait longer
+ * than ~2 s gives up and sets RPL_DERR_PEER. */
+#define RPL_BOARD_WORDS(n_shards) (4 * (int64_t)(n_shards))
+
+/* rpl_sumtree_sample_sharded (stream mode, compacted) with the K5 exchange fused in: the
+ * kernel publishes this tree's total to every peer's board and reads all n_shards totals
+ * from its own, replacing rpl_sumtree_total + an all-gather + the sampler.  out_count
+ * (device int64[2]) is required: [m, k0] as in rpl_sumtree_sample_sharded.  Give the same
+ * boards to rpl_gather (rpl_gather_desc.peer_boards) for the fused K7. */
+int rpl_sumtree_sample_sharded_p2p(const rpl_tree_layout* L, int64_t* tree, int32_t rank, int32_t n_shards,
+                                   int64_t shard_leaves, int64_t* const* boards, int64_t n, uint64_t seed,
+                                   int64_t* out_idx, int64_t* out_q, int64_t* out_count, int32_t* dev_err,
+                                   void* stream);
+
 /* Descent for explicit prefixes: out_idx[k] = leaf with C_i <= prefix[k] < C_{i+1}.
  * prefix >= total -> clamped to the last non-empty leaf + RPL_DERR_TREE. */
 int rpl_sumtree_find(const rpl_tree_layout* L, const int64_t* tree, const int64_t* prefix,
@@ -343,6 +369,15 @@ typedef struct {
    * slots are padding (§8c #13).  With RPL_OUT_UNIQUE it is all a consumer needs to
    * rebuild the k-stacks (rpl_stack_frames) — Mode C ships unique rows + offsets. */
   int8_t* o_start;
+  /* Optional (SEQUENCE, default kernel only; qmin must be NULL): the K7 exchange fused into
+   * the gather.  peer_boards = the device pointer array given to
+   * rpl_sumtree_sample_sharded_p2p, peer_world = n_shards, peer_rank = this rank.  CTA 0
+   * publishes this rank's batch-min q (over its owned entries; INT64_MAX if none) to every
+   * board; the IS weights use the min over all ranks' values, read while the frame copy
+   * runs.  The step's tag is read from this rank's own board (written by its sampler). */
+  int64_t* const* peer_boards;
+  int32_t peer_world;
+  int32_t peer_rank;
 } rpl_gather_desc;
 
 int rpl_gather(const rpl_gather_desc* desc /* host */, const int64_t* idx, const int64_t* q,

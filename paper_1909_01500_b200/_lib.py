@@ -54,6 +54,7 @@ class GatherDesc(C.Structure):
         ("n_active", C.c_void_p),
         ("col_offset", C.c_void_p),
         ("o_start", C.c_void_p),
+        ("peer_boards", C.c_void_p), ("peer_world", C.c_int32), ("peer_rank", C.c_int32),
     ]
 
 
@@ -83,6 +84,8 @@ _SIGS = {
     "rpl_ring_append_rows": ([P, I64, I64, I64, P, I64, P], C.c_int),
     "rpl_sumtree_update_sample": ([C.POINTER(TreeLayout), P, P, P, I64, I64, D, D, D, I32, I64, U64, P, P, P, P],
                                   C.c_int),
+    "rpl_sumtree_sample_sharded_p2p": ([C.POINTER(TreeLayout), P, I32, I32, I64, P, I64, U64, P, P, P, P, P],
+                                       C.c_int),
     "rpl_sumtree_sample_sharded": ([C.POINTER(TreeLayout), P, I32, I32, I64, P, I64, P, U64, U64, I32, P, P, P, P,
                                     P, P], C.c_int),
     "rpl_sumtree_find": ([C.POINTER(TreeLayout), P, P, I64, P, P, P], C.c_int),

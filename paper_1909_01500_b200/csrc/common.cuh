@@ -110,6 +110,39 @@ __device__ __forceinline__ void set_err(int32_t* err, int32_t bits) {
   if (err) atomicOr(err, bits);
 }
 
+// ---- peer exchange boards (rpl.h RPL_BOARD_WORDS; K5 / K7 over NVLink peer memory) ----
+constexpr int BOARD_MAX_WORLD = 64;
+
+// slot = {value, tag}: the value store is ordered before the tag by the release (sys scope:
+// the slot may live in a peer GPU's memory).
+__device__ __forceinline__ void board_publish(int64_t* slot, int64_t value, uint64_t tag) {
+  asm volatile("st.relaxed.sys.global.s64 [%0], %1;" ::"l"(slot), "l"(value) : "memory");
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot + 1), "l"(tag) : "memory");
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Spin until the slot carries `tag`, then read its value; false after ~2 s (peer missing).
+__device__ __forceinline__ bool board_wait(const int64_t* slot, uint64_t tag, int64_t* value) {
+  const uint64_t t0 = global_ns();
+  while (true) {
+    uint64_t t;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(t) : "l"(slot + 1) : "memory");
+    if (t == tag) {
+      int64_t v;
+      asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(slot) : "memory");
+      *value = v;
+      return true;
+    }
+    if (global_ns() - t0 > 2000000000ull) return false;
+    __nanosleep(64);
+  }
+}
+
 // 64-bit warp shuffles (int64 payloads)
 __device__ __forceinline__ int64_t shfl_up64(int64_t v, int d) {
   return (int64_t)__shfl_up_sync(0xffffffffu, (unsigned long long)v, d);

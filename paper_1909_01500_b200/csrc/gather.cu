@@ -178,6 +178,8 @@ struct GDesc {
   const int64_t* n_active;  // device count of leading entries to gather (NULL: all n)
   const int64_t* col_offset;  // device output column offset (NULL: 0)
   int8_t* o_start;            // per-row episode-start offsets [L, n] (NULL: not produced)
+  int64_t* const* peer_boards;  // K7 fused (rpl_gather_desc.peer_boards; NULL: off)
+  int peer_world, peer_rank;
 };
 
 // Output column offset (rpl_gather_desc.col_offset); read after pdl_wait.
@@ -889,6 +891,20 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   const int rpc = D.n_active ? (total + (int)gridDim.x - 1) / (int)gridDim.x : (int)rows_per_cta;
   const int g0 = (int)blockIdx.x * rpc;
   const int g1 = min(total, g0 + rpc);
+  // K7 fused (peer boards): the step's tag comes from this rank's own board (its sampler's
+  // K5 slot); CTA 0 publishes this rank's batch-min q over its owned entries to every rank
+  // — before any early exit, so a rank that owns nothing still publishes (INT64_MAX)
+  const bool peer = D.peer_boards != nullptr && D.o_w != nullptr && q != nullptr;
+  uint64_t ptag = 0;
+  if (peer) {
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];"
+                 : "=l"(ptag) : "l"(D.peer_boards[D.peer_rank] + 2 * D.peer_rank + 1) : "memory");
+    if (blockIdx.x == 0 && warp == 1) {
+      const int64_t qm_local = warp_batch_qmin(nullptr, idx, q, n);
+      if (lane < D.peer_world)
+        board_publish(D.peer_boards[lane] + 2 * D.peer_world + 2 * D.peer_rank, qm_local, ptag);
+    }
+  }
   if (g0 >= g1) return;
   const int nrows = g1 - g0;
   const int s_first = g0 / L;
@@ -1022,7 +1038,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
 
     if (warp == 1) {
       // ---------------- meta warp: per-row fields, IS weights ----------------
-      const int64_t qm = (D.o_w && q) ? warp_batch_qmin(qmin, idx, q, n) : 0;
+      const int64_t qm = (D.o_w && q && !peer) ? warp_batch_qmin(qmin, idx, q, n) : 0;
       const int64_t ab = D.act_bytes;
       const bool a8 = ab == 8 && ((reinterpret_cast<uintptr_t>(D.act) | reinterpret_cast<uintptr_t>(D.o_act) |
                                    reinterpret_cast<uintptr_t>(D.o_prev_act)) & 7) == 0;
@@ -1057,9 +1073,28 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         if (D.o_prev_rew) D.o_prev_rew[o] = pd ? 0.0f : prw;
         if (D.o_done) D.o_done[o] = dd;
         if (D.o_start) D.o_start[o] = start_off[c];
-        if (tau == 0 && D.o_w && q) {
+        if (tau == 0 && D.o_w && q && !peer) {
           const int64_t qs = q[sm];
           D.o_w[coff + sm] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
+        }
+      }
+      if (peer) {  // global batch min over every rank's published value, then the IS weights
+        int64_t v = INT64_MAX;
+        if (lane < D.peer_world &&
+            !board_wait(D.peer_boards[D.peer_rank] + 2 * D.peer_world + 2 * lane, ptag, &v)) {
+          set_err(err, RPL_DERR_PEER);
+          v = INT64_MAX;
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          const int64_t x = (int64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)v, o);
+          v = x < v ? x : v;
+        }
+        for (int c = lane; c < nrows; c += 32) {
+          if (row_first[c] < 0 || row_tau[c] != 0) continue;
+          const int sm = s_first + row_piece[c];
+          const int64_t qs = q[sm];
+          D.o_w[coff + sm] = qs > 0 ? (float)pow((double)v / (double)qs, beta) : 0.0f;
         }
       }
       // stored recurrent state of every sample whose first row lives here
@@ -1205,6 +1240,20 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   const int rpc = D.n_active ? (total + (int)gridDim.x - 1) / (int)gridDim.x : (int)rows_per_cta;
   const int g0 = (int)blockIdx.x * rpc;
   const int g1 = min(total, g0 + rpc);
+  // K7 fused (peer boards): the step's tag comes from this rank's own board (its sampler's
+  // K5 slot); CTA 0 publishes this rank's batch-min q over its owned entries to every rank
+  // — before any early exit, so a rank that owns nothing still publishes (INT64_MAX)
+  const bool peer = D.peer_boards != nullptr && D.o_w != nullptr && q != nullptr;
+  uint64_t ptag = 0;
+  if (peer) {
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];"
+                 : "=l"(ptag) : "l"(D.peer_boards[D.peer_rank] + 2 * D.peer_rank + 1) : "memory");
+    if (blockIdx.x == 0 && warp == 1) {
+      const int64_t qm_local = warp_batch_qmin(nullptr, idx, q, n);
+      if (lane < D.peer_world)
+        board_publish(D.peer_boards[lane] + 2 * D.peer_world + 2 * D.peer_rank, qm_local, ptag);
+    }
+  }
   if (g0 >= g1) return;
   const int nrows = g1 - g0;
   const int s_first = g0 / L;
@@ -1629,6 +1678,9 @@ GDesc to_dev(const rpl_gather_desc* d) {
   g.n_active = d->n_active;
   g.col_offset = d->col_offset;
   g.o_start = d->o_start;
+  g.peer_boards = d->peer_boards;
+  g.peer_world = d->peer_world;
+  g.peer_rank = d->peer_rank;
   return g;
 }
 
@@ -1667,9 +1719,13 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
   if (desc->pad_mode != RPL_PAD_REPEAT && desc->pad_mode != RPL_PAD_ZERO) return RPL_EINVAL;
   if ((desc->o_act || desc->o_prev_act) && (!desc->act || desc->act_bytes < 1)) return RPL_EINVAL;
   if (desc->o_w && !(beta >= 0.0)) return RPL_EINVAL;
+  if (desc->peer_boards && (desc->kind != RPL_GATHER_SEQUENCE || qmin || desc->peer_world < 1 ||
+                            desc->peer_world > BOARD_MAX_WORLD || desc->peer_rank < 0 ||
+                            desc->peer_rank >= desc->peer_world))
+    return RPL_EINVAL;
   GDesc g = to_dev(desc);
-  // col_offset / o_start: default kernels only
-  const int seq_variant = (desc->col_offset || desc->o_start) ? 0 : g_seq_variant;
+  // col_offset / o_start / peer boards: default kernels only
+  const int seq_variant = (desc->col_offset || desc->o_start || desc->peer_boards) ? 0 : g_seq_variant;
   const bool tma_ok = (desc->obs_bytes % 16 == 0) && aligned16(desc->obs) && aligned16(desc->o_obs) &&
                       aligned16(desc->o_next_obs) && desc->obs_bytes <= 32768;
   cudaStream_t st = as_stream(stream);
@@ -1756,7 +1812,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       }
     }
     if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs &&
-        (seq_variant == 3 || (seq_variant == 0 && !desc->col_offset && !desc->o_start))) {
+        (seq_variant == 3 || (seq_variant == 0 && !desc->col_offset && !desc->o_start && !desc->peer_boards))) {
       // persistent TMA pipeline: NS frame slots (+1 zero slot); CTAs_per_SM CTAs per SM
       // Slots the consumer may need beyond the released ones: G+1 rows of advance, the
       // k-1 window, and k-1 per piece boundary crossed.  With L > G at most two boundaries
@@ -1787,7 +1843,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
         return launch_status();
       }
     }
-    if (desc->o_start) return RPL_EUNSUPPORTED;  // produced by the persistent default kernel only
+    if (desc->o_start || desc->peer_boards) return RPL_EUNSUPPORTED;  // persistent default kernel only
     const int64_t smem = (int64_t)(SEQ_CHUNK + desc->k) * desc->obs_bytes;
     g.use_tma = (tma_ok && smem <= 200 * 1024) ? 1 : 0;
     const size_t dyn = g.use_tma ? (size_t)smem : 0;

@@ -282,7 +282,8 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
               uint64_t seed, uint64_t offset, double beta, int64_t* __restrict__ out_idx,
               int64_t* __restrict__ out_q, int64_t* __restrict__ out_qmin, float* __restrict__ out_w,
               int32_t* err, int rank, int n_shards, int64_t shard_leaves,
-              const int64_t* __restrict__ totals, int use_stream, int64_t* __restrict__ out_count) {
+              const int64_t* __restrict__ totals, int use_stream, int64_t* __restrict__ out_count,
+              int64_t* const* boards) {
   const int lane = threadIdx.x & 31;
   pdl_wait();
   // Without a batch reduction (no IS weights, no qmin requested) there is no grid-wide
@@ -302,10 +303,25 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
   const int64_t k = (int64_t)blockIdx.x * SAMPLE_WARPS + (threadIdx.x >> 5);
   int32_t errbits = 0;
   uint64_t Q, own_lo = 0, own_T = 0;
+  __shared__ int64_t s_tot[SHARDED ? BOARD_MAX_WORLD : 1];
+  if (SHARDED && boards) {
+    // K5 fused (rpl_sumtree_sample_sharded_p2p): CTA 0 publishes this shard's total to every
+    // rank's board, every CTA reads all totals from its own board; tag = stream position
+    // after this step (identical on every rank)
+    const uint64_t tag = spos + (uint64_t)n;
+    if (blockIdx.x == 0 && threadIdx.x < n_shards)
+      board_publish(boards[threadIdx.x] + 2 * rank, __ldcg(tree + L.level_off[0]), tag);
+    if (threadIdx.x < n_shards) {
+      int64_t v = 0;
+      if (!board_wait(boards[rank] + 2 * threadIdx.x, tag, &v)) set_err(err, RPL_DERR_PEER);
+      s_tot[threadIdx.x] = v;
+    }
+    __syncthreads();
+  }
   if (SHARDED) {
     Q = 0;
     for (int g = 0; g < n_shards; ++g) {
-      const uint64_t tg = (uint64_t)totals[g];
+      const uint64_t tg = (uint64_t)(boards ? s_tot[g] : totals[g]);
       if (g < rank) own_lo += tg;
       if (g == rank) own_T = tg;
       Q += tg;
@@ -755,7 +771,7 @@ extern "C" int rpl_sumtree_sample(const rpl_tree_layout* L, int64_t* tree, int64
   const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
   return launch_pdl(k_tree_sample<false>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
                     tree_dev(L), tree, n, draws, seed, offset, beta, out_idx, out_q, out_qmin, out_w, dev_err, 0, 1,
-                    (int64_t)0, (const int64_t*)nullptr, 0, (int64_t*)nullptr);
+                    (int64_t)0, (const int64_t*)nullptr, 0, (int64_t*)nullptr, (int64_t* const*)nullptr);
 }
 
 extern "C" int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree, int64_t n, uint64_t seed,
@@ -766,7 +782,8 @@ extern "C" int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree
   const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
   return launch_pdl(k_tree_sample<false>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
                     tree_dev(L), tree, n, (const uint64_t*)nullptr, seed, (uint64_t)0, beta, out_idx, out_q, out_qmin,
-                    out_w, dev_err, 0, 1, (int64_t)0, (const int64_t*)nullptr, 1, (int64_t*)nullptr);
+                    out_w, dev_err, 0, 1, (int64_t)0, (const int64_t*)nullptr, 1, (int64_t*)nullptr,
+                    (int64_t* const*)nullptr);
 }
 
 extern "C" int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t rank, int32_t n_shards,
@@ -780,7 +797,23 @@ extern "C" int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tre
   const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
   return launch_pdl(k_tree_sample<true>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
                     tree_dev(L), tree, n, draws, seed, offset, 0.0, out_idx, out_q, out_qmin, (float*)nullptr, dev_err,
-                    (int)rank, (int)n_shards, shard_leaves, shard_totals, (int)use_stream, out_count);
+                    (int)rank, (int)n_shards, shard_leaves, shard_totals, (int)use_stream, out_count,
+                    (int64_t* const*)nullptr);
+}
+
+extern "C" int rpl_sumtree_sample_sharded_p2p(const rpl_tree_layout* L, int64_t* tree, int32_t rank,
+                                              int32_t n_shards, int64_t shard_leaves, int64_t* const* boards,
+                                              int64_t n, uint64_t seed, int64_t* out_idx, int64_t* out_q,
+                                              int64_t* out_count, int32_t* dev_err, void* stream) {
+  if (!layout_ok(L) || !tree || !out_idx || !out_q || !out_count || !boards || n < 1 || n > (1ll << 30))
+    return RPL_EINVAL;
+  if (n_shards < 1 || n_shards > BOARD_MAX_WORLD || rank < 0 || rank >= n_shards || shard_leaves < L->n_leaves)
+    return RPL_EINVAL;
+  const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
+  return launch_pdl(k_tree_sample<true>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
+                    tree_dev(L), tree, n, (const uint64_t*)nullptr, seed, (uint64_t)0, 0.0, out_idx, out_q,
+                    (int64_t*)nullptr, (float*)nullptr, dev_err, (int)rank, (int)n_shards, shard_leaves,
+                    (const int64_t*)nullptr, 1, out_count, boards);
 }
 
 extern "C" int rpl_sumtree_find(const rpl_tree_layout* L, const int64_t* tree, const int64_t* prefix, int64_t n,

@@ -345,6 +345,25 @@ class SumTree:
               "rpl_sumtree_sample_sharded")
         return idx, q, qmin
 
+    def sample_sharded_p2p(self, rank, n_shards, board_ptrs, n, seed, count, out=None, err=None):
+        """rpl_sumtree_sample_sharded_p2p: compacted stream-mode sharded sampling with the
+        totals exchange (K5) fused in over the peer boards (board_ptrs: device int64 [n_shards]
+        of board addresses, see shard.PeerBoards).  Returns (idx, q); count = [m, k0]."""
+        n = int(n)
+        _req(board_ptrs, torch.int64, "board_ptrs", (n_shards,))
+        _req(count, torch.int64, "count", (2,))
+        if out is None:
+            idx = torch.empty(n, dtype=torch.int64, device=self.device)
+            q = torch.empty(n, dtype=torch.int64, device=self.device)
+        else:
+            idx, q = out
+        e = self.err if err is None else err
+        check(lib.rpl_sumtree_sample_sharded_p2p(self._lp, _ptr(self.storage), int(rank), int(n_shards),
+                                                 self.n_leaves, _ptr(board_ptrs), n, int(seed) & (2 ** 64 - 1),
+                                                 _ptr(idx), _ptr(q), _ptr(count), _ptr(e), self._s()),
+              "rpl_sumtree_sample_sharded_p2p")
+        return idx, q
+
     def find(self, prefix, err=None):
         _req(prefix, torch.int64, "prefix")
         out = torch.empty_like(prefix)
@@ -537,6 +556,14 @@ class GatherPlan:
     def set_cursor(self, cursor, size):
         self.desc.cursor = int(cursor)
         self.desc.size = int(size)
+
+    def set_peers(self, board_ptrs, world, rank):
+        """Fuse the batch-min exchange (K7) into the gather: board_ptrs as given to
+        SumTree.sample_sharded_p2p (None: off).  Needs with_weights and q at run time."""
+        self._peer_ptrs = board_ptrs  # keep the pointer array alive
+        self.desc.peer_boards = None if board_ptrs is None else board_ptrs.data_ptr()
+        self.desc.peer_world = int(world) if board_ptrs is not None else 0
+        self.desc.peer_rank = int(rank) if board_ptrs is not None else 0
 
     def run(self, idx, q=None, qmin=None, beta=0.0, err=None, stream=None):
         s = _stream(self.device) if stream is None else stream

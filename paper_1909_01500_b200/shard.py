@@ -19,6 +19,12 @@ concatenation of the trees (§8c #17; tests/test_gpu_sumtree.py).
 
 The tree object is duck-typed (total(), sample_sharded(), .device) so the
 protocol can be exercised with world-size-2 gloo on CPU (tests/test_shard_gloo.py).
+
+PeerBoards replaces both NCCL exchanges with stores into the peers' memory, fused into
+the kernels that need them: the sampler publishes its total and reads everyone's
+(rpl_sumtree_sample_sharded_p2p, K5), the gather publishes the batch-min q and reads
+everyone's while its frame copy runs (rpl_gather_desc.peer_boards, K7).  The step then has
+no collective launch at all: update -> sample -> gather -> n-step, as on one GPU.
 """
 from __future__ import annotations
 
@@ -104,3 +110,39 @@ class CentralBatch:
     def arrived(self):
         """K8: completion signal after this rank's gather (stream-ordered, 8 bytes)."""
         dist.all_reduce(self.flag, group=self.group)
+
+
+class PeerBoards:
+    """The exchange boards of rpl.h (RPL_BOARD_WORDS = 4 * world int64 words per rank):
+    this rank's board is allocated here, zeroed, exported through CUDA IPC and mapped by
+    every peer (all_gather_object of the IPC handles; NVLink P2P between GPUs, plain device
+    memory on a shared GPU).  `ptrs` is the device int64 [world] array of board addresses
+    the kernels take.  Construct on every rank at the same point (collective)."""
+
+    def __init__(self, group=None, device=None):
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.board = torch.zeros(4 * self.world, dtype=torch.int64, device=dev)
+        torch.cuda.synchronize(dev)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, reduce_tensor(self.board), group=group)
+        self._mapped = []
+        addrs = []
+        for g, (fn, args) in enumerate(handles):
+            if g == self.rank:
+                addrs.append(self.board.data_ptr())
+            else:
+                t = fn(*args)  # opens the peer's IPC handle in this process
+                self._mapped.append(t)
+                addrs.append(t.data_ptr())
+        self.ptrs = torch.tensor(addrs, dtype=torch.int64, device=dev)
+        dist.barrier(group=group)
+
+    @staticmethod
+    def local(boards):
+        """In-process boards for G 'ranks' sharing one process (tests): boards is a list of
+        device int64 tensors of 4*G words; returns the shared pointer array."""
+        return torch.tensor([b.data_ptr() for b in boards], dtype=torch.int64, device=boards[0].device)

@@ -49,16 +49,18 @@ def test_struct_layouts_match_c(tmp_path):
     prog = tmp_path / "sz.c"
     prog.write_text(
         '#include <stdio.h>\n#include <stddef.h>\n#include "rpl.h"\n'
-        "int main(){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(rpl_tree_layout),"
+        "int main(){printf(\"%zu %zu %zu %zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(rpl_tree_layout),"
         " offsetof(rpl_tree_layout, q_cap), offsetof(rpl_tree_layout, n_words), sizeof(rpl_gather_desc),"
         " offsetof(rpl_gather_desc, gamma), offsetof(rpl_gather_desc, o_rnn), offsetof(rpl_gather_desc, n_active),"
-        " offsetof(rpl_gather_desc, col_offset));return 0;}\n")
+        " offsetof(rpl_gather_desc, col_offset), offsetof(rpl_gather_desc, peer_boards),"
+        " offsetof(rpl_gather_desc, peer_rank));return 0;}\n")
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(prog), "-o", str(exe)])
     vals = [int(x) for x in subprocess.check_output([str(exe)]).split()]
     assert vals == [ctypes.sizeof(TreeLayout), TreeLayout.q_cap.offset, TreeLayout.n_words.offset,
                     ctypes.sizeof(GatherDesc), GatherDesc.gamma.offset, GatherDesc.o_rnn.offset,
-                    GatherDesc.n_active.offset, GatherDesc.col_offset.offset]
+                    GatherDesc.n_active.offset, GatherDesc.col_offset.offset, GatherDesc.peer_boards.offset,
+                    GatherDesc.peer_rank.offset]
 
 
 def test_host_validation_without_gpu(lib):
