@@ -369,7 +369,8 @@ typedef struct {
    * slots are padding (§8c #13).  With RPL_OUT_UNIQUE it is all a consumer needs to
    * rebuild the k-stacks (rpl_stack_frames) — Mode C ships unique rows + offsets. */
   int8_t* o_start;
-  /* Optional (SEQUENCE, default kernel only; qmin must be NULL): the K7 exchange fused into
+  /* Optional (SEQUENCE, default kernel only; q and o_w required, qmin NULL — else
+   * RPL_EINVAL): the K7 exchange fused into
    * the gather.  peer_boards = the device pointer array given to
    * rpl_sumtree_sample_sharded_p2p, peer_world = n_shards, peer_rank = this rank.  CTA 0
    * publishes this rank's batch-min q (over its owned entries; INT64_MAX if none) to every

@@ -1719,7 +1719,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
   if (desc->pad_mode != RPL_PAD_REPEAT && desc->pad_mode != RPL_PAD_ZERO) return RPL_EINVAL;
   if ((desc->o_act || desc->o_prev_act) && (!desc->act || desc->act_bytes < 1)) return RPL_EINVAL;
   if (desc->o_w && !(beta >= 0.0)) return RPL_EINVAL;
-  if (desc->peer_boards && (desc->kind != RPL_GATHER_SEQUENCE || qmin || desc->peer_world < 1 ||
+  if (desc->peer_boards && (desc->kind != RPL_GATHER_SEQUENCE || qmin || !q || !desc->o_w || desc->peer_world < 1 ||
                             desc->peer_world > BOARD_MAX_WORLD || desc->peer_rank < 0 ||
                             desc->peer_rank >= desc->peer_world))
     return RPL_EINVAL;

@@ -98,3 +98,27 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", txt, re.M), f
+
+
+def test_peer_gather_validation_without_gpu(lib):
+    # peer boards (fused K7) need q and o_w and no explicit qmin; rejected on the host
+    from paper_1909_01500_b200._lib import GatherDesc, lib as L
+    d = GatherDesc()
+    d.kind, d.k, d.cap_T, d.B, d.cursor, d.size, d.obs_bytes = 1, 4, 400, 4, 0, 400, 7056
+    d.seq_len, d.period = 45, 40
+    d.obs, d.done, d.o_obs, d.o_w = 16, 16, 16, 16          # never dereferenced on the host
+    d.peer_boards, d.peer_world, d.peer_rank = 16, 2, 0
+    one = ctypes.c_void_p(16)
+    assert L.rpl_gather(ctypes.byref(d), one, None, None, 0.6, 8, None, None) == -1      # q missing
+    assert L.rpl_gather(ctypes.byref(d), one, one, one, 0.6, 8, None, None) == -1       # explicit qmin
+    d.peer_rank = 2
+    assert L.rpl_gather(ctypes.byref(d), one, one, None, 0.6, 8, None, None) == -1      # rank >= world
+    d.peer_rank, d.kind = 0, 0
+    assert L.rpl_gather(ctypes.byref(d), one, one, None, 0.6, 8, None, None) == -1      # transitions
+    from paper_1909_01500_b200._lib import TreeLayout
+    lay = TreeLayout()
+    assert L.rpl_sumtree_layout(1000, 32, 32, ctypes.byref(lay)) == 0
+    sp = L.rpl_sumtree_sample_sharded_p2p
+    assert sp(ctypes.byref(lay), 16, 0, 2, 1000, None, 64, 1, 16, 16, 16, None, None) == -1   # no boards
+    assert sp(ctypes.byref(lay), 16, 0, 65, 1000, 16, 64, 1, 16, 16, 16, None, None) == -1    # > 64 shards
+    assert sp(ctypes.byref(lay), 16, 0, 2, 1000, 16, 64, 1, 16, 16, None, None, None) == -1   # no count
