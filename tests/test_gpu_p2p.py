@@ -155,3 +155,47 @@ def test_p2p_timeout_sets_error(rpl):
     t.sample_sharded_p2p(0, 2, ptrs, 16, 1, cnt, err=err)
     torch.cuda.synchronize()
     assert int(H(err)[0]) & 32
+
+
+def test_p2p_prefilled_peer(rpl):
+    # one rank's kernels alone, the peer's slots pre-written by the host with the step's tag
+    # (no concurrent kernel needed: also the sanitizer-friendly form of the protocol)
+    import torch
+    from paper_1909_01500_b200 import replay as R
+    from synth.device import make_ring_device
+    G, cap, B, period, L, k, n = 2, 400, 4, 40, 45, 4, 8
+    dev = torch.device("cuda")
+    ring = make_ring_device(301, cap, B, dev, ep_len=30.0, period=period, rnn_h=8, cursor=123, frame_shape=(8, 16))
+    t = rpl.SumTree((cap // period) * B, 32)
+    valid = R.leaves_of(R.valid_sequence_blocks(cap, period, ring.cursor, ring.size, k, L), B)
+    td = td_abs(rng(3), valid.size)
+    t.update(T_(valid), T_(td), 0.9)
+    o = OS.SumTreeOracle(t.n_leaves)
+    o.update([int(x) for x in valid], [float(x) for x in td], 0.9)
+    peer = OS.SumTreeOracle(t.n_leaves)  # rank 1: a copy of rank 0's shard
+    peer.q = list(o.q)
+    tag = n * G                           # stream position after the first step
+    board = torch.zeros(4 * G, dtype=torch.int64, device=dev)
+    board[2 * 1], board[2 * 1 + 1] = peer.total(), tag           # rank 1's K5 slot
+    ptrs = torch.tensor([board.data_ptr(), board.data_ptr()], dtype=torch.int64, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    idx, q = t.sample_sharded_p2p(0, G, ptrs, n * G, 5, cnt, err=err)
+    torch.cuda.synchronize()
+    ref_idx, ref_q, _ = OS.sharded_sample([o, peer], n * G, OP.draws_u64(5, 0, n * G))
+    m = int(H(cnt)[0])
+    own = [(i, qq) for i, qq in zip(ref_idx, ref_q) if i < t.n_leaves]
+    assert m == len(own) and H(idx)[:m].tolist() == [i for i, _ in own] and H(q)[:m].tolist() == [qq for _, qq in own]
+    peer_min = min(qq for i, qq in zip(ref_idx, ref_q) if i >= t.n_leaves)
+    board[2 * G + 2], board[2 * G + 3] = peer_min, tag          # rank 1's K7 slot
+    plan = rpl.GatherPlan(ring, n * G, kind="sequence", k=k, seq_len=L, period=period, with_weights=True)
+    plan.desc.n_active = cnt.data_ptr()
+    plan.set_peers(ptrs, G, 0)
+    out = plan.run(idx, q=q, beta=0.6, err=err)
+    torch.cuda.synchronize()
+    assert int(H(err)[0]) == 0
+    gmin = min(min(qq for _, qq in own), peer_min)
+    w = H(out["w"])[:m]
+    ref_w = [(gmin / qq) ** 0.6 for _, qq in own]
+    assert np.allclose(w, ref_w, rtol=1e-6, atol=0)
+    assert int(H(board)[2 * G]) == min(qq for _, qq in own) and int(H(board)[2 * G + 1]) == tag
