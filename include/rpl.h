@@ -491,6 +491,12 @@ int rpl_debug_set_gather_variant(int32_t variant);
  * (segment boundaries differ).  RPL_EINVAL outside 0..6. */
 int rpl_debug_set_scan_variant(int32_t variant);
 
+/* Measurement / test only: 1 (default; initial value from RPL_TREE_STAGE, "0" = off) lets
+ * the samplers stage the tree's top levels (whole levels, up to 4351 words from the root) in
+ * shared memory before the descent; 0 descends from global memory only.  Identical outputs.
+ * RPL_EINVAL for other values. */
+int rpl_debug_set_tree_stage(int32_t on);
+
 /* Diagnostics (measurement only): bit mask applied to the default sequence gather.
  * 1 = skip the frame stores, 2 = skip the frame loads (outputs are then garbage),
  * 4 = normal-priority frame stores, 8 = normal L2 policy on the frame loads (the default is

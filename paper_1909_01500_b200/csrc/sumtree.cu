@@ -17,6 +17,9 @@
 //          ballot(prefix < incl) picks the child.  The last CTA (ticket in the tree
 //          header) reduces the batch-min q and writes the IS weights (a9).
 #include <math.h>
+#include <stdlib.h>
+
+#include <atomic>
 
 #include "common.cuh"
 #include "crpow.cuh"
@@ -28,6 +31,27 @@ constexpr int UPD_THREADS = 1024;
 constexpr int HASH_SLOTS = 2048;
 constexpr unsigned long long HASH_EMPTY = ~0ull;
 constexpr int SAMPLE_WARPS = 8;
+// Shared-memory staging of the tree's top levels in the sampler (34 KB): R2D2 1M-step
+// (25,600 leaves) stages root + 2 levels, DQN 2^20 leaves root + 2 of 4, toy trees all.
+constexpr int STAGE_WORDS = 4352;
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// Words of the tree the sampler may stage (0 = none: base not 16-B aligned for the
+// 16-B async copies, or RPL_TREE_STAGE=0 for A/B measurement).  The copy of an odd last
+// word reads one word past the staged levels, which is still inside the tree (header).
+std::atomic<int> g_tree_stage{-1};  // -1: not set yet (read RPL_TREE_STAGE once)
+
+int64_t stage_cap(const int64_t* tree) {
+  int on = g_tree_stage.load(std::memory_order_relaxed);
+  if (on < 0) {
+    const char* e = getenv("RPL_TREE_STAGE");
+    int expect = -1;
+    g_tree_stage.compare_exchange_strong(expect, (e && e[0] == '0') ? 0 : 1);
+    on = g_tree_stage.load(std::memory_order_relaxed);
+  }
+  return (on && (reinterpret_cast<uintptr_t>(tree) & 15) == 0) ? (int64_t)STAGE_WORDS - 1 : 0;
+}
 
 enum { MODE_TD = 0, MODE_Q = 1, MODE_MAXSEEN = 2, MODE_SEQ = 3 };
 
@@ -239,15 +263,18 @@ __device__ __forceinline__ int64_t first_stratum_at_least(uint64_t x, uint64_t Q
   return lo;
 }
 
-// Descend from the root for `prefix` (< node sum); returns leaf index, writes q.
+// Descend from the root for `prefix` (< node sum); returns leaf index, writes q.  Words
+// [0, n_top) of the tree (whole top levels) may be staged in shared memory (`top`): those
+// levels are read from there, the rest from global memory.
 __device__ __forceinline__ int64_t descend(const TreeDev& L, const int64_t* __restrict__ tree,
-                                           int64_t prefix, int64_t* q_out, int32_t* errbits) {
+                                           int64_t prefix, int64_t* q_out, int32_t* errbits,
+                                           const int64_t* top = nullptr, int64_t n_top = 0) {
   const int lane = threadIdx.x & 31;
   int64_t node = 0;
   int64_t c = 0;
   for (int l = 0; l < L.depth; ++l) {
     const int64_t base = L.level_off[l + 1] + (node << L.log2w);
-    c = lane < L.fanout ? tree[base + lane] : 0;
+    c = lane < L.fanout ? (base < n_top ? top[base + lane] : tree[base + lane]) : 0;
     int64_t incl = c;
 #pragma unroll
     for (int dlt = 1; dlt < 32; dlt <<= 1) {
@@ -283,9 +310,22 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
               int64_t* __restrict__ out_q, int64_t* __restrict__ out_qmin, float* __restrict__ out_w,
               int32_t* err, int rank, int n_shards, int64_t shard_leaves,
               const int64_t* __restrict__ totals, int use_stream, int64_t* __restrict__ out_count,
-              int64_t* const* boards) {
+              int64_t* const* boards, int64_t stage_cap) {
   const int lane = threadIdx.x & 31;
   pdl_wait();
+  // Stage the top levels (root .. the deepest level that still fits STAGE_WORDS) in shared
+  // memory with one round of asynchronous 16-B copies, so the descent's first levels and Q
+  // cost one L2 round trip in total instead of one each.  Levels are contiguous from word 0.
+  __shared__ __align__(16) int64_t s_top[STAGE_WORDS];
+  int64_t n_top = 0;
+  for (int l = 0; l <= L.depth; ++l) {
+    const int64_t end = l < L.depth ? L.level_off[l + 1] : L.hdr_off;
+    if (end > stage_cap) break;
+    n_top = end;
+  }
+  for (int64_t j = 2 * (int64_t)threadIdx.x; j < n_top; j += 2 * (int64_t)blockDim.x)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s_u32(s_top + j)), "l"(tree + j) : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
   // Without a batch reduction (no IS weights, no qmin requested) there is no grid-wide
   // end ticket; a stream-mode call then takes its ticket at the start instead: every CTA
   // reads the stream position (acquire: ordered before its ticket increment) and the CTA
@@ -298,6 +338,8 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
   }
   __shared__ unsigned long long s_t0;
   if (use_stream && !reduce && threadIdx.x == 0) s_t0 = atomicAdd(ticket, 1ull);
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
   // Philox counter base: offset, plus the tree's stream position when use_stream
   const uint64_t ctr0 = offset + spos;
   const int64_t k = (int64_t)blockIdx.x * SAMPLE_WARPS + (threadIdx.x >> 5);
@@ -327,7 +369,7 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
       Q += tg;
     }
   } else {
-    Q = (uint64_t)tree[L.level_off[0]];
+    Q = (uint64_t)(n_top > 0 ? s_top[0] : tree[L.level_off[0]]);
   }
   // compacted sharded output: the owned run of strata [k0, k1) goes to positions
   // 0 .. m-1 (stratum order), positions m .. n-1 get -1; *out_count = m
@@ -350,7 +392,7 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
         prefix -= own_lo;
       }
       if (mine) {
-        leaf = descend(L, tree, (int64_t)prefix, &q, &errbits);
+        leaf = descend(L, tree, (int64_t)prefix, &q, &errbits, s_top, n_top);
         // global index (shard-major, §8c #17); the compacted form keeps the LOCAL leaf
         // for the owner's own update / gather
         if (SHARDED && !compact) leaf += (int64_t)rank * shard_leaves;
@@ -771,7 +813,7 @@ extern "C" int rpl_sumtree_sample(const rpl_tree_layout* L, int64_t* tree, int64
   const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
   return launch_pdl(k_tree_sample<false>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
                     tree_dev(L), tree, n, draws, seed, offset, beta, out_idx, out_q, out_qmin, out_w, dev_err, 0, 1,
-                    (int64_t)0, (const int64_t*)nullptr, 0, (int64_t*)nullptr, (int64_t* const*)nullptr);
+                    (int64_t)0, (const int64_t*)nullptr, 0, (int64_t*)nullptr, (int64_t* const*)nullptr, stage_cap(tree));
 }
 
 extern "C" int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree, int64_t n, uint64_t seed,
@@ -783,7 +825,7 @@ extern "C" int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree
   return launch_pdl(k_tree_sample<false>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
                     tree_dev(L), tree, n, (const uint64_t*)nullptr, seed, (uint64_t)0, beta, out_idx, out_q, out_qmin,
                     out_w, dev_err, 0, 1, (int64_t)0, (const int64_t*)nullptr, 1, (int64_t*)nullptr,
-                    (int64_t* const*)nullptr);
+                    (int64_t* const*)nullptr, stage_cap(tree));
 }
 
 extern "C" int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t rank, int32_t n_shards,
@@ -798,7 +840,7 @@ extern "C" int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tre
   return launch_pdl(k_tree_sample<true>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
                     tree_dev(L), tree, n, draws, seed, offset, 0.0, out_idx, out_q, out_qmin, (float*)nullptr, dev_err,
                     (int)rank, (int)n_shards, shard_leaves, shard_totals, (int)use_stream, out_count,
-                    (int64_t* const*)nullptr);
+                    (int64_t* const*)nullptr, stage_cap(tree));
 }
 
 extern "C" int rpl_sumtree_sample_sharded_p2p(const rpl_tree_layout* L, int64_t* tree, int32_t rank,
@@ -813,7 +855,7 @@ extern "C" int rpl_sumtree_sample_sharded_p2p(const rpl_tree_layout* L, int64_t*
   return launch_pdl(k_tree_sample<true>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
                     tree_dev(L), tree, n, (const uint64_t*)nullptr, seed, (uint64_t)0, 0.0, out_idx, out_q,
                     (int64_t*)nullptr, (float*)nullptr, dev_err, (int)rank, (int)n_shards, shard_leaves,
-                    (const int64_t*)nullptr, 1, out_count, boards);
+                    (const int64_t*)nullptr, 1, out_count, boards, stage_cap(tree));
 }
 
 extern "C" int rpl_sumtree_find(const rpl_tree_layout* L, const int64_t* tree, const int64_t* prefix, int64_t n,
@@ -929,4 +971,10 @@ extern "C" int rpl_sumtree_update_sample(const rpl_tree_layout* L, int64_t* tree
   return launch_pdl(k_tree_update_sample, dim3((unsigned)blocks), dim3(FUSED_THREADS), 0, as_stream(stream),
                     tree_dev(L), tree, idx, td, n_upd, T_p, eta, alpha, eps_p, (flags & RPL_UPD_LIVE_ONLY) ? 1 : 0, n,
                     seed, out_idx, out_q, dev_err);
+}
+
+extern "C" int rpl_debug_set_tree_stage(int32_t on) {
+  if (on != 0 && on != 1) return RPL_EINVAL;
+  g_tree_stage.store(on);
+  return RPL_OK;
 }

@@ -1,0 +1,26 @@
+// Size-matched floors for one PPO return call ([128,4096]: 4.6 MB in, 4.2 MB out), for
+// context on the scan's per-call time (not product code).  which: 0 = empty kernel
+// (launch floor), 1 = GAE-shaped streaming pass (r, V, d in; two f32 outputs; no scan).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+__global__ void k_empty() {}
+
+__global__ void k_stream(const float4* __restrict__ r, const float4* __restrict__ v, const uchar4* __restrict__ d,
+                         float4* __restrict__ o0, float4* __restrict__ o1, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 a = __ldg(r + i), b = __ldg(v + i);
+    const uchar4 m = __ldg(d + i);
+    o0[i] = make_float4(a.x - b.x * m.x, a.y - b.y * m.y, a.z - b.z * m.z, a.w - b.w * m.w);
+    o1[i] = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+  }
+}
+
+extern "C" int ppo_floor(int which, const void* r, const void* v, const void* d, void* o0, void* o1, int64_t n,
+                         int grid, int block, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (which == 0) k_empty<<<1, 32, 0, st>>>();
+  else k_stream<<<grid, block, 0, st>>>((const float4*)r, (const float4*)v, (const uchar4*)d, (float4*)o0,
+                                        (float4*)o1, n / 4);
+  return (int)cudaGetLastError();
+}

@@ -112,8 +112,17 @@ def test_priority_values_near_midpoints(rpl):
     assert np.array_equal(H(v_fast), H(v_slow))
 
 
+@pytest.fixture(params=[1, 0])
+def tree_stage(rpl, request):
+    # 1: the sampler stages the top levels in shared memory (all of a small tree; root +
+    # 3 levels of 70000 leaves); 0: every level from global memory
+    assert rpl._lib.lib.rpl_debug_set_tree_stage(request.param) == 0
+    yield request.param
+    rpl._lib.lib.rpl_debug_set_tree_stage(1)
+
+
 @pytest.mark.parametrize("n_leaves,W", [(16, 32), (100, 4), (1000, 32), (5000, 16), (70000, 32)])
-def test_random_updates_vs_oracle(rpl, n_leaves, W):
+def test_random_updates_vs_oracle(rpl, n_leaves, W, tree_stage):
     g = rng(n_leaves + W)
     tree = rpl.SumTree(n_leaves, W)
     orc = OS.SumTreeOracle(n_leaves)
