@@ -332,14 +332,22 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
   // that arrives last advances the position once all CTAs have read it.
   const bool reduce = out_w != nullptr || out_qmin != nullptr;
   unsigned long long* ticket = reinterpret_cast<unsigned long long*>(tree + L.hdr_off + 1);
+  // Thread 0 alone reads the stream position (acquire), in flight with the staging copies,
+  // and broadcasts it at the staging barrier; its ticket increment follows the read in
+  // program order, so no CTA can advance the position before every CTA has read it.  The
+  // ticket value stays in thread 0's register until the end, so that round trip overlaps
+  // the descent.
   uint64_t spos = 0;
-  if (use_stream) {
+  __shared__ uint64_t s_spos;
+  unsigned long long t0 = 0;
+  if (use_stream && threadIdx.x == 0) {
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(spos) : "l"(tree + L.hdr_off + 2) : "memory");
+    s_spos = spos;
+    if (!reduce) t0 = atomicAdd(ticket, 1ull);
   }
-  __shared__ unsigned long long s_t0;
-  if (use_stream && !reduce && threadIdx.x == 0) s_t0 = atomicAdd(ticket, 1ull);
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
+  if (use_stream) spos = s_spos;
   // Philox counter base: offset, plus the tree's stream position when use_stream
   const uint64_t ctr0 = offset + spos;
   const int64_t k = (int64_t)blockIdx.x * SAMPLE_WARPS + (threadIdx.x >> 5);
@@ -421,9 +429,8 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
   if (lane == 0 && errbits) set_err(err, errbits);
 
   if (!reduce) {
-    if (use_stream) {
-      __syncthreads();
-      if (threadIdx.x == 0 && s_t0 == (unsigned long long)gridDim.x - 1) {
+    if (use_stream) {  // only thread 0s read the position (before their tickets): no barrier
+      if (threadIdx.x == 0 && t0 == (unsigned long long)gridDim.x - 1) {
         tree[L.hdr_off + 2] = (int64_t)(spos + (uint64_t)n);  // advance the stream
         *ticket = 0ull;
       }
@@ -435,13 +442,16 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
   __shared__ int64_t s_min[SAMPLE_WARPS];
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned long long t = atomicAdd(ticket, 1ull);
+    // acq_rel ticket instead of __threadfence + atomicAdd: the CTA's output writes (ordered
+    // before thread 0 by the barrier) are released with the arrival, and the last CTA
+    // acquires every other CTA's.  A full fence.sc costs ~1 us here (measured on the
+    // update+sample overlay trial, profiles/r1/README.md).
+    unsigned long long t;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(t) : "l"(ticket) : "memory");
     s_last = (t == (unsigned long long)gridDim.x - 1);
   }
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   int64_t m = INT64_MAX;
   for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
     const int64_t qj = __ldcg(out_q + j);
@@ -489,11 +499,12 @@ __device__ __forceinline__ void grid_barrier(int64_t* hdr) {
     unsigned long long* gen = reinterpret_cast<unsigned long long*>(hdr + 4);
     unsigned long long g;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(g) : "l"(gen) : "memory");
-    __threadfence();  // this CTA's tree writes before its arrival
-    const unsigned long long t = atomicAdd(cnt, 1ull);
+    // acq_rel arrival: this CTA's tree writes (ordered before thread 0 by the barrier) are
+    // released with it, and the last arriver acquires them all (no fence.sc; see k_tree_sample)
+    unsigned long long t;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(t) : "l"(cnt) : "memory");
     if (t == (unsigned long long)gridDim.x - 1) {
-      *cnt = 0ull;
-      __threadfence();
+      *cnt = 0ull;  // ordered before the generation bump by its release
       asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(gen), "l"(g + 1ull) : "memory");
     } else {
       unsigned long long cur;
