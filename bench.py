@@ -433,7 +433,19 @@ def run_rpl(args):
     for i in range(Kg):
         step(i, evs[i])
     torch.cuda.synchronize()
-    g_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    g_ms_eager = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    # the same launch inside the timed configuration: a graph of P steps whose gathers are
+    # bracketed by event-record nodes (cudaEventRecordExternal), so no host enqueue gap
+    # falls inside the interval.  The nodes break the PDL edge into the gather (its launch
+    # latency is inside the interval), so this is still an upper bound on the launch's
+    # share of the graph step.
+    g_ms_graph = None
+    if use_graph and world == 1:
+        try:
+            g_ms_graph = gather_ms_in_graph(dev, step, P)
+        except Exception as e:  # pragma: no cover - keep the eager figure
+            print(f"[bench] in-graph gather timing failed ({type(e).__name__}: {e})", file=sys.stderr)
+    g_ms = g_ms_graph if g_ms_graph is not None else g_ms_eager
     owned = n  # per rank, on average
     alg_bytes = owned * seq_bytes_per_sample(c)
     if mode_c:  # Mode C gathers unique rows (the learner re-stacks them)
@@ -468,6 +480,10 @@ def run_rpl(args):
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic.get("bytes"), "traffic_source": traffic.get("source"),
                      "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": g_ms,
+                     "avg_launch_ms_eager": g_ms_eager,
+                     "launch_timing": ("event-record nodes around each gather in the CUDA graph of the timed "
+                                       "steps (mean of P launches x 25 replays)" if g_ms_graph is not None
+                                       else "events around the gather in eager steps"),
                      "step_share": g_ms / (ms / K_eff),
                      "frac_of_spec": achieved / SPEC_HBM_GBS, "spec_peak": SPEC_HBM_GBS,
                      "spec_note": "north_star's ~8 TB/s nominal (DGX B200 figure) as the second denominator"},
@@ -850,6 +866,56 @@ def tree_latency(dev, rpl):
         res[f"N{N}_n{n}"] = {"sample_us": us_s, "update_us": us_u, "depth": t.depth}
         del t
     return {"unit": "us per launch (graph-replayed, back to back)", **res}
+
+
+class _ExtEvent:
+    """A timing event recorded with cudaEventRecordExternal, so that inside stream capture
+    it becomes an event-record node of the graph (torch's Event.record there only marks a
+    capture dependency)."""
+    _rt = None
+
+    def __init__(self):
+        import torch
+        self.ev = torch.cuda.Event(enable_timing=True)
+        self.ev.record()  # create the CUDA event
+        if _ExtEvent._rt is None:
+            import ctypes
+            import glob
+            import os as _os
+            import nvidia.cuda_runtime as _cr
+            libs = sorted(glob.glob(_os.path.join(list(_cr.__path__)[0], "lib", "libcudart.so*")))
+            rt = ctypes.CDLL(libs[0])
+            rt.cudaEventRecordWithFlags.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint]
+            rt.cudaEventRecordWithFlags.restype = ctypes.c_int
+            _ExtEvent._rt = rt
+
+    def record(self):
+        import torch
+        st = torch.cuda.current_stream().cuda_stream
+        rc = _ExtEvent._rt.cudaEventRecordWithFlags(self.ev.cuda_event, st, 1)  # cudaEventRecordExternal
+        if rc != 0:
+            raise RuntimeError(f"cudaEventRecordWithFlags failed ({rc})")
+
+
+def gather_ms_in_graph(dev, step, P, reps=25):
+    """Mean gather launch duration (ms) over the P gathers of a graph of P steps, each
+    bracketed by event-record nodes; averaged over `reps` replays."""
+    import torch
+    evs = [(_ExtEvent(), _ExtEvent()) for _ in range(P)]
+    torch.cuda.synchronize()
+    st = torch.cuda.Stream(dev)
+    st.wait_stream(torch.cuda.current_stream(dev))
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=st):
+        for i in range(P):
+            step(i, evs[i])
+    torch.cuda.synchronize()
+    tot = 0.0
+    for _ in range(reps):
+        gr.replay()
+        torch.cuda.synchronize()
+        tot += sum(a.ev.elapsed_time(b.ev) for a, b in evs) / P
+    return tot / reps
 
 
 def _graph_time(dev, step, P=8, reps=25):
