@@ -251,6 +251,14 @@ int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t 
  * than ~2 s gives up and sets RPL_DERR_PEER. */
 #define RPL_BOARD_WORDS(n_shards) (4 * (int64_t)(n_shards))
 
+/* Host plumbing for the boards: lets kernels running on the calling thread's current device
+ * load from / store to memory of device `peer_device` (a peer rank's board mapped through
+ * CUDA IPC lives in that device's memory), i.e. cudaDeviceEnablePeerAccess from the current
+ * device.  RPL_OK if access is now enabled, was already enabled, or peer_device is the
+ * current device; RPL_EUNSUPPORTED if the two devices cannot access each other (no
+ * NVLink / PCIe P2P path); RPL_EINVAL for a bad device index.  Synchronous, host only. */
+int rpl_peer_access(int32_t peer_device);
+
 /* rpl_sumtree_sample_sharded (stream mode, compacted) with the K5 exchange fused in: the
  * kernel publishes this tree's total to every peer's board and reads all n_shards totals
  * from its own, replacing rpl_sumtree_total + an all-gather + the sampler.  out_count

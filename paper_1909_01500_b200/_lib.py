@@ -104,6 +104,7 @@ _SIGS = {
                             C.c_int),
     "rpl_debug_priority_values": ([P, I64, D, D, I32, P, P, P], C.c_int),
     "rpl_debug_set_gather_variant": ([I32], C.c_int),
+    "rpl_peer_access": ([I32], C.c_int),
     "rpl_debug_set_scan_variant": ([I32], C.c_int),
     "rpl_debug_set_tree_stage": ([I32], C.c_int),
     "rpl_debug_set_gather_diag": ([I32], C.c_int),

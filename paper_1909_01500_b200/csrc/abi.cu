@@ -31,3 +31,19 @@ extern "C" const char* rpl_strerror(int status) {
 extern "C" int rpl_abi_version(void) { return RPL_ABI_VERSION; }
 
 extern "C" int64_t rpl_launch_count(void) { return rpl::g_launches.load(); }
+
+extern "C" int rpl_peer_access(int32_t peer) {
+  int cur = 0, n = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess || cudaGetDeviceCount(&n) != cudaSuccess) return RPL_ECUDA;
+  if (peer < 0 || peer >= n) return RPL_EINVAL;
+  if (peer == cur) return RPL_OK;
+  int can = 0;
+  if (cudaDeviceCanAccessPeer(&can, cur, peer) != cudaSuccess) return RPL_ECUDA;
+  if (!can) return RPL_EUNSUPPORTED;
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    (void)cudaGetLastError();  // clear the sticky-free status the call left
+    return RPL_OK;
+  }
+  return e == cudaSuccess ? RPL_OK : RPL_ECUDA;
+}

@@ -136,6 +136,15 @@ class PeerBoards:
                 addrs.append(self.board.data_ptr())
             else:
                 t = fn(*args)  # opens the peer's IPC handle in this process
+                if t.device != self.board.device:
+                    # the mapping lives in the peer GPU's memory: this device's kernels need
+                    # peer access to it (NVLink P2P); fail loudly when there is no path
+                    from . import _lib
+                    with torch.cuda.device(self.board.device):
+                        rc = _lib.lib.rpl_peer_access(t.device.index)
+                    if rc != 0:
+                        raise RuntimeError(f"rpl_peer_access({t.device.index}) from {self.board.device}: "
+                                           f"{_lib.lib.rpl_strerror(rc).decode()}")
                 self._mapped.append(t)
                 addrs.append(t.data_ptr())
         self.ptrs = torch.tensor(addrs, dtype=torch.int64, device=dev)
