@@ -285,8 +285,17 @@ def run_rpl(args):
             plan.desc.col_offset = n_owned.data_ptr() + 8
         if p2p:  # K5 / K7 through peer-memory boards, fused into the sampler and the gather
             from paper_1909_01500_b200.shard import PeerBoards
-            boards = PeerBoards(device=dev)
-            plan.set_peers(boards.ptrs, world, rank)
+            try:
+                boards = PeerBoards(device=dev)
+                ok = torch.tensor([1], dtype=torch.int32, device=dev)
+            except RuntimeError as e:  # no peer path to some rank: every rank falls back together
+                print(f"[bench] rank {rank}: peer boards unavailable ({e}); using NCCL collectives", file=sys.stderr)
+                ok = torch.tensor([0], dtype=torch.int32, device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 1:
+                plan.set_peers(boards.ptrs, world, rank)
+            else:
+                p2p, boards = False, None
 
     def all_gather_totals():
         if args.backend == "nccl":

@@ -131,6 +131,18 @@ class PeerBoards:
         dist.all_gather_object(handles, reduce_tensor(self.board), group=group)
         self._mapped = []
         addrs = []
+        failure = None
+        try:
+            self._map(handles, dev, addrs)
+        except RuntimeError as e:  # agree on the outcome before raising (no rank left in a collective)
+            failure = e
+        ok = torch.tensor([0 if failure else 1], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            raise RuntimeError(f"peer boards unavailable on some rank ({failure or 'a peer failed'})")
+        self.ptrs = torch.tensor(addrs, dtype=torch.int64, device=dev)
+
+    def _map(self, handles, dev, addrs):
         for g, (fn, args) in enumerate(handles):
             if g == self.rank:
                 addrs.append(self.board.data_ptr())
@@ -147,8 +159,6 @@ class PeerBoards:
                                            f"{_lib.lib.rpl_strerror(rc).decode()}")
                 self._mapped.append(t)
                 addrs.append(t.data_ptr())
-        self.ptrs = torch.tensor(addrs, dtype=torch.int64, device=dev)
-        dist.barrier(group=group)
 
     @staticmethod
     def local(boards):
