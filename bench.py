@@ -538,7 +538,14 @@ def e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K, world):
     inputs (the previous batch's |delta| and the target-net Q rows) from pinned host
     memory and reads the step's result (targets, IS weights, indices) back."""
     import torch
-    K = min(K, 300)
+    K = min(K, 320)
+    # graphs of PE steps: the one join per graph (the last step's D2H read-back) is paid
+    # once per PE steps; every step still copies its own inputs and results
+    PE = 32 if world == 1 and not args.no_graph else P
+    rep = [j % P for j in range(PE)]
+    td0, q0 = td_pool, q_pool  # the buffers step(i) reads in the eager path
+    td_pool = td_pool[rep].contiguous()
+    q_pool = q_pool[rep].contiguous()
     h_td = torch.empty(td_pool.shape, dtype=torch.float32).pin_memory()
     h_q = torch.empty(q_pool.shape, dtype=torch.float32).pin_memory()
     h_td.copy_(td_pool.cpu())
@@ -549,8 +556,8 @@ def e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K, world):
     torch.cuda.synchronize()
 
     def e2e_step(i):
-        td_pool[i % P].copy_(h_td[i % P], non_blocking=True)
-        q_pool[i % P].copy_(h_q[i % P], non_blocking=True)
+        td0[i % P].copy_(h_td[i % P], non_blocking=True)
+        q0[i % P].copy_(h_q[i % P], non_blocking=True)
         step(i)
         h_y.copy_(y, non_blocking=True)
         h_w.copy_(w, non_blocking=True)
@@ -564,21 +571,21 @@ def e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K, world):
     cs = torch.cuda.Stream(dev)
     td_set = [td_pool, torch.empty_like(td_pool)]
     q_set = [q_pool, torch.empty_like(q_pool)]
-    idx_all = [torch.full_like(idx_buf[0], -1) for _ in range(P)]
-    y_all = [torch.empty_like(y) for _ in range(P)]
-    w_all = [torch.empty_like(w) for _ in range(P)]
-    h_y_all = [torch.empty(y.shape, dtype=torch.float32).pin_memory() for _ in range(P)]
-    h_w_all = [torch.empty(w.shape, dtype=torch.float32).pin_memory() for _ in range(P)]
-    h_i_all = [torch.empty(idx_buf[0].shape, dtype=torch.int64).pin_memory() for _ in range(P)]
+    idx_all = [torch.full_like(idx_buf[0], -1) for _ in range(PE)]
+    y_all = [torch.empty_like(y) for _ in range(PE)]
+    w_all = [torch.empty_like(w) for _ in range(PE)]
+    h_y_all = [torch.empty(y.shape, dtype=torch.float32).pin_memory() for _ in range(PE)]
+    h_w_all = [torch.empty(w.shape, dtype=torch.float32).pin_memory() for _ in range(PE)]
+    h_i_all = [torch.empty(idx_buf[0].shape, dtype=torch.int64).pin_memory() for _ in range(PE)]
 
     def prefetched(par):
         main = torch.cuda.current_stream(dev)
         cs.wait_stream(main)
         with torch.cuda.stream(cs):  # the next graph's inputs (set 1 - par)
-            for j in range(P):
+            for j in range(PE):
                 td_set[1 - par][j].copy_(h_td[j], non_blocking=True)
                 q_set[1 - par][j].copy_(h_q[j], non_blocking=True)
-        for j in range(P):
+        for j in range(PE):
             step(j, y_out=y_all[j], w_out=w_all[j], io=(td_set[par][j], q_set[par][j], idx_all[j], idx_all[j - 1]))
             ev = torch.cuda.Event()
             ev.record(main)
@@ -610,8 +617,8 @@ def e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K, world):
             print(f"[bench] e2e graph capture failed ({e}); eager", file=sys.stderr)
             graphs = None
             torch.cuda.synchronize()
-    reps = max(2, K // P)
-    K = reps * P if graphs is not None else K
+    reps = max(2, K // PE)
+    K = reps * PE if graphs is not None else K
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     if graphs is not None:
@@ -627,7 +634,7 @@ def e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K, world):
     db = y.numel() * 4 + w.numel() * 4 + idx_buf[0].numel() * 8
     return {"value": K * n * world / (ms / 1e3), "unit": "sequences/s", "h2d_bytes_per_step": hb,
             "d2h_bytes_per_step": db, "steps": K,
-            "timing": ("cuda graphs of 8 steps; per step one pinned-host H2D input set (prefetched one graph "
+            "timing": (f"cuda graphs of {PE} steps; per step one pinned-host H2D input set (prefetched one graph "
                        "ahead into alternating slots) and the D2H of its results right after it, on a copy "
                        "stream overlapping compute") if graphs is not None
             else "eager launches incl. pinned-host H2D/D2H copies"}
