@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="rpl", choices=["rpl", "reference"])
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph")
+    ap.add_argument("--graph-steps", type=int, default=8, help="steps per captured CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget (cpu_baseline)")
@@ -237,7 +238,7 @@ def run_rpl(args):
     g = rng(77 + rank)
     td0 = np.abs(g.normal(size=valid.numel())).astype(np.float32)
     tree.update(valid, torch.from_numpy(td0).to(dev), c["alpha"], c["eps_p"])
-    P = 8  # distinct per-step |delta| and target-Q inputs (cycled)
+    P = args.graph_steps  # steps per CUDA graph = distinct per-step |delta| and target-Q inputs (cycled)
     # per-step |delta| of the previous batch's train rows, [P][train, n_glob] (R2D2 learner output)
     td_pool = torch.from_numpy(np.abs(g.normal(size=(P, c["train"], n * max(1, world)))).astype(np.float32)).to(dev)
     n_glob = n * world
@@ -479,7 +480,7 @@ def run_rpl(args):
         "dtype": "u8 frames + f32 (fp64 accum) + int64 tree",
         "data": "synthetic (seeded; uniform-random 84x84 u8 frames, R2D2 reward/episode recipe, DESIGN.md)",
         "config": dict(r2d2_config(c, world, args.mode),
-                       timing="cuda graph of 8 steps, replayed" if use_graph else "eager launches",
+                       timing=f"cuda graph of {P} steps, replayed" if use_graph else "eager launches",
                        tree=("update+sample fused (rpl_sumtree_update_sample)" if world == 1 and args.tree_fused
                              else "update_seq, then sample"),
                        exchange=(None if world == 1 else "p2p boards (K5 in the sampler, K7 in the gather)" if p2p

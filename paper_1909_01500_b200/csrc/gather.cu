@@ -883,6 +883,13 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   const int nv = ob / 16;
   const int cap = (int)D.cap_T, Bc = (int)D.B, period = (int)D.period;
   const int64_t nleaves = (int64_t)(cap / period) * Bc;
+  // shared-memory setup that reads no global memory runs before the dependency wait, while
+  // the sampler finishes
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+  }
+  for (int c = tid; c < PL_MAX_ROWS; c += NT) row_done[c] = 0;
   pdl_wait();  // idx (and n_active) come from the sampler launched just before
   // rows g = s*L + tau of the active samples, split evenly over the grid
   const int total = (int)(active_n(D, n) * L);
@@ -910,12 +917,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   const int s_first = g0 / L;
   const int npieces = (g1 - 1) / L - s_first + 1;
 
-  if (tid == 0) {
-    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
-    fence_mbar_init();
-    s_npieces = npieces;
-  }
-  for (int c = tid; c < nrows; c += NT) row_done[c] = 0;
+  if (tid == 0) s_npieces = npieces;
   // (A) pieces, in parallel: one sampled leaf each
   for (int pc = tid; pc < npieces; pc += NT) {
     const int sm = s_first + pc;
