@@ -890,6 +890,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
     fence_mbar_init();
   }
   for (int c = tid; c < PL_MAX_ROWS; c += NT) row_done[c] = 0;
+  if (RPL_PDL_EARLY & 4) pdl_trigger();  // A/B knob (common.cuh)
   pdl_wait();  // idx (and n_active) come from the sampler launched just before
   // rows g = s*L + tau of the active samples, split evenly over the grid
   const int total = (int)(active_n(D, n) * L);

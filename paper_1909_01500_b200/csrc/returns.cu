@@ -420,6 +420,7 @@ __global__ void k_nstep(const float* __restrict__ r, const uint8_t* __restrict__
                         float* __restrict__ out, uint8_t* __restrict__ done_out) {
   const int64_t rows = T - n + 1;
   const int64_t total = rows * B;
+  if (RPL_PDL_EARLY & 8) pdl_trigger();  // A/B knob (common.cuh)
   pdl_wait();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {

@@ -230,6 +230,7 @@ k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__
               const float* __restrict__ td, const int64_t* __restrict__ qin, int mode, int64_t n,
               double alpha, double eps_p, int32_t* err, int force_slow, int64_t T_p, double eta, int live_only) {
   __shared__ UpdSmem S;
+  if (RPL_PDL_EARLY & 1) pdl_trigger();  // A/B knob (common.cuh)
   pdl_wait();
   tree_update_block<UPD_THREADS>(S, L, tree, idx, td, qin, mode, n, alpha, eps_p, err, force_slow, T_p, eta,
                                  live_only);
@@ -312,6 +313,7 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
               const int64_t* __restrict__ totals, int use_stream, int64_t* __restrict__ out_count,
               int64_t* const* boards, int64_t stage_cap) {
   const int lane = threadIdx.x & 31;
+  if (RPL_PDL_EARLY & 2) pdl_trigger();  // A/B knob (common.cuh)
   pdl_wait();
   // Stage the top levels (root .. the deepest level that still fits STAGE_WORDS) in shared
   // memory with one round of asynchronous 16-B copies, so the descent's first levels and Q
