@@ -27,10 +27,16 @@
 namespace rpl {
 namespace {
 
-constexpr int UPD_THREADS = 1024;
+#ifndef RPL_UPD_THREADS  // build-flag knobs for A/B measurement (scripts/ab_flags.sh)
+#define RPL_UPD_THREADS 512  // same-box A/B: 68.87 vs 69.25 us per R2D2 step at 1024 (256: two td passes, +1.1 us)
+#endif
+#ifndef RPL_SAMPLE_WARPS
+#define RPL_SAMPLE_WARPS 8
+#endif
+constexpr int UPD_THREADS = RPL_UPD_THREADS;
 constexpr int HASH_SLOTS = 2048;
 constexpr unsigned long long HASH_EMPTY = ~0ull;
-constexpr int SAMPLE_WARPS = 8;
+constexpr int SAMPLE_WARPS = RPL_SAMPLE_WARPS;
 // Shared-memory staging of the tree's top levels in the sampler (34 KB): R2D2 1M-step
 // (25,600 leaves) stages root + 2 levels, DQN 2^20 leaves root + 2 of 4, toy trees all.
 constexpr int STAGE_WORDS = 4352;
