@@ -485,9 +485,9 @@ int rpl_debug_priority_values(const float* td_abs, int64_t n, double alpha, doub
                               int32_t force_slow, float* out_v, uint8_t* out_slow, void* stream);
 
 /* Diagnostics (tests only): select the sequence-gather kernel, 0 = persistent pipeline with
- * TMA loads and LSU stores (default, 8 consumer warps), 1 = one CTA per 8-row chunk (TMA both
+ * TMA loads and LSU stores (default, 4 consumer warps), 1 = one CTA per 8-row chunk (TMA both
  * ways), 2 = frame-centric LSU copy, 3 = persistent all-TMA pipeline, 4 / 5 = variant 0 with
- * 14 / 4 consumer warps, 6 = LSU frame loads with TMA bulk stores.  All produce identical
+ * 14 / 8 consumer warps, 6 = LSU frame loads with TMA bulk stores.  All produce identical
  * outputs. */
 int rpl_debug_set_gather_variant(int32_t variant);
 

@@ -1690,9 +1690,15 @@ GDesc to_dev(const rpl_gather_desc* d) {
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 
-// 0: TMA-load / LSU-store pipeline (default, 8 consumer warps; 4: 14, 5: 4), 1: chunked all-TMA kernel, 2: frame-centric
+// 0: TMA-load / LSU-store pipeline (default, RPL_SEQ_CONSUMERS = 4 consumer warps; 4: 14, 5: 8), 1: chunked all-TMA kernel, 2: frame-centric
 // LSU, 3: all-TMA pipeline
 int g_seq_variant = 0;
+// Consumer warps of the default sequence gather (build-flag A/B knob).  Same-box A/B of the
+// R2D2 step (scripts/ab_flags.sh, 3 rounds; profiles/r1/README.md): 4 -> 68.88 us, 6 -> 69.04,
+// 8 -> 69.29, 5 -> 69.77; back to back the gather alone prefers 8, inside the step 4 wins.
+#ifndef RPL_SEQ_CONSUMERS
+#define RPL_SEQ_CONSUMERS 4
+#endif
 
 }  // namespace
 }  // namespace rpl
@@ -1794,7 +1800,10 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       // default: TMA-load / LSU-store pipeline.  The producer runs up to NS frames past the
       // release point of the done-frontier row f, whose own window starts exactly there, so
       // NS >= k guarantees progress; more slots let the other consumers run ahead.
-      int NS = (int)(200 * 1024 / desc->obs_bytes);
+#ifndef RPL_SEQ_SLOT_KB  // frame-slot budget of the default sequence gather (build-flag A/B knob)
+#define RPL_SEQ_SLOT_KB 200
+#endif
+      int NS = (int)(RPL_SEQ_SLOT_KB * 1024 / desc->obs_bytes);
       if (NS > PIPE_MAX_NS) NS = PIPE_MAX_NS;
       const int k = desc->k;
       const int64_t total = n * (int64_t)desc->seq_len;
@@ -1806,12 +1815,13 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
         if (rows_per_cta > PL_MAX_ROWS) rows_per_cta = PL_MAX_ROWS;
         grid = (total + rows_per_cta - 1) / rows_per_cta;
         g.use_tma = 1;
-        // consumer warps: 8 (default), 14 (variant 4), 4 (variant 5)
+        // consumer warps: RPL_SEQ_CONSUMERS (default), 14 (variant 4), 8 (variant 5)
         if (seq_variant == 4) return launch_seq_lsu<14>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn,
                                                           grid, st);
-        if (seq_variant == 5) return launch_seq_lsu<4>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn,
+        if (seq_variant == 5) return launch_seq_lsu<8>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn,
                                                          grid, st);
-        return launch_seq_lsu<8>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn, grid, st);
+        return launch_seq_lsu<RPL_SEQ_CONSUMERS>(g, idx, n, NS, rows_per_cta, q, qmin, beta, dev_err, dyn, grid,
+                                                 st);
       }
     }
     if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs &&

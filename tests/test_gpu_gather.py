@@ -104,7 +104,7 @@ def test_transition_fused_is_weights(rpl):
     check_rel(H(out["w"]), ref, what="fused w")
 
 
-@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6], ids=["pipe", "chunk", "lsu", "tmapipe", "pipe14", "pipe4", "ldgbulk"])
+@pytest.fixture(params=[0, 1, 2, 3, 4, 5, 6], ids=["pipe", "chunk", "lsu", "tmapipe", "pipe14", "pipe8", "ldgbulk"])
 def variant(rpl, request):
     assert rpl._lib.lib.rpl_debug_set_gather_variant(request.param) == 0
     yield request.param
