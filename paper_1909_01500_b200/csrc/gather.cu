@@ -1749,10 +1749,14 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       int64_t spc = (n + sm_count() - 1) / sm_count();
       if (SPF >= 2 && spc <= TP_MAX_S) {
         const size_t dyn = (size_t)SPF * NR * desc->obs_bytes;
-        ensure_smem(reinterpret_cast<const void*>(k_gather_trans_pipe<8>), dyn);
+#ifndef RPL_TRANS_CONSUMERS  // consumer warps of the transition pipeline (build-flag A/B knob)
+#define RPL_TRANS_CONSUMERS 8
+#endif
+        ensure_smem(reinterpret_cast<const void*>(k_gather_trans_pipe<RPL_TRANS_CONSUMERS>), dyn);
         const int64_t grid = (n + spc - 1) / spc;
         g.use_tma = 1;
-        return launch_pdl(k_gather_trans_pipe<8>, dim3((unsigned)grid), dim3(10 * 32), dyn, st, g, idx, n, SPF,
+        return launch_pdl(k_gather_trans_pipe<RPL_TRANS_CONSUMERS>, dim3((unsigned)grid),
+                          dim3((RPL_TRANS_CONSUMERS + 2) * 32), dyn, st, g, idx, n, SPF,
                           (int)spc, q, qmin, beta, dev_err);
       }
     }
