@@ -1750,7 +1750,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       if (SPF >= 2 && spc <= TP_MAX_S) {
         const size_t dyn = (size_t)SPF * NR * desc->obs_bytes;
 #ifndef RPL_TRANS_CONSUMERS  // consumer warps of the transition pipeline (build-flag A/B knob)
-#define RPL_TRANS_CONSUMERS 8
+#define RPL_TRANS_CONSUMERS 4  // same-box DQN bs 512 step: 22.14 us vs 22.79 at 8 (6: 22.19, 12: 22.80)
 #endif
         ensure_smem(reinterpret_cast<const void*>(k_gather_trans_pipe<RPL_TRANS_CONSUMERS>), dyn);
         const int64_t grid = (n + spc - 1) / spc;

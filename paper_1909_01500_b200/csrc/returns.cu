@@ -26,8 +26,14 @@ namespace rpl {
 
 namespace {
 
-constexpr int SCAN_WARPS = 16;
-constexpr int SCAN_S = 8;
+#ifndef RPL_SCAN_WARPS  // build-flag A/B knobs: warps x rows per thread of a 128-row chunk
+#define RPL_SCAN_WARPS 16
+#endif
+#ifndef RPL_SCAN_S
+#define RPL_SCAN_S 8
+#endif
+constexpr int SCAN_WARPS = RPL_SCAN_WARPS;
+constexpr int SCAN_S = RPL_SCAN_S;
 
 template <int WARPS, int S, bool GAE>
 __global__ void __launch_bounds__(WARPS * 32)
