@@ -25,7 +25,10 @@
 namespace rpl {
 namespace {
 
-constexpr int G_THREADS = 128;
+#ifndef RPL_G_THREADS  // one-CTA-per-sample gathers (build-flag A/B knob)
+#define RPL_G_THREADS 128
+#endif
+constexpr int G_THREADS = RPL_G_THREADS;
 constexpr int SEQ_CHUNK = 8;  // output rows per sequence task
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
