@@ -31,15 +31,21 @@ namespace {
 #define RPL_UPD_THREADS 512  // same-box A/B: 68.87 vs 69.25 us per R2D2 step at 1024 (256: two td passes, +1.1 us)
 #endif
 #ifndef RPL_SAMPLE_WARPS
-#define RPL_SAMPLE_WARPS 8
+#define RPL_SAMPLE_WARPS 4  // same-box A/B: R2D2 step 69.06 vs 69.20 us at 8; DQN bs32 / 512 step 15.67 / 22.00 vs 15.83 / 22.14
 #endif
 constexpr int UPD_THREADS = RPL_UPD_THREADS;
-constexpr int HASH_SLOTS = 2048;
+#ifndef RPL_HASH_SLOTS  // build-flag A/B knob (>= 2 x the update chunk, a power of two)
+#define RPL_HASH_SLOTS 2048
+#endif
+constexpr int HASH_SLOTS = RPL_HASH_SLOTS;
 constexpr unsigned long long HASH_EMPTY = ~0ull;
 constexpr int SAMPLE_WARPS = RPL_SAMPLE_WARPS;
 // Shared-memory staging of the tree's top levels in the sampler (34 KB): R2D2 1M-step
 // (25,600 leaves) stages root + 2 levels, DQN 2^20 leaves root + 2 of 4, toy trees all.
-constexpr int STAGE_WORDS = 4352;
+#ifndef RPL_STAGE_WORDS  // build-flag A/B knob
+#define RPL_STAGE_WORDS 4352
+#endif
+constexpr int STAGE_WORDS = RPL_STAGE_WORDS;
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -525,7 +531,7 @@ __device__ __forceinline__ void grid_barrier(int64_t* hdr) {
 }
 
 // 256 threads: measured 9.2 us for update + sample against 10.2 us with 1024-thread CTAs
-constexpr int FUSED_THREADS = SAMPLE_WARPS * 32;
+constexpr int FUSED_THREADS = 256;
 constexpr int FUSED_WARPS = FUSED_THREADS / 32;
 
 __global__ void __launch_bounds__(FUSED_THREADS)
