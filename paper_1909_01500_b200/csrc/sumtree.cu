@@ -78,7 +78,24 @@ __device__ __forceinline__ float sequence_td8(const float* __restrict__ steps, i
   const int j = threadIdx.x & 7;
   double mx = 0.0, sm = 0.0;
   if (active) {
-    for (int64_t t = j; t < T_p; t += 8) {
+    // the first 8 * TD8_BATCH rows: every load issued before the first is consumed (one L2
+    // round trip, not one per unrolled group), then the same in-order accumulation
+    constexpr int TD8_BATCH = 16;
+    float vals[TD8_BATCH];
+#pragma unroll
+    for (int u = 0; u < TD8_BATCH; ++u) {
+      const int64_t t = j + 8 * (int64_t)u;
+      vals[u] = t < T_p ? __ldg(steps + t * n + i) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < TD8_BATCH; ++u) {
+      if (j + 8 * (int64_t)u < T_p) {
+        const double v = fabs((double)vals[u]);
+        if (v > mx) mx = v;
+        sm = __dadd_rn(sm, v);
+      }
+    }
+    for (int64_t t = j + 8 * (int64_t)TD8_BATCH; t < T_p; t += 8) {
       const double v = fabs((double)__ldg(steps + t * n + i));
       if (v > mx) mx = v;
       sm = __dadd_rn(sm, v);
