@@ -432,19 +432,15 @@ __global__ void k_nstep(const float* __restrict__ r, const uint8_t* __restrict__
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = e / B;
     const int64_t b = e - t * B;
-    double acc = 0.0;
-    if (q != nullptr) {
-      const double qv = (t + n < T) ? (double)__ldg(q + (t + n) * B + b) : (double)__ldg(q_boot + b);
-      acc = rescale ? h_inv(qv, eps) : qv;
-    }
     uint8_t dn = 0;
     // Horner from the last of the n rows; rows are fetched in blocks of 8 whose loads
-    // are all issued before the recurrence consumes them (one latency per block, not per row)
+    // are all issued before the recurrence consumes them (one latency per block, not per row).
+    // The last block's loads are issued before the bootstrap's load and h^-1, so that
+    // round trip overlaps the fp64 square root and divisions instead of following them.
     constexpr int NB = 8;
-    for (int hi = n; hi > 0; hi -= NB) {
-      const int lo = hi > NB ? hi - NB : 0;
-      float rb[NB];
-      uint8_t db[NB];
+    float rb[NB];
+    uint8_t db[NB];
+    auto load_block = [&](int lo, int hi) {
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         const int i = lo + j;
@@ -452,6 +448,16 @@ __global__ void k_nstep(const float* __restrict__ r, const uint8_t* __restrict__
         rb[j] = i < hi ? __ldg(r + o) : 0.0f;
         db[j] = i < hi ? __ldg(d + o) : (uint8_t)0;
       }
+    };
+    load_block(n > NB ? n - NB : 0, n);
+    double acc = 0.0;
+    if (q != nullptr) {
+      const double qv = (t + n < T) ? (double)__ldg(q + (t + n) * B + b) : (double)__ldg(q_boot + b);
+      acc = rescale ? h_inv(qv, eps) : qv;
+    }
+    for (int hi = n; hi > 0; hi -= NB) {
+      const int lo = hi > NB ? hi - NB : 0;
+      if (hi != n) load_block(lo, hi);
 #pragma unroll
       for (int j = NB - 1; j >= 0; --j) {
         if (lo + j < hi) {
