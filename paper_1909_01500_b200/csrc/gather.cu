@@ -604,6 +604,9 @@ k_gather_seq_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, i
             if (i >= NS) {
               while (free_count <= i - NS) __nanosleep(20);
               fence_proxy_async();
+              // observe the slot's previous phase before re-arming it, so every arrive on a
+              // barrier follows the completion of its previous phase (synccheck)
+              mbar_wait(&full[slot], (uint32_t)(((i / NS) - 1) & 1));
             }
             mbar_expect_tx(&full[slot], (uint32_t)ob);
             bulk_g2s(smem + (int64_t)slot * ob, D.obs + (wrap(first + w, D.cap_T) * D.B + b) * ob, (uint32_t)ob,
