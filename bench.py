@@ -65,6 +65,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget (cpu_baseline)")
+    ap.add_argument("--cpu-baseline-leg", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/baseline/e2e)")
     ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "collective"],
                     help="N>1: K5/K7 over peer-memory boards fused into the sampler and gather (p2p) or "
@@ -238,7 +239,7 @@ def run_rpl(args):
     g = rng(77 + rank)
     td0 = np.abs(g.normal(size=valid.numel())).astype(np.float32)
     tree.update(valid, torch.from_numpy(td0).to(dev), c["alpha"], c["eps_p"])
-    P = args.graph_steps  # steps per CUDA graph = distinct per-step |delta| and target-Q inputs (cycled)
+    P = max(2, args.graph_steps + (args.graph_steps % 2))  # steps per CUDA graph (even: idx buffers alternate)
     # per-step |delta| of the previous batch's train rows, [P][train, n_glob] (R2D2 learner output)
     td_pool = torch.from_numpy(np.abs(g.normal(size=(P, c["train"], n * max(1, world)))).astype(np.float32)).to(dev)
     n_glob = n * world
@@ -374,42 +375,64 @@ def run_rpl(args):
     torch.cuda.synchronize()
     rpl.check_err(err)
 
-    # CUDA graph of P steps; with N > 1 the NCCL collectives are captured too (gloo: eager)
+    # CUDA graphs: one of P steps, replayed K // P times, and one of the K % P remaining steps,
+    # so exactly K steps are timed.  With N > 1 the NCCL collectives are captured too (gloo: eager).
+    K = args.steps
+    reps, rem = divmod(K, P)
     use_graph = (not args.no_graph) and (world == 1 or args.backend == "nccl")
-    graph = None
+    graph = graph_rem = None
+    per_graph = per_rem = 0
     if use_graph:
         try:
             s = torch.cuda.Stream(dev)
             s.wait_stream(torch.cuda.current_stream(dev))
+            c0 = rpl.launch_count()
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=s):
                 for i in range(P):
                     step(i)
+            per_graph = rpl.launch_count() - c0
+            if rem:
+                c0 = rpl.launch_count()
+                graph_rem = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph_rem, stream=s):
+                    for i in range(rem):  # P is even: step 0 here continues after step P-1
+                        step(i)
+                per_rem = rpl.launch_count() - c0
+            torch.cuda.synchronize()
+            # warm the captured graphs (first replays upload / instantiate lazily)
+            for _ in range(3):
+                graph.replay()
+            if graph_rem is not None:
+                graph_rem.replay()
             torch.cuda.synchronize()
         except Exception as e:  # capture unsupported here: fall back to eager launches
             print(f"[bench] graph capture failed ({type(e).__name__}: {e}); timing eager steps", file=sys.stderr)
-            graph = None
+            graph = graph_rem = None
             use_graph = False
             torch.cuda.synchronize()
-    K = args.steps
-    reps = math.ceil(K / P) if use_graph else K
-    K_eff = reps * P if use_graph else K
+    K_eff = K
 
     clocks = ClockSampler(local)
     if not args.profile:
         clocks.start()
         time.sleep(0.3)
-    # timed region
+    # timed region: exactly K steps; an event before each replay gives per-replay durations
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 2)] if use_graph else []
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     launches0 = rpl.launch_count()
     e0.record()
     if use_graph:
-        for _ in range(reps):
+        for j in range(reps):
+            evs[j].record()
             graph.replay()
+        evs[reps].record()
+        if graph_rem is not None:
+            graph_rem.replay()
     else:
         for i in range(K_eff):
             step(i)
@@ -418,14 +441,29 @@ def run_rpl(args):
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    launches = ((rpl.launch_count() - launches0) if not use_graph
-                else (4 if world == 1 else (3 if p2p else 4) + int(learner) + int(mode_c and rank == 0)) * K_eff)
+    launches = ((rpl.launch_count() - launches0) if not use_graph else per_graph * reps + per_rem)
     clk = clocks.stop() if not args.profile else {}
     ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
     value = K_eff * n * world / (ms / 1e3)
+    timed_stats = None
+    if use_graph and reps >= 1:
+        per = [evs[j].elapsed_time(evs[j + 1]) / P * 1e3 for j in range(reps)]
+        timed_stats = _stats(per)
+    # SURVEY §8d protocol on the same warm graph: >= 200 replays, per-replay durations
+    replay_stats = None
+    if use_graph and not args.profile:
+        nr = 200
+        ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(nr + 1)]
+        torch.cuda.synchronize()
+        for j in range(nr):
+            ev2[j].record()
+            graph.replay()
+        ev2[nr].record()
+        torch.cuda.synchronize()
+        replay_stats = dict(_stats([ev2[j].elapsed_time(ev2[j + 1]) / P * 1e3 for j in range(nr)]), replays=nr)
 
     pipelined = None
     if world == 1 and not args.no_secondary and not args.profile:
@@ -474,13 +512,19 @@ def run_rpl(args):
         "steps": K_eff,
         "warmup": max(args.warmup, 2),
         "ms_per_step": ms / K_eff,
+        "step_us_stats": {"timed": timed_stats, "replays_200": replay_stats,
+                          "note": ("per-step us over the timed region's graph replays (timed) and over 200 further "
+                                   "replays of the same warm graph (SURVEY §8d protocol); value = K / timed total")},
+        "knobs": dict(rpl._lib.config(), env={k_: v_ for k_, v_ in os.environ.items() if k_.startswith("RPL_")}),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "u8 frames + f32 (fp64 accum) + int64 tree",
         "data": "synthetic (seeded; uniform-random 84x84 u8 frames, R2D2 reward/episode recipe, DESIGN.md)",
         "config": dict(r2d2_config(c, world, args.mode),
-                       timing=f"cuda graph of {P} steps, replayed" if use_graph else "eager launches",
+                       timing=(f"cuda graph of {P} steps replayed {reps}x" + (f" + a graph of {rem} steps" if rem else "")
+                               + " (both warmed by 3 replays first); exactly K steps timed" if use_graph
+                               else "eager launches"),
                        tree=("update+sample fused (rpl_sumtree_update_sample)" if world == 1 and args.tree_fused
                              else "update_seq, then sample"),
                        exchange=(None if world == 1 else "p2p boards (K5 in the sampler, K7 in the gather)" if p2p
@@ -525,7 +569,8 @@ def run_rpl(args):
                     break
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         try:
-            result["cpu_baseline"] = cpu_baseline(c, host, args.cpu_seconds)
+            del host  # the leg rebuilds the same seeded ring in its own process
+            result["cpu_baseline"] = cpu_baseline_subprocess(args.cpu_seconds)
         except Exception as e:  # pragma: no cover
             result["cpu_baseline"] = {"error": f"{type(e).__name__}: {e}"[:300], "kind": "oracle"}
     if world > 1:
@@ -935,6 +980,12 @@ def gather_ms_in_graph(dev, step, P, reps=25):
     return tot / reps
 
 
+def _stats(us):
+    a = np.asarray(us, np.float64)
+    return {"n": int(a.size), "median_us": float(np.median(a)), "p10_us": float(np.percentile(a, 10)),
+            "p90_us": float(np.percentile(a, 90)), "mean_us": float(a.mean())}
+
+
 def _graph_time(dev, step, P=8, reps=25):
     """Capture P consecutive steps in one CUDA graph (after warm-up) and return the
     mean device time per step over `reps` replays (CUDA events on the replay stream)."""
@@ -1063,18 +1114,21 @@ class OracleStep:
     n-step targets) on host copies of the same inputs."""
 
     def __init__(self, c, host, seed=77):
+        # oracle + synth only: this arm never imports the product package (no librpl.so)
+        from oracle import gather as OG
         from oracle import sumtree as OS
-        from paper_1909_01500_b200 import replay as R  # host index logic only (valid leaves)
         self.c, self.h = c, host
         B = host.obs.shape[1]
         self.B = B
-        n_leaves = (c["cap_T"] // c["period"]) * B
-        self.tree = OS.SumTreeOracle(n_leaves)
-        blocks = R.valid_sequence_blocks(c["cap_T"], c["period"], host.cursor, host.size, c["k"], c["L"])
-        valid = R.leaves_of(blocks, B)
+        n_blocks = c["cap_T"] // c["period"]
+        self.tree = OS.SumTreeOracle(n_blocks * B)
+        # every leaf (block * B + b) whose sequence window is stored (§8c #16)
+        valid = [blk * B + b for blk in range(n_blocks)
+                 if OG.window_valid_sequence(blk * c["period"], c["cap_T"], host.cursor, host.size, c["k"], c["L"])
+                 for b in range(B)]
         g = np.random.Generator(np.random.PCG64(seed))
-        td0 = np.abs(g.normal(size=valid.size)).astype(np.float32)
-        self.tree.update([int(x) for x in valid], [float(x) for x in td0], c["alpha"], c["eps_p"])
+        td0 = np.abs(g.normal(size=len(valid))).astype(np.float32)
+        self.tree.update(valid, [float(x) for x in td0], c["alpha"], c["eps_p"])
         self.g = g
         self.prev = []
         self.ctr = 0
@@ -1120,6 +1174,19 @@ def _cores():
     return aff, model
 
 
+def cpu_baseline_subprocess(seconds):
+    """The cpu_baseline leg in a fresh interpreter (oracle + synth only), so the oracle never
+    runs in a process that has the product library mapped."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE")}
+    cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--cpu-baseline-leg",
+           "--cpu-seconds", str(seconds)]
+    res = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=600)
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    if res.returncode != 0 or not lines:
+        raise RuntimeError(f"cpu_baseline leg failed (rc={res.returncode}): {res.stderr[-300:]}")
+    return json.loads(lines[-1])
+
+
 def cpu_baseline(c, host, seconds):
     for v in ("OMP_NUM_THREADS", "MKL_NUM_THREADS", "OPENBLAS_NUM_THREADS"):
         os.environ[v] = "1"
@@ -1149,6 +1216,9 @@ def run_reference(args):
     c = dict(R2D2)
     host = make_ring(2019, c["cap_T"], c["B"], ep_len=2000.0, reward_kind="r2d2", period=c["period"],
                      rnn_parts=c["rnn_parts"], rnn_h=c["rnn_h"], cursor=1234 % c["cap_T"])
+    if args.cpu_baseline_leg:  # the product arm's cpu_baseline, run in this separate process
+        print(json.dumps(cpu_baseline(c, host, args.cpu_seconds)))
+        return
     o = OracleStep(c, host)
     t0 = time.time()
     o.step(2)

@@ -62,6 +62,14 @@ const char* rpl_strerror(int status);
 int rpl_abi_version(void);
 /* Number of kernel launches this process has issued through librpl (host counter). */
 int64_t rpl_launch_count(void);
+/* The library's effective configuration as a one-line JSON object written into buf (host,
+ * len bytes incl. the terminating NUL): every build-flag knob (launch shapes, RPL_PDL_EARLY,
+ * whether the -DRPL_DIAG diagnostics are compiled in) and every runtime knob (RPL_PDL,
+ * RPL_TREE_STAGE, RPL_SCAN_VARIANT, RPL_SCAN_TRIGGER, the debug gather variant / diag mask).
+ * bench.py records it in its JSON line so that no knob can change the timed path unseen.
+ * RPL_EINVAL for a NULL / empty buffer, RPL_ERANGE if it is too short (buf then holds a
+ * truncated string). */
+int rpl_config(char* buf, int64_t len);
 
 /* =========================================================================
  * (1) Return estimation over time-major [T,B] buffers.  fp32 I/O, fp64
@@ -505,12 +513,14 @@ int rpl_debug_set_scan_variant(int32_t variant);
  * RPL_EINVAL for other values. */
 int rpl_debug_set_tree_stage(int32_t on);
 
-/* Diagnostics (measurement only): bit mask applied to the default sequence gather.
+/* Diagnostics (measurement only; compiled in only with -DRPL_DIAG, see build.py
+ * RPL_NVCC_EXTRA): bit mask applied to the default sequence gather.
  * 1 = skip the frame stores, 2 = skip the frame loads (outputs are then garbage),
  * 4 = normal-priority frame stores, 8 = normal L2 policy on the frame loads (the default is
  * evict-first for both: frames are streamed once),
  * 16 = skip the per-row fields and stored state.
- * 0 (default) restores normal operation.  Returns RPL_EINVAL for other values. */
+ * 0 (default) restores normal operation.  Returns RPL_EINVAL for other values, and
+ * RPL_EUNSUPPORTED for a non-zero mask in the default build (RPL_GATHER_DIAG is ignored there). */
 int rpl_debug_set_gather_diag(int32_t mask);
 
 #ifdef __cplusplus

@@ -68,6 +68,7 @@ _SIGS = {
     "rpl_strerror": ([C.c_int], C.c_char_p),
     "rpl_abi_version": ([], C.c_int),
     "rpl_launch_count": ([], I64),
+    "rpl_config": ([C.c_char_p, I64], C.c_int),
     "rpl_returns_discounted": ([P, P, P, I64, I64, D, P, P], C.c_int),
     "rpl_returns_nstep": ([P, P, I64, I64, I32, D, P, P, I32, D, P, P, P], C.c_int),
     "rpl_gae": ([P, P, P, P, I64, I64, D, D, P, P, P], C.c_int),
@@ -127,6 +128,14 @@ def _load():
 
 lib = _load()
 assert lib.rpl_abi_version() == 1, "librpl ABI version mismatch"
+
+
+def config() -> dict:
+    """rpl_config: the library's build-flag and runtime knob state."""
+    import json
+    buf = C.create_string_buffer(1024)
+    check(lib.rpl_config(buf, len(buf)), "rpl_config")
+    return json.loads(buf.value.decode())
 
 
 class RplError(RuntimeError):

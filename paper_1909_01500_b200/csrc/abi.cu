@@ -1,6 +1,7 @@
 // ABI helpers: version, error strings, launch counter (include/rpl.h).
 #include "common.cuh"
 
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -14,7 +15,11 @@ bool pdl_enabled() {
   }();
   return on;
 }
-}
+void cfg_tree(int* stage_on, int* upd_threads, int* sample_warps, int* stage_words, int* hash_slots);
+void cfg_scan(int* variant, int* trigger);
+void cfg_gather(int* variant, int* diag, int* diag_build, int* seq_consumers, int* trans_consumers, int* slot_kb,
+                int* g_threads);
+}  // namespace rpl
 
 extern "C" const char* rpl_strerror(int status) {
   switch (status) {
@@ -46,4 +51,20 @@ extern "C" int rpl_peer_access(int32_t peer) {
     return RPL_OK;
   }
   return e == cudaSuccess ? RPL_OK : RPL_ECUDA;
+}
+
+extern "C" int rpl_config(char* buf, int64_t len) {
+  if (!buf || len < 1) return RPL_EINVAL;
+  int st, ut, sw, sword, hs, sv, strig, gv, gd, gdb, sc, tc, skb, gt;
+  rpl::cfg_tree(&st, &ut, &sw, &sword, &hs);
+  rpl::cfg_scan(&sv, &strig);
+  rpl::cfg_gather(&gv, &gd, &gdb, &sc, &tc, &skb, &gt);
+  const int w = snprintf(buf, (size_t)len,
+                         "{\"abi\": %d, \"pdl\": %d, \"pdl_early\": %d, \"tree_stage\": %d, \"upd_threads\": %d, "
+                         "\"sample_warps\": %d, \"stage_words\": %d, \"hash_slots\": %d, \"scan_variant\": %d, "
+                         "\"scan_trigger\": %d, \"gather_variant\": %d, \"gather_diag\": %d, \"diag_build\": %d, "
+                         "\"seq_consumers\": %d, \"trans_consumers\": %d, \"seq_slot_kb\": %d, \"g_threads\": %d}",
+                         RPL_ABI_VERSION, rpl::pdl_enabled() ? 1 : 0, (int)RPL_PDL_EARLY, st, ut, sw, sword, hs, sv,
+                         strig, gv, gd, gdb, sc, tc, skb, gt);
+  return (w < 0 || w >= len) ? RPL_ERANGE : RPL_OK;
 }

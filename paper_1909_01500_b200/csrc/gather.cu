@@ -29,6 +29,12 @@ namespace {
 #define RPL_G_THREADS 128
 #endif
 constexpr int G_THREADS = RPL_G_THREADS;
+#ifndef RPL_TRANS_CONSUMERS  // consumer warps of the transition pipeline (build-flag A/B knob)
+#define RPL_TRANS_CONSUMERS 4  // same-box DQN bs 512 step: 22.14 us vs 22.79 at 8 (6: 22.19, 12: 22.80)
+#endif
+#ifndef RPL_SEQ_SLOT_KB  // frame-slot budget of the default sequence gather (build-flag A/B knob)
+#define RPL_SEQ_SLOT_KB 200
+#endif
 constexpr int SEQ_CHUNK = 8;  // output rows per sequence task
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -153,6 +159,12 @@ __device__ __forceinline__ void coop_zero(void* dst, int64_t bytes, int t, int n
     for (int64_t i = t; i < bytes; i += nt) d[i] = 0;
   }
 }
+
+#ifdef RPL_DIAG
+#define GDIAG(D) ((D).diag)
+#else
+#define GDIAG(D) 0
+#endif
 
 struct GDesc {
   int32_t kind, pad_mode, out_mode, k;
@@ -874,7 +886,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   __shared__ int p_blk[PL_MAX_ROWS];   // storage block (stored RNN state)
   __shared__ int p_F[PL_MAX_ROWS];     // frame position of the piece's first frame
   // per output row c
-  __shared__ int row_first[PL_MAX_ROWS];  // frame position of the row's window start (-1: skipped)
+  __shared__ int row_new[PL_MAX_ROWS];    // frame position of the row's NEWEST frame (-1: skipped)
   __shared__ int rel[PL_MAX_ROWS];        // frames released once rows <= c are done
   __shared__ int row_ring[PL_MAX_ROWS];   // ring row
   __shared__ short row_piece[PL_MAX_ROWS];
@@ -948,7 +960,11 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
     p_blk[pc] = blk;
   }
   __syncthreads();
-  // (B) frame positions: exclusive scan over pieces (serial: a CTA holds one to a few pieces)
+  // (B) frame positions: exclusive scan over pieces (serial: a CTA holds one to a few pieces).
+  //     A piece loads window rows tau0-(k-1) .. tau0+R-1, except in RPL_OUT_UNIQUE mode when it
+  //     starts mid-sample (tau0 > 0, only a CTA's first piece): its rows store only their newest
+  //     frame, so the k-1 history rows are not loaded (`skip`).
+  const int skip0 = (unique && g0 > s_first * L) ? k - 1 : 0;
   if (tid == 0) {
     int F = 0;
     for (int pc = 0; pc < npieces; ++pc) {
@@ -956,7 +972,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       if (p_b[pc] >= 0) {
         const int sm = s_first + pc;
         const int R = min(g1, (sm + 1) * L) - max(g0, sm * L);
-        F += R + k - 1;
+        F += R + k - 1 - (pc == 0 ? skip0 : 0);
       }
     }
   }
@@ -973,11 +989,12 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         if (bcol < 0) continue;
         const int sm = s_first + pc;
         const int R = min(g1, (sm + 1) * L) - max(g0, sm * L);
-        int row = p_row0[pc] - (k - 1);
+        const int skip = pc == 0 ? skip0 : 0;
+        int row = p_row0[pc] - (k - 1) + skip;
         while (row < 0) row += cap;
         const uint8_t* col = D.obs + (int64_t)bcol * ob;
         const int64_t rstride = (int64_t)Bc * ob;
-        for (int w = 0; w < R + k - 1; ++w, ++i) {
+        for (int w = skip; w < R + k - 1; ++w, ++i) {
           if (i >= NS) {
             while (released <= i - NS) {
               if (frontier < nrows && flag_acquire(&row_done[frontier])) {
@@ -990,20 +1007,24 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
             fence_proxy_async();
             // the slot's previous phase completed before its readers finished: observe it, so
             // every arrive on a barrier follows the completion of its previous phase
-            if (!(D.diag & 2)) mbar_wait(&full[slot], (uint32_t)(((i / NS) - 1) & 1));
+            if (!(GDIAG(D) & 2)) mbar_wait(&full[slot], (uint32_t)(((i / NS) - 1) & 1));
           }
-          if (!(D.diag & 2)) {
+          if (!(GDIAG(D) & 2)) {
             mbar_expect_tx(&full[slot], (uint32_t)ob);
             const uint8_t* src = col + (int64_t)row * rstride;
             // frames are streamed once: evict-first keeps the L2 for the sum tree and the
             // small per-row fields (measured: step 74.6 -> 69.8 us with the stores below)
-            if (D.diag & 8) bulk_g2s(smem + slot * ob, src, (uint32_t)ob, &full[slot]);
+            if (GDIAG(D) & 8) bulk_g2s(smem + slot * ob, src, (uint32_t)ob, &full[slot]);
             else bulk_g2s_evict_first(smem + slot * ob, src, (uint32_t)ob, &full[slot]);
           }
           if (++row == cap) row = 0;
           if (++slot == NS) slot = 0;
         }
       }
+      // tail: observe the last phase of every armed slot, so the CTA never exits with bulk
+      // copies into its shared memory in flight (also frames no row reads)
+      if (!(GDIAG(D) & 2))
+        for (int p = i > NS ? i - NS : 0; p < i; ++p) mbar_wait(&full[p % NS], (uint32_t)((p / NS) & 1));
     }
   } else {
     // (C) row tables + episode-start offsets, rows spread over warps 1..NC+1; the
@@ -1019,9 +1040,13 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       int ring = 0;
       if (bcol >= 0) {
         const int R = min(g1, (sm + 1) * L) - max(g0, sm * L);
+        const int skip = pc == 0 ? skip0 : 0;
         const int F = p_F[pc];
-        row_first[c] = F + m;
-        rel[c] = m == R - 1 ? F + R + k - 1 : F + m + 1;
+        const int nw = F + m + (k - 1) - skip;  // window row m+k-1 (the row's newest frame)
+        row_new[c] = nw;
+        // stacked: the row's oldest frame is no longer needed; unique: each row reads only its
+        // newest frame (and the sample's first row its history too); end of piece: all of it
+        rel[c] = m == R - 1 ? F + R + k - 1 - skip : (unique ? nw + 1 : nw - (k - 1) + 1);
         ring = p_row0[pc] + m;
         if (ring >= cap) ring -= cap;
         uint8_t dw[8];
@@ -1035,7 +1060,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         for (int j = 1; j < 8; ++j)
           if (dw[j]) so = (int8_t)j;  // latest episode start in the window wins
       } else {
-        row_first[c] = -1;
+        row_new[c] = -1;
         rel[c] = p_F[pc];
       }
       row_ring[c] = ring;
@@ -1051,8 +1076,8 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       const int64_t ab = D.act_bytes;
       const bool a8 = ab == 8 && ((reinterpret_cast<uintptr_t>(D.act) | reinterpret_cast<uintptr_t>(D.o_act) |
                                    reinterpret_cast<uintptr_t>(D.o_prev_act)) & 7) == 0;
-      for (int c = lane; c < nrows && !(D.diag & 16); c += 32) {
-        if (row_first[c] < 0) continue;
+      for (int c = lane; c < nrows && !(GDIAG(D) & 16); c += 32) {
+        if (row_new[c] < 0) continue;
         const int pc = row_piece[c];
         const int sm = s_first + pc;
         const int tau = row_tau[c];
@@ -1100,14 +1125,14 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
           v = x < v ? x : v;
         }
         for (int c = lane; c < nrows; c += 32) {
-          if (row_first[c] < 0 || row_tau[c] != 0) continue;
+          if (row_new[c] < 0 || row_tau[c] != 0) continue;
           const int sm = s_first + row_piece[c];
           const int64_t qs = q[sm];
           D.o_w[coff + sm] = qs > 0 ? (float)pow((double)v / (double)qs, beta) : 0.0f;
         }
       }
       // stored recurrent state of every sample whose first row lives here
-      if (D.o_rnn && !(D.diag & 16)) {
+      if (D.o_rnn && !(GDIAG(D) & 16)) {
         const int nparts = D.rnn_parts;
         const int64_t rb = D.rnn_bytes;
         for (int pc = 0; pc < npieces; ++pc) {
@@ -1121,55 +1146,55 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
     } else {
       // ---------------- consumers: one k-stack per row, LSU stores ----------------
       for (int c = warp - 2; c < nrows; c += NC) {
-        const int p0 = row_first[c];
-        if (p0 >= 0 && unique) {
+        const int pn = row_new[c];
+        // slot / mbarrier parity of window index j (position pn - (k-1) + j)
+        const int sn = pn % NS;
+        const uint32_t parn = (uint32_t)((pn / NS) & 1);
+        auto slot_of = [&](int j, uint32_t* par) {
+          int sl = sn - (k - 1 - j);
+          *par = parn;
+          if (sl < 0) {
+            sl += NS;
+            *par ^= 1u;
+          }
+          return sl;
+        };
+        if (pn >= 0 && unique) {
           // RPL_OUT_UNIQUE: raw rows, each written once — row tau stores its newest frame
           // (unique row tau+k-1); the sample's first row also stores unique rows 0..k-2
           const int sm = s_first + row_piece[c];
           const int tau = row_tau[c];
-          const int s0 = p0 % NS;
-          const uint32_t par0 = (uint32_t)((p0 / NS) & 1);
           for (int j = tau == 0 ? 0 : k - 1; j < k; ++j) {
-            int sl = s0 + j;
-            uint32_t par = par0;
-            if (sl >= NS) {
-              sl -= NS;
-              par ^= 1u;
-            }
-            if (!(D.diag & 2)) mbar_wait(&full[sl], par);
-            if (D.diag & 1) continue;
+            uint32_t par;
+            const int sl = slot_of(j, &par);
+            if (!(GDIAG(D) & 2)) mbar_wait(&full[sl], par);
+            if (GDIAG(D) & 1) continue;
             int4* d = reinterpret_cast<int4*>(D.o_obs + ((int64_t)(tau + j) * n + coff + sm) * ob);
             const int4* sp = reinterpret_cast<const int4*>(smem + sl * ob);
 #pragma unroll 4
             for (int v = lane; v < nv; v += 32) __stcs(d + v, sp[v]);
           }
-        } else if (p0 >= 0) {
+        } else if (pn >= 0) {
           const int so = start_off[c];
           const int sm = s_first + row_piece[c];
           const int tau = row_tau[c];
-          const int s0 = p0 % NS;
-          const uint32_t par0 = (uint32_t)((p0 / NS) & 1);
-          if (!(D.diag & 2))
+          if (!(GDIAG(D) & 2))
             for (int j = so; j < k; ++j) {
-              int sl = s0 + j;
-              uint32_t par = par0;
-              if (sl >= NS) {
-                sl -= NS;
-                par ^= 1u;
-              }
+              uint32_t par;
+              const int sl = slot_of(j, &par);
               mbar_wait(&full[sl], par);
             }
           int4* dst = reinterpret_cast<int4*>(D.o_obs + ((int64_t)tau * n + coff + sm) * k * ob);
-          if (!(D.diag & 1))
+          if (!(GDIAG(D) & 1))
             for (int j = 0; j < k; ++j) {
               int4* d = dst + j * nv;
               if (j < so && D.pad_mode == RPL_PAD_ZERO) {
                 for (int v = lane; v < nv; v += 32) d[v] = make_int4(0, 0, 0, 0);
               } else {
-                int sl = s0 + (j < so ? so : j);
-                if (sl >= NS) sl -= NS;
+                uint32_t par;
+                const int sl = slot_of(j < so ? so : j, &par);
                 const int4* sp = reinterpret_cast<const int4*>(smem + sl * ob);
-                if (D.diag & 4) {
+                if (GDIAG(D) & 4) {
 #pragma unroll 4
                   for (int v = lane; v < nv; v += 32) d[v] = sp[v];
                 } else {  // streaming (evict-first) stores
@@ -1353,7 +1378,7 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
       for (int c = 0; c < nrows; ++c) {
         const int p0 = row_first[c];
-        if (p0 >= 0 && !(D.diag & 1)) {
+        if (p0 >= 0 && !(GDIAG(D) & 1)) {
           const int so = start_off[c];
           const int sm = s_first + row_piece[c];
           const int tau = row_tau[c];
@@ -1393,7 +1418,7 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
     const int64_t ab = D.act_bytes;
     const bool a8 = ab == 8 && ((reinterpret_cast<uintptr_t>(D.act) | reinterpret_cast<uintptr_t>(D.o_act) |
                                  reinterpret_cast<uintptr_t>(D.o_prev_act)) & 7) == 0;
-    for (int c = lane; c < nrows && !(D.diag & 16); c += 32) {
+    for (int c = lane; c < nrows && !(GDIAG(D) & 16); c += 32) {
       if (row_first[c] < 0) continue;
       const int pc = row_piece[c];
       const int sm = s_first + pc;
@@ -1428,7 +1453,7 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         D.o_w[coff + sm] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
       }
     }
-    if (D.o_rnn && !(D.diag & 16)) {
+    if (D.o_rnn && !(GDIAG(D) & 16)) {
       const int nparts = D.rnn_parts;
       const int64_t rb = D.rnn_bytes;
       for (int pc = 0; pc < npieces; ++pc) {
@@ -1452,7 +1477,7 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       while (f >= flag_acquire(&s_released) + NS) __nanosleep(20);
       const int sl = f % NS;
       int4* dst = reinterpret_cast<int4*>(smem + sl * ob);
-      if (!(D.diag & 2)) {
+      if (!(GDIAG(D) & 2)) {
         constexpr int U = 8;
         for (int v0 = lane; v0 < nv; v0 += 32 * U) {
           int4 r[U];
@@ -1504,6 +1529,8 @@ k_gather_trans_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int SPF
   __shared__ int s_r[TP_MAX_S];            // ring row of the transition
   __shared__ int8_t ssl[TP_MAX_S][2][8];   // stack slot -> window index (-1: zero)
   __shared__ volatile int sdone[TP_MAX_S]; // stacks written (0..2)
+  __shared__ int s_arm[TP_MAX_S];          // armed (loaded) samples before this one (-1: skipped)
+  __shared__ int s_of_arm[TP_MAX_S];       // sample of armed index a
   constexpr int NT = (NC + 2) * 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k = D.k, ns = D.n_step, NR = k + ns;
@@ -1537,6 +1564,22 @@ k_gather_trans_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int SPF
     sdone[j] = bcol < 0 ? 2 : 0;
   }
   __syncthreads();
+  // Slot groups and mbarrier phases follow the ARMED samples only (skipped entries — idx < 0
+  // or out of range — load nothing and must not consume a phase): armed index a of sample j
+  // is the number of loaded samples before it; group a % SPF, phase (a / SPF) & 1.
+  if (warp == 0) {
+    int base = 0;
+    for (int j0 = 0; j0 < nsm; j0 += 32) {
+      const int j = j0 + lane;
+      const bool ok = j < nsm && s_b[j] >= 0;
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      const int a = base + __popc(m & ((1u << lane) - 1u));
+      if (j < nsm) s_arm[j] = ok ? a : -1;
+      if (ok) s_of_arm[a] = j;
+      base += __popc(m);
+    }
+  }
+  __syncthreads();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1545,11 +1588,12 @@ k_gather_trans_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int SPF
       for (int j = 0; j < nsm; ++j) {
         const int bcol = s_b[j];
         if (bcol < 0) continue;
-        const int grp = j % SPF;
-        if (j >= SPF) {
-          while (flag_acquire(&sdone[j - SPF]) < 2) __nanosleep(20);
+        const int a = s_arm[j];
+        const int grp = a % SPF;
+        if (a >= SPF) {  // the group's previous sample must have both stacks written
+          while (flag_acquire(&sdone[s_of_arm[a - SPF]]) < 2) __nanosleep(20);
           fence_proxy_async();
-          mbar_wait(&full[grp], (uint32_t)(((j / SPF) - 1) & 1));  // previous phase completed
+          mbar_wait(&full[grp], (uint32_t)(((a / SPF) - 1) & 1));  // previous phase completed
         }
         mbar_expect_tx(&full[grp], (uint32_t)(NR * ob));
         int row = s_r[j] - (k - 1);
@@ -1615,9 +1659,12 @@ k_gather_trans_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int SPF
       const int j = it >> 1, which = it & 1;
       if (s_b[j] < 0) continue;
       uint8_t* outb = which ? D.o_next_obs : D.o_obs;
+      const int a = s_arm[j];
+      const int grp = a % SPF;
+      // every consumer observes its group's phase (even without an output), so no CTA exits
+      // with bulk copies into its shared memory still in flight
+      mbar_wait(&full[grp], (uint32_t)((a / SPF) & 1));
       if (outb) {
-        const int grp = j % SPF;
-        mbar_wait(&full[grp], (uint32_t)((j / SPF) & 1));
         int4* dst = reinterpret_cast<int4*>(outb + (coff + s0 + j) * (int64_t)k * ob);
         for (int jj = 0; jj < k; ++jj) {
           int4* d = dst + jj * nv;
@@ -1642,11 +1689,17 @@ k_gather_trans_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int SPF
   pdl_trigger();
 }
 
+// Work-skipping diagnostics (rpl_debug_set_gather_diag, RPL_GATHER_DIAG) exist only in a
+// -DRPL_DIAG build; in the default build GDIAG() is the constant 0 and the branches compile out.
+#ifdef RPL_DIAG
 int env_diag() {
   const char* v = getenv("RPL_GATHER_DIAG");  // measurement only (rpl_debug_set_gather_diag)
   return v ? atoi(v) : 0;
 }
 int g_seq_diag = env_diag();
+#else
+int g_seq_diag = 0;
+#endif
 
 GDesc to_dev(const rpl_gather_desc* d) {
   GDesc g;
@@ -1719,9 +1772,30 @@ extern "C" int rpl_debug_set_gather_variant(int32_t variant) {
 
 extern "C" int rpl_debug_set_gather_diag(int32_t mask) {
   if (mask < 0 || mask > 31) return RPL_EINVAL;
+#ifdef RPL_DIAG
   g_seq_diag = mask;
   return RPL_OK;
+#else
+  return mask == 0 ? RPL_OK : RPL_EUNSUPPORTED;  // default build: diagnostics compiled out
+#endif
 }
+
+namespace rpl {
+void cfg_gather(int* variant, int* diag, int* diag_build, int* seq_consumers, int* trans_consumers, int* slot_kb,
+                int* g_threads) {  // knob state for rpl_config (abi.cu)
+  *variant = g_seq_variant;
+  *diag = g_seq_diag;
+#ifdef RPL_DIAG
+  *diag_build = 1;
+#else
+  *diag_build = 0;
+#endif
+  *seq_consumers = RPL_SEQ_CONSUMERS;
+  *trans_consumers = RPL_TRANS_CONSUMERS;
+  *slot_kb = RPL_SEQ_SLOT_KB;
+  *g_threads = G_THREADS;
+}
+}  // namespace rpl
 
 extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q, const int64_t* qmin,
                           double beta, int64_t n, int32_t* dev_err, void* stream) {
@@ -1749,15 +1823,13 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
     if ((desc->o_ret || desc->o_done_n) && !desc->rew) return RPL_EINVAL;
     const int NR = desc->k + desc->n_step;
     // large batches: persistent pipeline (several samples per CTA, loads overlapping stores)
-    if (tma_ok && seq_variant != 1 && n >= 2 * (int64_t)sm_count() && NR <= 30 && desc->k <= 8) {
+    if (tma_ok && (desc->o_obs || desc->o_next_obs) && seq_variant != 1 && n >= 2 * (int64_t)sm_count() &&
+        NR <= 30 && desc->k <= 8) {
       int SPF = (int)(200 * 1024 / ((int64_t)NR * desc->obs_bytes));
       if (SPF > TP_MAX_G) SPF = TP_MAX_G;
       int64_t spc = (n + sm_count() - 1) / sm_count();
       if (SPF >= 2 && spc <= TP_MAX_S) {
         const size_t dyn = (size_t)SPF * NR * desc->obs_bytes;
-#ifndef RPL_TRANS_CONSUMERS  // consumer warps of the transition pipeline (build-flag A/B knob)
-#define RPL_TRANS_CONSUMERS 4  // same-box DQN bs 512 step: 22.14 us vs 22.79 at 8 (6: 22.19, 12: 22.80)
-#endif
         ensure_smem(reinterpret_cast<const void*>(k_gather_trans_pipe<RPL_TRANS_CONSUMERS>), dyn);
         const int64_t grid = (n + spc - 1) / spc;
         g.use_tma = 1;
@@ -1810,9 +1882,6 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       // default: TMA-load / LSU-store pipeline.  The producer runs up to NS frames past the
       // release point of the done-frontier row f, whose own window starts exactly there, so
       // NS >= k guarantees progress; more slots let the other consumers run ahead.
-#ifndef RPL_SEQ_SLOT_KB  // frame-slot budget of the default sequence gather (build-flag A/B knob)
-#define RPL_SEQ_SLOT_KB 200
-#endif
       int NS = (int)(RPL_SEQ_SLOT_KB * 1024 / desc->obs_bytes);
       if (NS > PIPE_MAX_NS) NS = PIPE_MAX_NS;
       const int k = desc->k;

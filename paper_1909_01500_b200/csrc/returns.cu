@@ -542,6 +542,13 @@ int scan_trigger() {
   return t;
 }
 
+namespace rpl {
+void cfg_scan(int* variant, int* trigger) {  // knob state for rpl_config (abi.cu)
+  *variant = scan_variant();
+  *trigger = scan_trigger();
+}
+}  // namespace rpl
+
 typedef CUresult (*encode_fn_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);

@@ -54,7 +54,7 @@ __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cv
 // word reads one word past the staged levels, which is still inside the tree (header).
 std::atomic<int> g_tree_stage{-1};  // -1: not set yet (read RPL_TREE_STAGE once)
 
-int64_t stage_cap(const int64_t* tree) {
+int tree_stage_on() {
   int on = g_tree_stage.load(std::memory_order_relaxed);
   if (on < 0) {
     const char* e = getenv("RPL_TREE_STAGE");
@@ -62,7 +62,11 @@ int64_t stage_cap(const int64_t* tree) {
     g_tree_stage.compare_exchange_strong(expect, (e && e[0] == '0') ? 0 : 1);
     on = g_tree_stage.load(std::memory_order_relaxed);
   }
-  return (on && (reinterpret_cast<uintptr_t>(tree) & 15) == 0) ? (int64_t)STAGE_WORDS - 1 : 0;
+  return on;
+}
+
+int64_t stage_cap(const int64_t* tree) {
+  return (tree_stage_on() && (reinterpret_cast<uintptr_t>(tree) & 15) == 0) ? (int64_t)STAGE_WORDS - 1 : 0;
 }
 
 enum { MODE_TD = 0, MODE_Q = 1, MODE_MAXSEEN = 2, MODE_SEQ = 3 };
@@ -789,6 +793,15 @@ int launch_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, c
 }
 
 }  // namespace
+
+// Knob state for rpl_config (abi.cu).
+void cfg_tree(int* stage_on, int* upd_threads, int* sample_warps, int* stage_words, int* hash_slots) {
+  *stage_on = tree_stage_on();
+  *upd_threads = UPD_THREADS;
+  *sample_warps = SAMPLE_WARPS;
+  *stage_words = STAGE_WORDS;
+  *hash_slots = HASH_SLOTS;
+}
 }  // namespace rpl
 
 using namespace rpl;

@@ -122,3 +122,16 @@ def test_peer_gather_validation_without_gpu(lib):
     assert sp(ctypes.byref(lay), 16, 0, 2, 1000, None, 64, 1, 16, 16, 16, None, None) == -1   # no boards
     assert sp(ctypes.byref(lay), 16, 0, 65, 1000, 16, 64, 1, 16, 16, 16, None, None) == -1    # > 64 shards
     assert sp(ctypes.byref(lay), 16, 0, 2, 1000, 16, 64, 1, 16, 16, None, None, None) == -1   # no count
+
+
+def test_config_reports_knobs_and_no_diag_build():
+    from paper_1909_01500_b200 import _lib
+    cfg = _lib.config()
+    for key in ("pdl", "tree_stage", "scan_variant", "gather_variant", "gather_diag", "diag_build",
+                "seq_consumers", "upd_threads", "sample_warps"):
+        assert key in cfg, key
+    # the default build carries no work-skipping diagnostics
+    assert cfg["diag_build"] == 0 and cfg["gather_diag"] == 0
+    assert _lib.lib.rpl_debug_set_gather_diag(1) == -5 and _lib.lib.rpl_debug_set_gather_diag(0) == 0
+    buf = ctypes.create_string_buffer(8)
+    assert _lib.lib.rpl_config(buf, 8) == -2
