@@ -151,10 +151,12 @@ int rpl_sumtree_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* i
 /* R2D2 sequence priorities (§8f NEXT-1; "eta = 0.9 mix of max and mean", reading
  * R26): td_steps [T_p, n] f32, time-major per-step |delta| of the n sampled sequences
  * (e.g. the 80 train rows).  Sequence k gets
- *   td_k = RN32(eta * max_t |d_tk| + (1 - eta) * (sum_t |d_tk|) / T_p)
- * (fp64, sum in increasing t, no fused multiply-add), then exactly rpl_sumtree_update's
+ *   td_k = RN32(RN64(RN64(eta * max_t |d_tk|) + RN64(RN64(1 - eta) * mean_k))),
+ *   mean_k = RN64(S_k / T_p),  S_k = RN64(the EXACT sum over t of |d_tk|)
+ * (S_k is rounded once, so it does not depend on any summation order; NaN if a |d| is NaN,
+ * +inf if one is infinite; no fused multiply-add), then exactly rpl_sumtree_update's
  * transform and write: identical to rpl_sumtree_update(idx, td, n, alpha, eps_p).
- * eta in [0, 1]; T_p >= 1.  flags: 0 or RPL_UPD_LIVE_ONLY. */
+ * eta in [0, 1]; 1 <= T_p <= 2^30.  flags: 0 or RPL_UPD_LIVE_ONLY. */
 int rpl_sumtree_update_seq(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx,
                            const float* td_steps, int64_t T_p, int64_t n, double eta, double alpha,
                            double eps_p, int32_t flags, int32_t* dev_err, void* stream);
@@ -344,6 +346,10 @@ int rpl_is_weights(const int64_t* q, const int64_t* qmin, int64_t n, double beta
  * pointers uses TMA bulk copies; other sizes use vectorised LSU copies.
  * ========================================================================= */
 enum { RPL_GATHER_TRANSITION = 0, RPL_GATHER_SEQUENCE = 1 };
+/* Done-flag values (u8): 0 = the episode continues; any non-zero value = the episode ended
+ * after this row (frame stacks restart, prev fields zero); RPL_DONE_TIMEOUT = it ended by a
+ * time limit, which the _tl / v_term paths bootstrap from the supplied terminal value (R34). */
+enum { RPL_DONE_TERMINAL = 1, RPL_DONE_TIMEOUT = 2 };
 enum { RPL_PAD_REPEAT = 0, RPL_PAD_ZERO = 1 };
 enum { RPL_OUT_STACKED = 0, RPL_OUT_UNIQUE = 1 };
 
@@ -395,6 +401,34 @@ typedef struct {
   int64_t* const* peer_boards;
   int32_t peer_world;
   int32_t peer_rank;
+  /* Optional fused n-step targets (SEQUENCE, default kernel only — RPL_EUNSUPPORTED when it
+   * cannot run; a2 + a4 over the gathered rows, readings R5 / R24 / R34).  With o_tgt
+   * non-NULL, for t in [0, tgt_T) and output row tau = tgt_lo + t of each sample:
+   *   R   = Horner over the sample's rows tau .. tau+n_step-1 (fp64): acc = r + gamma acc,
+   *         acc = r at a done row (and r + gamma v_term at a time-limit row, R34), starting
+   *         from acc = q = q_tgt[tau + n_step, column] (h^-1(q) when rescale) or 0 without q_tgt;
+   *   o_tgt[t, column]      = RN32(rescale ? h(R, rescale_eps) : R)
+   *   o_tgt_done[t, column] = OR of the done flags of those rows (may be NULL)
+   * — bit-identical to rpl_returns_nstep over the gathered rew / done rows tgt_lo ..
+   * tgt_lo+tgt_T+n_step-2 with q = q_tgt rows tgt_lo+n_step .. and q_boot = the last one.
+   * q_tgt f32 [seq_len, n] (time-major by output row, device, may be NULL), o_tgt f32
+   * [tgt_T, n], o_tgt_done u8 [tgt_T, n]; column = *col_offset + k.  Requires n_step >= 1,
+   * tgt_lo >= 0, tgt_T >= 1, tgt_lo + tgt_T + n_step <= seq_len (RPL_EINVAL otherwise). */
+  const float* q_tgt;
+  float* o_tgt;
+  uint8_t* o_tgt_done;
+  int32_t tgt_lo, tgt_T;
+  int32_t rescale, _pad1;
+  double rescale_eps;
+  /* Optional time-limit bootstrap (R34; P:95 fn "bootstrapping the value function when the
+   * trajectory ends due to time limit"): ring array f32 [cap_T, B] (device, may be NULL).
+   * A ring row whose done flag is RPL_DONE_TIMEOUT (2) ended its episode by a time limit;
+   * v_term[row] is the value of its final observation.  With v_term non-NULL every fused
+   * n-step return (TRANSITION o_ret, SEQUENCE o_tgt) that stops at such a row adds
+   * gamma^(j+1) v_term[row] (j = the row's offset in the n rows): the recursion is cut at the
+   * episode boundary and bootstrapped from the supplied value; done_n stays 1 (the learner
+   * must not bootstrap again).  With v_term NULL any non-zero done flag is a terminal. */
+  const float* v_term;
 } rpl_gather_desc;
 
 int rpl_gather(const rpl_gather_desc* desc /* host */, const int64_t* idx, const int64_t* q,

@@ -16,6 +16,7 @@ significand by explicit integer arithmetic, so nothing depends on a libm.
 from __future__ import annotations
 
 import math
+from fractions import Fraction
 
 import mpmath
 
@@ -102,18 +103,30 @@ def value_float(M: int, E) -> float:
     return math.inf if E is None else math.ldexp(M, E)
 
 
+def sequence_sum(vals) -> float:
+    """S = RN64(sum of |v|) with the sum taken EXACTLY (rational arithmetic) and rounded
+    once; NaN if any entry is NaN, else +inf if any is infinite (reading R26)."""
+    vals = [abs(float(x)) for x in vals]
+    if any(math.isnan(v) for v in vals):
+        return math.nan
+    if any(math.isinf(v) for v in vals):
+        return math.inf
+    exact = sum((Fraction(v) for v in vals), Fraction(0))
+    return float(exact)                          # int / int true division: correctly rounded
+
+
 def sequence_td(td_steps, eta: float) -> float:
     """R2D2 sequence priority (§8f NEXT-1, S:663 "eta = 0.9 mix of max and mean";
     [EXT: R2D2 eq. p = eta max_i |delta_i| + (1 - eta) mean |delta|]), reading R26:
 
-        mx   = max_t |d_t|                         (NaN entries never win the max)
-        S    = the fp64 sum of the |d_t| in a FIXED order: eight partial sums
-               p_j = (((0 + |d_j|) + |d_{j+8}|) + |d_{j+16}|) + ...   (t = j mod 8, increasing t),
-               then S = ((p0 + p1) + (p2 + p3)) + ((p4 + p5) + (p6 + p7))
-        mean = S / T
+        mx   = max_t |d_t|                          (NaN entries never win the max)
+        S    = RN64(sum_t |d_t|)                    the EXACT sum (rational arithmetic),
+                                                    rounded once to fp64 — no summation order
+        mean = RN64(S / T)                          (IEEE division)
         mix  = RN64(RN64(eta * mx) + RN64(RN64(1 - eta) * mean))   (no fused multiply-add)
         td   = RN32(mix)
 
+    A NaN entry makes S NaN, an infinite one +inf (the transform then saturates).
     `td` then enters the ordinary priority transform (priority_value) as |delta|."""
     vals = [abs(float(x)) for x in td_steps]
     if not vals:
@@ -122,10 +135,6 @@ def sequence_td(td_steps, eta: float) -> float:
     for v in vals:
         if v > mx:
             mx = v
-    p = [0.0] * 8
-    for t, v in enumerate(vals):
-        p[t % 8] = p[t % 8] + v
-    sm = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]))
-    mean = sm / float(len(vals))
+    mean = sequence_sum(vals) / float(len(vals))
     mix = (float(eta) * mx) + ((1.0 - float(eta)) * mean)
     return rn32(mix) if math.isfinite(mix) else mix

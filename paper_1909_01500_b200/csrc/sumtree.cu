@@ -72,19 +72,110 @@ int64_t stage_cap(const int64_t* tree) {
 enum { MODE_TD = 0, MODE_Q = 1, MODE_MAXSEEN = 2, MODE_SEQ = 3 };
 
 // R2D2 sequence priority (§8f NEXT-1, reading R26): column i of the time-major per-step
-// |delta| [T_p, n] -> RN32(eta * max + (1 - eta) * mean).  Eight lanes per sequence:
-// lane j sums rows t = j (mod 8) in increasing t (its loads all in flight at once), then
-// the fixed pairwise tree ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)) via xor-shuffles 1, 2, 4 —
-// the oracle's exact fp64 operation order; no FMA contraction.  All 32 lanes of the warp
-// must call (groups of 8 consecutive lanes share i).
+// |delta| [T_p, n] -> RN32(eta * max + (1 - eta) * RN64(exact sum) / T_p).  The sum is the
+// EXACT sum rounded once to fp64 — the same value for any order of the inputs — computed by
+// eight lanes per sequence (lane j takes rows t = j mod 8):
+//   fast path  an fp64 sum, which is exact in ANY order when every non-zero |d| is a multiple
+//              of the smallest one's fp32 quantum 2^(Emin-150) and the total is below
+//              2^53 of those quanta: Emax - Emin + 24 + ceil(log2 T_p) <= 53 (exponents of
+//              the non-zero entries; typical priority columns span far fewer binades);
+//   slow path  otherwise (taken by the whole warp if any of its sequences needs it): a
+//              fixed-point superaccumulator in units of 2^-149 (the fp32 quantum), nine int64
+//              bins of 32-bit digits (24-bit significand << up to 253), lanes combined by
+//              integer adds, carries propagated, the top 64 bits rounded once to fp64 with a
+//              sticky bit.
+// All 32 lanes of the warp must call (groups of 8 consecutive lanes share i).  No FMA.
+constexpr int SA_DIGITS = 9;
+
+__device__ __forceinline__ void sa_add(int64_t (&bins)[SA_DIGITS], uint32_t bits) {
+  const uint32_t E = (bits >> 23) & 0xffu;
+  const uint32_t M = E ? ((bits & 0x7fffffu) | 0x800000u) : (bits & 0x7fffffu);
+  const int sh = E ? (int)E - 1 : 0;  // value = M << sh in units of 2^-149
+  const int d = sh >> 5;
+  const uint64_t part = (uint64_t)M << (sh & 31);
+  const int64_t lo = (int64_t)(part & 0xffffffffull), hi = (int64_t)(part >> 32);
+#pragma unroll
+  for (int k = 0; k < SA_DIGITS; ++k) bins[k] += (k == d ? lo : 0) + (k == d + 1 ? hi : 0);
+}
+
+// RN64 of the superaccumulator's value (digits in base 2^32, units of 2^-149).
+__device__ __forceinline__ double sa_round(const int64_t (&bins)[SA_DIGITS]) {
+  uint32_t dg[SA_DIGITS + 1];
+  uint64_t carry = 0;
+#pragma unroll
+  for (int k = 0; k < SA_DIGITS; ++k) {
+    const uint64_t v = (uint64_t)bins[k] + carry;
+    dg[k] = (uint32_t)v;
+    carry = v >> 32;
+  }
+  dg[SA_DIGITS] = (uint32_t)carry;
+  int h = -1;
+#pragma unroll
+  for (int k = 0; k <= SA_DIGITS; ++k)
+    if (dg[k]) h = k;
+  if (h < 0) return 0.0;
+  uint32_t a = 0, b = 0, c = 0;
+  bool sticky = false;
+#pragma unroll
+  for (int k = 0; k <= SA_DIGITS; ++k) {
+    if (k == h) a = dg[k];
+    if (k == h - 1) b = dg[k];
+    if (k == h - 2) c = dg[k];
+    if (k < h - 2 && dg[k]) sticky = true;
+  }
+  const int lz = __clz(a);
+  const uint64_t ab = ((uint64_t)a << 32) | b;
+  uint64_t top = lz ? ((ab << lz) | (c >> (32 - lz))) : ab;  // bit 63: the leading one
+  const uint32_t rest = lz ? (c << lz) : c;
+  if (rest) sticky = true;
+  if (sticky) top |= 1ull;  // below the rounding position of 64 -> 53 bits: exact RN
+  // top's bit 0 has weight 2^(32 h - 32 - lz) units of 2^-149
+  return ldexp(__ull2double_rn(top), 32 * h - 32 - lz - 149);
+}
+
+// Exact sum of the |d| of rows t = j (mod 8) over the 8-lane group, rounded once (RN64).
+// All 32 lanes call.  Non-finite entries are skipped (the caller handles them).
+__device__ __noinline__ double seq_exact_sum(const float* __restrict__ steps, int64_t T_p, int64_t n, int64_t i,
+                                             bool active) {
+  int64_t bins[SA_DIGITS];
+#pragma unroll
+  for (int k = 0; k < SA_DIGITS; ++k) bins[k] = 0;
+  if (active)
+    for (int64_t t = threadIdx.x & 7; t < T_p; t += 8) {
+      const uint32_t bits = __float_as_uint(__ldg(steps + t * n + i)) & 0x7fffffffu;
+      if ((bits >> 23) != 255u) sa_add(bins, bits);
+    }
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1)
+#pragma unroll
+    for (int k = 0; k < SA_DIGITS; ++k)
+      bins[k] += (int64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)bins[k], o);
+  return sa_round(bins);
+}
+
 __device__ __forceinline__ float sequence_td8(const float* __restrict__ steps, int64_t T_p, int64_t n, int64_t i,
                                               bool active, double eta) {
   const int j = threadIdx.x & 7;
   double mx = 0.0, sm = 0.0;
+  int emin = 255, emax = 0, nonfin = 0;  // exponents of the non-zero finite entries; 1 inf, 2 NaN
+  auto take = [&](float x) {
+    const uint32_t bits = __float_as_uint(x) & 0x7fffffffu;
+    const int E = (int)(bits >> 23);
+    if (E == 255) {
+      nonfin |= (bits & 0x7fffffu) ? 2 : 1;
+    } else if (bits) {
+      const int Ee = E ? E : 1;
+      emin = Ee < emin ? Ee : emin;
+      emax = Ee > emax ? Ee : emax;
+    }
+    const double v = (double)__uint_as_float(bits);
+    if (v > mx) mx = v;  // NaN never wins
+    sm = __dadd_rn(sm, v);
+  };
+  constexpr int TD8_BATCH = 16;
   if (active) {
     // the first 8 * TD8_BATCH rows: every load issued before the first is consumed (one L2
-    // round trip, not one per unrolled group), then the same in-order accumulation
-    constexpr int TD8_BATCH = 16;
+    // round trip, not one per unrolled group)
     float vals[TD8_BATCH];
 #pragma unroll
     for (int u = 0; u < TD8_BATCH; ++u) {
@@ -92,26 +183,30 @@ __device__ __forceinline__ float sequence_td8(const float* __restrict__ steps, i
       vals[u] = t < T_p ? __ldg(steps + t * n + i) : 0.0f;
     }
 #pragma unroll
-    for (int u = 0; u < TD8_BATCH; ++u) {
-      if (j + 8 * (int64_t)u < T_p) {
-        const double v = fabs((double)vals[u]);
-        if (v > mx) mx = v;
-        sm = __dadd_rn(sm, v);
-      }
-    }
-    for (int64_t t = j + 8 * (int64_t)TD8_BATCH; t < T_p; t += 8) {
-      const double v = fabs((double)__ldg(steps + t * n + i));
-      if (v > mx) mx = v;
-      sm = __dadd_rn(sm, v);
-    }
+    for (int u = 0; u < TD8_BATCH; ++u)
+      if (j + 8 * (int64_t)u < T_p) take(vals[u]);
+    for (int64_t t = j + 8 * (int64_t)TD8_BATCH; t < T_p; t += 8) take(__ldg(steps + t * n + i));
   }
 #pragma unroll
   for (int o = 1; o < 8; o <<= 1) {
     const double so = __shfl_xor_sync(0xffffffffu, sm, o);
     const double mo = __shfl_xor_sync(0xffffffffu, mx, o);
+    const int lo = __shfl_xor_sync(0xffffffffu, emin, o);
+    const int hi = __shfl_xor_sync(0xffffffffu, emax, o);
+    nonfin |= __shfl_xor_sync(0xffffffffu, nonfin, o);
     sm = __dadd_rn(sm, so);  // IEEE addition is commutative: both partners get the same sum
     if (mo > mx) mx = mo;
+    emin = lo < emin ? lo : emin;
+    emax = hi > emax ? hi : emax;
   }
+  const int lgT = T_p <= 1 ? 0 : 64 - __clzll((unsigned long long)(T_p - 1));  // ceil(log2 T_p)
+  const bool exact = nonfin || emax == 0 || (emax - emin + 24 + lgT <= 53);
+  if (__any_sync(0xffffffffu, active && !exact)) {
+    // slow path (whole warp, out of line: it is rare and must not bloat the hot code)
+    const double se = seq_exact_sum(steps, T_p, n, i, active);
+    if (!exact) sm = se;
+  }
+  if (nonfin) sm = (nonfin & 2) ? __longlong_as_double(0x7ff8000000000000ll) : __longlong_as_double(0x7ff0000000000000ll);
   const double mean = __ddiv_rn(sm, (double)T_p);
   const double mix = __dadd_rn(__dmul_rn(eta, mx), __dmul_rn(__dadd_rn(1.0, -eta), mean));
   return __double2float_rn(mix);
@@ -976,7 +1071,7 @@ extern "C" int rpl_sample_uniform(int64_t n, uint64_t seed, uint64_t offset, uin
 extern "C" int rpl_sumtree_update_seq(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx,
                                       const float* td_steps, int64_t T_p, int64_t n, double eta, double alpha,
                                       double eps_p, int32_t flags, int32_t* dev_err, void* stream) {
-  if (n > 0 && (!td_steps || T_p < 1)) return RPL_EINVAL;
+  if (n > 0 && (!td_steps || T_p < 1 || T_p > (1ll << 30))) return RPL_EINVAL;
   if (!(alpha >= 0.0) || !(eps_p >= 0.0) || !(eta >= 0.0 && eta <= 1.0) || (flags & ~RPL_UPD_LIVE_ONLY))
     return RPL_EINVAL;
   return launch_update(L, tree, idx, td_steps, nullptr, MODE_SEQ, n, alpha, eps_p, dev_err, stream, 0, T_p, eta,
@@ -1016,7 +1111,8 @@ extern "C" int rpl_sumtree_update_sample(const rpl_tree_layout* L, int64_t* tree
                                          const float* td, int64_t T_p, int64_t n_upd, double eta, double alpha,
                                          double eps_p, int32_t flags, int64_t n, uint64_t seed, int64_t* out_idx,
                                          int64_t* out_q, int32_t* dev_err, void* stream) {
-  if (!layout_ok(L) || !tree || !out_idx || !out_q || n < 1 || n > (1ll << 30) || n_upd < 0 || T_p < 0)
+  if (!layout_ok(L) || !tree || !out_idx || !out_q || n < 1 || n > (1ll << 30) || n_upd < 0 || T_p < 0 ||
+      T_p > (1ll << 30))
     return RPL_EINVAL;
   if (n_upd > 0 && (!idx || !td)) return RPL_EINVAL;
   if (!(alpha >= 0.0) || !(eps_p >= 0.0) || !(eta >= 0.0 && eta <= 1.0) || (flags & ~RPL_UPD_LIVE_ONLY))

@@ -603,3 +603,53 @@ def test_update_sample_graph_replay(rpl):
         r.update_seq(uidx, utd, 0.6, eta=0.9)
         ri, rq, _, _ = r.sample_stream(64, 5, want_qmin=False)
         assert np.array_equal(H(oi), H(ri)) and np.array_equal(H(oq), H(rq)), step
+
+
+def test_update_seq_exact_sum_order_independent(rpl):
+    # Reading R26: the sequence mean uses the EXACT sum rounded once (oracle.priority.sequence_sum),
+    # so the GPU must match for any order of the rows.  alpha = 1, eps_p = 0, F = 20 make the
+    # leaf q = td * 2^20 exactly (td >= 8), i.e. the leaves expose td bit for bit.  Columns:
+    # the order-sensitive column of test_oracle_priority (bigs first / permuted), wide-exponent
+    # columns (2^-60 .. 2^24 plus zeros and subnormals: the superaccumulator path) and narrow
+    # ones (the any-order fp64 fast path) — fast and slow sequences share warps.
+    import torch
+    g = rng(1234)
+    N, T_p, n = 25600, 64, 96
+    base = np.array([2.0 ** 40] * 31 + [2.0 ** 20] + [2.0 ** -10] * 32, np.float32)
+    base_small = (base.astype(np.float64) / 2.0 ** 20).astype(np.float32)  # same shape, fits F=20
+    cols = []
+    for k in range(n):
+        kind = k % 4
+        if kind == 0:
+            cols.append(base_small)
+        elif kind == 1:
+            cols.append(g.permutation(base_small))
+        elif kind == 2:
+            c = (2.0 ** g.uniform(-60, 24, T_p)).astype(np.float32)
+            c[g.random(T_p) < 0.1] = 0.0
+            c[0] = np.float32(1e-44)                      # a subnormal
+            cols.append(c)
+        else:
+            cols.append((np.abs(g.normal(0, 1, T_p)) * 64 + 8).astype(np.float32))
+    steps = np.ascontiguousarray(np.stack(cols, axis=1))
+    idx = g.choice(N, n, replace=False).astype(np.int64)
+    t = rpl.SumTree(N, 32, 20)
+    t.update_seq(T_(idx), T_(steps), 1.0, eta=0.0, eps_p=0.0)
+    orc = OS.SumTreeOracle(N, 20)
+    td = [OPR.sequence_td(steps[:, k], 0.0) for k in range(n)]
+    orc.update([int(x) for x in idx], td, 1.0, 0.0)
+    check_tree_consistent(t, orc)
+    leaves = H(t.leaves)
+    for k in range(n):
+        assert int(leaves[idx[k]]) == orc.q[int(idx[k])], k
+    # the order-sensitive columns take the exact-sum value (a lossy order rounds one ulp lower)
+    assert orc.q[int(idx[0])] == int((31 * 2.0 ** 14 + 2.0 ** -5) * 2 ** 20)
+    # eta = 0.9 on the same columns plus NaN / inf columns: saturation flags, tree consistent
+    steps2 = steps.copy()
+    steps2[3, 2] = np.inf
+    steps2[5, 6] = np.nan
+    t2 = rpl.SumTree(N, 32, 20)
+    t2.update_seq(T_(idx), T_(steps2), 0.9, eta=0.9, eps_p=1e-3)
+    orc2 = OS.SumTreeOracle(N, 20)
+    orc2.update([int(x) for x in idx], [OPR.sequence_td(steps2[:, k], 0.9) for k in range(n)], 0.9, 1e-3)
+    check_tree_consistent(t2, orc2)

@@ -130,3 +130,47 @@ def test_sequence_td_order_of_max_and_abs():
     a = P.sequence_td([-4.0, 1.0, 2.0], 0.5)
     b = P.sequence_td([2.0, 1.0, 4.0], 0.5)
     assert a == b == float(np.float32(0.5 * 4 + 0.5 * (7 / 3)))
+
+
+def _order_sensitive_column():
+    # 31 x 2^40, then 2^20, then 32 x 2^-10 (T = 64, all fp32-exact).  The exact sum is
+    # 31*2^40 + 2^20 + 2^-5 (50 significant bits: representable, so S is exactly that); any
+    # fp64 accumulation that adds a 2^-10 to the ~2^45 partial sum loses it (ulp there is
+    # 2^-8, half-ulp 2^-9), giving 31*2^40 + 2^20.  The mean then straddles an fp32 tie:
+    # exact 31*2^34 + 2^14 + 2^-11 -> 31*2^34 + 2^15; lossy 31*2^34 + 2^14 (a tie) -> 31*2^34.
+    return [2.0 ** 40] * 31 + [2.0 ** 20] + [2.0 ** -10] * 32
+
+
+def test_sequence_sum_exact_hand_value_and_order_independence():
+    col = _order_sensitive_column()
+    assert P.sequence_sum(col) == 31 * 2.0 ** 40 + 2.0 ** 20 + 2.0 ** -5
+    naive = 0.0
+    for v in col:                    # sequential fp64 (what a loop in increasing t would give)
+        naive += v
+    assert naive == 31 * 2.0 ** 40 + 2.0 ** 20          # the small terms are lost
+    # eta = 0: td is RN32 of the mean; hand-derived values above
+    assert P.sequence_td(col, 0.0) == 31 * 2.0 ** 34 + 2.0 ** 15
+    assert float(np.float32(naive / 64)) == 31 * 2.0 ** 34  # the lossy sum would round down
+    g = np.random.default_rng(3)
+    for _ in range(20):              # any order of the same multiset: identical result
+        perm = list(g.permutation(col))
+        assert P.sequence_sum(perm) == P.sequence_sum(col)
+        assert P.sequence_td(perm, 0.9) == P.sequence_td(col, 0.9)
+
+
+def test_sequence_sum_matches_fsum_on_wide_columns():
+    # math.fsum (Shewchuk's algorithm, correctly rounded) is an independent exact-sum routine
+    import math
+    g = np.random.default_rng(4)
+    for trial in range(200):
+        T = int(g.integers(1, 200))
+        if trial % 2:
+            col = np.exp(g.normal(0, 6, T)).astype(np.float32)        # heavy-tailed
+        else:
+            col = (10.0 ** g.uniform(-38, 38, T)).astype(np.float32)    # every fp32 binade
+        col[g.random(T) < 0.1] = 0.0
+        vals = [float(x) for x in col]
+        assert P.sequence_sum(vals) == math.fsum(vals)
+    assert math.isnan(P.sequence_sum([1.0, float("nan"), float("inf")]))
+    assert P.sequence_sum([1.0, float("inf")]) == float("inf")
+    assert P.sequence_sum([0.0] * 7) == 0.0
