@@ -6,10 +6,10 @@ elems/sec, 1/2/4/8 B200".  One STEP = one learner update's replay work on the
 R2D2 config (BASELINE.json configs[4]):
 
     rpl_sumtree_update   64 sequence priorities of the previous batch  (a5-a7)
-    rpl_sumtree_sample   64 stratified draws + IS weights               (a8-a9)
+    rpl_sumtree_sample   64 stratified draws                            (a8)
     rpl_gather           64 sequences x 125 rows, frame stacks, prev fields,
-                         stored LSTM state                              (a11)
-    rpl_returns_nstep    rescaled 5-step targets for the 80 train rows  (a2, a4)
+                         stored LSTM state, IS weights (a9) and the
+                         rescaled 5-step targets of the 80 train rows   (a11, a2, a4)
 
 `value` = sequences/s over all ranks (weak scaling: 64 sequences per rank per
 step, Mode L of SURVEY.md §8e).  A secondary line-item times GAE + discounted
@@ -176,6 +176,12 @@ def gather_traffic():
         return {}
 
 
+def r2d2_targets(c, q):
+    """Fused rescaled n-step targets of the train rows (rpl_gather_desc.o_tgt): rows
+    burn_in .. burn_in+train-1, bootstrap q [L, n] at row tau + n_step (R5, R24)."""
+    return dict(lo=c["burn_in"], T=c["train"], n_step=c["n_step"], gamma=c["gamma"], rescale=True, eps=c["eps"], q=q)
+
+
 def seq_bytes_per_sample(c, act_bytes=8):
     """Algorithmic HBM bytes one sequence of rpl_gather moves:
     reads the L+k-1 unique frames, the per-row scalars and the stored state;
@@ -187,6 +193,8 @@ def seq_bytes_per_sample(c, act_bytes=8):
     wr = L * k * FRAME                            # stacked observations
     wr += L * (2 * act_bytes + 4 + 4 + 1)         # act, prev_act, rew, prev_rew, done
     wr += c["rnn_parts"] * c["rnn_h"] * 4
+    rd += c["train"] * 4                          # fused targets: bootstrap q of each train row
+    wr += c["train"] * (4 + 1)                    # target y and done^n
     return rd + wr
 
 
@@ -266,14 +274,19 @@ def run_rpl(args):
         if rank == 0:
             stacked = torch.empty((L, n_glob, k) + tuple(ring.item_shape), dtype=torch.uint8, device=dev)
     else:
-        plan = rpl.GatherPlan(ring, n_glob, kind="sequence", k=k, seq_len=L, period=period, with_weights=True)
+        plan = rpl.GatherPlan(ring, n_glob, kind="sequence", k=k, seq_len=L, period=period, with_weights=True,
+                              targets=r2d2_targets(c, q_pool[0]))
     out = plan.outputs
+    fused_tgt = not mode_c  # Mode C: the learner computes targets after the central batch lands
     idx_buf = [torch.full((n_glob,), -1, dtype=torch.int64, device=dev) for _ in range(2)]
     q_buf = torch.zeros(n_glob, dtype=torch.int64, device=dev)
     qmin = torch.zeros(1, dtype=torch.int64, device=dev)
     w = plan.outputs["w"]  # IS weights: written by the gather (1 GPU) or rpl_is_weights (Mode L)
-    y = torch.empty((c["train"], n_glob), dtype=torch.float32, device=dev)
-    dn = torch.empty((c["train"], n_glob), dtype=torch.uint8, device=dev)
+    if fused_tgt:
+        y, dn = out["tgt"], out["tgt_done"]
+    else:
+        y = torch.empty((c["train"], n_glob), dtype=torch.float32, device=dev)
+        dn = torch.empty((c["train"], n_glob), dtype=torch.uint8, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     totals = torch.zeros(world, dtype=torch.int64, device=dev)
     my_total = torch.zeros(1, dtype=torch.int64, device=dev)
@@ -351,10 +364,16 @@ def run_rpl(args):
         # IS weights fused into the gather: batch min (1 GPU) or the all-reduced global min (Mode L)
         if w_out is not None:
             plan.desc.o_w = w_out.data_ptr()
-        # (K7 fused with p2p: the gather publishes / reads the batch mins over the boards)
-        plan.run(cur, q=q_buf, qmin=None if (world == 1 or p2p) else qmin, beta=c["beta"], err=err, stream=s)
+        if fused_tgt and y_out is not None:
+            plan.desc.o_tgt = y_out.data_ptr()
+        # (K7 fused with p2p: the gather publishes / reads the batch mins over the boards;
+        #  a2 + a4 fused: the rescaled 5-step targets of the train rows, bootstrap q_i)
+        plan.run(cur, q=q_buf, qmin=None if (world == 1 or p2p) else qmin, beta=c["beta"], err=err, stream=s,
+                 q_tgt=q_i if fused_tgt else None)
         if w_out is not None:
             plan.desc.o_w = w.data_ptr()
+        if fused_tgt and y_out is not None:
+            plan.desc.o_tgt = y.data_ptr()
         if gather_events is not None:
             gather_events[1].record()
         if mode_c:
@@ -362,7 +381,7 @@ def run_rpl(args):
             if rank == 0:  # learner: k-stacks from the shipped unique rows (local HBM)
                 rpl._lib.check(lib.rpl_stack_frames(P_(out["obs"]), P_(out["start"]), L, n_glob, k, ring.obs_bytes,
                                                     0, P_(stacked), None, s), "stack")
-        if learner:
+        if learner and not fused_tgt:
             rpl._lib.check(lib.rpl_returns_nstep(P_(r_tr), P_(d_tr), Tn, n_glob, c["n_step"], c["gamma"],
                                                  P_(q_i[c["burn_in"]:c["burn_in"] + Tn]),
                                                  P_(q_i[c["burn_in"] + Tn]), 1, c["eps"],
@@ -473,8 +492,7 @@ def run_rpl(args):
     pipelined = None
     if world == 1 and not args.no_secondary and not args.profile:
         try:
-            pipelined = pipelined_step(dev, rpl, tree, plan, idx_buf, td_pool, q_pool, r_tr, d_tr, y, dn, err, c, n,
-                                       P, seed, Tn)
+            pipelined = pipelined_step(dev, rpl, tree, plan, idx_buf, td_pool, q_pool, err, c, n, P, seed)
         except Exception as e:  # pragma: no cover
             pipelined = {"error": f"{type(e).__name__}: {e}"[:300]}
 
@@ -746,7 +764,7 @@ def bench_ppo(dev, rpl):
             "timing": "CUDA graph of one call per pool entry, replayed; per-call average"}
 
 
-def pipelined_step(dev, rpl, tree, plan, idx_buf, td_pool, q_pool, r_tr, d_tr, y, dn, err, c, n, P, seed, Tn):
+def pipelined_step(dev, rpl, tree, plan, idx_buf, td_pool, q_pool, err, c, n, P, seed):
     """SURVEY §8d's secondary step variant: the same four calls, but update(i+1) +
     sample(i+1) run on a second stream while gather(i) + n-step(i) run (the paper's
     asynchronous sampler/optimiser overlap, Fig. 3).  Dependencies: gather(i) waits for
@@ -775,11 +793,7 @@ def pipelined_step(dev, rpl, tree, plan, idx_buf, td_pool, q_pool, r_tr, d_tr, y
             with torch.cuda.stream(sB):
                 sB.wait_event(ev_s[i % P])
                 b = rpl.ops._stream(dev)
-                plan.run(cur, q=qb[i % 2], qmin=None, beta=c["beta"], err=err, stream=b)
-                rpl._lib.check(lib.rpl_returns_nstep(P_(r_tr), P_(d_tr), Tn, n, c["n_step"], c["gamma"],
-                                                     P_(q_pool[i % P][c["burn_in"]:c["burn_in"] + Tn]),
-                                                     P_(q_pool[i % P][c["burn_in"] + Tn]), 1, c["eps"], P_(y),
-                                                     P_(dn), b), "nstep")
+                plan.run(cur, q=qb[i % 2], qmin=None, beta=c["beta"], err=err, stream=b, q_tgt=q_pool[i % P])
                 ev_g[i % P].record(sB)
 
     cap = torch.cuda.Stream(dev)
@@ -808,7 +822,7 @@ def pipelined_step(dev, rpl, tree, plan, idx_buf, td_pool, q_pool, r_tr, d_tr, y
     rpl.check_err(err)
     ms = e0.elapsed_time(e1) / (reps * P)
     return {"us_per_step": ms * 1e3, "sequences_per_s": n / (ms / 1e3),
-            "timing": "CUDA graph of 8 steps on two streams (update+sample || gather+n-step), replayed"}
+            "timing": "CUDA graph of 8 steps on two streams (update+sample || gather with fused targets), replayed"}
 
 
 def bench_r2d2_1mseq(dev, rpl, c):
@@ -841,18 +855,16 @@ def time_r2d2_step(dev, rpl, c, cap, B, seed, cursor, workload):
     g = torch.Generator(device=dev)
     g.manual_seed(seed)
     tree.update(valid, torch.randn(valid.numel(), generator=g, device=dev).abs(), c["alpha"], c["eps_p"])
-    plan = rpl.GatherPlan(ring, n, kind="sequence", k=k, seq_len=L, period=period, with_weights=True)
-    out = plan.outputs
+    qv = None
+    plan = None
     idx = [torch.full((n,), -1, dtype=torch.int64, device=dev) for _ in range(2)]
     q = torch.zeros(n, dtype=torch.int64, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     td = torch.randn((8, c["train"], n), generator=g, device=dev).abs()
     qv = torch.randn((8, L, n), generator=g, device=dev) * 10
-    Tn = c["train"] + c["n_step"] - 1
-    r_tr = out["rew"][c["burn_in"]:c["burn_in"] + Tn]
-    d_tr = out["done"][c["burn_in"]:c["burn_in"] + Tn]
-    y = torch.empty((c["train"], n), dtype=torch.float32, device=dev)
-    dn = torch.empty((c["train"], n), dtype=torch.uint8, device=dev)
+    plan = rpl.GatherPlan(ring, n, kind="sequence", k=k, seq_len=L, period=period, with_weights=True,
+                          targets=r2d2_targets(c, qv[0]))
+    out = plan.outputs
     lib, P_ = rpl._lib.lib, rpl.ops._ptr
 
     def step(i):
@@ -861,10 +873,7 @@ def time_r2d2_step(dev, rpl, c, cap, B, seed, cursor, workload):
                                                   c["train"], n, c["eta"], c["alpha"], c["eps_p"], 0, None, s), "upd")
         rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, 0xBEEF, c["beta"], P_(idx[i % 2]),
                                                      P_(q), None, None, P_(err), s), "sample")
-        plan.run(idx[i % 2], q=q, qmin=None, beta=c["beta"], err=err, stream=s)
-        rpl._lib.check(lib.rpl_returns_nstep(P_(r_tr), P_(d_tr), Tn, n, c["n_step"], c["gamma"],
-                                             P_(qv[i % 8][c["burn_in"]:c["burn_in"] + Tn]),
-                                             P_(qv[i % 8][c["burn_in"] + Tn]), 1, c["eps"], P_(y), P_(dn), s), "nstep")
+        plan.run(idx[i % 2], q=q, qmin=None, beta=c["beta"], err=err, stream=s, q_tgt=qv[i % 8])
 
     ms = _graph_time(dev, step, P=8, reps=50)
     rpl.check_err(err)
@@ -885,14 +894,8 @@ def unique_output_step(dev, rpl, tree, ring, idx_buf, td_pool, q_pool, err, c, n
     lib, P_ = rpl._lib.lib, rpl.ops._ptr
     L, k, period = c["L"], c["k"], c["period"]
     plan = rpl.GatherPlan(ring, n, kind="sequence", k=k, seq_len=L, period=period, with_weights=True,
-                          out_mode=_lib.OUT_UNIQUE)
-    out = plan.outputs
+                          out_mode=_lib.OUT_UNIQUE, targets=r2d2_targets(c, q_pool[0]))
     q = torch.zeros(n, dtype=torch.int64, device=dev)
-    Tn = c["train"] + c["n_step"] - 1
-    r_tr = out["rew"][c["burn_in"]:c["burn_in"] + Tn]
-    d_tr = out["done"][c["burn_in"]:c["burn_in"] + Tn]
-    y = torch.empty((c["train"], n), dtype=torch.float32, device=dev)
-    dn = torch.empty((c["train"], n), dtype=torch.uint8, device=dev)
 
     def step(i):
         s = rpl.ops._stream(dev)
@@ -901,11 +904,7 @@ def unique_output_step(dev, rpl, tree, ring, idx_buf, td_pool, q_pool, err, c, n
                                                   c["train"], n, c["eta"], c["alpha"], c["eps_p"], 0, None, s), "upd")
         rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, seed, c["beta"], P_(cur), P_(q),
                                                      None, None, P_(err), s), "sample")
-        plan.run(cur, q=q, qmin=None, beta=c["beta"], err=err, stream=s)
-        rpl._lib.check(lib.rpl_returns_nstep(P_(r_tr), P_(d_tr), Tn, n, c["n_step"], c["gamma"],
-                                             P_(q_pool[i % P][c["burn_in"]:c["burn_in"] + Tn]),
-                                             P_(q_pool[i % P][c["burn_in"] + Tn]), 1, c["eps"], P_(y), P_(dn), s),
-                       "nstep")
+        plan.run(cur, q=q, qmin=None, beta=c["beta"], err=err, stream=s, q_tgt=q_pool[i % P])
 
     ms = _graph_time(dev, step, P=8, reps=50)
     rpl.check_err(err)

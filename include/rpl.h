@@ -74,7 +74,8 @@ int rpl_config(char* buf, int64_t len);
 /* =========================================================================
  * (1) Return estimation over time-major [T,B] buffers.  fp32 I/O, fp64
  *     accumulation, one rounding to fp32 per output (§8c #21).
- *     r: rewards f32 [T,B]; d: done u8 [T,B] (1 = episode ended after row t, §8c #1).
+ *     r: rewards f32 [T,B]; d: done u8 [T,B] (non-zero = episode ended after row t, §8c #1;
+ *     2 = ended by a time limit, bootstrapped by the _tl variants below, R34).
  * ========================================================================= */
 
 /* R_t = r_t + gamma (1 - d_t) R_{t+1},  R_T = bootstrap[b] (or 0 if bootstrap == NULL).
@@ -99,6 +100,26 @@ int rpl_returns_nstep(const float* r, const uint8_t* d, int64_t T, int64_t B, in
  * v: f32 [T,B]; bootstrap_v: f32 [B] (required); adv, ret: f32 [T,B] (ret may be NULL). */
 int rpl_gae(const float* r, const float* v, const uint8_t* d, const float* bootstrap_v,
             int64_t T, int64_t B, double gamma, double lambda, float* adv, float* ret, void* stream);
+
+/* Time-limit bootstrap variants (reading R34; P:95 fn "bootstrapping the value function when
+ * the trajectory ends due to time limit").  d may hold RPL_DONE_TIMEOUT (2): the
+ * episode ended after row t by a time limit.  Every non-zero d_t ends the episode (the
+ * recursion is cut as above); with v_term (f32 [T,B], device, may be NULL) a time-limit row
+ * bootstraps from the value of its final observation: the term gamma * v_term_t stands where
+ * gamma * (next value) would have stood —
+ *   discounted  R_t = r_t + gamma v_term_t                       at a time-limit row
+ *   n-step      R^n_t gets gamma^(j+1) v_term_{t+j} when its first ended row t+j is a
+ *               time-limit row (done^n_t stays 1: the learner must not bootstrap again)
+ *   GAE         delta_t = r_t + gamma v_term_t - V_t             at a time-limit row
+ * v_term is read only at time-limit rows.  With v_term NULL these equal the plain entries
+ * (which treat d = 2 as a terminal). */
+int rpl_returns_discounted_tl(const float* r, const uint8_t* d, const float* v_term, const float* bootstrap,
+                              int64_t T, int64_t B, double gamma, float* ret, void* stream);
+int rpl_returns_nstep_tl(const float* r, const uint8_t* d, const float* v_term, int64_t T, int64_t B, int32_t n,
+                         double gamma, const float* q, const float* q_boot, int32_t rescale, double rescale_eps,
+                         float* ret_n, uint8_t* done_n, void* stream);
+int rpl_gae_tl(const float* r, const float* v, const uint8_t* d, const float* v_term, const float* bootstrap_v,
+               int64_t T, int64_t B, double gamma, double lambda, float* adv, float* ret, void* stream);
 
 /* Value rescaling h (inverse == 0) or h^-1 (inverse != 0), elementwise over n floats, S:810:
  *   h(x) = sign(x)(sqrt(|x|+1) - 1) + eps x, evaluated in fp64 in the cancellation-free

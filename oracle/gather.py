@@ -70,8 +70,9 @@ def window_valid_sequence(row0, cap, cursor, size, k, L):
     return (L - 1) <= age and age + max(k - 1, 1) <= size - 1
 
 
-def gather_transitions(idx, B, obs, act, rew, done, k, n, gamma, pad_mode=PAD_REPEAT):
-    """DQN / Mujoco transition gather.
+def gather_transitions(idx, B, obs, act, rew, done, k, n, gamma, pad_mode=PAD_REPEAT, v_term=None):
+    """DQN / Mujoco transition gather.  v_term [cap, B] (optional):
+    terminal values of time-limit rows (done == 2), bootstrapped by the n-step return (R34).
 
     obs [cap, B, *item], act [cap, B, *a], rew [cap, B] f32, done [cap, B] u8.
     Returns dict: obs [n_s, k, *item], next_obs [n_s, k, *item], act [n_s, *a],
@@ -94,7 +95,8 @@ def gather_transitions(idx, B, obs, act, rew, done, k, n, gamma, pad_mode=PAD_RE
         o_next[s] = wrapper_stacks(obs, done, b, [r + n], k, pad_mode)[0]
         o_act[s] = act[r, b]
         rows = [_row(r + i, cap) for i in range(n)]
-        R, dn = _ret.nstep_return(rew[rows, b][:, None], done[rows, b][:, None], n, gamma)
+        R, dn = _ret.nstep_return(rew[rows, b][:, None], done[rows, b][:, None], n, gamma,
+                                  v_term=None if v_term is None else v_term[rows, b][:, None])
         o_ret[s] = R[0, 0]
         o_dn[s] = dn[0, 0]
     return dict(obs=o_obs, next_obs=o_next, act=o_act, ret=o_ret, done_n=o_dn)

@@ -22,6 +22,7 @@ DERR = {1: "RPL_DERR_IDX", 2: "RPL_DERR_SATURATED", 4: "RPL_DERR_EMPTY", 8: "RPL
 GATHER_TRANSITION, GATHER_SEQUENCE = 0, 1
 PAD_REPEAT, PAD_ZERO = 0, 1
 OUT_STACKED, OUT_UNIQUE = 0, 1
+DONE_TERMINAL, DONE_TIMEOUT = 1, 2
 
 
 class TreeLayout(C.Structure):
@@ -55,6 +56,10 @@ class GatherDesc(C.Structure):
         ("col_offset", C.c_void_p),
         ("o_start", C.c_void_p),
         ("peer_boards", C.c_void_p), ("peer_world", C.c_int32), ("peer_rank", C.c_int32),
+        ("q_tgt", C.c_void_p), ("o_tgt", C.c_void_p), ("o_tgt_done", C.c_void_p),
+        ("tgt_lo", C.c_int32), ("tgt_T", C.c_int32), ("rescale", C.c_int32), ("_pad1", C.c_int32),
+        ("rescale_eps", C.c_double),
+        ("v_term", C.c_void_p),
     ]
 
 
@@ -73,6 +78,9 @@ _SIGS = {
     "rpl_returns_nstep": ([P, P, I64, I64, I32, D, P, P, I32, D, P, P, P], C.c_int),
     "rpl_gae": ([P, P, P, P, I64, I64, D, D, P, P, P], C.c_int),
     "rpl_value_rescale": ([P, P, I64, D, I32, P], C.c_int),
+    "rpl_returns_discounted_tl": ([P, P, P, P, I64, I64, D, P, P], C.c_int),
+    "rpl_returns_nstep_tl": ([P, P, P, I64, I64, I32, D, P, P, I32, D, P, P, P], C.c_int),
+    "rpl_gae_tl": ([P, P, P, P, P, I64, I64, D, D, P, P, P], C.c_int),
     "rpl_sumtree_layout": ([I64, I32, I32, C.POINTER(TreeLayout)], C.c_int),
     "rpl_sumtree_init": ([C.POINTER(TreeLayout), P, P], C.c_int),
     "rpl_sumtree_update": ([C.POINTER(TreeLayout), P, P, P, I64, D, D, P, P], C.c_int),

@@ -111,6 +111,21 @@ int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cud
   return launch_pdl_cluster(kernel, grid, block, smem, st, 1u, args...);
 }
 
+__device__ __forceinline__ double h_fwd(double x, double eps) {
+  // h(x) = x (1/(sqrt(|x|+1)+1) + eps)  ==  sign(x)(sqrt(|x|+1)-1) + eps x   (§8c #4)
+  return x * (1.0 / (sqrt(fabs(x) + 1.0) + 1.0) + eps);
+}
+
+__device__ __forceinline__ double h_inv(double y, double eps) {
+  // s = sqrt(x+1) solves eps s^2 + s - (1 + eps + |y|) = 0 (rationalised root);
+  // x = (s-1)(s+1) with s-1 = |y| / (1 + eps (s+1))            (§8c #4)
+  const double a = fabs(y);
+  const double c = a + 1.0 + eps;
+  const double s = 2.0 * c / (1.0 + sqrt(1.0 + 4.0 * eps * c));
+  const double x = a * (s + 1.0) / (1.0 + eps * (s + 1.0));
+  return copysign(x, y);
+}
+
 __device__ __forceinline__ void set_err(int32_t* err, int32_t bits) {
   if (err) atomicOr(err, bits);
 }

@@ -195,6 +195,12 @@ struct GDesc {
   int8_t* o_start;            // per-row episode-start offsets [L, n] (NULL: not produced)
   int64_t* const* peer_boards;  // K7 fused (rpl_gather_desc.peer_boards; NULL: off)
   int peer_world, peer_rank;
+  const float* q_tgt;  // fused n-step targets (rpl_gather_desc.q_tgt / o_tgt / ...)
+  float* o_tgt;
+  uint8_t* o_tgt_done;
+  int tgt_lo, tgt_T, rescale;
+  double rescale_eps;
+  const float* v_term;  // time-limit bootstrap values (R34; NULL: every done is terminal)
 };
 
 // Output column offset (rpl_gather_desc.col_offset); read after pdl_wait.
@@ -223,6 +229,49 @@ __device__ __forceinline__ int stack_src(const uint8_t* dwin, int ti, int j, int
   const int want = ti - k + 1 + j;
   if (want >= s) return want;
   return pad_mode == RPL_PAD_ZERO ? -1 : s;
+}
+
+// n-step return over ring rows row .. row+ns-1 (mod cap_T) of column b (a2, R24): fp64
+// Horner from the last row, starting from the bootstrap value `acc`; a done row cuts the
+// recursion (acc = r), and with v_term given a time-limit row (done == RPL_DONE_TIMEOUT)
+// bootstraps from its terminal value instead (acc = r + gamma v_term, R34).  *dn = OR of the
+// done flags.  Rows are loaded in blocks of 8, all in flight before the recurrence uses them.
+__device__ __forceinline__ double nstep_rows(const GDesc& D, int64_t row, int64_t b, int ns, double acc,
+                                             uint8_t* dn) {
+  constexpr int NB = 8;
+  uint8_t d_or = 0;
+  for (int hi = ns; hi > 0; hi -= NB) {
+    const int lo = hi > NB ? hi - NB : 0;
+    float rb[NB];
+    uint8_t db[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      int64_t rr = row + lo + j;
+      while (rr >= D.cap_T) rr -= D.cap_T;
+      const bool in = lo + j < hi;
+      rb[j] = in ? __ldg(D.rew + rr * D.B + b) : 0.0f;
+      db[j] = in ? __ldg(D.done + rr * D.B + b) : (uint8_t)0;
+    }
+#pragma unroll
+    for (int j = NB - 1; j >= 0; --j) {
+      if (lo + j < hi) {
+        const double ri = (double)rb[j];
+        if (db[j]) {
+          acc = ri;
+          if (db[j] == RPL_DONE_TIMEOUT && D.v_term) {
+            int64_t rr = row + lo + j;
+            while (rr >= D.cap_T) rr -= D.cap_T;
+            acc = fma(D.gamma, (double)__ldg(D.v_term + rr * D.B + b), ri);
+          }
+        } else {
+          acc = fma(D.gamma, acc, ri);
+        }
+        d_or |= db[j];
+      }
+    }
+  }
+  *dn = d_or;
+  return acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -285,25 +334,10 @@ k_gather_transition(GDesc D, const int64_t* __restrict__ idx, int64_t n, const i
       uint8_t* dst = D.o_act + sc * D.act_bytes;
       for (int64_t i = l; i < D.act_bytes; i += 32) dst[i] = src[i];
     }
-    // n-step rows: lane i < n loads row r+i (all loads in flight at once), lane 0 runs the
-    // Horner recurrence over the shuffled values (R24)
-    float ri_l = 0.0f;
-    uint8_t di_l = 0;
-    if ((D.o_ret || D.o_done_n) && l < ns) {
-      const int64_t row = wrap(r + l, D.cap_T);
-      di_l = __ldg(D.done + row * D.B + b);
-      ri_l = __ldg(D.rew + row * D.B + b);
-    }
-    double acc = 0.0;
-    uint8_t dn = 0;
-    for (int i = ns - 1; i >= 0; --i) {  // ns <= 31 (host check)
-      const float ri = __shfl_sync(0xffffffffu, ri_l, i);
-      const uint8_t di = (uint8_t)__shfl_sync(0xffffffffu, (int)di_l, i);
-      acc = di ? (double)ri : fma(D.gamma, acc, (double)ri);
-      dn |= di;
-    }
     if (l == 0) {
-      if (D.o_ret || D.o_done_n) {
+      if (D.o_ret || D.o_done_n) {  // fused n-step return (R24, R34)
+        uint8_t dn = 0;
+        const double acc = nstep_rows(D, r, b, ns, 0.0, &dn);
         if (D.o_ret) D.o_ret[sc] = (float)acc;
         if (D.o_done_n) D.o_done_n[sc] = dn ? 1 : 0;
       }
@@ -1112,6 +1146,27 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
           D.o_w[coff + sm] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
         }
       }
+      // fused n-step targets (a2 + a4, R5 / R24 / R34) for the target rows in this CTA:
+      // rows tau .. tau+n_step-1 straight from the ring, bootstrap q_tgt[tau + n_step]
+      if (D.o_tgt) {
+        const int ns = D.n_step;
+        for (int c = lane; c < nrows; c += 32) {
+          if (row_new[c] < 0) continue;
+          const int t = row_tau[c] - D.tgt_lo;
+          if (t < 0 || t >= D.tgt_T) continue;
+          const int64_t col = coff + s_first + row_piece[c];
+          double acc = 0.0;
+          if (D.q_tgt) {
+            const double qv = (double)__ldg(D.q_tgt + (int64_t)(row_tau[c] + ns) * n + col);
+            acc = D.rescale ? h_inv(qv, D.rescale_eps) : qv;
+          }
+          uint8_t dn = 0;
+          acc = nstep_rows(D, row_ring[c], p_b[row_piece[c]], ns, acc, &dn);
+          if (D.rescale) acc = h_fwd(acc, D.rescale_eps);
+          D.o_tgt[(int64_t)t * n + col] = (float)acc;
+          if (D.o_tgt_done) D.o_tgt_done[(int64_t)t * n + col] = dn ? 1 : 0;
+        }
+      }
       if (peer) {  // global batch min over every rank's published value, then the IS weights
         int64_t v = INT64_MAX;
         if (lane < D.peer_world &&
@@ -1629,21 +1684,9 @@ k_gather_trans_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int SPF
       const int64_t sc = coff + s0 + j;
       const int64_t r = s_r[j];
       if (D.o_act) coop_copy(D.o_act + sc * D.act_bytes, D.act + (r * Bc + bcol) * D.act_bytes, D.act_bytes, 0, 1);
-      if (D.o_ret || D.o_done_n) {
-        float rb[32];
-        uint8_t db[32];
-        int64_t row = r;
-        for (int i = 0; i < ns; ++i) {  // all n rows in flight before the recurrence
-          rb[i] = __ldg(D.rew + row * Bc + bcol);
-          db[i] = __ldg(D.done + row * Bc + bcol);
-          if (++row == cap) row = 0;
-        }
-        double acc = 0.0;
+      if (D.o_ret || D.o_done_n) {  // fused n-step return (R24, R34)
         uint8_t dn = 0;
-        for (int i = ns - 1; i >= 0; --i) {  // Horner (R24)
-          acc = db[i] ? (double)rb[i] : fma(D.gamma, acc, (double)rb[i]);
-          dn |= db[i];
-        }
+        const double acc = nstep_rows(D, r, bcol, ns, 0.0, &dn);
         if (D.o_ret) D.o_ret[sc] = (float)acc;
         if (D.o_done_n) D.o_done_n[sc] = dn ? 1 : 0;
       }
@@ -1743,6 +1786,14 @@ GDesc to_dev(const rpl_gather_desc* d) {
   g.peer_boards = d->peer_boards;
   g.peer_world = d->peer_world;
   g.peer_rank = d->peer_rank;
+  g.q_tgt = d->q_tgt;
+  g.o_tgt = d->o_tgt;
+  g.o_tgt_done = d->o_tgt_done;
+  g.tgt_lo = d->tgt_lo;
+  g.tgt_T = d->tgt_T;
+  g.rescale = d->rescale;
+  g.rescale_eps = d->rescale_eps;
+  g.v_term = d->v_term;
   return g;
 }
 
@@ -1812,9 +1863,15 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
                             desc->peer_world > BOARD_MAX_WORLD || desc->peer_rank < 0 ||
                             desc->peer_rank >= desc->peer_world))
     return RPL_EINVAL;
+  if (desc->o_tgt && (desc->kind != RPL_GATHER_SEQUENCE || !desc->rew || desc->n_step < 1 || desc->n_step > 64 ||
+                      desc->tgt_lo < 0 || desc->tgt_T < 1 ||
+                      (int64_t)desc->tgt_lo + desc->tgt_T + desc->n_step > desc->seq_len ||
+                      !(desc->rescale_eps >= 0.0) || (desc->rescale != 0 && desc->rescale != 1)))
+    return RPL_EINVAL;
   GDesc g = to_dev(desc);
-  // col_offset / o_start / peer boards: default kernels only
-  const int seq_variant = (desc->col_offset || desc->o_start || desc->peer_boards) ? 0 : g_seq_variant;
+  // col_offset / o_start / peer boards / fused targets: default kernels only
+  const int seq_variant =
+      (desc->col_offset || desc->o_start || desc->peer_boards || desc->o_tgt) ? 0 : g_seq_variant;
   const bool tma_ok = (desc->obs_bytes % 16 == 0) && aligned16(desc->obs) && aligned16(desc->o_obs) &&
                       aligned16(desc->o_next_obs) && desc->obs_bytes <= 32768;
   cudaStream_t st = as_stream(stream);
@@ -1935,7 +1992,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
         return launch_status();
       }
     }
-    if (desc->o_start || desc->peer_boards) return RPL_EUNSUPPORTED;  // persistent default kernel only
+    if (desc->o_start || desc->peer_boards || desc->o_tgt) return RPL_EUNSUPPORTED;  // persistent default only
     const int64_t smem = (int64_t)(SEQ_CHUNK + desc->k) * desc->obs_bytes;
     g.use_tma = (tma_ok && smem <= 200 * 1024) ? 1 : 0;
     const size_t dyn = g.use_tma ? (size_t)smem : 0;

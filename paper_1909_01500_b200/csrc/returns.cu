@@ -39,7 +39,7 @@ template <int WARPS, int S, bool GAE>
 __global__ void __launch_bounds__(WARPS * 32)
 k_scan(const float* __restrict__ r, const float* __restrict__ v, const uint8_t* __restrict__ d,
        const float* __restrict__ boot, int64_t T, int64_t B, double gamma, double lam,
-       float* __restrict__ out0, float* __restrict__ out1) {
+       float* __restrict__ out0, float* __restrict__ out1, const float* __restrict__ vterm) {
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const int64_t col = (int64_t)blockIdx.x * 32 + lane;
@@ -62,7 +62,7 @@ k_scan(const float* __restrict__ r, const float* __restrict__ v, const uint8_t* 
     double b[S];
     float vv[S];
     float rr[S];
-    uint32_t dmask = 0;
+    uint32_t dmask = 0, tmask = 0;
 #pragma unroll
     for (int i = 0; i < S; ++i) {
       const int64_t t = t0 + i;
@@ -70,6 +70,7 @@ k_scan(const float* __restrict__ r, const float* __restrict__ v, const uint8_t* 
       rr[i] = ok ? __ldg(r + t * B + col) : 0.f;
       const uint8_t di = ok ? __ldg(d + t * B + col) : (uint8_t)0;
       dmask |= (di ? 1u : 0u) << i;
+      tmask |= (di == RPL_DONE_TIMEOUT ? 1u : 0u) << i;
       if (GAE) vv[i] = ok ? __ldg(v + t * B + col) : 0.f;
     }
     double vseg_next = 0.0;
@@ -82,13 +83,17 @@ k_scan(const float* __restrict__ r, const float* __restrict__ v, const uint8_t* 
 #pragma unroll
     for (int i = 0; i < S; ++i) {
       const double nd = ((dmask >> i) & 1u) ? 0.0 : 1.0;
+      // time-limit row (R34): gamma * v_term where gamma * (next value) would stand (rare: the
+      // load is issued only for such rows)
+      const double tl = (vterm && ((tmask >> i) & 1u) && i < nvalid)
+                            ? gamma * (double)__ldg(vterm + (t0 + i) * B + col) : 0.0;
       if (GAE) {
         double vnext;
         if (i + 1 < S) vnext = (i + 1 < nvalid) ? (double)vv[i + 1] : bootv;
         else vnext = vseg_next;
-        b[i] = i < nvalid ? ((double)rr[i] + gamma * nd * vnext) - (double)vv[i] : 0.0;
+        b[i] = i < nvalid ? (((double)rr[i] + gamma * nd * vnext) + tl) - (double)vv[i] : 0.0;
       } else {
-        b[i] = i < nvalid ? (double)rr[i] : 0.0;
+        b[i] = i < nvalid ? (double)rr[i] + tl : 0.0;
       }
     }
 #define RPL_A(i) ((i) < nvalid ? (((dmask >> (i)) & 1u) ? 0.0 : ga) : 1.0)
@@ -137,7 +142,7 @@ __global__ void __launch_bounds__(WARPS * 32)
 k_scan_tma(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUtensorMap tm_v,
            const __grid_constant__ CUtensorMap tm_d, const float* __restrict__ v, const float* __restrict__ boot,
            int64_t T, int64_t B, double gamma, double lam, float* __restrict__ out0, float* __restrict__ out1,
-           int early_trigger) {
+           int early_trigger, const float* __restrict__ vterm) {
   constexpr int CH = WARPS * S;
   __shared__ __align__(128) float s_r[CH][32];
   __shared__ __align__(128) float s_v[GAE ? CH : 1][32];
@@ -196,11 +201,12 @@ k_scan_tma(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUt
     double b[S];
     float vv[S];
     float rr[S];
-    uint32_t dmask = 0;
+    uint32_t dmask = 0, tmask = 0;
 #pragma unroll
     for (int i = 0; i < S; ++i) {
       rr[i] = s_r[w * S + i][lane];
       dmask |= (s_d[w * S + i][lane] ? 1u : 0u) << i;
+      tmask |= (s_d[w * S + i][lane] == RPL_DONE_TIMEOUT ? 1u : 0u) << i;
       if (GAE) vv[i] = s_v[w * S + i][lane];
     }
     double vseg_next = 0.0;
@@ -215,13 +221,17 @@ k_scan_tma(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUt
 #pragma unroll
     for (int i = 0; i < S; ++i) {
       const double nd = ((dmask >> i) & 1u) ? 0.0 : 1.0;
+      // time-limit row (R34): gamma * v_term where gamma * (next value) would stand (rare: the
+      // load is issued only for such rows)
+      const double tl = (vterm && ((tmask >> i) & 1u) && i < nvalid)
+                            ? gamma * (double)__ldg(vterm + (t0 + i) * B + col) : 0.0;
       if (GAE) {
         double vnext;
         if (i + 1 < S) vnext = (i + 1 < nvalid) ? (double)vv[i + 1] : bootv;
         else vnext = vseg_next;
-        b[i] = i < nvalid ? ((double)rr[i] + gamma * nd * vnext) - (double)vv[i] : 0.0;
+        b[i] = i < nvalid ? (((double)rr[i] + gamma * nd * vnext) + tl) - (double)vv[i] : 0.0;
       } else {
-        b[i] = i < nvalid ? (double)rr[i] : 0.0;
+        b[i] = i < nvalid ? (double)rr[i] + tl : 0.0;
       }
     }
 #define RPL_A(i) ((i) < nvalid ? (((dmask >> (i)) & 1u) ? 0.0 : ga) : 1.0)
@@ -269,7 +279,8 @@ template <int WARPS, int S, int CL, bool GAE>
 __global__ void __launch_bounds__(WARPS * 32)
 k_scan_cluster(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUtensorMap tm_v,
                const __grid_constant__ CUtensorMap tm_d, const float* __restrict__ v, const float* __restrict__ boot,
-               int64_t T, int64_t B, double gamma, double lam, float* __restrict__ out0, float* __restrict__ out1) {
+               int64_t T, int64_t B, double gamma, double lam, float* __restrict__ out0, float* __restrict__ out1,
+               const float* __restrict__ vterm) {
   constexpr int CH = WARPS * S;  // rows per CTA
   __shared__ __align__(128) float s_r[CH][32];
   __shared__ __align__(128) float s_v[GAE ? CH : 1][32];
@@ -329,11 +340,12 @@ k_scan_cluster(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__
   double b[S];
   float vv[S];
   float rr[S];
-  uint32_t dmask = 0;
+  uint32_t dmask = 0, tmask = 0;
 #pragma unroll
   for (int i = 0; i < S; ++i) {
     rr[i] = has_rows ? s_r[w * S + i][lane] : 0.f;
     dmask |= ((has_rows && s_d[w * S + i][lane]) ? 1u : 0u) << i;
+    tmask |= ((has_rows && s_d[w * S + i][lane] == RPL_DONE_TIMEOUT) ? 1u : 0u) << i;
     if (GAE) vv[i] = has_rows ? s_v[w * S + i][lane] : 0.f;
   }
   double vseg_next = 0.0;
@@ -346,13 +358,15 @@ k_scan_cluster(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__
 #pragma unroll
   for (int i = 0; i < S; ++i) {
     const double nd = ((dmask >> i) & 1u) ? 0.0 : 1.0;
+    const double tl = (vterm && ((tmask >> i) & 1u) && i < nvalid)
+                          ? gamma * (double)__ldg(vterm + (t0 + i) * B + col) : 0.0;  // R34
     if (GAE) {
       double vn;
       if (i + 1 < S) vn = (i + 1 < nvalid) ? (double)vv[i + 1] : bootv;
       else vn = vseg_next;
-      b[i] = i < nvalid ? ((double)rr[i] + gamma * nd * vn) - (double)vv[i] : 0.0;
+      b[i] = i < nvalid ? (((double)rr[i] + gamma * nd * vn) + tl) - (double)vv[i] : 0.0;
     } else {
-      b[i] = i < nvalid ? (double)rr[i] : 0.0;
+      b[i] = i < nvalid ? (double)rr[i] + tl : 0.0;
     }
   }
 #define RPL_A(i) ((i) < nvalid ? (((dmask >> (i)) & 1u) ? 0.0 : ga) : 1.0)
@@ -405,25 +419,10 @@ k_scan_cluster(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // keep sMap alive for the readers
 }
 
-__device__ __forceinline__ double h_fwd(double x, double eps) {
-  // h(x) = x (1/(sqrt(|x|+1)+1) + eps)  ==  sign(x)(sqrt(|x|+1)-1) + eps x   (§8c #4)
-  return x * (1.0 / (sqrt(fabs(x) + 1.0) + 1.0) + eps);
-}
-
-__device__ __forceinline__ double h_inv(double y, double eps) {
-  // s = sqrt(x+1) solves eps s^2 + s - (1 + eps + |y|) = 0 (rationalised root);
-  // x = (s-1)(s+1) with s-1 = |y| / (1 + eps (s+1))            (§8c #4)
-  const double a = fabs(y);
-  const double c = a + 1.0 + eps;
-  const double s = 2.0 * c / (1.0 + sqrt(1.0 + 4.0 * eps * c));
-  const double x = a * (s + 1.0) / (1.0 + eps * (s + 1.0));
-  return copysign(x, y);
-}
-
 __global__ void k_nstep(const float* __restrict__ r, const uint8_t* __restrict__ d, int64_t T,
                         int64_t B, int n, double gamma, const float* __restrict__ q,
                         const float* __restrict__ q_boot, int rescale, double eps,
-                        float* __restrict__ out, uint8_t* __restrict__ done_out) {
+                        float* __restrict__ out, uint8_t* __restrict__ done_out, const float* __restrict__ vterm) {
   const int64_t rows = T - n + 1;
   const int64_t total = rows * B;
   if (RPL_PDL_EARLY & 8) pdl_trigger();  // A/B knob (common.cuh)
@@ -462,7 +461,12 @@ __global__ void k_nstep(const float* __restrict__ r, const uint8_t* __restrict__
       for (int j = NB - 1; j >= 0; --j) {
         if (lo + j < hi) {
           const double ri = (double)rb[j];
-          acc = db[j] ? ri : fma(gamma, acc, ri);
+          if (db[j]) {  // cut; a time-limit row bootstraps from its terminal value (R34)
+            acc = (vterm && db[j] == RPL_DONE_TIMEOUT) ? fma(gamma, (double)__ldg(vterm + (t + lo + j) * B + b), ri)
+                                                       : ri;
+          } else {
+            acc = fma(gamma, acc, ri);
+          }
           dn |= db[j];
         }
       }
@@ -582,7 +586,8 @@ bool tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esize
 
 template <int WARPS, int S, int CL, bool GAE>
 int launch_scan_cluster(const float* r, const float* v, const uint8_t* d, const float* boot, int64_t T, int64_t B,
-                        double gamma, double lam, float* o0, float* o1, cudaStream_t st, bool* used) {
+                        double gamma, double lam, float* o0, float* o1, cudaStream_t st, bool* used,
+                        const float* vterm) {
   *used = false;
   constexpr int CH = WARPS * S;
   if (T > (int64_t)CL * CH) return RPL_OK;
@@ -595,12 +600,12 @@ int launch_scan_cluster(const float* r, const float* v, const uint8_t* d, const 
   *used = true;
   const dim3 grid((unsigned)(((B + 31) / 32) * CL));
   return launch_pdl_cluster(k_scan_cluster<WARPS, S, CL, GAE>, grid, dim3(WARPS * 32), 0, st, (unsigned)CL, mr, mv,
-                            md, v, boot, T, B, gamma, lam, o0, o1);
+                            md, v, boot, T, B, gamma, lam, o0, o1, vterm);
 }
 
 template <bool GAE>
 int launch_scan(const float* r, const float* v, const uint8_t* d, const float* boot, int64_t T, int64_t B,
-                double gamma, double lam, float* o0, float* o1, cudaStream_t st) {
+                double gamma, double lam, float* o0, float* o1, cudaStream_t st, const float* vterm) {
   dim3 grid((unsigned)((B + 31) / 32));
   const int var = scan_variant();
   if ((var == 4 || var == 5) && T < (1ll << 31) && B < (1ll << 31)) {
@@ -609,8 +614,9 @@ int launch_scan(const float* r, const float* v, const uint8_t* d, const float* b
     // 4.96 us): the call is latency-bound, and cluster scheduling plus two cluster
     // barriers cost more than the per-CTA bytes they save.  Kept selectable.
     bool used = false;
-    const int rc = var == 4 ? launch_scan_cluster<16, 4, 2, GAE>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, &used)
-                            : launch_scan_cluster<8, 4, 4, GAE>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, &used);
+    const int rc = var == 4
+                       ? launch_scan_cluster<16, 4, 2, GAE>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, &used, vterm)
+                       : launch_scan_cluster<8, 4, 4, GAE>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, &used, vterm);
     if (used) return rc;
   }
   if ((var == 0 || var == 6) && T < (1ll << 31) && B < (1ll << 31)) {
@@ -621,40 +627,50 @@ int launch_scan(const float* r, const float* v, const uint8_t* d, const float* b
         (!GAE || tmap_2d(&mv, v, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH))) {
       if (!GAE) mv = mr;
       return launch_pdl(k_scan_tma<SCAN_WARPS, SCAN_S, GAE>, grid, dim3(SCAN_WARPS * 32), 0, st, mr, mv, md, v,
-                        boot, T, B, gamma, lam, o0, o1, scan_trigger());
+                        boot, T, B, gamma, lam, o0, o1, scan_trigger(), vterm);
     }
   }
   switch (scan_variant()) {
     case 1:
-      return launch_pdl(k_scan<32, 4, GAE>, grid, dim3(32 * 32), 0, st, r, v, d, boot, T, B, gamma, lam, o0, o1);
+      return launch_pdl(k_scan<32, 4, GAE>, grid, dim3(32 * 32), 0, st, r, v, d, boot, T, B, gamma, lam, o0, o1,
+                        vterm);
     case 2:
-      return launch_pdl(k_scan<8, 16, GAE>, grid, dim3(8 * 32), 0, st, r, v, d, boot, T, B, gamma, lam, o0, o1);
+      return launch_pdl(k_scan<8, 16, GAE>, grid, dim3(8 * 32), 0, st, r, v, d, boot, T, B, gamma, lam, o0, o1,
+                        vterm);
     default:
       return launch_pdl(k_scan<SCAN_WARPS, SCAN_S, GAE>, grid, dim3(SCAN_WARPS * 32), 0, st, r, v, d, boot, T, B,
-                        gamma, lam, o0, o1);
+                        gamma, lam, o0, o1, vterm);
   }
+}
+
+extern "C" int rpl_returns_discounted_tl(const float* r, const uint8_t* d, const float* v_term,
+                                         const float* bootstrap, int64_t T, int64_t B, double gamma, float* ret,
+                                         void* stream) {
+  if (!r || !d || !ret || T < 1 || B < 1) return RPL_EINVAL;
+  return launch_scan<false>(r, nullptr, d, bootstrap, T, B, gamma, 0.0, ret, nullptr, as_stream(stream), v_term);
 }
 
 extern "C" int rpl_returns_discounted(const float* r, const uint8_t* d, const float* bootstrap,
                                       int64_t T, int64_t B, double gamma, float* ret, void* stream) {
-  if (!r || !d || !ret || T < 1 || B < 1) return RPL_EINVAL;
-  dim3 grid((unsigned)((B + 31) / 32));
-  (void)grid;
-  return launch_scan<false>(r, nullptr, d, bootstrap, T, B, gamma, 0.0, ret, nullptr, as_stream(stream));
+  return rpl_returns_discounted_tl(r, d, nullptr, bootstrap, T, B, gamma, ret, stream);
+}
+
+extern "C" int rpl_gae_tl(const float* r, const float* v, const uint8_t* d, const float* v_term,
+                          const float* bootstrap_v, int64_t T, int64_t B, double gamma, double lambda, float* adv,
+                          float* ret, void* stream) {
+  if (!r || !v || !d || !bootstrap_v || !adv || T < 1 || B < 1) return RPL_EINVAL;
+  return launch_scan<true>(r, v, d, bootstrap_v, T, B, gamma, lambda, adv, ret, as_stream(stream), v_term);
 }
 
 extern "C" int rpl_gae(const float* r, const float* v, const uint8_t* d, const float* bootstrap_v,
                        int64_t T, int64_t B, double gamma, double lambda, float* adv, float* ret,
                        void* stream) {
-  if (!r || !v || !d || !bootstrap_v || !adv || T < 1 || B < 1) return RPL_EINVAL;
-  dim3 grid((unsigned)((B + 31) / 32));
-  (void)grid;
-  return launch_scan<true>(r, v, d, bootstrap_v, T, B, gamma, lambda, adv, ret, as_stream(stream));
+  return rpl_gae_tl(r, v, d, nullptr, bootstrap_v, T, B, gamma, lambda, adv, ret, stream);
 }
 
-extern "C" int rpl_returns_nstep(const float* r, const uint8_t* d, int64_t T, int64_t B, int32_t n,
-                                 double gamma, const float* q, const float* q_boot, int32_t rescale,
-                                 double rescale_eps, float* ret_n, uint8_t* done_n, void* stream) {
+extern "C" int rpl_returns_nstep_tl(const float* r, const uint8_t* d, const float* v_term, int64_t T, int64_t B,
+                                    int32_t n, double gamma, const float* q, const float* q_boot, int32_t rescale,
+                                    double rescale_eps, float* ret_n, uint8_t* done_n, void* stream) {
   if (!r || !d || !ret_n || T < 1 || B < 1) return RPL_EINVAL;
   if (n < 1 || n > T) return RPL_ERANGE;
   if (q != nullptr && q_boot == nullptr) return RPL_EINVAL;
@@ -665,7 +681,13 @@ extern "C" int rpl_returns_nstep(const float* r, const uint8_t* d, int64_t T, in
 #endif
   const int threads = RPL_NSTEP_THREADS;
   return launch_pdl(k_nstep, dim3(elementwise_grid(work, threads)), dim3(threads), 0, as_stream(stream), r, d, T, B,
-                    (int)n, gamma, q, q_boot, rescale ? 1 : 0, rescale_eps, ret_n, done_n);
+                    (int)n, gamma, q, q_boot, rescale ? 1 : 0, rescale_eps, ret_n, done_n, v_term);
+}
+
+extern "C" int rpl_returns_nstep(const float* r, const uint8_t* d, int64_t T, int64_t B, int32_t n,
+                                 double gamma, const float* q, const float* q_boot, int32_t rescale,
+                                 double rescale_eps, float* ret_n, uint8_t* done_n, void* stream) {
+  return rpl_returns_nstep_tl(r, d, nullptr, T, B, n, gamma, q, q_boot, rescale, rescale_eps, ret_n, done_n, stream);
 }
 
 extern "C" int rpl_value_rescale(const float* x, float* y, int64_t n, double eps, int32_t inverse,

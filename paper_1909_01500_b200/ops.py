@@ -58,22 +58,30 @@ def check_err(dev_err: torch.Tensor, allowed: int = 0):
 
 
 # ---------------------------------------------------------------- returns
-def returns_discounted(r, d, bootstrap, gamma, out=None):
+def returns_discounted(r, d, bootstrap, gamma, out=None, v_term=None):
+    """rpl_returns_discounted (rpl_returns_discounted_tl with v_term [T, B]: time-limit rows,
+    d == 2, bootstrap from their terminal value, R34)."""
     T, B = r.shape
     _req(r, torch.float32, "r")
     _req(d, torch.uint8, "d", (T, B))
     if bootstrap is not None:
         _req(bootstrap, torch.float32, "bootstrap", (B,))
+    if v_term is not None:
+        _req(v_term, torch.float32, "v_term", (T, B))
     out = torch.empty_like(r) if out is None else _req(out, torch.float32, "out", (T, B))
-    check(lib.rpl_returns_discounted(_ptr(r), _ptr(d), _ptr(bootstrap), T, B, float(gamma), _ptr(out),
-                                     _stream(r.device)), "rpl_returns_discounted")
+    check(lib.rpl_returns_discounted_tl(_ptr(r), _ptr(d), _ptr(v_term), _ptr(bootstrap), T, B, float(gamma),
+                                        _ptr(out), _stream(r.device)), "rpl_returns_discounted_tl")
     return out
 
 
-def returns_nstep(r, d, n, gamma, q=None, q_boot=None, rescale=False, eps=1e-3, out=None, done_out=None):
+def returns_nstep(r, d, n, gamma, q=None, q_boot=None, rescale=False, eps=1e-3, out=None, done_out=None,
+                  v_term=None):
+    """rpl_returns_nstep (rpl_returns_nstep_tl with v_term [T, B], R34)."""
     T, B = r.shape
     _req(r, torch.float32, "r")
     _req(d, torch.uint8, "d", (T, B))
+    if v_term is not None:
+        _req(v_term, torch.float32, "v_term", (T, B))
     if q is not None:
         _req(q, torch.float32, "q", (T, B))
         _req(q_boot, torch.float32, "q_boot", (B,))
@@ -82,9 +90,9 @@ def returns_nstep(r, d, n, gamma, q=None, q_boot=None, rescale=False, eps=1e-3, 
         out = torch.empty((max(rows, 0), B), dtype=torch.float32, device=r.device)
     if done_out is None:
         done_out = torch.empty((max(rows, 0), B), dtype=torch.uint8, device=r.device)
-    check(lib.rpl_returns_nstep(_ptr(r), _ptr(d), T, B, int(n), float(gamma), _ptr(q), _ptr(q_boot),
-                                1 if rescale else 0, float(eps), _ptr(out), _ptr(done_out), _stream(r.device)),
-          "rpl_returns_nstep")
+    check(lib.rpl_returns_nstep_tl(_ptr(r), _ptr(d), _ptr(v_term), T, B, int(n), float(gamma), _ptr(q),
+                                   _ptr(q_boot), 1 if rescale else 0, float(eps), _ptr(out), _ptr(done_out),
+                                   _stream(r.device)), "rpl_returns_nstep_tl")
     return out, done_out
 
 
@@ -125,16 +133,19 @@ def c51_project(p_target, q_online, R, done_n, v_min, v_max, gamma_n, out=None):
     return out, a_star
 
 
-def gae(r, v, d, bootstrap_v, gamma, lam, adv=None, ret=None):
+def gae(r, v, d, bootstrap_v, gamma, lam, adv=None, ret=None, v_term=None):
+    """rpl_gae (rpl_gae_tl with v_term [T, B], R34)."""
     T, B = r.shape
     _req(r, torch.float32, "r")
     _req(v, torch.float32, "v", (T, B))
     _req(d, torch.uint8, "d", (T, B))
     _req(bootstrap_v, torch.float32, "bootstrap_v", (B,))
+    if v_term is not None:
+        _req(v_term, torch.float32, "v_term", (T, B))
     adv = torch.empty_like(r) if adv is None else adv
     ret = torch.empty_like(r) if ret is None else ret
-    check(lib.rpl_gae(_ptr(r), _ptr(v), _ptr(d), _ptr(bootstrap_v), T, B, float(gamma), float(lam), _ptr(adv),
-                      _ptr(ret), _stream(r.device)), "rpl_gae")
+    check(lib.rpl_gae_tl(_ptr(r), _ptr(v), _ptr(d), _ptr(v_term), _ptr(bootstrap_v), T, B, float(gamma), float(lam),
+                         _ptr(adv), _ptr(ret), _stream(r.device)), "rpl_gae_tl")
     return adv, ret
 
 
@@ -424,6 +435,7 @@ class GatherRing:
     cursor: int
     size: int
     rnn: torch.Tensor | None = None  # [cap_T/period, B, parts, H] f32
+    v_term: torch.Tensor | None = None  # [cap_T, B] f32 terminal values of time-limit rows (R34)
 
     @property
     def cap_T(self):
@@ -462,6 +474,9 @@ def _desc(ring: GatherRing, kind, k, pad_mode, out_mode, n_step, seq_len, period
     g.n_step, g.seq_len, g.period = n_step, seq_len, period
     g.gamma = float(gamma)
     g.obs, g.act, g.rew, g.done = ring.obs.data_ptr(), ring.act.data_ptr(), ring.rew.data_ptr(), ring.done.data_ptr()
+    if ring.v_term is not None:
+        _req(ring.v_term, torch.float32, "ring.v_term", (ring.cap_T, ring.B))
+        g.v_term = ring.v_term.data_ptr()
     if ring.rnn is not None:
         g.rnn = ring.rnn.data_ptr()
         g.rnn_parts = int(ring.rnn.shape[2])
@@ -469,10 +484,28 @@ def _desc(ring: GatherRing, kind, k, pad_mode, out_mode, n_step, seq_len, period
     return g
 
 
+def _set_targets(g, targets, seq_len, n, o, alloc):
+    """Fused sequence n-step targets (rpl_gather_desc.q_tgt / o_tgt, R5 / R24 / R34):
+    targets = dict(lo, T, n_step, gamma, rescale=False, eps=1e-3, q=None) with q f32 [L, n]."""
+    lo, T = int(targets["lo"]), int(targets["T"])
+    g.n_step = int(targets["n_step"])
+    g.gamma = float(targets["gamma"])
+    g.tgt_lo, g.tgt_T = lo, T
+    g.rescale = 1 if targets.get("rescale", False) else 0
+    g.rescale_eps = float(targets.get("eps", 1e-3))
+    qt = targets.get("q")
+    if qt is not None:
+        _req(qt, torch.float32, "targets['q']", (seq_len, n))
+        g.q_tgt = qt.data_ptr()
+    alloc("tgt", (T, n), torch.float32, force=True)
+    alloc("tgt_done", (T, n), torch.uint8, force=True)
+
+
 def gather(ring: GatherRing, idx, kind="transition", k=4, n_step=1, gamma=0.99, seq_len=1, period=1,
            pad_mode=_lib.PAD_REPEAT, out_mode=_lib.OUT_STACKED, q=None, qmin=None, beta=0.0, outputs=None,
-           err=None, want=None):
-    """rpl_gather.  Returns a dict of output tensors (allocated unless given in `outputs`)."""
+           err=None, want=None, targets=None):
+    """rpl_gather.  Returns a dict of output tensors (allocated unless given in `outputs`).
+    targets (SEQUENCE): fused n-step targets, see _set_targets (outputs "tgt", "tgt_done")."""
     _req(idx, torch.int64, "idx")
     n = idx.numel()
     dev = ring.obs.device
@@ -483,8 +516,8 @@ def gather(ring: GatherRing, idx, kind="transition", k=4, n_step=1, gamma=0.99, 
     od = ring.obs.dtype
     wants = set(want) if want is not None else None
 
-    def alloc(name, shape, dtype):
-        if name not in o and (wants is None or name in wants):
+    def alloc(name, shape, dtype, force=False):
+        if name not in o and (force or wants is None or name in wants):
             o[name] = torch.empty(shape, dtype=dtype, device=dev)
 
     if kind_i == _lib.GATHER_TRANSITION:
@@ -508,11 +541,13 @@ def gather(ring: GatherRing, idx, kind="transition", k=4, n_step=1, gamma=0.99, 
             alloc("rnn", (int(ring.rnn.shape[2]), n, int(ring.rnn.shape[3])), ring.rnn.dtype)
         if wants is not None and "start" in wants:  # episode-start offsets (Mode C shipping)
             alloc("start", (L, n), torch.int8)
+        if targets is not None:
+            _set_targets(g, targets, L, n, o, alloc)
     if q is not None:
         alloc("w", (n,), torch.float32)
     fields = {"obs": "o_obs", "next_obs": "o_next_obs", "act": "o_act", "prev_act": "o_prev_act", "rew": "o_rew",
               "prev_rew": "o_prev_rew", "done": "o_done", "ret": "o_ret", "done_n": "o_done_n", "w": "o_w",
-              "rnn": "o_rnn", "start": "o_start"}
+              "rnn": "o_rnn", "start": "o_start", "tgt": "o_tgt", "tgt_done": "o_tgt_done"}
     for name, f in fields.items():
         if name in o and o[name] is not None:
             setattr(g, f, o[name].data_ptr())
@@ -528,16 +563,19 @@ class GatherPlan:
     capturable in a CUDA graph)."""
 
     def __init__(self, ring: GatherRing, n, kind="transition", k=4, n_step=1, gamma=0.99, seq_len=1, period=1,
-                 pad_mode=_lib.PAD_REPEAT, out_mode=_lib.OUT_STACKED, want=None, with_weights=False, outputs=None):
+                 pad_mode=_lib.PAD_REPEAT, out_mode=_lib.OUT_STACKED, want=None, with_weights=False, outputs=None,
+                 targets=None):
         """outputs: optional dict of preallocated output tensors (e.g. a central learner's
-        buffers mapped over CUDA IPC, Mode C); missing ones are allocated here."""
+        buffers mapped over CUDA IPC, Mode C); missing ones are allocated here.
+        targets: fused sequence n-step targets (see _set_targets; the bootstrap q may be
+        swapped per call with run(q_tgt=...))."""
         dev = ring.obs.device
         self.n = int(n)
         dummy = torch.zeros(self.n, dtype=torch.int64, device=dev)
         # allocate via gather() on an all-skip index vector (no kernel work: idx < 0)
         self.outputs = gather(ring, torch.full_like(dummy, -1), kind=kind, k=k, n_step=n_step, gamma=gamma,
                               seq_len=seq_len, period=period, pad_mode=pad_mode, out_mode=out_mode, want=want,
-                              outputs=outputs)
+                              outputs=outputs, targets=targets)
         if with_weights and "w" not in self.outputs:
             self.outputs["w"] = torch.empty(self.n, dtype=torch.float32, device=dev)
         kind_i = _lib.GATHER_TRANSITION if kind == "transition" else _lib.GATHER_SEQUENCE
@@ -545,7 +583,9 @@ class GatherPlan:
         fields = {"obs": "o_obs", "next_obs": "o_next_obs", "act": "o_act", "prev_act": "o_prev_act",
                   "rew": "o_rew", "prev_rew": "o_prev_rew", "done": "o_done", "ret": "o_ret", "done_n": "o_done_n",
                   "w": "o_w", "rnn": "o_rnn",
-                  "start": "o_start"}
+                  "start": "o_start", "tgt": "o_tgt", "tgt_done": "o_tgt_done"}
+        if targets is not None:
+            _set_targets(self.desc, targets, seq_len, self.n, self.outputs, lambda *a, **kw: None)
         for name, f in fields.items():
             if name in self.outputs:
                 setattr(self.desc, f, self.outputs[name].data_ptr())
@@ -565,8 +605,12 @@ class GatherPlan:
         self.desc.peer_world = int(world) if board_ptrs is not None else 0
         self.desc.peer_rank = int(rank) if board_ptrs is not None else 0
 
-    def run(self, idx, q=None, qmin=None, beta=0.0, err=None, stream=None):
+    def run(self, idx, q=None, qmin=None, beta=0.0, err=None, stream=None, q_tgt=None):
+        """q_tgt: this call's bootstrap values for the fused targets (f32 [L, n]; None keeps
+        the one set before)."""
         s = _stream(self.device) if stream is None else stream
+        if q_tgt is not None:
+            self.desc.q_tgt = q_tgt.data_ptr()
         check(lib.rpl_gather(self._dp, _ptr(idx), _ptr(q), _ptr(qmin), float(beta), self.n, _ptr(err), s),
               "rpl_gather")
         return self.outputs

@@ -488,3 +488,87 @@ def test_transition_pipeline_scalars_only(rpl):
     assert np.array_equal(H(out["act"]), ref["act"])
     assert np.array_equal(H(out["done_n"]), ref["done_n"])
     check_rel(H(out["ret"]), ref["ret"], absR, what="scalars-only ret")
+
+
+def _with_timeouts(ring, g, frac=0.5):
+    """Turn a fraction of the ring's episode ends into time-limit ends (done = 2) and give
+    every row a terminal value (read only at those rows, R34)."""
+    done = ring.done.copy()
+    ends = np.argwhere(done == 1)
+    pick = ends[g.random(len(ends)) < frac]
+    done[pick[:, 0], pick[:, 1]] = 2
+    v_term = g.normal(0, 10, done.shape).astype(np.float32)
+    return done, v_term
+
+
+@pytest.mark.parametrize("rescale,with_q,timeouts,lo,Tt", [(True, True, False, 40, 80), (False, True, True, 40, 80),
+                                                            (True, True, True, 0, 120), (False, False, False, 3, 1),
+                                                            (True, False, True, 7, 113)])
+def test_sequence_fused_targets(rpl, rescale, with_q, timeouts, lo, Tt):
+    # a2 + a4 fused into the sequence gather (rpl_gather_desc.o_tgt): rescaled 5-step targets of
+    # the target rows vs the oracle's n-step over the oracle-gathered rows (and, without time
+    # limits, bit-identical to rpl_returns_nstep over the gathered rows)
+    import torch
+    period, L, k, n_s, ns, gamma = 40, 125, 4, 64, 5, 0.997
+    ring = make_ring(61, cap=400, B=4, ep_len=12.0, period=period, rnn_h=8, reward_kind="r2d2")
+    g = rng(62)
+    v_term = None
+    if timeouts:
+        ring.done, v_term = _with_timeouts(ring, g)
+    dr = dev_ring(rpl, ring)
+    if v_term is not None:
+        dr.v_term = T_(v_term)
+    idx = []
+    while len(idx) < n_s:
+        blk, b = int(g.integers(0, 10)), int(g.integers(0, 4))
+        if OG.window_valid_sequence(blk * period, 400, ring.cursor, ring.size, k, L):
+            idx.append(blk * 4 + b)
+    idx = np.array(idx, np.int64)
+    idx[9] = -1
+    qv = g.normal(0, 10, (L, n_s)).astype(np.float32)
+    tg = dict(lo=lo, T=Tt, n_step=ns, gamma=gamma, rescale=rescale, eps=1e-3, q=T_(qv) if with_q else None)
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = rpl.gather(dr, T_(idx), kind="sequence", k=k, seq_len=L, period=period, targets=tg, err=err)
+    torch.cuda.synchronize()
+    assert int(H(err)[0]) == 0
+    ref = OG.gather_sequences(idx, 4, ring.obs, ring.act, ring.rew, ring.done, ring.rnn, k, L, period)
+    Tn = Tt + ns - 1
+    vt_rows = None
+    if v_term is not None:  # per gathered row: v_term of its ring row
+        vt_rows = np.zeros((L, n_s), np.float32)
+        for s_, leaf in enumerate(idx):
+            if leaf >= 0:
+                blk, b = divmod(int(leaf), 4)
+                vt_rows[:, s_] = v_term[(blk * period + np.arange(L)) % 400, b]
+        vt_rows = vt_rows[lo:lo + Tn]
+    yr, dnr = OR.nstep_return(ref["rew"][lo:lo + Tn], ref["done"][lo:lo + Tn], ns, gamma,
+                              q=qv[lo:lo + Tn] if with_q else None, q_boot=qv[lo + Tn] if with_q else None,
+                              rescale=rescale, v_term=vt_rows)
+    ok = idx >= 0
+    assert out["tgt"].shape == (Tt, n_s)
+    check_rel(H(out["tgt"])[:, ok], yr[:, ok], (np.abs(yr) + 1e-3)[:, ok], what="fused targets")
+    assert np.array_equal(H(out["tgt_done"])[:, ok], dnr[:, ok])
+    if v_term is None:  # the same arithmetic as the standalone kernel, bit for bit
+        y2, dn2 = rpl.returns_nstep(out["rew"][lo:lo + Tn].contiguous(), out["done"][lo:lo + Tn].contiguous(), ns,
+                                    gamma, q=T_(qv[lo:lo + Tn]) if with_q else None,
+                                    q_boot=T_(qv[lo + Tn]) if with_q else None, rescale=rescale)
+        assert np.array_equal(H(y2)[:, ok], H(out["tgt"])[:, ok])
+
+
+def test_transition_time_limit_bootstrap(rpl):
+    # R34 in the transition gather: n-step returns stopping at a time-limit row add gamma^(j+1) v_term
+    import torch
+    ring = make_ring(63, cap=128, B=8, ep_len=5.0, reward_kind="heavy")
+    g = rng(64)
+    ring.done, v_term = _with_timeouts(ring, g)
+    dr = dev_ring(rpl, ring)
+    dr.v_term = T_(v_term)
+    for nn in (37, 700):  # one-CTA-per-sample kernel and the persistent pipeline
+        idx = valid_transition_leaves(ring, 4, 3, nn, g)
+        out = rpl.gather(dr, T_(idx), kind="transition", k=4, n_step=3, gamma=0.99)
+        ref = OG.gather_transitions(idx, 8, ring.obs, ring.act, ring.rew, ring.done, 4, 3, 0.99, v_term=v_term)
+        absR = OG.gather_transitions(idx, 8, ring.obs, ring.act, np.abs(ring.rew), ring.done, 4, 3, 0.99,
+                                     v_term=np.abs(v_term))["ret"]
+        check_rel(H(out["ret"]), ref["ret"], absR, what="time-limit ret")
+        assert np.array_equal(H(out["done_n"]), ref["done_n"])
+        assert np.array_equal(H(out["obs"]), ref["obs"]) and np.array_equal(H(out["next_obs"]), ref["next_obs"])

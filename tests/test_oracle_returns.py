@@ -191,3 +191,76 @@ def test_nstep_random_vs_direct_loops():
                     disc *= _frac(gamma)
                 assert abs(Rn[t, b] - float(tot)) <= 1e-13 * max(1, abs(float(tot)))
                 assert dn[t, b] == done
+
+
+# ---- time-limit bootstrap (reading R34; P:95 fn) ----
+def _truncated_pair(seed, T=40, B=6, k=17):
+    """A long episode (no dones, bootstrap b) and the same rows cut by a time limit after
+    row k, whose v_term is the untruncated return / value of row k+1; the rows after k are
+    replaced by an unrelated new episode."""
+    g = np.random.default_rng(seed)
+    r = g.normal(0, 1, (T, B))
+    v = g.normal(0, 3, (T, B))
+    boot = g.normal(0, 3, B)
+    d0 = np.zeros((T, B), np.uint8)
+    r2, v2 = r.copy(), v.copy()
+    r2[k + 1:] = g.normal(0, 5, (T - k - 1, B))
+    v2[k + 1:] = g.normal(0, 5, (T - k - 1, B))
+    d2 = np.zeros((T, B), np.uint8)
+    d2[k] = 2
+    return r, v, boot, d0, r2, v2, d2, k
+
+
+def test_timeout_with_exact_bootstrap_equals_untruncated():
+    gamma = 0.97
+    r, v, boot, d0, r2, v2, d2, k = _truncated_pair(1)
+    full = R.discounted_return(r, d0, boot, gamma)
+    vt = np.zeros_like(r)
+    vt[k] = full[k + 1]                                   # the value the cut removed
+    cut = R.discounted_return(r2, d2, np.zeros(r.shape[1]), gamma, v_term=vt)
+    np.testing.assert_allclose(cut[:k + 1], full[:k + 1], rtol=1e-12, atol=1e-12)
+    # n-step: a window containing row k equals the untruncated full return (its v_term is
+    # exactly what the cut removed); a window before the cut equals the plain n-step sum
+    n = 5
+    Rn_plain, _ = R.nstep_return(r, d0, n, gamma)
+    Rn_cut, dn = R.nstep_return(r2, d2, n, gamma, v_term=vt)
+    for t in range(k - n + 1, k + 1):
+        np.testing.assert_allclose(Rn_cut[t], full[t], rtol=1e-12, atol=1e-12)
+        assert dn[t].all()
+    np.testing.assert_allclose(Rn_cut[:k - n + 1], Rn_plain[:k - n + 1], rtol=1e-12, atol=1e-12)
+    assert not dn[:k - n + 1].any()
+    # identity check of the plain sum itself: R^n_t = R_t - gamma^n R_{t+n} without dones
+    np.testing.assert_allclose(Rn_plain[:k], full[:k] - gamma ** n * full[n:k + n], rtol=1e-9, atol=1e-9)
+
+
+def test_timeout_gae_lambda_limits():
+    gamma = 0.99
+    r, v, boot, d0, r2, v2, d2, k = _truncated_pair(2)
+    vt = np.zeros_like(r)
+    vt[k] = v[k + 1]                                      # V of the final observation
+    # lambda = 0: A_t = delta_t, identical to the untruncated delta for t <= k
+    a0, _ = R.gae(r, v, d0, boot, gamma, 0.0)
+    a0c, _ = R.gae(r2, v, d2, boot, gamma, 0.0, v_term=vt)
+    np.testing.assert_allclose(a0c[:k + 1], a0[:k + 1], rtol=1e-12, atol=1e-12)
+    # lambda = 1: ret = the discounted return with the same time-limit bootstrap (S:755)
+    _, ret1 = R.gae(r2, v2, d2, boot, gamma, 1.0, v_term=vt)
+    np.testing.assert_allclose(ret1, R.discounted_return(r2, d2, boot, gamma, v_term=vt), rtol=1e-10, atol=1e-10)
+
+
+def test_timeout_closed_form_and_plain_terminal_without_values():
+    gamma, c, rc, k = 0.9, 7.0, 1.5, 6
+    T = 12
+    r = np.full((T, 1), rc)
+    d = np.zeros((T, 1), np.uint8)
+    d[k] = 2
+    vt = np.zeros((T, 1))
+    vt[k] = c
+    Rt = R.discounted_return(r, d, np.array([100.0]), gamma, v_term=vt)
+    assert abs(Rt[0, 0] - (rc * (1 - gamma ** (k + 1)) / (1 - gamma) + gamma ** (k + 1) * c)) < 1e-12
+    # without v_term a time-limit row is a plain terminal: same as done = 1
+    d1 = np.where(d == 2, 1, 0).astype(np.uint8)
+    np.testing.assert_array_equal(R.discounted_return(r, d, None, gamma), R.discounted_return(r, d1, None, gamma))
+    y2, dn2 = R.nstep_return(r, d, 3, gamma)
+    y1, dn1 = R.nstep_return(r, d1, 3, gamma)
+    np.testing.assert_array_equal(y2, y1)
+    np.testing.assert_array_equal(dn2, dn1)
