@@ -266,6 +266,159 @@ k_scan_tma(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUt
 }
 
 // ---------------------------------------------------------------------------
+// Column-group TMA scan with double-buffered chunks: a CTA owns COLS (16 or 32) columns;
+// with COLS = 16 each warp's lanes split into two 16-column halves, so a 256-thread CTA
+// still covers 128 rows per chunk with S = 8 rows per thread, and a PPO call
+// ([128, 4096]) runs 256 CTAs — every SM works, two or three CTAs resident per SM so one
+// CTA's stores overlap another's loads.  Chunks are prefetched one ahead into the second
+// tile buffer (TMA), so for long horizons the next chunk's load overlaps this chunk's scan
+// and stores.  The V value just after a chunk (GAE) is kept from the chunk processed before
+// it (the scan runs from the end), not reloaded.  Same fp64 affine-map arithmetic.
+// ---------------------------------------------------------------------------
+template <int COLS, int WARPS, int S, bool GAE>
+__global__ void __launch_bounds__(WARPS * 32)
+k_scan_tma2(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUtensorMap tm_v,
+            const __grid_constant__ CUtensorMap tm_d, const float* __restrict__ boot, int64_t T, int64_t B,
+            double gamma, double lam, float* __restrict__ out0, float* __restrict__ out1, int early_trigger,
+            const float* __restrict__ vterm) {
+  constexpr int SUB = 32 / COLS;       // segments per warp
+  constexpr int SEGS = WARPS * SUB;
+  constexpr int CH = SEGS * S;         // rows per chunk
+  __shared__ __align__(128) float s_r[2][CH][COLS];
+  __shared__ __align__(128) float s_v[2][GAE ? CH : 1][COLS];
+  __shared__ __align__(128) uint8_t s_d[2][CH][COLS];
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ double sA[SEGS][COLS];
+  __shared__ double sB[SEGS][COLS];
+  __shared__ double sCarry[COLS];
+  __shared__ float sVnext[COLS];       // V of the first row of the chunk processed last (GAE)
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int ci = lane % COLS;
+  const int seg = w * SUB + lane / COLS;
+  const int64_t col = (int64_t)blockIdx.x * COLS + ci;
+  const bool cv = col < B;
+  const int64_t nchunks = (T + CH - 1) / CH;
+  constexpr uint32_t BYTES = (uint32_t)(CH * COLS * 4 * (GAE ? 2 : 1) + CH * COLS);
+  auto issue = [&](int64_t c, int stg) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&bar[stg])), "r"(BYTES)
+                 : "memory");
+    const int x = (int)(blockIdx.x * COLS), y = (int)(c * CH);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(s_u32(&s_r[stg][0][0])), "l"(&tm_r), "r"(x), "r"(y), "r"(s_u32(&bar[stg])) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(s_u32(&s_d[stg][0][0])), "l"(&tm_d), "r"(x), "r"(y), "r"(s_u32(&bar[stg])) : "memory");
+    if (GAE)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+          ::"r"(s_u32(&s_v[stg][0][0])), "l"(&tm_v), "r"(x), "r"(y), "r"(s_u32(&bar[stg])) : "memory");
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&bar[0])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&bar[1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_r) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_d) : "memory");
+    if (GAE) asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_v) : "memory");
+  }
+  __syncthreads();
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    issue(nchunks - 1, (int)((nchunks - 1) & 1));
+    if (nchunks > 1) issue(nchunks - 2, (int)((nchunks - 2) & 1));
+  }
+  if (early_trigger) pdl_trigger();  // the next grid's prologue may start (it still waits in pdl_wait)
+  const double bootv = (GAE && cv) ? (double)boot[col] : 0.0;
+  if (w == 0 && lane < COLS) {
+    sCarry[lane] = (!GAE && boot != nullptr && cv) ? (double)boot[col] : 0.0;
+    if (GAE) sVnext[lane] = (float)bootv;
+  }
+  const double ga = GAE ? gamma * lam : gamma;
+  uint32_t phases = 0;  // bit s: parity to wait for on stage s
+  for (int64_t c = nchunks - 1; c >= 0; --c) {
+    const int stg = (int)(c & 1);
+    {
+      uint32_t done = 0;
+      const uint32_t ph = (phases >> stg) & 1u;
+      while (!done)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(s_u32(&bar[stg])), "r"(ph) : "memory");
+      phases ^= 1u << stg;
+    }
+    const int64_t t0 = c * CH + (int64_t)seg * S;
+    double b[S];
+    float vv[S];
+    float rr[S];
+    uint32_t dmask = 0, tmask = 0;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      rr[i] = s_r[stg][seg * S + i][ci];
+      const uint8_t di = s_d[stg][seg * S + i][ci];
+      dmask |= (di ? 1u : 0u) << i;
+      tmask |= (di == RPL_DONE_TIMEOUT ? 1u : 0u) << i;
+      if (GAE) vv[i] = s_v[stg][seg * S + i][ci];
+    }
+    double vseg_next = 0.0;
+    if (GAE) {
+      if (t0 + S >= T) vseg_next = bootv;
+      else if (seg + 1 < SEGS) vseg_next = (double)s_v[stg][(seg + 1) * S][ci];
+      else vseg_next = (double)sVnext[ci];
+    }
+    __syncthreads();  // every thread holds its rows: this stage may be refilled
+    if (threadIdx.x == 0 && c >= 2) issue(c - 2, stg);
+    const int nvalid = cv ? (int)max((int64_t)0, min((int64_t)S, T - t0)) : 0;
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      const double nd = ((dmask >> i) & 1u) ? 0.0 : 1.0;
+      const double tl = (vterm && ((tmask >> i) & 1u) && i < nvalid)
+                            ? gamma * (double)__ldg(vterm + (t0 + i) * B + col) : 0.0;  // R34
+      if (GAE) {
+        double vnext;
+        if (i + 1 < S) vnext = (i + 1 < nvalid) ? (double)vv[i + 1] : bootv;
+        else vnext = vseg_next;
+        b[i] = i < nvalid ? (((double)rr[i] + gamma * nd * vnext) + tl) - (double)vv[i] : 0.0;
+      } else {
+        b[i] = i < nvalid ? (double)rr[i] + tl : 0.0;
+      }
+    }
+#define RPL_A(i) ((i) < nvalid ? (((dmask >> (i)) & 1u) ? 0.0 : ga) : 1.0)
+    double A = 1.0, Bc = 0.0;
+#pragma unroll
+    for (int i = S - 1; i >= 0; --i) {
+      const double ai = RPL_A(i);
+      Bc = fma(ai, Bc, b[i]);
+      A = ai * A;
+    }
+    sA[seg][ci] = A;
+    sB[seg][ci] = Bc;
+    __syncthreads();
+    double x = sCarry[ci];
+#pragma unroll
+    for (int ss = SEGS - 1; ss > 0; --ss) {
+      if (ss > seg) x = fma(sA[ss][ci], x, sB[ss][ci]);
+    }
+#pragma unroll
+    for (int i = S - 1; i >= 0; --i) {
+      x = fma(RPL_A(i), x, b[i]);
+      const int64_t t = t0 + i;
+      if (i < nvalid) {
+        out0[t * B + col] = (float)x;
+        if (GAE && out1 != nullptr) out1[t * B + col] = (float)(x + (double)vv[i]);
+      }
+    }
+#undef RPL_A
+    __syncthreads();
+    if (seg == 0) {
+      sCarry[ci] = x;
+      if (GAE) sVnext[ci] = vv[0];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Cluster variant for short horizons (T <= CL * WARPS * S, e.g. PPO's T = 128; selectable,
 // not the default — see launch_scan for the measurement): the rows
 // of a 32-column group are split over a thread-block cluster of CL CTAs along T, so each
@@ -526,7 +679,7 @@ int scan_variant() {
   if (v < 0) {
     const char* e = getenv("RPL_SCAN_VARIANT");
     int want = e ? atoi(e) : 0;
-    if (want < 0 || want > 6) want = 0;
+    if (want < 0 || want > 8) want = 0;
     int expect = -1;
     g_scan_variant.compare_exchange_strong(expect, want);
     v = g_scan_variant.load(std::memory_order_relaxed);
@@ -572,12 +725,12 @@ encode_fn_t encode_fn() {
 // [T, B] row-major tensor map with a [box_rows x 32 columns] box; false if the layout is
 // not TMA-addressable (base not 16-B aligned, row pitch not a multiple of 16 B).
 bool tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, int esize, int64_t T, int64_t B,
-             int box_rows) {
+             int box_rows, int box_cols = 32) {
   encode_fn_t fn = encode_fn();
   if (!fn || !base || (reinterpret_cast<uintptr_t>(base) & 15) || ((B * esize) & 15)) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)B, (cuuint64_t)T};
   const cuuint64_t strides[1] = {(cuuint64_t)(B * esize)};
-  const cuuint32_t box[2] = {32u, (cuuint32_t)box_rows};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1u, 1u};
   return fn(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
@@ -618,6 +771,21 @@ int launch_scan(const float* r, const float* v, const uint8_t* d, const float* b
                        ? launch_scan_cluster<16, 4, 2, GAE>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, &used, vterm)
                        : launch_scan_cluster<8, 4, 4, GAE>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, &used, vterm);
     if (used) return rc;
+  }
+  if ((var == 7 || var == 8) && T < (1ll << 31) && B < (1ll << 31)) {
+    CUtensorMap mr, mv, md;
+    const int CH = var == 7 ? 128 : 64;  // 7: 16 cols x (8 warps x 2 halves x 8 rows); 8: 32 cols x 16 warps x 4 rows
+    const int cols = var == 7 ? 16 : 32;
+    if (tmap_2d(&mr, r, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH, cols) &&
+        tmap_2d(&md, d, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, T, B, CH, cols) &&
+        (!GAE || tmap_2d(&mv, v, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH, cols))) {
+      if (!GAE) mv = mr;
+      if (var == 7)
+        return launch_pdl(k_scan_tma2<16, 8, 8, GAE>, dim3((unsigned)((B + 15) / 16)), dim3(8 * 32), 0, st, mr, mv,
+                          md, boot, T, B, gamma, lam, o0, o1, scan_trigger(), vterm);
+      return launch_pdl(k_scan_tma2<32, 16, 4, GAE>, dim3((unsigned)((B + 31) / 32)), dim3(16 * 32), 0, st, mr, mv,
+                        md, boot, T, B, gamma, lam, o0, o1, scan_trigger(), vterm);
+    }
   }
   if ((var == 0 || var == 6) && T < (1ll << 31) && B < (1ll << 31)) {
     CUtensorMap mr, mv, md;
@@ -700,7 +868,7 @@ extern "C" int rpl_value_rescale(const float* x, float* y, int64_t n, double eps
 }
 
 extern "C" int rpl_debug_set_scan_variant(int32_t variant) {
-  if (variant < 0 || variant > 6) return RPL_EINVAL;
+  if (variant < 0 || variant > 8) return RPL_EINVAL;
   g_scan_variant.store(variant);
   return RPL_OK;
 }

@@ -19,6 +19,10 @@ __global__ void k_stream(const float4* __restrict__ r, const float4* __restrict_
 extern "C" int ppo_floor(int which, const void* r, const void* v, const void* d, void* o0, void* o1, int64_t n,
                          int grid, int block, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  if (grid <= 0) {  // one pass with every SM busy: up to 4 CTAs per SM
+    int64_t g = (n / 4 + block - 1) / block;
+    grid = (int)(g < 148 * 4 ? g : 148 * 4);
+  }
   if (which == 0) k_empty<<<1, 32, 0, st>>>();
   else k_stream<<<grid, block, 0, st>>>((const float4*)r, (const float4*)v, (const uchar4*)d, (float4*)o0,
                                         (float4*)o1, n / 4);

@@ -107,4 +107,24 @@ def test_mode_c_central_batch(cuda):
                                   PERIOD)
         for name in ("obs", "act", "prev_act", "rew", "prev_rew", "done", "rnn"):
             assert np.array_equal(res[name][:, col], ref[name][:, 0]), (name, col)
-    assert (res["w"] > 0).all() and np.isclose(res["w"].max(), 1.0)
+    # IS weights and the sample itself vs the oracle: sharded sampling == sampling the
+    # shard-major concatenation (§8c #17) with the same Philox stream; weights normalised by
+    # the global batch max (§8c #10)
+    from oracle import philox as OP
+    from oracle import sumtree as OS
+    from tests._tol import check_rel
+    shards = []
+    for r, h in enumerate(rings):
+        Bl = B_TOT // 2
+        o = OS.SumTreeOracle((CAP // PERIOD) * Bl)
+        valid = [blk * Bl + b for blk in range(CAP // PERIOD)
+                 if OG.window_valid_sequence(blk * PERIOD, CAP, h.cursor, h.size, K, L) for b in range(Bl)]
+        g = np.random.default_rng(5 + r)
+        td = np.abs(g.normal(size=len(valid))).astype(np.float32)
+        o.update(valid, [float(x) for x in td], 0.9)
+        shards.append(o)
+    n_glob = 2 * N_PER
+    oi, oq, _ = OS.sharded_sample(shards, n_glob, OP.draws_u64(17, 0, n_glob))
+    assert glob == oi
+    Q = sum(sh.total() for sh in shards)
+    check_rel(res["w"], OS.is_weights(oq, Q, 2 * n_leaves, 0.6), what="mode C w")

@@ -159,3 +159,38 @@ def test_errors(rpl):
         rpl.returns_discounted(r.cpu(), d, None, 0.9)
     with pytest.raises(rpl._lib.RplError):
         rpl.returns_nstep(r, d, 2, 0.9, rescale=True, eps=0.0)
+
+
+@pytest.mark.parametrize("T,B", [(1, 1), (16, 32), (129, 31), (300, 48), (128, 4096), (1000, 80), (33, 4096)])
+def test_time_limit_bootstrap_tl_entries(rpl, T, B, scan_variant):
+    # R34: half of the episode ends are time limits (d = 2) with terminal values v_term;
+    # discounted / GAE / n-step through the rpl_*_tl entries vs the oracle, every element
+    g = rng(T * 13 + B)
+    r, v, d, boot = returns_inputs(2000 + T + B, T, B, reward_kind="heavy", p_done=0.08)
+    d = d.copy()
+    d[(d == 1) & (g.random(d.shape) < 0.5)] = 2
+    vt = g.normal(0, 5, (T, B)).astype(np.float32)
+    for gamma, lam in [(0.99, 0.95), (0.997, 1.0)]:
+        ref = OR.discounted_return(r, d, boot, gamma, v_term=vt)
+        S = OR.abs_scale_discounted(r, d, boot, gamma, v_term=vt)
+        check_rel(H(rpl.returns_discounted(T_(r), T_(d), T_(boot), gamma, v_term=T_(vt))), ref, S, what="disc tl")
+        adv_ref, ret_ref = OR.gae(r, v, d, boot, gamma, lam, v_term=vt)
+        Sg = OR.abs_scale_gae(r, v, d, boot, gamma, lam, v_term=vt)
+        adv, ret = rpl.gae(T_(r), T_(v), T_(d), T_(boot), gamma, lam, v_term=T_(vt))
+        check_rel(H(adv), adv_ref, Sg, what="adv tl")
+        check_rel(H(ret), ret_ref, Sg, what="ret tl")
+        # without v_term a time-limit row is a plain terminal (== d = 1)
+        d1 = np.where(d != 0, 1, 0).astype(np.uint8)
+        assert np.array_equal(H(rpl.returns_discounted(T_(r), T_(d), T_(boot), gamma)),
+                              H(rpl.returns_discounted(T_(r), T_(d1), T_(boot), gamma)))
+    for n in (1, 3, 5):
+        if n > T:
+            continue
+        q = g.normal(0, 10, (T, B)).astype(np.float32)
+        qb = g.normal(0, 10, B).astype(np.float32)
+        for rescale in (False, True):
+            y, dn = rpl.returns_nstep(T_(r), T_(d), n, 0.99, q=T_(q), q_boot=T_(qb), rescale=rescale, v_term=T_(vt))
+            yr, dnr = OR.nstep_return(r, d, n, 0.99, q=q, q_boot=qb, rescale=rescale, v_term=vt)
+            sc, _ = OR.nstep_return(np.abs(r), d, n, 0.99, q=np.abs(q), q_boot=np.abs(qb), v_term=np.abs(vt))
+            check_rel(H(y), yr, sc + np.abs(yr) + 1e-3, what=f"nstep tl n={n} rescale={rescale}")
+            assert np.array_equal(H(dn), dnr)
