@@ -271,6 +271,7 @@ def run_rpl(args):
         plan = root_plan if rank == 0 else rpl.GatherPlan(ring, n_glob, kind="sequence", k=k, seq_len=L,
                                                           period=period, with_weights=True, out_mode=_L.OUT_UNIQUE,
                                                           want=want, outputs=central.outputs)
+        central.attach(plan)  # the gather signals the learner's flag when its last CTA is done
         if rank == 0:
             stacked = torch.empty((L, n_glob, k) + tuple(ring.item_shape), dtype=torch.uint8, device=dev)
     else:
@@ -377,8 +378,8 @@ def run_rpl(args):
         if gather_events is not None:
             gather_events[1].record()
         if mode_c:
-            central.arrived()                                                    # K8: batch complete on rank 0
-            if rank == 0:  # learner: k-stacks from the shipped unique rows (local HBM)
+            if rank == 0:  # learner: wait for every owner's completion flag (K8, no collective),
+                central.wait(stream=s)  # then the k-stacks from the shipped unique rows (local HBM)
                 rpl._lib.check(lib.rpl_stack_frames(P_(out["obs"]), P_(out["start"]), L, n_glob, k, ring.obs_bytes,
                                                     0, P_(stacked), None, s), "stack")
         if learner and not fused_tgt:
@@ -568,6 +569,11 @@ def run_rpl(args):
     if not args.profile:
         result["clocks"] = clk
         result["e2e"] = e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K_eff, world)
+        # a1-a4 at every N: each rank scans its own [128, 4096] columns, no collective
+        try:
+            result["returns"] = returns_line(dev, rpl, world, dist if world > 1 else None)
+        except Exception as e:  # pragma: no cover
+            result["returns"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if world == 1 and not args.no_secondary and not args.profile:
         # each secondary is isolated: a failure is reported in its slot, never loses the line
         jobs = [("r2d2_seeds", lambda: seed_sweep(dev, rpl, c, ms / K_eff * 1e3)),
@@ -576,7 +582,6 @@ def run_rpl(args):
                 ("r2d2_unique_output", lambda: unique_output_step(dev, rpl, tree, ring, idx_buf, td_pool, q_pool, err,
                                                                   c, n, P, seed)),
                 ("tree_latency", lambda: tree_latency(dev, rpl)),
-                ("ppo_returns", lambda: bench_ppo(dev, rpl)),
                 ("dqn_replay", lambda: bench_dqn(dev, rpl)),
                 ("mujoco_replay", lambda: bench_mujoco(dev, rpl))]
         result["secondary"] = {}
@@ -709,6 +714,30 @@ def e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K, world):
             else "eager launches incl. pinned-host H2D/D2H copies"}
 
 
+def returns_line(dev, rpl, world, dist):
+    """Return estimation (a1-a4) at N GPUs, weak scaling: every rank runs GAE, the discounted
+    return and the rescaled 5-step target on its own PPO-shaped [128, 4096] buffers (columns
+    are independent: no collective on the data path).  Per-call device time is the max over
+    ranks; aggregate elems/s = N x 128 x 4096 / that time."""
+    import torch
+    r = bench_ppo(dev, rpl)
+    keys = ("gae_us_per_call", "disc_us_per_call", "nstep_us_per_call")
+    t = torch.tensor([r[k] for k in keys], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    T, B = PPO["T"], PPO["B"]
+    out = {"workload": f"ppo_[{T},{B}] per rank", "unit": "elems/s", "n_gpus": world, "scaling": "weak",
+           "exchange": "none (columns independent)", "timing": r["timing"], "l2": r["l2"]}
+    peak, _ = measured_peaks()
+    for k, nb in zip(keys, (17, 9, 14)):  # bytes per element: GAE, discounted, n-step with bootstrap q
+        us = float(t[keys.index(k)].item())
+        name = k.split("_")[0]
+        out[f"{name}_us_per_call_max_over_ranks"] = us
+        out[f"{name}_elems_per_s_aggregate"] = world * T * B / (us * 1e-6)
+        out[f"{name}_frac_per_gpu"] = T * B * nb / (us * 1e-6) / 1e9 / peak
+    return out
+
+
 def bench_ppo(dev, rpl):
     """GAE + discounted returns on [128, 4096] (configs[1]); inputs rotate over a
     pool larger than L2 so every call reads HBM."""
@@ -751,8 +780,13 @@ def bench_ppo(dev, rpl):
 
     g_gae = capture(lambda i: rpl.gae(R[i], V[i], D[i], BT, PPO["gamma"], PPO["lam"], adv=A[i], ret=RT[i]))
     g_disc = capture(lambda i: rpl.returns_discounted(R[i], D[i], BT, PPO["gamma"], out=RT[i]))
+    QB = torch.zeros_like(BT)
+    DN = torch.empty((T - 4, B), dtype=torch.uint8, device=dev)
+    g_nstep = capture(lambda i: rpl.returns_nstep(R[i], D[i], 5, PPO["gamma"], q=V[i], q_boot=QB, rescale=True,
+                                                  out=A[i][:T - 4], done_out=DN))
     ms_gae = timeit(g_gae)
     ms_disc = timeit(g_disc)
+    ms_nstep = timeit(g_nstep)
     peak, kind = measured_peaks()
     gae_gbs = T * B * 17 / (ms_gae / 1e3) / 1e9
     disc_gbs = (T * B * 9 + B * 4) / (ms_disc / 1e3) / 1e9
@@ -760,6 +794,7 @@ def bench_ppo(dev, rpl):
             "gae_elems_per_s": T * B / (ms_gae / 1e3), "gae_us_per_call": ms_gae * 1e3, "gae_GBps": gae_gbs,
             "gae_frac": gae_gbs / peak, "disc_elems_per_s": T * B / (ms_disc / 1e3),
             "disc_us_per_call": ms_disc * 1e3, "disc_GBps": disc_gbs, "disc_frac": disc_gbs / peak,
+            "nstep_us_per_call": ms_nstep * 1e3, "nstep_note": "rescaled 5-step target, bootstrap q = V rows",
             "l2": f"input pool {pool} x {per/1e6:.1f} MB > 4 x L2",
             "timing": "CUDA graph of one call per pool entry, replayed; per-call average"}
 

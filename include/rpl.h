@@ -279,7 +279,8 @@ int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t 
  * 0, strictly increasing).  One slot per source suffices: a rank cannot publish step j+1's
  * total before every peer has consumed step j's values (step j's gather on each rank waits
  * for every rank's K7 value, which each rank publishes after its K5 read).  A wait longer
- * than ~2 s gives up and sets RPL_DERR_PEER. */
+ * than ~2 s is a failed exchange: the kernel sets RPL_DERR_PEER and traps, so the failure
+ * surfaces at the next synchronisation instead of a step computed from a missing value. */
 #define RPL_BOARD_WORDS(n_shards) (4 * (int64_t)(n_shards))
 
 /* Host plumbing for the boards: lets kernels running on the calling thread's current device
@@ -450,10 +451,28 @@ typedef struct {
    * episode boundary and bootstrapped from the supplied value; done_n stays 1 (the learner
    * must not bootstrap again).  With v_term NULL any non-zero done flag is a terminal. */
   const float* v_term;
+  /* Optional completion signal (SEQUENCE, default kernel only; both or neither, else
+   * RPL_EINVAL): done_seq = device int64 [2] in this rank's memory, zero-initialised (a call
+   * counter and a CTA ticket); done_flag = a device int64 (typically another GPU's memory
+   * mapped over NVLink).  When the call's last CTA has finished, every output store of the
+   * call is made visible at system scope and done_flag := ++done_seq[0] (st.release.sys).
+   * Mode C: each owner signals the learner this way; the learner waits with rpl_wait_flags. */
+  int64_t* done_flag;
+  int64_t* done_seq;
 } rpl_gather_desc;
 
 int rpl_gather(const rpl_gather_desc* desc /* host */, const int64_t* idx, const int64_t* q,
                const int64_t* qmin, double beta, int64_t n, int32_t* dev_err, void* stream);
+
+/* Stream-ordered wait for n completion flags (device int64 [n], e.g. the learner's flag array
+ * that n owners' gathers signal through rpl_gather_desc.done_flag): returns at once, the
+ * enqueued one-warp kernel spins with ld.acquire.sys until flags[i] >= *expect for every i
+ * (expect: device int64, e.g. the learner's own done_seq[0]), then fences at system scope, so
+ * work enqueued after it on the stream reads every owner's stores.  A flag still short after
+ * ~2 s sets RPL_DERR_PEER in *dev_err and traps the kernel (the context then reports the
+ * failure at the next synchronisation): an exchange never continues with a partial batch.
+ * n in [1, 1024]. */
+int rpl_wait_flags(const int64_t* flags, int32_t n, const int64_t* expect, int32_t* dev_err, void* stream);
 
 /* k-stacks from unique rows (Mode C learner side, §8e): uniq [L+k-1, n, obs_bytes] as written
  * by rpl_gather with RPL_OUT_UNIQUE, start int8 [L, n] its o_start; out [L, n, k, obs_bytes]

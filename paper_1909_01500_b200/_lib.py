@@ -60,6 +60,7 @@ class GatherDesc(C.Structure):
         ("tgt_lo", C.c_int32), ("tgt_T", C.c_int32), ("rescale", C.c_int32), ("_pad1", C.c_int32),
         ("rescale_eps", C.c_double),
         ("v_term", C.c_void_p),
+        ("done_flag", C.c_void_p), ("done_seq", C.c_void_p),
     ]
 
 
@@ -106,6 +107,7 @@ _SIGS = {
     "rpl_sample_uniform": ([I64, U64, U64, P, I64, I64, I64, I64, P, P], C.c_int),
     "rpl_gather": ([C.POINTER(GatherDesc), P, P, P, D, I64, P, P], C.c_int),
     "rpl_ring_append": ([C.POINTER(GatherDesc), P, P, P, P, P, I64, P], C.c_int),
+    "rpl_wait_flags": ([P, I32, P, P, P], C.c_int),
     "rpl_stack_frames": ([P, P, I64, I64, I32, I64, I32, P, P, P], C.c_int),
     "rpl_returns_nstep_dq": ([P, P, I64, I64, I32, D, P, P, I32, I32, D, P, P, P, P], C.c_int),
     "rpl_c51_project": ([P, P, P, P, I64, I32, I32, D, D, D, P, P, P], C.c_int),

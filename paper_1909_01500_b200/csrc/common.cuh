@@ -111,6 +111,50 @@ int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cud
   return launch_pdl_cluster(kernel, grid, block, smem, st, 1u, args...);
 }
 
+// Cooperative launch (cudaLaunchAttributeCooperative) for kernels with a grid-wide barrier:
+// the runtime guarantees every CTA is co-resident or fails the launch (never a silent
+// deadlock next to other streams' work).  The grid must not exceed the occupancy-derived
+// capacity (checked here: RPL_EINVAL).  PDL is added when enabled; if the runtime rejects the
+// combination the launch is retried cooperative-only.
+template <typename... KArgs, typename... Args>
+int launch_coop(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, (int)(block.x * block.y * block.z), smem) !=
+          cudaSuccess ||
+      (int64_t)grid.x * grid.y * grid.z > (int64_t)per_sm * sm_count()) {
+    cudaGetLastError();
+    return RPL_EINVAL;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  int na = 1;
+  if (pdl_enabled()) {
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    na = 2;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess && na == 2) {
+    cudaGetLastError();
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  }
+  ++g_launches;
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return RPL_ECUDA;
+  }
+  return RPL_OK;
+}
+
 __device__ __forceinline__ double h_fwd(double x, double eps) {
   // h(x) = x (1/(sqrt(|x|+1)+1) + eps)  ==  sign(x)(sqrt(|x|+1)-1) + eps x   (§8c #4)
   return x * (1.0 / (sqrt(fabs(x) + 1.0) + 1.0) + eps);
@@ -161,6 +205,15 @@ __device__ __forceinline__ bool board_wait(const int64_t* slot, uint64_t tag, in
     if (global_ns() - t0 > 2000000000ull) return false;
     __nanosleep(64);
   }
+}
+
+// A peer that never published within board_wait's ~2 s: the exchange failed.  Set the device
+// error bit and trap, so the failure surfaces at the next synchronisation (the context reports
+// a launch failure) instead of the step continuing on a default value.
+__device__ __forceinline__ void board_fail(int32_t* err) {
+  set_err(err, RPL_DERR_PEER);
+  __threadfence_system();
+  __trap();
 }
 
 // 64-bit warp shuffles (int64 payloads)

@@ -201,6 +201,8 @@ struct GDesc {
   int tgt_lo, tgt_T, rescale;
   double rescale_eps;
   const float* v_term;  // time-limit bootstrap values (R34; NULL: every done is terminal)
+  int64_t* done_flag;   // completion signal (Mode C; NULL: off)
+  int64_t* done_seq;    // [2] call counter + CTA ticket (device, this rank's memory)
 };
 
 // Output column offset (rpl_gather_desc.col_offset); read after pdl_wait.
@@ -965,7 +967,8 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         board_publish(D.peer_boards[lane] + 2 * D.peer_world + 2 * D.peer_rank, qm_local, ptag);
     }
   }
-  if (g0 >= g1) return;
+  do {  // (break = this CTA has no rows; the completion epilogue below still runs)
+  if (g0 >= g1) break;
   const int nrows = g1 - g0;
   const int s_first = g0 / L;
   const int npieces = (g1 - 1) / L - s_first + 1;
@@ -1171,8 +1174,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         int64_t v = INT64_MAX;
         if (lane < D.peer_world &&
             !board_wait(D.peer_boards[D.peer_rank] + 2 * D.peer_world + 2 * lane, ptag, &v)) {
-          set_err(err, RPL_DERR_PEER);
-          v = INT64_MAX;
+          board_fail(err);
         }
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) {
@@ -1267,9 +1269,27 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       }
     }
   }
+  } while (0);
+  // Completion signal (rpl_gather_desc.done_flag, Mode C): every CTA publishes its stores at
+  // system scope and takes a ticket; the last CTA bumps the call counter done_seq[0] and
+  // writes it to done_flag with st.release.sys (peer memory over NVLink), so the learner's
+  // rpl_wait_flags observes the whole batch without any collective.
+  if (D.done_flag) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const unsigned t = atomicAdd(reinterpret_cast<unsigned*>(D.done_seq + 1), 1u);
+      if (t == gridDim.x - 1) {
+        __threadfence_system();
+        D.done_seq[1] = 0;
+        const int64_t sq = D.done_seq[0] + 1;
+        D.done_seq[0] = sq;
+        asm volatile("st.release.sys.global.s64 [%0], %1;" ::"l"(D.done_flag), "l"(sq) : "memory");
+      }
+    }
+  }
   pdl_trigger();
 }
-
 template <int NC>
 int launch_seq_lsu(const GDesc& g, const int64_t* idx, int64_t n, int NS, int64_t rows_per_cta, const int64_t* q,
                    const int64_t* qmin, double beta, int32_t* dev_err, size_t dyn, int64_t grid, cudaStream_t st) {
@@ -1794,6 +1814,8 @@ GDesc to_dev(const rpl_gather_desc* d) {
   g.rescale = d->rescale;
   g.rescale_eps = d->rescale_eps;
   g.v_term = d->v_term;
+  g.done_flag = d->done_flag;
+  g.done_seq = d->done_seq;
   return g;
 }
 
@@ -1870,8 +1892,9 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
     return RPL_EINVAL;
   GDesc g = to_dev(desc);
   // col_offset / o_start / peer boards / fused targets: default kernels only
+  if ((desc->done_flag != nullptr) != (desc->done_seq != nullptr)) return RPL_EINVAL;
   const int seq_variant =
-      (desc->col_offset || desc->o_start || desc->peer_boards || desc->o_tgt) ? 0 : g_seq_variant;
+      (desc->col_offset || desc->o_start || desc->peer_boards || desc->o_tgt || desc->done_flag) ? 0 : g_seq_variant;
   const bool tma_ok = (desc->obs_bytes % 16 == 0) && aligned16(desc->obs) && aligned16(desc->o_obs) &&
                       aligned16(desc->o_next_obs) && desc->obs_bytes <= 32768;
   cudaStream_t st = as_stream(stream);
@@ -1992,7 +2015,8 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
         return launch_status();
       }
     }
-    if (desc->o_start || desc->peer_boards || desc->o_tgt) return RPL_EUNSUPPORTED;  // persistent default only
+    if (desc->o_start || desc->peer_boards || desc->o_tgt || desc->done_flag)
+      return RPL_EUNSUPPORTED;  // persistent default kernel only
     const int64_t smem = (int64_t)(SEQ_CHUNK + desc->k) * desc->obs_bytes;
     g.use_tma = (tma_ok && smem <= 200 * 1024) ? 1 : 0;
     const size_t dyn = g.use_tma ? (size_t)smem : 0;
@@ -2057,4 +2081,42 @@ extern "C" int rpl_stack_frames(const void* uniq, const int8_t* start, int64_t L
   return launch_pdl(k_stack_frames, grid, dim3(ST_WARPS * 32), 0, as_stream(stream),
                     static_cast<const uint8_t*>(uniq), start, (int)L, n, (int)k, obs_bytes, (int)pad_mode,
                     static_cast<uint8_t*>(out), n_active);
+}
+
+// ---------------------------------------------------------------------------
+// Learner-side wait for the owners' completion signals (Mode C, §8e): lane i spins with
+// ld.acquire.sys until flags[i] >= *expect (the learner's own call counter, bumped by its own
+// gather earlier on this stream), then the warp issues a system-scope fence so the next
+// kernel on the stream reads the owners' peer stores.  A peer that does not signal within
+// ~2 s is a failed exchange: RPL_DERR_PEER is set and the kernel traps, so the error
+// surfaces at the next synchronisation instead of a silently incomplete batch.
+// ---------------------------------------------------------------------------
+namespace rpl {
+namespace {
+__global__ void k_wait_flags(const int64_t* flags, int n, const int64_t* expect, int32_t* err) {
+  pdl_wait();
+  const int64_t want = *expect;
+  for (int i = threadIdx.x; i < n; i += 32) {
+    const uint64_t t0 = global_ns();
+    while (true) {
+      int64_t v;
+      asm volatile("ld.acquire.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(flags + i) : "memory");
+      if (v >= want) break;
+      if (global_ns() - t0 > 2000000000ull) {
+        board_fail(err);
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncwarp();
+  __threadfence_system();
+  pdl_trigger();
+}
+}  // namespace
+}  // namespace rpl
+
+extern "C" int rpl_wait_flags(const int64_t* flags, int32_t n, const int64_t* expect, int32_t* dev_err,
+                              void* stream) {
+  if (!flags || !expect || n < 1 || n > 1024) return RPL_EINVAL;
+  return launch_pdl(k_wait_flags, dim3(1), dim3(32), 0, as_stream(stream), flags, (int)n, expect, dev_err);
 }

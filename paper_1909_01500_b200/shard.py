@@ -84,32 +84,69 @@ class CentralBatch:
     into the gather, no staging copy and no NCCL send of frames.  Used with a compacted
     ShardedSampler: count = [m, k0] feeds rpl_gather_desc.n_active / col_offset.
 
-    A small all-reduce after the gather (K8, `arrived`) tells the learner the batch is
-    complete: a rank's NCCL kernel runs after its gather on the same stream, so its
-    completion on the learner implies every owner's peer writes have landed."""
+    Completion (K8) needs no collective either: the learner also owns a flag word per rank
+    (int64 [world], mapped like the outputs).  `attach(plan)` makes a rank's gather signal
+    its flag when its last CTA finishes (rpl_gather_desc.done_flag: every store made visible
+    at system scope, then st.release.sys of the rank's call counter); on the learner
+    `wait()` enqueues rpl_wait_flags, which spins until every rank's flag has reached the
+    learner's own call count (fails loudly after ~2 s), so work enqueued after it reads the
+    complete batch.  A mapped buffer in another GPU's memory gets peer access from this
+    rank's device (rpl_peer_access); all ranks agree on the outcome before raising."""
 
     def __init__(self, outputs_on_root, group=None, root: int = 0):
         from torch.multiprocessing.reductions import reduce_tensor
         self.group = group
         self.root = root
         self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        local = torch.device("cuda", torch.cuda.current_device())
         names = sorted(outputs_on_root) if outputs_on_root is not None else None
         if self.rank == root:
-            payload = [[(n, reduce_tensor(outputs_on_root[n])) for n in names]]
+            dev = next(iter(outputs_on_root.values())).device
+            self.flags = torch.zeros(self.world, dtype=torch.int64, device=dev)
+            torch.cuda.synchronize(dev)
+            payload = [[(n, reduce_tensor(outputs_on_root[n])) for n in names] +
+                       [("__flags__", reduce_tensor(self.flags))]]
         else:
             payload = [None]
         dist.broadcast_object_list(payload, src=root, group=group)
+        failure = None
         if self.rank == root:
             self.outputs = dict(outputs_on_root)
         else:
-            self.outputs = {n: fn(*args) for n, (fn, args) in payload[0]}
-        dev = next(iter(self.outputs.values())).device if self.rank == root else torch.device("cuda",
-                                                                                             torch.cuda.current_device())
-        self.flag = torch.zeros(1, dtype=torch.int64, device=dev)
+            mapped = {n: fn(*args) for n, (fn, args) in payload[0]}
+            self.flags = mapped.pop("__flags__")
+            self.outputs = mapped
+            failure = self._peer_access(list(mapped.values()) + [self.flags], local)
+        ok = torch.tensor([0 if failure else 1], dtype=torch.int32, device=local)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            raise RuntimeError(f"central batch unreachable from some rank ({failure or 'a peer failed'})")
+        self.seq = torch.zeros(2, dtype=torch.int64, device=local)  # rpl_gather_desc.done_seq
+        self.err = torch.zeros(1, dtype=torch.int32, device=local)
 
-    def arrived(self):
-        """K8: completion signal after this rank's gather (stream-ordered, 8 bytes)."""
-        dist.all_reduce(self.flag, group=self.group)
+    @staticmethod
+    def _peer_access(tensors, local):
+        from . import _lib
+        for dev_index in sorted({t.device.index for t in tensors if t.device != local}):
+            with torch.cuda.device(local):
+                rc = _lib.lib.rpl_peer_access(dev_index)
+            if rc != 0:
+                return f"rpl_peer_access({dev_index}) from {local}: {_lib.lib.rpl_strerror(rc).decode()}"
+        return None
+
+    def attach(self, plan):
+        """Make this rank's gather (a GatherPlan writing into self.outputs) signal completion."""
+        plan.desc.done_flag = self.flags[self.rank].data_ptr()
+        plan.desc.done_seq = self.seq.data_ptr()
+
+    def wait(self, stream=None):
+        """Learner only: enqueue the wait for every rank's completion flag (K8)."""
+        from . import _lib
+        from .ops import _stream
+        s = _stream(self.flags.device) if stream is None else stream
+        _lib.check(_lib.lib.rpl_wait_flags(self.flags.data_ptr(), self.world, self.seq.data_ptr(),
+                                           self.err.data_ptr(), s), "rpl_wait_flags")
 
 
 class PeerBoards:

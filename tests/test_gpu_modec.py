@@ -60,14 +60,15 @@ def _worker(rank, world, port, queue):
                                                       with_weights=True, out_mode=1, want=want, outputs=cb.outputs)
     plan.desc.n_active = smp.count.data_ptr()
     plan.desc.col_offset = smp.count.data_ptr() + 8
+    cb.attach(plan)  # completion flag (K8) instead of a collective
     if rank == 0:
         for t in cb.outputs.values():
             t.zero_()
     dist.barrier()
     idx, q, w = smp.sample(0.6)  # compacted: this rank's LOCAL leaves first
     plan.run(idx, q=q, qmin=smp.qmin, beta=0.6)
-    torch.cuda.synchronize()
-    cb.arrived()
+    if rank == 0:
+        cb.wait()  # spins until both ranks' gathers signalled (st.release.sys flags)
     torch.cuda.synchronize()
     # every rank reports its global sample (compacted) so rank 0 can rebuild the global order
     m = int(smp.count[0].item())

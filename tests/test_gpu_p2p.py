@@ -143,18 +143,33 @@ def test_p2p_gather_weights(rpl, empty):
             assert b[2 * G::2].tolist() == mins
 
 
-def test_p2p_timeout_sets_error(rpl):
-    # a peer that never publishes: the wait gives up after ~2 s with RPL_DERR_PEER
-    import torch
-    t = rpl.SumTree(100, 32)
-    t.update(T_(np.arange(100, dtype=np.int64)), T_(np.ones(100, np.float32)), 0.9)
-    boards = [torch.zeros(8, dtype=torch.int64, device="cuda") for _ in range(2)]
-    ptrs = torch.tensor([b.data_ptr() for b in boards], dtype=torch.int64, device="cuda")
-    err = torch.zeros(1, dtype=torch.int32, device="cuda")
-    cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
-    t.sample_sharded_p2p(0, 2, ptrs, 16, 1, cnt, err=err)
+def test_p2p_timeout_fails_loudly(cuda):
+    # a peer that never publishes: after ~2 s the sampler sets RPL_DERR_PEER and traps, so the
+    # step fails at the next synchronisation (run in a child process: the trap ends its context)
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = """
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_1909_01500_b200 as rpl
+t = rpl.SumTree(100, 32)
+t.update(torch.arange(100, device="cuda"), torch.ones(100, device="cuda"), 0.9)
+boards = [torch.zeros(8, dtype=torch.int64, device="cuda") for _ in range(2)]
+ptrs = torch.tensor([b.data_ptr() for b in boards], dtype=torch.int64, device="cuda")
+err = torch.zeros(1, dtype=torch.int32, device="cuda")
+cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
+t.sample_sharded_p2p(0, 2, ptrs, 16, 1, cnt, err=err)
+try:
     torch.cuda.synchronize()
-    assert int(H(err)[0]) & 32
+except RuntimeError as e:
+    print("FAILED-LOUDLY", str(e).splitlines()[0])
+    sys.exit(3)
+print("CONTINUED", int(err.cpu()[0]))
+""" % root
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert res.returncode == 3 and "FAILED-LOUDLY" in res.stdout, (res.returncode, res.stdout, res.stderr[-500:])
 
 
 def test_p2p_prefilled_peer(rpl):
