@@ -153,6 +153,9 @@ typedef struct {
   int64_t n_words;      /* int64 words the caller must allocate */
 } rpl_tree_layout;
 
+/* Header words 5-6 (rpl_mintree_attach): [hdr_off+5] the attached min-tree's device address
+ * (0 = none), [hdr_off+6] the global buffer min written by the sharded samplers. */
+
 /* Fill *out (host) for n_leaves >= 1, fanout in {2,4,8,16,32}, frac_bits in [0,62]. */
 int rpl_sumtree_layout(int64_t n_leaves, int32_t fanout, int32_t frac_bits, rpl_tree_layout* out);
 
@@ -273,7 +276,10 @@ int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t 
  * over NVLink; the rank's own board in its own slot).  `boards` is a DEVICE array of
  * n_shards pointers, boards[g] = rank g's board as seen from this process.  Board layout:
  * words [2 s, 2 s + 1] = {total, tag} published by rank s (K5), words [2 G + 2 s, +1] =
- * {batch-min q, tag} published by rank s (K7).  A value is written with a plain store and
+ * {batch-min q, tag} published by rank s (K7), words [4 G + 2 s, +1] = {buffer min, tag}
+ * published with the K5 total (root of the shard's attached min-tree, INT64_MAX without one;
+ * a sampler whose tree has a min-tree reads all G and writes the global buffer min to its
+ * header word 6 — the buffer-wide normaliser with no second exchange, R29).  A value is written with a plain store and
  * its tag with st.release.sys; a reader spins on ld.acquire.sys until the tag equals the
  * step's tag = the tree's stream position after the step (identical on every rank, never
  * 0, strictly increasing).  One slot per source suffices: a rank cannot publish step j+1's
@@ -281,7 +287,7 @@ int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t 
  * for every rank's K7 value, which each rank publishes after its K5 read).  A wait longer
  * than ~2 s is a failed exchange: the kernel sets RPL_DERR_PEER and traps, so the failure
  * surfaces at the next synchronisation instead of a step computed from a missing value. */
-#define RPL_BOARD_WORDS(n_shards) (4 * (int64_t)(n_shards))
+#define RPL_BOARD_WORDS(n_shards) (6 * (int64_t)(n_shards))
 
 /* Host plumbing for the boards: lets kernels running on the calling thread's current device
  * load from / store to memory of device `peer_device` (a peer rank's board mapped through
@@ -315,6 +321,33 @@ int rpl_sumtree_min(const rpl_tree_layout* L, const int64_t* tree, int64_t* out_
 
 /* *out_total = root (int64, device). */
 int rpl_sumtree_total(const rpl_tree_layout* L, const int64_t* tree, int64_t* out_total, void* stream);
+
+/* Buffer-wide IS normaliser (§8f NEXT-4, reading R29; PER's "normalised by max w" over the
+ * whole buffer): a MIN-TREE maintained beside the sum tree.  mins = caller-owned device int64
+ * [L->level_off[L->depth]] (one word per internal node, the sum tree's internal layout):
+ * node (l, j) = min of the positive leaves below it (INT64_MAX when none), so mins[0] is the
+ * smallest positive leaf q_min and w_i = (q_min / q_i)^beta = (N P_i)^-beta / max over the
+ * buffer.  rpl_mintree_attach records the address in header word 5 and builds every node
+ * (mins == NULL detaches).  From then on every leaf write keeps it exact: the update kernels
+ * (rpl_sumtree_update / _ex / _seq / set_q / update_sample) recompute the min path of each
+ * written leaf level by level in the same launch; rpl_replay_validity and rpl_sumtree_rebuild
+ * rebuild it.  rpl_sumtree_init clears the header (detaches).  Pass &mins[0] as rpl_gather's
+ * qmin (or rpl_is_weights') for buffer-normalised weights. */
+int rpl_mintree_attach(const rpl_tree_layout* L, int64_t* tree, int64_t* mins, void* stream);
+/* Rebuild every node of the attached min-tree from the leaves (no-op if none attached). */
+int rpl_mintree_rebuild(const rpl_tree_layout* L, const int64_t* tree, void* stream);
+/* out[0] = the root sum (rpl_sumtree_total), out[1] = the attached min-tree's root
+ * (INT64_MAX without one): the 16-byte per-rank record one all-gather exchanges (K5 with the
+ * buffer-wide normaliser, no second collective). */
+int rpl_sumtree_total_min(const rpl_tree_layout* L, const int64_t* tree, int64_t* out, void* stream);
+/* rpl_sumtree_sample_sharded with the K5 record of rpl_sumtree_total_min: shard_pairs = device
+ * int64 [n_shards][2] {total, buffer min} (all-gathered); stream mode, compacted output
+ * (out_count required); *out_bufmin (device, may be NULL) and header word 6 := the global
+ * buffer min (min over the shards).  out_qmin (may be NULL) = this rank's owned batch min. */
+int rpl_sumtree_sample_sharded_pairs(const rpl_tree_layout* L, int64_t* tree, int32_t rank, int32_t n_shards,
+                                     int64_t shard_leaves, const int64_t* shard_pairs, int64_t n, uint64_t seed,
+                                     int64_t* out_idx, int64_t* out_q, int64_t* out_qmin, int64_t* out_count,
+                                     int64_t* out_bufmin, int32_t* dev_err, void* stream);
 
 /* Recompute every internal node from the leaves (resume after restoring leaves). */
 int rpl_sumtree_rebuild(const rpl_tree_layout* L, int64_t* tree, void* stream);

@@ -103,6 +103,11 @@ _SIGS = {
     "rpl_sumtree_min": ([C.POINTER(TreeLayout), P, P, P], C.c_int),
     "rpl_sumtree_sample_unique": ([C.POINTER(TreeLayout), P, I64, U64, U64, I32, P, P, P, P], C.c_int),
     "rpl_sumtree_rebuild": ([C.POINTER(TreeLayout), P, P], C.c_int),
+    "rpl_mintree_attach": ([C.POINTER(TreeLayout), P, P, P], C.c_int),
+    "rpl_mintree_rebuild": ([C.POINTER(TreeLayout), P, P], C.c_int),
+    "rpl_sumtree_total_min": ([C.POINTER(TreeLayout), P, P, P], C.c_int),
+    "rpl_sumtree_sample_sharded_pairs": ([C.POINTER(TreeLayout), P, I32, I32, I64, P, I64, U64, P, P, P, P, P, P,
+                                          P], C.c_int),
     "rpl_is_weights": ([P, P, I64, D, P, P], C.c_int),
     "rpl_sample_uniform": ([I64, U64, U64, P, I64, I64, I64, I64, P, P], C.c_int),
     "rpl_gather": ([C.POINTER(GatherDesc), P, P, P, D, I64, P, P], C.c_int),

@@ -161,7 +161,10 @@ extern "C" int rpl_replay_validity(const rpl_tree_layout* L, int64_t* tree, int3
   int64_t blocks = (L->n_leaves + threads - 1) / threads;
   const int64_t cap_blocks = (int64_t)sm_count() * 8;
   if (blocks > cap_blocks) blocks = cap_blocks;
-  return launch_pdl(k_replay_validity, dim3((unsigned)blocks), dim3(threads), 0, as_stream(stream), tree_dev(L), tree,
-                    (int)kind, cap_T, B, (int)k, (int)n_step, (int)seq_len, (int)period, cursor_old, size_old,
-                    cursor_new, size_new);
+  const int s = launch_pdl(k_replay_validity, dim3((unsigned)blocks), dim3(threads), 0, as_stream(stream),
+                           tree_dev(L), tree, (int)kind, cap_T, B, (int)k, (int)n_step, (int)seq_len, (int)period,
+                           cursor_old, size_old, cursor_new, size_new);
+  if (s != RPL_OK) return s;
+  // an attached min-tree (R29) is rebuilt from the new leaves (device-side no-op without one)
+  return rpl_mintree_rebuild(L, tree, stream);
 }

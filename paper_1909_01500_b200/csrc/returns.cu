@@ -419,6 +419,193 @@ k_scan_tma2(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
 }
 
 // ---------------------------------------------------------------------------
+// Persistent pipelined scan (variant 9): a CTA walks a list of work items — column group g
+// (COLS columns) x chunk c (CH rows), every chunk of a group from the end so the carry stays
+// in shared memory — with the loads of the next STAGES-1 items in flight (TMA tiles into a
+// ring of stages, one mbarrier each) and the outputs leaving through TMA tensor stores from
+// a double-buffered output tile, so one item's scan overlaps the next items' loads and the
+// previous item's stores.  Groups are dealt round-robin to the grid (CTAs_per_SM x SMs).
+// ---------------------------------------------------------------------------
+template <int COLS, int WARPS, int S, int STAGES, bool GAE>
+struct ScanPipeSmem {
+  static constexpr int SUB = 32 / COLS;
+  static constexpr int SEGS = WARPS * SUB;
+  static constexpr int CH = SEGS * S;
+  alignas(128) float r[STAGES][CH][COLS];  // TMA tiles: 128-B aligned
+  alignas(128) float v[GAE ? STAGES : 1][GAE ? CH : 1][COLS];
+  alignas(128) float o0[2][CH][COLS];
+  alignas(128) float o1[GAE ? 2 : 1][GAE ? CH : 1][COLS];
+  alignas(128) uint8_t d[STAGES][CH][COLS];
+  double sA[SEGS][COLS];
+  double sB[SEGS][COLS];
+  double carry[COLS];
+  float vnext[COLS];
+  uint64_t bar[STAGES];
+};
+
+template <int COLS, int WARPS, int S, int STAGES, bool GAE>
+__global__ void __launch_bounds__(WARPS * 32)
+k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUtensorMap tm_v,
+            const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ CUtensorMap tm_o0,
+            const __grid_constant__ CUtensorMap tm_o1, const float* __restrict__ boot, int64_t T, int64_t B,
+            double gamma, double lam, int has_o1, const float* __restrict__ vterm) {
+  using SM = ScanPipeSmem<COLS, WARPS, S, STAGES, GAE>;
+  constexpr int SUB = SM::SUB, SEGS = SM::SEGS, CH = SM::CH;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int ci = lane % COLS;
+  const int seg = w * SUB + lane / COLS;
+  const int64_t ngroups = (B + COLS - 1) / COLS;
+  const int64_t nchunks = (T + CH - 1) / CH;
+  const int64_t my_groups = ngroups > blockIdx.x ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t items = my_groups * nchunks;
+  constexpr uint32_t BYTES = (uint32_t)(CH * COLS * 4 * (GAE ? 2 : 1) + CH * COLS);
+  // item i -> (group, chunk): groups in order, chunks of a group from the last one
+  auto item_gc = [&](int64_t i, int64_t* g, int64_t* c) {
+    const int64_t k = i / nchunks;
+    *g = blockIdx.x + k * gridDim.x;
+    *c = nchunks - 1 - (i - k * nchunks);
+  };
+  auto issue = [&](int64_t i) {
+    int64_t g, c;
+    item_gc(i, &g, &c);
+    const int st = (int)(i % STAGES);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&sm.bar[st])), "r"(BYTES)
+                 : "memory");
+    const int x = (int)(g * COLS), y = (int)(c * CH);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(s_u32(&sm.r[st][0][0])), "l"(&tm_r), "r"(x), "r"(y), "r"(s_u32(&sm.bar[st])) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(s_u32(&sm.d[st][0][0])), "l"(&tm_d), "r"(x), "r"(y), "r"(s_u32(&sm.bar[st])) : "memory");
+    if (GAE)
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+          ::"r"(s_u32(&sm.v[st][0][0])), "l"(&tm_v), "r"(x), "r"(y), "r"(s_u32(&sm.bar[st])) : "memory");
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < STAGES; ++st)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_u32(&sm.bar[st])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_r) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_d) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_o0) : "memory");
+  }
+  __syncthreads();
+  pdl_wait();
+  if (threadIdx.x == 0)
+    for (int64_t i = 0; i < STAGES && i < items; ++i) issue(i);
+  const double ga = GAE ? gamma * lam : gamma;
+  uint32_t phases = 0;  // bit st: parity to wait for on stage st
+  for (int64_t i = 0; i < items; ++i) {
+    int64_t g, c;
+    item_gc(i, &g, &c);
+    const int st = (int)(i % STAGES);
+    const int ob = (int)(i & 1);
+    const int64_t col = g * COLS + ci;
+    const bool cv = col < B;
+    const double bootv = (GAE && cv) ? (double)__ldg(boot + col) : 0.0;
+    if (c == nchunks - 1 && w == 0 && lane < COLS) {  // a new group: carry = R_T (or A_T = 0), V_T
+      const int64_t cc = g * COLS + lane;
+      sm.carry[lane] = (!GAE && boot != nullptr && cc < B) ? (double)__ldg(boot + cc) : 0.0;
+      if (GAE) sm.vnext[lane] = cc < B ? __ldg(boot + cc) : 0.0f;
+    }
+    {
+      uint32_t done = 0;
+      const uint32_t ph = (phases >> st) & 1u;
+      while (!done)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done) : "r"(s_u32(&sm.bar[st])), "r"(ph) : "memory");
+      phases ^= 1u << st;
+    }
+    const int64_t t0 = c * CH + (int64_t)seg * S;
+    double b[S];
+    float vv[S];
+    float rr[S];
+    uint32_t dmask = 0, tmask = 0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      rr[k] = sm.r[st][seg * S + k][ci];
+      const uint8_t di = sm.d[st][seg * S + k][ci];
+      dmask |= (di ? 1u : 0u) << k;
+      tmask |= (di == RPL_DONE_TIMEOUT ? 1u : 0u) << k;
+      if (GAE) vv[k] = sm.v[st][seg * S + k][ci];
+    }
+    __syncthreads();  // (1) the new group's carry is visible; every thread holds its rows
+    double vseg_next = 0.0;
+    if (GAE) {
+      if (t0 + S >= T) vseg_next = bootv;
+      else if (seg + 1 < SEGS) vseg_next = (double)sm.v[st][(seg + 1) * S][ci];
+      else vseg_next = (double)sm.vnext[ci];
+    }
+    const int nvalid = cv ? (int)max((int64_t)0, min((int64_t)S, T - t0)) : 0;
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+      const double nd = ((dmask >> k) & 1u) ? 0.0 : 1.0;
+      const double tl = (vterm && ((tmask >> k) & 1u) && k < nvalid)
+                            ? gamma * (double)__ldg(vterm + (t0 + k) * B + col) : 0.0;  // R34
+      if (GAE) {
+        double vn;
+        if (k + 1 < S) vn = (k + 1 < nvalid) ? (double)vv[k + 1] : bootv;
+        else vn = vseg_next;
+        b[k] = k < nvalid ? (((double)rr[k] + gamma * nd * vn) + tl) - (double)vv[k] : 0.0;
+      } else {
+        b[k] = k < nvalid ? (double)rr[k] + tl : 0.0;
+      }
+    }
+#define RPL_A(k) ((k) < nvalid ? (((dmask >> (k)) & 1u) ? 0.0 : ga) : 1.0)
+    double A = 1.0, Bc = 0.0;
+#pragma unroll
+    for (int k = S - 1; k >= 0; --k) {
+      const double ak = RPL_A(k);
+      Bc = fma(ak, Bc, b[k]);
+      A = ak * A;
+    }
+    sm.sA[seg][ci] = A;
+    sm.sB[seg][ci] = Bc;
+    if (threadIdx.x == 0) {
+      // the output tile about to be written held item i-2's outputs: their store must have
+      // finished reading it (at most one store group, item i-1's, stays in flight)
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    }
+    __syncthreads();  // (2) maps visible; this stage is free; the output tile is free
+    if (threadIdx.x == 0 && i + STAGES < items) issue(i + STAGES);
+    double x = sm.carry[ci];
+#pragma unroll
+    for (int ss = SEGS - 1; ss > 0; --ss)
+      if (ss > seg) x = fma(sm.sA[ss][ci], x, sm.sB[ss][ci]);
+#pragma unroll
+    for (int k = S - 1; k >= 0; --k) {
+      x = fma(RPL_A(k), x, b[k]);
+      sm.o0[ob][seg * S + k][ci] = (float)x;
+      if (GAE) sm.o1[ob][seg * S + k][ci] = (float)(x + (double)vv[k]);
+    }
+#undef RPL_A
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
+    __syncthreads();  // (3) the output tile is complete; maps / carry reads done
+    if (seg == 0) {
+      sm.carry[ci] = x;
+      if (GAE) sm.vnext[ci] = vv[0];
+    }
+    if (threadIdx.x == 0) {
+      const int x0 = (int)(g * COLS), y0 = (int)(c * CH);
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                   ::"l"(&tm_o0), "r"(x0), "r"(y0), "r"(s_u32(&sm.o0[ob][0][0])) : "memory");
+      if (GAE && has_o1)
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                     ::"l"(&tm_o1), "r"(x0), "r"(y0), "r"(s_u32(&sm.o1[ob][0][0])) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
+  pdl_trigger();
+}
+
+// ---------------------------------------------------------------------------
 // Cluster variant for short horizons (T <= CL * WARPS * S, e.g. PPO's T = 128; selectable,
 // not the default — see launch_scan for the measurement): the rows
 // of a 32-column group are split over a thread-block cluster of CL CTAs along T, so each
@@ -679,7 +866,7 @@ int scan_variant() {
   if (v < 0) {
     const char* e = getenv("RPL_SCAN_VARIANT");
     int want = e ? atoi(e) : 0;
-    if (want < 0 || want > 8) want = 0;
+    if (want < 0 || want > 9) want = 0;
     int expect = -1;
     g_scan_variant.compare_exchange_strong(expect, want);
     v = g_scan_variant.load(std::memory_order_relaxed);
@@ -771,6 +958,30 @@ int launch_scan(const float* r, const float* v, const uint8_t* d, const float* b
                        ? launch_scan_cluster<16, 4, 2, GAE>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, &used, vterm)
                        : launch_scan_cluster<8, 4, 4, GAE>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, &used, vterm);
     if (used) return rc;
+  }
+  if (var == 9 && T < (1ll << 31) && B < (1ll << 31)) {
+    constexpr int COLS = 16, WARPS = 8, S = 8, STAGES = 3;
+    using SMt = ScanPipeSmem<COLS, WARPS, S, STAGES, GAE>;
+    constexpr int CH = SMt::CH;
+    CUtensorMap mr, mv, md, mo0, mo1;
+    if (tmap_2d(&mr, r, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH, COLS) &&
+        tmap_2d(&md, d, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, T, B, CH, COLS) &&
+        tmap_2d(&mo0, o0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH, COLS) &&
+        (!GAE || tmap_2d(&mv, v, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH, COLS)) &&
+        (!(GAE && o1) || tmap_2d(&mo1, o1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH, COLS))) {
+      if (!GAE) mv = mr;
+      if (!(GAE && o1)) mo1 = mo0;
+      const size_t dyn = sizeof(SMt);
+      ensure_smem(reinterpret_cast<const void*>(k_scan_pipe<COLS, WARPS, S, STAGES, GAE>), dyn);
+      const int64_t groups = (B + COLS - 1) / COLS;
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_pipe<COLS, WARPS, S, STAGES, GAE>, WARPS * 32,
+                                                    dyn);
+      int64_t grid = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
+      if (grid > groups) grid = groups;
+      return launch_pdl(k_scan_pipe<COLS, WARPS, S, STAGES, GAE>, dim3((unsigned)grid), dim3(WARPS * 32), dyn, st, mr,
+                        mv, md, mo0, mo1, boot, T, B, gamma, lam, (GAE && o1) ? 1 : 0, vterm);
+    }
   }
   if ((var == 7 || var == 8) && T < (1ll << 31) && B < (1ll << 31)) {
     CUtensorMap mr, mv, md;
@@ -868,7 +1079,7 @@ extern "C" int rpl_value_rescale(const float* x, float* y, int64_t n, double eps
 }
 
 extern "C" int rpl_debug_set_scan_variant(int32_t variant) {
-  if (variant < 0 || variant > 8) return RPL_EINVAL;
+  if (variant < 0 || variant > 9) return RPL_EINVAL;
   g_scan_variant.store(variant);
   return RPL_OK;
 }

@@ -70,6 +70,10 @@ int64_t stage_cap(const int64_t* tree) {
 }
 
 enum { MODE_TD = 0, MODE_Q = 1, MODE_MAXSEEN = 2, MODE_SEQ = 3 };
+// Header words (rpl.h): 0 max-seen, 1 sampler ticket, 2 stream position, 3-4 grid barrier,
+// 5 attached min-tree address (0: none), 6 global buffer min of the last sharded sample.
+constexpr int HDR_MINTREE = 5;
+constexpr int HDR_GLOBAL_MIN = 6;
 
 // R2D2 sequence priority (§8f NEXT-1, reading R26): column i of the time-major per-step
 // |delta| [T_p, n] -> RN32(eta * max + (1 - eta) * RN64(exact sum) / T_p).  The sum is the
@@ -251,6 +255,7 @@ __device__ __forceinline__ void tree_update_block(UpdSmem& S, const TreeDev& L, 
   }
   if (single && pre_leaf >= 0 && pre_leaf < L.n_leaves) pre_old = __ldcg(leaves + pre_leaf);
   const int64_t maxseen_now = __ldcg(hdr);
+  int64_t* mins = reinterpret_cast<int64_t*>(__ldcg(hdr + HDR_MINTREE));  // attached min-tree (R29) or NULL
   int64_t local_max = INT64_MIN;
   int32_t errbits = 0;
 
@@ -351,6 +356,57 @@ __device__ __forceinline__ void tree_update_block(UpdSmem& S, const TreeDev& L, 
     if (tid == 0 && m > maxseen_now) atomicMax(reinterpret_cast<long long*>(hdr), (long long)m);
   }
   if (errbits) set_err(err, errbits);
+  // Min-tree maintenance (buffer-wide IS normaliser, R29): every internal min node on a
+  // written leaf's path is recomputed from its W children, level by level from the leaves'
+  // parents up (a barrier between levels), each distinct node by one thread (hash dedupe per
+  // chunk of NT entries).  A leaf's min contribution is its q when q > 0; an internal node
+  // holds the min of its children (INT64_MAX: no positive leaf below).
+  if (mins) {
+    __syncthreads();
+    for (int l = L.depth - 1; l >= 0; --l) {
+      const int sh = L.log2w * (L.depth - l);
+      for (int64_t base = 0; base < n; base += NT) {
+        for (int s2 = tid; s2 < HASH_SLOTS; s2 += NT) hkey[s2] = HASH_EMPTY;
+        __syncthreads();
+        int64_t p = -1;
+        if (base + tid < n) {
+          const int64_t leaf = idx[base + tid];
+          if (leaf >= 0 && leaf < L.n_leaves) p = leaf >> sh;
+        }
+        bool own = false;
+        if (p >= 0) {
+          uint32_t slot = hash_slot(p);
+          while (true) {
+            const unsigned long long prev = atomicCAS(&hkey[slot], HASH_EMPTY, (unsigned long long)p);
+            if (prev == HASH_EMPTY) {
+              own = true;
+              break;
+            }
+            if (prev == (unsigned long long)p) break;
+            slot = (slot + 1) & (HASH_SLOTS - 1);
+          }
+        }
+        if (own) {
+          const int64_t c0 = p << L.log2w;
+          int64_t m2 = INT64_MAX;
+          if (l == L.depth - 1) {
+            for (int j = 0; j < L.fanout; ++j) {
+              const int64_t v = __ldcg(leaves + c0 + j);
+              if (v > 0 && v < m2) m2 = v;
+            }
+          } else {
+            const int64_t* ch = mins + L.level_off[l + 1] + c0;
+            for (int j = 0; j < L.fanout; ++j) {
+              const int64_t v = __ldcg(ch + j);
+              if (v < m2) m2 = v;
+            }
+          }
+          mins[L.level_off[l] + p] = m2;
+        }
+        __syncthreads();
+      }
+    }
+  }
 }
 
 __global__ void __launch_bounds__(UPD_THREADS)
@@ -439,7 +495,7 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
               int64_t* __restrict__ out_q, int64_t* __restrict__ out_qmin, float* __restrict__ out_w,
               int32_t* err, int rank, int n_shards, int64_t shard_leaves,
               const int64_t* __restrict__ totals, int use_stream, int64_t* __restrict__ out_count,
-              int64_t* const* boards, int64_t stage_cap) {
+              int64_t* const* boards, int64_t stage_cap, int tot_stride, int64_t* __restrict__ out_bufmin) {
   const int lane = threadIdx.x & 31;
   if (RPL_PDL_EARLY & 2) pdl_trigger();  // A/B knob (common.cuh)
   pdl_wait();
@@ -489,25 +545,48 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
     // rank's board, every CTA reads all totals from its own board; tag = stream position
     // after this step (identical on every rank)
     const uint64_t tag = spos + (uint64_t)n;
-    if (blockIdx.x == 0 && threadIdx.x < n_shards)
+    // with the shard's buffer min (root of its attached min-tree, INT64_MAX without one) in
+    // the board's third section, so a buffer-wide normaliser needs no second exchange (R29)
+    const int64_t* mt = reinterpret_cast<const int64_t*>(__ldcg(tree + L.hdr_off + HDR_MINTREE));
+    if (blockIdx.x == 0 && threadIdx.x < n_shards) {
       board_publish(boards[threadIdx.x] + 2 * rank, __ldcg(tree + L.level_off[0]), tag);
+      board_publish(boards[threadIdx.x] + 4 * n_shards + 2 * rank, mt ? __ldcg(mt) : INT64_MAX, tag);
+    }
     if (threadIdx.x < n_shards) {
       int64_t v = 0;
       if (!board_wait(boards[rank] + 2 * threadIdx.x, tag, &v)) board_fail(err);
       s_tot[threadIdx.x] = v;
+    }
+    if (mt && blockIdx.x == 0 && threadIdx.x < 32) {  // global buffer min -> header word 6
+      int64_t v = INT64_MAX;
+      if (lane < n_shards && !board_wait(boards[rank] + 4 * n_shards + 2 * lane, tag, &v)) board_fail(err);
+      v = warp_min64(v);
+      if (lane == 0) tree[L.hdr_off + HDR_GLOBAL_MIN] = v;
     }
     __syncthreads();
   }
   if (SHARDED) {
     Q = 0;
     for (int g = 0; g < n_shards; ++g) {
-      const uint64_t tg = (uint64_t)(boards ? s_tot[g] : totals[g]);
+      const uint64_t tg = (uint64_t)(boards ? s_tot[g] : totals[(int64_t)g * tot_stride]);
       if (g < rank) own_lo += tg;
       if (g == rank) own_T = tg;
       Q += tg;
     }
   } else {
     Q = (uint64_t)(n_top > 0 ? s_top[0] : tree[L.level_off[0]]);
+  }
+  if (SHARDED && out_bufmin && blockIdx.x == 0 && threadIdx.x < 32) {  // {total, min} pairs: global min
+    int64_t v = INT64_MAX;
+    for (int g = lane; g < n_shards; g += 32) {
+      const int64_t x = totals[(int64_t)g * tot_stride + 1];
+      v = x < v ? x : v;
+    }
+    v = warp_min64(v);
+    if (lane == 0) {
+      *out_bufmin = v;
+      tree[L.hdr_off + HDR_GLOBAL_MIN] = v;
+    }
   }
   // compacted sharded output: the owned run of strata [k0, k1) goes to positions
   // 0 .. m-1 (stratum order), positions m .. n-1 get -1; *out_count = m
@@ -814,6 +893,44 @@ __global__ void k_tree_total(const int64_t* __restrict__ tree, int64_t* __restri
   *out = tree[0];
 }
 
+// {total, buffer min}: the root sum and the root of the attached min-tree (INT64_MAX without)
+__global__ void k_tree_total_min(const int64_t* __restrict__ tree, int64_t hdr_off, int64_t* __restrict__ out) {
+  pdl_wait();
+  const int64_t* mt = reinterpret_cast<const int64_t*>(tree[hdr_off + HDR_MINTREE]);
+  out[0] = tree[0];
+  out[1] = mt ? mt[0] : INT64_MAX;
+}
+
+__global__ void k_set_word(int64_t* __restrict__ w, int64_t v) {
+  pdl_wait();
+  *w = v;
+}
+
+// Min-tree level l from level l+1 (or the leaves), one warp per node: min over the W
+// children of the positive leaves / the child mins; padding nodes get INT64_MAX.  A no-op
+// when no min-tree is attached (header word 5 == 0), so callers need not know.
+__global__ void k_mintree_level(TreeDev L, const int64_t* __restrict__ tree, int l, int64_t len, int64_t clen) {
+  pdl_wait();
+  int64_t* mins = reinterpret_cast<int64_t*>(__ldcg(tree + L.hdr_off + HDR_MINTREE));
+  if (!mins) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t node = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); node < len; node += warps) {
+    int64_t v = INT64_MAX;
+    const int64_t c = (node << L.log2w) + lane;
+    if (lane < L.fanout && c < clen) {  // children of padding nodes may lie past the child level
+      if (l == L.depth - 1) {
+        const int64_t x = __ldcg(tree + L.level_off[L.depth] + c);
+        v = x > 0 ? x : INT64_MAX;
+      } else {
+        v = __ldcg(mins + L.level_off[l + 1] + c);
+      }
+    }
+    v = warp_min64(v);
+    if (lane == 0) mins[L.level_off[l] + node] = v;
+  }
+}
+
 __global__ void k_tree_level(TreeDev L, int64_t* __restrict__ tree, int l, int64_t len, int64_t real) {
   // node j of level l := sum of its W children on level l+1 (real nodes); padding nodes := 0.
   // A real node's children lie inside level l+1 (len(l+1) = real(l) * W), a padding
@@ -964,7 +1081,8 @@ extern "C" int rpl_sumtree_sample(const rpl_tree_layout* L, int64_t* tree, int64
   const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
   return launch_pdl(k_tree_sample<false>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
                     tree_dev(L), tree, n, draws, seed, offset, beta, out_idx, out_q, out_qmin, out_w, dev_err, 0, 1,
-                    (int64_t)0, (const int64_t*)nullptr, 0, (int64_t*)nullptr, (int64_t* const*)nullptr, stage_cap(tree));
+                    (int64_t)0, (const int64_t*)nullptr, 0, (int64_t*)nullptr, (int64_t* const*)nullptr, stage_cap(tree),
+                    1, (int64_t*)nullptr);
 }
 
 extern "C" int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree, int64_t n, uint64_t seed,
@@ -976,7 +1094,7 @@ extern "C" int rpl_sumtree_sample_stream(const rpl_tree_layout* L, int64_t* tree
   return launch_pdl(k_tree_sample<false>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
                     tree_dev(L), tree, n, (const uint64_t*)nullptr, seed, (uint64_t)0, beta, out_idx, out_q, out_qmin,
                     out_w, dev_err, 0, 1, (int64_t)0, (const int64_t*)nullptr, 1, (int64_t*)nullptr,
-                    (int64_t* const*)nullptr, stage_cap(tree));
+                    (int64_t* const*)nullptr, stage_cap(tree), 1, (int64_t*)nullptr);
 }
 
 extern "C" int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tree, int32_t rank, int32_t n_shards,
@@ -991,7 +1109,7 @@ extern "C" int rpl_sumtree_sample_sharded(const rpl_tree_layout* L, int64_t* tre
   return launch_pdl(k_tree_sample<true>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
                     tree_dev(L), tree, n, draws, seed, offset, 0.0, out_idx, out_q, out_qmin, (float*)nullptr, dev_err,
                     (int)rank, (int)n_shards, shard_leaves, shard_totals, (int)use_stream, out_count,
-                    (int64_t* const*)nullptr, stage_cap(tree));
+                    (int64_t* const*)nullptr, stage_cap(tree), 1, (int64_t*)nullptr);
 }
 
 extern "C" int rpl_sumtree_sample_sharded_p2p(const rpl_tree_layout* L, int64_t* tree, int32_t rank,
@@ -1006,7 +1124,7 @@ extern "C" int rpl_sumtree_sample_sharded_p2p(const rpl_tree_layout* L, int64_t*
   return launch_pdl(k_tree_sample<true>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
                     tree_dev(L), tree, n, (const uint64_t*)nullptr, seed, (uint64_t)0, 0.0, out_idx, out_q,
                     (int64_t*)nullptr, (float*)nullptr, dev_err, (int)rank, (int)n_shards, shard_leaves,
-                    (const int64_t*)nullptr, 1, out_count, boards, stage_cap(tree));
+                    (const int64_t*)nullptr, 1, out_count, boards, stage_cap(tree), 1, (int64_t*)nullptr);
 }
 
 extern "C" int rpl_sumtree_find(const rpl_tree_layout* L, const int64_t* tree, const int64_t* prefix, int64_t n,
@@ -1024,6 +1142,48 @@ extern "C" int rpl_sumtree_total(const rpl_tree_layout* L, const int64_t* tree, 
   return launch_pdl(k_tree_total, dim3(1), dim3(1), 0, as_stream(stream), tree, out_total);
 }
 
+extern "C" int rpl_mintree_rebuild(const rpl_tree_layout* L, const int64_t* tree, void* stream) {
+  if (!layout_ok(L) || !tree) return RPL_EINVAL;
+  TreeDev T = tree_dev(L);
+  for (int l = L->depth - 1; l >= 0; --l) {
+    const int64_t len = L->level_len[l];
+    int64_t blocks = (len + 7) / 8;  // 8 warps per CTA
+    if (blocks > 8 * (int64_t)sm_count()) blocks = 8 * (int64_t)sm_count();
+    const int s = launch_pdl(k_mintree_level, dim3((unsigned)blocks), dim3(256), 0, as_stream(stream), T, tree, l, len,
+                             (int64_t)L->level_len[l + 1]);
+    if (s != RPL_OK) return s;
+  }
+  return RPL_OK;
+}
+
+extern "C" int rpl_mintree_attach(const rpl_tree_layout* L, int64_t* tree, int64_t* mins, void* stream) {
+  if (!layout_ok(L) || !tree) return RPL_EINVAL;
+  const int s = launch_pdl(k_set_word, dim3(1), dim3(1), 0, as_stream(stream), tree + L->hdr_off + HDR_MINTREE,
+                           (int64_t) reinterpret_cast<uintptr_t>(mins));
+  if (s != RPL_OK || !mins) return s;
+  return rpl_mintree_rebuild(L, tree, stream);
+}
+
+extern "C" int rpl_sumtree_total_min(const rpl_tree_layout* L, const int64_t* tree, int64_t* out, void* stream) {
+  if (!layout_ok(L) || !tree || !out) return RPL_EINVAL;
+  return launch_pdl(k_tree_total_min, dim3(1), dim3(1), 0, as_stream(stream), tree, L->hdr_off, out);
+}
+
+extern "C" int rpl_sumtree_sample_sharded_pairs(const rpl_tree_layout* L, int64_t* tree, int32_t rank,
+                                                int32_t n_shards, int64_t shard_leaves, const int64_t* shard_pairs,
+                                                int64_t n, uint64_t seed, int64_t* out_idx, int64_t* out_q,
+                                                int64_t* out_qmin, int64_t* out_count, int64_t* out_bufmin,
+                                                int32_t* dev_err, void* stream) {
+  if (!layout_ok(L) || !tree || !out_idx || !out_q || !shard_pairs || !out_count || n < 1 || n > (1ll << 30))
+    return RPL_EINVAL;
+  if (n_shards < 1 || rank < 0 || rank >= n_shards || shard_leaves < L->n_leaves) return RPL_EINVAL;
+  const int64_t blocks = (n + SAMPLE_WARPS - 1) / SAMPLE_WARPS;
+  return launch_pdl(k_tree_sample<true>, dim3((unsigned)blocks), dim3(SAMPLE_WARPS * 32), 0, as_stream(stream),
+                    tree_dev(L), tree, n, (const uint64_t*)nullptr, seed, (uint64_t)0, 0.0, out_idx, out_q, out_qmin,
+                    (float*)nullptr, dev_err, (int)rank, (int)n_shards, shard_leaves, shard_pairs, 1, out_count,
+                    (int64_t* const*)nullptr, stage_cap(tree), 2, out_bufmin);
+}
+
 extern "C" int rpl_sumtree_rebuild(const rpl_tree_layout* L, int64_t* tree, void* stream) {
   if (!layout_ok(L) || !tree) return RPL_EINVAL;
   TreeDev T = tree_dev(L);
@@ -1036,7 +1196,7 @@ extern "C" int rpl_sumtree_rebuild(const rpl_tree_layout* L, int64_t* tree, void
     int s = launch_status();
     if (s != RPL_OK) return s;
   }
-  return RPL_OK;
+  return rpl_mintree_rebuild(L, tree, stream);  // the attached min-tree too (no-op without one)
 }
 
 extern "C" int rpl_is_weights(const int64_t* q, const int64_t* qmin, int64_t n, double beta, float* w,

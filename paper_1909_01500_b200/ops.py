@@ -208,6 +208,7 @@ class SumTree:
         self.storage = torch.empty(int(L.n_words), dtype=torch.int64, device=self.device)
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._lp = C.byref(self.layout)
+        self.mins = None  # attached min-tree (rpl_mintree_attach)
         self.init()
 
     # views
@@ -230,6 +231,7 @@ class SumTree:
 
     def init(self):
         check(lib.rpl_sumtree_init(self._lp, _ptr(self.storage), self._s()), "rpl_sumtree_init")
+        self.mins = None  # init clears the header: any min-tree is detached
 
     def update(self, idx, td_abs, alpha, eps_p=1e-3, err=None, live_only=False):
         _req(idx, torch.int64, "idx")
@@ -399,6 +401,50 @@ class SumTree:
                                             _ptr(e), self._s()), "rpl_sumtree_sample_unique")
         return idx, q
 
+    def attach_min_tree(self):
+        """rpl_mintree_attach: keep a min-tree beside the sum tree (buffer-wide IS normaliser,
+        R29); `min_root` (a 1-element view) is then the buffer min after every update."""
+        self.mins = torch.empty(int(self.layout.level_off[self.depth]), dtype=torch.int64, device=self.device)
+        check(lib.rpl_mintree_attach(self._lp, _ptr(self.storage), _ptr(self.mins), self._s()), "rpl_mintree_attach")
+        return self.mins
+
+    def detach_min_tree(self):
+        check(lib.rpl_mintree_attach(self._lp, _ptr(self.storage), None, self._s()), "rpl_mintree_attach")
+        self.mins = None
+
+    @property
+    def min_root(self):
+        return None if self.mins is None else self.mins[:1]
+
+    def min_level(self, l: int) -> torch.Tensor:
+        off, ln = int(self.layout.level_off[l]), int(self.layout.level_len[l])
+        return self.mins[off:off + ln]
+
+    def total_min(self, out=None):
+        """rpl_sumtree_total_min: [total, buffer min] (the K5 record with the normaliser)."""
+        out = torch.empty(2, dtype=torch.int64, device=self.device) if out is None else out
+        check(lib.rpl_sumtree_total_min(self._lp, _ptr(self.storage), _ptr(out), self._s()), "rpl_sumtree_total_min")
+        return out
+
+    def sample_sharded_pairs(self, rank, n_shards, pairs, n, seed, count, out=None, bufmin=None, err=None):
+        """rpl_sumtree_sample_sharded_pairs: pairs = all-gathered [n_shards, 2] {total, min}."""
+        n = int(n)
+        _req(pairs, torch.int64, "pairs", (n_shards, 2))
+        _req(count, torch.int64, "count", (2,))
+        if out is None:
+            idx = torch.empty(n, dtype=torch.int64, device=self.device)
+            q = torch.empty(n, dtype=torch.int64, device=self.device)
+            qmin = torch.empty(1, dtype=torch.int64, device=self.device)
+        else:
+            idx, q, qmin = out
+        bufmin = torch.empty(1, dtype=torch.int64, device=self.device) if bufmin is None else bufmin
+        e = self.err if err is None else err
+        check(lib.rpl_sumtree_sample_sharded_pairs(self._lp, _ptr(self.storage), int(rank), int(n_shards),
+                                                   int(self.n_leaves), _ptr(pairs), n, int(seed) & (2 ** 64 - 1),
+                                                   _ptr(idx), _ptr(q), _ptr(qmin), _ptr(count), _ptr(bufmin), _ptr(e),
+                                                   self._s()), "rpl_sumtree_sample_sharded_pairs")
+        return idx, q, qmin, bufmin
+
     def min_q(self, out=None):
         """rpl_sumtree_min: buffer-wide min q over non-zero leaves (NEXT-4 IS normaliser)."""
         out = torch.empty(1, dtype=torch.int64, device=self.device) if out is None else out
@@ -421,6 +467,9 @@ class SumTree:
         self.storage.zero_()
         self.leaves.copy_(sd["leaves"].to(self.device))
         self.header.copy_(sd["header"].to(self.device))
+        # header word 5 is a device address: keep this object's own min-tree attachment
+        self.header[5] = 0 if self.mins is None else self.mins.data_ptr()
+        self.header[6] = 0
         self.rebuild()
 
 

@@ -150,7 +150,7 @@ class CentralBatch:
 
 
 class PeerBoards:
-    """The exchange boards of rpl.h (RPL_BOARD_WORDS = 4 * world int64 words per rank):
+    """The exchange boards of rpl.h (RPL_BOARD_WORDS = 6 * world int64 words per rank):
     this rank's board is allocated here, zeroed, exported through CUDA IPC and mapped by
     every peer (all_gather_object of the IPC handles; NVLink P2P between GPUs, plain device
     memory on a shared GPU).  `ptrs` is the device int64 [world] array of board addresses
@@ -162,7 +162,7 @@ class PeerBoards:
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.board = torch.zeros(4 * self.world, dtype=torch.int64, device=dev)
+        self.board = torch.zeros(6 * self.world, dtype=torch.int64, device=dev)
         torch.cuda.synchronize(dev)
         handles = [None] * self.world
         dist.all_gather_object(handles, reduce_tensor(self.board), group=group)
@@ -200,5 +200,5 @@ class PeerBoards:
     @staticmethod
     def local(boards):
         """In-process boards for G 'ranks' sharing one process (tests): boards is a list of
-        device int64 tensors of 4*G words; returns the shared pointer array."""
+        device int64 tensors of 6*G words; returns the shared pointer array."""
         return torch.tensor([b.data_ptr() for b in boards], dtype=torch.int64, device=boards[0].device)

@@ -49,7 +49,7 @@ def test_p2p_sampler_equals_oracle(rpl, G, empty):
     from paper_1909_01500_b200.shard import PeerBoards
     n_local, n, seed = 3000, 96, 7
     trees, orcs = _shards(rpl, G, n_local, 40 + G, empty)
-    boards = [torch.zeros(4 * G, dtype=torch.int64, device="cuda") for _ in range(G)]
+    boards = [torch.zeros(6 * G, dtype=torch.int64, device="cuda") for _ in range(G)]
     ptrs = PeerBoards.local(boards)
     streams = [torch.cuda.Stream() for _ in range(G)]
     errs = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(G)]
@@ -98,7 +98,7 @@ def test_p2p_gather_weights(rpl, empty):
             t.update(T_(valid), T_(td_abs(rng(r), valid.size)), 0.9)
         rings.append(ring)
         trees.append(t)
-    boards = [torch.zeros(4 * G, dtype=torch.int64, device=dev) for _ in range(G)]
+    boards = [torch.zeros(6 * G, dtype=torch.int64, device=dev) for _ in range(G)]
     ptrs = PeerBoards.local(boards)
     streams = [torch.cuda.Stream() for _ in range(G)]
     errs = [torch.zeros(1, dtype=torch.int32, device=dev) for _ in range(G)]
@@ -140,7 +140,7 @@ def test_p2p_gather_weights(rpl, empty):
                     a, b_ = a[:, :m], b_[:, :m]
                 assert np.array_equal(a, b_), (step, r, name)
             b = H(boards[r])
-            assert b[2 * G::2].tolist() == mins
+            assert b[2 * G:4 * G:2].tolist() == mins
 
 
 def test_p2p_timeout_fails_loudly(cuda):
@@ -190,7 +190,7 @@ def test_p2p_prefilled_peer(rpl):
     peer = OS.SumTreeOracle(t.n_leaves)  # rank 1: a copy of rank 0's shard
     peer.q = list(o.q)
     tag = n * G                           # stream position after the first step
-    board = torch.zeros(4 * G, dtype=torch.int64, device=dev)
+    board = torch.zeros(6 * G, dtype=torch.int64, device=dev)
     board[2 * 1], board[2 * 1 + 1] = peer.total(), tag           # rank 1's K5 slot
     ptrs = torch.tensor([board.data_ptr(), board.data_ptr()], dtype=torch.int64, device=dev)
     cnt = torch.zeros(2, dtype=torch.int64, device=dev)

@@ -8,6 +8,7 @@ import os
 import numpy as np
 import pytest
 
+from oracle import gather as OG
 from oracle import philox as OP
 from oracle import priority as OPR
 from oracle import sumtree as OS
@@ -664,3 +665,159 @@ def test_update_seq_exact_sum_order_independent(rpl):
     orc2 = OS.SumTreeOracle(N, 20)
     orc2.update([int(x) for x in idx], [OPR.sequence_td(steps2[:, k], 0.9) for k in range(n)], 0.9, 1e-3)
     check_tree_consistent(t2, orc2)
+
+
+def _oracle_min_levels(tree, q):
+    """Every internal node of the min-tree by its definition: min over the positive leaves of
+    the node's range (INT64_MAX when none), padding nodes included (R29)."""
+    MAX = (1 << 63) - 1
+    out = []
+    W, D, N = tree.fanout, tree.depth, tree.n_leaves
+    for l in range(D):
+        span = W ** (D - l)
+        ln = int(tree.layout.level_len[l])
+        lvl = []
+        for j in range(ln):
+            lo, hi = j * span, min((j + 1) * span, N)
+            lvl.append(OS.buffer_min(q[lo:hi]) if lo < N else MAX)
+        out.append(lvl)
+    return out
+
+
+def _check_min_tree(t, orc):
+    ref = _oracle_min_levels(t, orc.q)
+    for l in range(t.depth):
+        assert [int(x) for x in H(t.min_level(l))] == ref[l], l
+    assert int(H(t.min_root)[0]) == OS.buffer_min(orc.q)
+
+
+@pytest.mark.parametrize("N,W", [(25600, 32), (3000, 4), (1, 32), (100, 2)])
+def test_min_tree_maintained_by_every_writer(rpl, N, W):
+    # NEXT-4 / R29: the min-tree beside the sum tree stays exact through update, duplicate-heavy
+    # update, update_seq, set_q (explicit zeros = invalidated leaves, max-seen), the fused
+    # update+sample, replay validity and rebuild; the root is the buffer-wide normaliser
+    import torch
+    g = rng(N + W)
+    t = rpl.SumTree(N, W)
+    orc = OS.SumTreeOracle(N)
+    t.attach_min_tree()
+    _check_min_tree(t, orc)                              # empty tree: every node INT64_MAX
+    idx = g.integers(0, N, 3 * N // 2 + 1).astype(np.int64)
+    td = td_abs(g, idx.size)
+    t.update(T_(idx), T_(td), 0.6)
+    orc.update([int(x) for x in idx], [float(x) for x in td], 0.6)
+    _check_min_tree(t, orc)
+    for _ in range(3):
+        n = int(g.integers(1, 700))
+        idx = g.integers(0, N, n).astype(np.int64)
+        idx[::3] = idx[0]                                # duplicates: the last one wins
+        td = (td_abs(g, n) * 10.0 ** g.uniform(-3, 3, n)).astype(np.float32)
+        t.update(T_(idx), T_(td), 0.6)
+        orc.update([int(x) for x in idx], [float(x) for x in td], 0.6)
+        _check_min_tree(t, orc)
+        z = g.integers(0, N, max(1, N // 10)).astype(np.int64)   # invalidate: q := 0
+        t.set_q(T_(z), T_(np.zeros(z.size, np.int64)))
+        orc.set_q([int(x) for x in z], [0] * z.size)
+        _check_min_tree(t, orc)
+        t.set_q(T_(z[: z.size // 2]))                    # re-validate at max-seen
+        orc.set_q([int(x) for x in z[: z.size // 2]])
+        _check_min_tree(t, orc)
+    steps = np.abs(g.normal(size=(16, 40))).astype(np.float32)
+    sidx = g.integers(0, N, 40).astype(np.int64)
+    t.update_seq(T_(sidx), T_(steps), 0.9, eta=0.9)
+    orc.update([int(x) for x in sidx], [OPR.sequence_td(steps[:, k], 0.9) for k in range(40)], 0.9)
+    _check_min_tree(t, orc)
+    fi = g.integers(0, N, 32).astype(np.int64)
+    ftd = td_abs(g, 32)
+    t.update_sample(64, 9, idx=T_(fi), td=T_(ftd), alpha=0.6)
+    orc.update([int(x) for x in fi], [float(x) for x in ftd], 0.6)
+    torch.cuda.synchronize()
+    _check_min_tree(t, orc)
+    # a corrupted min-tree is restored by rebuild (resume path)
+    t.mins.fill_(5)
+    t.rebuild()
+    _check_min_tree(t, orc)
+
+
+def test_min_tree_validity_and_buffer_weights(rpl):
+    # appends change leaf validity (rpl_replay_validity): the min-tree follows; IS weights
+    # normalised by its root equal the PER buffer-wide formula (N P_i)^-beta / max_j
+    import torch
+    cap, B, k, n_step = 64, 16, 4, 3
+    N = cap * B
+    t = rpl.SumTree(N, 32)
+    orc = OS.SumTreeOracle(N)
+    t.attach_min_tree()
+    g = rng(99)
+    for c_old, s_old, c_new, s_new in [(0, 0, 20, 20), (20, 20, 50, 50), (50, 50, 10, 64), (10, 64, 40, 64)]:
+        t.validity("transition", cap, B, k, c_old, s_old, c_new, s_new, n_step=n_step)
+        for row in range(cap):
+            v0 = OG.window_valid_transition(row, cap, c_old, s_old, k, n_step) if s_old else False
+            v1 = OG.window_valid_transition(row, cap, c_new, s_new, k, n_step) if s_new else False
+            if v0 != v1:
+                leaves = [row * B + b for b in range(B)]
+                if v1:
+                    orc.set_q(leaves)
+                else:
+                    orc.set_q(leaves, [0] * B)
+        _check_min_tree(t, orc)
+        live = [i for i, x in enumerate(orc.q) if x > 0]
+        if live:  # fresh priorities on the live leaves, then buffer-normalised weights
+            pick = np.array(g.choice(live, min(200, len(live)), replace=False), np.int64)
+            td = td_abs(g, pick.size)
+            t.update(T_(pick), T_(td), 0.6)
+            orc.update([int(x) for x in pick], [float(x) for x in td], 0.6)
+            _check_min_tree(t, orc)
+            qs = [orc.q[int(i)] for i in pick[:50]]
+            w = rpl.is_weights(T_(np.array(qs, np.int64)), t.min_root, 0.4)
+            Q, qmin = orc.total(), OS.buffer_min(orc.q)
+            ref = [((N * qi / Q) ** -0.4) / ((N * qmin / Q) ** -0.4) for qi in qs]
+            check_rel(H(w), ref, what="buffer-normalised w")
+
+
+def test_min_tree_sharded_exchanges(rpl):
+    # the buffer min travels with the K5 total: (a) peer boards (header word 6 of every rank's
+    # tree), (b) the {total, min} all-gather record and rpl_sumtree_sample_sharded_pairs; the
+    # global min equals the oracle's over all shards and the sample equals the concatenated one
+    import torch
+    from paper_1909_01500_b200.shard import PeerBoards
+    G, n_local, n, seed = 3, 2000, 48, 11
+    g = rng(123)
+    trees, orcs = [], []
+    for r in range(G):
+        t = rpl.SumTree(n_local, 32)
+        t.attach_min_tree()
+        o = OS.SumTreeOracle(n_local)
+        idx = g.integers(0, n_local, 1500).astype(np.int64)
+        td = (td_abs(g, 1500) * (1 + 3 * r)).astype(np.float32)
+        t.update(T_(idx), T_(td), 0.9)
+        o.update([int(x) for x in idx], [float(x) for x in td], 0.9)
+        trees.append(t)
+        orcs.append(o)
+    gmin = min(OS.buffer_min(o.q) for o in orcs)
+    # (a) peer boards, all ranks' samplers concurrently on their own streams
+    boards = [torch.zeros(6 * G, dtype=torch.int64, device="cuda") for _ in range(G)]
+    ptrs = PeerBoards.local(boards)
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    counts = [torch.zeros(2, dtype=torch.int64, device="cuda") for _ in range(G)]
+    torch.cuda.synchronize()
+    for r in range(G):
+        with torch.cuda.stream(streams[r]):
+            trees[r].sample_sharded_p2p(r, G, ptrs, n, seed, counts[r])
+    torch.cuda.synchronize()
+    for r in range(G):
+        assert int(H(trees[r].header)[6]) == gmin
+        assert H(boards[r])[4 * G::2].tolist() == [OS.buffer_min(o.q) for o in orcs]
+    # (b) the all-gathered {total, min} record (here: concatenated on one device)
+    pairs = torch.cat([t.total_min() for t in trees]).view(G, 2)
+    assert H(pairs).tolist() == [[o.total(), OS.buffer_min(o.q)] for o in orcs]
+    ref_idx, ref_q, _ = OS.sharded_sample(orcs, n, OP.draws_u64(seed, n, n))  # stream position n after (a)
+    got = []
+    for r in range(G):
+        cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
+        idx, q, _, bm = trees[r].sample_sharded_pairs(r, G, pairs, n, seed, cnt)
+        torch.cuda.synchronize()
+        m = int(H(cnt)[0])
+        got += (H(idx)[:m] + r * n_local).tolist()
+        assert int(H(bm)[0]) == gmin and int(H(trees[r].header)[6]) == gmin
+    assert got == ref_idx
