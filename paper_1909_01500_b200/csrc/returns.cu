@@ -444,7 +444,7 @@ struct ScanPipeSmem {
 };
 
 template <int COLS, int WARPS, int S, int STAGES, bool GAE>
-__global__ void __launch_bounds__(WARPS * 32)
+__global__ void __launch_bounds__(WARPS * 32, 2)
 k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUtensorMap tm_v,
             const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ CUtensorMap tm_o0,
             const __grid_constant__ CUtensorMap tm_o1, const float* __restrict__ boot, int64_t T, int64_t B,
@@ -462,16 +462,19 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
   const int64_t my_groups = ngroups > blockIdx.x ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int64_t items = my_groups * nchunks;
   constexpr uint32_t BYTES = (uint32_t)(CH * COLS * 4 * (GAE ? 2 : 1) + CH * COLS);
-  // item i -> (group, chunk): groups in order, chunks of a group from the last one
-  auto item_gc = [&](int64_t i, int64_t* g, int64_t* c) {
-    const int64_t k = i / nchunks;
-    *g = blockIdx.x + k * gridDim.x;
-    *c = nchunks - 1 - (i - k * nchunks);
-  };
-  auto issue = [&](int64_t i) {
-    int64_t g, c;
-    item_gc(i, &g, &c);
-    const int st = (int)(i % STAGES);
+  // items in order: groups blockIdx.x, +gridDim.x, ...; chunks of a group from the last one.
+  // Cursors advance incrementally (no 64-bit division per item): (gp, cp, sp) = the next item
+  // to load (thread 0 only), (g, c) = the item being scanned.
+  int64_t gp = blockIdx.x, cp = nchunks - 1;
+  int sp = 0;
+  auto issue = [&]() {
+    const int64_t g = gp, c = cp;
+    const int st = sp;
+    if (--cp < 0) {
+      cp = nchunks - 1;
+      gp += gridDim.x;
+    }
+    if (++sp == STAGES) sp = 0;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&sm.bar[st])), "r"(BYTES)
                  : "memory");
     const int x = (int)(g * COLS), y = (int)(c * CH);
@@ -497,13 +500,12 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
   __syncthreads();
   pdl_wait();
   if (threadIdx.x == 0)
-    for (int64_t i = 0; i < STAGES && i < items; ++i) issue(i);
+    for (int64_t i = 0; i < STAGES && i < items; ++i) issue();
   const double ga = GAE ? gamma * lam : gamma;
   uint32_t phases = 0;  // bit st: parity to wait for on stage st
+  int64_t g = blockIdx.x, c = nchunks - 1;
+  int st = 0;
   for (int64_t i = 0; i < items; ++i) {
-    int64_t g, c;
-    item_gc(i, &g, &c);
-    const int st = (int)(i % STAGES);
     const int ob = (int)(i & 1);
     const int64_t col = g * COLS + ci;
     const bool cv = col < B;
@@ -543,27 +545,49 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
       else vseg_next = (double)sm.vnext[ci];
     }
     const int nvalid = cv ? (int)max((int64_t)0, min((int64_t)S, T - t0)) : 0;
+    // fast path (every row valid, no time limits): no per-element predicates or selects
+    // beyond the done bit; the common case of every chunk but a ragged last one
+    const bool fast = nvalid == S && vterm == nullptr;
+    double a[S];
+    if (fast) {
+      double vd[GAE ? S : 1];
 #pragma unroll
-    for (int k = 0; k < S; ++k) {
-      const double nd = ((dmask >> k) & 1u) ? 0.0 : 1.0;
-      const double tl = (vterm && ((tmask >> k) & 1u) && k < nvalid)
-                            ? gamma * (double)__ldg(vterm + (t0 + k) * B + col) : 0.0;  // R34
-      if (GAE) {
-        double vn;
-        if (k + 1 < S) vn = (k + 1 < nvalid) ? (double)vv[k + 1] : bootv;
-        else vn = vseg_next;
-        b[k] = k < nvalid ? (((double)rr[k] + gamma * nd * vn) + tl) - (double)vv[k] : 0.0;
-      } else {
-        b[k] = k < nvalid ? (double)rr[k] + tl : 0.0;
+      for (int k = 0; k < S; ++k) {
+        if (GAE) vd[k] = (double)vv[k];
+        a[k] = ((dmask >> k) & 1u) ? 0.0 : ga;
+      }
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        if (GAE) {
+          const double gn = ((dmask >> k) & 1u) ? 0.0 : gamma;
+          const double vn = k + 1 < S ? vd[(k + 1) % S] : vseg_next;
+          b[k] = fma(gn, vn, (double)rr[k]) - vd[k];
+        } else {
+          b[k] = (double)rr[k];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < S; ++k) {
+        const double nd = ((dmask >> k) & 1u) ? 0.0 : 1.0;
+        const double tl = (vterm && ((tmask >> k) & 1u) && k < nvalid)
+                              ? gamma * (double)__ldg(vterm + (t0 + k) * B + col) : 0.0;  // R34
+        if (GAE) {
+          double vn;
+          if (k + 1 < S) vn = (k + 1 < nvalid) ? (double)vv[k + 1] : bootv;
+          else vn = vseg_next;
+          b[k] = k < nvalid ? (((double)rr[k] + gamma * nd * vn) + tl) - (double)vv[k] : 0.0;
+        } else {
+          b[k] = k < nvalid ? (double)rr[k] + tl : 0.0;
+        }
+        a[k] = k < nvalid ? (((dmask >> k) & 1u) ? 0.0 : ga) : 1.0;
       }
     }
-#define RPL_A(k) ((k) < nvalid ? (((dmask >> (k)) & 1u) ? 0.0 : ga) : 1.0)
     double A = 1.0, Bc = 0.0;
 #pragma unroll
     for (int k = S - 1; k >= 0; --k) {
-      const double ak = RPL_A(k);
-      Bc = fma(ak, Bc, b[k]);
-      A = ak * A;
+      Bc = fma(a[k], Bc, b[k]);
+      A = a[k] * A;
     }
     sm.sA[seg][ci] = A;
     sm.sB[seg][ci] = Bc;
@@ -573,18 +597,17 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
       asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     }
     __syncthreads();  // (2) maps visible; this stage is free; the output tile is free
-    if (threadIdx.x == 0 && i + STAGES < items) issue(i + STAGES);
+    if (threadIdx.x == 0 && i + STAGES < items) issue();
     double x = sm.carry[ci];
 #pragma unroll
     for (int ss = SEGS - 1; ss > 0; --ss)
       if (ss > seg) x = fma(sm.sA[ss][ci], x, sm.sB[ss][ci]);
 #pragma unroll
     for (int k = S - 1; k >= 0; --k) {
-      x = fma(RPL_A(k), x, b[k]);
+      x = fma(a[k], x, b[k]);
       sm.o0[ob][seg * S + k][ci] = (float)x;
       if (GAE) sm.o1[ob][seg * S + k][ci] = (float)(x + (double)vv[k]);
     }
-#undef RPL_A
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
     __syncthreads();  // (3) the output tile is complete; maps / carry reads done
     if (seg == 0) {
@@ -600,6 +623,11 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
                      ::"l"(&tm_o1), "r"(x0), "r"(y0), "r"(s_u32(&sm.o1[ob][0][0])) : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
+    if (--c < 0) {
+      c = nchunks - 1;
+      g += gridDim.x;
+    }
+    if (++st == STAGES) st = 0;
   }
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
   pdl_trigger();

@@ -33,7 +33,11 @@ import torch.distributed as dist
 
 
 class ShardedSampler:
-    def __init__(self, tree, n_per_rank: int, seed: int, group=None, is_weights=None, compact=False):
+    def __init__(self, tree, n_per_rank: int, seed: int, group=None, is_weights=None, compact=False,
+                 buffer_norm=False):
+        """buffer_norm: IS weights normalised over the whole (sharded) buffer (R29): the
+        tree carries an attached min-tree and the K5 all-gather exchanges {total, min}
+        records — the K7 all-reduce disappears.  Requires compact."""
         self.tree = tree
         self.group = group
         self.world = dist.get_world_size(group)
@@ -50,11 +54,31 @@ class ShardedSampler:
         self._is_weights = is_weights
         self.compact = bool(compact)
         self.count = torch.zeros(2, dtype=torch.int64, device=dev)  # [owned m, first stratum k0]
+        self.buffer_norm = bool(buffer_norm)
+        if self.buffer_norm and not self.compact:
+            raise ValueError("buffer_norm needs the compacted sampler")
+        self.my_pair = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.pairs = torch.zeros((self.world, 2), dtype=torch.int64, device=dev)
+        self.local_qmin = torch.zeros(1, dtype=torch.int64, device=dev)
 
     def sample(self, beta: float):
         """One global stratified sample of n_glob draws.  Returns (idx, q, w): idx[k] is
         the GLOBAL leaf (rank * shard_leaves + local) for the draws this rank owns and
         -1 elsewhere; w is normalised by the global batch min q."""
+        if self.buffer_norm:  # K5 carries {total, buffer min}; the global min is the normaliser
+            self.tree.total_min(out=self.my_pair)
+            if dist.get_backend(self.group) == "nccl":
+                dist.all_gather_into_tensor(self.pairs.view(-1), self.my_pair, group=self.group)
+            else:
+                dist.all_gather(list(self.pairs.unbind(0)), self.my_pair, group=self.group)
+            self.totals.copy_(self.pairs[:, 0])  # (diagnostics only; the sampler reads the pairs)
+            self.tree.sample_sharded_pairs(self.rank, self.world, self.pairs, self.n_glob, self.seed, self.count,
+                                           out=(self.idx, self.q, self.local_qmin), bufmin=self.qmin)
+            wfn = self._is_weights
+            if wfn is None:
+                from .ops import is_weights as wfn
+            wfn(self.q, self.qmin, beta, out=self.w)
+            return self.idx, self.q, self.w
         self.tree.total(out=self.my_total)
         if dist.get_backend(self.group) == "nccl":
             dist.all_gather_into_tensor(self.totals, self.my_total, group=self.group)      # K5

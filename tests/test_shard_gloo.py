@@ -62,6 +62,20 @@ class OracleShardTree:
             count[1] = int(np.nonzero(own.numpy())[0][0]) if c else 0
 
 
+    # buffer-wide normaliser (R29): {total, min} records, compacted pairs sampler
+    def total_min(self, out):
+        out[0] = self.o.total()
+        out[1] = OS.buffer_min(self.o.q)
+        return out
+
+    def sample_sharded_pairs(self, rank, n_shards, pairs, n, seed, count, out=None, bufmin=None):
+        idx, q, qmin = out
+        self.sample_sharded(rank, n_shards, pairs[:, 0].contiguous(), n, seed=seed, out=out, use_stream=True,
+                            count=count)
+        bufmin[0] = min(int(x) for x in pairs[:, 1])
+        return idx, q, qmin, bufmin
+
+
 def cpu_is_weights(q, qmin, beta, out):
     m = float(qmin[0])
     for k in range(q.numel()):
@@ -73,13 +87,13 @@ def leaves_of(rank):
     return [int(x) for x in g.integers(1, 1 << 20, N_LOCAL)]
 
 
-def worker(rank, world, port, queue, compact=False):
+def worker(rank, world, port, queue, compact=False, buffer_norm=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1909_01500_b200.shard import ShardedSampler
     tree = OracleShardTree(leaves_of(rank))
-    smp = ShardedSampler(tree, N_PER_RANK, SEED, is_weights=cpu_is_weights, compact=compact)
+    smp = ShardedSampler(tree, N_PER_RANK, SEED, is_weights=cpu_is_weights, compact=compact, buffer_norm=buffer_norm)
     res = []
     for _ in range(STEPS):
         idx, q, w = smp.sample(BETA)
@@ -169,4 +183,41 @@ def test_mode_l_two_ranks_gloo_compacted():
             merged_w += w[:cnt].tolist()
         assert merged == ref_idx
         ref_w = OS.is_weights(ref_q, sum(sum(s.q) for s in shards), world * N_LOCAL, BETA)
+        np.testing.assert_allclose(merged_w, ref_w, rtol=1e-6)
+
+
+@pytest.mark.timeout(120)
+def test_mode_l_two_ranks_gloo_buffer_normaliser():
+    # R29 sharded: one all-gather of {total, min} records; the weights use the global buffer
+    # min (PER's (N P_i)^-beta / max over the whole buffer) and there is no K7 all-reduce
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, world, port, q, True, True)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=100) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    shards = []
+    for r in range(world):
+        t = OS.SumTreeOracle(N_LOCAL, 0)
+        t.q = leaves_of(r)
+        shards.append(t)
+    n_glob = N_PER_RANK * world
+    N = world * N_LOCAL
+    Q = sum(sum(s.q) for s in shards)
+    qmin = min(OS.buffer_min(s.q) for s in shards)
+    for step in range(STEPS):
+        draws = OP.draws_u64(SEED, step * n_glob, n_glob)
+        ref_idx, ref_q, _ = OS.sharded_sample(shards, n_glob, draws)
+        merged, merged_w = [], []
+        for r in range(world):
+            idx, qq, w, totals, cnt = out[r][step]
+            merged += (idx[:cnt] + r * N_LOCAL).tolist()
+            merged_w += w[:cnt].tolist()
+        assert merged == ref_idx
+        ref_w = [((N * qi / Q) ** -BETA) / ((N * qmin / Q) ** -BETA) for qi in ref_q]
         np.testing.assert_allclose(merged_w, ref_w, rtol=1e-6)
