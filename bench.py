@@ -74,6 +74,9 @@ def parse():
                     help="1 GPU: priority update + sampling as one launch (rpl_sumtree_update_sample; "
                          "measured 1.7 us/step slower than the PDL-chained pair)")
     ap.add_argument("--seq-variant", type=int, default=None, help="diagnostics: sequence-gather kernel variant")
+    ap.add_argument("--fused-sample", type=int, default=1, choices=[0, 1],
+                    help="1 GPU: stratified sampling inside the sequence gather (rpl_gather_sample), so the step "
+                         "is update_seq -> gather; 0: a separate rpl_sumtree_sample_stream launch")
     ap.add_argument("--mode", default="L", choices=["L", "C"],
                     help="N > 1 replay mode (SURVEY §8e): L = owner computes, each rank feeds its own learner; "
                          "C = every owner's gather writes into the rank-0 learner's batch over NVLink (CUDA IPC)")
@@ -218,6 +221,7 @@ def run_rpl(args):
     import paper_1909_01500_b200 as rpl
     from paper_1909_01500_b200 import replay as R
     from synth import make_ring, rng
+    FUSED_SAMPLE[0] = bool(args.fused_sample) and not args.tree_fused
     if args.seq_variant is not None:
         rpl._lib.check(rpl._lib.lib.rpl_debug_set_gather_variant(int(args.seq_variant)), "variant")
 
@@ -343,7 +347,7 @@ def run_rpl(args):
             rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(prev), P_(td_i),
                                                       c["train"], n_glob, c["eta"], c["alpha"], c["eps_p"], 0, None,
                                                       s), "update_seq")
-        if world == 1 and not args.tree_fused:
+        if world == 1 and not args.tree_fused and not args.fused_sample:
             # (a8) draws only; the batch-min normaliser and IS weights (a9) are fused into the gather
             rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, seed, c["beta"], P_(cur),
                                                          P_(q_buf), None, None, P_(err), s), "sample")
@@ -369,8 +373,12 @@ def run_rpl(args):
             plan.desc.o_tgt = y_out.data_ptr()
         # (K7 fused with p2p: the gather publishes / reads the batch mins over the boards;
         #  a2 + a4 fused: the rescaled 5-step targets of the train rows, bootstrap q_i)
-        plan.run(cur, q=q_buf, qmin=None if (world == 1 or p2p) else qmin, beta=c["beta"], err=err, stream=s,
-                 q_tgt=q_i if fused_tgt else None)
+        if world == 1 and args.fused_sample and not args.tree_fused:
+            # (a8 + a9 + a11 + a2/a4) the gather draws its own strata from the updated tree
+            plan.run_sample(tree, seed, cur, q_buf, beta=c["beta"], err=err, stream=s, q_tgt=q_i)
+        else:
+            plan.run(cur, q=q_buf, qmin=None if (world == 1 or p2p) else qmin, beta=c["beta"], err=err, stream=s,
+                     q_tgt=q_i if fused_tgt else None)
         if w_out is not None:
             plan.desc.o_w = w.data_ptr()
         if fused_tgt and y_out is not None:
@@ -550,7 +558,8 @@ def run_rpl(args):
                                + " (both warmed by 3 replays first); exactly K steps timed" if use_graph
                                else "eager launches"),
                        tree=("update+sample fused (rpl_sumtree_update_sample)" if world == 1 and args.tree_fused
-                             else "update_seq, then sample"),
+                             else "update_seq, then sampling inside the gather (rpl_gather_sample)"
+                             if world == 1 and args.fused_sample else "update_seq, then sample"),
                        exchange=(None if world == 1 else "p2p boards (K5 in the sampler, K7 in the gather)" if p2p
                                  else f"{args.backend} collectives")),
         "gpu_launches": launches,
@@ -868,6 +877,9 @@ def bench_r2d2_1mseq(dev, rpl, c):
                           "r2d2_1mseq_one_shard")
 
 
+FUSED_SAMPLE = [True]  # set from --fused-sample (the secondaries time the headline's step shape)
+
+
 def seed_sweep(dev, rpl, c, main_us):
     """seeds 0-4, median reported — seed 0 is the headline measurement; seeds 1-4
     rebuild the [4000, 256] ring (device generator), tree and graph and re-time the step."""
@@ -906,6 +918,9 @@ def time_r2d2_step(dev, rpl, c, cap, B, seed, cursor, workload):
         s = rpl.ops._stream(dev)
         rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(idx[(i + 1) % 2]), P_(td[i % 8]),
                                                   c["train"], n, c["eta"], c["alpha"], c["eps_p"], 0, None, s), "upd")
+        if FUSED_SAMPLE[0]:
+            plan.run_sample(tree, 0xBEEF, idx[i % 2], q, beta=c["beta"], err=err, stream=s, q_tgt=qv[i % 8])
+            return
         rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, 0xBEEF, c["beta"], P_(idx[i % 2]),
                                                      P_(q), None, None, P_(err), s), "sample")
         plan.run(idx[i % 2], q=q, qmin=None, beta=c["beta"], err=err, stream=s, q_tgt=qv[i % 8])
@@ -937,6 +952,9 @@ def unique_output_step(dev, rpl, tree, ring, idx_buf, td_pool, q_pool, err, c, n
         cur, prev = idx_buf[i % 2], idx_buf[(i + 1) % 2]
         rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(prev), P_(td_pool[i % P]),
                                                   c["train"], n, c["eta"], c["alpha"], c["eps_p"], 0, None, s), "upd")
+        if FUSED_SAMPLE[0]:
+            plan.run_sample(tree, seed, cur, q, beta=c["beta"], err=err, stream=s, q_tgt=q_pool[i % P])
+            return
         rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), n, seed, c["beta"], P_(cur), P_(q),
                                                      None, None, P_(err), s), "sample")
         plan.run(cur, q=q, qmin=None, beta=c["beta"], err=err, stream=s, q_tgt=q_pool[i % P])

@@ -497,6 +497,19 @@ typedef struct {
 int rpl_gather(const rpl_gather_desc* desc /* host */, const int64_t* idx, const int64_t* q,
                const int64_t* qmin, double beta, int64_t n, int32_t* dev_err, void* stream);
 
+/* Sampling fused into the sequence gather (a8 + a11 in one launch; R2D2's learner step
+ * becomes update -> gather): the call draws n stratified samples from `tree` exactly as
+ * rpl_sumtree_sample_stream(L, tree, n, seed, ...) would (the tree's Philox stream position,
+ * advanced by n on the device) and gathers them as rpl_gather(desc, idx_out, q_out, NULL,
+ * beta, n, ...) would — every CTA descends the tree for the samples its rows need, the CTA
+ * owning a sample's first row writes idx_out[k] / q_out[k] (device int64 [n]), and the last
+ * CTA to finish writes the IS weights (batch min) into desc->o_w.  Bit-identical outputs to
+ * the two calls.  SEQUENCE only; no n_active / col_offset / peer_boards / done_flag (those
+ * are the sharded paths: RPL_EINVAL); L must describe cap_T/period x B leaves.  Runs on the
+ * default persistent kernel (RPL_EUNSUPPORTED when it cannot: frames not TMA-addressable). */
+int rpl_gather_sample(const rpl_gather_desc* desc, const rpl_tree_layout* L, int64_t* tree, uint64_t seed,
+                      int64_t* idx_out, int64_t* q_out, double beta, int64_t n, int32_t* dev_err, void* stream);
+
 /* Stream-ordered wait for n completion flags (device int64 [n], e.g. the learner's flag array
  * that n owners' gathers signal through rpl_gather_desc.done_flag): returns at once, the
  * enqueued one-warp kernel spins with ld.acquire.sys until flags[i] >= *expect for every i

@@ -295,4 +295,61 @@ __device__ __forceinline__ uint64_t philox_u64(uint64_t seed, uint64_t c) {
   return (uint64_t)c0 | ((uint64_t)c1 << 32);
 }
 
+// ---- stratified sampling by descent (a8, §8c #8; shared by the samplers and the fused gather) ----
+__device__ __forceinline__ uint64_t stratum_lo(uint64_t k, uint64_t Q, uint64_t n) {
+  // floor(k Q / n) without 128-bit products: k*(Q/n) + floor(k*(Q%n)/n); k <= n < 2^31
+  return k * (Q / n) + (k * (Q % n)) / n;
+}
+
+// Global prefix of stratum k (a8, §8c #8): lo_k + floor(u_k (hi_k - lo_k) / 2^64).
+// Non-decreasing in k (prefix_k < hi_k = lo_{k+1} <= prefix_{k+1}, or = lo_k for an
+// empty stratum), so the strata a shard owns form one contiguous run.
+__device__ __forceinline__ uint64_t stratum_prefix(int64_t k, uint64_t Q, int64_t n, const uint64_t* draws,
+                                                   uint64_t seed, uint64_t ctr0) {
+  const uint64_t lo = stratum_lo((uint64_t)k, Q, (uint64_t)n);
+  const uint64_t hi = stratum_lo((uint64_t)k + 1, Q, (uint64_t)n);
+  const uint64_t u = draws ? draws[k] : philox_u64(seed, ctr0 + (uint64_t)k);
+  return lo + __umul64hi(u, hi - lo);
+}
+
+// Descend from the root for `prefix` (< node sum); returns leaf index, writes q.  Words
+// [0, n_top) of the tree (whole top levels) may be staged in shared memory (`top`): those
+// levels are read from there, the rest from global memory.
+__device__ __forceinline__ int64_t descend(const TreeDev& L, const int64_t* __restrict__ tree,
+                                           int64_t prefix, int64_t* q_out, int32_t* errbits,
+                                           const int64_t* top = nullptr, int64_t n_top = 0) {
+  const int lane = threadIdx.x & 31;
+  int64_t node = 0;
+  int64_t c = 0;
+  for (int l = 0; l < L.depth; ++l) {
+    const int64_t base = L.level_off[l + 1] + (node << L.log2w);
+    c = lane < L.fanout ? (base < n_top ? top[base + lane] : tree[base + lane]) : 0;
+    int64_t incl = c;
+#pragma unroll
+    for (int dlt = 1; dlt < 32; dlt <<= 1) {
+      const int64_t o = shfl_up64(incl, dlt);
+      if (lane >= dlt) incl += o;
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, prefix < incl);
+    int f;
+    if (bal == 0) {  // prefix >= node sum: inconsistent tree / out of range -> clamp
+      *errbits |= RPL_DERR_TREE;
+      const unsigned nz = __ballot_sync(0xffffffffu, c > 0);
+      f = nz ? 31 - __clz(nz) : 0;
+      const int64_t inc_last = shfl64(incl, f);
+      prefix = nz ? inc_last - 1 : 0;  // the last unit of the last non-empty child
+    } else {
+      f = __ffs(bal) - 1;
+    }
+    const int64_t inc_f = shfl64(incl, f);
+    const int64_t c_f = shfl64(c, f);
+    prefix -= inc_f - c_f;
+    if (prefix < 0) prefix = 0;
+    node = (node << L.log2w) + f;
+    c = c_f;
+  }
+  *q_out = c;
+  return node;
+}
+
 }  // namespace rpl

@@ -203,6 +203,9 @@ struct GDesc {
   const float* v_term;  // time-limit bootstrap values (R34; NULL: every done is terminal)
   int64_t* done_flag;   // completion signal (Mode C; NULL: off)
   int64_t* done_seq;    // [2] call counter + CTA ticket (device, this rank's memory)
+  int64_t* smp_tree;    // fused stratified sampling (rpl_gather_sample; NULL: idx given)
+  TreeDev smp_L;
+  uint64_t smp_seed;
 };
 
 // Output column offset (rpl_gather_desc.col_offset); read after pdl_wait.
@@ -930,6 +933,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   __shared__ int8_t start_off[PL_MAX_ROWS];
   __shared__ volatile int row_done[PL_MAX_ROWS];
   __shared__ int s_npieces;
+  __shared__ int64_t p_leaf[PL_MAX_ROWS];  // fused sampling: the piece's sampled leaf
   constexpr int NT = (NC + 2) * 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k = D.k, L = D.seq_len;
@@ -946,6 +950,14 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   for (int c = tid; c < PL_MAX_ROWS; c += NT) row_done[c] = 0;
   if (RPL_PDL_EARLY & 4) pdl_trigger();  // A/B knob (common.cuh)
   pdl_wait();  // idx (and n_active) come from the sampler launched just before
+  // Fused sampling (rpl_gather_sample): the tree was updated by the kernel before; every
+  // thread reads the root and the stream position (the last CTA advances it at the end)
+  const bool smp = D.smp_tree != nullptr;
+  uint64_t smp_Q = 0, smp_pos = 0;
+  if (smp) {
+    smp_Q = (uint64_t)__ldcg(D.smp_tree + D.smp_L.level_off[0]);
+    smp_pos = (uint64_t)__ldcg(D.smp_tree + D.smp_L.hdr_off + 2);
+  }
   // rows g = s*L + tau of the active samples, split evenly over the grid
   const int total = (int)(active_n(D, n) * L);
   const int64_t coff = col_off(D);  // output column of entry 0 (Mode C)
@@ -974,11 +986,36 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   const int npieces = (g1 - 1) / L - s_first + 1;
 
   if (tid == 0) s_npieces = npieces;
+  if (smp) {
+    // (S) one warp per piece descends the tree for the piece's stratum (a8; the same strata
+    //     and Philox stream as rpl_sumtree_sample_stream); the CTA owning a sample's first
+    //     row writes its index and q
+    int32_t eb = 0;
+    for (int pc = warp; pc < npieces; pc += NT / 32) {
+      const int sm = s_first + pc;
+      int64_t leaf = -1, qv = 0;
+      if (smp_Q == 0) {
+        eb |= RPL_DERR_EMPTY;
+      } else {
+        const uint64_t prefix = stratum_prefix(sm, smp_Q, n, nullptr, D.smp_seed, smp_pos);
+        leaf = descend(D.smp_L, D.smp_tree, (int64_t)prefix, &qv, &eb);
+      }
+      if (lane == 0) {
+        p_leaf[pc] = leaf;
+        if (sm * L >= g0) {
+          const_cast<int64_t*>(idx)[sm] = leaf;
+          const_cast<int64_t*>(q)[sm] = qv;
+        }
+      }
+    }
+    if (lane == 0 && eb) set_err(err, eb);
+    __syncthreads();
+  }
   // (A) pieces, in parallel: one sampled leaf each
   for (int pc = tid; pc < npieces; pc += NT) {
     const int sm = s_first + pc;
     const int tau0 = max(g0 - sm * L, 0);
-    const int64_t leaf = idx[sm];
+    const int64_t leaf = smp ? p_leaf[pc] : idx[sm];
     int bcol = -1, row0 = 0, blk = 0;
     if (leaf >= 0 && leaf < nleaves) {
       blk = (int)(leaf / Bc);
@@ -1109,7 +1146,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
 
     if (warp == 1) {
       // ---------------- meta warp: per-row fields, IS weights ----------------
-      const int64_t qm = (D.o_w && q && !peer) ? warp_batch_qmin(qmin, idx, q, n) : 0;
+      const int64_t qm = (D.o_w && q && !peer && !smp) ? warp_batch_qmin(qmin, idx, q, n) : 0;
       const int64_t ab = D.act_bytes;
       const bool a8 = ab == 8 && ((reinterpret_cast<uintptr_t>(D.act) | reinterpret_cast<uintptr_t>(D.o_act) |
                                    reinterpret_cast<uintptr_t>(D.o_prev_act)) & 7) == 0;
@@ -1144,7 +1181,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         if (D.o_prev_rew) D.o_prev_rew[o] = pd ? 0.0f : prw;
         if (D.o_done) D.o_done[o] = dd;
         if (D.o_start) D.o_start[o] = start_off[c];
-        if (tau == 0 && D.o_w && q && !peer) {
+        if (tau == 0 && D.o_w && q && !peer && !smp) {
           const int64_t qs = q[sm];
           D.o_w[coff + sm] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
         }
@@ -1270,6 +1307,42 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
     }
   }
   } while (0);
+  // Fused sampling epilogue: the last CTA (ticket = the tree's sampler-ticket header word)
+  // reduces the batch-min q over every CTA's written samples (acquired through the acq_rel
+  // ticket), writes the IS weights (a9) and advances the tree's stream position.
+  if (smp) {
+    __shared__ int s_last;
+    __shared__ int64_t s_qm[NC + 2];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;"
+                   : "=l"(t) : "l"(D.smp_tree + D.smp_L.hdr_off + 1) : "memory");
+      s_last = t == (unsigned long long)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      int64_t m = INT64_MAX;
+      for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+        const int64_t ij = __ldcg(idx + j), qj = __ldcg(q + j);
+        if (ij >= 0 && qj < m) m = qj;
+      }
+      m = warp_min64(m);
+      if ((threadIdx.x & 31) == 0) s_qm[threadIdx.x >> 5] = m;
+      __syncthreads();
+      m = INT64_MAX;
+      for (int k2 = 0; k2 < NC + 2; ++k2) m = s_qm[k2] < m ? s_qm[k2] : m;
+      if (D.o_w)
+        for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+          const int64_t qj = __ldcg(q + j);
+          D.o_w[j] = qj > 0 ? (float)pow((double)m / (double)qj, beta) : 0.0f;
+        }
+      if (threadIdx.x == 0) {
+        D.smp_tree[D.smp_L.hdr_off + 1] = 0;
+        D.smp_tree[D.smp_L.hdr_off + 2] = (int64_t)(smp_pos + (uint64_t)n);
+      }
+    }
+  }
   // Completion signal (rpl_gather_desc.done_flag, Mode C): every CTA publishes its stores at
   // system scope and takes a ticket; the last CTA bumps the call counter done_seq[0] and
   // writes it to done_flag with st.release.sys (peer memory over NVLink), so the learner's
@@ -1816,6 +1889,8 @@ GDesc to_dev(const rpl_gather_desc* d) {
   g.v_term = d->v_term;
   g.done_flag = d->done_flag;
   g.done_seq = d->done_seq;
+  g.smp_tree = nullptr;
+  g.smp_seed = 0;
   return g;
 }
 
@@ -1870,8 +1945,42 @@ void cfg_gather(int* variant, int* diag, int* diag_build, int* seq_consumers, in
 }
 }  // namespace rpl
 
+namespace rpl {
+namespace {
+struct SmpArgs {
+  int64_t* tree;
+  TreeDev L;
+  uint64_t seed;
+};
+int gather_run(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q, const int64_t* qmin, double beta,
+               int64_t n, int32_t* dev_err, void* stream, const SmpArgs* smp);
+}  // namespace
+}  // namespace rpl
+
 extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q, const int64_t* qmin,
                           double beta, int64_t n, int32_t* dev_err, void* stream) {
+  return gather_run(desc, idx, q, qmin, beta, n, dev_err, stream, nullptr);
+}
+
+extern "C" int rpl_gather_sample(const rpl_gather_desc* desc, const rpl_tree_layout* L, int64_t* tree, uint64_t seed,
+                                 int64_t* idx_out, int64_t* q_out, double beta, int64_t n, int32_t* dev_err,
+                                 void* stream) {
+  if (!desc || !L || !tree || !idx_out || !q_out || n < 1 || n > (1ll << 30)) return RPL_EINVAL;
+  if (desc->kind != RPL_GATHER_SEQUENCE || desc->n_active || desc->col_offset || desc->peer_boards || desc->done_flag)
+    return RPL_EINVAL;
+  if (desc->period < 1 || desc->cap_T % desc->period != 0 || L->n_leaves != (desc->cap_T / desc->period) * desc->B)
+    return RPL_EINVAL;
+  SmpArgs a;
+  a.tree = tree;
+  a.L = tree_dev(L);
+  a.seed = seed;
+  return gather_run(desc, idx_out, q_out, nullptr, beta, n, dev_err, stream, &a);
+}
+
+namespace rpl {
+namespace {
+int gather_run(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q, const int64_t* qmin, double beta,
+               int64_t n, int32_t* dev_err, void* stream, const SmpArgs* smp) {
   if (!desc || n < 0) return RPL_EINVAL;
   if (n == 0) return RPL_OK;
   if (!idx || !desc->done || !desc->obs || desc->cap_T < 1 || desc->B < 1 || desc->k < 1 || desc->k > 8 ||
@@ -1891,10 +2000,17 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
                       !(desc->rescale_eps >= 0.0) || (desc->rescale != 0 && desc->rescale != 1)))
     return RPL_EINVAL;
   GDesc g = to_dev(desc);
-  // col_offset / o_start / peer boards / fused targets: default kernels only
+  if (smp) {
+    g.smp_tree = smp->tree;
+    g.smp_L = smp->L;
+    g.smp_seed = smp->seed;
+  }
+  // col_offset / o_start / peer boards / fused targets / fused sampling: default kernels only
   if ((desc->done_flag != nullptr) != (desc->done_seq != nullptr)) return RPL_EINVAL;
   const int seq_variant =
-      (desc->col_offset || desc->o_start || desc->peer_boards || desc->o_tgt || desc->done_flag) ? 0 : g_seq_variant;
+      (desc->col_offset || desc->o_start || desc->peer_boards || desc->o_tgt || desc->done_flag || smp)
+          ? 0
+          : g_seq_variant;
   const bool tma_ok = (desc->obs_bytes % 16 == 0) && aligned16(desc->obs) && aligned16(desc->o_obs) &&
                       aligned16(desc->o_next_obs) && desc->obs_bytes <= 32768;
   cudaStream_t st = as_stream(stream);
@@ -1984,7 +2100,9 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
       }
     }
     if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs &&
-        (seq_variant == 3 || (seq_variant == 0 && !desc->col_offset && !desc->o_start && !desc->peer_boards))) {
+        (seq_variant == 3 ||
+         (seq_variant == 0 && !desc->col_offset && !desc->o_start && !desc->peer_boards && !desc->o_tgt &&
+          !desc->done_flag && !smp))) {
       // persistent TMA pipeline: NS frame slots (+1 zero slot); CTAs_per_SM CTAs per SM
       // Slots the consumer may need beyond the released ones: G+1 rows of advance, the
       // k-1 window, and k-1 per piece boundary crossed.  With L > G at most two boundaries
@@ -2015,7 +2133,7 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
         return launch_status();
       }
     }
-    if (desc->o_start || desc->peer_boards || desc->o_tgt || desc->done_flag)
+    if (desc->o_start || desc->peer_boards || desc->o_tgt || desc->done_flag || smp)
       return RPL_EUNSUPPORTED;  // persistent default kernel only
     const int64_t smem = (int64_t)(SEQ_CHUNK + desc->k) * desc->obs_bytes;
     g.use_tma = (tma_ok && smem <= 200 * 1024) ? 1 : 0;
@@ -2030,6 +2148,8 @@ extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const
   }
   return RPL_EINVAL;
 }
+}  // namespace
+}  // namespace rpl
 
 // ---------------------------------------------------------------------------
 // k-stacks from unique rows (Mode C learner side, §8e): out[tau, s] slot j = unique row

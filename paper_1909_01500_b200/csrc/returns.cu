@@ -426,15 +426,15 @@ k_scan_tma2(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
 // a double-buffered output tile, so one item's scan overlaps the next items' loads and the
 // previous item's stores.  Groups are dealt round-robin to the grid (CTAs_per_SM x SMs).
 // ---------------------------------------------------------------------------
-template <int COLS, int WARPS, int S, int STAGES, bool GAE>
+template <int COLS, int WARPS, int S, int STAGES, bool GAE, int OB = 2>
 struct ScanPipeSmem {
   static constexpr int SUB = 32 / COLS;
   static constexpr int SEGS = WARPS * SUB;
   static constexpr int CH = SEGS * S;
   alignas(128) float r[STAGES][CH][COLS];  // TMA tiles: 128-B aligned
   alignas(128) float v[GAE ? STAGES : 1][GAE ? CH : 1][COLS];
-  alignas(128) float o0[2][CH][COLS];
-  alignas(128) float o1[GAE ? 2 : 1][GAE ? CH : 1][COLS];
+  alignas(128) float o0[OB][CH][COLS];
+  alignas(128) float o1[GAE ? OB : 1][GAE ? CH : 1][COLS];
   alignas(128) uint8_t d[STAGES][CH][COLS];
   double sA[SEGS][COLS];
   double sB[SEGS][COLS];
@@ -443,13 +443,13 @@ struct ScanPipeSmem {
   uint64_t bar[STAGES];
 };
 
-template <int COLS, int WARPS, int S, int STAGES, bool GAE>
-__global__ void __launch_bounds__(WARPS * 32, 2)
+template <int COLS, int WARPS, int S, int STAGES, bool GAE, int MINB = 2, int OB = 2>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
 k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUtensorMap tm_v,
             const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ CUtensorMap tm_o0,
             const __grid_constant__ CUtensorMap tm_o1, const float* __restrict__ boot, int64_t T, int64_t B,
             double gamma, double lam, int has_o1, const float* __restrict__ vterm) {
-  using SM = ScanPipeSmem<COLS, WARPS, S, STAGES, GAE>;
+  using SM = ScanPipeSmem<COLS, WARPS, S, STAGES, GAE, OB>;
   constexpr int SUB = SM::SUB, SEGS = SM::SEGS, CH = SM::CH;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
@@ -506,7 +506,7 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
   int64_t g = blockIdx.x, c = nchunks - 1;
   int st = 0;
   for (int64_t i = 0; i < items; ++i) {
-    const int ob = (int)(i & 1);
+    const int ob = OB == 1 ? 0 : (int)(i & 1);
     const int64_t col = g * COLS + ci;
     const bool cv = col < B;
     const double bootv = (GAE && cv) ? (double)__ldg(boot + col) : 0.0;
@@ -594,7 +594,8 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
     if (threadIdx.x == 0) {
       // the output tile about to be written held item i-2's outputs: their store must have
       // finished reading it (at most one store group, item i-1's, stays in flight)
-      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      if (OB == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     }
     __syncthreads();  // (2) maps visible; this stage is free; the output tile is free
     if (threadIdx.x == 0 && i + STAGES < items) issue();
@@ -882,11 +883,14 @@ int elementwise_grid(int64_t work, int threads) {
 
 using namespace rpl;
 
-// Measurement-only knob (RPL_SCAN_VARIANT): 0 = default (TMA tiles when the layout allows,
-// else LDG 16 warps x 8 rows), 4 = cluster of 2 CTAs x 64 rows (T <= 128, else default),
-// 5 = cluster of 4 CTAs x 32 rows (T <= 128, else default), 6 = TMA tiles, 3 = LDG
-// 16 warps x 8 rows, 1 = LDG 32 warps x 4 rows, 2 = LDG 8 warps x 16 rows.  Same fp64
-// affine-map arithmetic; segment boundaries differ.
+// Measurement-only knob (RPL_SCAN_VARIANT): 0 = default (the persistent pipelined scan,
+// k_scan_pipe, when the layout is TMA-addressable — B % 4 == 0 for f32 and B % 16 == 0 for
+// the u8 done tiles — else LDG 16 warps x 8 rows), 9 = the same pipeline, 6 = whole-column
+// TMA tiles (the round-1 default), 7 = 16-column TMA tiles, double-buffered chunks, 8 = 32
+// columns x 64 rows double-buffered, 4 = cluster of 2 CTAs x 64 rows (T <= 128, else
+// default), 5 = cluster of 4 CTAs x 32 rows, 3 = LDG 16 warps x 8 rows, 1 = LDG 32 warps x 4
+// rows, 2 = LDG 8 warps x 16 rows.  Same fp64 affine-map arithmetic; segment boundaries
+// differ (results within the 1e-5 bound, not bit-identical across variants).
 std::atomic<int> g_scan_variant{-1};  // -1: not set yet (read RPL_SCAN_VARIANT once)
 
 int scan_variant() {
@@ -894,7 +898,7 @@ int scan_variant() {
   if (v < 0) {
     const char* e = getenv("RPL_SCAN_VARIANT");
     int want = e ? atoi(e) : 0;
-    if (want < 0 || want > 9) want = 0;
+    if (want < 0 || want > 17) want = 0;
     int expect = -1;
     g_scan_variant.compare_exchange_strong(expect, want);
     v = g_scan_variant.load(std::memory_order_relaxed);
@@ -971,6 +975,34 @@ int launch_scan_cluster(const float* r, const float* v, const uint8_t* d, const 
                             md, v, boot, T, B, gamma, lam, o0, o1, vterm);
 }
 
+template <int COLS, int WARPS, int S, int STAGES, bool GAE, int MINB, int OB = 2>
+int launch_scan_pipe(const float* r, const float* v, const uint8_t* d, const float* boot, int64_t T, int64_t B,
+                     double gamma, double lam, float* o0, float* o1, cudaStream_t st, const float* vterm, bool* used) {
+  using SMt = ScanPipeSmem<COLS, WARPS, S, STAGES, GAE, OB>;
+  constexpr int CH = SMt::CH;
+  CUtensorMap mr, mv, md, mo0, mo1;
+  *used = false;
+  if (!(tmap_2d(&mr, r, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH, COLS) &&
+        tmap_2d(&md, d, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, T, B, CH, COLS) &&
+        tmap_2d(&mo0, o0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH, COLS) &&
+        (!GAE || tmap_2d(&mv, v, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH, COLS)) &&
+        (!(GAE && o1) || tmap_2d(&mo1, o1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH, COLS))))
+    return RPL_OK;
+  *used = true;
+  if (!GAE) mv = mr;
+  if (!(GAE && o1)) mo1 = mo0;
+  auto kern = k_scan_pipe<COLS, WARPS, S, STAGES, GAE, MINB, OB>;
+  const size_t dyn = sizeof(SMt);
+  ensure_smem(reinterpret_cast<const void*>(kern), dyn);
+  const int64_t groups = (B + COLS - 1) / COLS;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, dyn);
+  int64_t grid = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
+  if (grid > groups) grid = groups;
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(WARPS * 32), dyn, st, mr, mv, md, mo0, mo1, boot, T, B, gamma,
+                    lam, (GAE && o1) ? 1 : 0, vterm);
+}
+
 template <bool GAE>
 int launch_scan(const float* r, const float* v, const uint8_t* d, const float* boot, int64_t T, int64_t B,
                 double gamma, double lam, float* o0, float* o1, cudaStream_t st, const float* vterm) {
@@ -987,29 +1019,25 @@ int launch_scan(const float* r, const float* v, const uint8_t* d, const float* b
                        : launch_scan_cluster<8, 4, 4, GAE>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, &used, vterm);
     if (used) return rc;
   }
-  if (var == 9 && T < (1ll << 31) && B < (1ll << 31)) {
-    constexpr int COLS = 16, WARPS = 8, S = 8, STAGES = 3;
-    using SMt = ScanPipeSmem<COLS, WARPS, S, STAGES, GAE>;
-    constexpr int CH = SMt::CH;
-    CUtensorMap mr, mv, md, mo0, mo1;
-    if (tmap_2d(&mr, r, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH, COLS) &&
-        tmap_2d(&md, d, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, T, B, CH, COLS) &&
-        tmap_2d(&mo0, o0, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH, COLS) &&
-        (!GAE || tmap_2d(&mv, v, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH, COLS)) &&
-        (!(GAE && o1) || tmap_2d(&mo1, o1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH, COLS))) {
-      if (!GAE) mv = mr;
-      if (!(GAE && o1)) mo1 = mo0;
-      const size_t dyn = sizeof(SMt);
-      ensure_smem(reinterpret_cast<const void*>(k_scan_pipe<COLS, WARPS, S, STAGES, GAE>), dyn);
-      const int64_t groups = (B + COLS - 1) / COLS;
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_pipe<COLS, WARPS, S, STAGES, GAE>, WARPS * 32,
-                                                    dyn);
-      int64_t grid = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
-      if (grid > groups) grid = groups;
-      return launch_pdl(k_scan_pipe<COLS, WARPS, S, STAGES, GAE>, dim3((unsigned)grid), dim3(WARPS * 32), dyn, st, mr,
-                        mv, md, mo0, mo1, boot, T, B, gamma, lam, (GAE && o1) ? 1 : 0, vterm);
+  if ((var == 0 || var == 9) && T < (1ll << 31) && B < (1ll << 31)) {  // default: persistent pipeline
+    bool used = false;
+    const int rc = launch_scan_pipe<16, 8, 8, 3, GAE, 2>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used);
+    if (used) return rc;
+  }
+  if (var >= 10 && var <= 17 && T < (1ll << 31) && B < (1ll << 31)) {  // pipeline shapes (A/B)
+    bool used = false;
+    int rc = RPL_OK;
+    switch (var) {
+      case 10: rc = launch_scan_pipe<32, 8, 16, 2, GAE, 1>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used); break;
+      case 11: rc = launch_scan_pipe<32, 16, 8, 2, GAE, 1>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used); break;
+      case 12: rc = launch_scan_pipe<16, 8, 8, 2, GAE, 3>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used); break;
+      case 13: rc = launch_scan_pipe<32, 8, 8, 2, GAE, 2>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used); break;
+      case 14: rc = launch_scan_pipe<32, 8, 16, 3, GAE, 1>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used); break;
+      case 15: rc = launch_scan_pipe<32, 8, 8, 3, GAE, 2>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used); break;
+      case 16: rc = launch_scan_pipe<32, 8, 16, 2, GAE, 2, 1>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used); break;
+      default: rc = launch_scan_pipe<32, 4, 32, 2, GAE, 2, 1>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used); break;
     }
+    if (used) return rc;
   }
   if ((var == 7 || var == 8) && T < (1ll << 31) && B < (1ll << 31)) {
     CUtensorMap mr, mv, md;
@@ -1026,7 +1054,7 @@ int launch_scan(const float* r, const float* v, const uint8_t* d, const float* b
                         md, boot, T, B, gamma, lam, o0, o1, scan_trigger(), vterm);
     }
   }
-  if ((var == 0 || var == 6) && T < (1ll << 31) && B < (1ll << 31)) {
+  if ((var == 0 || var == 6) && T < (1ll << 31) && B < (1ll << 31)) {  // whole-column tiles (r1 default)
     CUtensorMap mr, mv, md;
     constexpr int CH = SCAN_WARPS * SCAN_S;
     if (tmap_2d(&mr, r, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, T, B, CH) &&
@@ -1107,7 +1135,7 @@ extern "C" int rpl_value_rescale(const float* x, float* y, int64_t n, double eps
 }
 
 extern "C" int rpl_debug_set_scan_variant(int32_t variant) {
-  if (variant < 0 || variant > 9) return RPL_EINVAL;
+  if (variant < 0 || variant > 17) return RPL_EINVAL;
   g_scan_variant.store(variant);
   return RPL_OK;
 }

@@ -654,6 +654,16 @@ class GatherPlan:
         self.desc.peer_world = int(world) if board_ptrs is not None else 0
         self.desc.peer_rank = int(rank) if board_ptrs is not None else 0
 
+    def run_sample(self, tree, seed, idx_out, q_out, beta=0.0, err=None, stream=None, q_tgt=None):
+        """rpl_gather_sample: draw this call's n stratified samples from `tree` (its stream)
+        inside the gather; idx_out / q_out receive them, outputs["w"] the IS weights."""
+        s = _stream(self.device) if stream is None else stream
+        if q_tgt is not None:
+            self.desc.q_tgt = q_tgt.data_ptr()
+        check(lib.rpl_gather_sample(self._dp, tree._lp, _ptr(tree.storage), int(seed) & (2 ** 64 - 1), _ptr(idx_out),
+                                    _ptr(q_out), float(beta), self.n, _ptr(err), s), "rpl_gather_sample")
+        return self.outputs
+
     def run(self, idx, q=None, qmin=None, beta=0.0, err=None, stream=None, q_tgt=None):
         """q_tgt: this call's bootstrap values for the fused targets (f32 [L, n]; None keeps
         the one set before)."""

@@ -572,3 +572,43 @@ def test_transition_time_limit_bootstrap(rpl):
         check_rel(H(out["ret"]), ref["ret"], absR, what="time-limit ret")
         assert np.array_equal(H(out["done_n"]), ref["done_n"])
         assert np.array_equal(H(out["obs"]), ref["obs"]) and np.array_equal(H(out["next_obs"]), ref["next_obs"])
+
+
+@pytest.mark.parametrize("L,k,n_s,period", [(125, 4, 64, 40), (45, 4, 300, 40), (5, 4, 33, 8), (1, 1, 7, 4)])
+def test_gather_sample_equals_sample_then_gather(rpl, L, k, n_s, period):
+    # a8 fused into the sequence gather (rpl_gather_sample): same indices, q, IS weights and
+    # every output as rpl_sumtree_sample_stream followed by rpl_gather, over three chained
+    # calls (the tree's stream position advances identically)
+    import torch
+    cap, B = 400, 4
+    ring = make_ring(70 + L, cap=cap, B=B, ep_len=12.0, period=period, rnn_h=8, reward_kind="r2d2",
+                     obs_shape=(16, 24))
+    dr = dev_ring(rpl, ring)
+    nb = cap // period
+    g = rng(L + n_s)
+    t1, t2 = rpl.SumTree(nb * B, 32), rpl.SumTree(nb * B, 32)
+    valid = [b_ * B + c for b_ in range(nb) if OG.window_valid_sequence(b_ * period, cap, ring.cursor, ring.size, k, L)
+             for c in range(B)]
+    td = np.abs(g.normal(size=len(valid))).astype(np.float32)
+    for t in (t1, t2):
+        t.update(T_(np.array(valid, np.int64)), T_(td), 0.9)
+    tg = dict(lo=0, T=max(1, L - 6), n_step=5, gamma=0.99, rescale=True, q=T_(g.normal(0, 5, (L, n_s)).astype(np.float32))) if L > 6 else None
+    p1 = rpl.GatherPlan(dr, n_s, kind="sequence", k=k, seq_len=L, period=period, with_weights=True, targets=tg)
+    p2 = rpl.GatherPlan(dr, n_s, kind="sequence", k=k, seq_len=L, period=period, with_weights=True, targets=tg)
+    e1, e2 = (torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(2))
+    for step in range(3):
+        i1, q1 = (torch.empty(n_s, dtype=torch.int64, device="cuda") for _ in range(2))
+        t1.sample_stream(n_s, 77, out=(i1, q1, None, None), err=e1, want_qmin=False)
+        o1 = p1.run(i1, q=q1, beta=0.6, err=e1)
+        i2, q2 = (torch.full((n_s,), -9, dtype=torch.int64, device="cuda") for _ in range(2))
+        o2 = p2.run_sample(t2, 77, i2, q2, beta=0.6, err=e2)
+        torch.cuda.synchronize()
+        assert np.array_equal(H(i1), H(i2)) and np.array_equal(H(q1), H(q2)), step
+        for name in o1:
+            assert np.array_equal(H(o1[name]), H(o2[name])), (step, name)
+        assert np.array_equal(H(t1.header), H(t2.header)), step
+        assert int(H(e1)[0]) == int(H(e2)[0]) == 0
+        # the next step's priorities for the sampled leaves (same on both trees)
+        ntd = np.abs(g.normal(size=n_s)).astype(np.float32)
+        t1.update(i1, T_(ntd), 0.9)
+        t2.update(i2, T_(ntd), 0.9)
