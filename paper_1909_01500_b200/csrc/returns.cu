@@ -884,8 +884,9 @@ int elementwise_grid(int64_t work, int threads) {
 using namespace rpl;
 
 // Measurement-only knob (RPL_SCAN_VARIANT): 0 = default (the persistent pipelined scan,
-// k_scan_pipe, when the layout is TMA-addressable — B % 4 == 0 for f32 and B % 16 == 0 for
-// the u8 done tiles — else LDG 16 warps x 8 rows), 9 = the same pipeline, 6 = whole-column
+// k_scan_pipe, 32 x 128 tiles, when the layout is TMA-addressable — B % 4 == 0 for f32 and
+// B % 16 == 0 for the u8 done tiles — else LDG 16 warps x 8 rows), 9 = the pipeline with 16 x
+// 128 tiles and two CTAs per SM, 10-17 = further pipeline shapes (A/B), 6 = whole-column
 // TMA tiles (the round-1 default), 7 = 16-column TMA tiles, double-buffered chunks, 8 = 32
 // columns x 64 rows double-buffered, 4 = cluster of 2 CTAs x 64 rows (T <= 128, else
 // default), 5 = cluster of 4 CTAs x 32 rows, 3 = LDG 16 warps x 8 rows, 1 = LDG 32 warps x 4
@@ -1020,8 +1021,14 @@ int launch_scan(const float* r, const float* v, const uint8_t* d, const float* b
     if (used) return rc;
   }
   if ((var == 0 || var == 9) && T < (1ll << 31) && B < (1ll << 31)) {  // default: persistent pipeline
+    // default shape: 32-column groups (128-B tile rows), 8 warps x 16 rows = 128-row chunks, 3
+    // load stages, one CTA per SM (scan size sweep, profiles/r2/scan_ab_*.json: GAE 0.75-0.76
+    // and discounted 0.58-0.74 of measured HBM on 34-285 MB calls, PPO GAE 4.49 us); variant 9
+    // keeps the 16-column / 2-CTAs-per-SM shape measured first.
     bool used = false;
-    const int rc = launch_scan_pipe<16, 8, 8, 3, GAE, 2>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used);
+    const int rc = var == 0
+                       ? launch_scan_pipe<32, 8, 16, 3, GAE, 1>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used)
+                       : launch_scan_pipe<16, 8, 8, 3, GAE, 2>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used);
     if (used) return rc;
   }
   if (var >= 10 && var <= 17 && T < (1ll << 31) && B < (1ll << 31)) {  // pipeline shapes (A/B)

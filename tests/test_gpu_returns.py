@@ -64,7 +64,7 @@ SHAPES = [(1, 1), (1, 7), (5, 3), (16, 32), (127, 33), (128, 64), (129, 31), (30
           (129, 16), (1000, 80), (257, 4096), (20, 64), (65, 16), (97, 48), (33, 4096)]
 
 
-@pytest.fixture(params=[0, 6, 4, 5, 3, 7, 8])
+@pytest.fixture(params=[0, 9, 6, 4, 5, 3, 7, 16])
 def scan_variant(rpl, request):
     assert rpl._lib.lib.rpl_debug_set_scan_variant(request.param) == 0
     yield request.param
