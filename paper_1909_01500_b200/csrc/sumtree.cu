@@ -10,7 +10,7 @@
 //  update  one CTA: priority transform (crpow.cuh) -> last-writer-wins dedupe in a
 //          shared-memory hash table (atomicMax of batch position per leaf) -> the
 //          winner writes its leaf and adds its int64 delta to each ancestor
-//          (root delta warp-aggregated).  Chunks of 1024 entries are applied in
+//          (root delta warp-aggregated).  Chunks of 512 entries (the CTA size) are applied in
 //          batch order, so any batch size keeps last-write-wins.
 //  sample  one warp per draw: integer stratum -> prefix -> per level the warp loads
 //          the W child sums (one coalesced 256-B load), inclusive int64 warp scan,
