@@ -138,7 +138,9 @@ int rpl_value_rescale(const float* x, float* y, int64_t n, double eps, int32_t i
  *     (§8c #7).  Header: [hdr_off+0] max-priority-seen, [hdr_off+1] sampler
  *     ticket (library scratch, always 0 between calls), [hdr_off+2] Philox stream
  *     position used by rpl_sumtree_sample_stream (0 after init), [hdr_off+3] grid-barrier
- *     arrivals (scratch, 0 between calls), [hdr_off+4] grid-barrier generation (scratch).
+ *     arrivals (scratch, 0 between calls), [hdr_off+4] grid-barrier generation (scratch),
+ *     [hdr_off+5] the attached min-tree's device address (0 = none; rpl_mintree_attach),
+ *     [hdr_off+6] the global buffer min written by the sharded samplers, [hdr_off+7] unused.
  * ========================================================================= */
 typedef struct {
   int64_t n_leaves;
@@ -152,9 +154,6 @@ typedef struct {
   int64_t hdr_off;
   int64_t n_words;      /* int64 words the caller must allocate */
 } rpl_tree_layout;
-
-/* Header words 5-6 (rpl_mintree_attach): [hdr_off+5] the attached min-tree's device address
- * (0 = none), [hdr_off+6] the global buffer min written by the sharded samplers. */
 
 /* Fill *out (host) for n_leaves >= 1, fanout in {2,4,8,16,32}, frac_bits in [0,62]. */
 int rpl_sumtree_layout(int64_t n_leaves, int32_t fanout, int32_t frac_bits, rpl_tree_layout* out);

@@ -155,9 +155,31 @@ int launch_coop(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
   return RPL_OK;
 }
 
+// fp64 reciprocal and square root without the IEEE slow paths: the hardware approximation
+// (MUFU on the high word) refined by two Newton steps to full double precision (relative
+// error ~1e-16; not always correctly rounded).  Arguments here are finite and >= 1, or
+// inf / NaN which propagate.  Used by h / h^-1, whose outputs are rounded to fp32.
+__device__ __forceinline__ double rcp64(double y) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+  double e = fma(-y, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-y, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double sqrt64(double y) {  // y >= 1 (or inf / NaN)
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+  const double hy = 0.5 * y;
+  r = r * fma(-hy * r, r, 1.5);
+  r = r * fma(-hy * r, r, 1.5);
+  const double s = y * r;
+  return isinf(y) ? y : fma(0.5 * r, fma(-s, s, y), s);
+}
+
 __device__ __forceinline__ double h_fwd(double x, double eps) {
   // h(x) = x (1/(sqrt(|x|+1)+1) + eps)  ==  sign(x)(sqrt(|x|+1)-1) + eps x   (§8c #4)
-  return x * (1.0 / (sqrt(fabs(x) + 1.0) + 1.0) + eps);
+  return x * (rcp64(sqrt64(fabs(x) + 1.0) + 1.0) + eps);
 }
 
 __device__ __forceinline__ double h_inv(double y, double eps) {
@@ -165,8 +187,8 @@ __device__ __forceinline__ double h_inv(double y, double eps) {
   // x = (s-1)(s+1) with s-1 = |y| / (1 + eps (s+1))            (§8c #4)
   const double a = fabs(y);
   const double c = a + 1.0 + eps;
-  const double s = 2.0 * c / (1.0 + sqrt(1.0 + 4.0 * eps * c));
-  const double x = a * (s + 1.0) / (1.0 + eps * (s + 1.0));
+  const double s = 2.0 * c * rcp64(1.0 + sqrt64(1.0 + 4.0 * eps * c));
+  const double x = a * (s + 1.0) * rcp64(1.0 + eps * (s + 1.0));
   return copysign(x, y);
 }
 

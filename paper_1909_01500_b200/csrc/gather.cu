@@ -932,6 +932,10 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   __shared__ short row_tau[PL_MAX_ROWS];
   __shared__ int8_t start_off[PL_MAX_ROWS];
   __shared__ volatile int row_done[PL_MAX_ROWS];
+  // frame positions issued so far (producer, release): a consumer waits on a slot's mbarrier
+  // only once the phase it needs is armed, so a parity test can never match a phase two
+  // rounds old (a consumer warp may run ahead of another warp's rows)
+  __shared__ volatile int s_issued;
   __shared__ int s_npieces;
   __shared__ int64_t p_leaf[PL_MAX_ROWS];  // fused sampling: the piece's sampled leaf
   constexpr int NT = (NC + 2) * 32;
@@ -948,6 +952,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
     fence_mbar_init();
   }
   for (int c = tid; c < PL_MAX_ROWS; c += NT) row_done[c] = 0;
+  if (tid == 0) s_issued = 0;
   if (RPL_PDL_EARLY & 4) pdl_trigger();  // A/B knob (common.cuh)
   pdl_wait();  // idx (and n_active) come from the sampler launched just before
   // Fused sampling (rpl_gather_sample): the tree was updated by the kernel before; every
@@ -1091,6 +1096,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
             if (GDIAG(D) & 8) bulk_g2s(smem + slot * ob, src, (uint32_t)ob, &full[slot]);
             else bulk_g2s_evict_first(smem + slot * ob, src, (uint32_t)ob, &full[slot]);
           }
+          flag_release(&s_issued, i + 1);
           if (++row == cap) row = 0;
           if (++slot == NS) slot = 0;
         }
@@ -1253,6 +1259,8 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
           }
           return sl;
         };
+        if (pn >= 0)  // every frame this row reads (positions <= pn) has its phase armed
+          while (flag_acquire(&s_issued) <= pn) __nanosleep(20);
         if (pn >= 0 && unique) {
           // RPL_OUT_UNIQUE: raw rows, each written once — row tau stores its newest frame
           // (unique row tau+k-1); the sample's first row also stores unique rows 0..k-2
@@ -1679,6 +1687,7 @@ k_gather_trans_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int SPF
   __shared__ volatile int sdone[TP_MAX_S]; // stacks written (0..2)
   __shared__ int s_arm[TP_MAX_S];          // armed (loaded) samples before this one (-1: skipped)
   __shared__ int s_of_arm[TP_MAX_S];       // sample of armed index a
+  __shared__ volatile int s_armed;         // armed samples issued so far (producer, release)
   constexpr int NT = (NC + 2) * 32;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k = D.k, ns = D.n_step, NR = k + ns;
@@ -1711,6 +1720,7 @@ k_gather_trans_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int SPF
     s_r[j] = row;
     sdone[j] = bcol < 0 ? 2 : 0;
   }
+  if (tid == 0) s_armed = 0;
   __syncthreads();
   // Slot groups and mbarrier phases follow the ARMED samples only (skipped entries — idx < 0
   // or out of range — load nothing and must not consume a phase): armed index a of sample j
@@ -1751,6 +1761,7 @@ k_gather_trans_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int SPF
           bulk_g2s_evict_first(smem + (grp * NR + w) * ob, col + (int64_t)row * rstride, (uint32_t)ob, &full[grp]);
           if (++row == cap) row = 0;
         }
+        flag_release(&s_armed, a + 1);
       }
     }
   } else if (warp == 1) {
@@ -1797,8 +1808,11 @@ k_gather_trans_pipe(GDesc D, const int64_t* __restrict__ idx, int64_t n, int SPF
       uint8_t* outb = which ? D.o_next_obs : D.o_obs;
       const int a = s_arm[j];
       const int grp = a % SPF;
-      // every consumer observes its group's phase (even without an output), so no CTA exits
-      // with bulk copies into its shared memory still in flight
+      // wait until this sample's phase is armed (a consumer warp may run ahead of the warps
+      // still on the group's previous sample: a bare parity test could then match the phase
+      // two rounds old), then observe it — even without an output, so no CTA exits with
+      // bulk copies into its shared memory still in flight
+      while (flag_acquire(&s_armed) <= a) __nanosleep(20);
       mbar_wait(&full[grp], (uint32_t)((a / SPF) & 1));
       if (outb) {
         int4* dst = reinterpret_cast<int4*>(outb + (coff + s0 + j) * (int64_t)k * ob);

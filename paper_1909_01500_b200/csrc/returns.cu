@@ -846,6 +846,71 @@ __global__ void k_nstep(const float* __restrict__ r, const uint8_t* __restrict__
   }
 }
 
+// n-step targets for n <= NS_MAXN (the common case): thread = (column b, run of NS_U
+// consecutive outputs t0 .. t0+NS_U-1).  The run's NS_U + n - 1 reward / done rows are loaded
+// once into registers (coalesced across the warp's columns, all in flight together) and
+// shared by the run's outputs; the grid is 2-D (columns x runs), so no 64-bit division.
+// Same arithmetic per output as k_nstep (fp64 Horner from the bootstrap, R24 / R34 / R5).
+#ifndef RPL_NSTEP_U  // outputs per thread of k_nstep_runs (build-flag A/B knob; PPO [128,4096] n=5
+#define RPL_NSTEP_U 4  // rescaled: U=1 8.86, 2 8.16, 4 6.94, 8 9.69 us per call, scripts/gpu_ab_nstep.sh)
+#endif
+constexpr int NS_U = RPL_NSTEP_U;
+constexpr int NS_MAXN = 8;
+
+__global__ void __launch_bounds__(128)
+k_nstep_runs(const float* __restrict__ r, const uint8_t* __restrict__ d, int64_t T, int64_t B, int n, double gamma,
+             const float* __restrict__ q, const float* __restrict__ q_boot, int rescale, double eps,
+             float* __restrict__ out, uint8_t* __restrict__ done_out, const float* __restrict__ vterm) {
+  if (RPL_PDL_EARLY & 8) pdl_trigger();  // A/B knob (common.cuh)
+  pdl_wait();
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t rows = T - n + 1;
+  const int64_t t0 = (int64_t)blockIdx.y * NS_U;
+  if (b >= B || t0 >= rows) return;
+  constexpr int W = NS_U + NS_MAXN - 1;
+  float rw[W];
+  uint8_t dw[W];
+  const int nload = (int)min((int64_t)(NS_U + n - 1), T - t0);
+  const float* rp = r + t0 * B + b;
+  const uint8_t* dp = d + t0 * B + b;
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    rw[i] = i < nload ? __ldg(rp + (int64_t)i * B) : 0.0f;
+    dw[i] = i < nload ? __ldg(dp + (int64_t)i * B) : (uint8_t)0;
+  }
+  float qv[NS_U];
+  if (q != nullptr) {
+#pragma unroll
+    for (int u = 0; u < NS_U; ++u) {
+      const int64_t tq = t0 + u + n;
+      qv[u] = t0 + u < rows ? (tq < T ? __ldg(q + tq * B + b) : __ldg(q_boot + b)) : 0.0f;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < NS_U; ++u) {
+    if (t0 + u >= rows) break;
+    double acc = 0.0;
+    if (q != nullptr) acc = rescale ? h_inv((double)qv[u], eps) : (double)qv[u];
+    uint8_t dn = 0;
+#pragma unroll
+    for (int j = NS_MAXN - 1; j >= 0; --j) {
+      if (j < n) {
+        const int i = u + j;
+        const double ri = (double)rw[i];
+        if (dw[i]) {
+          acc = (vterm && dw[i] == RPL_DONE_TIMEOUT) ? fma(gamma, (double)__ldg(vterm + (t0 + i) * B + b), ri) : ri;
+        } else {
+          acc = fma(gamma, acc, ri);
+        }
+        dn |= dw[i];
+      }
+    }
+    if (rescale) acc = h_fwd(acc, eps);
+    out[(t0 + u) * B + b] = (float)acc;
+    if (done_out != nullptr) done_out[(t0 + u) * B + b] = dn ? 1 : 0;
+  }
+}
+
 __global__ void k_rescale(const float* __restrict__ x, float* __restrict__ y, int64_t n,
                           double eps, int inverse) {
   pdl_wait();
@@ -1122,6 +1187,11 @@ extern "C" int rpl_returns_nstep_tl(const float* r, const uint8_t* d, const floa
 #define RPL_NSTEP_THREADS 128  // same-box A/B: 69.55 vs 69.82 us per R2D2 step at 256 (64: 69.68)
 #endif
   const int threads = RPL_NSTEP_THREADS;
+  const int64_t runs = (T - n + 1 + NS_U - 1) / NS_U;
+  if (n <= NS_MAXN && runs < 65536)  // register runs (the common n), 2-D grid
+    return launch_pdl(k_nstep_runs, dim3((unsigned)((B + 127) / 128), (unsigned)runs), dim3(128), 0,
+                      as_stream(stream), r, d, T, B, (int)n, gamma, q, q_boot, rescale ? 1 : 0, rescale_eps, ret_n,
+                      done_n, v_term);
   return launch_pdl(k_nstep, dim3(elementwise_grid(work, threads)), dim3(threads), 0, as_stream(stream), r, d, T, B,
                     (int)n, gamma, q, q_boot, rescale ? 1 : 0, rescale_eps, ret_n, done_n, v_term);
 }
