@@ -55,7 +55,9 @@ def test_c51_projection(rpl, n, A, N):
     m, a = rpl.c51_project(T_(p), None if qo is None else T_(qo), T_(R), T_(dn), -10.0, 10.0, 0.99 ** 3)
     ref = OT.c51_targets(p, qo, R, dn, 0.99 ** 3, -10.0, 10.0)
     mm = H(m)
-    assert np.abs(mm - ref).max() <= 1e-6                     # probabilities: absolute 1e-6
+    # R21's rule with the distribution's total mass (1) as the scale: 1e-5 relative per atom,
+    # and for atoms below 1e-6 of the mass (pure rounding territory) 1e-11 absolute
+    check_rel(mm, ref, np.ones_like(ref), what="c51 projection")
     assert np.allclose(mm.sum(-1), p.sum(-1)[np.arange(n), H(a)], atol=1e-5)
     if qo is not None:
         assert np.array_equal(H(a), [OT.argmax_first(qo[s]) for s in range(n)])
