@@ -328,7 +328,7 @@ def run_rpl(args):
     Tn = c["train"] + c["n_step"] - 1
     lib, P_ = rpl._lib.lib, rpl.ops._ptr
 
-    def step(i, gather_events=None, y_out=None, w_out=None, io=None):
+    def step(i, gather_events=None, y_out=None, w_out=None, io=None, skip_gather=False):
         # y_out / w_out: per-step output buffers; io = (td, q, cur_idx, prev_idx) per-step
         # inputs / index buffers (the e2e schedule gives every step of a graph its own)
         s = rpl.ops._stream(dev)
@@ -365,6 +365,8 @@ def run_rpl(args):
                                                           P_(totals), n_glob, None, seed, 0, 1, P_(cur), P_(q_buf),
                                                           P_(qmin), P_(n_owned), P_(err), s), "sample_sharded")
             dist.all_reduce(qmin, op=dist.ReduceOp.MIN)                          # K7: global batch min
+        if skip_gather:  # marginal-cost measurement: the same step without the gather launch
+            return
         if gather_events is not None:
             gather_events[0].record()
         # IS weights fused into the gather: batch min (1 GPU) or the all-reduced global min (Mode L)
@@ -527,6 +529,16 @@ def run_rpl(args):
         except Exception as e:  # pragma: no cover - keep the eager figure
             print(f"[bench] in-graph gather timing failed ({type(e).__name__}: {e})", file=sys.stderr)
     g_ms = g_ms_graph if g_ms_graph is not None else g_ms_eager
+    # the gather's marginal cost in the timed configuration: graphs of P steps with and
+    # without the gather launch (no event node inside the graph, so the PDL edges stay intact)
+    g_ms_marginal = None
+    if use_graph and world == 1:
+        try:
+            full_ms = _graph_time(dev, step, P=P, reps=50)
+            nog_ms = _graph_time(dev, lambda i: step(i, skip_gather=True), P=P, reps=50)
+            g_ms_marginal = full_ms - nog_ms
+        except Exception as e:  # pragma: no cover
+            print(f"[bench] marginal gather timing failed ({type(e).__name__}: {e})", file=sys.stderr)
     owned = n  # per rank, on average
     alg_bytes = owned * seq_bytes_per_sample(c)
     if mode_c:  # Mode C gathers unique rows (the learner re-stacks them)
@@ -569,6 +581,11 @@ def run_rpl(args):
                      "traffic": traffic.get("bytes"), "traffic_source": traffic.get("source"),
                      "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": g_ms,
                      "avg_launch_ms_eager": g_ms_eager,
+                     "marginal_ms": g_ms_marginal,
+                     "frac_marginal": (alg_bytes / (g_ms_marginal / 1e3) / 1e9 / peak) if g_ms_marginal else None,
+                     "marginal_note": ("step graph minus the same graph without the gather launch: the gather's "
+                                       "in-step cost with the PDL edges intact (frac uses the event-bracketed "
+                                       "avg_launch_ms, which includes the gather's launch latency)"),
                      "launch_timing": ("event-record nodes around each gather in the CUDA graph of the timed "
                                        "steps (mean of P launches x 25 replays)" if g_ms_graph is not None
                                        else "events around the gather in eager steps"),

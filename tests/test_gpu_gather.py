@@ -231,15 +231,25 @@ def test_r2d2_full_size_sampled(rpl):
     torch.cuda.empty_cache()
 
 
+def _row_window(dr, row, b, lo, hi):
+    """Host copy of ring rows row+lo .. row+hi-1 (mod cap_T) of column b as a one-column ring."""
+    import torch
+    cap = dr.obs.shape[0]
+    rows = torch.from_numpy((row + np.arange(lo, hi)) % cap).cuda()
+    return (H(dr.obs[rows, b:b + 1]), H(dr.act[rows, b:b + 1]), H(dr.rew[rows, b:b + 1]), H(dr.done[rows, b:b + 1]))
+
+
 def test_dqn_full_size_sampled(rpl):
     # BASELINE configs[2]: [4096, 256] frame ring (2^20 transitions, 7.4 GB), batch 512,
-    # k=4, n=3, gamma=0.99 with fused n-step and IS weights — sampled transitions vs the oracle
+    # k=4, n=3, gamma=0.99 with fused n-step and IS weights — EVERY transition of the batch vs
+    # the oracle, on a ring with short episodes (mean 30 rows) so that episode starts inside
+    # the frame stacks occur at full size
     import torch
     from paper_1909_01500_b200 import replay as R
     from synth.device import make_ring_device
     dev = torch.device("cuda")
     cap, B, k, n = 4096, 256, 4, 3
-    dr = make_ring_device(7, cap, B, dev, ep_len=2000.0, period=64, rnn_h=1, cursor=777)
+    dr = make_ring_device(7, cap, B, dev, ep_len=30.0, period=64, rnn_h=1, cursor=777)
     dr.rnn = None
     rows = R.valid_transition_rows(cap, dr.cursor, dr.size, k, n)
     g = rng(12)
@@ -253,15 +263,18 @@ def test_dqn_full_size_sampled(rpl):
     assert int(H(err)[0]) == 0
     w_ref = OS.is_weights([int(x) for x in q], int(q.sum()), cap * B, 0.4)
     check_rel(H(out["w"]), w_ref, what="w")
-    for s in list(range(0, 512, 37)) + [511]:
+    o_obs, o_next, o_act, o_dn, o_ret = (H(out[x]) for x in ("obs", "next_obs", "act", "done_n", "ret"))
+    padded = 0
+    for s in range(512):
         row, b = divmod(int(leaves[s]), B)
-        obs, act, rew, done, _ = _column_ring(dr, b, False)
-        ref = OG.gather_transitions(np.array([row], np.int64), 1, obs, act, rew, done, k, n, 0.99)
-        assert np.array_equal(H(out["obs"][s]), ref["obs"][0]), s
-        assert np.array_equal(H(out["next_obs"][s]), ref["next_obs"][0]), s
-        assert int(H(out["act"][s])) == int(ref["act"][0])
-        assert int(H(out["done_n"][s])) == int(ref["done_n"][0])
-        check_rel(H(out["ret"][s:s + 1]), ref["ret"][:1], np.abs(ref["ret"][:1]) + 1.0, what="ret")
+        obs, act, rew, done = _row_window(dr, row, b, -8, n + 2)   # the transition sits at window row 8
+        ref = OG.gather_transitions(np.array([8], np.int64), 1, obs, act, rew, done, k, n, 0.99)
+        assert np.array_equal(o_obs[s], ref["obs"][0]), s
+        assert np.array_equal(o_next[s], ref["next_obs"][0]), s
+        assert int(o_act[s]) == int(ref["act"][0]) and int(o_dn[s]) == int(ref["done_n"][0]), s
+        check_rel(o_ret[s:s + 1], ref["ret"][:1], np.abs(ref["ret"][:1]) + 1.0, what="ret")
+        padded += int(done[4:8, 0].any() or done[4 + n:8 + n, 0].any())
+    assert padded > 0  # some stacks crossed an episode start
     del dr
     torch.cuda.empty_cache()
 
