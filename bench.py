@@ -595,6 +595,15 @@ def run_rpl(args):
     }
     if not args.profile:
         result["clocks"] = clk
+    if mode_c:
+        # the central learner's NVLink ingress bounds Mode C — the other ranks' unique
+        # rows + fields cross into rank 0 every step (spec 900 GB/s per direction; not measured here)
+        per_seq = seq_bytes_per_sample(c) - L * k * FRAME + (L + k - 1) * FRAME
+        ingress = (world - 1) / world * n_glob * per_seq
+        result["mode_c_ceiling"] = {"bytes_into_learner_per_step": ingress, "nvlink_ingress_GBps_spec": 900.0,
+                                    "us_per_step_floor": ingress / 900e9 * 1e6,
+                                    "sequences_per_s_ceiling": n_glob / (ingress / 900e9) if ingress else None,
+                                    "note": "the learner then re-stacks the k-frame stacks locally (rpl_stack_frames)"}
         result["e2e"] = e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K_eff, world)
         # a1-a4 at every N: each rank scans its own [128, 4096] columns, no collective
         try:

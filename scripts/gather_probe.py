@@ -20,7 +20,7 @@ for cap, B in [(4000, 256), (1024000, 1)]:
     blocks = R.valid_sequence_blocks(cap, 40, ring.cursor, ring.size, 4, 125)
     leaves = R.leaves_of(blocks, B)
     g = np.random.default_rng(0)
-    for variant in (0, 1, 4, 5):
+    for variant in [int(v) for v in os.environ.get("VARIANTS", "0,1,4,5").split(",")]:
         rpl._lib.lib.rpl_debug_set_gather_variant(variant)
         for mode in ("stacked", "unique"):
             if mode == "unique" and variant not in (0, 1):

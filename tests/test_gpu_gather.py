@@ -461,8 +461,10 @@ def test_random_gather_stress(rpl):
             total_tr += idx.size
 
 
-@pytest.mark.parametrize("skip_pattern", ["isolated", "odd_runs"])
-def test_transition_pipeline_skipped_entries(rpl, skip_pattern):
+@pytest.mark.parametrize("skip_pattern,n_step", [("isolated", 3), ("odd_runs", 3), ("isolated", 5), ("odd_runs", 6)])
+def test_transition_pipeline_skipped_entries(rpl, skip_pattern, n_step):
+    # n_step 5 / 6 give 9 / 10 frames per sample, i.e. 3 / 2 slot groups (an odd group count:
+    # consumer warps then run ahead of the group's previous sample, the armed counter case)
     # Persistent transition pipeline with more samples per CTA than slot groups (n = 2048,
     # Atari frames: ~14 samples per CTA, 4 groups) and skipped entries (idx = -1) in between:
     # slot groups / mbarrier phases follow the loaded samples only (a skipped entry used to
@@ -471,17 +473,17 @@ def test_transition_pipeline_skipped_entries(rpl, skip_pattern):
     ring = make_ring(77, cap=256, B=8, ep_len=40.0)
     dr = dev_ring(rpl, ring)
     g = rng(8)
-    idx = valid_transition_leaves(ring, 4, 3, 2048, g)
+    idx = valid_transition_leaves(ring, 4, n_step, 2048, g)
     if skip_pattern == "isolated":
         idx[1::7] = -1
     else:  # runs of 1, 3 and 5 skipped entries
         for s0, ln in ((1, 1), (20, 3), (100, 5), (1500, 1), (2040, 3)):
             idx[s0:s0 + ln] = -1
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
-    out = rpl.gather(dr, T_(idx), kind="transition", k=4, n_step=3, gamma=0.99, err=err)
+    out = rpl.gather(dr, T_(idx), kind="transition", k=4, n_step=n_step, gamma=0.99, err=err)
     torch.cuda.synchronize()
     assert int(H(err)[0]) == 0
-    ref = OG.gather_transitions(idx, 8, ring.obs, ring.act, ring.rew, ring.done, 4, 3, 0.99)
+    ref = OG.gather_transitions(idx, 8, ring.obs, ring.act, ring.rew, ring.done, 4, n_step, 0.99)
     ok = idx >= 0
     assert np.array_equal(H(out["obs"])[ok], ref["obs"][ok])
     assert np.array_equal(H(out["next_obs"])[ok], ref["next_obs"][ok])
