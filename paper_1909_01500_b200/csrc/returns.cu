@@ -630,8 +630,10 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
     }
     if (++st == STAGES) st = 0;
   }
-  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
+  // the dependent grid may launch now; the CTA stays until its last output tile has been read
+  // out of shared memory (the bulk stores complete before the grid does, as for any store)
   pdl_trigger();
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
