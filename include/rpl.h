@@ -155,7 +155,13 @@ typedef struct {
   int64_t n_words;      /* int64 words the caller must allocate */
 } rpl_tree_layout;
 
-/* Fill *out (host) for n_leaves >= 1, fanout in {2,4,8,16,32}, frac_bits in [0,62]. */
+/* The tree of n_leaves leaves ("prioritized replay (sum tree)"; S:556-557 sum tree over
+ * the priorities; reading R7 for F = frac_bits, the fixed-point fraction of a leaf q, and
+ * q_cap = floor((2^63-1)/n_leaves), so the root of any leaf values <= q_cap fits in int64):
+ * fills *out (host POD) with the depth, every level's offset and padded length and n_words,
+ * the int64 words the caller allocates (the library never allocates).  n_leaves >= 1, fanout
+ * in {2,4,8,16,32}, frac_bits in [0,62]; RPL_EINVAL otherwise, RPL_EUNSUPPORTED when the depth
+ * would exceed RPL_MAX_LEVELS - 1.  Host only: enqueues nothing. */
 int rpl_sumtree_layout(int64_t n_leaves, int32_t fanout, int32_t frac_bits, rpl_tree_layout* out);
 
 /* Zero every node and set max-seen to 2^F (priority 1.0, §8c #12). */
@@ -318,7 +324,8 @@ int rpl_sumtree_find(const rpl_tree_layout* L, const int64_t* tree, const int64_
  * grid-wide read of the leaf level. */
 int rpl_sumtree_min(const rpl_tree_layout* L, const int64_t* tree, int64_t* out_min, void* stream);
 
-/* *out_total = root (int64, device). */
+/* *out_total = the root, i.e. the exact total priority mass Q = sum of the leaves (S:601-603
+ * "total()"; the K5 value a shard publishes, §8e).  out_total: device int64.  One thread. */
 int rpl_sumtree_total(const rpl_tree_layout* L, const int64_t* tree, int64_t* out_total, void* stream);
 
 /* Buffer-wide IS normaliser (§8f NEXT-4, reading R29; PER's "normalised by max w" over the
@@ -348,7 +355,10 @@ int rpl_sumtree_sample_sharded_pairs(const rpl_tree_layout* L, int64_t* tree, in
                                      int64_t* out_idx, int64_t* out_q, int64_t* out_qmin, int64_t* out_count,
                                      int64_t* out_bufmin, int32_t* dev_err, void* stream);
 
-/* Recompute every internal node from the leaves (resume after restoring leaves). */
+/* Recompute every internal node from the leaves as their exact int64 range sums (the
+ * sum-tree invariant; SURVEY §5 checkpoint / resume: a checkpoint stores leaves + header
+ * words, and this restores the rest), and rebuild an attached min-tree (R29).  Level by level
+ * from the leaves' parents to the root; padding nodes become 0. */
 int rpl_sumtree_rebuild(const rpl_tree_layout* L, int64_t* tree, void* stream);
 
 /* Uniform replay (SAC/TD3 Mujoco config, BASELINE configs[3]; "uniform
