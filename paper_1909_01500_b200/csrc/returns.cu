@@ -505,11 +505,12 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
   uint32_t phases = 0;  // bit st: parity to wait for on stage st
   int64_t g = blockIdx.x, c = nchunks - 1;
   int st = 0;
+  float boot_f = 0.0f;  // V_T of this thread's column (GAE): loaded once per group, only read in its last chunk
   for (int64_t i = 0; i < items; ++i) {
     const int ob = OB == 1 ? 0 : (int)(i & 1);
     const int64_t col = g * COLS + ci;
     const bool cv = col < B;
-    const double bootv = (GAE && cv) ? (double)__ldg(boot + col) : 0.0;
+    if (GAE && c == nchunks - 1) boot_f = cv ? __ldg(boot + col) : 0.0f;  // in flight during the tile wait
     if (c == nchunks - 1 && w == 0 && lane < COLS) {  // a new group: carry = R_T (or A_T = 0), V_T
       const int64_t cc = g * COLS + lane;
       sm.carry[lane] = (!GAE && boot != nullptr && cc < B) ? (double)__ldg(boot + cc) : 0.0;
@@ -534,10 +535,11 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
       rr[k] = sm.r[st][seg * S + k][ci];
       const uint8_t di = sm.d[st][seg * S + k][ci];
       dmask |= (di ? 1u : 0u) << k;
-      tmask |= (di == RPL_DONE_TIMEOUT ? 1u : 0u) << k;
+      if (vterm) tmask |= (di == RPL_DONE_TIMEOUT ? 1u : 0u) << k;
       if (GAE) vv[k] = sm.v[st][seg * S + k][ci];
     }
     __syncthreads();  // (1) the new group's carry is visible; every thread holds its rows
+    const double bootv = (double)boot_f;
     double vseg_next = 0.0;
     if (GAE) {
       if (t0 + S >= T) vseg_next = bootv;
