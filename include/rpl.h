@@ -652,6 +652,11 @@ int rpl_debug_set_tree_stage(int32_t on);
  * RPL_EUNSUPPORTED for a non-zero mask in the default build (RPL_GATHER_DIAG is ignored there). */
 int rpl_debug_set_gather_diag(int32_t mask);
 
+/* Measurement builds only (-DRPL_TRACE): copies the update kernel's last globaltimer
+ * timeline (n <= 16 int64 ns stamps, host out) — kernel start, staged / mixed sequence
+ * priorities, hash reset, dedupe, leaf writes, end.  RPL_EUNSUPPORTED in the default build. */
+int rpl_debug_trace(int64_t* out, int32_t n);
+
 #ifdef __cplusplus
 }
 #endif

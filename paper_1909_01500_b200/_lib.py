@@ -125,6 +125,7 @@ _SIGS = {
     "rpl_debug_set_scan_variant": ([I32], C.c_int),
     "rpl_debug_set_tree_stage": ([I32], C.c_int),
     "rpl_debug_set_gather_diag": ([I32], C.c_int),
+    "rpl_debug_trace": ([P, I32], C.c_int),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -73,6 +73,18 @@ enum { MODE_TD = 0, MODE_Q = 1, MODE_MAXSEEN = 2, MODE_SEQ = 3 };
 // Header words (rpl.h): 0 max-seen, 1 sampler ticket, 2 stream position, 3-4 grid barrier,
 // 5 attached min-tree address (0: none), 6 global buffer min of the last sharded sample.
 constexpr int HDR_MINTREE = 5;
+// Measurement-only timeline of the update kernel (-DRPL_TRACE builds; rpl_debug_trace).
+#ifdef RPL_TRACE
+__device__ unsigned long long g_trace[16];
+#define UPD_TRACE(k)                                          \
+  do {                                                        \
+    if (threadIdx.x == 0 && blockIdx.x == 0) g_trace[k] = global_ns(); \
+  } while (0)
+#else
+#define UPD_TRACE(k) \
+  do {               \
+  } while (0)
+#endif
 constexpr int HDR_GLOBAL_MIN = 6;
 
 // R2D2 sequence priority (§8f NEXT-1, reading R26): column i of the time-major per-step
@@ -220,6 +232,7 @@ __device__ __forceinline__ uint32_t hash_slot(int64_t leaf) {
   return (uint32_t)(((unsigned long long)leaf * 0x9E3779B97F4A7C15ull) >> 53) & (HASH_SLOTS - 1);
 }
 
+
 struct UpdSmem {
   unsigned long long hkey[HASH_SLOTS];
   int hval[HASH_SLOTS];
@@ -229,10 +242,10 @@ struct UpdSmem {
 
 // The whole batch update by ONE block of NT threads (NT <= UPD_THREADS, a multiple of 32;
 // every thread must call): entries are processed in chunks of NT in batch order.
-template <int NT>
+template <int NT, int mode>
 __device__ __forceinline__ void tree_update_block(UpdSmem& S, const TreeDev& L, int64_t* __restrict__ tree,
                                                   const int64_t* __restrict__ idx, const float* __restrict__ td,
-                                                  const int64_t* __restrict__ qin, int mode, int64_t n, double alpha,
+                                                  const int64_t* __restrict__ qin, int64_t n, double alpha,
                                                   double eps_p, int32_t* err, int force_slow, int64_t T_p, double eta,
                                                   int live_only) {
   unsigned long long* hkey = S.hkey;
@@ -260,10 +273,6 @@ __device__ __forceinline__ void tree_update_block(UpdSmem& S, const TreeDev& L, 
   int32_t errbits = 0;
 
   for (int64_t base = 0; base < n; base += NT) {
-    for (int s = tid; s < HASH_SLOTS; s += NT) {
-      hkey[s] = HASH_EMPTY;
-      hval[s] = -1;
-    }
     if (mode == MODE_SEQ) {  // this chunk's sequence priorities, 8 lanes per sequence
       const int64_t cnt = min((int64_t)NT, n - base);
       for (int64_t r0 = 0; r0 < cnt; r0 += NT / 8) {
@@ -271,8 +280,14 @@ __device__ __forceinline__ void tree_update_block(UpdSmem& S, const TreeDev& L, 
         const float v = sequence_td8(td, T_p, n, base + jj, jj < cnt, eta);
         if ((tid & 7) == 0 && jj < cnt) s_td[jj] = v;
       }
+      UPD_TRACE(2);
+    }
+    for (int s = tid; s < HASH_SLOTS; s += NT) {
+      hkey[s] = HASH_EMPTY;
+      hval[s] = -1;
     }
     __syncthreads();
+    UPD_TRACE(3);
     const int64_t i = base + tid;
     int64_t leaf = -1, q = 0;
     if (i < n) {
@@ -326,6 +341,7 @@ __device__ __forceinline__ void tree_update_block(UpdSmem& S, const TreeDev& L, 
       atomicMax(&hval[slot], tid);  // last position in the batch wins
     }
     __syncthreads();
+    UPD_TRACE(4);
     int64_t delta = 0;
     if (leaf >= 0 && hval[slot] == tid) {
       // earlier chunks may have rewritten this leaf: reload unless the batch is one chunk
@@ -345,6 +361,7 @@ __device__ __forceinline__ void tree_update_block(UpdSmem& S, const TreeDev& L, 
     if (lane == 0 && rd != 0)
       atomicAdd(reinterpret_cast<unsigned long long*>(tree + L.level_off[0]), (unsigned long long)rd);
     __syncthreads();
+    UPD_TRACE(5);
   }
   // max-priority-seen
   int64_t m = warp_max64(local_max);
@@ -356,6 +373,7 @@ __device__ __forceinline__ void tree_update_block(UpdSmem& S, const TreeDev& L, 
     if (tid == 0 && m > maxseen_now) atomicMax(reinterpret_cast<long long*>(hdr), (long long)m);
   }
   if (errbits) set_err(err, errbits);
+  UPD_TRACE(6);
   // Min-tree maintenance (buffer-wide IS normaliser, R29): every internal min node on a
   // written leaf's path is recomputed from its W children, level by level from the leaves'
   // parents up (a barrier between levels), each distinct node by one thread (hash dedupe per
@@ -409,14 +427,18 @@ __device__ __forceinline__ void tree_update_block(UpdSmem& S, const TreeDev& L, 
   }
 }
 
+// One instantiation per mode: each kernel carries only its own path (the MODE_SEQ code in a
+// shared kernel cost every launch ~1.7 us of instruction fetch, scripts/update_tp_sweep.py).
+template <int mode>
 __global__ void __launch_bounds__(UPD_THREADS)
 k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__ idx,
-              const float* __restrict__ td, const int64_t* __restrict__ qin, int mode, int64_t n,
+              const float* __restrict__ td, const int64_t* __restrict__ qin, int64_t n,
               double alpha, double eps_p, int32_t* err, int force_slow, int64_t T_p, double eta, int live_only) {
   __shared__ UpdSmem S;
   if (RPL_PDL_EARLY & 1) pdl_trigger();  // A/B knob (common.cuh)
   pdl_wait();
-  tree_update_block<UPD_THREADS>(S, L, tree, idx, td, qin, mode, n, alpha, eps_p, err, force_slow, T_p, eta,
+  UPD_TRACE(0);
+  tree_update_block<UPD_THREADS, mode>(S, L, tree, idx, td, qin, n, alpha, eps_p, err, force_slow, T_p, eta,
                                  live_only);
 }
 
@@ -686,7 +708,8 @@ k_tree_update_sample(TreeDev L, int64_t* __restrict__ tree, const int64_t* __res
   if (threadIdx.x == 0)
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(spos) : "l"(hdr + 2) : "memory");
   if (blockIdx.x == 0 && n_upd > 0)
-    tree_update_block<FUSED_THREADS>(S, L, tree, idx, td, nullptr, T_p > 0 ? MODE_SEQ : MODE_TD, n_upd, alpha, eps_p,
+    (T_p > 0 ? tree_update_block<FUSED_THREADS, MODE_SEQ> : tree_update_block<FUSED_THREADS, MODE_TD>)(
+        S, L, tree, idx, td, nullptr, n_upd, alpha, eps_p,
                                      err, 0, T_p, eta, live_only);
   grid_barrier(hdr);  // orders every CTA's read of hdr[2] before CTA 0 advances it below
   __shared__ uint64_t s_spos;
@@ -945,8 +968,13 @@ int launch_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, c
   if (!layout_ok(L) || !tree || n < 0) return RPL_EINVAL;
   if (n == 0) return RPL_OK;
   if (!idx) return RPL_EINVAL;
-  return launch_pdl(k_tree_update, dim3(1), dim3(UPD_THREADS), 0, as_stream(stream), tree_dev(L), tree, idx, td, q,
-                    mode, n, alpha, eps_p, err, force_slow, T_p, eta, live_only);
+  void (*kern)(TreeDev, int64_t*, const int64_t*, const float*, const int64_t*, int64_t, double, double, int32_t*, int,
+               int64_t, double, int) = mode == MODE_SEQ  ? k_tree_update<MODE_SEQ>
+                                        : mode == MODE_Q ? k_tree_update<MODE_Q>
+                                        : mode == MODE_MAXSEEN ? k_tree_update<MODE_MAXSEEN>
+                                                               : k_tree_update<MODE_TD>;
+  return launch_pdl(kern, dim3(1), dim3(UPD_THREADS), 0, as_stream(stream), tree_dev(L), tree, idx, td, q, n, alpha,
+                    eps_p, err, force_slow, T_p, eta, live_only);
 }
 
 }  // namespace
@@ -1234,4 +1262,15 @@ extern "C" int rpl_debug_set_tree_stage(int32_t on) {
   if (on != 0 && on != 1) return RPL_EINVAL;
   g_tree_stage.store(on);
   return RPL_OK;
+}
+
+extern "C" int rpl_debug_trace(int64_t* out, int32_t n) {
+#ifdef RPL_TRACE
+  if (!out || n < 1 || n > 16) return RPL_EINVAL;
+  return cudaMemcpyFromSymbol(out, rpl::g_trace, sizeof(int64_t) * (size_t)n) == cudaSuccess ? RPL_OK : RPL_ECUDA;
+#else
+  (void)out;
+  (void)n;
+  return RPL_EUNSUPPORTED;  // measurement builds only (-DRPL_TRACE)
+#endif
 }

@@ -374,7 +374,8 @@ def test_sharded_compacted(rpl, mode):
         assert collected == ref_idx and collected_q == ref_q
 
 
-@pytest.mark.parametrize("T_p,n,eta", [(80, 64, 0.9), (1, 5, 0.9), (7, 300, 0.0), (80, 1200, 1.0), (33, 64, 0.37)])
+@pytest.mark.parametrize("T_p,n,eta", [(80, 64, 0.9), (1, 5, 0.9), (7, 300, 0.0), (80, 1200, 1.0), (33, 64, 0.37),
+                                        (90, 100, 0.9), (91, 100, 0.9), (200, 70, 0.5)])
 def test_update_seq_vs_oracle(rpl, T_p, n, eta):
     # NEXT-1: R2D2 eta-mix of per-step |delta| per sequence, then the update — tree bit-exact
     import torch
