@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CUtensorMap tm_v,
             const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ CUtensorMap tm_o0,
             const __grid_constant__ CUtensorMap tm_o1, const float* __restrict__ boot, int64_t T, int64_t B,
-            double gamma, double lam, int has_o1, const float* __restrict__ vterm) {
+            double gamma, double lam, int has_o1, const float* __restrict__ vterm, int early_trigger) {
   using SM = ScanPipeSmem<COLS, WARPS, S, STAGES, GAE, OB>;
   constexpr int SUB = SM::SUB, SEGS = SM::SEGS, CH = SM::CH;
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -501,6 +501,9 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
   pdl_wait();
   if (threadIdx.x == 0)
     for (int64_t i = 0; i < STAGES && i < items; ++i) issue();
+  // measurement knob (RPL_SCAN_TRIGGER=2): let the dependent grid launch once the first tiles
+  // are requested (it still waits for this grid's completion in its griddepcontrol.wait)
+  if (early_trigger == 2) pdl_trigger();
   const double ga = GAE ? gamma * lam : gamma;
   uint32_t phases = 0;  // bit st: parity to wait for on stage st
   int64_t g = blockIdx.x, c = nchunks - 1;
@@ -980,10 +983,10 @@ int scan_variant() {
 // at exit (PPO [128,4096], graph of back-to-back calls: GAE 4.90 -> 4.80 us, discounted
 // 3.71 -> 3.66 us; profiles/r1/ppo_floor.json).  RPL_SCAN_TRIGGER=0 restores the exit
 // trigger (A/B measurement).
-int scan_trigger() {
+int scan_trigger() {  // 0: exit trigger, 1: default, 2: the pipelined scan triggers after its first loads
   static const int t = [] {
     const char* e = getenv("RPL_SCAN_TRIGGER");
-    return (e && e[0] == '0') ? 0 : 1;
+    return (e && e[0] == '0') ? 0 : (e && e[0] == '2') ? 2 : 1;
   }();
   return t;
 }
@@ -1070,7 +1073,7 @@ int launch_scan_pipe(const float* r, const float* v, const uint8_t* d, const flo
   int64_t grid = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
   if (grid > groups) grid = groups;
   return launch_pdl(kern, dim3((unsigned)grid), dim3(WARPS * 32), dyn, st, mr, mv, md, mo0, mo1, boot, T, B, gamma,
-                    lam, (GAE && o1) ? 1 : 0, vterm);
+                    lam, (GAE && o1) ? 1 : 0, vterm, scan_trigger());
 }
 
 template <bool GAE>
@@ -1094,10 +1097,13 @@ int launch_scan(const float* r, const float* v, const uint8_t* d, const float* b
     // load stages, one CTA per SM (scan size sweep, profiles/r2/scan_ab_*.json: GAE 0.75-0.76
     // and discounted 0.58-0.74 of measured HBM on 34-285 MB calls, PPO GAE 4.49 us); variant 9
     // keeps the 16-column / 2-CTAs-per-SM shape measured first.
+    // One chunk per group (T <= 128, e.g. PPO): the 16-column shape, twice the CTAs (PPO GAE
+    // 4.40 vs 4.56 us); longer horizons: the 32-column shape (wider TMA rows win there).
     bool used = false;
-    const int rc = var == 0
-                       ? launch_scan_pipe<32, 8, 16, 3, GAE, 1>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used)
-                       : launch_scan_pipe<16, 8, 8, 3, GAE, 2>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used);
+    const bool narrow = var == 9 || T <= 128;
+    const int rc = narrow
+                       ? launch_scan_pipe<16, 8, 8, 3, GAE, 2>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used)
+                       : launch_scan_pipe<32, 8, 16, 3, GAE, 1>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used);
     if (used) return rc;
   }
   if (var >= 10 && var <= 17 && T < (1ll << 31) && B < (1ll << 31)) {  // pipeline shapes (A/B)
