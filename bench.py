@@ -604,12 +604,12 @@ def run_rpl(args):
                                     "us_per_step_floor": ingress / 900e9 * 1e6,
                                     "sequences_per_s_ceiling": n_glob / (ingress / 900e9) if ingress else None,
                                     "note": "the learner then re-stacks the k-frame stacks locally (rpl_stack_frames)"}
-        result["e2e"] = e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K_eff, world)
-        # a1-a4 at every N: each rank scans its own [128, 4096] columns, no collective
-        try:
-            result["returns"] = returns_line(dev, rpl, world, dist if world > 1 else None)
-        except Exception as e:  # pragma: no cover
-            result["returns"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    result["e2e"] = e2e_rpl(args, dev, step, idx_buf, y, w, td_pool, q_pool, n, P, K_eff, world)
+    # a1-a4 at every N: each rank scans its own [128, 4096] columns, no collective
+    try:
+        result["returns"] = returns_line(dev, rpl, world, dist if world > 1 else None)
+    except Exception as e:  # pragma: no cover
+        result["returns"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     if world == 1 and not args.no_secondary and not args.profile:
         # each secondary is isolated: a failure is reported in its slot, never loses the line
         jobs = [("r2d2_seeds", lambda: seed_sweep(dev, rpl, c, ms / K_eff * 1e3)),
