@@ -82,4 +82,6 @@ def sweep(shapes):
 if __name__ == "__main__":
     shapes = [(128, 4096), (256, 4096), (512, 4096), (1024, 4096), (2048, 4096), (128, 16384), (128, 65536),
               (1024, 16384)]
+    if os.environ.get("SHAPES"):  # e.g. SHAPES="2048x4736,1024x18944"
+        shapes = [tuple(int(x) for x in sh.split("x")) for sh in os.environ["SHAPES"].split(",")]
     print(json.dumps({"peak_gbs": PEAK, "sweep": sweep(shapes)}))
