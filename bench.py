@@ -74,10 +74,11 @@ def parse():
                     help="1 GPU: priority update + sampling as one launch (rpl_sumtree_update_sample; "
                          "measured 1.7 us/step slower than the PDL-chained pair)")
     ap.add_argument("--seq-variant", type=int, default=None, help="diagnostics: sequence-gather kernel variant")
-    ap.add_argument("--fused-sample", type=int, default=0, choices=[0, 1],
+    ap.add_argument("--fused-sample", type=int, default=1, choices=[0, 1],
                     help="1 GPU: stratified sampling inside the sequence gather (rpl_gather_sample), so the step "
-                         "is update_seq -> gather; 0 (default): a separate rpl_sumtree_sample_stream launch "
-                         "(same-box A/B: 66.57 vs 67.05 us per step, profiles/r2/ab_fused_sample.txt)")
+                         "is update_seq -> gather (default: same-box A/B 68.1 vs 69.45 us per step with the "
+                         "top levels staged in shared memory, profiles/r2/ab_fused_sample_staged.txt); 0: a "
+                         "separate rpl_sumtree_sample_stream launch")
     ap.add_argument("--mode", default="L", choices=["L", "C"],
                     help="N > 1 replay mode (SURVEY §8e): L = owner computes, each rank feeds its own learner; "
                          "C = every owner's gather writes into the rank-0 learner's batch over NVLink (CUDA IPC)")

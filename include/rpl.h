@@ -65,7 +65,7 @@ int64_t rpl_launch_count(void);
 /* The library's effective configuration as a one-line JSON object written into buf (host,
  * len bytes incl. the terminating NUL): every build-flag knob (launch shapes, RPL_PDL_EARLY,
  * whether the -DRPL_DIAG diagnostics are compiled in) and every runtime knob (RPL_PDL,
- * RPL_TREE_STAGE, RPL_SCAN_VARIANT, RPL_SCAN_TRIGGER, the debug gather variant / diag mask).
+ * RPL_TREE_STAGE, RPL_SCAN_VARIANT, RPL_SCAN_TRIGGER, RPL_CARVEOUT, the debug gather variant / diag mask).
  * bench.py records it in its JSON line so that no knob can change the timed path unseen.
  * RPL_EINVAL for a NULL / empty buffer, RPL_ERANGE if it is too short (buf then holds a
  * truncated string). */
@@ -656,6 +656,14 @@ int rpl_debug_set_gather_diag(int32_t mask);
  * timeline (n <= 16 int64 ns stamps, host out) — kernel start, staged / mixed sequence
  * priorities, hash reset, dedupe, leaf writes, end.  RPL_EUNSUPPORTED in the default build. */
 int rpl_debug_trace(int64_t* out, int32_t n);
+/* Measurement builds only (-DRPL_TRACE): the R2D2 step timeline.  rpl_debug_trace slots 7
+ * (update kernel entry), 8 (sampler past its dependency wait), 9 (last sampler CTA end);
+ * rpl_debug_gather_trace (n <= 8): 0 sequence-gather CTA 0 entry, 1 CTA 0 past its
+ * dependency wait, 2 CTA 0's first frames landed, 3 last CTA end.  The _reset calls clear
+ * both (rpl_debug_trace_reset) or the gather's only.  RPL_EUNSUPPORTED in the default build. */
+int rpl_debug_trace_reset(void);
+int rpl_debug_gather_trace(int64_t* out, int32_t n);
+int rpl_debug_gather_trace_reset(void);
 
 #ifdef __cplusplus
 }

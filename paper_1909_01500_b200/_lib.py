@@ -126,6 +126,9 @@ _SIGS = {
     "rpl_debug_set_tree_stage": ([I32], C.c_int),
     "rpl_debug_set_gather_diag": ([I32], C.c_int),
     "rpl_debug_trace": ([P, I32], C.c_int),
+    "rpl_debug_trace_reset": ([], C.c_int),
+    "rpl_debug_gather_trace": ([P, I32], C.c_int),
+    "rpl_debug_gather_trace_reset": ([], C.c_int),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -15,6 +15,15 @@ bool pdl_enabled() {
   }();
   return on;
 }
+int carveout_knob() {
+  static const int c = [] {
+    const char* v = getenv("RPL_CARVEOUT");
+    if (!v) return -1;
+    const int x = atoi(v);
+    return (x < 0 || x > 100) ? -1 : x;
+  }();
+  return c;
+}
 void cfg_tree(int* stage_on, int* upd_threads, int* sample_warps, int* stage_words, int* hash_slots);
 void cfg_scan(int* variant, int* trigger);
 void cfg_gather(int* variant, int* diag, int* diag_build, int* seq_consumers, int* trans_consumers, int* slot_kb,
@@ -63,8 +72,9 @@ extern "C" int rpl_config(char* buf, int64_t len) {
                          "{\"abi\": %d, \"pdl\": %d, \"pdl_early\": %d, \"tree_stage\": %d, \"upd_threads\": %d, "
                          "\"sample_warps\": %d, \"stage_words\": %d, \"hash_slots\": %d, \"scan_variant\": %d, "
                          "\"scan_trigger\": %d, \"gather_variant\": %d, \"gather_diag\": %d, \"diag_build\": %d, "
-                         "\"seq_consumers\": %d, \"trans_consumers\": %d, \"seq_slot_kb\": %d, \"g_threads\": %d}",
+                         "\"seq_consumers\": %d, \"trans_consumers\": %d, \"seq_slot_kb\": %d, \"g_threads\": %d, "
+                         "\"carveout\": %d}",
                          RPL_ABI_VERSION, rpl::pdl_enabled() ? 1 : 0, (int)RPL_PDL_EARLY, st, ut, sw, sword, hs, sv,
-                         strig, gv, gd, gdb, sc, tc, skb, gt);
+                         strig, gv, gd, gdb, sc, tc, skb, gt, rpl::carveout_knob());
   return (w < 0 || w >= len) ? RPL_ERANGE : RPL_OK;
 }

@@ -73,9 +73,29 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 bool pdl_enabled();
 
+// Shared-memory carveout of every hot-path kernel (RPL_CARVEOUT: -1 = leave the driver's
+// choice, else the percentage passed as cudaFuncAttributePreferredSharedMemoryCarveout): an
+// SM whose carveout differs between consecutive kernels must be reconfigured between them.
+int carveout_knob();
+inline void set_carveout(const void* kernel) {
+  const int c = carveout_knob();
+  if (c < 0) return;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(cache_mutex());
+  int& cur = done[std::make_pair(dev, kernel)];
+  if (cur != c + 1) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, c);
+    cudaGetLastError();
+    cur = c + 1;
+  }
+}
+
 template <typename... KArgs, typename... Args>
 int launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        unsigned cluster_x, Args... args) {
+  set_carveout(reinterpret_cast<const void*>(kernel));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -118,6 +138,7 @@ int launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cud
 // combination the launch is retried cooperative-only.
 template <typename... KArgs, typename... Args>
 int launch_coop(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  set_carveout(reinterpret_cast<const void*>(kernel));
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, (int)(block.x * block.y * block.z), smem) !=
           cudaSuccess ||
@@ -321,6 +342,47 @@ __device__ __forceinline__ uint64_t philox_u64(uint64_t seed, uint64_t c) {
 __device__ __forceinline__ uint64_t stratum_lo(uint64_t k, uint64_t Q, uint64_t n) {
   // floor(k Q / n) without 128-bit products: k*(Q/n) + floor(k*(Q%n)/n); k <= n < 2^31
   return k * (Q / n) + (k * (Q % n)) / n;
+}
+
+// Exact division by a fixed n (1 <= n < 2^31) without a 64-bit divide on the critical path:
+// m = floor((2^64 - 1) / n) is computed once (it depends on n alone, so before any dependency
+// wait); q = mulhi(x, m) undershoots floor(x / n) by at most 2, fixed by the remainder test.
+struct DivN {
+  uint64_t n, m;
+};
+__device__ __forceinline__ DivN divn_make(uint64_t n) { return DivN{n, ~0ull / n}; }
+__device__ __forceinline__ uint64_t divn(uint64_t x, const DivN& d, uint64_t* rem) {
+  uint64_t q = __umul64hi(x, d.m);
+  uint64_t r = x - q * d.n;
+  while (r >= d.n) {
+    ++q;
+    r -= d.n;
+  }
+  *rem = r;
+  return q;
+}
+// Stratum bounds for a fixed Q (Qn = Q / n, Qr = Q % n): the same integers as stratum_lo.
+struct Strata {
+  uint64_t Q, Qn, Qr;
+  DivN dn;
+};
+__device__ __forceinline__ Strata strata_make(uint64_t Q, const DivN& dn) {
+  Strata s;
+  s.Q = Q;
+  s.dn = dn;
+  s.Qn = divn(Q, dn, &s.Qr);
+  return s;
+}
+__device__ __forceinline__ uint64_t strata_lo(uint64_t k, const Strata& s) {
+  uint64_t r;
+  return k * s.Qn + divn(k * s.Qr, s.dn, &r);  // k * Qr < n^2 <= 2^62
+}
+__device__ __forceinline__ uint64_t strata_prefix(int64_t k, const Strata& s, const uint64_t* draws, uint64_t seed,
+                                                  uint64_t ctr0) {
+  const uint64_t lo = strata_lo((uint64_t)k, s);
+  const uint64_t hi = strata_lo((uint64_t)k + 1, s);
+  const uint64_t u = draws ? draws[k] : philox_u64(seed, ctr0 + (uint64_t)k);
+  return lo + __umul64hi(u, hi - lo);
 }
 
 // Global prefix of stratum k (a8, §8c #8): lo_k + floor(u_k (hi_k - lo_k) / 2^64).

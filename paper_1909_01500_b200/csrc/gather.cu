@@ -913,6 +913,48 @@ __global__ void k_gather_seq_fields(GDesc D, const int64_t* __restrict__ idx, in
 // ---------------------------------------------------------------------------
 constexpr int PL_MAX_ROWS = 256;  // output rows per CTA (host caps rows_per_cta)
 
+// Measurement-only step timeline of the sequence gather (-DRPL_TRACE builds; rpl_debug_gather_trace):
+// 0 CTA 0 entry, 1 CTA 0 past its dependency wait, 2 CTA 0's first frame landed
+// (its first consumer row's mbarrier), 3 last CTA end (max).
+#ifdef RPL_TRACE
+__device__ unsigned long long g_gtrace[8];
+#endif
+
+// Fused sampling's batch reduction (one warp of the CTA that took the last ticket): the batch
+// min q over the n samples (every CTA's index / q writes were released with its ticket and
+// acquired by this CTA's), the IS weights (a9, R10) and the stream-position advance.
+__device__ __noinline__ void smp_finish(const GDesc& D, const int64_t* idx, const int64_t* q, int64_t n, double beta,
+                                        uint64_t smp_pos) {
+  const int lane = threadIdx.x & 31;
+  int64_t m = INT64_MAX;
+  for (int64_t j = lane; j < n; j += 32) {
+    const int64_t ij = __ldcg(idx + j), qj = __ldcg(q + j);
+    if (ij >= 0 && qj < m) m = qj;
+  }
+  m = warp_min64(m);
+  if (D.o_w)
+    for (int64_t j = lane; j < n; j += 32) {
+      const int64_t qj = __ldcg(q + j);
+      D.o_w[j] = qj > 0 ? (float)pow((double)m / (double)qj, beta) : 0.0f;
+    }
+  if (lane == 0) {
+    D.smp_tree[D.smp_L.hdr_off + 1] = 0;
+    D.smp_tree[D.smp_L.hdr_off + 2] = (int64_t)(smp_pos + (uint64_t)n);
+  }
+}
+// One warp per CTA, after a barrier that follows the CTA's index / q writes: take the ticket
+// (acq_rel releases them, and the last taker acquires everyone's); the last one finishes.
+// Taken by the meta warp (or warp 0 of a CTA without rows), so no copy warp waits on it.
+__device__ __forceinline__ void smp_ticket_finish(const GDesc& D, const int64_t* idx, const int64_t* q, int64_t n,
+                                                  double beta, uint64_t smp_pos) {
+  unsigned long long t = 0;
+  if ((threadIdx.x & 31) == 0)
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;"
+                 : "=l"(t) : "l"(D.smp_tree + D.smp_L.hdr_off + 1) : "memory");
+  t = __shfl_sync(0xffffffffu, t, 0);
+  if (t == (unsigned long long)gridDim.x - 1) smp_finish(D, idx, q, n, beta, smp_pos);
+}
+
 template <int NC>
 __global__ void __launch_bounds__((NC + 2) * 32, 1)
 k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, int64_t rows_per_cta,
@@ -954,15 +996,13 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   for (int c = tid; c < PL_MAX_ROWS; c += NT) row_done[c] = 0;
   if (tid == 0) s_issued = 0;
   if (RPL_PDL_EARLY & 4) pdl_trigger();  // A/B knob (common.cuh)
+#ifdef RPL_TRACE
+  if (tid == 0 && blockIdx.x == 0) g_gtrace[0] = global_ns();
+#endif
   pdl_wait();  // idx (and n_active) come from the sampler launched just before
-  // Fused sampling (rpl_gather_sample): the tree was updated by the kernel before; every
-  // thread reads the root and the stream position (the last CTA advances it at the end)
-  const bool smp = D.smp_tree != nullptr;
-  uint64_t smp_Q = 0, smp_pos = 0;
-  if (smp) {
-    smp_Q = (uint64_t)__ldcg(D.smp_tree + D.smp_L.level_off[0]);
-    smp_pos = (uint64_t)__ldcg(D.smp_tree + D.smp_L.hdr_off + 2);
-  }
+#ifdef RPL_TRACE
+  if (tid == 0 && blockIdx.x == 0) g_gtrace[1] = global_ns();
+#endif
   // rows g = s*L + tau of the active samples, split evenly over the grid
   const int total = (int)(active_n(D, n) * L);
   const int64_t coff = col_off(D);  // output column of entry 0 (Mode C)
@@ -970,6 +1010,70 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   const int rpc = D.n_active ? (total + (int)gridDim.x - 1) / (int)gridDim.x : (int)rows_per_cta;
   const int g0 = (int)blockIdx.x * rpc;
   const int g1 = min(total, g0 + rpc);
+  // (S) Fused sampling (rpl_gather_sample; the tree was updated by the kernel before).  The
+  //     tree's top levels (root .. the deepest level that fits the frame-slot area, which no
+  //     TMA load has touched yet) are staged in shared memory with one round of 16-B cp.async,
+  //     in flight with the stream-position read, so the root and the upper levels of every
+  //     descent cost one L2 round trip.  One warp per piece then descends for the piece's
+  //     stratum (a8; the same strata and Philox stream as rpl_sumtree_sample_stream); the CTA
+  //     owning a sample's first row writes its index and q.  Every CTA then takes a ticket
+  //     (acq_rel: its index / q writes are released with it); the LAST one computes the
+  //     batch-min IS weights (a9) and advances the stream position — in its meta warp, while
+  //     its consumer warps stream frames, so no CTA's copy waits for the batch reduction.
+  const bool smp = D.smp_tree != nullptr;
+  uint64_t smp_pos = 0;
+  const DivN smp_dn = divn_make(smp ? (uint64_t)n : 1ull);  // before any global read: n alone
+  if (smp) {
+    const int64_t* top = reinterpret_cast<const int64_t*>(smem);
+    int64_t ntop = 0;
+    const int64_t cap_words = (int64_t)NS * ob / 8;
+    for (int l = 0; l <= D.smp_L.depth; ++l) {
+      const int64_t end = l < D.smp_L.depth ? D.smp_L.level_off[l + 1] : D.smp_L.hdr_off;
+      if (end > cap_words) break;
+      ntop = end;
+    }
+    for (int64_t j = 2 * (int64_t)tid; j < ntop; j += 2 * NT)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem + j * 8)), "l"(D.smp_tree + j)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    smp_pos = (uint64_t)__ldcg(D.smp_tree + D.smp_L.hdr_off + 2);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+#ifdef RPL_TRACE
+    if (tid == 0 && blockIdx.x == 0) g_gtrace[4] = global_ns();
+#endif
+    const uint64_t smp_Q = (uint64_t)(ntop > 0 ? top[0] : __ldcg(D.smp_tree + D.smp_L.level_off[0]));
+    const Strata smp_st = strata_make(smp_Q, smp_dn);
+    if (g0 < g1) {
+      const int s_first = g0 / L;
+      const int npieces = (g1 - 1) / L - s_first + 1;
+      int32_t eb = 0;
+      for (int pc = warp; pc < npieces; pc += NT / 32) {
+        const int sm = s_first + pc;
+        int64_t leaf = -1, qv = 0;
+        if (smp_Q == 0) {
+          eb |= RPL_DERR_EMPTY;
+        } else {
+          const uint64_t prefix = strata_prefix(sm, smp_st, nullptr, D.smp_seed, smp_pos);
+          leaf = descend(D.smp_L, D.smp_tree, (int64_t)prefix, &qv, &eb, top, ntop);
+        }
+        if (lane == 0) {
+          p_leaf[pc] = leaf;
+          if (sm * L >= g0) {
+            const_cast<int64_t*>(idx)[sm] = leaf;
+            const_cast<int64_t*>(q)[sm] = qv;
+          }
+        }
+      }
+      if (lane == 0 && eb) set_err(err, eb);
+    }
+    fence_proxy_async();  // the staged words were read through the generic proxy; TMA refills them
+    __syncthreads();
+#ifdef RPL_TRACE
+    if (tid == 0 && blockIdx.x == 0) g_gtrace[5] = global_ns();
+#endif
+    if (g0 >= g1 && warp == 0) smp_ticket_finish(D, idx, q, n, beta, smp_pos);  // no rows: take the ticket now
+  }
   // K7 fused (peer boards): the step's tag comes from this rank's own board (its sampler's
   // K5 slot); CTA 0 publishes this rank's batch-min q over its owned entries to every rank
   // — before any early exit, so a rank that owns nothing still publishes (INT64_MAX)
@@ -991,31 +1095,6 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   const int npieces = (g1 - 1) / L - s_first + 1;
 
   if (tid == 0) s_npieces = npieces;
-  if (smp) {
-    // (S) one warp per piece descends the tree for the piece's stratum (a8; the same strata
-    //     and Philox stream as rpl_sumtree_sample_stream); the CTA owning a sample's first
-    //     row writes its index and q
-    int32_t eb = 0;
-    for (int pc = warp; pc < npieces; pc += NT / 32) {
-      const int sm = s_first + pc;
-      int64_t leaf = -1, qv = 0;
-      if (smp_Q == 0) {
-        eb |= RPL_DERR_EMPTY;
-      } else {
-        const uint64_t prefix = stratum_prefix(sm, smp_Q, n, nullptr, D.smp_seed, smp_pos);
-        leaf = descend(D.smp_L, D.smp_tree, (int64_t)prefix, &qv, &eb);
-      }
-      if (lane == 0) {
-        p_leaf[pc] = leaf;
-        if (sm * L >= g0) {
-          const_cast<int64_t*>(idx)[sm] = leaf;
-          const_cast<int64_t*>(q)[sm] = qv;
-        }
-      }
-    }
-    if (lane == 0 && eb) set_err(err, eb);
-    __syncthreads();
-  }
   // (A) pieces, in parallel: one sampled leaf each
   for (int pc = tid; pc < npieces; pc += NT) {
     const int sm = s_first + pc;
@@ -1023,9 +1102,15 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
     const int64_t leaf = smp ? p_leaf[pc] : idx[sm];
     int bcol = -1, row0 = 0, blk = 0;
     if (leaf >= 0 && leaf < nleaves) {
-      blk = (int)(leaf / Bc);
-      bcol = (int)(leaf - (int64_t)blk * Bc);
-      row0 = (int)(((int64_t)blk * period + tau0) % cap);
+      if (nleaves < (1ll << 31)) {  // 32-bit division (every value below fits)
+        blk = (int)((uint32_t)leaf / (uint32_t)Bc);
+        bcol = (int)leaf - blk * Bc;
+        row0 = (int)((uint32_t)(blk * period + tau0) % (uint32_t)cap);
+      } else {
+        blk = (int)(leaf / Bc);
+        bcol = (int)(leaf - (int64_t)blk * Bc);
+        row0 = (int)(((int64_t)blk * period + tau0) % cap);
+      }
       if (tau0 == 0) {
         const int64_t age = wrap(D.cursor - 1 - (int64_t)blk * period, D.cap_T);
         const int hist = k - 1 > 1 ? k - 1 : 1;
@@ -1089,6 +1174,9 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
             if (!(GDIAG(D) & 2)) mbar_wait(&full[slot], (uint32_t)(((i / NS) - 1) & 1));
           }
           if (!(GDIAG(D) & 2)) {
+#ifdef RPL_TRACE
+            if (i == 0 && blockIdx.x == 0) g_gtrace[6] = global_ns();
+#endif
             mbar_expect_tx(&full[slot], (uint32_t)ob);
             const uint8_t* src = col + (int64_t)row * rstride;
             // frames are streamed once: evict-first keeps the L2 for the sum tree and the
@@ -1152,6 +1240,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
 
     if (warp == 1) {
       // ---------------- meta warp: per-row fields, IS weights ----------------
+      if (smp) smp_ticket_finish(D, idx, q, n, beta, smp_pos);  // fused sampling's ticket / batch reduction
       const int64_t qm = (D.o_w && q && !peer && !smp) ? warp_batch_qmin(qmin, idx, q, n) : 0;
       const int64_t ab = D.act_bytes;
       const bool a8 = ab == 8 && ((reinterpret_cast<uintptr_t>(D.act) | reinterpret_cast<uintptr_t>(D.o_act) |
@@ -1286,6 +1375,9 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
               const int sl = slot_of(j, &par);
               mbar_wait(&full[sl], par);
             }
+#ifdef RPL_TRACE
+          if (c == 0 && lane == 0 && blockIdx.x == 0) g_gtrace[2] = global_ns();
+#endif
           int4* dst = reinterpret_cast<int4*>(D.o_obs + ((int64_t)tau * n + coff + sm) * k * ob);
           if (!(GDIAG(D) & 1))
             for (int j = 0; j < k; ++j) {
@@ -1315,42 +1407,6 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
     }
   }
   } while (0);
-  // Fused sampling epilogue: the last CTA (ticket = the tree's sampler-ticket header word)
-  // reduces the batch-min q over every CTA's written samples (acquired through the acq_rel
-  // ticket), writes the IS weights (a9) and advances the tree's stream position.
-  if (smp) {
-    __shared__ int s_last;
-    __shared__ int64_t s_qm[NC + 2];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long t;
-      asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;"
-                   : "=l"(t) : "l"(D.smp_tree + D.smp_L.hdr_off + 1) : "memory");
-      s_last = t == (unsigned long long)gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-      int64_t m = INT64_MAX;
-      for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-        const int64_t ij = __ldcg(idx + j), qj = __ldcg(q + j);
-        if (ij >= 0 && qj < m) m = qj;
-      }
-      m = warp_min64(m);
-      if ((threadIdx.x & 31) == 0) s_qm[threadIdx.x >> 5] = m;
-      __syncthreads();
-      m = INT64_MAX;
-      for (int k2 = 0; k2 < NC + 2; ++k2) m = s_qm[k2] < m ? s_qm[k2] : m;
-      if (D.o_w)
-        for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-          const int64_t qj = __ldcg(q + j);
-          D.o_w[j] = qj > 0 ? (float)pow((double)m / (double)qj, beta) : 0.0f;
-        }
-      if (threadIdx.x == 0) {
-        D.smp_tree[D.smp_L.hdr_off + 1] = 0;
-        D.smp_tree[D.smp_L.hdr_off + 2] = (int64_t)(smp_pos + (uint64_t)n);
-      }
-    }
-  }
   // Completion signal (rpl_gather_desc.done_flag, Mode C): every CTA publishes its stores at
   // system scope and takes a ticket; the last CTA bumps the call counter done_seq[0] and
   // writes it to done_flag with st.release.sys (peer memory over NVLink), so the learner's
@@ -1369,6 +1425,10 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       }
     }
   }
+#ifdef RPL_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&g_gtrace[3], (unsigned long long)global_ns());
+#endif
   pdl_trigger();
 }
 template <int NC>
@@ -1925,6 +1985,26 @@ int g_seq_variant = 0;
 }  // namespace rpl
 
 using namespace rpl;
+
+extern "C" int rpl_debug_gather_trace_reset(void) {
+#ifdef RPL_TRACE
+  unsigned long long z[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+  return cudaMemcpyToSymbol(rpl::g_gtrace, z, sizeof(z)) == cudaSuccess ? RPL_OK : RPL_ECUDA;
+#else
+  return RPL_EUNSUPPORTED;
+#endif
+}
+
+extern "C" int rpl_debug_gather_trace(int64_t* out, int32_t n) {
+#ifdef RPL_TRACE
+  if (!out || n < 1 || n > 8) return RPL_EINVAL;
+  return cudaMemcpyFromSymbol(out, rpl::g_gtrace, sizeof(int64_t) * (size_t)n) == cudaSuccess ? RPL_OK : RPL_ECUDA;
+#else
+  (void)out;
+  (void)n;
+  return RPL_EUNSUPPORTED;
+#endif
+}
 
 extern "C" int rpl_debug_set_gather_variant(int32_t variant) {
   if (variant < 0 || variant > 6) return RPL_EINVAL;

@@ -34,6 +34,12 @@ namespace {
 #define RPL_SAMPLE_WARPS 4  // same-box A/B: R2D2 step 69.06 vs 69.20 us at 8; DQN bs32 / 512 step 15.67 / 22.00 vs 15.83 / 22.14
 #endif
 constexpr int UPD_THREADS = RPL_UPD_THREADS;
+#ifndef RPL_UPD_TRIGGER_AT  // with RPL_PDL_EARLY & 1: where the single-chunk update triggers (0 entry, 3/2/4 stages)
+#define RPL_UPD_TRIGGER_AT 0
+#endif
+#ifndef RPL_UPD_SINGLE  // build-flag A/B knob: 0 = every batch through the chunked update
+#define RPL_UPD_SINGLE 1
+#endif
 #ifndef RPL_HASH_SLOTS  // build-flag A/B knob (>= 2 x the update chunk, a power of two)
 #define RPL_HASH_SLOTS 2048
 #endif
@@ -80,7 +86,15 @@ __device__ unsigned long long g_trace[16];
   do {                                                        \
     if (threadIdx.x == 0 && blockIdx.x == 0) g_trace[k] = global_ns(); \
   } while (0)
+// step timeline slots: 7 update entry, 8 sampler after its dependency wait, 9 sampler end (max)
+#define SMP_TRACE_END()                                                   \
+  do {                                                                    \
+    if (threadIdx.x == 0) atomicMax(&g_trace[9], (unsigned long long)global_ns()); \
+  } while (0)
 #else
+#define SMP_TRACE_END() \
+  do {                  \
+  } while (0)
 #define UPD_TRACE(k) \
   do {               \
   } while (0)
@@ -169,8 +183,21 @@ __device__ __noinline__ double seq_exact_sum(const float* __restrict__ steps, in
   return sa_round(bins);
 }
 
-__device__ __forceinline__ float sequence_td8(const float* __restrict__ steps, int64_t T_p, int64_t n, int64_t i,
-                                              bool active, double eta) {
+constexpr int TD8_BATCH = 16;
+// The first 8 * TD8_BATCH rows of a sequence's column: every load issued before the first is
+// consumed (one L2 round trip, not one per unrolled group)
+__device__ __forceinline__ void sequence_td8_load(float (&vals)[TD8_BATCH], const float* __restrict__ steps,
+                                                  int64_t T_p, int64_t n, int64_t i, bool active) {
+  const int j = threadIdx.x & 7;
+#pragma unroll
+  for (int u = 0; u < TD8_BATCH; ++u) {
+    const int64_t t = j + 8 * (int64_t)u;
+    vals[u] = (active && t < T_p) ? __ldg(steps + t * n + i) : 0.0f;
+  }
+}
+
+__device__ __forceinline__ float sequence_td8_finish(const float (&vals)[TD8_BATCH], const float* __restrict__ steps,
+                                                     int64_t T_p, int64_t n, int64_t i, bool active, double eta) {
   const int j = threadIdx.x & 7;
   double mx = 0.0, sm = 0.0;
   int emin = 255, emax = 0, nonfin = 0;  // exponents of the non-zero finite entries; 1 inf, 2 NaN
@@ -188,16 +215,7 @@ __device__ __forceinline__ float sequence_td8(const float* __restrict__ steps, i
     if (v > mx) mx = v;  // NaN never wins
     sm = __dadd_rn(sm, v);
   };
-  constexpr int TD8_BATCH = 16;
   if (active) {
-    // the first 8 * TD8_BATCH rows: every load issued before the first is consumed (one L2
-    // round trip, not one per unrolled group)
-    float vals[TD8_BATCH];
-#pragma unroll
-    for (int u = 0; u < TD8_BATCH; ++u) {
-      const int64_t t = j + 8 * (int64_t)u;
-      vals[u] = t < T_p ? __ldg(steps + t * n + i) : 0.0f;
-    }
 #pragma unroll
     for (int u = 0; u < TD8_BATCH; ++u)
       if (j + 8 * (int64_t)u < T_p) take(vals[u]);
@@ -228,6 +246,13 @@ __device__ __forceinline__ float sequence_td8(const float* __restrict__ steps, i
   return __double2float_rn(mix);
 }
 
+__device__ __forceinline__ float sequence_td8(const float* __restrict__ steps, int64_t T_p, int64_t n, int64_t i,
+                                              bool active, double eta) {
+  float vals[TD8_BATCH];
+  sequence_td8_load(vals, steps, T_p, n, i, active);
+  return sequence_td8_finish(vals, steps, T_p, n, i, active, eta);
+}
+
 __device__ __forceinline__ uint32_t hash_slot(int64_t leaf) {
   return (uint32_t)(((unsigned long long)leaf * 0x9E3779B97F4A7C15ull) >> 53) & (HASH_SLOTS - 1);
 }
@@ -239,6 +264,65 @@ struct UpdSmem {
   int64_t sred[UPD_THREADS / 32];
   float s_td[UPD_THREADS];  // MODE_SEQ: this chunk's sequence priorities
 };
+
+// Min-tree maintenance (buffer-wide IS normaliser, R29): every internal min node on a
+// written leaf's path is recomputed from its W children, level by level from the leaves'
+// parents up (a barrier between levels), each distinct node by one thread (hash dedupe per
+// chunk of NT entries).  A leaf's min contribution is its q when q > 0; an internal node
+// holds the min of its children (INT64_MAX: no positive leaf below).  No-op without one.
+template <int NT>
+__device__ __forceinline__ void mintree_update(UpdSmem& S, const TreeDev& L, int64_t* __restrict__ tree,
+                                               const int64_t* __restrict__ idx, int64_t n, int64_t* mins) {
+  unsigned long long* hkey = S.hkey;
+  const int tid = threadIdx.x;
+  const int64_t* leaves = tree + L.level_off[L.depth];
+  if (mins) {
+    __syncthreads();
+    for (int l = L.depth - 1; l >= 0; --l) {
+      const int sh = L.log2w * (L.depth - l);
+      for (int64_t base = 0; base < n; base += NT) {
+        for (int s2 = tid; s2 < HASH_SLOTS; s2 += NT) hkey[s2] = HASH_EMPTY;
+        __syncthreads();
+        int64_t p = -1;
+        if (base + tid < n) {
+          const int64_t leaf = idx[base + tid];
+          if (leaf >= 0 && leaf < L.n_leaves) p = leaf >> sh;
+        }
+        bool own = false;
+        if (p >= 0) {
+          uint32_t slot = hash_slot(p);
+          while (true) {
+            const unsigned long long prev = atomicCAS(&hkey[slot], HASH_EMPTY, (unsigned long long)p);
+            if (prev == HASH_EMPTY) {
+              own = true;
+              break;
+            }
+            if (prev == (unsigned long long)p) break;
+            slot = (slot + 1) & (HASH_SLOTS - 1);
+          }
+        }
+        if (own) {
+          const int64_t c0 = p << L.log2w;
+          int64_t m2 = INT64_MAX;
+          if (l == L.depth - 1) {
+            for (int j = 0; j < L.fanout; ++j) {
+              const int64_t v = __ldcg(leaves + c0 + j);
+              if (v > 0 && v < m2) m2 = v;
+            }
+          } else {
+            const int64_t* ch = mins + L.level_off[l + 1] + c0;
+            for (int j = 0; j < L.fanout; ++j) {
+              const int64_t v = __ldcg(ch + j);
+              if (v < m2) m2 = v;
+            }
+          }
+          mins[L.level_off[l] + p] = m2;
+        }
+        __syncthreads();
+      }
+    }
+  }
+}
 
 // The whole batch update by ONE block of NT threads (NT <= UPD_THREADS, a multiple of 32;
 // every thread must call): entries are processed in chunks of NT in batch order.
@@ -374,57 +458,140 @@ __device__ __forceinline__ void tree_update_block(UpdSmem& S, const TreeDev& L, 
   }
   if (errbits) set_err(err, errbits);
   UPD_TRACE(6);
-  // Min-tree maintenance (buffer-wide IS normaliser, R29): every internal min node on a
-  // written leaf's path is recomputed from its W children, level by level from the leaves'
-  // parents up (a barrier between levels), each distinct node by one thread (hash dedupe per
-  // chunk of NT entries).  A leaf's min contribution is its q when q > 0; an internal node
-  // holds the min of its children (INT64_MAX: no positive leaf below).
-  if (mins) {
-    __syncthreads();
-    for (int l = L.depth - 1; l >= 0; --l) {
-      const int sh = L.log2w * (L.depth - l);
-      for (int64_t base = 0; base < n; base += NT) {
-        for (int s2 = tid; s2 < HASH_SLOTS; s2 += NT) hkey[s2] = HASH_EMPTY;
-        __syncthreads();
-        int64_t p = -1;
-        if (base + tid < n) {
-          const int64_t leaf = idx[base + tid];
-          if (leaf >= 0 && leaf < L.n_leaves) p = leaf >> sh;
-        }
-        bool own = false;
-        if (p >= 0) {
-          uint32_t slot = hash_slot(p);
-          while (true) {
-            const unsigned long long prev = atomicCAS(&hkey[slot], HASH_EMPTY, (unsigned long long)p);
-            if (prev == HASH_EMPTY) {
-              own = true;
-              break;
-            }
-            if (prev == (unsigned long long)p) break;
-            slot = (slot + 1) & (HASH_SLOTS - 1);
-          }
-        }
-        if (own) {
-          const int64_t c0 = p << L.log2w;
-          int64_t m2 = INT64_MAX;
-          if (l == L.depth - 1) {
-            for (int j = 0; j < L.fanout; ++j) {
-              const int64_t v = __ldcg(leaves + c0 + j);
-              if (v > 0 && v < m2) m2 = v;
-            }
-          } else {
-            const int64_t* ch = mins + L.level_off[l + 1] + c0;
-            for (int j = 0; j < L.fanout; ++j) {
-              const int64_t v = __ldcg(ch + j);
-              if (v < m2) m2 = v;
-            }
-          }
-          mins[L.level_off[l] + p] = m2;
-        }
-        __syncthreads();
+  mintree_update<NT>(S, L, tree, idx, n, mins);
+}
+
+// The update of a batch that fits one chunk (n <= NT; MODE_SEQ: n <= NT / 8, eight lanes per
+// sequence), with the kernel's round trips overlapped: the entry indices, the |delta| (or
+// q / the per-step |delta| of every sequence) and the header are requested together; the
+// duplicate resolution (a hash of the leaf indices alone: the last batch position of every
+// distinct leaf wins, S:624 — independent of the priorities) and the leaves' current values
+// follow as soon as the indices land, in flight while the priorities are computed.  The same
+// result as tree_update_block (which the multi-chunk batches keep): an entry skipped by
+// RPL_UPD_LIVE_ONLY shares its leaf's current value with every duplicate, so skipping after
+// the hash selects the same winners.
+template <int NT, int mode>
+__device__ __forceinline__ void tree_update_single(UpdSmem& S, const TreeDev& L, int64_t* __restrict__ tree,
+                                                   const int64_t* __restrict__ idx, const float* __restrict__ td,
+                                                   const int64_t* __restrict__ qin, int64_t n, double alpha,
+                                                   double eps_p, int32_t* err, int force_slow, int64_t T_p,
+                                                   double eta, int live_only) {
+  unsigned long long* hkey = S.hkey;
+  int* hval = S.hval;
+  int64_t* sred = S.sred;
+  float* s_td = S.s_td;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  int64_t* leaves = tree + L.level_off[L.depth];
+  int64_t* hdr = tree + L.hdr_off;
+  // (1) every independent load in flight at once
+  int64_t leaf = tid < n ? idx[tid] : -1;
+  float tdi = 0.0f;
+  int64_t qi = 0;
+  if (mode == MODE_TD && tid < n) tdi = td[tid];
+  if (mode == MODE_Q && tid < n) qi = qin[tid];
+  float vals[mode == MODE_SEQ ? TD8_BATCH : 1];
+  const int64_t jj = tid >> 3;  // MODE_SEQ: this lane's sequence
+  if (mode == MODE_SEQ) sequence_td8_load(reinterpret_cast<float(&)[TD8_BATCH]>(vals), td, T_p, n, jj, jj < n);
+  const int64_t maxseen_now = __ldcg(hdr);
+  int64_t* mins = reinterpret_cast<int64_t*>(__ldcg(hdr + HDR_MINTREE));  // attached min-tree (R29) or NULL
+  for (int s2 = tid; s2 < HASH_SLOTS; s2 += NT) {
+    hkey[s2] = HASH_EMPTY;
+    hval[s2] = -1;
+  }
+  __syncthreads();
+  UPD_TRACE(3);
+  if ((RPL_PDL_EARLY & 1) && RPL_UPD_TRIGGER_AT == 3) pdl_trigger();  // A/B: the dependent launch from here
+  // (2) duplicate resolution on the indices, and the leaves' current values
+  int32_t errbits = 0;
+  if (leaf >= L.n_leaves) {
+    errbits |= RPL_DERR_IDX;
+    leaf = -1;
+  } else if (leaf < 0) {
+    leaf = -1;  // padding entry, skipped silently
+  } else if (mode == MODE_Q && qi < 0) {
+    errbits |= RPL_DERR_IDX;  // an explicit q < 0 is an invalid entry: it never takes part in the dedupe
+    leaf = -1;
+  }
+  uint32_t slot = 0;
+  int64_t old = 0;
+  if (leaf >= 0) {
+    old = __ldcg(leaves + leaf);
+    slot = hash_slot(leaf);
+    while (true) {
+      unsigned long long prev = atomicCAS(&hkey[slot], HASH_EMPTY, (unsigned long long)leaf);
+      if (prev == HASH_EMPTY || prev == (unsigned long long)leaf) break;
+      slot = (slot + 1) & (HASH_SLOTS - 1);
+    }
+    atomicMax(&hval[slot], tid);  // last position in the batch wins
+  }
+  // (3) the priorities (R26 sequence mix, R7 transform)
+  if (mode == MODE_SEQ) {
+    const float v = sequence_td8_finish(reinterpret_cast<const float(&)[TD8_BATCH]>(vals), td, T_p, n, jj, jj < n,
+                                        eta);
+    if ((tid & 7) == 0 && jj < n) s_td[jj] = v;
+  }
+  UPD_TRACE(2);
+  if ((RPL_PDL_EARLY & 1) && RPL_UPD_TRIGGER_AT == 2) pdl_trigger();
+  __syncthreads();  // s_td and the hash table complete
+  int64_t q = 0;
+  if (leaf >= 0) {
+    if (mode == MODE_TD || mode == MODE_SEQ) {
+      const float t = mode == MODE_SEQ ? s_td[tid] : tdi;
+      const double p = (double)fabsf(t) + eps_p;  // RN64(|delta| + eps_p)
+      float v;
+      if (!isfinite(p)) {
+        v = __int_as_float(0x7f800000);
+      } else {
+        bool slow = false;
+        v = cr_powf(p, alpha, force_slow != 0, &slow);
+      }
+      bool sat = false;
+      q = quantise_q(v, L.frac_bits, L.q_cap, &sat);
+      if (sat) errbits |= RPL_DERR_SATURATED;
+    } else if (mode == MODE_Q) {
+      q = qi;
+      if (q > L.q_cap) {
+        q = L.q_cap;
+        errbits |= RPL_DERR_SATURATED;
+      }
+    } else {
+      q = maxseen_now;
+    }
+  }
+  // RPL_UPD_LIVE_ONLY: a leaf that is currently 0 is left untouched (R30)
+  if (leaf >= 0 && live_only && old == 0) leaf = -1;
+  int64_t local_max = (leaf >= 0 && mode != MODE_MAXSEEN) ? q : INT64_MIN;
+  UPD_TRACE(4);
+  if ((RPL_PDL_EARLY & 1) && RPL_UPD_TRIGGER_AT == 4) pdl_trigger();
+  int64_t delta = 0;
+  if (leaf >= 0 && hval[slot] == tid) {
+    leaves[leaf] = q;
+    delta = q - old;
+    if (delta != 0) {
+      int64_t node = leaf;
+      for (int l = L.depth - 1; l >= 1; --l) {
+        node >>= L.log2w;
+        atomicAdd(reinterpret_cast<unsigned long long*>(tree + L.level_off[l] + node), (unsigned long long)delta);
       }
     }
   }
+  const int64_t rd = warp_sum64(delta);
+  if (lane == 0 && rd != 0)
+    atomicAdd(reinterpret_cast<unsigned long long*>(tree + L.level_off[0]), (unsigned long long)rd);
+  UPD_TRACE(5);
+  // max-priority-seen
+  int64_t m = warp_max64(local_max);
+  if (lane == 0) sred[tid >> 5] = m;
+  __syncthreads();
+  if (tid < 32) {
+    m = tid < NT / 32 ? sred[tid] : INT64_MIN;
+    m = warp_max64(m);
+    if (tid == 0 && m > maxseen_now) atomicMax(reinterpret_cast<long long*>(hdr), (long long)m);
+  }
+  if (errbits) set_err(err, errbits);
+  UPD_TRACE(6);
+  mintree_update<NT>(S, L, tree, idx, n, mins);
 }
 
 // One instantiation per mode: each kernel carries only its own path (the MODE_SEQ code in a
@@ -435,11 +602,16 @@ k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__
               const float* __restrict__ td, const int64_t* __restrict__ qin, int64_t n,
               double alpha, double eps_p, int32_t* err, int force_slow, int64_t T_p, double eta, int live_only) {
   __shared__ UpdSmem S;
-  if (RPL_PDL_EARLY & 1) pdl_trigger();  // A/B knob (common.cuh)
+  if ((RPL_PDL_EARLY & 1) && RPL_UPD_TRIGGER_AT == 0) pdl_trigger();  // A/B knob (common.cuh)
+  UPD_TRACE(7);
   pdl_wait();
   UPD_TRACE(0);
-  tree_update_block<UPD_THREADS, mode>(S, L, tree, idx, td, qin, n, alpha, eps_p, err, force_slow, T_p, eta,
-                                 live_only);
+  if (RPL_UPD_SINGLE && n <= (mode == MODE_SEQ ? UPD_THREADS / 8 : UPD_THREADS))
+    tree_update_single<UPD_THREADS, mode>(S, L, tree, idx, td, qin, n, alpha, eps_p, err, force_slow, T_p, eta,
+                                          live_only);
+  else
+    tree_update_block<UPD_THREADS, mode>(S, L, tree, idx, td, qin, n, alpha, eps_p, err, force_slow, T_p, eta,
+                                   live_only);
 }
 
 // First stratum k in [0, n] whose prefix is >= x (n if none).
@@ -463,8 +635,10 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
               const int64_t* __restrict__ totals, int use_stream, int64_t* __restrict__ out_count,
               int64_t* const* boards, int64_t stage_cap, int tot_stride, int64_t* __restrict__ out_bufmin) {
   const int lane = threadIdx.x & 31;
+  const DivN dn = divn_make((uint64_t)(n > 0 ? n : 1));  // n alone: before the dependency wait
   if (RPL_PDL_EARLY & 2) pdl_trigger();  // A/B knob (common.cuh)
   pdl_wait();
+  UPD_TRACE(8);
   // Stage the top levels (root .. the deepest level that still fits STAGE_WORDS) in shared
   // memory with one round of asynchronous 16-B copies, so the descent's first levels and Q
   // cost one L2 round trip in total instead of one each.  Levels are contiguous from word 0.
@@ -568,7 +742,7 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
     if (Q == 0) {
       errbits |= RPL_DERR_EMPTY;
     } else {
-      uint64_t prefix = stratum_prefix(k, Q, n, draws, seed, ctr0);
+      uint64_t prefix = strata_prefix(k, strata_make(Q, dn), draws, seed, ctr0);
       mine = true;
       if (SHARDED) {
         mine = prefix >= own_lo && prefix < own_lo + own_T;
@@ -610,6 +784,7 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
         *ticket = 0ull;
       }
     }
+    SMP_TRACE_END();
     return;
   }
   // last CTA: batch-min q and IS weights (§8c #10)
@@ -626,7 +801,10 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
     s_last = (t == (unsigned long long)gridDim.x - 1);
   }
   __syncthreads();
-  if (!s_last) return;
+  if (!s_last) {
+    SMP_TRACE_END();
+    return;
+  }
   int64_t m = INT64_MAX;
   for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
     const int64_t qj = __ldcg(out_q + j);
@@ -1262,6 +1440,16 @@ extern "C" int rpl_debug_set_tree_stage(int32_t on) {
   if (on != 0 && on != 1) return RPL_EINVAL;
   g_tree_stage.store(on);
   return RPL_OK;
+}
+
+extern "C" int rpl_debug_trace_reset(void) {
+#ifdef RPL_TRACE
+  unsigned long long z[16] = {0};
+  return cudaMemcpyToSymbol(rpl::g_trace, z, sizeof(z)) == cudaSuccess && rpl_debug_gather_trace_reset() == RPL_OK
+             ? RPL_OK : RPL_ECUDA;
+#else
+  return RPL_EUNSUPPORTED;
+#endif
 }
 
 extern "C" int rpl_debug_trace(int64_t* out, int32_t n) {

@@ -5,7 +5,8 @@ Launch configuration of bench.py: [4000, 256] ring (7.2 GB, BASELINE configs[4])
 episodes (mean 25 rows, so episode starts fall inside frame stacks), 25,600-leaf tree,
 64 sequences x 125 rows, k = 4, n = 5, gamma 0.997, alpha 0.9, beta 0.6, eta 0.9, the
 three-launch step (update_seq -> sample_stream -> gather with stacked frames, batch-min IS
-weights and fused rescaled 5-step targets), PDL-chained and captured in one CUDA graph of P
+weights and fused rescaled 5-step targets) and bench.py's default two-launch step
+(update_seq -> rpl_gather_sample: the stratified draws inside the gather), PDL-chained and captured in one CUDA graph of P
 steps, replayed twice.  Every step's tree, indices, q, weights, every output of all 64
 sequences and every target are compared with the oracle doing the same chain from the same
 seeded inputs (its own priority transform, sequence mix, Philox draws, stratified search,
@@ -46,7 +47,8 @@ def _window(dr, leaf):
 
 
 @pytest.mark.timeout(900)
-def test_r2d2_step_chain_vs_oracle(cuda):
+@pytest.mark.parametrize("mode", ["fused", "pair"])
+def test_r2d2_step_chain_vs_oracle(cuda, mode):
     import torch
     import paper_1909_01500_b200 as rpl
     from synth.device import make_ring_device
@@ -81,6 +83,9 @@ def test_r2d2_step_chain_vs_oracle(cuda):
         cur, prev = idx_b[j], idx_b[(j - 1) % P]
         rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(prev), P_(td_slot[j]), TRAIN, N,
                                                   ETA, ALPHA, EPS_P, 0, None, s), "update_seq")
+        if mode == "fused":
+            plans[j].run_sample(tree, SEED, cur, q_b[j], beta=BETA, err=err, stream=s, q_tgt=q_slot[j])
+            return
         rpl._lib.check(lib.rpl_sumtree_sample_stream(tree._lp, P_(tree.storage), N, SEED, BETA, P_(cur),
                                                      P_(q_b[j]), None, None, P_(err), s), "sample")
         plans[j].run(cur, q=q_b[j], qmin=None, beta=BETA, err=err, stream=s, q_tgt=q_slot[j])
