@@ -662,6 +662,15 @@ int rpl_debug_trace(int64_t* out, int32_t n);
  * dependency wait, 2 CTA 0's first frames landed, 3 last CTA end.  The _reset calls clear
  * both (rpl_debug_trace_reset) or the gather's only.  RPL_EUNSUPPORTED in the default build. */
 int rpl_debug_trace_reset(void);
+/* Measurement knob (process-global, read at each update launch): where rpl_sumtree_update(_ex /
+ * _seq / set_q)'s kernel lets the dependent grid launch — -1 at exit, 0 at entry, 3 after its
+ * loads are issued, 2 (default) after the priorities, 4 after the power transform (2-4: a batch
+ * of one chunk; larger batches trigger at exit).  RPL_EINVAL for other values. */
+int rpl_debug_set_upd_trigger(int32_t at);
+/* Measurement knob (process-global, read at each sequence-gather launch): where the default
+ * sequence gather lets the dependent grid launch — -1 at exit (default), 0 at entry, 1 once
+ * every CTA's producer has issued its last frame load.  RPL_EINVAL for other values. */
+int rpl_debug_set_gather_trigger(int32_t at);
 int rpl_debug_gather_trace(int64_t* out, int32_t n);
 int rpl_debug_gather_trace_reset(void);
 

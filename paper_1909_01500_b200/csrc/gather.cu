@@ -958,7 +958,8 @@ __device__ __forceinline__ void smp_ticket_finish(const GDesc& D, const int64_t*
 template <int NC>
 __global__ void __launch_bounds__((NC + 2) * 32, 1)
 k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, int64_t rows_per_cta,
-                      const int64_t* __restrict__ q, const int64_t* __restrict__ qmin, double beta, int32_t* err) {
+                      const int64_t* __restrict__ q, const int64_t* __restrict__ qmin, double beta, int32_t* err,
+                      int trig_at) {
   extern __shared__ __align__(128) uint8_t smem[];  // NS frame slots
   __shared__ __align__(8) uint64_t full[PIPE_MAX_NS];
   // per piece p (sample s = s_first + p)
@@ -995,7 +996,7 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   }
   for (int c = tid; c < PL_MAX_ROWS; c += NT) row_done[c] = 0;
   if (tid == 0) s_issued = 0;
-  if (RPL_PDL_EARLY & 4) pdl_trigger();  // A/B knob (common.cuh)
+  if (trig_at == 0) pdl_trigger();  // A/B knob (rpl_debug_set_gather_trigger; RPL_PDL_EARLY & 4 sets 0)
 #ifdef RPL_TRACE
   if (tid == 0 && blockIdx.x == 0) g_gtrace[0] = global_ns();
 #endif
@@ -1124,6 +1125,9 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
     p_blk[pc] = blk;
   }
   __syncthreads();
+#ifdef RPL_TRACE
+  if (tid == 0 && blockIdx.x == 0) g_gtrace[7] = global_ns();
+#endif
   // (B) frame positions: exclusive scan over pieces (serial: a CTA holds one to a few pieces).
   //     A piece loads window rows tau0-(k-1) .. tau0+R-1, except in RPL_OUT_UNIQUE mode when it
   //     starts mid-sample (tau0 > 0, only a CTA's first piece): its rows store only their newest
@@ -1189,6 +1193,8 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
           if (++slot == NS) slot = 0;
         }
       }
+      // knob 1: the dependent grid may launch once every CTA's producer has issued its last load
+      if (trig_at == 1) pdl_trigger();
       // tail: observe the last phase of every armed slot, so the CTA never exits with bulk
       // copies into its shared memory in flight (also frames no row reads)
       if (!(GDIAG(D) & 2))
@@ -1431,12 +1437,16 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
 #endif
   pdl_trigger();
 }
+// Measurement knob: where the sequence gather lets its dependent grid launch (-1 at exit,
+// 0 at entry, 1 once the CTA's producer has issued its last load); rpl_debug_set_gather_trigger.
+std::atomic<int> g_gather_trigger{(RPL_PDL_EARLY & 4) ? 0 : -1};
+
 template <int NC>
 int launch_seq_lsu(const GDesc& g, const int64_t* idx, int64_t n, int NS, int64_t rows_per_cta, const int64_t* q,
                    const int64_t* qmin, double beta, int32_t* dev_err, size_t dyn, int64_t grid, cudaStream_t st) {
   ensure_smem(reinterpret_cast<const void*>(k_gather_seq_pipe_lsu<NC>), dyn);
   return launch_pdl(k_gather_seq_pipe_lsu<NC>, dim3((unsigned)grid), dim3((NC + 2) * 32), dyn, st, g, idx, n, NS,
-                    rows_per_cta, q, qmin, beta, dev_err);
+                    rows_per_cta, q, qmin, beta, dev_err, g_gather_trigger.load(std::memory_order_relaxed));
 }
 
 // ---------------------------------------------------------------------------
@@ -2004,6 +2014,12 @@ extern "C" int rpl_debug_gather_trace(int64_t* out, int32_t n) {
   (void)n;
   return RPL_EUNSUPPORTED;
 #endif
+}
+
+extern "C" int rpl_debug_set_gather_trigger(int32_t at) {
+  if (at < -1 || at > 1) return RPL_EINVAL;
+  g_gather_trigger.store(at);
+  return RPL_OK;
 }
 
 extern "C" int rpl_debug_set_gather_variant(int32_t variant) {

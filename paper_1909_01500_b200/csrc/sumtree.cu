@@ -34,9 +34,6 @@ namespace {
 #define RPL_SAMPLE_WARPS 4  // same-box A/B: R2D2 step 69.06 vs 69.20 us at 8; DQN bs32 / 512 step 15.67 / 22.00 vs 15.83 / 22.14
 #endif
 constexpr int UPD_THREADS = RPL_UPD_THREADS;
-#ifndef RPL_UPD_TRIGGER_AT  // with RPL_PDL_EARLY & 1: where the single-chunk update triggers (0 entry, 3/2/4 stages)
-#define RPL_UPD_TRIGGER_AT 0
-#endif
 #ifndef RPL_UPD_SINGLE  // build-flag A/B knob: 0 = every batch through the chunked update
 #define RPL_UPD_SINGLE 1
 #endif
@@ -475,7 +472,7 @@ __device__ __forceinline__ void tree_update_single(UpdSmem& S, const TreeDev& L,
                                                    const int64_t* __restrict__ idx, const float* __restrict__ td,
                                                    const int64_t* __restrict__ qin, int64_t n, double alpha,
                                                    double eps_p, int32_t* err, int force_slow, int64_t T_p,
-                                                   double eta, int live_only) {
+                                                   double eta, int live_only, int trig_at) {
   unsigned long long* hkey = S.hkey;
   int* hval = S.hval;
   int64_t* sred = S.sred;
@@ -501,7 +498,7 @@ __device__ __forceinline__ void tree_update_single(UpdSmem& S, const TreeDev& L,
   }
   __syncthreads();
   UPD_TRACE(3);
-  if ((RPL_PDL_EARLY & 1) && RPL_UPD_TRIGGER_AT == 3) pdl_trigger();  // A/B: the dependent launch from here
+  if (trig_at == 3) pdl_trigger();  // A/B knob: the dependent launch from here
   // (2) duplicate resolution on the indices, and the leaves' current values
   int32_t errbits = 0;
   if (leaf >= L.n_leaves) {
@@ -532,7 +529,7 @@ __device__ __forceinline__ void tree_update_single(UpdSmem& S, const TreeDev& L,
     if ((tid & 7) == 0 && jj < n) s_td[jj] = v;
   }
   UPD_TRACE(2);
-  if ((RPL_PDL_EARLY & 1) && RPL_UPD_TRIGGER_AT == 2) pdl_trigger();
+  if (trig_at == 2) pdl_trigger();
   __syncthreads();  // s_td and the hash table complete
   int64_t q = 0;
   if (leaf >= 0) {
@@ -563,7 +560,7 @@ __device__ __forceinline__ void tree_update_single(UpdSmem& S, const TreeDev& L,
   if (leaf >= 0 && live_only && old == 0) leaf = -1;
   int64_t local_max = (leaf >= 0 && mode != MODE_MAXSEEN) ? q : INT64_MIN;
   UPD_TRACE(4);
-  if ((RPL_PDL_EARLY & 1) && RPL_UPD_TRIGGER_AT == 4) pdl_trigger();
+  if (trig_at == 4) pdl_trigger();
   int64_t delta = 0;
   if (leaf >= 0 && hval[slot] == tid) {
     leaves[leaf] = q;
@@ -600,15 +597,16 @@ template <int mode>
 __global__ void __launch_bounds__(UPD_THREADS)
 k_tree_update(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__ idx,
               const float* __restrict__ td, const int64_t* __restrict__ qin, int64_t n,
-              double alpha, double eps_p, int32_t* err, int force_slow, int64_t T_p, double eta, int live_only) {
+              double alpha, double eps_p, int32_t* err, int force_slow, int64_t T_p, double eta, int live_only,
+              int trig_at) {
   __shared__ UpdSmem S;
-  if ((RPL_PDL_EARLY & 1) && RPL_UPD_TRIGGER_AT == 0) pdl_trigger();  // A/B knob (common.cuh)
+  if (trig_at == 0) pdl_trigger();  // A/B knob (rpl_debug_set_upd_trigger; RPL_PDL_EARLY & 1 sets 0)
   UPD_TRACE(7);
   pdl_wait();
   UPD_TRACE(0);
   if (RPL_UPD_SINGLE && n <= (mode == MODE_SEQ ? UPD_THREADS / 8 : UPD_THREADS))
     tree_update_single<UPD_THREADS, mode>(S, L, tree, idx, td, qin, n, alpha, eps_p, err, force_slow, T_p, eta,
-                                          live_only);
+                                          live_only, trig_at);
   else
     tree_update_block<UPD_THREADS, mode>(S, L, tree, idx, td, qin, n, alpha, eps_p, err, force_slow, T_p, eta,
                                    live_only);
@@ -1140,6 +1138,16 @@ bool layout_ok(const rpl_tree_layout* L) {
          L->depth >= 1 && L->depth < RPL_MAX_LEVELS && L->frac_bits >= 0 && L->frac_bits <= 62;
 }
 
+// Where the update kernel lets its dependent grid launch (-1 at exit, 0 at entry, 3 after its
+// loads are issued, 2 after the priorities, 4 after the power transform; rpl_debug_set_upd_trigger).
+// Default 2: the next kernel's launch (the sequence gather's 146 CTAs take ~3 us to become
+// resident) overlaps the update's last ~2.5 us; it still waits for the update's completion in
+// its griddepcontrol.wait.  In-process A/B of the R2D2 step (scripts/ab_inproc.py, alternating
+// graphs): -1.0 us per step against the exit trigger, reproduced three times; entry (0) or
+// after the loads (3) gain less (-0.3 / 0.0 us), since the resident gather CTAs then slow the
+// update's loads (profiles/r2/ab_trigger_inproc.txt).
+std::atomic<int> g_upd_trigger{(RPL_PDL_EARLY & 1) ? 0 : 2};
+
 int launch_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, const float* td,
                   const int64_t* q, int mode, int64_t n, double alpha, double eps_p, int32_t* err,
                   void* stream, int force_slow, int64_t T_p = 0, double eta = 0.0, int live_only = 0) {
@@ -1147,12 +1155,12 @@ int launch_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, c
   if (n == 0) return RPL_OK;
   if (!idx) return RPL_EINVAL;
   void (*kern)(TreeDev, int64_t*, const int64_t*, const float*, const int64_t*, int64_t, double, double, int32_t*, int,
-               int64_t, double, int) = mode == MODE_SEQ  ? k_tree_update<MODE_SEQ>
+               int64_t, double, int, int) = mode == MODE_SEQ  ? k_tree_update<MODE_SEQ>
                                         : mode == MODE_Q ? k_tree_update<MODE_Q>
                                         : mode == MODE_MAXSEEN ? k_tree_update<MODE_MAXSEEN>
                                                                : k_tree_update<MODE_TD>;
   return launch_pdl(kern, dim3(1), dim3(UPD_THREADS), 0, as_stream(stream), tree_dev(L), tree, idx, td, q, n, alpha,
-                    eps_p, err, force_slow, T_p, eta, live_only);
+                    eps_p, err, force_slow, T_p, eta, live_only, g_upd_trigger.load(std::memory_order_relaxed));
 }
 
 }  // namespace
@@ -1439,6 +1447,12 @@ extern "C" int rpl_sumtree_update_sample(const rpl_tree_layout* L, int64_t* tree
 extern "C" int rpl_debug_set_tree_stage(int32_t on) {
   if (on != 0 && on != 1) return RPL_EINVAL;
   g_tree_stage.store(on);
+  return RPL_OK;
+}
+
+extern "C" int rpl_debug_set_upd_trigger(int32_t at) {
+  if (at != -1 && at != 0 && at != 2 && at != 3 && at != 4) return RPL_EINVAL;
+  g_upd_trigger.store(at);
   return RPL_OK;
 }
 
