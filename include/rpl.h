@@ -667,6 +667,10 @@ int rpl_debug_trace_reset(void);
  * loads are issued, 2 (default) after the priorities, 4 after the power transform (2-4: a batch
  * of one chunk; larger batches trigger at exit).  RPL_EINVAL for other values. */
 int rpl_debug_set_upd_trigger(int32_t at);
+/* Measurement knob (process-global): 1 (default) = update batches of n <= 1024 run on
+ * ceil(n / 64) CTAs (MODE_SEQ: n / 8), each resolving duplicates over the whole batch; 0 = the
+ * single-CTA kernels.  Identical results.  RPL_EINVAL for other values. */
+int rpl_debug_set_upd_multi(int32_t on);
 /* Measurement knob (process-global, read at each sequence-gather launch): where the default
  * sequence gather lets the dependent grid launch — -1 at exit (default), 0 at entry, 1 once
  * every CTA's producer has issued its last frame load.  RPL_EINVAL for other values. */

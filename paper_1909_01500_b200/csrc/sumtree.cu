@@ -97,6 +97,7 @@ __device__ unsigned long long g_trace[16];
   } while (0)
 #endif
 constexpr int HDR_GLOBAL_MIN = 6;
+constexpr int HDR_UPD_TICKET = 7;  // multi-CTA update's ticket (scratch, 0 between calls)
 
 // R2D2 sequence priority (§8f NEXT-1, reading R26): column i of the time-major per-step
 // |delta| [T_p, n] -> RN32(eta * max + (1 - eta) * RN64(exact sum) / T_p).  The sum is the
@@ -589,6 +590,159 @@ __device__ __forceinline__ void tree_update_single(UpdSmem& S, const TreeDev& L,
   if (errbits) set_err(err, errbits);
   UPD_TRACE(6);
   mintree_update<NT>(S, L, tree, idx, n, mins);
+}
+
+// Multi-CTA update of a batch of n <= HASH_SLOTS / 2 entries (the default for such batches).
+// One CTA is issue-bound: its 16 warps share one SM's four schedulers through ~1,500
+// instructions each of loads, the sequence mix and the power transform (the update was
+// ~5.5 us of the R2D2 step, scripts/step_trace.py).  Here each CTA owns UPDM_EPC entries
+// (MODE_SEQ: 8 sequences, eight lanes each; else one entry per thread) and the batch is
+// spread over ceil(n / UPDM_EPC) SMs.  Duplicate resolution stays exact without any
+// cross-CTA exchange: every CTA inserts ALL n indices into its own shared-memory hash (the
+// last valid position of every distinct leaf, S:624 — the indices alone decide it), so all
+// CTAs agree on the winners and each writes only its own winning entries.  Leaf writes are
+// plain stores to distinct leaves, propagation is int64 atomics (order-free, exact), max-seen
+// an atomicMax per CTA.  With a min-tree attached (R29) the CTA that takes the last ticket
+// (header word 7, acq_rel: it observes every CTA's leaf writes) recomputes the min paths of
+// all n entries.  Same result as tree_update_single / tree_update_block.
+constexpr int UPDM_THREADS = 64;
+template <int mode>
+__global__ void __launch_bounds__(UPDM_THREADS)
+k_tree_update_multi(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__ idx,
+                    const float* __restrict__ td, const int64_t* __restrict__ qin, int64_t n, double alpha,
+                    double eps_p, int32_t* err, int force_slow, int64_t T_p, double eta, int live_only, int trig_at) {
+  constexpr int EPC = mode == MODE_SEQ ? UPDM_THREADS / 8 : UPDM_THREADS;  // entries per CTA
+  __shared__ UpdSmem S;
+  unsigned long long* hkey = S.hkey;
+  int* hval = S.hval;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  for (int s2 = tid; s2 < HASH_SLOTS; s2 += UPDM_THREADS) {  // no global access: before the wait
+    hkey[s2] = HASH_EMPTY;
+    hval[s2] = -1;
+  }
+  if (trig_at == 0) pdl_trigger();
+  UPD_TRACE(7);
+  pdl_wait();
+  UPD_TRACE(0);
+  int64_t* leaves = tree + L.level_off[L.depth];
+  int64_t* hdr = tree + L.hdr_off;
+  const int64_t e0 = (int64_t)blockIdx.x * EPC;
+  const int64_t my = e0 + tid;  // this thread's entry (tid < EPC)
+  // (1) every independent load in flight at once
+  int64_t leaf = (tid < EPC && my < n) ? idx[my] : -1;
+  float tdi = 0.0f;
+  int64_t qi = 0;
+  if (mode == MODE_TD && tid < EPC && my < n) tdi = td[my];
+  if (mode == MODE_Q && tid < EPC && my < n) qi = qin[my];
+  float vals[mode == MODE_SEQ ? TD8_BATCH : 1];
+  const int64_t jj = e0 + (tid >> 3);  // MODE_SEQ: this lane's sequence
+  if (mode == MODE_SEQ) sequence_td8_load(reinterpret_cast<float(&)[TD8_BATCH]>(vals), td, T_p, n, jj, jj < n);
+  const int64_t maxseen_now = __ldcg(hdr);
+  const int64_t* mins = reinterpret_cast<const int64_t*>(__ldcg(hdr + HDR_MINTREE));
+  __syncthreads();  // the hash reset is complete
+  // (2) every index of the batch into this CTA's hash: the last valid position of each leaf
+  for (int64_t j = tid; j < n; j += UPDM_THREADS) {
+    const int64_t lj = idx[j];
+    bool vj = lj >= 0 && lj < L.n_leaves;
+    if (mode == MODE_Q && vj) vj = qin[j] >= 0;
+    if (vj) {
+      uint32_t slot = hash_slot(lj);
+      while (true) {
+        const unsigned long long prev = atomicCAS(&hkey[slot], HASH_EMPTY, (unsigned long long)lj);
+        if (prev == HASH_EMPTY || prev == (unsigned long long)lj) break;
+        slot = (slot + 1) & (HASH_SLOTS - 1);
+      }
+      atomicMax(&hval[slot], (int)j);
+    }
+  }
+  UPD_TRACE(3);
+  int32_t errbits = 0;
+  if (leaf >= L.n_leaves) {
+    errbits |= RPL_DERR_IDX;
+    leaf = -1;
+  } else if (leaf < 0) {
+    leaf = -1;  // padding entry (or no entry), skipped silently
+  } else if (mode == MODE_Q && qi < 0) {
+    errbits |= RPL_DERR_IDX;
+    leaf = -1;
+  }
+  const int64_t old = leaf >= 0 ? __ldcg(leaves + leaf) : 0;  // in flight during the priorities
+  // (3) the priorities (R26 sequence mix, R7 transform)
+  if (mode == MODE_SEQ) {
+    const float v = sequence_td8_finish(reinterpret_cast<const float(&)[TD8_BATCH]>(vals), td, T_p, n, jj, jj < n,
+                                        eta);
+    if ((tid & 7) == 0) S.s_td[tid >> 3] = v;
+  }
+  UPD_TRACE(2);
+  if (trig_at == 2) pdl_trigger();
+  __syncthreads();  // this CTA's sequence priorities and the hash complete
+  int64_t q = 0;
+  if (leaf >= 0) {
+    if (mode == MODE_TD || mode == MODE_SEQ) {
+      const float t = mode == MODE_SEQ ? S.s_td[tid] : tdi;
+      const double p = (double)fabsf(t) + eps_p;  // RN64(|delta| + eps_p)
+      float v;
+      if (!isfinite(p)) {
+        v = __int_as_float(0x7f800000);
+      } else {
+        bool slow = false;
+        v = cr_powf(p, alpha, force_slow != 0, &slow);
+      }
+      bool sat = false;
+      q = quantise_q(v, L.frac_bits, L.q_cap, &sat);
+      if (sat) errbits |= RPL_DERR_SATURATED;
+    } else if (mode == MODE_Q) {
+      q = qi;
+      if (q > L.q_cap) {
+        q = L.q_cap;
+        errbits |= RPL_DERR_SATURATED;
+      }
+    } else {
+      q = maxseen_now;
+    }
+  }
+  if (leaf >= 0 && live_only && old == 0) leaf = -1;  // R30
+  const int64_t local_max = (leaf >= 0 && mode != MODE_MAXSEEN) ? q : INT64_MIN;
+  UPD_TRACE(4);
+  if (trig_at == 4) pdl_trigger();
+  int64_t delta = 0;
+  if (leaf >= 0) {
+    uint32_t slot = hash_slot(leaf);
+    while (hkey[slot] != (unsigned long long)leaf) slot = (slot + 1) & (HASH_SLOTS - 1);
+    if (hval[slot] == (int)my) {  // the batch's last position of this leaf
+      leaves[leaf] = q;
+      delta = q - old;
+      if (delta != 0) {
+        int64_t node = leaf;
+        for (int l = L.depth - 1; l >= 1; --l) {
+          node >>= L.log2w;
+          atomicAdd(reinterpret_cast<unsigned long long*>(tree + L.level_off[l] + node), (unsigned long long)delta);
+        }
+      }
+    }
+  }
+  const int64_t rd = warp_sum64(delta);
+  if (lane == 0 && rd != 0)
+    atomicAdd(reinterpret_cast<unsigned long long*>(tree + L.level_off[0]), (unsigned long long)rd);
+  UPD_TRACE(5);
+  int64_t m = warp_max64(local_max);  // max-priority-seen
+  if (lane == 0 && m > maxseen_now) atomicMax(reinterpret_cast<long long*>(hdr), (long long)m);
+  if (errbits) set_err(err, errbits);
+  UPD_TRACE(6);
+  if (mins) {  // R29: the last CTA recomputes every written leaf's min path
+    __shared__ int s_last;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long t;
+      asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;"
+                   : "=l"(t) : "l"(hdr + HDR_UPD_TICKET) : "memory");
+      s_last = t == (unsigned long long)gridDim.x - 1;
+      if (s_last) hdr[HDR_UPD_TICKET] = 0;
+    }
+    __syncthreads();
+    if (s_last) mintree_update<UPDM_THREADS>(S, L, tree, idx, n, const_cast<int64_t*>(mins));
+  }
 }
 
 // One instantiation per mode: each kernel carries only its own path (the MODE_SEQ code in a
@@ -1147,6 +1301,9 @@ bool layout_ok(const rpl_tree_layout* L) {
 // after the loads (3) gain less (-0.3 / 0.0 us), since the resident gather CTAs then slow the
 // update's loads (profiles/r2/ab_trigger_inproc.txt).
 std::atomic<int> g_upd_trigger{(RPL_PDL_EARLY & 1) ? 0 : 2};
+// Measurement knob (rpl_debug_set_upd_multi): 1 (default) = batches of n <= HASH_SLOTS / 2 take
+// the multi-CTA update kernel, 0 = the single-CTA kernels only.
+std::atomic<int> g_upd_multi{1};
 
 int launch_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, const float* td,
                   const int64_t* q, int mode, int64_t n, double alpha, double eps_p, int32_t* err,
@@ -1159,8 +1316,19 @@ int launch_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, c
                                         : mode == MODE_Q ? k_tree_update<MODE_Q>
                                         : mode == MODE_MAXSEEN ? k_tree_update<MODE_MAXSEEN>
                                                                : k_tree_update<MODE_TD>;
+  const int trig = g_upd_trigger.load(std::memory_order_relaxed);
+  if (g_upd_multi.load(std::memory_order_relaxed) && n <= HASH_SLOTS / 2) {
+    void (*km)(TreeDev, int64_t*, const int64_t*, const float*, const int64_t*, int64_t, double, double, int32_t*, int,
+               int64_t, double, int, int) = mode == MODE_SEQ  ? k_tree_update_multi<MODE_SEQ>
+                                            : mode == MODE_Q ? k_tree_update_multi<MODE_Q>
+                                            : mode == MODE_MAXSEEN ? k_tree_update_multi<MODE_MAXSEEN>
+                                                                   : k_tree_update_multi<MODE_TD>;
+    const int epc = mode == MODE_SEQ ? UPDM_THREADS / 8 : UPDM_THREADS;
+    return launch_pdl(km, dim3((unsigned)((n + epc - 1) / epc)), dim3(UPDM_THREADS), 0, as_stream(stream), tree_dev(L),
+                      tree, idx, td, q, n, alpha, eps_p, err, force_slow, T_p, eta, live_only, trig);
+  }
   return launch_pdl(kern, dim3(1), dim3(UPD_THREADS), 0, as_stream(stream), tree_dev(L), tree, idx, td, q, n, alpha,
-                    eps_p, err, force_slow, T_p, eta, live_only, g_upd_trigger.load(std::memory_order_relaxed));
+                    eps_p, err, force_slow, T_p, eta, live_only, trig);
 }
 
 }  // namespace
@@ -1447,6 +1615,12 @@ extern "C" int rpl_sumtree_update_sample(const rpl_tree_layout* L, int64_t* tree
 extern "C" int rpl_debug_set_tree_stage(int32_t on) {
   if (on != 0 && on != 1) return RPL_EINVAL;
   g_tree_stage.store(on);
+  return RPL_OK;
+}
+
+extern "C" int rpl_debug_set_upd_multi(int32_t on) {
+  if (on != 0 && on != 1) return RPL_EINVAL;
+  g_upd_multi.store(on);
   return RPL_OK;
 }
 

@@ -18,6 +18,7 @@ KNOB = os.environ.get("KNOB", "upd_trigger")
 VA, VB = int(os.environ.get("A", "-1")), int(os.environ.get("B", "3"))
 setter = {"upd_trigger": rpl._lib.lib.rpl_debug_set_upd_trigger,
           "gather_trigger": rpl._lib.lib.rpl_debug_set_gather_trigger,
+          "upd_multi": rpl._lib.lib.rpl_debug_set_upd_multi,
           "gather_variant": rpl._lib.lib.rpl_debug_set_gather_variant,
           "scan_variant": rpl._lib.lib.rpl_debug_set_scan_variant}[KNOB]
 dev = torch.device("cuda:0")
@@ -57,6 +58,7 @@ def step(i):
 BASE = {k_: int(v_) for k_, v_ in (kv.split("=") for kv in os.environ.get("BASE", "").split(",") if kv)}
 for k_, v_ in BASE.items():  # other knobs held fixed for both graphs, e.g. BASE=upd_trigger=2
     assert {"upd_trigger": rpl._lib.lib.rpl_debug_set_upd_trigger,
+            "upd_multi": rpl._lib.lib.rpl_debug_set_upd_multi,
             "gather_trigger": rpl._lib.lib.rpl_debug_set_gather_trigger}[k_](v_) == 0
 
 

@@ -37,10 +37,15 @@ lib, P_ = rpl._lib.lib, rpl.ops._ptr
 MODE = os.environ.get("STEP", "pair")  # pair: update -> sample -> gather; fused: update -> gather_sample
 
 
+DOUBLE = os.environ.get("DOUBLE_UPD", "0") == "1"  # run the update twice (the trace shows the second)
+
+
 def step(i):
     s = rpl.ops._stream(dev)
-    rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(idx[(i + 1) % 2]), P_(td[i % 8]),
-                                              c["train"], n, c["eta"], c["alpha"], c["eps_p"], 0, None, s), "upd")
+    for _ in range(2 if DOUBLE else 1):
+        rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(idx[(i + 1) % 2]), P_(td[i % 8]),
+                                                  c["train"], n, c["eta"], c["alpha"], c["eps_p"], 0, None, s),
+                       "upd")
     if MODE == "fused":
         plan.run_sample(tree, 0xBEEF, idx[i % 2], q, beta=c["beta"], err=err, stream=s, q_tgt=qv[i % 8])
         return

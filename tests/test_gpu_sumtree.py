@@ -114,6 +114,14 @@ def test_priority_values_near_midpoints(rpl):
 
 
 @pytest.fixture(params=[1, 0])
+def upd_multi(rpl, request):
+    # 1: batches of n <= 1024 on the multi-CTA update kernel (default); 0: single-CTA kernels
+    assert rpl._lib.lib.rpl_debug_set_upd_multi(request.param) == 0
+    yield request.param
+    rpl._lib.lib.rpl_debug_set_upd_multi(1)
+
+
+@pytest.fixture(params=[1, 0])
 def tree_stage(rpl, request):
     # 1: the sampler stages the top levels in shared memory (all of a small tree; root +
     # 3 levels of 70000 leaves); 0: every level from global memory
@@ -123,7 +131,7 @@ def tree_stage(rpl, request):
 
 
 @pytest.mark.parametrize("n_leaves,W", [(16, 32), (100, 4), (1000, 32), (5000, 16), (70000, 32)])
-def test_random_updates_vs_oracle(rpl, n_leaves, W, tree_stage):
+def test_random_updates_vs_oracle(rpl, n_leaves, W, tree_stage, upd_multi):
     g = rng(n_leaves + W)
     tree = rpl.SumTree(n_leaves, W)
     orc = OS.SumTreeOracle(n_leaves)
@@ -150,7 +158,7 @@ def test_random_updates_vs_oracle(rpl, n_leaves, W, tree_stage):
         assert list(H(idx2)) == oi
 
 
-def test_set_q_maxseen_and_find(rpl):
+def test_set_q_maxseen_and_find(rpl, upd_multi):
     g = rng(3)
     n_leaves = 3000
     tree = rpl.SumTree(n_leaves, 32)
@@ -376,7 +384,7 @@ def test_sharded_compacted(rpl, mode):
 
 @pytest.mark.parametrize("T_p,n,eta", [(80, 64, 0.9), (1, 5, 0.9), (7, 300, 0.0), (80, 1200, 1.0), (33, 64, 0.37),
                                         (90, 100, 0.9), (91, 100, 0.9), (200, 70, 0.5)])
-def test_update_seq_vs_oracle(rpl, T_p, n, eta):
+def test_update_seq_vs_oracle(rpl, T_p, n, eta, upd_multi):
     # NEXT-1: R2D2 eta-mix of per-step |delta| per sequence, then the update — tree bit-exact
     import torch
     g = rng(T_p * 1000 + n)
@@ -418,7 +426,7 @@ def test_buffer_min_and_buffer_normalised_weights(rpl):
 
 
 @pytest.mark.parametrize("seq", [False, True])
-def test_update_live_only(rpl, seq):
+def test_update_live_only(rpl, seq, upd_multi):
     # RPL_UPD_LIVE_ONLY (R30): entries on zero leaves are skipped (no revival, no max-seen)
     g = rng(71)
     N = 5000
@@ -693,7 +701,7 @@ def _check_min_tree(t, orc):
 
 
 @pytest.mark.parametrize("N,W", [(25600, 32), (3000, 4), (1, 32), (100, 2)])
-def test_min_tree_maintained_by_every_writer(rpl, N, W):
+def test_min_tree_maintained_by_every_writer(rpl, N, W, upd_multi):
     # NEXT-4 / R29: the min-tree beside the sum tree stays exact through update, duplicate-heavy
     # update, update_seq, set_q (explicit zeros = invalidated leaves, max-seen), the fused
     # update+sample, replay validity and rebuild; the root is the buffer-wide normaliser
