@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define RPL_ABI_VERSION 1
+#define RPL_ABI_VERSION 2  /* 2: rpl_gather_desc.work appended */
 #define RPL_MAX_LEVELS 24
 
 typedef enum {
@@ -501,6 +501,14 @@ typedef struct {
    * Mode C: each owner signals the learner this way; the learner waits with rpl_wait_flags. */
   int64_t* done_flag;
   int64_t* done_seq;
+  /* Optional dynamic work distribution (SEQUENCE; one learner's whole batch: no col_offset,
+   * n_active, peer_boards or done_flag; also with rpl_gather_sample): device int64 [4],
+   * zero-initialised, owned by the caller.  With it the persistent gather splits a share of
+   * the rows statically and hands out the rest at run time in units of a few rows of one
+   * sample through an atomic counter in work[0], so CTAs on SMs that see less memory
+   * throughput take fewer rows (same outputs, bit for bit).  The call's last CTA re-zeroes
+   * work[0..3]; calls sharing a buffer must be stream-ordered.  NULL: the static split. */
+  int64_t* work;
 } rpl_gather_desc;
 
 int rpl_gather(const rpl_gather_desc* desc /* host */, const int64_t* idx, const int64_t* q,
@@ -658,8 +666,8 @@ int rpl_debug_set_gather_diag(int32_t mask);
 int rpl_debug_trace(int64_t* out, int32_t n);
 /* Measurement builds only (-DRPL_TRACE): the R2D2 step timeline.  rpl_debug_trace slots 7
  * (update kernel entry), 8 (sampler past its dependency wait), 9 (last sampler CTA end);
- * rpl_debug_gather_trace (n <= 8): 0 sequence-gather CTA 0 entry, 1 CTA 0 past its
- * dependency wait, 2 CTA 0's first frames landed, 3 last CTA end.  The _reset calls clear
+ * rpl_debug_gather_trace (n <= 9): 0 sequence-gather CTA 0 entry, 1 CTA 0 past its
+ * dependency wait, 2 CTA 0's first frames landed, 3 last CTA end, 4-7 CTA 0's fused-sampling stages, 8 first CTA end.  The _reset calls clear
  * both (rpl_debug_trace_reset) or the gather's only.  RPL_EUNSUPPORTED in the default build. */
 int rpl_debug_trace_reset(void);
 /* Measurement knob (process-global, read at each update launch): where rpl_sumtree_update(_ex /
@@ -675,7 +683,21 @@ int rpl_debug_set_upd_multi(int32_t on);
  * sequence gather lets the dependent grid launch — -1 at exit (default), 0 at entry, 1 once
  * every CTA's producer has issued its last frame load.  RPL_EINVAL for other values. */
 int rpl_debug_set_gather_trigger(int32_t at);
+/* Measurement knobs of the dynamic-tail sequence gather (rpl_gather_desc.work): pct = the
+ * static share of the rows in percent of an even split (0: every row dynamic; -1: the static
+ * kernel; default 88), rows = the longest grab (1..32, default 16; a grab takes about
+ * 1/grid of the dynamic rows left, at least 2), lookahead = rows published but not yet stored
+ * below which a CTA grabs again (default 12).
+ * RPL_EINVAL out of range. */
+int rpl_debug_set_gather_dyn(int32_t pct, int32_t rows, int32_t lookahead);
 int rpl_debug_gather_trace(int64_t* out, int32_t n);
+/* Measurement builds only: for the first n (<= 512) CTAs of the last sequence-gather launch
+ * (host out, 3n int64): out[0, n) each CTA's globaltimer end; dynamic-tail kernel only:
+ * out[n, 2n) when its static rows were stored, out[2n, 3n) the dynamic units it took. */
+int rpl_debug_gather_cta_ends(int64_t* out, int32_t n);
+/* Measurement builds only: the dynamic tail's first 8 grabs of each of the first n CTAs (host
+ * out, 16n int64: per grab its globaltimer time and (rows << 32) | rows queued at the grab). */
+int rpl_debug_gather_grabs(int64_t* out, int32_t n);
 int rpl_debug_gather_trace_reset(void);
 
 #ifdef __cplusplus

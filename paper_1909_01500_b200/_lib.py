@@ -61,6 +61,7 @@ class GatherDesc(C.Structure):
         ("rescale_eps", C.c_double),
         ("v_term", C.c_void_p),
         ("done_flag", C.c_void_p), ("done_seq", C.c_void_p),
+        ("work", C.c_void_p),
     ]
 
 
@@ -130,7 +131,10 @@ _SIGS = {
     "rpl_debug_set_upd_trigger": ([I32], C.c_int),
     "rpl_debug_set_gather_trigger": ([I32], C.c_int),
     "rpl_debug_set_upd_multi": ([I32], C.c_int),
+    "rpl_debug_set_gather_dyn": ([I32, I32, I32], C.c_int),
     "rpl_debug_gather_trace": ([P, I32], C.c_int),
+    "rpl_debug_gather_cta_ends": ([P, I32], C.c_int),
+    "rpl_debug_gather_grabs": ([P, I32], C.c_int),
     "rpl_debug_gather_trace_reset": ([], C.c_int),
 }
 
@@ -150,7 +154,7 @@ def _load():
 
 
 lib = _load()
-assert lib.rpl_abi_version() == 1, "librpl ABI version mismatch"
+assert lib.rpl_abi_version() == 2, "librpl ABI version mismatch"
 
 
 def config() -> dict:

@@ -75,6 +75,11 @@ __device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src,
 __device__ __forceinline__ void flag_release(volatile int* f, int v) {
   asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32((const void*)f)), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const int64_t* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ int flag_acquire(volatile int* f) {
   int v;
   asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32((const void*)f)) : "memory");
@@ -206,6 +211,7 @@ struct GDesc {
   int64_t* smp_tree;    // fused stratified sampling (rpl_gather_sample; NULL: idx given)
   TreeDev smp_L;
   uint64_t smp_seed;
+  int64_t* work;        // dynamic-tail unit counter + ticket (rpl_gather_desc.work; NULL: static split)
 };
 
 // Output column offset (rpl_gather_desc.col_offset); read after pdl_wait.
@@ -917,7 +923,11 @@ constexpr int PL_MAX_ROWS = 256;  // output rows per CTA (host caps rows_per_cta
 // 0 CTA 0 entry, 1 CTA 0 past its dependency wait, 2 CTA 0's first frame landed
 // (its first consumer row's mbarrier), 3 last CTA end (max).
 #ifdef RPL_TRACE
-__device__ unsigned long long g_gtrace[8];
+__device__ unsigned long long g_gtrace[9];
+__device__ unsigned long long g_gend[512];  // per-CTA end of the last launch
+__device__ unsigned long long g_gstatic[512];  // dynamic tail: per-CTA time its static rows were stored
+__device__ unsigned long long g_gunits[512];   // dynamic tail: per-CTA units taken
+__device__ unsigned long long g_ggrab[512][8][2];  // dynamic tail: per-CTA first grabs: time, (rows << 32) | queued
 #endif
 
 // Fused sampling's batch reduction (one warp of the CTA that took the last ticket): the batch
@@ -1002,7 +1012,11 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
 #endif
   pdl_wait();  // idx (and n_active) come from the sampler launched just before
 #ifdef RPL_TRACE
-  if (tid == 0 && blockIdx.x == 0) g_gtrace[1] = global_ns();
+  if (tid == 0 && blockIdx.x == 0) {  // the previous launch is complete: this launch's end slots
+    g_gtrace[1] = global_ns();
+    g_gtrace[3] = 0;
+    g_gtrace[8] = ~0ull;
+  }
 #endif
   // rows g = s*L + tau of the active samples, split evenly over the grid
   const int total = (int)(active_n(D, n) * L);
@@ -1113,7 +1127,9 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
         row0 = (int)(((int64_t)blk * period + tau0) % cap);
       }
       if (tau0 == 0) {
-        const int64_t age = wrap(D.cursor - 1 - (int64_t)blk * period, D.cap_T);
+        // cursor, blk * period < cap_T < 2^30 (host-checked): 32-bit modulo
+        int age = ((int)D.cursor - 1 - blk * period) % cap;
+        if (age < 0) age += cap;
         const int hist = k - 1 > 1 ? k - 1 : 1;
         if (!(age >= L - 1 && age + hist <= D.size - 1)) set_err(err, RPL_DERR_INVALID_LEAF);
       }
@@ -1433,13 +1449,25 @@ k_gather_seq_pipe_lsu(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
   }
 #ifdef RPL_TRACE
   __syncthreads();
-  if (threadIdx.x == 0) atomicMax(&g_gtrace[3], (unsigned long long)global_ns());
+  if (threadIdx.x == 0) {
+    const unsigned long long t = global_ns();
+    atomicMax(&g_gtrace[3], t);
+    atomicMin(&g_gtrace[8], t);
+    if (blockIdx.x < 512) g_gend[blockIdx.x] = t;
+  }
 #endif
   pdl_trigger();
 }
 // Measurement knob: where the sequence gather lets its dependent grid launch (-1 at exit,
 // 0 at entry, 1 once the CTA's producer has issued its last load); rpl_debug_set_gather_trigger.
 std::atomic<int> g_gather_trigger{(RPL_PDL_EARLY & 4) ? 0 : -1};
+// Dynamic-tail sequence gather (k_gather_seq_dyn): the static share of the rows (percent of
+// an even split, 0 = every row dynamic; -1 = the static kernel), the rows per dynamic unit, and the look-ahead (rows
+// published but not yet stored below which the meta warp grabs the next unit).
+// rpl_debug_set_gather_dyn.
+std::atomic<int> g_dyn_pct{88};   // in-process sweeps (scripts/ab_dyn_sweep.py, profiles/r2/dyn_sweep.txt)
+std::atomic<int> g_dyn_rows{16};
+std::atomic<int> g_dyn_look{12};
 
 template <int NC>
 int launch_seq_lsu(const GDesc& g, const int64_t* idx, int64_t n, int NS, int64_t rows_per_cta, const int64_t* q,
@@ -1447,6 +1475,564 @@ int launch_seq_lsu(const GDesc& g, const int64_t* idx, int64_t n, int NS, int64_
   ensure_smem(reinterpret_cast<const void*>(k_gather_seq_pipe_lsu<NC>), dyn);
   return launch_pdl(k_gather_seq_pipe_lsu<NC>, dim3((unsigned)grid), dim3((NC + 2) * 32), dyn, st, g, idx, n, NS,
                     rows_per_cta, q, qmin, beta, dev_err, g_gather_trigger.load(std::memory_order_relaxed));
+}
+
+// ---------------------------------------------------------------------------
+// Sequences with a DYNAMIC TAIL (default when rpl_gather_desc.work is given and the call is a
+// single learner's batch: no col_offset / n_active / peer boards / completion flag / fused
+// sampling).  Same pipeline and roles as k_gather_seq_pipe_lsu, but the rows are not all split
+// statically: measured with the step timeline (-DRPL_TRACE, scripts/step_trace.py), the 146
+// CTAs of the static split finish between 44 and 63 us for the same 55 rows — the SMs do not
+// all see the same memory throughput — so the launch ended ~8 us after its median CTA.  Here
+// CTA c takes the static rows [c*rs, (c+1)*rs) (rs = a fraction of the even share) and the
+// remaining rows are handed out at run time through an atomic row counter (work[0]), GUIDED:
+// a grab takes ~1/(2 grid) of the rows still left, between 2 and `dyn_rows`, so the early
+// grabs are long and the last ones short.  The meta warp grabs when fewer than `lookahead` of
+// the CTA's published rows are not yet stored, publishes the grab's pieces and row tables
+// (the producer and the consumers pick them up through release/acquire counters), then
+// writes their per-row fields.  A piece that starts mid-sample reloads its k-1 history frames.
+// The last CTA to leave (ticket work[1]) re-zeroes the counters.
+// ---------------------------------------------------------------------------
+constexpr int DY_MAX_ROWS = 256;
+constexpr int DY_MAX_PIECES = 96;
+
+template <int NC>
+__global__ void __launch_bounds__((NC + 3) * 32, 1)
+k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, int rs, int dyn_rows,
+                 int lookahead, const int64_t* __restrict__ q, const int64_t* __restrict__ qmin, double beta,
+                 int32_t* err, int trig_at) {
+  extern __shared__ __align__(128) uint8_t smem[];  // NS frame slots
+  __shared__ __align__(8) uint64_t full[PIPE_MAX_NS];
+  // per piece (a run of rows of one sample)
+  __shared__ int p_s[DY_MAX_PIECES];        // sample (batch position)
+  __shared__ int p_b[DY_MAX_PIECES];        // ring column, -1: skipped sample
+  __shared__ int p_row0[DY_MAX_PIECES];     // ring row of the piece's first output row
+  __shared__ int p_blk[DY_MAX_PIECES];      // storage block (stored RNN state)
+  __shared__ int p_F[DY_MAX_PIECES];        // frame position of the piece's first loaded frame
+  __shared__ short p_tau0[DY_MAX_PIECES];   // tau of the piece's first row
+  __shared__ short p_R[DY_MAX_PIECES];      // rows
+  __shared__ int8_t p_skip[DY_MAX_PIECES];  // leading history frames not loaded (unique mode)
+  // per output row c
+  __shared__ int row_new[DY_MAX_ROWS];  // frame position of the row's NEWEST frame (-1: skipped)
+  __shared__ int rel[DY_MAX_ROWS];      // frames released once rows <= c are done
+  __shared__ int row_ring[DY_MAX_ROWS];
+  __shared__ short row_piece[DY_MAX_ROWS];
+  __shared__ short row_tau[DY_MAX_ROWS];
+  __shared__ int8_t start_off[DY_MAX_ROWS];
+  __shared__ volatile int row_done[DY_MAX_ROWS];
+  __shared__ volatile int s_issued;      // frame positions issued (producer, release)
+  __shared__ volatile int s_pieces_pub;  // pieces whose tables are complete (release)
+  __shared__ volatile int s_rows_pub;    // rows whose tables are complete (release)
+  __shared__ volatile int s_frontier;    // rows [0, s_frontier) stored (producer's view)
+  __shared__ volatile int s_more;        // 0 once no further piece will be published
+  constexpr int NT = (NC + 3) * 32;  // producer, meta, fields, NC consumers
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int k = D.k, L = D.seq_len;
+  const int ob = (int)D.obs_bytes;
+  const int nv = ob / 16;
+  const int cap = (int)D.cap_T, Bc = (int)D.B, period = (int)D.period;
+  const int64_t nleaves = (int64_t)(cap / period) * Bc;
+  const bool unique = D.out_mode == RPL_OUT_UNIQUE;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+    s_issued = 0;
+    s_frontier = 0;
+    s_more = 1;
+  }
+  for (int c = tid; c < DY_MAX_ROWS; c += NT) row_done[c] = 0;
+  if (trig_at == 0) pdl_trigger();
+#ifdef RPL_TRACE
+  if (tid == 0 && blockIdx.x == 0) g_gtrace[0] = global_ns();
+#endif
+  pdl_wait();  // idx / q come from the sampler launched just before
+#ifdef RPL_TRACE
+  if (tid == 0 && blockIdx.x == 0) {
+    g_gtrace[1] = global_ns();
+    g_gtrace[3] = 0;
+    g_gtrace[8] = ~0ull;
+  }
+#endif
+  const int total = (int)(n * L);
+  const int g0 = min(total, (int)blockIdx.x * rs);
+  const int g1 = min(total, g0 + rs);
+  // dynamic units over rows [gridDim.x * rs, total): a partial first sample, then whole samples
+  const int r0 = min(total, (int)gridDim.x * rs);
+  const int su0 = r0 / L, tu0 = r0 - su0 * L;
+  const int sfull = su0 + (tu0 > 0 ? 1 : 0);  // the first wholly dynamic sample
+  const int s_first = g0 / L;
+  const int np0 = g1 > g0 ? (g1 - 1) / L - s_first + 1 : 0;
+  // (S) fused sampling (rpl_gather_sample), as in k_gather_seq_pipe_lsu: top levels staged in
+  //     the frame-slot area, one warp per static piece descends; CTA c also descends the
+  //     wholly dynamic samples sfull + c + j * grid (their units may run on any CTA: they read the index from
+  //     global memory once every CTA has counted itself into work[2]).  Each sample's index /
+  //     q is written once (its first row's static owner, or its assigned CTA); the ticket /
+  //     batch-min weights / stream advance follow in the meta warp.
+  const bool smp = D.smp_tree != nullptr;
+  __shared__ int64_t p_leaf[DY_MAX_PIECES];
+  uint64_t smp_pos = 0;
+  const DivN smp_dn = divn_make(smp ? (uint64_t)n : 1ull);
+  if (smp) {
+    const int64_t* top = reinterpret_cast<const int64_t*>(smem);
+    int64_t ntop = 0;
+    const int64_t cap_words = (int64_t)NS * ob / 8;
+    for (int l = 0; l <= D.smp_L.depth; ++l) {
+      const int64_t end = l < D.smp_L.depth ? D.smp_L.level_off[l + 1] : D.smp_L.hdr_off;
+      if (end > cap_words) break;
+      ntop = end;
+    }
+    for (int64_t j = 2 * (int64_t)tid; j < ntop; j += 2 * NT)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem + j * 8)), "l"(D.smp_tree + j)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    smp_pos = (uint64_t)__ldcg(D.smp_tree + D.smp_L.hdr_off + 2);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const uint64_t smp_Q = (uint64_t)(ntop > 0 ? top[0] : __ldcg(D.smp_tree + D.smp_L.level_off[0]));
+    const Strata smp_st = strata_make(smp_Q, smp_dn);
+    // wholly dynamic samples sfull + blockIdx.x + j * gridDim.x are this CTA's to descend
+    const int first_x = sfull + (int)blockIdx.x;
+    const int extra = (r0 < total && first_x < (int)n) ? ((int)n - first_x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+    int32_t eb = 0;
+    for (int pc = warp; pc < np0 + extra; pc += NT / 32) {
+      const int sm = pc < np0 ? s_first + pc : first_x + (pc - np0) * (int)gridDim.x;
+      int64_t leaf = -1, qv = 0;
+      if (smp_Q == 0) {
+        eb |= RPL_DERR_EMPTY;
+      } else {
+        const uint64_t prefix = strata_prefix(sm, smp_st, nullptr, D.smp_seed, smp_pos);
+        leaf = descend(D.smp_L, D.smp_tree, (int64_t)prefix, &qv, &eb, top, ntop);
+      }
+      if (lane == 0) {
+        if (pc < np0) p_leaf[pc] = leaf;
+        if (pc >= np0 || sm * L >= g0) {
+          const_cast<int64_t*>(idx)[sm] = leaf;
+          const_cast<int64_t*>(q)[sm] = qv;
+        }
+      }
+    }
+    if (lane == 0 && eb) set_err(err, eb);
+    fence_proxy_async();  // the staged words were read through the generic proxy; TMA refills them
+    __syncthreads();
+    if (tid == 0) {  // this CTA's index / q writes are done (release)
+      __threadfence();
+      atomicAdd(reinterpret_cast<unsigned long long*>(D.work + 2), 1ull);
+    }
+    if (g1 <= g0 && warp == 0) smp_ticket_finish(D, idx, q, n, beta, smp_pos);  // no static rows: ticket now
+  }
+  // ---- (A) static pieces (one per sample overlapping [g0, g1)), in parallel
+  for (int pc = tid; pc < np0; pc += NT) {
+    const int sm = s_first + pc;
+    const int tau0 = max(g0 - sm * L, 0);
+    const int R = min(g1, (sm + 1) * L) - max(g0, sm * L);
+    const int64_t leaf = smp ? p_leaf[pc] : idx[sm];
+    int bcol = -1, row0 = 0, blk = 0;
+    if (leaf >= 0 && leaf < nleaves) {
+      blk = (int)(leaf / Bc);
+      bcol = (int)(leaf - (int64_t)blk * Bc);
+      row0 = (int)(((int64_t)blk * period + tau0) % cap);
+      if (tau0 == 0) {
+        int age = ((int)D.cursor - 1 - blk * period) % cap;
+        if (age < 0) age += cap;
+        const int hist = k - 1 > 1 ? k - 1 : 1;
+        if (!(age >= L - 1 && age + hist <= D.size - 1)) set_err(err, RPL_DERR_INVALID_LEAF);
+      }
+    } else if (leaf >= nleaves && tau0 == 0) {
+      set_err(err, RPL_DERR_IDX);
+    }
+    p_s[pc] = sm;
+    p_b[pc] = bcol;
+    p_row0[pc] = row0;
+    p_blk[pc] = blk;
+    p_tau0[pc] = (short)tau0;
+    p_R[pc] = (short)R;
+    p_skip[pc] = (int8_t)((unique && tau0 > 0) ? k - 1 : 0);
+  }
+  __syncthreads();
+  // ---- (B) frame positions of the static pieces (serial: one to a few)
+  __shared__ int s_F_total;
+  if (tid == 0) {
+    int F = 0;
+    for (int pc = 0; pc < np0; ++pc) {
+      p_F[pc] = F;
+      if (p_b[pc] >= 0) F += p_R[pc] + k - 1 - p_skip[pc];
+    }
+    s_F_total = F;
+    s_pieces_pub = np0;
+    s_rows_pub = g1 - g0;
+  }
+  __syncthreads();
+  // row-table entry of row c (piece pc, m-th row of the piece); done flags loaded together
+  auto row_entry = [&](int c, int pc, int m) {
+    const int bcol = p_b[pc];
+    const int R = p_R[pc];
+    const int skip = p_skip[pc];
+    const int F = p_F[pc];
+    int8_t so = 0;
+    int ring = 0;
+    if (bcol >= 0) {
+      const int nw = F + m + (k - 1) - skip;
+      row_new[c] = nw;
+      rel[c] = m == R - 1 ? F + R + k - 1 - skip : (unique ? nw + 1 : nw - (k - 1) + 1);
+      ring = p_row0[pc] + m;
+      if (ring >= cap) ring -= cap;
+      uint8_t dw[8];
+#pragma unroll
+      for (int j = 1; j < 8; ++j) {
+        int rr = ring - k + j;
+        while (rr < 0) rr += cap;
+        dw[j] = j < k ? __ldg(D.done + (int64_t)rr * Bc + bcol) : (uint8_t)0;
+      }
+#pragma unroll
+      for (int j = 1; j < 8; ++j)
+        if (dw[j]) so = (int8_t)j;
+    } else {
+      row_new[c] = -1;
+      rel[c] = F;
+    }
+    row_ring[c] = ring;
+    row_piece[c] = (short)pc;
+    row_tau[c] = (short)(p_tau0[pc] + m);
+    start_off[c] = so;
+  };
+  // per-row fields, fused targets, IS weight and stored state of rows [ca, cb) (meta warp)
+  auto row_fields = [&](int ca, int cb, int64_t qm) {
+    const int64_t ab = D.act_bytes;
+    const bool a8 = ab == 8 && ((reinterpret_cast<uintptr_t>(D.act) | reinterpret_cast<uintptr_t>(D.o_act) |
+                                 reinterpret_cast<uintptr_t>(D.o_prev_act)) & 7) == 0;
+    for (int c = ca + lane; c < cb; c += 32) {
+      if (row_new[c] < 0) continue;
+      const int pc = row_piece[c];
+      const int sm = p_s[pc];
+      const int tau = row_tau[c];
+      const int bcol = p_b[pc];
+      const int ring = row_ring[c];
+      const int prow = ring == 0 ? cap - 1 : ring - 1;
+      const int64_t e = (int64_t)ring * Bc + bcol, pe = (int64_t)prow * Bc + bcol;
+      const uint8_t pd = __ldg(D.done + pe);
+      const uint8_t dd = __ldg(D.done + e);
+      const float rw = D.o_rew ? __ldg(D.rew + e) : 0.0f;
+      const float prw = D.o_prev_rew ? __ldg(D.rew + pe) : 0.0f;
+      const int64_t o = (int64_t)tau * n + sm;
+      if (a8) {
+        const uint64_t* a = reinterpret_cast<const uint64_t*>(D.act);
+        const uint64_t av = D.o_act ? __ldg(a + e) : 0ull;
+        const uint64_t pav = D.o_prev_act ? __ldg(a + pe) : 0ull;
+        if (D.o_act) reinterpret_cast<uint64_t*>(D.o_act)[o] = av;
+        if (D.o_prev_act) reinterpret_cast<uint64_t*>(D.o_prev_act)[o] = pd ? 0ull : pav;
+      } else {
+        if (D.o_act) coop_copy(D.o_act + o * ab, D.act + e * ab, ab, 0, 1);
+        if (D.o_prev_act) {
+          if (pd) coop_zero(D.o_prev_act + o * ab, ab, 0, 1);
+          else coop_copy(D.o_prev_act + o * ab, D.act + pe * ab, ab, 0, 1);
+        }
+      }
+      if (D.o_rew) D.o_rew[o] = rw;
+      if (D.o_prev_rew) D.o_prev_rew[o] = pd ? 0.0f : prw;
+      if (D.o_done) D.o_done[o] = dd;
+      if (D.o_start) D.o_start[o] = start_off[c];
+      if (tau == 0 && D.o_w && q && !smp) {
+        const int64_t qs = q[sm];
+        D.o_w[sm] = qs > 0 ? (float)pow((double)qm / (double)qs, beta) : 0.0f;
+      }
+    }
+    if (D.o_tgt) {  // fused n-step targets (a2 + a4, R5 / R24 / R34)
+      const int ns = D.n_step;
+      for (int c = ca + lane; c < cb; c += 32) {
+        if (row_new[c] < 0) continue;
+        const int t = row_tau[c] - D.tgt_lo;
+        if (t < 0 || t >= D.tgt_T) continue;
+        const int64_t col = p_s[row_piece[c]];
+        double acc = 0.0;
+        if (D.q_tgt) {
+          const double qv = (double)__ldg(D.q_tgt + (int64_t)(row_tau[c] + ns) * n + col);
+          acc = D.rescale ? h_inv(qv, D.rescale_eps) : qv;
+        }
+        uint8_t dn = 0;
+        acc = nstep_rows(D, row_ring[c], p_b[row_piece[c]], ns, acc, &dn);
+        if (D.rescale) acc = h_fwd(acc, D.rescale_eps);
+        D.o_tgt[(int64_t)t * n + col] = (float)acc;
+        if (D.o_tgt_done) D.o_tgt_done[(int64_t)t * n + col] = dn ? 1 : 0;
+      }
+    }
+    if (D.o_rnn) {  // stored recurrent state of every sample whose first row is in [ca, cb)
+      const int nparts = D.rnn_parts;
+      const int64_t rb = D.rnn_bytes;
+      for (int c = ca; c < cb; ++c) {
+        if (row_tau[c] != 0 || row_new[c] < 0) continue;
+        const int pc = row_piece[c];
+        const int64_t blk = p_blk[pc], bcol = p_b[pc];
+        const int sm = p_s[pc];
+        for (int pp = 0; pp < nparts; ++pp)
+          coop_copy(D.o_rnn + (pp * n + sm) * rb, D.rnn + ((blk * Bc + bcol) * nparts + pp) * rb, rb, lane, 32);
+      }
+    }
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- producer: TMA loads of every published piece ----------------
+      int frontier = 0, released = 0, i = 0, slot = 0;
+      auto advance = [&]() {  // the contiguous done-frontier (also read by the meta warp)
+        if (frontier < flag_acquire(&s_rows_pub) && flag_acquire(&row_done[frontier])) {
+          released = rel[frontier];
+          ++frontier;
+          s_frontier = frontier;
+#ifdef RPL_TRACE
+          if (frontier == g1 - g0 && blockIdx.x < 512) g_gstatic[blockIdx.x] = global_ns();
+#endif
+          return true;
+        }
+        return false;
+      };
+      for (int pc = 0;; ++pc) {
+        while (pc >= flag_acquire(&s_pieces_pub)) {  // wait for the next piece (or the end)
+          if (!flag_acquire(&s_more) && pc >= flag_acquire(&s_pieces_pub)) goto prod_done;
+          if (!advance()) __nanosleep(32);
+        }
+        const int bcol = p_b[pc];
+        if (bcol < 0) continue;
+        const int R = p_R[pc];
+        const int skip = p_skip[pc];
+        int row = p_row0[pc] - (k - 1) + skip;
+        while (row < 0) row += cap;
+        const uint8_t* col = D.obs + (int64_t)bcol * ob;
+        const int64_t rstride = (int64_t)Bc * ob;
+        for (int w = skip; w < R + k - 1; ++w, ++i) {
+          if (i >= NS) {
+            while (released <= i - NS)
+              if (!advance()) __nanosleep(20);
+            fence_proxy_async();
+            mbar_wait(&full[slot], (uint32_t)(((i / NS) - 1) & 1));
+          }
+          mbar_expect_tx(&full[slot], (uint32_t)ob);
+          bulk_g2s_evict_first(smem + slot * ob, col + (int64_t)row * rstride, (uint32_t)ob, &full[slot]);
+          flag_release(&s_issued, i + 1);
+          if (++row == cap) row = 0;
+          if (++slot == NS) slot = 0;
+        }
+      }
+    prod_done:
+      if (trig_at == 1) pdl_trigger();
+      // observe the last phase of every armed slot: no bulk copy into shared memory is in
+      // flight when the CTA exits
+      for (int p = i > NS ? i - NS : 0; p < i; ++p) mbar_wait(&full[p % NS], (uint32_t)((p / NS) & 1));
+    }
+  } else {
+    // (C) static row tables, rows spread over warps 1..NC+2
+    for (int c = tid - 32; c < g1 - g0; c += NT - 32) {
+      const int g = g0 + c;
+      const int pc = g / L - s_first;
+      row_entry(c, pc, g - max(g0, p_s[pc] * L));
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"((NC + 2) * 32) : "memory");
+    if (warp == 2) {
+      // ---------------- fields warp: per-row fields of every published row, in order ----------------
+      const int64_t qm = (D.o_w && q && !smp) ? warp_batch_qmin(qmin, idx, q, n) : 0;
+      int fd = 0;
+      while (true) {
+        const int rp = flag_acquire(&s_rows_pub);
+        if (fd < rp) {
+          const int fe = min(rp, fd + 32);
+          row_fields(fd, fe, qm);
+          fd = fe;
+        } else if (!flag_acquire(&s_more) && fd >= flag_acquire(&s_rows_pub)) {
+          break;
+        } else {
+          __nanosleep(64);
+        }
+      }
+    } else if (warp == 1) {
+      // ---------------- meta warp: the dynamic tail ----------------
+      if (smp && g1 > g0) smp_ticket_finish(D, idx, q, n, beta, smp_pos);  // fused sampling's ticket / weights
+      bool idx_ready = !smp;
+      int F = s_F_total;
+      int pcn = np0, cn = g1 - g0;
+      const int ndyn = total - r0;  // dynamic rows [r0, total); work[0] counts the rows taken
+      int grabs = 0;
+      bool exhausted = ndyn <= 0;
+      while (!exhausted) {
+        // grab only when this CTA is about to run dry (a slower SM takes less), and GUIDED: a
+        // grab takes ~1/grid of what is left, between 2 and dyn_rows rows, so early grabs are
+        // long (few reloaded history frames) and the last ones short (fine balance)
+        if (cn - s_frontier <= lookahead) {
+          if (cn + dyn_rows > DY_MAX_ROWS || pcn + 2 > DY_MAX_PIECES) {
+            exhausted = true;
+            continue;
+          }
+          int start = 0, cnt = 0;
+          if (lane == 0) {
+            const int taken = (int)__ldcg(D.work);
+            int sz = (ndyn - taken) / (int)gridDim.x;
+            sz = sz < 2 ? 2 : (sz > dyn_rows ? dyn_rows : sz);
+            if (sz > L) sz = L;  // a grab spans at most two samples (two pieces)
+            start = (int)atomicAdd(reinterpret_cast<unsigned long long*>(D.work), (unsigned long long)sz);
+            cnt = min(sz, ndyn - start);
+          }
+          start = __shfl_sync(0xffffffffu, start, 0);
+          cnt = __shfl_sync(0xffffffffu, cnt, 0);
+          if (cnt <= 0) {
+            exhausted = true;
+            continue;
+          }
+#ifdef RPL_TRACE
+          if (lane == 0 && blockIdx.x < 512 && grabs < 8) {
+            g_ggrab[blockIdx.x][grabs][0] = global_ns();
+            g_ggrab[blockIdx.x][grabs][1] = ((unsigned long long)cnt << 32) | (unsigned)(cn - s_frontier);
+          }
+#endif
+          ++grabs;
+          if (!idx_ready) {  // fused sampling: every CTA has written its samples' indices
+            if (lane == 0)
+              while (ld_acquire_u64(D.work + 2) < (unsigned long long)gridDim.x) __nanosleep(64);
+            __syncwarp();
+            idx_ready = true;
+          }
+          // the grabbed rows [ga, gb) as pieces of whole samples: tables first (published), fields later
+          for (int ga = r0 + start, gb = r0 + start + cnt; ga < gb;) {
+            const int sm = ga / L;
+            const int tau0 = ga - sm * L;
+            const int R = min(gb, (sm + 1) * L) - ga;
+            if (lane == 0) {
+              const int64_t leaf = __ldcg(idx + sm);
+              int bcol = -1, row0 = 0, blk = 0;
+              if (leaf >= 0 && leaf < nleaves) {
+                blk = (int)(leaf / Bc);
+                bcol = (int)(leaf - (int64_t)blk * Bc);
+                row0 = (int)(((int64_t)blk * period + tau0) % cap);
+                if (tau0 == 0) {
+                  int age = ((int)D.cursor - 1 - blk * period) % cap;
+                  if (age < 0) age += cap;
+                  const int hist = k - 1 > 1 ? k - 1 : 1;
+                  if (!(age >= L - 1 && age + hist <= D.size - 1)) set_err(err, RPL_DERR_INVALID_LEAF);
+                }
+              } else if (leaf >= nleaves && tau0 == 0) {
+                set_err(err, RPL_DERR_IDX);
+              }
+              const int skip = (unique && tau0 > 0) ? k - 1 : 0;
+              p_s[pcn] = sm;
+              p_b[pcn] = bcol;
+              p_row0[pcn] = row0;
+              p_blk[pcn] = blk;
+              p_F[pcn] = F;
+              p_tau0[pcn] = (short)tau0;
+              p_R[pcn] = (short)R;
+              p_skip[pcn] = (int8_t)skip;
+            }
+            __syncwarp();
+            if (lane < R) row_entry(cn + lane, pcn, lane);
+            __syncwarp();
+            if (p_b[pcn] >= 0) F += R + k - 1 - p_skip[pcn];
+            if (lane == 0) {
+              flag_release(&s_rows_pub, cn + R);
+              flag_release(&s_pieces_pub, pcn + 1);
+            }
+            cn += R;
+            ++pcn;
+            ga += R;
+          }
+        } else {
+          __nanosleep(64);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) flag_release(&s_more, 0);
+#ifdef RPL_TRACE
+      if (lane == 0 && blockIdx.x < 512) g_gunits[blockIdx.x] = (unsigned long long)grabs;
+#endif
+    } else {
+      // ---------------- consumers: one k-stack per published row ----------------
+      for (int c = warp - 3;; c += NC) {
+        while (c >= flag_acquire(&s_rows_pub)) {
+          if (!flag_acquire(&s_more) && c >= flag_acquire(&s_rows_pub)) goto cons_done;
+          __nanosleep(32);
+        }
+        {
+          const int pn = row_new[c];
+          const int sn = pn % NS;
+          const uint32_t parn = (uint32_t)((pn / NS) & 1);
+          auto slot_of = [&](int j, uint32_t* par) {
+            int sl = sn - (k - 1 - j);
+            *par = parn;
+            if (sl < 0) {
+              sl += NS;
+              *par ^= 1u;
+            }
+            return sl;
+          };
+          if (pn >= 0)
+            while (flag_acquire(&s_issued) <= pn) __nanosleep(20);
+          const int sm = p_s[row_piece[c]];
+          const int tau = row_tau[c];
+          if (pn >= 0 && unique) {
+            for (int j = tau == 0 ? 0 : k - 1; j < k; ++j) {
+              uint32_t par;
+              const int sl = slot_of(j, &par);
+              mbar_wait(&full[sl], par);
+              int4* d = reinterpret_cast<int4*>(D.o_obs + ((int64_t)(tau + j) * n + sm) * ob);
+              const int4* sp = reinterpret_cast<const int4*>(smem + sl * ob);
+#pragma unroll 4
+              for (int v = lane; v < nv; v += 32) __stcs(d + v, sp[v]);
+            }
+          } else if (pn >= 0) {
+            const int so = start_off[c];
+            for (int j = so; j < k; ++j) {
+              uint32_t par;
+              const int sl = slot_of(j, &par);
+              mbar_wait(&full[sl], par);
+            }
+            int4* dst = reinterpret_cast<int4*>(D.o_obs + ((int64_t)tau * n + sm) * k * ob);
+            for (int j = 0; j < k; ++j) {
+              int4* d = dst + j * nv;
+              if (j < so && D.pad_mode == RPL_PAD_ZERO) {
+                for (int v = lane; v < nv; v += 32) d[v] = make_int4(0, 0, 0, 0);
+              } else {
+                uint32_t par;
+                const int sl = slot_of(j < so ? so : j, &par);
+                const int4* sp = reinterpret_cast<const int4*>(smem + sl * ob);
+#pragma unroll 4
+                for (int v = lane; v < nv; v += 32) __stcs(d + v, sp[v]);
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) {
+            fence_proxy_async();
+            flag_release(&row_done[c], 1);
+          }
+        }
+      }
+    cons_done:;
+    }
+  }
+  __syncthreads();
+#ifdef RPL_TRACE
+  if (threadIdx.x == 0) {
+    const unsigned long long t = global_ns();
+    atomicMax(&g_gtrace[3], t);
+    atomicMin(&g_gtrace[8], t);
+    if (blockIdx.x < 512) g_gend[blockIdx.x] = t;
+  }
+#endif
+  if (threadIdx.x == 0) {  // the last CTA out re-zeroes the unit counter and the ticket
+    unsigned long long t;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(t) : "l"(D.work + 1) : "memory");
+    if (t == (unsigned long long)gridDim.x - 1) {
+      D.work[0] = 0;
+      D.work[1] = 0;
+      D.work[2] = 0;
+    }
+  }
+  if (trig_at != 0 && trig_at != 1) pdl_trigger();
+}
+
+template <int NC>
+int launch_seq_dyn(const GDesc& g, const int64_t* idx, int64_t n, int NS, int rs, int dyn_rows, int lookahead,
+                   const int64_t* q, const int64_t* qmin, double beta, int32_t* dev_err, size_t dyn, int64_t grid,
+                   cudaStream_t st) {
+  ensure_smem(reinterpret_cast<const void*>(k_gather_seq_dyn<NC>), dyn);
+  return launch_pdl(k_gather_seq_dyn<NC>, dim3((unsigned)grid), dim3((NC + 3) * 32), dyn, st, g, idx, n, NS, rs,
+                    dyn_rows, lookahead, q, qmin, beta, dev_err, g_gather_trigger.load(std::memory_order_relaxed));
 }
 
 // ---------------------------------------------------------------------------
@@ -1536,7 +2122,9 @@ k_gather_seq_ldg_bulk(GDesc D, const int64_t* __restrict__ idx, int64_t n, int N
       bcol = (int)(leaf - (int64_t)blk * Bc);
       row0 = (int)(((int64_t)blk * period + tau0) % cap);
       if (tau0 == 0) {
-        const int64_t age = wrap(D.cursor - 1 - (int64_t)blk * period, D.cap_T);
+        // cursor, blk * period < cap_T < 2^30 (host-checked): 32-bit modulo
+        int age = ((int)D.cursor - 1 - blk * period) % cap;
+        if (age < 0) age += cap;
         const int hist = k - 1 > 1 ? k - 1 : 1;
         if (!(age >= L - 1 && age + hist <= D.size - 1)) set_err(err, RPL_DERR_INVALID_LEAF);
       }
@@ -1973,6 +2561,7 @@ GDesc to_dev(const rpl_gather_desc* d) {
   g.v_term = d->v_term;
   g.done_flag = d->done_flag;
   g.done_seq = d->done_seq;
+  g.work = d->work;
   g.smp_tree = nullptr;
   g.smp_seed = 0;
   return g;
@@ -1998,22 +2587,56 @@ using namespace rpl;
 
 extern "C" int rpl_debug_gather_trace_reset(void) {
 #ifdef RPL_TRACE
-  unsigned long long z[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long z[9] = {0, 0, 0, 0, 0, 0, 0, 0, ~0ull};
   return cudaMemcpyToSymbol(rpl::g_gtrace, z, sizeof(z)) == cudaSuccess ? RPL_OK : RPL_ECUDA;
 #else
   return RPL_EUNSUPPORTED;
 #endif
 }
 
+extern "C" int rpl_debug_gather_cta_ends(int64_t* out, int32_t n) {
+#ifdef RPL_TRACE
+  if (!out || n < 1 || n > 512) return RPL_EINVAL;
+  // out[0..n): CTA ends; out[n..2n): static-rows-stored times; out[2n..3n): dynamic units taken
+  return (cudaMemcpyFromSymbol(out, rpl::g_gend, sizeof(int64_t) * (size_t)n) == cudaSuccess &&
+          cudaMemcpyFromSymbol(out + n, rpl::g_gstatic, sizeof(int64_t) * (size_t)n) == cudaSuccess &&
+          cudaMemcpyFromSymbol(out + 2 * n, rpl::g_gunits, sizeof(int64_t) * (size_t)n) == cudaSuccess)
+             ? RPL_OK : RPL_ECUDA;
+#else
+  (void)out;
+  (void)n;
+  return RPL_EUNSUPPORTED;
+#endif
+}
+
+extern "C" int rpl_debug_gather_grabs(int64_t* out, int32_t n) {
+#ifdef RPL_TRACE
+  if (!out || n < 1 || n > 512) return RPL_EINVAL;
+  return cudaMemcpyFromSymbol(out, rpl::g_ggrab, sizeof(int64_t) * 16 * (size_t)n) == cudaSuccess ? RPL_OK : RPL_ECUDA;
+#else
+  (void)out;
+  (void)n;
+  return RPL_EUNSUPPORTED;
+#endif
+}
+
 extern "C" int rpl_debug_gather_trace(int64_t* out, int32_t n) {
 #ifdef RPL_TRACE
-  if (!out || n < 1 || n > 8) return RPL_EINVAL;
+  if (!out || n < 1 || n > 9) return RPL_EINVAL;
   return cudaMemcpyFromSymbol(out, rpl::g_gtrace, sizeof(int64_t) * (size_t)n) == cudaSuccess ? RPL_OK : RPL_ECUDA;
 #else
   (void)out;
   (void)n;
   return RPL_EUNSUPPORTED;
 #endif
+}
+
+extern "C" int rpl_debug_set_gather_dyn(int32_t pct, int32_t rows, int32_t lookahead) {
+  if (pct < -1 || pct > 100 || rows < 1 || rows > 32 || lookahead < 1 || lookahead > 200) return RPL_EINVAL;
+  g_dyn_pct.store(pct);
+  g_dyn_rows.store(rows);
+  g_dyn_look.store(lookahead);
+  return RPL_OK;
 }
 
 extern "C" int rpl_debug_set_gather_trigger(int32_t at) {
@@ -2196,6 +2819,19 @@ int gather_run(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q
           desc->cap_T * desc->B < (1ll << 40)) {
         const size_t dyn = (size_t)NS * desc->obs_bytes;
         int64_t grid = (int64_t)sm_count();
+        // dynamic tail (rpl_gather_desc.work): one learner's whole batch only
+        const int dpct = g_dyn_pct.load(std::memory_order_relaxed);
+        const int drows = g_dyn_rows.load(std::memory_order_relaxed);
+        if (desc->work && dpct >= 0 && !desc->col_offset && !desc->n_active && !desc->peer_boards &&
+            !desc->done_flag && seq_variant == 0 && n <= (1 << 30) / desc->seq_len) {
+          int64_t rs = total * dpct / 100 / grid;
+          if (rs > DY_MAX_ROWS - 4 * drows) rs = DY_MAX_ROWS - 4 * drows;
+          if (rs < 0) rs = 0;
+          g.use_tma = 1;
+          return launch_seq_dyn<RPL_SEQ_CONSUMERS>(g, idx, n, NS, (int)rs, drows,
+                                                   g_dyn_look.load(std::memory_order_relaxed), q, qmin, beta,
+                                                   dev_err, dyn, grid, st);
+        }
         int64_t rows_per_cta = (total + grid - 1) / grid;
         if (rows_per_cta > PL_MAX_ROWS) rows_per_cta = PL_MAX_ROWS;
         grid = (total + rows_per_cta - 1) / rows_per_cta;

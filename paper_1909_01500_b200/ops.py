@@ -600,6 +600,10 @@ def gather(ring: GatherRing, idx, kind="transition", k=4, n_step=1, gamma=0.99, 
     for name, f in fields.items():
         if name in o and o[name] is not None:
             setattr(g, f, o[name].data_ptr())
+    work = None
+    if kind_i == _lib.GATHER_SEQUENCE:  # dynamic-tail work counter (rpl_gather_desc.work)
+        work = torch.zeros(4, dtype=torch.int64, device=dev)
+        g.work = work.data_ptr()
     e = err
     check(lib.rpl_gather(C.byref(g), _ptr(idx), _ptr(q), _ptr(qmin), float(beta), n, _ptr(e), _stream(dev)),
           "rpl_gather")
@@ -638,6 +642,9 @@ class GatherPlan:
         for name, f in fields.items():
             if name in self.outputs:
                 setattr(self.desc, f, self.outputs[name].data_ptr())
+        if kind_i == _lib.GATHER_SEQUENCE:  # dynamic-tail work counter (rpl_gather_desc.work)
+            self._work = torch.zeros(4, dtype=torch.int64, device=dev)
+            self.desc.work = self._work.data_ptr()
         self._dp = C.byref(self.desc)
         self.device = dev
         self.ring = ring

@@ -16,7 +16,15 @@ from synth.device import make_ring_device  # noqa: E402
 
 KNOB = os.environ.get("KNOB", "upd_trigger")
 VA, VB = int(os.environ.get("A", "-1")), int(os.environ.get("B", "3"))
+DYN_ROWS, DYN_LOOK = int(os.environ.get("DYN_ROWS", "5")), int(os.environ.get("DYN_LOOK", "8"))
+
+
+def _set_dyn(v):  # KNOB=dyn_pct: the static share of the dynamic-tail gather (0 = all dynamic? no: 0 = off)
+    return rpl._lib.lib.rpl_debug_set_gather_dyn(v, DYN_ROWS, DYN_LOOK)
+
+
 setter = {"upd_trigger": rpl._lib.lib.rpl_debug_set_upd_trigger,
+          "dyn_pct": _set_dyn,
           "gather_trigger": rpl._lib.lib.rpl_debug_set_gather_trigger,
           "upd_multi": rpl._lib.lib.rpl_debug_set_upd_multi,
           "gather_variant": rpl._lib.lib.rpl_debug_set_gather_variant,
@@ -63,7 +71,8 @@ for k_, v_ in BASE.items():  # other knobs held fixed for both graphs, e.g. BASE
 
 
 def capture(v):
-    assert setter(v) == 0
+    if v is not None:
+        assert setter(v) == 0
     for i in range(16):
         step(i)
     torch.cuda.synchronize()
@@ -77,18 +86,25 @@ def capture(v):
     return gr
 
 
-ga, gb = capture(VA), capture(VB)
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-res = {"A": [], "B": []}
-for r in range(20):
-    for name, gr in (("A", ga), ("B", gb)) if r % 2 == 0 else (("B", gb), ("A", ga)):
-        gr.replay()
-        e0.record()
-        for _ in range(10):
+def compare(graphs, rounds=20, reps=10):
+    """Median us per step of each graph, replayed round-robin (order rotated every round)."""
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    res = {name: [] for name in graphs}
+    names = list(graphs)
+    for r in range(rounds):
+        for name in names[r % len(names):] + names[:r % len(names)]:
+            gr = graphs[name]
             gr.replay()
-        e1.record()
-        torch.cuda.synchronize()
-        res[name].append(e0.elapsed_time(e1) * 1e3 / 80)
-med = {kk: sorted(v)[len(v) // 2] for kk, v in res.items()}
-print(json.dumps({"knob": KNOB, "A": VA, "B": VB, "step": "fused" if FUSED else "pair",
-                  "median_us_per_step": med, "delta_B_minus_A_us": med["B"] - med["A"]}))
+            e0.record()
+            for _ in range(reps):
+                gr.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            res[name].append(e0.elapsed_time(e1) * 1e3 / (8 * reps))
+    return {kk: sorted(v)[len(v) // 2] for kk, v in res.items()}
+
+
+if __name__ == "__main__":
+    med = compare({"A": capture(VA), "B": capture(VB)})
+    print(json.dumps({"knob": KNOB, "A": VA, "B": VB, "step": "fused" if FUSED else "pair",
+                      "median_us_per_step": med, "delta_B_minus_A_us": med["B"] - med["A"]}))

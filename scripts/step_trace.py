@@ -34,6 +34,8 @@ qv = torch.randn((8, L, n), generator=g, device=dev) * 10
 plan = rpl.GatherPlan(ring, n, kind="sequence", k=k, seq_len=L, period=period, with_weights=True,
                       targets=bench.r2d2_targets(c, qv[0]))
 lib, P_ = rpl._lib.lib, rpl.ops._ptr
+if os.environ.get("DYN"):  # DYN=pct,rows,lookahead (rpl_debug_set_gather_dyn)
+    assert lib.rpl_debug_set_gather_dyn(*(int(x) for x in os.environ["DYN"].split(","))) == 0
 MODE = os.environ.get("STEP", "pair")  # pair: update -> sample -> gather; fused: update -> gather_sample
 
 
@@ -69,9 +71,10 @@ torch.cuda.synchronize()
 names_u = {7: "update_entry", 0: "update_past_wait", 2: "update_mixed", 3: "update_hash_reset",
            4: "update_dedupe", 5: "update_leaves", 6: "update_end", 8: "sample_past_wait", 9: "sample_end"}
 names_g = {0: "gather_entry", 1: "gather_past_wait", 2: "gather_first_frames", 3: "gather_end",
-           4: "gather_smp_staged", 5: "gather_smp_sampled", 6: "gather_first_tma_issue", 7: "gather_pieces_done"}
+           4: "gather_smp_staged", 5: "gather_smp_sampled", 6: "gather_first_tma_issue", 7: "gather_pieces_done",
+           8: "gather_first_cta_end"}
 runs = []
-bu, bg = (ctypes.c_int64 * 16)(), (ctypes.c_int64 * 8)()
+bu, bg = (ctypes.c_int64 * 16)(), (ctypes.c_int64 * 9)()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 STEADY = os.environ.get("STEADY", "0") == "1"  # 1: 10 back-to-back replays per sample (steady state)
 for _ in range(30):
@@ -82,7 +85,7 @@ for _ in range(30):
         gr.replay()
     e1.record()
     torch.cuda.synchronize()
-    if lib.rpl_debug_trace(bu, 16) != 0 or lib.rpl_debug_gather_trace(bg, 8) != 0:  # not a trace build
+    if lib.rpl_debug_trace(bu, 16) != 0 or lib.rpl_debug_gather_trace(bg, 9) != 0:  # not a trace build
         runs.append({"graph_us_per_step": e0.elapsed_time(e1) * 1e3 / (80 if STEADY else 8)})
         continue
     t0 = bu[7]
@@ -91,5 +94,30 @@ for _ in range(30):
     r["graph_us_per_step"] = e0.elapsed_time(e1) * 1e3 / (80 if STEADY else 8)
     runs.append(r)
 med = {kk: sorted(r[kk] for r in runs if kk in r)[len([r for r in runs if kk in r]) // 2] for kk in runs[0]}
-print(json.dumps({"mode": MODE, "steady": STEADY, "ns_from_update_entry_median": dict(sorted(med.items(), key=lambda kv: kv[1])),
+ends = (ctypes.c_int64 * (3 * 146))()
+if lib.rpl_debug_gather_cta_ends(ends, 146) == 0:  # the last launch's per-CTA ends, relative to its update
+    import numpy as np
+    allv = np.array(list(ends), np.int64)
+    e = (allv[:146] - t0) / 1e3
+    st_ = (allv[146:292] - t0) / 1e3
+    un = allv[292:]
+    if un.sum() > 0:
+        order = np.argsort(e)
+        med["dyn_units_total"] = int(un.sum())
+        med["dyn_slowest8_end_static_units"] = [[int(i), round(float(e[i]), 2), round(float(st_[i]), 2), int(un[i])]
+                                                for i in order[-8:]]
+        med["dyn_fastest4_end_static_units"] = [[int(i), round(float(e[i]), 2), round(float(st_[i]), 2), int(un[i])]
+                                                for i in order[:4]]
+        gb = (ctypes.c_int64 * (16 * 146))()
+        if lib.rpl_debug_gather_grabs(gb, 146) == 0:
+            ga = np.array(list(gb), np.int64).reshape(146, 8, 2)
+            med["dyn_slowest4_grabs_t_rows_queued"] = [
+                [int(i), [[round((int(ga[i, j, 0]) - t0) / 1e3, 2), int(ga[i, j, 1]) >> 32, int(ga[i, j, 1]) & 0xffffffff]
+                          for j in range(min(8, int(un[i])))]] for i in order[-4:]]
+        med["dyn_static_done_p0_p50_p100"] = [round(float(np.percentile(st_[:145], p_)), 2) for p_ in (0, 50, 100)]
+    med["cta_end_us_percentiles_p0_p10_p50_p90_p100_last"] = [round(float(np.percentile(e[:145], p_)), 2)
+                                                            for p_ in (0, 10, 50, 90, 100)] + [round(float(e[145]), 2)]
+    med["cta_end_us_slowest_ctas"] = [int(x) for x in np.argsort(e)[-8:]]
+print(json.dumps({"mode": MODE, "steady": STEADY, "ns_from_update_entry_median": dict(sorted(med.items(), key=lambda kv: kv[1] if not isinstance(kv[1], list)
+                                                                     else 1e18)),
                   "note": "last step of a replayed 8-step graph; -DRPL_TRACE build"}, indent=1))

@@ -39,7 +39,7 @@ def test_exports_every_declared_symbol(lib):
 
 def test_version_and_strerror(lib):
     lib.rpl_abi_version.restype = ctypes.c_int
-    assert lib.rpl_abi_version() == 1
+    assert lib.rpl_abi_version() == 2
     lib.rpl_strerror.restype = ctypes.c_char_p
     assert b"invalid" in lib.rpl_strerror(-1)
 
