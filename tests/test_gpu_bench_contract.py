@@ -23,7 +23,7 @@ def test_bench_line_carries_every_contract_key(cuda):
                 "returns"):
         assert key in d, key
     assert d["steps"] == 8 and d["warmup"] == 3 and d["n_gpus"] == 1
-    assert d["value"] > 0 and d["gpu_launches"] >= 3 * 8
+    assert d["value"] > 0 and d["gpu_launches"] >= 2 * 8  # update + gather (sampling fused) per step
     r = d["roofline"]
     assert r["bound"] == "hbm" and 0 < r["frac"] < 1.2 and r["peak"] > 0
     e = d["e2e"]
