@@ -369,7 +369,13 @@ def run_rpl(args):
         if skip_gather:  # marginal-cost measurement: the same step without the gather launch
             return
         if gather_events is not None:
-            gather_events[0].record()
+            # the start event sits on a side branch that depends on the update's completion,
+            # so the update -> gather programmatic (PDL) edge stays intact; the gather itself
+            # waits for the same completion in its griddepcontrol.wait
+            side = gather_events[2]
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                gather_events[0].record()
         # IS weights fused into the gather: batch min (1 GPU) or the all-reduced global min (Mode L)
         if w_out is not None:
             plan.desc.o_w = w_out.data_ptr()
@@ -389,6 +395,7 @@ def run_rpl(args):
             plan.desc.o_tgt = y.data_ptr()
         if gather_events is not None:
             gather_events[1].record()
+            torch.cuda.current_stream(dev).wait_stream(gather_events[2])  # rejoin the side branch
         if mode_c:
             if rank == 0:  # learner: wait for every owner's completion flag (K8, no collective),
                 central.wait(stream=s)  # then the k-stacks from the shipped unique rows (local HBM)
@@ -512,17 +519,19 @@ def run_rpl(args):
     # dominant kernel (sequence gather): average launch duration with CUDA events on
     # the launching stream, over K eager steps of the same workload
     Kg = min(K_eff, 200)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(Kg)]
+    side = torch.cuda.Stream(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True), side) for _ in range(Kg)]
     torch.cuda.synchronize()
     for i in range(Kg):
         step(i, evs[i])
     torch.cuda.synchronize()
-    g_ms_eager = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    g_ms_eager = float(np.mean([a.elapsed_time(b) for a, b, _ in evs]))
     # the same launch inside the timed configuration: a graph of P steps whose gathers are
     # bracketed by event-record nodes (cudaEventRecordExternal), so no host enqueue gap
-    # falls inside the interval.  The nodes break the PDL edge into the gather (its launch
-    # latency is inside the interval), so this is still an upper bound on the launch's
-    # share of the graph step.
+    # falls inside the interval.  The start node sits on a side branch that waits for the
+    # update kernel's completion, so the update -> gather PDL edge stays intact (the gather's
+    # launch overlaps the update, and the interval starts where the gather's dependency wait
+    # ends); the end node follows the gather on the launching stream.
     g_ms_graph = None
     if use_graph and world == 1:
         try:
@@ -586,10 +595,12 @@ def run_rpl(args):
                      "frac_marginal": (alg_bytes / (g_ms_marginal / 1e3) / 1e9 / peak) if g_ms_marginal else None,
                      "marginal_note": ("step graph minus the same graph without the gather launch: the gather's "
                                        "in-step cost with the PDL edges intact (frac uses the event-bracketed "
-                                       "avg_launch_ms, which includes the gather's launch latency)"),
+                                       "avg_launch_ms)"),
                      "launch_timing": ("event-record nodes around each gather in the CUDA graph of the timed "
-                                       "steps (mean of P launches x 25 replays)" if g_ms_graph is not None
-                                       else "events around the gather in eager steps"),
+                                       "steps (the start node on a side branch after the update, so the PDL edge "
+                                       "into the gather stays intact; mean of P launches x 25 replays)"
+                                       if g_ms_graph is not None
+                                       else "events around the gather in eager steps (start event on a side branch)"),
                      "step_share": g_ms / (ms / K_eff),
                      "frac_of_spec": achieved / SPEC_HBM_GBS, "spec_peak": SPEC_HBM_GBS,
                      "spec_note": "north_star's ~8 TB/s nominal (DGX B200 figure) as the second denominator"},
@@ -1048,7 +1059,8 @@ def gather_ms_in_graph(dev, step, P, reps=25):
     """Mean gather launch duration (ms) over the P gathers of a graph of P steps, each
     bracketed by event-record nodes; averaged over `reps` replays."""
     import torch
-    evs = [(_ExtEvent(), _ExtEvent()) for _ in range(P)]
+    side = torch.cuda.Stream(dev)
+    evs = [(_ExtEvent(), _ExtEvent(), side) for _ in range(P)]
     torch.cuda.synchronize()
     st = torch.cuda.Stream(dev)
     st.wait_stream(torch.cuda.current_stream(dev))
@@ -1061,7 +1073,7 @@ def gather_ms_in_graph(dev, step, P, reps=25):
     for _ in range(reps):
         gr.replay()
         torch.cuda.synchronize()
-        tot += sum(a.ev.elapsed_time(b.ev) for a, b in evs) / P
+        tot += sum(a.ev.elapsed_time(b.ev) for a, b, _ in evs) / P
     return tot / reps
 
 
