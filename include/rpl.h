@@ -501,7 +501,7 @@ typedef struct {
    * Mode C: each owner signals the learner this way; the learner waits with rpl_wait_flags. */
   int64_t* done_flag;
   int64_t* done_seq;
-  /* Optional dynamic work distribution (SEQUENCE; one learner's whole batch: no col_offset,
+  /* Optional dynamic work distribution (SEQUENCE, stacked output; one learner's whole batch: no col_offset,
    * n_active, peer_boards or done_flag; also with rpl_gather_sample): device int64 [4],
    * zero-initialised, owned by the caller.  With it the persistent gather splits a share of
    * the rows statically and hands out the rest at run time in units of a few rows of one
@@ -675,9 +675,10 @@ int rpl_debug_trace_reset(void);
  * loads are issued, 2 (default) after the priorities, 4 after the power transform (2-4: a batch
  * of one chunk; larger batches trigger at exit).  RPL_EINVAL for other values. */
 int rpl_debug_set_upd_trigger(int32_t at);
-/* Measurement knob (process-global): 1 (default) = update batches of n <= 1024 run on
- * ceil(n / 64) CTAs (MODE_SEQ: n / 8), each resolving duplicates over the whole batch; 0 = the
- * single-CTA kernels.  Identical results.  RPL_EINVAL for other values. */
+/* Measurement knob (process-global): 1 (default) = rpl_sumtree_update_seq batches of n <= 1024
+ * run on ceil(n / 8) CTAs, rpl_sumtree_update / _ex / set_q batches of n <= 64 on one 64-thread
+ * CTA, each CTA resolving duplicates over the whole batch; 0 = the single-CTA kernels.
+ * Identical results.  RPL_EINVAL for other values. */
 int rpl_debug_set_upd_multi(int32_t on);
 /* Measurement knob (process-global, read at each sequence-gather launch): where the default
  * sequence gather lets the dependent grid launch — -1 at exit (default), 0 at entry, 1 once

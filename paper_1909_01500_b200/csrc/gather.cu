@@ -2822,12 +2822,20 @@ int gather_run(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q
         // dynamic tail (rpl_gather_desc.work): one learner's whole batch only
         const int dpct = g_dyn_pct.load(std::memory_order_relaxed);
         const int drows = g_dyn_rows.load(std::memory_order_relaxed);
+        // (stacked output only: unique rows are 4x cheaper, and the per-grab latency then costs
+        // more than the balance gains — the unique-output step measured 33.5 -> 43.4 us)
         if (desc->work && dpct >= 0 && !desc->col_offset && !desc->n_active && !desc->peer_boards &&
-            !desc->done_flag && seq_variant == 0 && n <= (1 << 30) / desc->seq_len) {
+            !desc->done_flag && seq_variant == 0 && desc->out_mode == RPL_OUT_STACKED &&
+            n <= (1 << 30) / desc->seq_len) {
           int64_t rs = total * dpct / 100 / grid;
           if (rs > DY_MAX_ROWS - 4 * drows) rs = DY_MAX_ROWS - 4 * drows;
           if (rs < 0) rs = 0;
           g.use_tma = 1;
+          // two SMs stay free for kernels running beside the gather (the pipelined step's
+          // update + sampler on a second stream), as with the static split's 146 CTAs
+          grid = grid > 8 ? grid - 2 : grid;
+          rs = total * dpct / 100 / grid;
+          if (rs > DY_MAX_ROWS - 4 * drows) rs = DY_MAX_ROWS - 4 * drows;
           return launch_seq_dyn<RPL_SEQ_CONSUMERS>(g, idx, n, NS, (int)rs, drows,
                                                    g_dyn_look.load(std::memory_order_relaxed), q, qmin, beta,
                                                    dev_err, dyn, grid, st);

@@ -1317,7 +1317,11 @@ int launch_update(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx, c
                                         : mode == MODE_MAXSEEN ? k_tree_update<MODE_MAXSEEN>
                                                                : k_tree_update<MODE_TD>;
   const int trig = g_upd_trigger.load(std::memory_order_relaxed);
-  if (g_upd_multi.load(std::memory_order_relaxed) && n <= HASH_SLOTS / 2) {
+  // multi-CTA where it wins (scripts/upd_multi_probe.py, graph of back-to-back updates): the
+  // sequence mix at every n <= 1024 (n = 64: 3.9 vs 4.9 us, 512: 7.8 vs 19.8 us); the plain
+  // transform only up to n = 64 (beyond, every CTA's hash of the whole batch costs more than
+  // the transform it spreads: n = 512 6.4 vs 3.5 us)
+  if (g_upd_multi.load(std::memory_order_relaxed) && n <= (mode == MODE_SEQ ? HASH_SLOTS / 2 : 64)) {
     void (*km)(TreeDev, int64_t*, const int64_t*, const float*, const int64_t*, int64_t, double, double, int32_t*, int,
                int64_t, double, int, int) = mode == MODE_SEQ  ? k_tree_update_multi<MODE_SEQ>
                                             : mode == MODE_Q ? k_tree_update_multi<MODE_Q>
