@@ -675,6 +675,10 @@ int rpl_debug_trace_reset(void);
  * loads are issued, 2 (default) after the priorities, 4 after the power transform (2-4: a batch
  * of one chunk; larger batches trigger at exit).  RPL_EINVAL for other values. */
 int rpl_debug_set_upd_trigger(int32_t at);
+/* Measurement builds only (-DRPL_TRACE): the last pipelined-scan launch's timeline (n <= 10
+ * globaltimer ns stamps, host out): CTA 0's entry, past its wait, first tiles landed, its three
+ * barriers, store issue and exit; the last and the first CTA's exits. */
+int rpl_debug_scan_trace(int64_t* out, int32_t n);
 /* Measurement knob (process-global): 1 (default) = rpl_sumtree_update_seq batches of n <= 1024
  * run on ceil(n / 8) CTAs, rpl_sumtree_update / _ex / set_q batches of n <= 64 on one 64-thread
  * CTA, each CTA resolving duplicates over the whole batch; 0 = the single-CTA kernels.

@@ -128,6 +128,7 @@ _SIGS = {
     "rpl_debug_set_gather_diag": ([I32], C.c_int),
     "rpl_debug_trace": ([P, I32], C.c_int),
     "rpl_debug_trace_reset": ([], C.c_int),
+    "rpl_debug_scan_trace": ([P, I32], C.c_int),
     "rpl_debug_set_upd_trigger": ([I32], C.c_int),
     "rpl_debug_set_gather_trigger": ([I32], C.c_int),
     "rpl_debug_set_upd_multi": ([I32], C.c_int),

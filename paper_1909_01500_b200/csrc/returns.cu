@@ -426,6 +426,21 @@ k_scan_tma2(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
 // a double-buffered output tile, so one item's scan overlaps the next items' loads and the
 // previous item's stores.  Groups are dealt round-robin to the grid (CTAs_per_SM x SMs).
 // ---------------------------------------------------------------------------
+// Measurement-only timeline of the pipelined scan (-DRPL_TRACE; rpl_debug_scan_trace): CTA 0's
+// first item: 0 entry, 1 past the dependency wait, 2 tiles landed, 3 barrier (1), 4 barrier (2),
+// 5 barrier (3), 6 store issued, 7 exit; 8 the last CTA's exit (max), 9 the first CTA's exit (min).
+#ifdef RPL_TRACE
+__device__ unsigned long long g_strace[10];
+#define SCAN_TRACE(k)                                                                \
+  do {                                                                               \
+    if (threadIdx.x == 0 && blockIdx.x == 0 && i == 0) g_strace[k] = global_ns();   \
+  } while (0)
+#else
+#define SCAN_TRACE(k) \
+  do {                \
+  } while (0)
+#endif
+
 template <int COLS, int WARPS, int S, int STAGES, bool GAE, int OB = 2>
 struct ScanPipeSmem {
   static constexpr int SUB = 32 / COLS;
@@ -498,7 +513,17 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_o0) : "memory");
   }
   __syncthreads();
+#ifdef RPL_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0) g_strace[0] = global_ns();
+#endif
   pdl_wait();
+#ifdef RPL_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    g_strace[1] = global_ns();
+    g_strace[8] = 0;
+    g_strace[9] = ~0ull;
+  }
+#endif
   if (threadIdx.x == 0)
     for (int64_t i = 0; i < STAGES && i < items; ++i) issue();
   // measurement knob (RPL_SCAN_TRIGGER=2): let the dependent grid launch once the first tiles
@@ -528,6 +553,7 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
             : "=r"(done) : "r"(s_u32(&sm.bar[st])), "r"(ph) : "memory");
       phases ^= 1u << st;
     }
+    SCAN_TRACE(2);
     const int64_t t0 = c * CH + (int64_t)seg * S;
     double b[S];
     float vv[S];
@@ -542,6 +568,7 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
       if (GAE) vv[k] = sm.v[st][seg * S + k][ci];
     }
     __syncthreads();  // (1) the new group's carry is visible; every thread holds its rows
+    SCAN_TRACE(3);
     const double bootv = (double)boot_f;
     double vseg_next = 0.0;
     if (GAE) {
@@ -603,6 +630,7 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
       else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     }
     __syncthreads();  // (2) maps visible; this stage is free; the output tile is free
+    SCAN_TRACE(4);
     if (threadIdx.x == 0 && i + STAGES < items) issue();
     double x = sm.carry[ci];
 #pragma unroll
@@ -616,6 +644,7 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy
     __syncthreads();  // (3) the output tile is complete; maps / carry reads done
+    SCAN_TRACE(5);
     if (seg == 0) {
       sm.carry[ci] = x;
       if (GAE) sm.vnext[ci] = vv[0];
@@ -629,6 +658,7 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
                      ::"l"(&tm_o1), "r"(x0), "r"(y0), "r"(s_u32(&sm.o1[ob][0][0])) : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
+    SCAN_TRACE(6);
     if (--c < 0) {
       c = nchunks - 1;
       g += gridDim.x;
@@ -639,6 +669,14 @@ k_scan_pipe(const __grid_constant__ CUtensorMap tm_r, const __grid_constant__ CU
   // out of shared memory (the bulk stores complete before the grid does, as for any store)
   pdl_trigger();
   if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#ifdef RPL_TRACE
+  if (threadIdx.x == 0) {
+    const unsigned long long t = global_ns();
+    if (blockIdx.x == 0) g_strace[7] = t;
+    atomicMax(&g_strace[8], t);
+    atomicMin(&g_strace[9], t);
+  }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -1219,6 +1257,17 @@ extern "C" int rpl_value_rescale(const float* x, float* y, int64_t n, double eps
   const int threads = 256;
   return launch_pdl(k_rescale, dim3(elementwise_grid((n + 3) / 4, threads)), dim3(threads), 0, as_stream(stream), x,
                     y, n, eps, inverse ? 1 : 0);
+}
+
+extern "C" int rpl_debug_scan_trace(int64_t* out, int32_t n) {
+#ifdef RPL_TRACE
+  if (!out || n < 1 || n > 10) return RPL_EINVAL;
+  return cudaMemcpyFromSymbol(out, rpl::g_strace, sizeof(int64_t) * (size_t)n) == cudaSuccess ? RPL_OK : RPL_ECUDA;
+#else
+  (void)out;
+  (void)n;
+  return RPL_EUNSUPPORTED;
+#endif
 }
 
 extern "C" int rpl_debug_set_scan_variant(int32_t variant) {

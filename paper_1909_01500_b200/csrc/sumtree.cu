@@ -196,22 +196,18 @@ __device__ __forceinline__ void sequence_td8_load(float (&vals)[TD8_BATCH], cons
 
 __device__ __forceinline__ float sequence_td8_finish(const float (&vals)[TD8_BATCH], const float* __restrict__ steps,
                                                      int64_t T_p, int64_t n, int64_t i, bool active, double eta) {
+  // The exponent window and the max come from the raw bits: |d| >= 0, so the bit patterns of
+  // the entries order like their values — the largest pattern is the max (and flags inf /
+  // NaN), the smallest non-zero pattern (min of bits - 1, a zero wrapping to 0xffffffff) gives
+  // the smallest exponent.  Three integer ops and one fp64 add per entry.
   const int j = threadIdx.x & 7;
-  double mx = 0.0, sm = 0.0;
-  int emin = 255, emax = 0, nonfin = 0;  // exponents of the non-zero finite entries; 1 inf, 2 NaN
+  double sm = 0.0;
+  uint32_t bmax = 0u, bmin1 = 0xffffffffu;
   auto take = [&](float x) {
     const uint32_t bits = __float_as_uint(x) & 0x7fffffffu;
-    const int E = (int)(bits >> 23);
-    if (E == 255) {
-      nonfin |= (bits & 0x7fffffu) ? 2 : 1;
-    } else if (bits) {
-      const int Ee = E ? E : 1;
-      emin = Ee < emin ? Ee : emin;
-      emax = Ee > emax ? Ee : emax;
-    }
-    const double v = (double)__uint_as_float(bits);
-    if (v > mx) mx = v;  // NaN never wins
-    sm = __dadd_rn(sm, v);
+    bmax = max(bmax, bits);
+    bmin1 = min(bmin1, bits - 1u);
+    sm = __dadd_rn(sm, (double)__uint_as_float(bits));
   };
   if (active) {
 #pragma unroll
@@ -222,15 +218,14 @@ __device__ __forceinline__ float sequence_td8_finish(const float (&vals)[TD8_BAT
 #pragma unroll
   for (int o = 1; o < 8; o <<= 1) {
     const double so = __shfl_xor_sync(0xffffffffu, sm, o);
-    const double mo = __shfl_xor_sync(0xffffffffu, mx, o);
-    const int lo = __shfl_xor_sync(0xffffffffu, emin, o);
-    const int hi = __shfl_xor_sync(0xffffffffu, emax, o);
-    nonfin |= __shfl_xor_sync(0xffffffffu, nonfin, o);
+    bmax = max(bmax, (uint32_t)__shfl_xor_sync(0xffffffffu, bmax, o));
+    bmin1 = min(bmin1, (uint32_t)__shfl_xor_sync(0xffffffffu, bmin1, o));
     sm = __dadd_rn(sm, so);  // IEEE addition is commutative: both partners get the same sum
-    if (mo > mx) mx = mo;
-    emin = lo < emin ? lo : emin;
-    emax = hi > emax ? hi : emax;
   }
+  const int nonfin = bmax > 0x7f800000u ? 2 : (bmax == 0x7f800000u ? 1 : 0);  // 2 NaN, 1 inf
+  const int emax = bmax == 0u ? 0 : max((int)(bmax >> 23), 1);              // denormals: exponent 1
+  const int emin = bmin1 == 0xffffffffu ? 255 : max((int)((bmin1 + 1u) >> 23), 1);
+  const double mx = nonfin == 2 ? 0.0 : (double)__uint_as_float(bmax);       // NaN never wins
   const int lgT = T_p <= 1 ? 0 : 64 - __clzll((unsigned long long)(T_p - 1));  // ceil(log2 T_p)
   const bool exact = nonfin || emax == 0 || (emax - emin + 24 + lgT <= 53);
   if (__any_sync(0xffffffffu, active && !exact)) {
