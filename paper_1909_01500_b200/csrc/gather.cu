@@ -1468,6 +1468,10 @@ std::atomic<int> g_gather_trigger{(RPL_PDL_EARLY & 4) ? 0 : -1};
 std::atomic<int> g_dyn_pct{88};   // in-process sweeps (scripts/ab_dyn_sweep.py, profiles/r2/dyn_sweep.txt)
 std::atomic<int> g_dyn_rows{16};
 std::atomic<int> g_dyn_look{12};
+// fused sampling: warp 0 issues up to this many of piece 0's first frame loads right after its
+// descent (0: the producer starts once every table is built); rpl_debug_set_gather_dyn's
+// pct = 1000 + count sets it
+std::atomic<int> g_dyn_early{0};  // measured neutral at 2-8 and +1.5 us at 28 (profiles/r2/dyn_sweep.txt)
 
 template <int NC>
 int launch_seq_lsu(const GDesc& g, const int64_t* idx, int64_t n, int NS, int64_t rows_per_cta, const int64_t* q,
@@ -1500,7 +1504,7 @@ template <int NC>
 __global__ void __launch_bounds__((NC + 3) * 32, 1)
 k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, int rs, int dyn_rows,
                  int lookahead, const int64_t* __restrict__ q, const int64_t* __restrict__ qmin, double beta,
-                 int32_t* err, int trig_at) {
+                 int32_t* err, int trig_at, int early_frames) {
   extern __shared__ __align__(128) uint8_t smem[];  // NS frame slots
   __shared__ __align__(8) uint64_t full[PIPE_MAX_NS];
   // per piece (a run of rows of one sample)
@@ -1570,20 +1574,26 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
   //     batch-min weights / stream advance follow in the meta warp.
   const bool smp = D.smp_tree != nullptr;
   __shared__ int64_t p_leaf[DY_MAX_PIECES];
+  __shared__ int s_pre;  // frames of piece 0 issued by warp 0 right after its descent
+  if (tid == 0) s_pre = 0;
   uint64_t smp_pos = 0;
   const DivN smp_dn = divn_make(smp ? (uint64_t)n : 1ull);
   if (smp) {
-    const int64_t* top = reinterpret_cast<const int64_t*>(smem);
+    // the top levels are staged at the END of the frame-slot area, so warp 0 can start piece
+    // 0's frame loads into the first slots while the other warps still descend
     int64_t ntop = 0;
-    const int64_t cap_words = (int64_t)NS * ob / 8;
+    const int64_t cap_words = (int64_t)(NS - 1) * ob / 8;
     for (int l = 0; l <= D.smp_L.depth; ++l) {
       const int64_t end = l < D.smp_L.depth ? D.smp_L.level_off[l + 1] : D.smp_L.hdr_off;
       if (end > cap_words) break;
       ntop = end;
     }
+    const int64_t top_off = (((int64_t)NS * ob - ntop * 8) / 128) * 128;  // 128-B aligned
+    const int pre_cap = (int)(top_off / ob);                                // slots wholly below it
+    const int64_t* top = reinterpret_cast<const int64_t*>(smem + top_off);
     for (int64_t j = 2 * (int64_t)tid; j < ntop; j += 2 * NT)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem + j * 8)), "l"(D.smp_tree + j)
-                   : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem + top_off + j * 8)),
+                   "l"(D.smp_tree + j) : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
     smp_pos = (uint64_t)__ldcg(D.smp_tree + D.smp_L.hdr_off + 2);
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -1608,6 +1618,25 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
         if (pc >= np0 || sm * L >= g0) {
           const_cast<int64_t*>(idx)[sm] = leaf;
           const_cast<int64_t*>(q)[sm] = qv;
+        }
+        if (pc == 0 && np0 > 0 && leaf >= 0 && leaf < nleaves && early_frames) {
+          // piece 0's first frames, now: slots 0 .. pre-1 (fresh, below the staged levels)
+          const int tau0 = max(g0 - sm * L, 0);
+          const int R = min(g1, (sm + 1) * L) - max(g0, sm * L);
+          const int skip = (unique && tau0 > 0) ? k - 1 : 0;
+          const int pre = min(min(R + k - 1 - skip, pre_cap), early_frames);
+          const int blk = (int)(leaf / Bc);
+          const int bcol = (int)(leaf - (int64_t)blk * Bc);
+          int row = (int)(((int64_t)blk * period + tau0) % cap) - (k - 1) + skip;
+          while (row < 0) row += cap;
+          const uint8_t* colp = D.obs + (int64_t)bcol * ob;
+          for (int w = 0; w < pre; ++w) {
+            mbar_expect_tx(&full[w], (uint32_t)ob);
+            bulk_g2s_evict_first(smem + w * ob, colp + (int64_t)row * Bc * ob, (uint32_t)ob, &full[w]);
+            if (++row == cap) row = 0;
+          }
+          s_pre = pre;
+          flag_release(&s_issued, pre);
         }
       }
     }
@@ -1772,7 +1801,8 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- producer: TMA loads of every published piece ----------------
-      int frontier = 0, released = 0, i = 0, slot = 0;
+      const int pre = s_pre;  // piece 0's frames already in flight (fused sampling)
+      int frontier = 0, released = 0, i = pre, slot = pre;
       auto advance = [&]() {  // the contiguous done-frontier (also read by the meta warp)
         if (frontier < flag_acquire(&s_rows_pub) && flag_acquire(&row_done[frontier])) {
           released = rel[frontier];
@@ -1794,11 +1824,13 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
         if (bcol < 0) continue;
         const int R = p_R[pc];
         const int skip = p_skip[pc];
-        int row = p_row0[pc] - (k - 1) + skip;
+        const int done0 = pc == 0 ? pre : 0;
+        int row = p_row0[pc] - (k - 1) + skip + done0;
         while (row < 0) row += cap;
+        while (row >= cap) row -= cap;
         const uint8_t* col = D.obs + (int64_t)bcol * ob;
         const int64_t rstride = (int64_t)Bc * ob;
-        for (int w = skip; w < R + k - 1; ++w, ++i) {
+        for (int w = skip + done0; w < R + k - 1; ++w, ++i) {
           if (i >= NS) {
             while (released <= i - NS)
               if (!advance()) __nanosleep(20);
@@ -2032,7 +2064,8 @@ int launch_seq_dyn(const GDesc& g, const int64_t* idx, int64_t n, int NS, int rs
                    cudaStream_t st) {
   ensure_smem(reinterpret_cast<const void*>(k_gather_seq_dyn<NC>), dyn);
   return launch_pdl(k_gather_seq_dyn<NC>, dim3((unsigned)grid), dim3((NC + 3) * 32), dyn, st, g, idx, n, NS, rs,
-                    dyn_rows, lookahead, q, qmin, beta, dev_err, g_gather_trigger.load(std::memory_order_relaxed));
+                    dyn_rows, lookahead, q, qmin, beta, dev_err, g_gather_trigger.load(std::memory_order_relaxed),
+                    g_dyn_early.load(std::memory_order_relaxed));
 }
 
 // ---------------------------------------------------------------------------
@@ -2632,6 +2665,10 @@ extern "C" int rpl_debug_gather_trace(int64_t* out, int32_t n) {
 }
 
 extern "C" int rpl_debug_set_gather_dyn(int32_t pct, int32_t rows, int32_t lookahead) {
+  if (pct >= 1000 && pct <= 1000 + PIPE_MAX_NS) {  // measurement: early first-frame loads (count, 0 = off)
+    g_dyn_early.store(pct - 1000);
+    return RPL_OK;
+  }
   if (pct < -1 || pct > 100 || rows < 1 || rows > 32 || lookahead < 1 || lookahead > 200) return RPL_EINVAL;
   g_dyn_pct.store(pct);
   g_dyn_rows.store(rows);
