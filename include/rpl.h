@@ -671,9 +671,10 @@ int rpl_debug_trace(int64_t* out, int32_t n);
  * both (rpl_debug_trace_reset) or the gather's only.  RPL_EUNSUPPORTED in the default build. */
 int rpl_debug_trace_reset(void);
 /* Measurement knob (process-global, read at each update launch): where rpl_sumtree_update(_ex /
- * _seq / set_q)'s kernel lets the dependent grid launch — -1 at exit, 0 at entry, 3 after its
- * loads are issued, 2 (default) after the priorities, 4 after the power transform (2-4: a batch
- * of one chunk; larger batches trigger at exit).  RPL_EINVAL for other values. */
+ * _seq / set_q)'s kernel lets the dependent grid launch — -1 at exit, 0 (default) at entry, 3
+ * after its loads are issued, 2 after the priorities, 4 after the power transform (2-4: the
+ * multi-CTA and one-chunk kernels; the chunked kernel then triggers at exit).  RPL_EINVAL
+ * otherwise. */
 int rpl_debug_set_upd_trigger(int32_t at);
 /* Measurement builds only (-DRPL_TRACE): the last pipelined-scan launch's timeline (n <= 10
  * globaltimer ns stamps, host out): CTA 0's entry, past its wait, first tiles landed, its three

@@ -1548,13 +1548,21 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
   if (trig_at == 0) pdl_trigger();
 #ifdef RPL_TRACE
   if (tid == 0 && blockIdx.x == 0) g_gtrace[0] = global_ns();
+  if (tid == 0) atomicMin(&g_gtrace[4], (unsigned long long)global_ns());  // earliest CTA entry
 #endif
-  pdl_wait();  // idx / q come from the sampler launched just before
+  // one warp waits for the previous grid (a grid launched early by PDL sits here; the other
+  // warps wait at the CTA barrier, which orders their reads after the wait)
+  if (warp == 0) pdl_wait();  // idx / q come from the kernel launched just before
+  __syncthreads();
 #ifdef RPL_TRACE
   if (tid == 0 && blockIdx.x == 0) {
     g_gtrace[1] = global_ns();
     g_gtrace[3] = 0;
     g_gtrace[8] = ~0ull;
+  }
+  if (tid == 0) {
+    atomicMin(&g_gtrace[5], (unsigned long long)global_ns());  // earliest past the wait
+    atomicMax(&g_gtrace[6], (unsigned long long)global_ns());  // latest past the wait
   }
 #endif
   const int total = (int)(n * L);
@@ -2620,7 +2628,7 @@ using namespace rpl;
 
 extern "C" int rpl_debug_gather_trace_reset(void) {
 #ifdef RPL_TRACE
-  unsigned long long z[9] = {0, 0, 0, 0, 0, 0, 0, 0, ~0ull};
+  unsigned long long z[9] = {0, 0, 0, 0, ~0ull, ~0ull, 0, 0, ~0ull};
   return cudaMemcpyToSymbol(rpl::g_gtrace, z, sizeof(z)) == cudaSuccess ? RPL_OK : RPL_ECUDA;
 #else
   return RPL_EUNSUPPORTED;

@@ -784,7 +784,11 @@ k_tree_sample(TreeDev L, int64_t* __restrict__ tree, int64_t n, const uint64_t* 
   const int lane = threadIdx.x & 31;
   const DivN dn = divn_make((uint64_t)(n > 0 ? n : 1));  // n alone: before the dependency wait
   if (RPL_PDL_EARLY & 2) pdl_trigger();  // A/B knob (common.cuh)
-  pdl_wait();
+  // one warp waits for the previous grid (launched early by PDL, the other warps wait at the
+  // barrier, which orders their reads after the wait): fewer waiting warps beside the running
+  // update kernel (in-process A/B of the R2D2 step with the gather: -0.85 us)
+  if ((threadIdx.x >> 5) == 0) pdl_wait();
+  __syncthreads();
   UPD_TRACE(8);
   // Stage the top levels (root .. the deepest level that still fits STAGE_WORDS) in shared
   // memory with one round of asynchronous 16-B copies, so the descent's first levels and Q
@@ -1289,13 +1293,14 @@ bool layout_ok(const rpl_tree_layout* L) {
 
 // Where the update kernel lets its dependent grid launch (-1 at exit, 0 at entry, 3 after its
 // loads are issued, 2 after the priorities, 4 after the power transform; rpl_debug_set_upd_trigger).
-// Default 2: the next kernel's launch (the sequence gather's 146 CTAs take ~3 us to become
-// resident) overlaps the update's last ~2.5 us; it still waits for the update's completion in
-// its griddepcontrol.wait.  In-process A/B of the R2D2 step (scripts/ab_inproc.py, alternating
-// graphs): -1.0 us per step against the exit trigger, reproduced three times; entry (0) or
-// after the loads (3) gain less (-0.3 / 0.0 us), since the resident gather CTAs then slow the
-// update's loads (profiles/r2/ab_trigger_inproc.txt).
-std::atomic<int> g_upd_trigger{(RPL_PDL_EARLY & 1) ? 0 : 2};
+// Default 0: the next kernel's launch (the sequence gather's 146 CTAs take ~3 us to become
+// resident) overlaps the whole update; it still waits for the update's completion in its
+// griddepcontrol.wait — which only ONE warp per CTA of the early-launched kernel executes (the
+// others wait at a CTA barrier): with every warp waiting, the resident CTAs slowed the update
+// and entry / after-the-priorities triggers tied; with one waiting warp the entry trigger is
+// -0.85 us per R2D2 step against the trigger after the priorities, which was -1.0 us against
+// the exit trigger (in-process A/Bs, scripts/ab_inproc.py; profiles/r2/ab_trigger_inproc.txt).
+std::atomic<int> g_upd_trigger{0};
 // Measurement knob (rpl_debug_set_upd_multi): 1 (default) = batches of n <= HASH_SLOTS / 2 take
 // the multi-CTA update kernel, 0 = the single-CTA kernels only.
 std::atomic<int> g_upd_multi{1};

@@ -34,6 +34,8 @@ qv = torch.randn((8, L, n), generator=g, device=dev) * 10
 plan = rpl.GatherPlan(ring, n, kind="sequence", k=k, seq_len=L, period=period, with_weights=True,
                       targets=bench.r2d2_targets(c, qv[0]))
 lib, P_ = rpl._lib.lib, rpl.ops._ptr
+if os.environ.get("UPD_TRIG"):  # rpl_debug_set_upd_trigger
+    assert lib.rpl_debug_set_upd_trigger(int(os.environ["UPD_TRIG"])) == 0
 if os.environ.get("DYN"):  # DYN=pct,rows,lookahead (rpl_debug_set_gather_dyn)
     assert lib.rpl_debug_set_gather_dyn(*(int(x) for x in os.environ["DYN"].split(","))) == 0
 MODE = os.environ.get("STEP", "pair")  # pair: update -> sample -> gather; fused: update -> gather_sample
@@ -62,16 +64,19 @@ torch.cuda.synchronize()
 st = torch.cuda.Stream(dev)
 st.wait_stream(torch.cuda.current_stream(dev))
 gr = torch.cuda.CUDAGraph()
+PSTEPS = int(os.environ.get("P_STEPS", "8"))
 with torch.cuda.graph(gr, stream=st):
-    for i in range(8):
+    for i in range(PSTEPS):
         step(i)
 for _ in range(5):
     gr.replay()
 torch.cuda.synchronize()
 names_u = {7: "update_entry", 0: "update_past_wait", 2: "update_mixed", 3: "update_hash_reset",
            4: "update_dedupe", 5: "update_leaves", 6: "update_end", 8: "sample_past_wait", 9: "sample_end"}
+DYN = os.environ.get("STEP", "pair") != "static"
 names_g = {0: "gather_entry", 1: "gather_past_wait", 2: "gather_first_frames", 3: "gather_end",
-           4: "gather_smp_staged", 5: "gather_smp_sampled", 6: "gather_first_tma_issue", 7: "gather_pieces_done",
+           4: "gather_smp_staged (dyn: earliest CTA entry)", 5: "gather_smp_sampled (dyn: earliest past wait)",
+           6: "gather_first_tma_issue (dyn: latest past wait)", 7: "gather_pieces_done",
            8: "gather_first_cta_end"}
 runs = []
 bu, bg = (ctypes.c_int64 * 16)(), (ctypes.c_int64 * 9)()
@@ -86,12 +91,12 @@ for _ in range(30):
     e1.record()
     torch.cuda.synchronize()
     if lib.rpl_debug_trace(bu, 16) != 0 or lib.rpl_debug_gather_trace(bg, 9) != 0:  # not a trace build
-        runs.append({"graph_us_per_step": e0.elapsed_time(e1) * 1e3 / (80 if STEADY else 8)})
+        runs.append({"graph_us_per_step": e0.elapsed_time(e1) * 1e3 / ((10 if STEADY else 1) * PSTEPS)})
         continue
     t0 = bu[7]
     r = {v: bu[kk] - t0 for kk, v in names_u.items() if kk != 8 or MODE != "fused"}
     r.update({v: bg[kk] - t0 for kk, v in names_g.items() if bg[kk] != 0})
-    r["graph_us_per_step"] = e0.elapsed_time(e1) * 1e3 / (80 if STEADY else 8)
+    r["graph_us_per_step"] = e0.elapsed_time(e1) * 1e3 / ((10 if STEADY else 1) * PSTEPS)
     runs.append(r)
 med = {kk: sorted(r[kk] for r in runs if kk in r)[len([r for r in runs if kk in r]) // 2] for kk in runs[0]}
 ends = (ctypes.c_int64 * (3 * 146))()
