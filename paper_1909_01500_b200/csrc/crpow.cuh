@@ -92,10 +92,94 @@ __device__ __noinline__ dd dd_log(double x) {
   return dd_add(dd{y0, 0.0}, t);
 }
 
+// Fast p^alpha for p > 0 finite: exp(alpha * ln p) in plain fp64 — ln m = 2 atanh(s),
+// s = (m-1)/(m+1) with m in [sqrt(1/2), sqrt(2)) (|s| <= 0.1716, odd series to s^21), ln p =
+// e ln2 + ln m with ln2 split hi (32 bits, so e ln2_hi is exact) / lo; exp(t) = 2^k exp(r),
+// |r| <= ln2 / 2, Taylor to r^13.  Every step is a few fp64 roundings, so the relative error
+// is below (|t| + 3) * 3e-16 (ln m to ~3 ulp absolute 1.2e-16, t = alpha ln p to |t| * 2^-52,
+// exp(r) to ~3 ulp); *mrel returns a bound 20-50x larger, (|t| + 8) * 2^-47, for the Ziv
+// test.  Returns -1 outside t in [-103, 88] (fp32 underflow / overflow region: the caller
+// uses the libm path there).  ~45 dependent fp64 operations instead of libm pow's double-
+// double log / exp (the update kernel's power stage: ~1 us).
+__device__ __forceinline__ double fast_pow(double p, double alpha, double* mrel) {
+  long long bits = __double_as_longlong(p);
+  int ex = (int)((bits >> 52) & 0x7ff);
+  int e = 0;
+  if (ex == 0) {  // subnormal: scale by 2^54
+    p *= 18014398509481984.0;
+    bits = __double_as_longlong(p);
+    ex = (int)((bits >> 52) & 0x7ff);
+    e = -54;
+  }
+  e += ex - 1023;
+  double m = __longlong_as_double((bits & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);  // [1, 2)
+  if (m > 1.4142135623730951) {
+    m *= 0.5;
+    e += 1;
+  }
+  const double f = m - 1.0;  // exact (m in [0.70, 1.42))
+  double rd;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(2.0 + f));
+  const double den = 2.0 + f;
+  double er = fma(-den, rd, 1.0);
+  rd = fma(rd, er, rd);
+  er = fma(-den, rd, 1.0);
+  rd = fma(rd, er, rd);
+  const double s = f * rd;
+  const double z = s * s;
+  double P = 1.0 / 21.0;
+  P = fma(P, z, 1.0 / 19.0);
+  P = fma(P, z, 1.0 / 17.0);
+  P = fma(P, z, 1.0 / 15.0);
+  P = fma(P, z, 1.0 / 13.0);
+  P = fma(P, z, 1.0 / 11.0);
+  P = fma(P, z, 1.0 / 9.0);
+  P = fma(P, z, 1.0 / 7.0);
+  P = fma(P, z, 1.0 / 5.0);
+  P = fma(P, z, 1.0 / 3.0);
+  P = fma(P, z, 1.0);
+  const double lnm = 2.0 * s * P;
+  constexpr double LN2_HI = 6.93147180369123816490e-01;  // 0x3fe62e42fee00000: 32 significant bits
+  constexpr double LN2_LO = 1.90821492927058770002e-10;
+  const double lp = fma((double)e, LN2_HI, fma((double)e, LN2_LO, lnm));
+  const double t = alpha * lp;
+  *mrel = (fabs(t) + 8.0) * 7.105427357601002e-15;  // 2^-47
+  if (!(t >= -103.0 && t <= 88.0)) return -1.0;
+  const double k = rint(t * 1.4426950408889634);
+  double r = fma(-k, LN2_HI, t);
+  r = fma(-k, LN2_LO, r);
+  double q = 1.0 / 6227020800.0;  // 1/13!
+  q = fma(q, r, 1.0 / 479001600.0);
+  q = fma(q, r, 1.0 / 39916800.0);
+  q = fma(q, r, 1.0 / 3628800.0);
+  q = fma(q, r, 1.0 / 362880.0);
+  q = fma(q, r, 1.0 / 40320.0);
+  q = fma(q, r, 1.0 / 5040.0);
+  q = fma(q, r, 1.0 / 720.0);
+  q = fma(q, r, 1.0 / 120.0);
+  q = fma(q, r, 1.0 / 24.0);
+  q = fma(q, r, 1.0 / 6.0);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = fma(q, r, 1.0);
+  return q * __longlong_as_double((long long)((int)k + 1023) << 52);
+}
+
 // v = RN32(p^alpha) for p > 0 (finite), alpha >= 0.  Sets *slow when the fallback ran.
 __device__ __forceinline__ float cr_powf(double p, double alpha, bool force_slow, bool* slow) {
   if (alpha == 0.0) return 1.0f;
   if (alpha == 1.0) return __double2float_rn(p);
+  if (!force_slow) {  // fast path: accepted when it lies beyond its error bound from the fp32 midpoint
+    double mrel;
+    const double yf = fast_pow(p, alpha, &mrel);
+    if (yf > 0.0) {
+      const float f = __double2float_rn(yf);
+      const double fd = (double)f;
+      const float nb = (yf >= fd) ? nextafterf(f, __int_as_float(0x7f800000)) : nextafterf(f, 0.0f);
+      const double mid = 0.5 * (fd + (double)nb);
+      if (fabs(yf - mid) > mrel * yf) return f;
+    }
+  }
   const double y = pow(p, alpha);
   if (!(y < 3.4028235677973366e38)) return __int_as_float(0x7f800000);  // overflow -> +inf
   const float f = __double2float_rn(y);

@@ -618,7 +618,8 @@ k_tree_update_multi(TreeDev L, int64_t* __restrict__ tree, const int64_t* __rest
   }
   if (trig_at == 0) pdl_trigger();
   UPD_TRACE(7);
-  pdl_wait();
+  if ((threadIdx.x >> 5) == 0) pdl_wait();  // one waiting warp (see g_upd_trigger)
+  __syncthreads();
   UPD_TRACE(0);
   int64_t* leaves = tree + L.level_off[L.depth];
   int64_t* hdr = tree + L.hdr_off;

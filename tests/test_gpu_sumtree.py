@@ -830,3 +830,23 @@ def test_min_tree_sharded_exchanges(rpl):
         got += (H(idx)[:m] + r * n_local).tolist()
         assert int(H(bm)[0]) == gmin and int(H(trees[r].header)[6]) == gmin
     assert got == ref_idx
+
+
+@pytest.mark.parametrize("alpha", [0.6, 0.9, 0.5, 0.123, 0.75, 2.0, 3.5, 0.999])
+def test_fast_power_path_equals_correctly_rounded(rpl, alpha):
+    # R7: the fast exp(alpha ln p) evaluation (crpow.cuh fast_pow, Ziv margin (|t|+8) 2^-47) must
+    # give the correctly rounded fp32 power on every input: 1.5M values spanning |delta| from
+    # 1e-9 to 1e9 (and the eps_p floor, p near 1, exact powers of two) against the forced
+    # double-double path, bit for bit
+    g = rng(int(alpha * 1000) + 7)
+    parts = [np.exp(g.uniform(np.log(1e-9), np.log(1e9), 1_000_000)),
+             g.uniform(0.0, 4.0, 300_000),
+             1.0 + g.normal(0, 1e-6, 100_000),
+             np.ldexp(1.0, g.integers(-30, 30, 50_000)),
+             np.zeros(50_000)]
+    td = np.abs(np.concatenate(parts)).astype(np.float32)
+    v_fast, _ = rpl.debug_priority_values(T_(td), alpha, 1e-3, force_slow=False)
+    v_slow, _ = rpl.debug_priority_values(T_(td), alpha, 1e-3, force_slow=True)
+    a, b = H(v_fast), H(v_slow)
+    bad = np.nonzero(a.view(np.uint32) != b.view(np.uint32))[0]
+    assert bad.size == 0, (alpha, td[bad[:5]], a[bad[:5]], b[bad[:5]])
