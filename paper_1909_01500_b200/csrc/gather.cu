@@ -2872,18 +2872,23 @@ int gather_run(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q
         if (desc->work && dpct >= 0 && !desc->col_offset && !desc->n_active && !desc->peer_boards &&
             !desc->done_flag && seq_variant == 0 && desc->out_mode == RPL_OUT_STACKED &&
             n <= (1 << 30) / desc->seq_len) {
-          int64_t rs = total * dpct / 100 / grid;
-          if (rs > DY_MAX_ROWS - 4 * drows) rs = DY_MAX_ROWS - 4 * drows;
-          if (rs < 0) rs = 0;
-          g.use_tma = 1;
           // two SMs stay free for kernels running beside the gather (the pipelined step's
           // update + sampler on a second stream), as with the static split's 146 CTAs
-          grid = grid > 8 ? grid - 2 : grid;
-          rs = total * dpct / 100 / grid;
+          const int64_t gd = grid > 8 ? grid - 2 : grid;
+          int64_t rs = total * dpct / 100 / gd;
           if (rs > DY_MAX_ROWS - 4 * drows) rs = DY_MAX_ROWS - 4 * drows;
-          return launch_seq_dyn<RPL_SEQ_CONSUMERS>(g, idx, n, NS, (int)rs, drows,
-                                                   g_dyn_look.load(std::memory_order_relaxed), q, qmin, beta,
-                                                   dev_err, dyn, grid, st);
+          // capacity: a CTA holds at most DY_MAX_ROWS rows and DY_MAX_PIECES pieces (its static
+          // pieces, then at most two per grab of >= 2 rows), so every row is taken only if the
+          // static pieces leave half the piece table and the dynamic rows fit what the grid can
+          // still take; otherwise the static split (any size)
+          const int64_t ldyn = total - gd * rs;
+          if (rs / desc->seq_len + 2 <= DY_MAX_PIECES / 2 && ldyn <= gd * (DY_MAX_PIECES / 2 - 2) &&
+              total <= gd * (DY_MAX_ROWS - 2 * drows)) {
+            g.use_tma = 1;
+            return launch_seq_dyn<RPL_SEQ_CONSUMERS>(g, idx, n, NS, (int)rs, drows,
+                                                     g_dyn_look.load(std::memory_order_relaxed), q, qmin, beta,
+                                                     dev_err, dyn, gd, st);
+          }
         }
         int64_t rows_per_cta = (total + grid - 1) / grid;
         if (rows_per_cta > PL_MAX_ROWS) rows_per_cta = PL_MAX_ROWS;

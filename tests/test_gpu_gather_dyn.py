@@ -41,7 +41,11 @@ def H(t):
 
 @pytest.mark.parametrize("L,k,n_s,out_mode,pad_mode", [(125, 4, 64, 0, 0), (125, 4, 64, 1, 0), (47, 2, 190, 0, 1),
                                                        (5, 4, 33, 0, 0), (1, 4, 7, 1, 1), (40, 1, 50, 0, 0),
-                                                       (120, 8, 20, 0, 1), (2, 4, 300, 1, 0)])
+                                                       (120, 8, 20, 0, 1), (2, 4, 300, 1, 0),
+                                                       # beyond the dynamic kernel's capacity (static split):
+                                                       (125, 4, 320, 0, 0), (1, 4, 20000, 0, 0),
+                                                       # many pieces per CTA at the edge of the piece table:
+                                                       (2, 4, 2400, 0, 1), (3, 4, 1900, 0, 0)])
 def test_dynamic_tail_vs_oracle(rpl, schedule, L, k, n_s, out_mode, pad_mode):
     import torch
     period = 40
