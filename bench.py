@@ -254,6 +254,12 @@ def run_rpl(args):
     td0 = np.abs(g.normal(size=valid.numel())).astype(np.float32)
     tree.update(valid, torch.from_numpy(td0).to(dev), c["alpha"], c["eps_p"])
     P = max(2, args.graph_steps + (args.graph_steps % 2))  # steps per CUDA graph (even: idx buffers alternate)
+    if args.steps % P:
+        # exactly K steps without a short remainder graph (its replay carries the graph launch
+        # over fewer steps): the even divisor of K in [4, 16] closest to the requested size
+        divs = [d for d in range(4, 17, 2) if args.steps % d == 0]
+        if divs:
+            P = min(divs, key=lambda d: (abs(d - P), -d))
     # per-step |delta| of the previous batch's train rows, [P][train, n_glob] (R2D2 learner output)
     td_pool = torch.from_numpy(np.abs(g.normal(size=(P, c["train"], n * max(1, world)))).astype(np.float32)).to(dev)
     n_glob = n * world
@@ -578,7 +584,7 @@ def run_rpl(args):
         "data": "synthetic (seeded; uniform-random 84x84 u8 frames, R2D2 reward/episode recipe, DESIGN.md)",
         "config": dict(r2d2_config(c, world, args.mode),
                        timing=(f"cuda graph of {P} steps replayed {reps}x" + (f" + a graph of {rem} steps" if rem else "")
-                               + " (both warmed by 3 replays first); exactly K steps timed" if use_graph
+                               + (" (both warmed" if rem else " (warmed") + " by 3 replays first); exactly K steps timed" if use_graph
                                else "eager launches"),
                        tree=("update+sample fused (rpl_sumtree_update_sample)" if world == 1 and args.tree_fused
                              else "update_seq, then sampling inside the gather (rpl_gather_sample)"
