@@ -79,6 +79,10 @@ def parse():
                          "is update_seq -> gather (default: same-box A/B 68.1 vs 69.45 us per step with the "
                          "top levels staged in shared memory, profiles/r2/ab_fused_sample_staged.txt); 0: a "
                          "separate rpl_sumtree_sample_stream launch")
+    ap.add_argument("--fused-update", type=int, default=0, choices=[0, 1],
+                    help="1 GPU with --fused-sample 1: the priority update runs inside the gather too "
+                         "(rpl_gather_update_sample: ONE launch per step; in-process A/B 64.8 vs 62.9 us, "
+                         "profiles/r2/ab_one_launch.txt); 0 (default): the 8-CTA update_seq, then the gather")
     ap.add_argument("--mode", default="L", choices=["L", "C"],
                     help="N > 1 replay mode (SURVEY §8e): L = owner computes, each rank feeds its own learner; "
                          "C = every owner's gather writes into the rank-0 learner's batch over NVLink (CUDA IPC)")
@@ -345,6 +349,25 @@ def run_rpl(args):
             td_i, q_i, cur, prev = io
         # (a5-a7) new priorities for the previous batch (entries < 0 — not owned — are skipped, R22)
         # (NEXT-1 fused) sequence priority = eta max + (1 - eta) mean of the 80 per-step |delta| (R26)
+        one_launch = world == 1 and args.fused_sample and args.fused_update and not args.tree_fused
+        if one_launch and not skip_gather:
+            # (a5-a8 + a9 + a11 + a2/a4) the whole step in one launch: every gather CTA applies
+            # the update to its staged copy of the tree and samples it; CTA 0 writes the update
+            if gather_events is not None:  # the one kernel is the step: events around it
+                gather_events[0].record()
+            if w_out is not None:
+                plan.desc.o_w = w_out.data_ptr()
+            if y_out is not None:
+                plan.desc.o_tgt = y_out.data_ptr()
+            plan.run_update_sample(tree, prev, td_i, seed, cur, q_buf, eta=c["eta"], alpha=c["alpha"],
+                                   eps_p=c["eps_p"], beta=c["beta"], err=err, stream=s, q_tgt=q_i)
+            if w_out is not None:
+                plan.desc.o_w = w.data_ptr()
+            if y_out is not None:
+                plan.desc.o_tgt = y.data_ptr()
+            if gather_events is not None:
+                gather_events[1].record()
+            return
         if world == 1 and args.tree_fused:
             # (a5-a8) update + stratified draws in one launch (grid barrier between them);
             # the batch-min normaliser and IS weights (a9) are fused into the gather

@@ -527,6 +527,24 @@ int rpl_gather(const rpl_gather_desc* desc /* host */, const int64_t* idx, const
 int rpl_gather_sample(const rpl_gather_desc* desc, const rpl_tree_layout* L, int64_t* tree, uint64_t seed,
                       int64_t* idx_out, int64_t* q_out, double beta, int64_t n, int32_t* dev_err, void* stream);
 
+/* The whole R2D2 replay step in ONE launch (a5-a7 + a8 + a9 + a11, R26; P:123 fn): exactly
+ * rpl_sumtree_update_seq(L, tree, upd_idx, upd_td, T_p, n_upd, eta, alpha, eps_p, flags, ...)
+ * followed by rpl_gather_sample(desc, L, tree, seed, idx_out, q_out, beta, n, ...) — same tree
+ * (leaves, nodes, header, attached min-tree), same draws, same outputs bit for bit.  Every CTA
+ * of the dynamic-tail gather computes the batch's sequence priorities, winners (last
+ * position of each leaf) and deltas, applies them to its staged copy of the internal
+ * levels and overlays the winners' new q on the leaf level it reads, so it samples the
+ * updated tree at once; CTA 0 writes the update to the tree after every CTA has finished
+ * reading it.  Requires desc->work, stacked output, 1 <= n_upd <= 128 and every internal tree
+ * level within the frame-slot area; otherwise (or for n_upd == 0) the call enqueues the two
+ * launches.  upd_idx: device int64 [n_upd] (< 0: padding, skipped; >= n_leaves:
+ * RPL_DERR_IDX); upd_td: device f32 [T_p, n_upd] per-step |delta|; flags: RPL_UPD_LIVE_ONLY.
+ * Argument errors as the two calls (RPL_EINVAL). */
+int rpl_gather_update_sample(const rpl_gather_desc* desc, const rpl_tree_layout* L, int64_t* tree,
+                             const int64_t* upd_idx, const float* upd_td, int64_t T_p, int64_t n_upd, double eta,
+                             double alpha, double eps_p, int32_t flags, uint64_t seed, int64_t* idx_out,
+                             int64_t* q_out, double beta, int64_t n, int32_t* dev_err, void* stream);
+
 /* Stream-ordered wait for n completion flags (device int64 [n], e.g. the learner's flag array
  * that n owners' gathers signal through rpl_gather_desc.done_flag): returns at once, the
  * enqueued one-warp kernel spins with ld.acquire.sys until flags[i] >= *expect for every i

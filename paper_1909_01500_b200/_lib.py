@@ -115,6 +115,9 @@ _SIGS = {
     "rpl_ring_append": ([C.POINTER(GatherDesc), P, P, P, P, P, I64, P], C.c_int),
     "rpl_wait_flags": ([P, I32, P, P, P], C.c_int),
     "rpl_gather_sample": ([C.POINTER(GatherDesc), C.POINTER(TreeLayout), P, U64, P, P, D, I64, P, P], C.c_int),
+    "rpl_gather_update_sample": ([C.POINTER(GatherDesc), C.POINTER(TreeLayout), P, P, P, I64, I64, D, D, D, I32, U64,
+                                  P, P, D, I64, P, P],
+                                 C.c_int),
     "rpl_stack_frames": ([P, P, I64, I64, I32, I64, I32, P, P, P], C.c_int),
     "rpl_returns_nstep_dq": ([P, P, I64, I64, I32, D, P, P, I32, I32, D, P, P, P, P], C.c_int),
     "rpl_c51_project": ([P, P, P, P, I64, I32, I32, D, D, D, P, P, P], C.c_int),

@@ -57,7 +57,7 @@ __device__ __forceinline__ dd dd_ldexp(dd a, int e) { return {ldexp(a.hi, e), ld
 #define RPL_LN2_LO 2.31904681384629955842e-17
 
 // exp of a double-double argument, |z| < 700, relative error ~1e-30.
-__device__ __noinline__ dd dd_exp(dd z) {
+static __device__ __noinline__ dd dd_exp(dd z) {
   const double k = rint(z.hi * 1.44269504088896338700);  // 1/ln2
   // r = z - k ln2 (k is an integer < 2^11: k*LN2_HI is exact up to the fma remainder)
   dd kl = two_prod(k, RPL_LN2_HI);
@@ -84,7 +84,7 @@ __device__ __noinline__ dd dd_exp(dd z) {
 
 // natural log of a positive double as double-double: one Newton step
 // y1 = y0 + x e^{-y0} - 1 from the libm value y0 (error squares: ~1e-32).
-__device__ __noinline__ dd dd_log(double x) {
+static __device__ __noinline__ dd dd_log(double x) {
   const double y0 = log(x);
   dd e = dd_exp(dd{-y0, 0.0});
   dd xe = dd_mul_d(e, x);

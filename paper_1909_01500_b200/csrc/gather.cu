@@ -21,9 +21,12 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "crpow.cuh"
 
 namespace rpl {
 namespace {
+
+#include "seqprio.cuh"  // sequence_td8 (R26): the fused update's sequence priorities
 
 #ifndef RPL_G_THREADS  // one-CTA-per-sample gathers (build-flag A/B knob)
 #define RPL_G_THREADS 128
@@ -212,6 +215,11 @@ struct GDesc {
   TreeDev smp_L;
   uint64_t smp_seed;
   int64_t* work;        // dynamic-tail unit counter + ticket (rpl_gather_desc.work; NULL: static split)
+  // fused priority update before the sampling (rpl_gather_update_sample; NULL: none)
+  const int64_t* upd_idx;
+  const float* upd_td;
+  int upd_n, upd_T, upd_live, upd_pad;
+  double upd_eta, upd_alpha, upd_eps;
 };
 
 // Output column offset (rpl_gather_desc.col_offset); read after pdl_wait.
@@ -1500,6 +1508,69 @@ int launch_seq_lsu(const GDesc& g, const int64_t* idx, int64_t n, int NS, int64_
 constexpr int DY_MAX_ROWS = 256;
 constexpr int DY_MAX_PIECES = 96;
 
+// Fused update (rpl_gather_update_sample): the new q of the batch's winning leaves, looked up
+// by leaf in a per-CTA open-addressing table.
+constexpr int UF_MAX = 128;   // update entries per call
+constexpr int UF_SLOTS = 256;  // table slots (>= 2 UF_MAX, a power of two)
+__device__ __forceinline__ int uf_slot(int64_t leaf) {
+  return (int)(((unsigned long long)leaf * 0x9E3779B97F4A7C15ull) >> 56) & (UF_SLOTS - 1);
+}
+// descend() with every internal level staged in shared memory (already carrying the update's
+// deltas) and the leaf level read from global memory with the update's new values overlaid
+__device__ __forceinline__ int64_t descend_overlay(const TreeDev& L, const int64_t* __restrict__ tree, int64_t prefix,
+                                                   int64_t* q_out, int32_t* errbits, const int64_t* top,
+                                                   const unsigned long long* ukey, const long long* uval) {
+  const int lane = threadIdx.x & 31;
+  int64_t node = 0;
+  int64_t c = 0;
+  for (int l = 0; l < L.depth; ++l) {
+    const int64_t base = L.level_off[l + 1] + (node << L.log2w);
+    if (lane < L.fanout) {
+      if (l + 1 < L.depth) {
+        c = top[base + lane];
+      } else {
+        const int64_t leaf = (node << L.log2w) + lane;
+        c = tree[base + lane];
+        int sl = uf_slot(leaf);
+        while (ukey[sl] != ~0ull) {
+          if (ukey[sl] == (unsigned long long)leaf) {
+            c = uval[sl];
+            break;
+          }
+          sl = (sl + 1) & (UF_SLOTS - 1);
+        }
+      }
+    } else {
+      c = 0;
+    }
+    int64_t incl = c;
+#pragma unroll
+    for (int dlt = 1; dlt < 32; dlt <<= 1) {
+      const int64_t o = shfl_up64(incl, dlt);
+      if (lane >= dlt) incl += o;
+    }
+    unsigned bal = __ballot_sync(0xffffffffu, prefix < incl);
+    int f;
+    if (bal == 0) {
+      *errbits |= RPL_DERR_TREE;
+      const unsigned nz = __ballot_sync(0xffffffffu, c > 0);
+      f = nz ? 31 - __clz(nz) : 0;
+      const int64_t inc_last = shfl64(incl, f);
+      prefix = nz ? inc_last - 1 : 0;
+    } else {
+      f = __ffs(bal) - 1;
+    }
+    const int64_t inc_f = shfl64(incl, f);
+    const int64_t c_f = shfl64(c, f);
+    prefix -= inc_f - c_f;
+    if (prefix < 0) prefix = 0;
+    node = (node << L.log2w) + f;
+    c = c_f;
+  }
+  *q_out = c;
+  return node;
+}
+
 template <int NC>
 __global__ void __launch_bounds__((NC + 3) * 32, 1)
 k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, int rs, int dyn_rows,
@@ -1582,6 +1653,12 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
   //     batch-min weights / stream advance follow in the meta warp.
   const bool smp = D.smp_tree != nullptr;
   __shared__ int64_t p_leaf[DY_MAX_PIECES];
+  __shared__ int64_t u_leaf[UF_MAX], u_old[UF_MAX], u_q[UF_MAX];
+  __shared__ float u_td[UF_MAX];
+  __shared__ int8_t u_win[UF_MAX];
+  __shared__ unsigned long long uf_key[UF_SLOTS];
+  __shared__ long long uf_val[UF_SLOTS];
+  __shared__ int uf_pos[UF_SLOTS];
   __shared__ int s_pre;  // frames of piece 0 issued by warp 0 right after its descent
   if (tid == 0) s_pre = 0;
   uint64_t smp_pos = 0;
@@ -1604,8 +1681,101 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
                    "l"(D.smp_tree + j) : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
     smp_pos = (uint64_t)__ldcg(D.smp_tree + D.smp_L.hdr_off + 2);
+    // (U) fused priority update (rpl_gather_update_sample, a5-a7 + R26): every CTA computes the
+    //     batch's sequence priorities, winners and deltas itself, applies the deltas to its
+    //     staged copy of the internal levels and overlays the winners' new q on the leaf level
+    //     it reads — so it samples the UPDATED tree without waiting for anyone; CTA 0 writes
+    //     the update to global memory once every CTA has finished reading the old tree
+    //     (work[3] counts the readers).  Same tree and draws as rpl_sumtree_update_seq
+    //     followed by rpl_gather_sample.
+    const bool upd = D.upd_td != nullptr;
+    const int nu = upd ? D.upd_n : 0;
+    if (upd) {
+      for (int s2 = tid; s2 < UF_SLOTS; s2 += NT) {
+        uf_key[s2] = ~0ull;
+        uf_pos[s2] = -1;
+      }
+      if (tid < nu) {
+        int64_t lf = D.upd_idx[tid];
+        if (lf < 0 || lf >= nleaves) lf = -1;
+        u_leaf[tid] = lf;
+        u_old[tid] = lf >= 0 ? __ldcg(D.smp_tree + D.smp_L.level_off[D.smp_L.depth] + lf) : 0;
+      }
+      // sequence priorities: eight lanes per sequence, NT / 8 sequences per pass; the next
+      // pass's loads are in flight while this pass reduces
+      float va[TD8_BATCH], vb[TD8_BATCH];
+      sequence_td8_load(va, D.upd_td, D.upd_T, nu, tid >> 3, (tid >> 3) < nu);
+      for (int p0 = 0; p0 < nu; p0 += NT / 8) {
+        const int jj = p0 + (tid >> 3), jn = jj + NT / 8;
+        if (p0 + NT / 8 < nu) sequence_td8_load(vb, D.upd_td, D.upd_T, nu, jn, jn < nu);
+        const float v = sequence_td8_finish(va, D.upd_td, D.upd_T, nu, jj, jj < nu, D.upd_eta);
+        if ((tid & 7) == 0 && jj < nu) u_td[jj] = v;
+#pragma unroll
+        for (int u2 = 0; u2 < TD8_BATCH; ++u2) va[u2] = vb[u2];
+      }
+    }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+#ifdef RPL_TRACE
+    if (tid == 0 && blockIdx.x == 0) g_gtrace[2] = global_ns();  // staged (+ the update's priorities)
+#endif
+    if (upd) {
+      // winners (the batch's last position of each leaf: a hash of the indices keeps the
+      // largest position), new q, deltas
+      int64_t* topw = reinterpret_cast<int64_t*>(smem + top_off);
+      int usl = -1;
+      if (tid < nu && u_leaf[tid] >= 0) {
+        const int64_t lf = u_leaf[tid];
+        usl = uf_slot(lf);
+        while (true) {
+          const unsigned long long prev = atomicCAS(&uf_key[usl], ~0ull, (unsigned long long)lf);
+          if (prev == ~0ull || prev == (unsigned long long)lf) break;
+          usl = (usl + 1) & (UF_SLOTS - 1);
+        }
+        atomicMax(&uf_pos[usl], tid);
+      }
+      __syncthreads();
+      int64_t root_delta = 0;
+      if (tid < nu) {
+        const int64_t lf = u_leaf[tid];
+        bool win = lf >= 0 && uf_pos[usl] == tid;
+        int64_t q = 0;
+        if (lf >= 0) {
+          const double p = (double)fabsf(u_td[tid]) + D.upd_eps;
+          float v;
+          if (!isfinite(p)) {
+            v = __int_as_float(0x7f800000);
+          } else {
+            bool slow = false;
+            v = cr_powf(p, D.upd_alpha, false, &slow);
+          }
+          bool sat = false;
+          q = quantise_q(v, D.smp_L.frac_bits, D.smp_L.q_cap, &sat);
+          if (D.upd_live && u_old[tid] == 0) win = false;  // R30: a zero leaf is left alone
+        }
+        u_win[tid] = win ? 1 : 0;
+        u_q[tid] = q;
+        // the leaf's value after the update, written once per leaf by its last batch position
+        if (lf >= 0 && uf_pos[usl] == tid) uf_val[usl] = (long long)(win ? q : u_old[tid]);
+        if (win) {
+          const int64_t delta = q - u_old[tid];
+          root_delta = delta;
+          if (delta != 0) {  // levels below the root: few entries per node
+            int64_t node = lf;
+            for (int l = D.smp_L.depth - 1; l >= 1; --l) {
+              node >>= D.smp_L.log2w;
+              atomicAdd(reinterpret_cast<unsigned long long*>(topw + D.smp_L.level_off[l] + node),
+                        (unsigned long long)delta);
+            }
+          }
+        }
+      }
+      // the root takes every delta: a warp sum, then one shared add per warp
+      root_delta = warp_sum64(root_delta);
+      if (lane == 0 && root_delta != 0)
+        atomicAdd(reinterpret_cast<unsigned long long*>(topw + D.smp_L.level_off[0]), (unsigned long long)root_delta);
+      __syncthreads();
+    }
     const uint64_t smp_Q = (uint64_t)(ntop > 0 ? top[0] : __ldcg(D.smp_tree + D.smp_L.level_off[0]));
     const Strata smp_st = strata_make(smp_Q, smp_dn);
     // wholly dynamic samples sfull + blockIdx.x + j * gridDim.x are this CTA's to descend
@@ -1619,7 +1789,8 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
         eb |= RPL_DERR_EMPTY;
       } else {
         const uint64_t prefix = strata_prefix(sm, smp_st, nullptr, D.smp_seed, smp_pos);
-        leaf = descend(D.smp_L, D.smp_tree, (int64_t)prefix, &qv, &eb, top, ntop);
+        leaf = upd ? descend_overlay(D.smp_L, D.smp_tree, (int64_t)prefix, &qv, &eb, top, uf_key, uf_val)
+                   : descend(D.smp_L, D.smp_tree, (int64_t)prefix, &qv, &eb, top, ntop);
       }
       if (lane == 0) {
         if (pc < np0) p_leaf[pc] = leaf;
@@ -1651,7 +1822,10 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
     if (lane == 0 && eb) set_err(err, eb);
     fence_proxy_async();  // the staged words were read through the generic proxy; TMA refills them
     __syncthreads();
-    if (tid == 0) {  // this CTA's index / q writes are done (release)
+#ifdef RPL_TRACE
+    if (tid == 0 && blockIdx.x == 0) g_gtrace[7] = global_ns();  // descents done
+#endif
+    if (tid == 0) {  // this CTA's index / q writes are done, and its reads of the old tree (release)
       __threadfence();
       atomicAdd(reinterpret_cast<unsigned long long*>(D.work + 2), 1ull);
     }
@@ -1866,6 +2040,71 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
       row_entry(c, pc, g - max(g0, p_s[pc] * L));
     }
     asm volatile("bar.sync 1, %0;" ::"n"((NC + 2) * 32) : "memory");
+    if (warp == 2 && blockIdx.x == 0 && D.upd_td != nullptr) {
+      // the fused update's global writes (a6-a7): once every CTA has read the old tree (each
+      // counted itself into work[2] after its descents), the winners' leaves, the int64 deltas
+      // of their ancestors, max-priority-seen and the error bits
+      if (lane == 0)
+        while (ld_acquire_u64(D.work + 2) < (unsigned long long)gridDim.x) __nanosleep(64);
+      __syncwarp();
+      int64_t* leaves = D.smp_tree + D.smp_L.level_off[D.smp_L.depth];
+      int64_t lmax = INT64_MIN;
+      int32_t eb = 0;
+      for (int j = lane; j < D.upd_n; j += 32) {
+        const int64_t raw = D.upd_idx[j];
+        if (raw >= nleaves) eb |= RPL_DERR_IDX;
+        const int64_t lf = u_leaf[j];
+        if (lf >= 0 && !(D.upd_live && u_old[j] == 0)) lmax = u_q[j] > lmax ? u_q[j] : lmax;
+        if (u_win[j]) {
+          leaves[lf] = u_q[j];
+          const int64_t delta = u_q[j] - u_old[j];
+          if (delta != 0) {
+            int64_t node = lf;
+            for (int l = D.smp_L.depth - 1; l >= 0; --l) {
+              node >>= D.smp_L.log2w;
+              atomicAdd(reinterpret_cast<unsigned long long*>(D.smp_tree + D.smp_L.level_off[l] + node),
+                        (unsigned long long)delta);
+            }
+          }
+        }
+      }
+      lmax = warp_max64(lmax);
+      int64_t* hdr = D.smp_tree + D.smp_L.hdr_off;
+      if (lane == 0) {
+        if (lmax > __ldcg(hdr)) atomicMax(reinterpret_cast<long long*>(hdr), (long long)lmax);
+        if (eb) set_err(err, eb);
+      }
+      // an attached min-tree (R29): every winner's min path, level by level from the leaves'
+      // parents up (a lane per winner; the W children loaded together)
+      int64_t* mins = reinterpret_cast<int64_t*>(__ldcg(hdr + 5));
+      if (mins) {
+        __threadfence_block();
+        __syncwarp();
+        for (int l = D.smp_L.depth - 1; l >= 0; --l) {
+          const int sh = D.smp_L.log2w * (D.smp_L.depth - l);
+          for (int j = lane; j < D.upd_n; j += 32) {
+            if (!u_win[j]) continue;
+            const int64_t node = u_leaf[j] >> sh;
+            const int64_t c0 = node << D.smp_L.log2w;
+            int64_t m2 = INT64_MAX;
+            if (l == D.smp_L.depth - 1) {
+              for (int c = 0; c < D.smp_L.fanout; ++c) {
+                const int64_t v = __ldcg(leaves + c0 + c);
+                if (v > 0 && v < m2) m2 = v;
+              }
+            } else {
+              for (int c = 0; c < D.smp_L.fanout; ++c) {
+                const int64_t v = __ldcg(mins + D.smp_L.level_off[l + 1] + c0 + c);
+                if (v < m2) m2 = v;
+              }
+            }
+            mins[D.smp_L.level_off[l] + node] = m2;
+          }
+          __threadfence_block();
+          __syncwarp();
+        }
+      }
+    }
     if (warp == 2) {
       // ---------------- fields warp: per-row fields of every published row, in order ----------------
       const int64_t qm = (D.o_w && q && !smp) ? warp_batch_qmin(qmin, idx, q, n) : 0;
@@ -2603,6 +2842,10 @@ GDesc to_dev(const rpl_gather_desc* d) {
   g.done_flag = d->done_flag;
   g.done_seq = d->done_seq;
   g.work = d->work;
+  g.upd_idx = nullptr;
+  g.upd_td = nullptr;
+  g.upd_n = g.upd_T = g.upd_live = g.upd_pad = 0;
+  g.upd_eta = g.upd_alpha = g.upd_eps = 0.0;
   g.smp_tree = nullptr;
   g.smp_seed = 0;
   return g;
@@ -2729,6 +2972,11 @@ struct SmpArgs {
   int64_t* tree;
   TreeDev L;
   uint64_t seed;
+  // fused update (rpl_gather_update_sample; upd_td NULL: none)
+  const int64_t* upd_idx = nullptr;
+  const float* upd_td = nullptr;
+  int upd_n = 0, upd_T = 0, upd_live = 0;
+  double upd_eta = 0.0, upd_alpha = 0.0, upd_eps = 0.0;
 };
 int gather_run(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q, const int64_t* qmin, double beta,
                int64_t n, int32_t* dev_err, void* stream, const SmpArgs* smp);
@@ -2738,6 +2986,52 @@ int gather_run(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q
 extern "C" int rpl_gather(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q, const int64_t* qmin,
                           double beta, int64_t n, int32_t* dev_err, void* stream) {
   return gather_run(desc, idx, q, qmin, beta, n, dev_err, stream, nullptr);
+}
+
+extern "C" int rpl_sumtree_update_seq(const rpl_tree_layout* L, int64_t* tree, const int64_t* idx,
+                                      const float* td_steps, int64_t T_p, int64_t n, double eta, double alpha,
+                                      double eps_p, int32_t flags, int32_t* dev_err, void* stream);
+
+extern "C" int rpl_gather_update_sample(const rpl_gather_desc* desc, const rpl_tree_layout* L, int64_t* tree,
+                                        const int64_t* upd_idx, const float* upd_td, int64_t T_p, int64_t n_upd,
+                                        double eta, double alpha, double eps_p, int32_t flags, uint64_t seed,
+                                        int64_t* idx_out, int64_t* q_out, double beta, int64_t n, int32_t* dev_err,
+                                        void* stream) {
+  if (!desc || !L || !tree || !idx_out || !q_out || n < 1 || n > (1ll << 30) || n_upd < 0) return RPL_EINVAL;
+  if (n_upd > 0 && (!upd_idx || !upd_td || T_p < 1 || T_p > (1ll << 30))) return RPL_EINVAL;
+  if (!(alpha >= 0.0) || !(eps_p >= 0.0) || !(eta >= 0.0 && eta <= 1.0) || (flags & ~RPL_UPD_LIVE_ONLY))
+    return RPL_EINVAL;
+  if (desc->kind != RPL_GATHER_SEQUENCE || desc->n_active || desc->col_offset || desc->peer_boards || desc->done_flag)
+    return RPL_EINVAL;
+  if (desc->period < 1 || desc->cap_T % desc->period != 0 || L->n_leaves != (desc->cap_T / desc->period) * desc->B)
+    return RPL_EINVAL;
+  SmpArgs a;
+  a.tree = tree;
+  a.L = tree_dev(L);
+  a.seed = seed;
+  // one launch when the dynamic-tail kernel runs, the batch fits its tables and every internal
+  // level fits the staging area (alpha 0 / 1 and an empty batch: the two-launch form)
+  int NS = (int)(RPL_SEQ_SLOT_KB * 1024 / (desc->obs_bytes > 0 ? desc->obs_bytes : 1));
+  if (NS > PIPE_MAX_NS) NS = PIPE_MAX_NS;
+  const bool fits = n_upd >= 1 && n_upd <= UF_MAX && L->depth >= 1 &&
+                    L->level_off[L->depth] <= (int64_t)(NS - 1) * desc->obs_bytes / 8;
+  if (fits) {
+    a.upd_idx = upd_idx;
+    a.upd_td = upd_td;
+    a.upd_n = (int)n_upd;
+    a.upd_T = (int)T_p;
+    a.upd_live = (flags & RPL_UPD_LIVE_ONLY) ? 1 : 0;
+    a.upd_eta = eta;
+    a.upd_alpha = alpha;
+    a.upd_eps = eps_p;
+    const int rc = gather_run(desc, idx_out, q_out, nullptr, beta, n, dev_err, stream, &a);
+    if (rc != RPL_EUNSUPPORTED) return rc;  // RPL_EUNSUPPORTED: nothing was enqueued
+    a.upd_td = nullptr;
+  }
+  const int rc = rpl_sumtree_update_seq(L, tree, upd_idx, upd_td, T_p, n_upd, eta, alpha, eps_p, flags, dev_err,
+                                        stream);
+  if (rc != RPL_OK) return rc;
+  return gather_run(desc, idx_out, q_out, nullptr, beta, n, dev_err, stream, &a);
 }
 
 extern "C" int rpl_gather_sample(const rpl_gather_desc* desc, const rpl_tree_layout* L, int64_t* tree, uint64_t seed,
@@ -2782,7 +3076,16 @@ int gather_run(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q
     g.smp_tree = smp->tree;
     g.smp_L = smp->L;
     g.smp_seed = smp->seed;
+    g.upd_idx = smp->upd_idx;
+    g.upd_td = smp->upd_td;
+    g.upd_n = smp->upd_n;
+    g.upd_T = smp->upd_T;
+    g.upd_live = smp->upd_live;
+    g.upd_eta = smp->upd_eta;
+    g.upd_alpha = smp->upd_alpha;
+    g.upd_eps = smp->upd_eps;
   }
+  const bool fused_upd = smp && smp->upd_td != nullptr;
   // col_offset / o_start / peer boards / fused targets / fused sampling: default kernels only
   if ((desc->done_flag != nullptr) != (desc->done_seq != nullptr)) return RPL_EINVAL;
   const int seq_variant =
@@ -2890,6 +3193,7 @@ int gather_run(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q
                                                      dev_err, dyn, gd, st);
           }
         }
+        if (fused_upd) return RPL_EUNSUPPORTED;  // the fused update needs the dynamic-tail kernel
         int64_t rows_per_cta = (total + grid - 1) / grid;
         if (rows_per_cta > PL_MAX_ROWS) rows_per_cta = PL_MAX_ROWS;
         grid = (total + rows_per_cta - 1) / rows_per_cta;
@@ -2903,6 +3207,7 @@ int gather_run(const rpl_gather_desc* desc, const int64_t* idx, const int64_t* q
                                                  st);
       }
     }
+    if (fused_upd) return RPL_EUNSUPPORTED;  // nothing enqueued: the caller runs the two-launch form
     if (tma_ok && desc->out_mode == RPL_OUT_STACKED && desc->o_obs &&
         (seq_variant == 3 ||
          (seq_variant == 0 && !desc->col_offset && !desc->o_start && !desc->peer_boards && !desc->o_tgt &&

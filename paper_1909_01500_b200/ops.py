@@ -671,6 +671,20 @@ class GatherPlan:
                                     _ptr(q_out), float(beta), self.n, _ptr(err), s), "rpl_gather_sample")
         return self.outputs
 
+    def run_update_sample(self, tree, upd_idx, upd_td, seed, idx_out, q_out, eta=0.9, alpha=0.9, eps_p=1e-3,
+                          beta=0.0, live_only=False, err=None, stream=None, q_tgt=None):
+        """rpl_gather_update_sample: rpl_sumtree_update_seq(upd_idx, upd_td [T_p, n_upd]) and
+        rpl_gather_sample in ONE launch when the dynamic-tail kernel can run it (else the two)."""
+        s = _stream(self.device) if stream is None else stream
+        if q_tgt is not None:
+            self.desc.q_tgt = q_tgt.data_ptr()
+        T_p, n_upd = (int(upd_td.shape[0]), int(upd_td.shape[1])) if upd_td.dim() == 2 else (1, int(upd_td.numel()))
+        check(lib.rpl_gather_update_sample(self._dp, tree._lp, _ptr(tree.storage), _ptr(upd_idx), _ptr(upd_td), T_p,
+                                           n_upd, float(eta), float(alpha), float(eps_p),
+                                           1 if live_only else 0, int(seed) & (2 ** 64 - 1), _ptr(idx_out),
+                                           _ptr(q_out), float(beta), self.n, _ptr(err), s), "rpl_gather_update_sample")
+        return self.outputs
+
     def run(self, idx, q=None, qmin=None, beta=0.0, err=None, stream=None, q_tgt=None):
         """q_tgt: this call's bootstrap values for the fused targets (f32 [L, n]; None keeps
         the one set before)."""

@@ -48,11 +48,15 @@ qv = torch.randn((8, L, n), generator=g, device=dev) * 10
 plan = rpl.GatherPlan(ring, n, kind="sequence", k=k, seq_len=L, period=period, with_weights=True,
                       targets=bench.r2d2_targets(c, qv[0]))
 lib, P_ = rpl._lib.lib, rpl.ops._ptr
-FUSED = os.environ.get("STEP", "fused") == "fused"
+FUSED = os.environ.get("STEP", "fused") in ("fused", "one")
 
 
 def step(i):
     s = rpl.ops._stream(dev)
+    if os.environ.get("STEP") == "one":  # update + sampling + gather in one launch
+        plan.run_update_sample(tree, idx[(i + 1) % 2], td[i % 8], 0xBEEF, idx[i % 2], q, eta=c["eta"], alpha=c["alpha"],
+                               eps_p=c["eps_p"], beta=c["beta"], err=err, stream=s, q_tgt=qv[i % 8])
+        return
     rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(idx[(i + 1) % 2]), P_(td[i % 8]),
                                               c["train"], n, c["eta"], c["alpha"], c["eps_p"], 0, None, s), "upd")
     if FUSED:

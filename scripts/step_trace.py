@@ -46,6 +46,10 @@ DOUBLE = os.environ.get("DOUBLE_UPD", "0") == "1"  # run the update twice (the t
 
 def step(i):
     s = rpl.ops._stream(dev)
+    if MODE == "one":  # update + sampling + gather in one launch
+        plan.run_update_sample(tree, idx[(i + 1) % 2], td[i % 8], 0xBEEF, idx[i % 2], q, eta=c["eta"], alpha=c["alpha"],
+                               eps_p=c["eps_p"], beta=c["beta"], err=err, stream=s, q_tgt=qv[i % 8])
+        return
     for _ in range(2 if DOUBLE else 1):
         rpl._lib.check(lib.rpl_sumtree_update_seq(tree._lp, P_(tree.storage), P_(idx[(i + 1) % 2]), P_(td[i % 8]),
                                                   c["train"], n, c["eta"], c["alpha"], c["eps_p"], 0, None, s),
@@ -74,9 +78,9 @@ torch.cuda.synchronize()
 names_u = {7: "update_entry", 0: "update_past_wait", 2: "update_mixed", 3: "update_hash_reset",
            4: "update_dedupe", 5: "update_leaves", 6: "update_end", 8: "sample_past_wait", 9: "sample_end"}
 DYN = os.environ.get("STEP", "pair") != "static"
-names_g = {0: "gather_entry", 1: "gather_past_wait", 2: "gather_first_frames", 3: "gather_end",
+names_g = {0: "gather_entry", 1: "gather_past_wait", 2: "gather_first_frames (dyn: staged)", 3: "gather_end",
            4: "gather_smp_staged (dyn: earliest CTA entry)", 5: "gather_smp_sampled (dyn: earliest past wait)",
-           6: "gather_first_tma_issue (dyn: latest past wait)", 7: "gather_pieces_done",
+           6: "gather_first_tma_issue (dyn: latest past wait)", 7: "gather_pieces_done (dyn: descents done)",
            8: "gather_first_cta_end"}
 runs = []
 bu, bg = (ctypes.c_int64 * 16)(), (ctypes.c_int64 * 9)()

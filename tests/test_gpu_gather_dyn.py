@@ -132,3 +132,73 @@ def test_dynamic_tail_fused_sampling(rpl, schedule, L, k, n_s, period):
         ntd = np.abs(g.normal(size=n_s)).astype(np.float32)
         t1.update(i1, T_(ntd), 0.9)
         t2.update(i2, T_(ntd), 0.9)
+
+
+@pytest.mark.parametrize("L,k,n_s,period,case", [(125, 4, 64, 40, "plain"), (125, 4, 64, 40, "dups"),
+                                                 (45, 4, 120, 40, "live"), (5, 4, 33, 8, "mintree"),
+                                                 (125, 4, 64, 40, "padding")])
+def test_fused_update_sample_equals_two_launches(rpl, L, k, n_s, period, case):
+    # rpl_gather_update_sample (update + sampling + gather in one launch) against
+    # rpl_sumtree_update_seq followed by rpl_gather_sample, over chained calls: the whole tree
+    # storage (leaves, nodes, header), an attached min-tree, indices, q, weights and every output
+    import torch
+    cap, B = 400, 4
+    ring = make_ring(190 + L, cap=cap, B=B, ep_len=12.0, period=period, rnn_h=8, reward_kind="r2d2",
+                     obs_shape=(16, 24))
+    dr = rpl.GatherRing(obs=T_(ring.obs), act=T_(ring.act), rew=T_(ring.rew), done=T_(ring.done),
+                        cursor=ring.cursor, size=ring.size, rnn=T_(ring.rnn))
+    nb = cap // period
+    g = rng(L * 3 + n_s)
+    N = nb * B
+    t1, t2 = rpl.SumTree(N, 32), rpl.SumTree(N, 32)
+    valid = [b_ * B + c for b_ in range(nb) if OG.window_valid_sequence(b_ * period, cap, ring.cursor, ring.size, k, L)
+             for c in range(B)]
+    td = np.abs(g.normal(size=len(valid))).astype(np.float32)
+    mins = []
+    for t in (t1, t2):
+        t.update(T_(np.array(valid, np.int64)), T_(td), 0.9)
+        if case == "mintree":
+            mins.append(t.attach_min_tree())
+    tg = dict(lo=0, T=max(1, L - 6), n_step=5, gamma=0.99, rescale=True,
+              q=T_(g.normal(0, 5, (L, n_s)).astype(np.float32))) if L > 6 else None
+    p1 = rpl.GatherPlan(dr, n_s, kind="sequence", k=k, seq_len=L, period=period, with_weights=True, targets=tg)
+    p2 = rpl.GatherPlan(dr, n_s, kind="sequence", k=k, seq_len=L, period=period, with_weights=True, targets=tg)
+    e1, e2 = (torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(2))
+    prev = torch.full((n_s,), -1, dtype=torch.int64, device="cuda")
+    live = case == "live"
+    for step in range(4):
+        T_p = 80 if L == 125 else 7
+        steps = np.abs(g.lognormal(0, 2, (T_p, n_s))).astype(np.float32)
+        pidx = prev.clone()
+        if case == "dups" and step > 0:
+            pidx[5] = pidx[0]
+            pidx[9] = pidx[0]
+        if case == "padding":
+            pidx[::7] = -1
+        if case == "live" and step > 0:  # some of the batch's leaves were invalidated meanwhile
+            z = pidx[pidx >= 0][:5]
+            for t in (t1, t2):
+                t.set_q(z, torch.zeros_like(z))
+        std = T_(steps)
+        i1, q1 = (torch.empty(n_s, dtype=torch.int64, device="cuda") for _ in range(2))
+        if step > 0:
+            t1.update_seq(pidx, std, 0.9, eta=0.9, live_only=live)
+        o1 = p1.run_sample(t1, 77, i1, q1, beta=0.6, err=e1)
+        i2, q2 = (torch.full((n_s,), -9, dtype=torch.int64, device="cuda") for _ in range(2))
+        if step > 0:
+            o2 = p2.run_update_sample(t2, pidx, std, 77, i2, q2, eta=0.9, alpha=0.9, beta=0.6, live_only=live, err=e2)
+        else:
+            o2 = p2.run_sample(t2, 77, i2, q2, beta=0.6, err=e2)
+        torch.cuda.synchronize()
+        s1, s2 = H(t1.storage).copy(), H(t2.storage).copy()
+        hdr = int(t1.layout.hdr_off)
+        s1[hdr + 5] = s2[hdr + 5] = 0  # header word 5: each tree's own min-tree address
+        assert np.array_equal(s1, s2), (case, step, "tree")
+        if mins:
+            assert np.array_equal(H(mins[0]), H(mins[1])), (case, step, "min-tree")
+        assert np.array_equal(H(i1), H(i2)) and np.array_equal(H(q1), H(q2)), (case, step)
+        for name in o1:
+            assert np.array_equal(H(o1[name]), H(o2[name])), (case, step, name)
+        assert int(H(e1)[0]) == int(H(e2)[0]), (case, step)
+        assert H(p2._work).tolist() == [0, 0, 0, 0]
+        prev = i2.clone()
