@@ -1371,7 +1371,19 @@ def run_reference(args):
                             "sample": f"{K} steps of {nseq} sequences (bounded sample of the 64-sequence step)",
                             "host_cpus": os.cpu_count(), "affinity": aff, "cpu_model": model},
            "e2e": {"value": val, "unit": "sequences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    res["native_so_loaded"] = _repo_so_mapped()  # evidence: the oracle arm maps no product library
     print(json.dumps(res))
+
+
+def _repo_so_mapped():
+    """Shared objects under this repository mapped into this process (/proc/self/maps)."""
+    root = os.path.dirname(os.path.abspath(__file__))
+    try:
+        with open("/proc/self/maps") as f:
+            paths = {ln.split()[-1] for ln in f if ln.rstrip().endswith(".so") or ".so." in ln}
+    except OSError:
+        return None
+    return sorted(p for p in paths if p.startswith(root))
 
 
 def main():
