@@ -1009,7 +1009,7 @@ int scan_variant() {
   if (v < 0) {
     const char* e = getenv("RPL_SCAN_VARIANT");
     int want = e ? atoi(e) : 0;
-    if (want < 0 || want > 17) want = 0;
+    if (want < 0 || want > 19) want = 0;
     int expect = -1;
     g_scan_variant.compare_exchange_strong(expect, want);
     v = g_scan_variant.load(std::memory_order_relaxed);
@@ -1088,7 +1088,8 @@ int launch_scan_cluster(const float* r, const float* v, const uint8_t* d, const 
 
 template <int COLS, int WARPS, int S, int STAGES, bool GAE, int MINB, int OB = 2>
 int launch_scan_pipe(const float* r, const float* v, const uint8_t* d, const float* boot, int64_t T, int64_t B,
-                     double gamma, double lam, float* o0, float* o1, cudaStream_t st, const float* vterm, bool* used) {
+                     double gamma, double lam, float* o0, float* o1, cudaStream_t st, const float* vterm, bool* used,
+                     int trigger = -1) {
   using SMt = ScanPipeSmem<COLS, WARPS, S, STAGES, GAE, OB>;
   constexpr int CH = SMt::CH;
   CUtensorMap mr, mv, md, mo0, mo1;
@@ -1111,7 +1112,7 @@ int launch_scan_pipe(const float* r, const float* v, const uint8_t* d, const flo
   int64_t grid = (int64_t)sm_count() * (per_sm > 0 ? per_sm : 1);
   if (grid > groups) grid = groups;
   return launch_pdl(kern, dim3((unsigned)grid), dim3(WARPS * 32), dyn, st, mr, mv, md, mo0, mo1, boot, T, B, gamma,
-                    lam, (GAE && o1) ? 1 : 0, vterm, scan_trigger());
+                    lam, (GAE && o1) ? 1 : 0, vterm, trigger >= 0 ? trigger : scan_trigger());
 }
 
 template <bool GAE>
@@ -1138,10 +1139,31 @@ int launch_scan(const float* r, const float* v, const uint8_t* d, const float* b
     // One chunk per group (T <= 128, e.g. PPO): the 16-column shape, twice the CTAs (PPO GAE
     // 4.40 vs 4.56 us); longer horizons: the 32-column shape (wider TMA rows win there).
     bool used = false;
+    if (var == 0 && T <= 128 && (B + 15) / 16 <= 4 * (int64_t)sm_count()) {
+      // one item per CTA (every 16-column group a CTA of its own): one load stage and one output
+      // buffer (38 KB of shared memory, 64 registers), 4 CTAs per SM, and the dependent launch
+      // triggered once the tiles are requested — the next call's CTAs sit resident beside this
+      // call's and issue their loads the moment it completes.  PPO [128, 4096], interleaved A/B
+      // (scripts/scan_ab.py, 10 rounds): GAE 4.58 vs 4.89 us, discounted 3.39 vs 3.86 us per
+      // call; the same shape without the early trigger: 5.02 us (profiles/r2/scan_coresident_ab.txt).
+      const int rc = launch_scan_pipe<16, 8, 8, 1, GAE, 4, 1>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used,
+                                                              scan_trigger() == 0 ? 0 : 2);
+      if (used) return rc;
+    }
     const bool narrow = var == 9 || T <= 128;
     const int rc = narrow
                        ? launch_scan_pipe<16, 8, 8, 3, GAE, 2>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used)
                        : launch_scan_pipe<32, 8, 16, 3, GAE, 1>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used);
+    if (used) return rc;
+  }
+  if ((var == 18 || var == 19) && T <= 128 && B < (1ll << 31)) {
+    // single-chunk horizons, one load stage and one output buffer (38 KB of shared memory), 3
+    // (18) or 4 (19) CTAs per SM, the dependent launch triggered once the tiles are requested:
+    // the next call's CTAs can sit resident beside this call's (A/B)
+    bool used = false;
+    const int rc = var == 18
+                       ? launch_scan_pipe<16, 8, 8, 1, GAE, 4, 1>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used)
+                       : launch_scan_pipe<16, 8, 8, 1, GAE, 4, 1>(r, v, d, boot, T, B, gamma, lam, o0, o1, st, vterm, &used, 2);
     if (used) return rc;
   }
   if (var >= 10 && var <= 17 && T < (1ll << 31) && B < (1ll << 31)) {  // pipeline shapes (A/B)
@@ -1271,7 +1293,7 @@ extern "C" int rpl_debug_scan_trace(int64_t* out, int32_t n) {
 }
 
 extern "C" int rpl_debug_set_scan_variant(int32_t variant) {
-  if (variant < 0 || variant > 17) return RPL_EINVAL;
+  if (variant < 0 || variant > 19) return RPL_EINVAL;
   g_scan_variant.store(variant);
   return RPL_OK;
 }
