@@ -64,7 +64,8 @@ inline int launch_status() {
 // pdl_trigger() lets the next grid start launching once every CTA has called it.
 // RPL_PDL=0 in the environment disables the attribute (A/B measurement).
 // Measurement knob (build flag, default 0): bit 1 update, 2 sampler, 4 sequence gather,
-// 8 n-step — that kernel triggers its dependent launch at entry instead of at exit.
+// (8, the n-step kernels: they now always trigger at entry) — that kernel triggers its
+// dependent launch at entry instead of at exit.
 #ifndef RPL_PDL_EARLY
 #define RPL_PDL_EARLY 0
 #endif

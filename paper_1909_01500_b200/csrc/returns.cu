@@ -839,7 +839,9 @@ __global__ void k_nstep(const float* __restrict__ r, const uint8_t* __restrict__
                         float* __restrict__ out, uint8_t* __restrict__ done_out, const float* __restrict__ vterm) {
   const int64_t rows = T - n + 1;
   const int64_t total = rows * B;
-  if (RPL_PDL_EARLY & 8) pdl_trigger();  // A/B knob (common.cuh)
+  // dependent launch at entry: the next call's CTAs sit resident beside this grid's (PPO
+  // [128, 4096] n = 5: 6.95 -> 6.83 us rescaled, 4.77 -> 4.55 us plain, profiles/r2/ab_nstep.txt)
+  pdl_trigger();
   pdl_wait();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -906,7 +908,7 @@ __global__ void __launch_bounds__(128)
 k_nstep_runs(const float* __restrict__ r, const uint8_t* __restrict__ d, int64_t T, int64_t B, int n, double gamma,
              const float* __restrict__ q, const float* __restrict__ q_boot, int rescale, double eps,
              float* __restrict__ out, uint8_t* __restrict__ done_out, const float* __restrict__ vterm) {
-  if (RPL_PDL_EARLY & 8) pdl_trigger();  // A/B knob (common.cuh)
+  pdl_trigger();  // at entry, as k_nstep
   pdl_wait();
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t rows = T - n + 1;
