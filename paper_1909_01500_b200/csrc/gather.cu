@@ -2130,11 +2130,18 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
       const int ndyn = total - r0;  // dynamic rows [r0, total); work[0] counts the rows taken
       int grabs = 0;
       bool exhausted = ndyn <= 0;
+      // lookahead: bits 0-7 the rows kept queued before a grab; bits 8-15 (if non-zero) the
+      // queue once fewer than bits 16-30 rows are left in the pool (the end of the pool: a
+      // shorter queue when it runs dry means less spread between the CTAs' ends)
+      const int look_base = lookahead & 0xff;
+      const int look_end = ((lookahead >> 8) & 0xff) ? ((lookahead >> 8) & 0xff) : look_base;
+      const int look_thr = lookahead >> 16;
+      int left = ndyn;  // rows left in the pool, as this warp last saw it
       while (!exhausted) {
         // grab only when this CTA is about to run dry (a slower SM takes less), and GUIDED: a
         // grab takes ~1/grid of what is left, between 2 and dyn_rows rows, so early grabs are
         // long (few reloaded history frames) and the last ones short (fine balance)
-        if (cn - s_frontier <= lookahead) {
+        if (cn - s_frontier <= (left < look_thr ? look_end : look_base)) {
           if (cn + dyn_rows > DY_MAX_ROWS || pcn + 2 > DY_MAX_PIECES) {
             exhausted = true;
             continue;
@@ -2154,6 +2161,7 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
             exhausted = true;
             continue;
           }
+          left = ndyn - start - cnt;
 #ifdef RPL_TRACE
           if (lane == 0 && blockIdx.x < 512 && grabs < 8) {
             g_ggrab[blockIdx.x][grabs][0] = global_ns();
@@ -2927,7 +2935,10 @@ extern "C" int rpl_debug_set_gather_dyn(int32_t pct, int32_t rows, int32_t looka
     g_dyn_early.store(pct - 1000);
     return RPL_OK;
   }
-  if (pct < -1 || pct > 100 || rows < 1 || rows > 32 || lookahead < 1 || lookahead > 200) return RPL_EINVAL;
+  // lookahead: the queue (1-200), optionally | (end-of-pool queue << 8) | (its threshold in rows << 16)
+  if (pct < -1 || pct > 100 || rows < 1 || rows > 32 || (lookahead & 0xff) < 1 || (lookahead & 0xff) > 200 ||
+      ((lookahead >> 8) & 0xff) > 200 || lookahead < 0)
+    return RPL_EINVAL;
   g_dyn_pct.store(pct);
   g_dyn_rows.store(rows);
   g_dyn_look.store(lookahead);
