@@ -498,6 +498,11 @@ def run_rpl(args):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     launches0 = rpl.launch_count()
+    # a ~100 us device spin BEFORE the start event (outside the timed region): the host enqueues
+    # the start event and all K steps' graph replays while it runs, so the region times K steps
+    # of device work back to back rather than the first graph launch's host submission latency
+    # (with K = 20 that gap alone read as +1.8 us per step: 65.07 vs 63.09 us per replay)
+    torch.cuda._sleep(int(2e5))
     e0.record()
     if use_graph:
         for j in range(reps):
