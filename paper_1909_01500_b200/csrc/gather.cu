@@ -1479,7 +1479,10 @@ std::atomic<int> g_dyn_look{12};
 // fused sampling: warp 0 issues up to this many of piece 0's first frame loads right after its
 // descent (0: the producer starts once every table is built); rpl_debug_set_gather_dyn's
 // pct = 1000 + count sets it
-std::atomic<int> g_dyn_early{0};  // measured neutral at 2-8 and +1.5 us at 28 (profiles/r2/dyn_sweep.txt)
+std::atomic<int> g_dyn_early{0};
+// measurement: 1 = every dynamic-tail launch takes the fused-update instantiation (the
+// default gather's code before it had its own); rpl_debug_set_gather_dyn's pct = 2000 + on
+std::atomic<int> g_dyn_updk{0};  // measured neutral at 2-8 and +1.5 us at 28 (profiles/r2/dyn_sweep.txt)
 
 template <int NC>
 int launch_seq_lsu(const GDesc& g, const int64_t* idx, int64_t n, int NS, int64_t rows_per_cta, const int64_t* q,
@@ -1571,7 +1574,7 @@ __device__ __forceinline__ int64_t descend_overlay(const TreeDev& L, const int64
   return node;
 }
 
-template <int NC>
+template <int NC, bool UPD>
 __global__ void __launch_bounds__((NC + 3) * 32, 1)
 k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, int rs, int dyn_rows,
                  int lookahead, const int64_t* __restrict__ q, const int64_t* __restrict__ qmin, double beta,
@@ -1653,12 +1656,14 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
   //     batch-min weights / stream advance follow in the meta warp.
   const bool smp = D.smp_tree != nullptr;
   __shared__ int64_t p_leaf[DY_MAX_PIECES];
-  __shared__ int64_t u_leaf[UF_MAX], u_old[UF_MAX], u_q[UF_MAX];
-  __shared__ float u_td[UF_MAX];
-  __shared__ int8_t u_win[UF_MAX];
-  __shared__ unsigned long long uf_key[UF_SLOTS];
-  __shared__ long long uf_val[UF_SLOTS];
-  __shared__ int uf_pos[UF_SLOTS];
+  // the fused update's tables (UPD: the rpl_gather_update_sample instantiation only)
+  constexpr int UFM = UPD ? UF_MAX : 1, UFS = UPD ? UF_SLOTS : 1;
+  __shared__ int64_t u_leaf[UFM], u_old[UFM], u_q[UFM];
+  __shared__ float u_td[UFM];
+  __shared__ int8_t u_win[UFM];
+  __shared__ unsigned long long uf_key[UFS];
+  __shared__ long long uf_val[UFS];
+  __shared__ int uf_pos[UFS];
   __shared__ int s_pre;  // frames of piece 0 issued by warp 0 right after its descent
   if (tid == 0) s_pre = 0;
   uint64_t smp_pos = 0;
@@ -1688,7 +1693,7 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
     //     the update to global memory once every CTA has finished reading the old tree
     //     (work[3] counts the readers).  Same tree and draws as rpl_sumtree_update_seq
     //     followed by rpl_gather_sample.
-    const bool upd = D.upd_td != nullptr;
+    const bool upd = UPD && D.upd_td != nullptr;
     const int nu = upd ? D.upd_n : 0;
     if (upd) {
       for (int s2 = tid; s2 < UF_SLOTS; s2 += NT) {
@@ -1701,17 +1706,19 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
         u_leaf[tid] = lf;
         u_old[tid] = lf >= 0 ? __ldcg(D.smp_tree + D.smp_L.level_off[D.smp_L.depth] + lf) : 0;
       }
-      // sequence priorities: eight lanes per sequence, NT / 8 sequences per pass; the next
-      // pass's loads are in flight while this pass reduces
-      float va[TD8_BATCH], vb[TD8_BATCH];
-      sequence_td8_load(va, D.upd_td, D.upd_T, nu, tid >> 3, (tid >> 3) < nu);
-      for (int p0 = 0; p0 < nu; p0 += NT / 8) {
-        const int jj = p0 + (tid >> 3), jn = jj + NT / 8;
-        if (p0 + NT / 8 < nu) sequence_td8_load(vb, D.upd_td, D.upd_T, nu, jn, jn < nu);
-        const float v = sequence_td8_finish(va, D.upd_td, D.upd_T, nu, jj, jj < nu, D.upd_eta);
-        if ((tid & 7) == 0 && jj < nu) u_td[jj] = v;
+      // sequence priorities: UG lanes per sequence, NT / UG sequences per pass (56: a 64-entry
+      // batch in two passes, where eight lanes took three); the next pass's loads are in flight
+      // while this pass reduces
+      constexpr int UG = 4, UB = 20;
+      float va[UB], vb[UB];
+      sequence_tdg_load<UG, UB>(va, D.upd_td, D.upd_T, nu, tid / UG, (tid / UG) < nu);
+      for (int p0 = 0; p0 < nu; p0 += NT / UG) {
+        const int jj = p0 + tid / UG, jn = jj + NT / UG;
+        if (p0 + NT / UG < nu) sequence_tdg_load<UG, UB>(vb, D.upd_td, D.upd_T, nu, jn, jn < nu);
+        const float v = sequence_tdg_finish<UG, UB>(va, D.upd_td, D.upd_T, nu, jj, jj < nu, D.upd_eta);
+        if ((tid & (UG - 1)) == 0 && jj < nu) u_td[jj] = v;
 #pragma unroll
-        for (int u2 = 0; u2 < TD8_BATCH; ++u2) va[u2] = vb[u2];
+        for (int u2 = 0; u2 < UB; ++u2) va[u2] = vb[u2];
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -2040,7 +2047,7 @@ k_gather_seq_dyn(GDesc D, const int64_t* __restrict__ idx, int64_t n, int NS, in
       row_entry(c, pc, g - max(g0, p_s[pc] * L));
     }
     asm volatile("bar.sync 1, %0;" ::"n"((NC + 2) * 32) : "memory");
-    if (warp == 2 && blockIdx.x == 0 && D.upd_td != nullptr) {
+    if (UPD && warp == 2 && blockIdx.x == 0 && D.upd_td != nullptr) {
       // the fused update's global writes (a6-a7): once every CTA has read the old tree (each
       // counted itself into work[2] after its descents), the winners' leaves, the int64 deltas
       // of their ancestors, max-priority-seen and the error bits
@@ -2317,7 +2324,11 @@ template <int NC>
 int launch_seq_dyn(const GDesc& g, const int64_t* idx, int64_t n, int NS, int rs, int dyn_rows, int lookahead,
                    const int64_t* q, const int64_t* qmin, double beta, int32_t* dev_err, size_t dyn, int64_t grid,
                    cudaStream_t st) {
-  ensure_smem(reinterpret_cast<const void*>(k_gather_seq_dyn<NC>), dyn);
+  // the fused update (rpl_gather_update_sample) has its own instantiation: the default gather
+  // carries none of its code, registers or tables
+  auto kern = (g.upd_td != nullptr || g_dyn_updk.load(std::memory_order_relaxed)) ? k_gather_seq_dyn<NC, true>
+                                                                                  : k_gather_seq_dyn<NC, false>;
+  ensure_smem(reinterpret_cast<const void*>(kern), dyn);
   // With the update fused in (rpl_gather_update_sample) the next kernel is usually the next
   // step's gather, whose CTAs only fit once this grid's CTAs leave: let it launch once each
   // CTA's producer has issued its last load, so its CTAs land (and run their prologue) on the
@@ -2326,7 +2337,7 @@ int launch_seq_dyn(const GDesc& g, const int64_t* idx, int64_t n, int NS, int rs
   // is small enough to sit beside the gather; an early trigger there costs 0.4 us).
   int trig = g_gather_trigger.load(std::memory_order_relaxed);
   if (trig == -1 && g.upd_td != nullptr) trig = 1;
-  return launch_pdl(k_gather_seq_dyn<NC>, dim3((unsigned)grid), dim3((NC + 3) * 32), dyn, st, g, idx, n, NS, rs,
+  return launch_pdl(kern, dim3((unsigned)grid), dim3((NC + 3) * 32), dyn, st, g, idx, n, NS, rs,
                     dyn_rows, lookahead, q, qmin, beta, dev_err, trig, g_dyn_early.load(std::memory_order_relaxed));
 }
 
@@ -2931,6 +2942,10 @@ extern "C" int rpl_debug_gather_trace(int64_t* out, int32_t n) {
 }
 
 extern "C" int rpl_debug_set_gather_dyn(int32_t pct, int32_t rows, int32_t lookahead) {
+  if (pct == 2000 || pct == 2001) {  // measurement: the fused-update instantiation for every launch
+    g_dyn_updk.store(pct - 2000);
+    return RPL_OK;
+  }
   if (pct >= 1000 && pct <= 1000 + PIPE_MAX_NS) {  // measurement: early first-frame loads (count, 0 = off)
     g_dyn_early.store(pct - 1000);
     return RPL_OK;
