@@ -711,9 +711,12 @@ int rpl_debug_set_gather_trigger(int32_t at);
  * static share of the rows in percent of an even split (0: every row dynamic; -1: the static
  * kernel; default 88), rows = the longest grab (1..32, default 16; a grab takes about
  * 1/grid of the dynamic rows left, at least 2), lookahead = rows published but not yet stored
- * below which a CTA grabs again (default 12).  pct = 1000 + c (rows, lookahead ignored)
- * sets how many of its first piece's frame loads a CTA issues right after its fused-sampling
- * descent (0 = none, the default: 2-8 measured neutral, 28 slower).
+ * below which a CTA grabs again (bits 0-7, 1..200, default 12; optionally bits 8-15 = that
+ * queue once fewer than bits 16-30 rows are left in the pool, 0 = unchanged).  pct = 1000 + c
+ * (rows, lookahead ignored) sets how many of its first piece's frame loads a CTA issues right
+ * after its fused-sampling descent (0 = none, the default: 2-8 measured neutral, 28 slower);
+ * pct = 2001 / 2000 makes every dynamic-tail launch take / not take the fused-update kernel
+ * instantiation (A/B of the default gather's own instantiation).
  * RPL_EINVAL out of range. */
 int rpl_debug_set_gather_dyn(int32_t pct, int32_t rows, int32_t lookahead);
 int rpl_debug_gather_trace(int64_t* out, int32_t n);
