@@ -709,9 +709,9 @@ int rpl_debug_set_upd_multi(int32_t on);
 int rpl_debug_set_gather_trigger(int32_t at);
 /* Measurement knobs of the dynamic-tail sequence gather (rpl_gather_desc.work): pct = the
  * static share of the rows in percent of an even split (0: every row dynamic; -1: the static
- * kernel; default 88), rows = the longest grab (1..32, default 16; a grab takes about
+ * kernel; default 80), rows = the longest grab (1..32, default 16; a grab takes about
  * 1/grid of the dynamic rows left, at least 2), lookahead = rows published but not yet stored
- * below which a CTA grabs again (bits 0-7, 1..200, default 12; optionally bits 8-15 = that
+ * below which a CTA grabs again (bits 0-7, 1..200, default 16; optionally bits 8-15 = that
  * queue once fewer than bits 16-30 rows are left in the pool, 0 = unchanged).  pct = 1000 + c
  * (rows, lookahead ignored) sets how many of its first piece's frame loads a CTA issues right
  * after its fused-sampling descent (0 = none, the default: 2-8 measured neutral, 28 slower);

@@ -1473,9 +1473,11 @@ std::atomic<int> g_gather_trigger{(RPL_PDL_EARLY & 4) ? 0 : -1};
 // an even split, 0 = every row dynamic; -1 = the static kernel), the rows per dynamic unit, and the look-ahead (rows
 // published but not yet stored below which the meta warp grabs the next unit).
 // rpl_debug_set_gather_dyn.
-std::atomic<int> g_dyn_pct{88};   // in-process sweeps (scripts/ab_dyn_sweep.py, profiles/r2/dyn_sweep.txt)
+// in-process sweeps (scripts/ab_dyn_sweep.py, profiles/r2/dyn_sweep.txt): 88 / 16 / 12 until the
+// default gather got its own instantiation; since then 80 / 16 / 16 (-1.0 us per R2D2 step)
+std::atomic<int> g_dyn_pct{80};
 std::atomic<int> g_dyn_rows{16};
-std::atomic<int> g_dyn_look{12};
+std::atomic<int> g_dyn_look{16};
 // fused sampling: warp 0 issues up to this many of piece 0's first frame loads right after its
 // descent (0: the producer starts once every table is built); rpl_debug_set_gather_dyn's
 // pct = 1000 + count sets it
