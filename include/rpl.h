@@ -714,7 +714,7 @@ int rpl_debug_set_gather_trigger(int32_t at);
  * below which a CTA grabs again (bits 0-7, 1..200, default 16; optionally bits 8-15 = that
  * queue once fewer than bits 16-30 rows are left in the pool, 0 = unchanged).  pct = 1000 + c
  * (rows, lookahead ignored) sets how many of its first piece's frame loads a CTA issues right
- * after its fused-sampling descent (0 = none, the default: 2-8 measured neutral, 28 slower);
+ * after its fused-sampling descent (default 10: -0.4 us per R2D2 step; 0 = none, 16 and 28 slower);
  * pct = 2001 / 2000 makes every dynamic-tail launch take / not take the fused-update kernel
  * instantiation (A/B of the default gather's own instantiation).
  * RPL_EINVAL out of range. */

@@ -1480,8 +1480,10 @@ std::atomic<int> g_dyn_rows{16};
 std::atomic<int> g_dyn_look{16};
 // fused sampling: warp 0 issues up to this many of piece 0's first frame loads right after its
 // descent (0: the producer starts once every table is built); rpl_debug_set_gather_dyn's
-// pct = 1000 + count sets it
-std::atomic<int> g_dyn_early{0};
+// pct = 1000 + count sets it (measured neutral at 2-8 and +1.5 us at 28 with the shared
+// instantiation; with the default gather's own instantiation and the 80 / 16 / 16 schedule 10
+// is -0.4 us per R2D2 step: profiles/r2/dyn_sweep.txt)
+std::atomic<int> g_dyn_early{10};
 // measurement: 1 = every dynamic-tail launch takes the fused-update instantiation (the
 // default gather's code before it had its own); rpl_debug_set_gather_dyn's pct = 2000 + on
 std::atomic<int> g_dyn_updk{0};  // measured neutral at 2-8 and +1.5 us at 28 (profiles/r2/dyn_sweep.txt)

@@ -92,8 +92,16 @@ def test_dynamic_tail_vs_oracle(rpl, schedule, L, k, n_s, out_mode, pad_mode):
             assert np.array_equal(H(out["tgt_done"])[:, ok], dnr[:, ok])
 
 
+@pytest.fixture(params=[10, 0, 28], ids=["early10", "early0", "early28"])
+def early(rpl, request):
+    # first-frame loads a CTA issues right after its fused descent (10: the default)
+    assert rpl._lib.lib.rpl_debug_set_gather_dyn(1000 + request.param, 1, 1) == 0
+    yield request.param
+    rpl._lib.lib.rpl_debug_set_gather_dyn(1010, 1, 1)
+
+
 @pytest.mark.parametrize("L,k,n_s,period", [(125, 4, 64, 40), (45, 4, 300, 40), (5, 4, 33, 8), (1, 1, 7, 4)])
-def test_dynamic_tail_fused_sampling(rpl, schedule, L, k, n_s, period):
+def test_dynamic_tail_fused_sampling(rpl, schedule, early, L, k, n_s, period):
     # rpl_gather_sample with the dynamic tail: indices, q, weights, tree header and every output
     # equal rpl_sumtree_sample_stream + rpl_gather with the static split, over chained calls
     import torch
