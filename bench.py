@@ -74,6 +74,8 @@ def parse():
                     help="1 GPU: priority update + sampling as one launch (rpl_sumtree_update_sample; "
                          "measured 1.7 us/step slower than the PDL-chained pair)")
     ap.add_argument("--seq-variant", type=int, default=None, help="diagnostics: sequence-gather kernel variant")
+    ap.add_argument("--gather-dyn", default=None,
+                    help="measurement: the dynamic-tail schedule pct,rows,lookahead (rpl_debug_set_gather_dyn)")
     ap.add_argument("--fused-sample", type=int, default=1, choices=[0, 1],
                     help="1 GPU: stratified sampling inside the sequence gather (rpl_gather_sample), so the step "
                          "is update_seq -> gather (default: same-box A/B 68.1 vs 69.45 us per step with the "
@@ -228,6 +230,9 @@ def run_rpl(args):
     from paper_1909_01500_b200 import replay as R
     from synth import make_ring, rng
     FUSED_SAMPLE[0] = bool(args.fused_sample) and not args.tree_fused
+    if args.gather_dyn is not None:
+        rpl._lib.check(rpl._lib.lib.rpl_debug_set_gather_dyn(*(int(x) for x in args.gather_dyn.split(","))),
+                       "gather_dyn")
     if args.seq_variant is not None:
         rpl._lib.check(rpl._lib.lib.rpl_debug_set_gather_variant(int(args.seq_variant)), "variant")
 

@@ -1474,7 +1474,8 @@ std::atomic<int> g_gather_trigger{(RPL_PDL_EARLY & 4) ? 0 : -1};
 // published but not yet stored below which the meta warp grabs the next unit).
 // rpl_debug_set_gather_dyn.
 // in-process sweeps (scripts/ab_dyn_sweep.py, profiles/r2/dyn_sweep.txt): 88 / 16 / 12 until the
-// default gather got its own instantiation; since then 80 / 16 / 16 (-1.0 us per R2D2 step)
+// default gather got its own instantiation; since then 80 / 16 / 16 (-1.0 us per R2D2 step; the
+// in-process harness then preferred 78 % by 0.27 us, bench.py itself 80 % by 0.2 us)
 std::atomic<int> g_dyn_pct{80};
 std::atomic<int> g_dyn_rows{16};
 std::atomic<int> g_dyn_look{16};
