@@ -455,7 +455,10 @@ __device__ __forceinline__ void tree_update_single(UpdSmem& S, const TreeDev& L,
 // an atomicMax per CTA.  With a min-tree attached (R29) the CTA that takes the last ticket
 // (header word 7, acq_rel: it observes every CTA's leaf writes) recomputes the min paths of
 // all n entries.  Same result as tree_update_single / tree_update_block.
-constexpr int UPDM_THREADS = 64;
+#ifndef RPL_UPDM_THREADS  // threads per CTA of the multi-CTA update (build-flag A/B knob)
+#define RPL_UPDM_THREADS 64
+#endif
+constexpr int UPDM_THREADS = RPL_UPDM_THREADS;
 template <int mode>
 __global__ void __launch_bounds__(UPDM_THREADS)
 k_tree_update_multi(TreeDev L, int64_t* __restrict__ tree, const int64_t* __restrict__ idx,
